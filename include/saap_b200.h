@@ -1,0 +1,220 @@
+/*
+ * saap_b200.h — C ABI of the B200-native SAAP hot path (arXiv 2502.08246).
+ *
+ * This is the drop-in boundary for the reference's C++ API in
+ * /root/reference/proj/core/include/saap/{partition,attention,qmodel}.hpp.
+ * Every entry point below names the reference interface it replaces.  The
+ * signatures use plain pointers and sizes only (no torch, no C++ types) so a
+ * ctypes / cgo / JNI stub binds them directly.
+ *
+ * Conventions
+ *  - Return value: SAAP_OK (0) or an error class.  SAAP_ERR_INVALID_ARGUMENT
+ *    corresponds one-to-one with the reference throwing std::invalid_argument
+ *    and carries the same message prefix (e.g. "sparse_attention: probes 17
+ *    exceed bucket count 16"); saap_last_error() returns the thread-local text.
+ *  - Host-pointer entry points ("drop-in" calls) are synchronous: they return
+ *    after results are back in host memory, like the reference's value
+ *    returns.  *_dev entry points take device pointers, are asynchronous on
+ *    the context's stream and are what a serving loop / the bench uses.
+ *  - Dtype contract: the reference API is f32 with fp64 math.  K/V caches are
+ *    stored in bf16 (RNE-rounded at upload), attention accumulates in fp32;
+ *    parity is defined on bf16-representable inputs (north star: 1e-3
+ *    relative).  Assignment, IVF offsets/ids, routed bucket lists and the
+ *    attention counters are bit-exact with the reference.
+ *  - Head dims supported by the kernels: 32, 64, 128 (SAAP_ERR_UNSUPPORTED
+ *    otherwise).  Any query-group size G >= 1.
+ *  - No CPU fallback: without a usable sm_100 device every call fails with
+ *    SAAP_ERR_NO_DEVICE.
+ */
+#ifndef SAAP_B200_H
+#define SAAP_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SAAP_API __attribute__((visibility("default")))
+#else
+#define SAAP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SAAP_OK 0
+#define SAAP_ERR_INVALID_ARGUMENT 1 /* reference: std::invalid_argument */
+#define SAAP_ERR_CUDA 2             /* CUDA runtime / launch failure */
+#define SAAP_ERR_UNSUPPORTED 3      /* shape outside the kernels' envelope */
+#define SAAP_ERR_NO_DEVICE 4        /* no sm_100 device: no fallback exists */
+
+typedef struct saap_ctx saap_ctx;             /* device + stream + scratch */
+typedef struct saap_partition saap_partition; /* saap::Partition (partition.hpp:14-23) */
+typedef struct saap_qmodel saap_qmodel;       /* saap::QModel (qmodel.hpp:15-28) */
+typedef struct saap_router saap_router;       /* saap::BucketRouter (attention.hpp:102-108) */
+typedef struct saap_layer saap_layer;         /* n_groups ContextStores (attention.hpp:76-86) */
+typedef struct saap_graph saap_graph;         /* captured decode step (CUDA graph) */
+
+/* saap::SparseAttnConfig (attention.hpp:21-25) with DenseWindow (:16-19). */
+typedef struct {
+    uint64_t probes;       /* l buckets per query group; 0 = window only */
+    uint64_t block_size;   /* bucket scan granularity; validated, no effect */
+    uint64_t sink_count;   /* must equal the store's id_offset */
+    uint64_t recent_count; /* dense recent window */
+} saap_sparse_cfg;
+
+/* Counters of saap::AttnResult (attention.hpp:142-147), per query group. */
+typedef struct {
+    uint64_t keys_scored;
+    uint64_t max_visited_bucket;
+    int32_t empty_attention;
+    int32_t reserved;
+} saap_attn_stats;
+
+SAAP_API const char* saap_last_error(void);
+SAAP_API const char* saap_version(void);
+
+/* ---- context ---------------------------------------------------------- */
+SAAP_API int saap_ctx_create(int device, saap_ctx** out);
+SAAP_API int saap_ctx_destroy(saap_ctx* ctx);
+/* Launch on a caller-owned cudaStream_t (e.g. a serving loop's stream). */
+SAAP_API int saap_ctx_set_stream(saap_ctx* ctx, void* cuda_stream);
+SAAP_API int saap_ctx_get_stream(saap_ctx* ctx, void** cuda_stream);
+SAAP_API int saap_ctx_synchronize(saap_ctx* ctx);
+SAAP_API int saap_ctx_sm_count(saap_ctx* ctx, int* out);
+
+/* ---- partitions, Q-models, routers ------------------------------------ */
+/* Partition{centroids C x d f32}; replaces holding a saap::Partition. */
+SAAP_API int saap_partition_create(saap_ctx* ctx, const float* centroids, uint64_t n_buckets,
+                          uint64_t dim, saap_partition** out);
+SAAP_API int saap_partition_destroy(saap_partition* p);
+
+/* QModel parameters in the reference's in-memory fp64 layout
+ * (qmodel.hpp:15-28): w1 d x h, b1/gamma/beta/run_mean/run_var 1 x h,
+ * w2 h x C, b2 1 x C, all row-major. */
+SAAP_API int saap_qmodel_create(saap_ctx* ctx, uint64_t dim, uint64_t hidden, uint64_t n_buckets,
+                       const double* w1, const double* b1, const double* bn_gamma,
+                       const double* bn_beta, const double* bn_run_mean,
+                       const double* bn_run_var, const double* w2, const double* b2,
+                       saap_qmodel** out);
+SAAP_API int saap_qmodel_destroy(saap_qmodel* m);
+
+/* CentroidRouter(partition, use_deroped)   attention.hpp:112-125 */
+SAAP_API int saap_router_create_centroid(saap_ctx* ctx, const saap_partition* p, int use_deroped,
+                                saap_router** out);
+/* QModelRouter(model)                      attention.hpp:127-140 */
+SAAP_API int saap_router_create_qmodel(saap_ctx* ctx, const saap_qmodel* m, saap_router** out);
+SAAP_API int saap_router_destroy(saap_router* r);
+
+/* BucketRouter::select(q_roped, q_deroped, l) -> l ids, score-descending,
+ * ties toward the smaller id.                attention.cpp:275-315 */
+SAAP_API int saap_router_select(saap_ctx* ctx, const saap_router* r, const float* q_roped,
+                       const float* q_deroped, uint64_t G, uint64_t dim, uint64_t l,
+                       uint32_t* out);
+/* batched_bucket_select(model, q_group, l)   qmodel.cpp:485-511 (throws for
+ * l outside [1, C], unlike the router which maps l=0 to {}). */
+SAAP_API int saap_batched_bucket_select(saap_ctx* ctx, const saap_qmodel* m, const float* q_deroped,
+                               uint64_t G, uint64_t dim, uint64_t l, uint32_t* out);
+
+/* ---- key assignment and IVF ------------------------------------------ */
+/* assign_keys(keys, partition)               partition.cpp:191-198 */
+SAAP_API int saap_assign_keys(saap_ctx* ctx, const saap_partition* p, const float* keys, uint64_t n,
+                     uint64_t dim, uint32_t* out);
+/* build_ivf(assignment, C) -> off[C+1], idx  partition.cpp:200-223 */
+SAAP_API int saap_build_ivf(saap_ctx* ctx, const uint32_t* assignment, uint64_t n, uint64_t n_buckets,
+                   uint64_t* off, uint64_t* idx);
+/* rope_remove_block(keys, positions, {dim, base})  rope.cpp:87-90 */
+SAAP_API int saap_rope_remove(saap_ctx* ctx, const float* x, uint64_t rows, uint64_t dim,
+                     const uint64_t* positions, double base, float* out);
+
+/* ---- context stores (one layer = n_groups (sequence, KV head) contexts) --
+ * Device layout per group: rows [0,sink) the sink keys,
+ * rows [sink, T) keys with position < T packed bucket-contiguously
+ * (ascending position inside a bucket), rows [T, n) the recent tail in
+ * position order; T = max(sink, n - recent_hint).  K and V are bf16. */
+SAAP_API int saap_layer_create(saap_ctx* ctx, uint64_t n_groups, uint64_t dim, uint64_t n_buckets,
+                      const uint64_t* n_keys, uint64_t sink, uint64_t recent_hint,
+                      saap_layer** out);
+SAAP_API int saap_layer_destroy(saap_layer* L);
+
+/* build_context_store(keys_roped, values, rope, partition, sink)
+ *                                            attention.cpp:249-255
+ * Host f32 inputs, concatenated over groups (group g owns rows
+ * [sum n_<g, sum n_<=g)).  keys_assign are the keys the partition sees (the
+ * de-roped keys); pass NULL to de-rope keys_roped on device with rope_base.
+ * parts has one partition per group. */
+SAAP_API int saap_layer_build(saap_ctx* ctx, saap_layer* L, const saap_partition* const* parts,
+                     const float* keys_roped, const float* values, const float* keys_assign,
+                     double rope_base);
+/* Same from device bf16 rows (asynchronous). */
+SAAP_API int saap_layer_build_dev(saap_ctx* ctx, saap_layer* L, const saap_partition* const* parts,
+                         const void* keys_roped_bf16, const void* values_bf16,
+                         const void* keys_assign_bf16);
+
+/* Read back ContextStore.assignment / index for group g (host). */
+SAAP_API int saap_layer_read_index(saap_ctx* ctx, const saap_layer* L, uint64_t group,
+                          uint32_t* assignment, uint64_t* off, uint64_t* idx);
+/* Device pointers of the packed cache (bf16 rows) for advanced callers. */
+SAAP_API int saap_layer_packed_rows(const saap_layer* L, void** k_dev, void** v_dev,
+                           uint64_t* total_rows);
+
+/* sparse_attention(q_roped, q_deroped, store, router, cfg) for every group
+ *                                            attention.cpp:317-376
+ * Host f32 queries [n_groups x G x dim]; out [n_groups x G x dim] f32;
+ * stats[n_groups]; selected (nullable) [n_groups x probes] routed buckets.
+ * routers: one per group. */
+SAAP_API int saap_sparse_attention(saap_ctx* ctx, const saap_layer* L,
+                          const saap_router* const* routers, const float* q_roped,
+                          const float* q_deroped, uint64_t G, const saap_sparse_cfg* cfg,
+                          float* out, saap_attn_stats* stats, uint32_t* selected);
+/* Device-pointer variant (asynchronous). */
+SAAP_API int saap_sparse_attention_dev(saap_ctx* ctx, const saap_layer* L,
+                              const saap_router* const* routers, const float* q_roped_dev,
+                              const float* q_deroped_dev, uint64_t G,
+                              const saap_sparse_cfg* cfg, float* out_dev,
+                              saap_attn_stats* stats_dev, uint32_t* selected_dev);
+
+/* full_attention(q, keys, values) over each group's whole context, from the
+ * layer's packed cache (permutation-invariant)     attention.cpp:163-195 */
+SAAP_API int saap_layer_full_attention(saap_ctx* ctx, const saap_layer* L, const float* q,
+                              uint64_t G, float* out);
+
+/* Dense decode baseline (the in-run comparator): a position-ordered bf16
+ * KV cache already on the device, borrowed (not copied).  Group g's rows
+ * start at row_base[g] and span n_keys[g] rows (host arrays).  Decoding it is
+ * full_attention (attention.cpp:163-195) for every group. */
+typedef struct saap_kvcache saap_kvcache;
+SAAP_API int saap_kvcache_create(saap_ctx* ctx, uint64_t n_groups, uint64_t dim, const void* keys_bf16,
+                        const void* values_bf16, const uint64_t* row_base,
+                        const uint64_t* n_keys, saap_kvcache** out);
+SAAP_API int saap_kvcache_destroy(saap_kvcache* c);
+SAAP_API int saap_dense_attention_dev(saap_ctx* ctx, const saap_kvcache* c, const float* q_dev,
+                             uint64_t G, float* out_dev);
+
+/* full_attention(q, keys, values) on host f32 arrays. attention.cpp:163-195 */
+SAAP_API int saap_full_attention(saap_ctx* ctx, const float* q, uint64_t G, const float* keys,
+                        const float* values, uint64_t n, uint64_t dim, float* out);
+
+/* ---- CUDA graphs over the asynchronous calls --------------------------- */
+SAAP_API int saap_graph_begin(saap_ctx* ctx);
+SAAP_API int saap_graph_end(saap_ctx* ctx, saap_graph** out);
+SAAP_API int saap_graph_launch(saap_ctx* ctx, saap_graph* g);
+SAAP_API int saap_graph_destroy(saap_graph* g);
+
+/* Kernel launches issued by this context so far (bench "gpu_launches"). */
+SAAP_API int saap_ctx_launch_count(saap_ctx* ctx, uint64_t* out);
+
+/* ---- diagnostics ------------------------------------------------------- */
+/* out[i] = the device port of glibc exp(x[i]) used by the Q-model router
+ * softmax (host arrays); lets tests pin it against the host libm. */
+SAAP_API int saap_debug_exp(saap_ctx* ctx, const double* x, uint64_t n, double* out);
+
+/* ---- synthetic data (bench tooling; counter-based, reproducible) ------- */
+/* Fills a device bf16 [rows x dim] buffer with clustered keys / values. */
+SAAP_API int saap_synth_fill_dev(saap_ctx* ctx, void* out_bf16, uint64_t rows, uint64_t dim,
+                        uint64_t seed, int kind, const float* centers_dev,
+                        uint64_t n_centers, float center_scale, float noise);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAAP_B200_H */

@@ -1,0 +1,586 @@
+"""B200-native SAAP hot path (arXiv 2502.08246) — Python host mirror.
+
+The product is ``libsaap_b200.so`` (C++ host + sm_100a CUDA kernels, C ABI in
+``include/saap_b200.h``).  This module binds it with ctypes and mirrors the
+reference's C++ API for the hot path, with the same names, argument meaning
+and error behaviour (``std::invalid_argument`` -> :class:`InvalidArgument`, a
+``ValueError`` carrying the reference's message prefix):
+
+=========================  ==================================================
+reference (proj/core)      here
+=========================  ==================================================
+assign_keys                :func:`assign_keys`  (partition.cpp:191-198)
+build_ivf                  :func:`build_ivf`    (partition.cpp:200-223)
+rope_remove_block          :func:`rope_remove_block` (rope.cpp:87-90)
+build_context_store        :func:`build_context_store` (attention.cpp:249-255)
+CentroidRouter / QModelRouter  :class:`CentroidRouter` / :class:`QModelRouter`
+batched_bucket_select      :func:`batched_bucket_select` (qmodel.cpp:485-511)
+sparse_attention           :func:`sparse_attention` (attention.cpp:317-376)
+full_attention             :func:`full_attention` (attention.cpp:163-195)
+selectivity / mse          :func:`selectivity` / :func:`mse`
+=========================  ==================================================
+
+There is no CPU fallback: importing works anywhere (so the library's exports
+can be checked on a CPU box), but every compute call needs an sm_100 GPU and
+raises :class:`NoDevice` otherwise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_DIR, "libsaap_b200.so")
+HEADER_PATH = os.path.join(os.path.dirname(_DIR), "include", "saap_b200.h")
+
+SAAP_OK, SAAP_ERR_INVALID_ARGUMENT, SAAP_ERR_CUDA, SAAP_ERR_UNSUPPORTED, SAAP_ERR_NO_DEVICE = range(5)
+
+
+class SaapError(RuntimeError):
+    code = SAAP_ERR_CUDA
+
+
+class InvalidArgument(ValueError):
+    """The reference would throw std::invalid_argument with this message."""
+    code = SAAP_ERR_INVALID_ARGUMENT
+
+
+class Unsupported(SaapError):
+    code = SAAP_ERR_UNSUPPORTED
+
+
+class NoDevice(SaapError):
+    code = SAAP_ERR_NO_DEVICE
+
+
+_lib = None
+
+
+def lib():
+    """Load libsaap_b200.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(make -C paper_2502_08246_b200)")
+        _lib = C.CDLL(LIB_PATH)
+        _lib.saap_last_error.restype = C.c_char_p
+        _lib.saap_version.restype = C.c_char_p
+    return _lib
+
+
+def _check(rc):
+    if rc == SAAP_OK:
+        return
+    msg = lib().saap_last_error().decode()
+    if rc == SAAP_ERR_INVALID_ARGUMENT:
+        raise InvalidArgument(msg)
+    if rc == SAAP_ERR_UNSUPPORTED:
+        raise Unsupported(msg)
+    if rc == SAAP_ERR_NO_DEVICE:
+        raise NoDevice(msg)
+    raise SaapError(msg)
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+_u64 = C.c_uint64
+
+
+def _dptr(x):
+    """Device pointer of a torch tensor / raw int (plumbing only)."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return C.c_void_p(x)
+    return C.c_void_p(x.data_ptr())
+
+
+class SparseAttnCfg(C.Structure):
+    _fields_ = [("probes", C.c_uint64), ("block_size", C.c_uint64),
+                ("sink_count", C.c_uint64), ("recent_count", C.c_uint64)]
+
+
+class AttnStats(C.Structure):
+    _fields_ = [("keys_scored", C.c_uint64), ("max_visited_bucket", C.c_uint64),
+                ("empty_attention", C.c_int32), ("reserved", C.c_int32)]
+
+
+@dataclass
+class DenseWindow:
+    """saap::DenseWindow (attention.hpp:16-19)."""
+    sink_count: int = 1
+    recent_count: int = 2047
+
+
+@dataclass
+class SparseAttnConfig:
+    """saap::SparseAttnConfig (attention.hpp:21-25)."""
+    probes: int = 16
+    block_size: int = 128
+    dense: DenseWindow = field(default_factory=DenseWindow)
+
+    def c(self):
+        return SparseAttnCfg(self.probes, self.block_size, self.dense.sink_count,
+                             self.dense.recent_count)
+
+
+@dataclass
+class AttnResult:
+    """saap::AttnResult (attention.hpp:142-147)."""
+    output: np.ndarray
+    keys_scored: int = 0
+    max_visited_bucket: int = 0
+    empty_attention: bool = False
+
+
+@dataclass
+class IVFIndex:
+    off: np.ndarray  # u64 [C+1]
+    idx: np.ndarray  # u64 [N]
+
+    def n_buckets(self):
+        return max(0, self.off.size - 1)
+
+    def bucket(self, c):
+        return self.idx[int(self.off[c]):int(self.off[c + 1])]
+
+    def bucket_size(self, c):
+        return int(self.off[c + 1] - self.off[c])
+
+
+# --------------------------------------------------------------------------
+class Context:
+    """Device + stream (saap_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _check(lib().saap_ctx_create(C.c_int(device), C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().saap_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        _check(lib().saap_ctx_synchronize(self.h))
+
+    @property
+    def stream(self) -> int:
+        s = C.c_void_p()
+        _check(lib().saap_ctx_get_stream(self.h, C.byref(s)))
+        return s.value or 0
+
+    def set_stream(self, stream_ptr: int):
+        _check(lib().saap_ctx_set_stream(self.h, C.c_void_p(stream_ptr)))
+
+    @property
+    def sm_count(self) -> int:
+        v = C.c_int()
+        _check(lib().saap_ctx_sm_count(self.h, C.byref(v)))
+        return v.value
+
+    @property
+    def launch_count(self) -> int:
+        v = C.c_uint64()
+        _check(lib().saap_ctx_launch_count(self.h, C.byref(v)))
+        return v.value
+
+    def graph_begin(self):
+        _check(lib().saap_graph_begin(self.h))
+
+    def graph_end(self) -> "Graph":
+        g = C.c_void_p()
+        _check(lib().saap_graph_end(self.h, C.byref(g)))
+        return Graph(self, g)
+
+
+class Graph:
+    def __init__(self, ctx, h):
+        self.ctx, self.h = ctx, h
+
+    def launch(self):
+        _check(lib().saap_graph_launch(self.ctx.h, self.h))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().saap_graph_destroy(self.h)
+            self.h = None
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(int(os.environ.get("LOCAL_RANK", "0")))
+    return _default_ctx
+
+
+# --------------------------------------------------------------------------
+class Partition:
+    """saap::Partition: C unit-norm centroids (partition.hpp:14-23)."""
+
+    def __init__(self, centroids, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.centroids = _f32(centroids)
+        if self.centroids.ndim != 2:
+            raise InvalidArgument("Partition: centroids must be C x d")
+        h = C.c_void_p()
+        _check(lib().saap_partition_create(self.ctx.h, _p(self.centroids),
+                                           _u64(self.centroids.shape[0]),
+                                           _u64(self.centroids.shape[1]), C.byref(h)))
+        self.h = h
+
+    def n_buckets(self):
+        return self.centroids.shape[0]
+
+    def dim(self):
+        return self.centroids.shape[1]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().saap_partition_destroy(self.h)
+            self.h = None
+
+
+QMODEL_FIELDS = ("w1", "b1", "bn_gamma", "bn_beta", "bn_run_mean", "bn_run_var", "w2", "b2")
+
+
+class QModel:
+    """saap::QModel in eval mode (qmodel.hpp:15-28); params as fp64 arrays."""
+
+    def __init__(self, params: dict, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.params = {k: _f64(params[k]) for k in QMODEL_FIELDS}
+        d, hid = self.params["w1"].shape
+        Cb = self.params["w2"].shape[1]
+        self.d, self.hidden, self.C = d, hid, Cb
+        h = C.c_void_p()
+        _check(lib().saap_qmodel_create(self.ctx.h, _u64(d), _u64(hid), _u64(Cb),
+                                        *[_p(self.params[k]) for k in QMODEL_FIELDS], C.byref(h)))
+        self.h = h
+
+    def n_buckets(self):
+        return self.C
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().saap_qmodel_destroy(self.h)
+            self.h = None
+
+
+class BucketRouter:
+    """saap::BucketRouter plugin (attention.hpp:102-108)."""
+
+    h = None
+    ctx: Context
+
+    def select(self, q_group_roped, q_group_deroped, l) -> np.ndarray:
+        qr = _f32(q_group_roped)
+        qd = _f32(q_group_deroped)
+        out = np.empty(int(l), np.uint32)
+        _check(lib().saap_router_select(self.ctx.h, self.h, _p(qr), _p(qd), _u64(qr.shape[0]),
+                                        _u64(qr.shape[1]), _u64(l), _p(out)))
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().saap_router_destroy(self.h)
+            self.h = None
+
+
+class CentroidRouter(BucketRouter):
+    """Top-l centroids by pooled fp64 score (attention.cpp:275-306)."""
+
+    def __init__(self, partition: Partition, use_deroped: bool):
+        self.ctx = partition.ctx
+        self.partition = partition
+        h = C.c_void_p()
+        _check(lib().saap_router_create_centroid(self.ctx.h, partition.h,
+                                                 C.c_int(1 if use_deroped else 0), C.byref(h)))
+        self.h = h
+
+
+class QModelRouter(BucketRouter):
+    """Top-l buckets of the summed classifier distribution (attention.cpp:308-315)."""
+
+    def __init__(self, model: QModel):
+        self.ctx = model.ctx
+        self.model = model
+        h = C.c_void_p()
+        _check(lib().saap_router_create_qmodel(self.ctx.h, model.h, C.byref(h)))
+        self.h = h
+
+
+def batched_bucket_select(model: QModel, query_group, l) -> np.ndarray:
+    q = _f32(query_group)
+    out = np.empty(max(int(l), 0), np.uint32)
+    _check(lib().saap_batched_bucket_select(model.ctx.h, model.h, _p(q), _u64(q.shape[0]),
+                                            _u64(q.shape[1]), _u64(l), _p(out)))
+    return out
+
+
+# --------------------------------------------------------------------------
+def assign_keys(keys, p: Partition) -> np.ndarray:
+    """KeyAssignment.bucket_of (partition.cpp:191-198), bit-exact."""
+    k = _f32(keys)
+    out = np.empty(k.shape[0], np.uint32)
+    _check(lib().saap_assign_keys(p.ctx.h, p.h, _p(k), _u64(k.shape[0]), _u64(k.shape[1]),
+                                  _p(out)))
+    return out
+
+
+def assign_key(key, p: Partition) -> int:
+    return int(assign_keys(np.asarray(key, np.float32)[None, :], p)[0])
+
+
+def build_ivf(assignment, n_buckets, ctx: Optional[Context] = None) -> IVFIndex:
+    ctx = ctx or default_context()
+    a = np.ascontiguousarray(assignment, dtype=np.uint32)
+    off = np.empty(int(n_buckets) + 1, np.uint64)
+    idx = np.empty(a.size, np.uint64)
+    _check(lib().saap_build_ivf(ctx.h, _p(a), _u64(a.size), _u64(n_buckets), _p(off), _p(idx)))
+    return IVFIndex(off, idx)
+
+
+def rope_remove_block(x, positions, base, ctx: Optional[Context] = None):
+    ctx = ctx or default_context()
+    x = _f32(x)
+    pos = np.ascontiguousarray(positions, dtype=np.uint64)
+    out = np.empty_like(x)
+    _check(lib().saap_rope_remove(ctx.h, _p(x), _u64(x.shape[0]), _u64(x.shape[1]), _p(pos),
+                                  C.c_double(base), _p(out)))
+    return out
+
+
+# --------------------------------------------------------------------------
+class Layer:
+    """n_groups ContextStores of one layer in one device allocation
+    (attention.hpp:76-86 per group); the batched decode step runs on all."""
+
+    def __init__(self, n_keys: Sequence[int], dim: int, n_buckets: int, sink: int = 1,
+                 recent_hint: int = 2047, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.n_keys = np.ascontiguousarray(n_keys, dtype=np.uint64)
+        self.n_groups = self.n_keys.size
+        self.dim, self.n_buckets_, self.sink, self.recent_hint = dim, n_buckets, sink, recent_hint
+        h = C.c_void_p()
+        _check(lib().saap_layer_create(self.ctx.h, _u64(self.n_groups), _u64(dim),
+                                       _u64(n_buckets), _p(self.n_keys), _u64(sink),
+                                       _u64(recent_hint), C.byref(h)))
+        self.h = h
+        self.partitions: list = []
+
+    def n_buckets(self):
+        return self.n_buckets_
+
+    def _parts(self, partitions):
+        if isinstance(partitions, Partition):
+            partitions = [partitions] * self.n_groups
+        if len(partitions) != self.n_groups:
+            raise InvalidArgument("one partition per group")
+        self.partitions = list(partitions)
+        return (C.c_void_p * self.n_groups)(*[p.h.value for p in partitions])
+
+    def build(self, partitions, keys_roped, values, keys_assign=None, rope_base=500000.0):
+        """Host f32 rows concatenated over groups."""
+        arr = self._parts(partitions)
+        kr, v = _f32(keys_roped), _f32(values)
+        ka = _f32(keys_assign) if keys_assign is not None else None
+        _check(lib().saap_layer_build(self.ctx.h, self.h, arr, _p(kr), _p(v),
+                                      _p(ka) if ka is not None else None, C.c_double(rope_base)))
+        return self
+
+    def build_dev(self, partitions, keys_roped_bf16, values_bf16, keys_assign_bf16):
+        arr = self._parts(partitions)
+        _check(lib().saap_layer_build_dev(self.ctx.h, self.h, arr, _dptr(keys_roped_bf16),
+                                          _dptr(values_bf16), _dptr(keys_assign_bf16)))
+        return self
+
+    def read_index(self, group: int):
+        n = int(self.n_keys[group]) - self.sink
+        a = np.empty(n, np.uint32)
+        off = np.empty(self.n_buckets_ + 1, np.uint64)
+        idx = np.empty(n, np.uint64)
+        _check(lib().saap_layer_read_index(self.ctx.h, self.h, _u64(group), _p(a), _p(off),
+                                           _p(idx)))
+        return a, IVFIndex(off, idx)
+
+    def _routers(self, routers):
+        if routers is None:
+            return None
+        if isinstance(routers, BucketRouter):
+            routers = [routers] * self.n_groups
+        self._keep_routers = list(routers)
+        return (C.c_void_p * self.n_groups)(*[r.h.value for r in routers])
+
+    def sparse_attention(self, routers, q_roped, q_deroped, cfg: SparseAttnConfig,
+                         want_selected=False):
+        """Batched sparse_attention: q [n_groups, G, d] -> out, stats, selected."""
+        qr = _f32(q_roped)
+        qd = _f32(q_deroped) if q_deroped is not None else None
+        G = qr.shape[1]
+        out = np.empty_like(qr)
+        stats = (AttnStats * self.n_groups)()
+        sel = np.empty((self.n_groups, max(cfg.probes, 1)), np.uint32) if want_selected else None
+        c = cfg.c()
+        _check(lib().saap_sparse_attention(self.ctx.h, self.h, self._routers(routers), _p(qr),
+                                           _p(qd) if qd is not None else None, _u64(G),
+                                           C.byref(c), _p(out), stats,
+                                           _p(sel) if sel is not None else None))
+        return out, stats, (sel[:, :cfg.probes] if sel is not None else None)
+
+    def sparse_attention_dev(self, routers, q_roped, q_deroped, G, cfg: SparseAttnConfig, out,
+                             stats=None, selected=None):
+        c = cfg.c()
+        _check(lib().saap_sparse_attention_dev(self.ctx.h, self.h, self._routers(routers),
+                                               _dptr(q_roped), _dptr(q_deroped), _u64(G),
+                                               C.byref(c), _dptr(out), _dptr(stats),
+                                               _dptr(selected)))
+
+    def full_attention(self, q):
+        q = _f32(q)
+        out = np.empty_like(q)
+        _check(lib().saap_layer_full_attention(self.ctx.h, self.h, _p(q), _u64(q.shape[1]),
+                                               _p(out)))
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().saap_layer_destroy(self.h)
+            self.h = None
+
+
+class ContextStore(Layer):
+    """One context: saap::ContextStore (attention.hpp:76-86)."""
+
+    def __init__(self, n_keys, dim, n_buckets, sink, recent_hint=2047, ctx=None):
+        super().__init__([n_keys], dim, n_buckets, sink, recent_hint, ctx)
+
+    @property
+    def id_offset(self):
+        return self.sink
+
+    def n_keys_(self):
+        return int(self.n_keys[0])
+
+    @property
+    def assignment(self):
+        return self.read_index(0)[0]
+
+    @property
+    def index(self) -> IVFIndex:
+        return self.read_index(0)[1]
+
+
+def build_context_store(keys_roped, values, rope_base, partition: Partition, sink_count,
+                        keys_deroped=None, recent_hint=2047) -> ContextStore:
+    """build_context_store(keys_roped, values, rope, partition, sink)
+    (attention.cpp:249-255).  keys_deroped, when given, are the keys the
+    partition sees (otherwise keys_roped are de-roped on the device)."""
+    kr = _f32(keys_roped)
+    v = _f32(values)
+    if kr.shape[0] != v.shape[0]:
+        raise InvalidArgument(f"attention: {kr.shape[0]} keys vs {v.shape[0]} values")
+    st = ContextStore(kr.shape[0], kr.shape[1], partition.n_buckets(), sink_count, recent_hint,
+                      partition.ctx)
+    st.build(partition, kr, v, keys_deroped, rope_base)
+    return st
+
+
+def sparse_attention(q_group_roped, q_group_deroped, store: ContextStore, router: BucketRouter,
+                     cfg: SparseAttnConfig) -> AttnResult:
+    qr = _f32(q_group_roped)[None]
+    qd = _f32(q_group_deroped)[None] if q_group_deroped is not None else None
+    out, stats, _ = store.sparse_attention(router, qr, qd, cfg)
+    s = stats[0]
+    return AttnResult(out[0], int(s.keys_scored), int(s.max_visited_bucket),
+                      bool(s.empty_attention))
+
+
+def full_attention(q_group, keys, values, ctx: Optional[Context] = None) -> np.ndarray:
+    ctx = ctx or default_context()
+    q, k, v = _f32(q_group), _f32(keys), _f32(values)
+    if k.shape[0] != v.shape[0]:
+        raise InvalidArgument(f"attention: {k.shape[0]} keys vs {v.shape[0]} values")
+    out = np.empty((q.shape[0], v.shape[1]), np.float32)
+    _check(lib().saap_full_attention(ctx.h, _p(q), _u64(q.shape[0]), _p(k), _p(v),
+                                     _u64(k.shape[0]), _u64(k.shape[1]), _p(out)))
+    return out
+
+
+def selectivity(result: AttnResult, n_keys: int) -> float:
+    """keys_scored / N (attention.cpp:378-383)."""
+    if n_keys == 0:
+        raise InvalidArgument("selectivity: empty context")
+    return result.keys_scored / n_keys
+
+
+def mse(approx, exact) -> float:
+    """Mean squared entrywise difference (attention.cpp:385-399)."""
+    a = np.asarray(approx, np.float64)
+    b = np.asarray(exact, np.float64)
+    if a.shape != b.shape:
+        raise InvalidArgument(f"mse: shapes {a.shape} vs {b.shape}")
+    if a.size == 0:
+        raise InvalidArgument("mse: empty inputs")
+    return float(np.mean((a - b) ** 2))
+
+
+class KVCache:
+    """Position-ordered bf16 cache on the device (dense in-run baseline)."""
+
+    def __init__(self, ctx: Context, n_groups, dim, keys_bf16, values_bf16, row_base, n_keys):
+        self.ctx = ctx
+        rb = np.ascontiguousarray(row_base, np.uint64)
+        nk = np.ascontiguousarray(n_keys, np.uint64)
+        h = C.c_void_p()
+        _check(lib().saap_kvcache_create(ctx.h, _u64(n_groups), _u64(dim), _dptr(keys_bf16),
+                                         _dptr(values_bf16), _p(rb), _p(nk), C.byref(h)))
+        self.h = h
+
+    def dense_attention_dev(self, q, G, out):
+        _check(lib().saap_dense_attention_dev(self.ctx.h, self.h, _dptr(q), _u64(G), _dptr(out)))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().saap_kvcache_destroy(self.h)
+            self.h = None
+
+
+def synth_fill(ctx: Context, out, rows, dim, seed, kind, centers=None, n_centers=0,
+               center_scale=0.0, noise=1.0):
+    _check(lib().saap_synth_fill_dev(ctx.h, _dptr(out), _u64(rows), _u64(dim), _u64(seed),
+                                     C.c_int(kind), _dptr(centers), _u64(n_centers),
+                                     C.c_float(center_scale), C.c_float(noise)))
+
+
+def exported_symbols():
+    """Names declared in include/saap_b200.h (for the export check)."""
+    import re
+    txt = open(HEADER_PATH).read()
+    return sorted(set(re.findall(r"SAAP_API\s+(?:int|const char\*)\s+(saap_\w+)\s*\(", txt)))

@@ -1,0 +1,1222 @@
+// C ABI of libsaap_b200: host orchestration of the sm_100a kernels behind the
+// reference's C++ API (see include/saap_b200.h for the interface map).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "args.cuh"
+
+namespace saap_b200 {
+
+// ---- kernels (decode.cu / pack.cu / route.cu / synth.cu)
+void launch_route_plan(const PlanArgs& a, uint32_t n_groups, cudaStream_t st);
+void launch_decode(int D, const DecodeArgs& a, int grid, cudaStream_t st);
+void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st);
+void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t n_tiles,
+                         const void* keys, const uint64_t* key_row0, const double* const* cent64,
+                         uint32_t C, uint32_t* out, const uint64_t* out_base, cudaStream_t st);
+void launch_pack(int D, const TileDesc* tiles, uint32_t n_tiles, const uint32_t* tile_first,
+                 uint32_t n_groups, const GroupMeta* meta, const uint32_t* assign, uint32_t C,
+                 uint32_t* hist, uint32_t* countA, uint32_t* off, uint32_t* offA, uint32_t* idx,
+                 uint32_t* invA, const uint16_t* Ksrc, const uint16_t* Vsrc,
+                 const uint64_t* src_row0, uint16_t* Kdst, uint16_t* Vdst, cudaStream_t st);
+void launch_f32_to_bf16(const float* in, uint16_t* out, uint64_t n, cudaStream_t st);
+void launch_derope(const float* x, const double* cs, uint64_t rows, uint32_t D, float* out,
+                   cudaStream_t st);
+void launch_debug_exp(const double* x, uint64_t n, double* y, cudaStream_t st);
+void launch_synth(uint16_t* out, uint64_t rows, uint32_t D, uint64_t seed, int kind,
+                  const float* centers, uint64_t n_centers, float center_scale, float noise,
+                  cudaStream_t st);
+
+}  // namespace saap_b200
+
+
+using namespace saap_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Failure {
+    int code;
+    std::string msg;
+};
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return SAAP_OK;
+    } catch (const Failure& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return SAAP_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SAAP_ERR_CUDA;
+    }
+}
+
+[[noreturn]] void invalid(const std::string& m) { throw Failure{SAAP_ERR_INVALID_ARGUMENT, m}; }
+[[noreturn]] void unsupported(const std::string& m) { throw Failure{SAAP_ERR_UNSUPPORTED, m}; }
+
+void need(const void* p, const char* what) {
+    if (!p) invalid(std::string(what) + ": null argument");
+}
+
+template <typename T>
+T* dmalloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    SAAP_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    return static_cast<T*>(p);
+}
+template <typename T>
+void dfree(T*& p) {
+    if (p) cudaFree((void*)p);
+    p = nullptr;
+}
+
+void* ensure(saap_ctx* c, saap_scratch& s, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (bytes <= s.cap) return s.p;
+    if (c->capturing)
+        throw Failure{SAAP_ERR_INVALID_ARGUMENT,
+                      "scratch grows during graph capture: run the call once uncaptured first"};
+    if (s.p) {
+        SAAP_CUDA(cudaStreamSynchronize(c->stream));
+        cudaFree(s.p);
+        s.p = nullptr;
+        s.cap = 0;
+    }
+    const size_t cap = std::max<size_t>(bytes, 4096) * 5 / 4;
+    SAAP_CUDA(cudaMalloc(&s.p, cap));
+    s.cap = cap;
+    return s.p;
+}
+
+void ensure_done(saap_ctx* c, size_t n) {
+    if (n <= c->done_cap) return;
+    if (c->capturing) invalid("scratch grows during graph capture: run the call once uncaptured first");
+    if (c->done) {
+        SAAP_CUDA(cudaStreamSynchronize(c->stream));
+        cudaFree(c->done);
+    }
+    const size_t cap = std::max<size_t>(n, 1024) * 2;
+    SAAP_CUDA(cudaMalloc(&c->done, cap * 4));
+    SAAP_CUDA(cudaMemset(c->done, 0, cap * 4));
+    c->done_cap = cap;
+}
+
+struct DeviceGuard {
+    explicit DeviceGuard(const saap_ctx* c) {
+        if (!c) invalid("null context");
+        SAAP_CUDA(cudaSetDevice(c->device));
+    }
+};
+
+void h2d(void* d, const void* h, size_t bytes, cudaStream_t st) {
+    if (bytes) SAAP_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
+}
+void d2h(void* h, const void* d, size_t bytes, cudaStream_t st) {
+    if (bytes) SAAP_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st));
+}
+void sync(saap_ctx* c) { SAAP_CUDA(cudaStreamSynchronize(c->stream)); }
+
+uint32_t next_pow2(uint32_t x) {
+    uint32_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+bool supported_dim(uint64_t d) { return d == 32 || d == 64 || d == 128; }
+
+// glibc-exact RoPE removal table: (cos, sin) of (-1.0 * p) * theta_j with
+// theta_j = pow(base, -2.0 * j * (1/dim))   rope.cpp:20-27, 29-41
+std::vector<double> rope_table(const uint64_t* positions, uint64_t rows, uint64_t dim,
+                               double base) {
+    const double inv_dim = 1.0 / static_cast<double>(dim);
+    std::vector<double> th(dim / 2);
+    for (size_t j = 0; j < th.size(); ++j)
+        th[j] = std::pow(base, -2.0 * static_cast<double>(j) * inv_dim);
+    std::vector<double> cs(rows * dim);
+    for (uint64_t i = 0; i < rows; ++i) {
+        const double p = static_cast<double>(positions[i]);
+        for (size_t j = 0; j < th.size(); ++j) {
+            const double angle = -1.0 * p * th[j];
+            cs[(i * (dim / 2) + j) * 2] = std::cos(angle);
+            cs[(i * (dim / 2) + j) * 2 + 1] = std::sin(angle);
+        }
+    }
+    return cs;
+}
+
+// Tiles of <= kPackTile local ids per group, in group order.
+void build_tiles(const std::vector<GroupMeta>& meta, std::vector<TileDesc>& tiles,
+                 std::vector<uint32_t>& first) {
+    tiles.clear();
+    first.assign(meta.size() + 1, 0);
+    for (size_t g = 0; g < meta.size(); ++g) {
+        first[g] = (uint32_t)tiles.size();
+        const uint32_t ns = meta[g].n - meta[g].sink;
+        for (uint32_t f = 0; f < ns; f += kPackTile)
+            tiles.push_back(TileDesc{(uint32_t)g, f, std::min(kPackTile, ns - f), 0});
+    }
+    first[meta.size()] = (uint32_t)tiles.size();
+}
+
+// Route pointer tables: one centT / Q-model triple per group, cached on the layer.
+void bind_routers(saap_layer* L, const saap_router* const* routers, int& mode, int& use_deroped) {
+    std::vector<const saap_router*> rs(routers, routers + L->n_groups);
+    for (auto* r : rs) need(r, "sparse_attention: router");
+    const int kind = rs[0]->kind;
+    use_deroped = rs[0]->use_deroped;
+    for (auto* r : rs) {
+        if (r->kind != kind) unsupported("sparse_attention: mixed router kinds in one call");
+        if (kind == 0 && r->use_deroped != use_deroped)
+            unsupported("sparse_attention: mixed roped/de-roped centroid routers in one call");
+    }
+    mode = kind == 0 ? 1 : 2;
+    if (rs == L->cached_routers) return;
+    if (L->ctx->capturing) invalid("router set changed during graph capture");
+    if (kind == 0) {
+        std::vector<const float*> p(L->n_groups);
+        for (size_t g = 0; g < p.size(); ++g) p[g] = rs[g]->part->centT;
+        if (!L->d_centT) L->d_centT = (const float**)(dmalloc<void*>(L->n_groups));
+        SAAP_CUDA(cudaMemcpy(L->d_centT, p.data(), p.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    } else {
+        std::vector<const double*> p(3 * L->n_groups);
+        for (size_t g = 0; g < L->n_groups; ++g) {
+            p[3 * g] = rs[g]->model->w1;
+            p[3 * g + 1] = rs[g]->model->w2;
+            p[3 * g + 2] = rs[g]->model->vec;
+        }
+        if (!L->d_qm) L->d_qm = (const double**)(dmalloc<void*>(3 * L->n_groups));
+        SAAP_CUDA(cudaMemcpy(L->d_qm, p.data(), p.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    }
+    L->cached_routers = rs;
+}
+
+void check_router_dims(const saap_router* r, uint64_t d, uint64_t C, uint64_t l) {
+    if (r->kind == 0) {
+        if (d != r->part->d)
+            invalid("CentroidRouter: query dim " + std::to_string(d) + " vs centroid dim " +
+                    std::to_string(r->part->d));
+        if (l > r->part->C) invalid("CentroidRouter: l exceeds bucket count");
+        if (C && r->part->C != C) invalid("sparse_attention: router bucket count differs from store");
+    } else {
+        if (d != r->model->d)
+            invalid("qmodel: query dim " + std::to_string(d) + " does not match model dim " +
+                    std::to_string(r->model->d));
+        if (l < 1 || l > r->model->C)
+            invalid("batched_bucket_select: l=" + std::to_string(l) + " outside [1, " +
+                    std::to_string(r->model->C) + "]");
+        if (C && r->model->C != C) invalid("sparse_attention: router bucket count differs from store");
+    }
+}
+
+constexpr uint32_t kItemKeysSparse = 512;
+constexpr uint32_t kItemKeysDense = 2048;
+
+// Enqueue one decode step (routing, planning, attention, combine) on the
+// context stream.  mode: 0 dense/full, 1 centroid, 2 Q-model, 3 window only.
+void enqueue_decode(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
+                    const GroupMeta* meta, const uint64_t* row_base, uint64_t max_n,
+                    const uint32_t* off, const uint32_t* offA, const uint32_t* idx,
+                    const uint32_t* assign, const uint32_t* invA, uint32_t* list,
+                    const uint16_t* K, const uint16_t* V, int mode, const float* const* centT,
+                    const double* const* qm, const float* q_roped, const float* q_route,
+                    uint64_t G, uint64_t probes, uint64_t recent, float* out,
+                    saap_attn_stats* stats, uint32_t* selected, uint32_t item_keys,
+                    uint32_t qm_hidden = 0) {
+    const cudaStream_t st = c->stream;
+    const uint64_t n_hchunks = (G + kHeadsPerSlot - 1) / kHeadsPerSlot;
+    const uint64_t qslots = n_groups * n_hchunks;
+    const uint64_t per_group_items = (max_n + item_keys - 1) / item_keys + probes + 8;
+    const uint64_t max_items = n_groups * per_group_items * n_hchunks;
+    Item* items = (Item*)ensure(c, c->items, max_items * sizeof(Item));
+    QSlot* qs = (QSlot*)ensure(c, c->qslots, qslots * sizeof(QSlot));
+    float* pO = (float*)ensure(c, c->part_O, max_items * kHeadsPerSlot * D * sizeof(float));
+    float* pml = (float*)ensure(c, c->part_ml, max_items * 8 * sizeof(float));
+    if (!stats) stats = (saap_attn_stats*)ensure(c, c->stats, n_groups * sizeof(saap_attn_stats));
+    ensure_done(c, qslots);
+    double* probs = nullptr;
+    if (mode == 2) probs = (double*)ensure(c, c->probs, n_groups * G * C * sizeof(double));
+
+    SAAP_CUDA(cudaMemsetAsync(c->counters, 0, sizeof(StepCounters), st));
+    if (mode == 2) {
+        QModelArgs qa{};
+        qa.q = q_route;
+        qa.prm = qm;
+        qa.G = (uint32_t)G;
+        qa.d = (uint32_t)D;
+        qa.h = qm_hidden;
+        qa.C = (uint32_t)C;
+        qa.probs = probs;
+        launch_qmodel_probs(qa, (uint32_t)n_groups, st);
+        c->launches++;
+    }
+    PlanArgs pa{};
+    pa.meta = meta;
+    pa.off = off;
+    pa.offA = offA;
+    pa.idx = idx;
+    pa.assign = assign;
+    pa.list = list;
+    pa.C = (uint32_t)C;
+    pa.mode = mode;
+    pa.centT = centT;
+    pa.q_route = q_route;
+    pa.scores = probs;
+    pa.G = (uint32_t)G;
+    pa.D = (uint32_t)D;
+    pa.n_hchunks = (uint32_t)n_hchunks;
+    pa.probes = (uint32_t)probes;
+    pa.recent = (uint32_t)std::min<uint64_t>(recent, 0xFFFFFFFFull);
+    pa.item_keys = item_keys;
+    pa.P2 = (mode == 1 || mode == 2) ? next_pow2((uint32_t)C) : 0;
+    pa.route_only = 0;
+    pa.items = items;
+    pa.ctr = c->counters;
+    pa.qslots = qs;
+    pa.stats = stats;
+    pa.selected = selected;
+    pa.out = out;
+    launch_route_plan(pa, (uint32_t)n_groups, st);
+    c->launches++;
+
+    DecodeArgs da{};
+    da.items = items;
+    da.ctr = c->counters;
+    da.K = K;
+    da.V = V;
+    da.row_base = row_base;
+    da.invA = invA;
+    da.list = list;
+    da.q = q_roped;
+    da.G = (uint32_t)G;
+    da.n_hchunks = (uint32_t)n_hchunks;
+    da.qscale = (float)(1.4426950408889634 / std::sqrt((double)D));
+    da.part_O = pO;
+    da.part_ml = pml;
+    da.qslots = qs;
+    da.done = c->done;
+    da.out = out;
+    const int grid = (int)std::min<uint64_t>((uint64_t)c->sm_count, max_items);
+    launch_decode((int)D, da, std::max(grid, 1), st);
+    c->launches++;
+}
+
+}  // namespace
+
+namespace saap_b200 {
+void set_error(const std::string& m) { g_err = m; }
+[[noreturn]] void fail(int code, const std::string& msg) { throw Failure{code, msg}; }
+void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Failure{SAAP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+    }
+}
+}  // namespace saap_b200
+
+extern "C" {
+
+const char* saap_last_error(void) { return g_err.c_str(); }
+const char* saap_version(void) { return "saap_b200 0.1 (sm_100a)"; }
+
+// ============================================================ context
+int saap_ctx_create(int device, saap_ctx** out) {
+    return guard([&] {
+        need(out, "saap_ctx_create");
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            throw Failure{SAAP_ERR_NO_DEVICE, "no CUDA device visible: libsaap_b200 has no CPU path"};
+        }
+        if (device < 0 || device >= n) invalid("saap_ctx_create: device out of range");
+        cudaDeviceProp prop;
+        SAAP_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10)
+            throw Failure{SAAP_ERR_NO_DEVICE,
+                          std::string("libsaap_b200 needs an sm_100 (B200) device, found ") +
+                                  prop.name};
+        SAAP_CUDA(cudaSetDevice(device));
+        auto* c = new saap_ctx;
+        c->device = device;
+        c->sm_count = prop.multiProcessorCount;
+        SAAP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+        c->counters = dmalloc<StepCounters>(1);
+        SAAP_CUDA(cudaMemset(c->counters, 0, sizeof(StepCounters)));
+        ensure_done(c, 4096);
+        *out = c;
+    });
+}
+
+int saap_ctx_destroy(saap_ctx* c) {
+    return guard([&] {
+        if (!c) return;
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->stream);
+        for (saap_scratch* s : {&c->items, &c->qslots, &c->part_O, &c->part_ml, &c->probs, &c->stats,
+                                &c->sel, &c->qr, &c->qd, &c->out, &c->misc, &c->zeros})
+            if (s->p) cudaFree(s->p);
+        dfree(c->counters);
+        dfree(c->done);
+        if (c->own_stream) cudaStreamDestroy(c->stream);
+        delete c;
+    });
+}
+
+int saap_ctx_set_stream(saap_ctx* c, void* stream) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        if (c->own_stream) {
+            SAAP_CUDA(cudaStreamSynchronize(c->stream));
+            cudaStreamDestroy(c->stream);
+        }
+        c->stream = (cudaStream_t)stream;
+        c->own_stream = false;
+    });
+}
+
+int saap_ctx_get_stream(saap_ctx* c, void** stream) {
+    return guard([&] {
+        need(c, "ctx");
+        need(stream, "stream");
+        *stream = (void*)c->stream;
+    });
+}
+
+int saap_ctx_synchronize(saap_ctx* c) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        sync(c);
+    });
+}
+
+int saap_ctx_sm_count(saap_ctx* c, int* out) {
+    return guard([&] {
+        need(c, "ctx");
+        *out = c->sm_count;
+    });
+}
+
+int saap_ctx_launch_count(saap_ctx* c, uint64_t* out) {
+    return guard([&] {
+        need(c, "ctx");
+        *out = c->launches;
+    });
+}
+
+// ============================================================ partitions / models / routers
+int saap_partition_create(saap_ctx* c, const float* cent, uint64_t C, uint64_t d,
+                          saap_partition** out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(cent, "saap_partition_create");
+        if (C == 0 || d == 0) invalid("Partition: empty centroid block");
+        auto* p = new saap_partition;
+        p->ctx = c;
+        p->C = C;
+        p->d = d;
+        p->host.assign(cent, cent + C * d);
+        std::vector<float> t(C * d);
+        std::vector<double> d64(C * d);
+        for (uint64_t i = 0; i < C; ++i)
+            for (uint64_t j = 0; j < d; ++j) {
+                t[j * C + i] = cent[i * d + j];
+                d64[i * d + j] = (double)cent[i * d + j];
+            }
+        p->cent = dmalloc<float>(C * d);
+        p->centT = dmalloc<float>(C * d);
+        p->cent64 = dmalloc<double>(C * d);
+        SAAP_CUDA(cudaMemcpy(p->cent, cent, C * d * 4, cudaMemcpyHostToDevice));
+        SAAP_CUDA(cudaMemcpy(p->centT, t.data(), C * d * 4, cudaMemcpyHostToDevice));
+        SAAP_CUDA(cudaMemcpy(p->cent64, d64.data(), C * d * 8, cudaMemcpyHostToDevice));
+        *out = p;
+    });
+}
+
+int saap_partition_destroy(saap_partition* p) {
+    return guard([&] {
+        if (!p) return;
+        cudaSetDevice(p->ctx->device);
+        dfree(p->cent);
+        dfree(p->centT);
+        dfree(p->cent64);
+        delete p;
+    });
+}
+
+int saap_qmodel_create(saap_ctx* c, uint64_t d, uint64_t h, uint64_t C, const double* w1,
+                       const double* b1, const double* gamma, const double* beta,
+                       const double* mean, const double* var, const double* w2, const double* b2,
+                       saap_qmodel** out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        if (d == 0 || h == 0 || C == 0) invalid("qmodel_init: zero dimension");
+        for (auto* p : {w1, b1, gamma, beta, mean, var, w2, b2}) need(p, "saap_qmodel_create");
+        const size_t smem = 4 * (d + h + C) * sizeof(double);
+        if (smem > 227 * 1024) unsupported("Q-model router: d + h + C too large for one CTA");
+        auto* m = new saap_qmodel;
+        m->ctx = c;
+        m->d = d;
+        m->h = h;
+        m->C = C;
+        m->w1 = dmalloc<double>(d * h);
+        m->w2 = dmalloc<double>(h * C);
+        m->vec = dmalloc<double>(5 * h + C);
+        SAAP_CUDA(cudaMemcpy(m->w1, w1, d * h * 8, cudaMemcpyHostToDevice));
+        SAAP_CUDA(cudaMemcpy(m->w2, w2, h * C * 8, cudaMemcpyHostToDevice));
+        const double* parts[5] = {b1, gamma, beta, mean, var};
+        for (int i = 0; i < 5; ++i)
+            SAAP_CUDA(cudaMemcpy(m->vec + i * h, parts[i], h * 8, cudaMemcpyHostToDevice));
+        SAAP_CUDA(cudaMemcpy(m->vec + 5 * h, b2, C * 8, cudaMemcpyHostToDevice));
+        *out = m;
+    });
+}
+
+int saap_qmodel_destroy(saap_qmodel* m) {
+    return guard([&] {
+        if (!m) return;
+        cudaSetDevice(m->ctx->device);
+        dfree(m->w1);
+        dfree(m->w2);
+        dfree(m->vec);
+        delete m;
+    });
+}
+
+int saap_router_create_centroid(saap_ctx* c, const saap_partition* p, int use_deroped,
+                                saap_router** out) {
+    return guard([&] {
+        need(c, "ctx");
+        need(p, "CentroidRouter: partition");
+        auto* r = new saap_router;
+        r->kind = 0;
+        r->use_deroped = use_deroped ? 1 : 0;
+        r->part = p;
+        *out = r;
+    });
+}
+
+int saap_router_create_qmodel(saap_ctx* c, const saap_qmodel* m, saap_router** out) {
+    return guard([&] {
+        need(c, "ctx");
+        need(m, "QModelRouter: model");
+        auto* r = new saap_router;
+        r->kind = 1;
+        r->model = m;
+        *out = r;
+    });
+}
+
+int saap_router_destroy(saap_router* r) {
+    delete r;
+    return SAAP_OK;
+}
+
+// Standalone routing runs the same route_plan kernel as a decode step, in
+// route-only mode, for one query group.
+static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, uint64_t G,
+                       uint64_t d, uint64_t l, uint32_t* out) {
+    const uint64_t C = r->kind == 0 ? r->part->C : r->model->C;
+    const cudaStream_t st = c->stream;
+    float* dq = (float*)ensure(c, c->qd, G * d * 4);
+    h2d(dq, q_route, G * d * 4, st);
+    uint32_t* dsel = (uint32_t*)ensure(c, c->sel, l * 4);
+    GroupMeta gm{0, 0, 2, 0, 0, 0};  // n > sink + recent so routing runs
+    GroupMeta* dmeta = (GroupMeta*)ensure(c, c->misc, sizeof(GroupMeta) + 2 * sizeof(void*) * 3);
+    void** dptr = reinterpret_cast<void**>(reinterpret_cast<char*>(dmeta) + sizeof(GroupMeta));
+    void* ptrs[3];
+    int mode;
+    double* probs = nullptr;
+    if (r->kind == 0) {
+        ptrs[0] = (void*)r->part->centT;
+        mode = 1;
+    } else {
+        ptrs[0] = (void*)r->model->w1;
+        ptrs[1] = (void*)r->model->w2;
+        ptrs[2] = (void*)r->model->vec;
+        mode = 2;
+        probs = (double*)ensure(c, c->probs, G * C * 8);
+    }
+    h2d(dmeta, &gm, sizeof gm, st);
+    h2d(dptr, ptrs, sizeof(void*) * 3, st);
+    if (mode == 2) {
+        QModelArgs qa{};
+        qa.q = dq;
+        qa.prm = (const double* const*)dptr;
+        qa.G = (uint32_t)G;
+        qa.d = (uint32_t)d;
+        qa.h = (uint32_t)r->model->h;
+        qa.C = (uint32_t)C;
+        qa.probs = probs;
+        launch_qmodel_probs(qa, 1, st);
+        c->launches++;
+    }
+    PlanArgs pa{};
+    pa.meta = dmeta;
+    pa.C = (uint32_t)C;
+    pa.mode = mode;
+    pa.centT = (const float* const*)dptr;
+    pa.q_route = dq;
+    pa.scores = probs;
+    pa.G = (uint32_t)G;
+    pa.D = (uint32_t)d;
+    pa.n_hchunks = 1;
+    pa.probes = (uint32_t)l;
+    pa.recent = 0;
+    pa.item_keys = kItemKeysSparse;
+    pa.P2 = next_pow2((uint32_t)C);
+    pa.route_only = 1;
+    pa.selected = dsel;
+    launch_route_plan(pa, 1, st);
+    c->launches++;
+    d2h(out, dsel, l * 4, st);
+    sync(c);
+}
+
+int saap_router_select(saap_ctx* c, const saap_router* r, const float* q_roped,
+                       const float* q_deroped, uint64_t G, uint64_t d, uint64_t l, uint32_t* out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(r, "router");
+        if (l == 0) return;  // attention.cpp:278-280, 311-313
+        check_router_dims(r, d, 0, l);
+        if (G == 0) invalid("qmodel: empty query batch");
+        const bool deroped = r->kind == 1 || r->use_deroped;
+        const float* q = deroped ? q_deroped : q_roped;
+        need(q, "router queries");
+        route_once(c, r, q, G, d, l, out);
+    });
+}
+
+int saap_batched_bucket_select(saap_ctx* c, const saap_qmodel* m, const float* q, uint64_t G,
+                               uint64_t d, uint64_t l, uint32_t* out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(m, "model");
+        saap_router r;
+        r.kind = 1;
+        r.model = m;
+        check_router_dims(&r, d, 0, l);
+        if (G == 0) invalid("qmodel: empty query batch");
+        route_once(c, &r, q, G, d, l, out);
+    });
+}
+
+// ============================================================ assignment / IVF / rope
+int saap_assign_keys(saap_ctx* c, const saap_partition* p, const float* keys, uint64_t n,
+                     uint64_t d, uint32_t* out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(p, "assign_keys: partition");
+        if (d != p->d)
+            invalid("assign_key: key dim " + std::to_string(d) + " does not match centroids " +
+                    std::to_string(p->C) + "x" + std::to_string(p->d));
+        if (!supported_dim(d)) unsupported("assign_keys: unsupported key dim " + std::to_string(d));
+        if (n == 0) return;
+        const cudaStream_t st = c->stream;
+        float* dk = (float*)ensure(c, c->qr, n * d * 4);
+        h2d(dk, keys, n * d * 4, st);
+        std::vector<GroupMeta> meta{GroupMeta{0, 0, (uint32_t)n, 0, 0, 0}};
+        std::vector<TileDesc> tiles;
+        std::vector<uint32_t> first;
+        build_tiles(meta, tiles, first);
+        char* base = (char*)ensure(c, c->misc, tiles.size() * sizeof(TileDesc) + 64 + n * 4);
+        TileDesc* dt = (TileDesc*)base;
+        uint64_t* zero64 = (uint64_t*)(base + tiles.size() * sizeof(TileDesc));
+        const double** dc = (const double**)(zero64 + 1);
+        uint32_t* dout = (uint32_t*)(base + tiles.size() * sizeof(TileDesc) + 64);
+        const uint64_t z = 0;
+        const double* cp = p->cent64;
+        h2d(dt, tiles.data(), tiles.size() * sizeof(TileDesc), st);
+        h2d(zero64, &z, 8, st);
+        h2d(dc, &cp, sizeof cp, st);
+        launch_assign_exact((int)d, false, dt, (uint32_t)tiles.size(), dk, zero64, dc,
+                            (uint32_t)p->C, dout, zero64, st);
+        c->launches++;
+        d2h(out, dout, n * 4, st);
+        sync(c);
+    });
+}
+
+int saap_build_ivf(saap_ctx* c, const uint32_t* assignment, uint64_t n, uint64_t C, uint64_t* off,
+                   uint64_t* idx) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        for (uint64_t i = 0; i < n; ++i)
+            if (assignment[i] >= C)
+                invalid("build_ivf: bucket id " + std::to_string(assignment[i]) +
+                        " out of range for " + std::to_string(C) + " buckets");
+        if (n >= 0xFFFFFFFFull) unsupported("build_ivf: more than 2^32-1 keys");
+        const cudaStream_t st = c->stream;
+        std::vector<GroupMeta> meta{GroupMeta{0, 0, (uint32_t)n, 0, 0, 0}};
+        std::vector<TileDesc> tiles;
+        std::vector<uint32_t> first;
+        build_tiles(meta, tiles, first);
+        const size_t nt = tiles.size();
+        // one scratch block: meta | tiles | first | hist | countA | off | offA | assign | idx | invA
+        size_t o = 0;
+        auto take = [&](size_t bytes) {
+            size_t r = o;
+            o += (bytes + 255) & ~size_t(255);
+            return r;
+        };
+        const size_t o_meta = take(sizeof(GroupMeta)), o_tiles = take(nt * sizeof(TileDesc)),
+                     o_first = take(first.size() * 4), o_hist = take(nt * C * 4),
+                     o_cA = take(C * 4), o_off = take((C + 1) * 4), o_offA = take((C + 1) * 4),
+                     o_as = take(n * 4), o_idx = take(n * 4), o_inv = take(n * 4);
+        char* b = (char*)ensure(c, c->misc, o);
+        h2d(b + o_meta, meta.data(), sizeof(GroupMeta), st);
+        h2d(b + o_tiles, tiles.data(), nt * sizeof(TileDesc), st);
+        h2d(b + o_first, first.data(), first.size() * 4, st);
+        h2d(b + o_as, assignment, n * 4, st);
+        launch_pack(32, (TileDesc*)(b + o_tiles), (uint32_t)nt, (uint32_t*)(b + o_first), 1,
+                    (GroupMeta*)(b + o_meta), (uint32_t*)(b + o_as), (uint32_t)C,
+                    (uint32_t*)(b + o_hist), (uint32_t*)(b + o_cA), (uint32_t*)(b + o_off),
+                    (uint32_t*)(b + o_offA), (uint32_t*)(b + o_idx), (uint32_t*)(b + o_inv),
+                    nullptr, nullptr, nullptr, nullptr, nullptr, st);
+        c->launches += 3;
+        std::vector<uint32_t> off32(C + 1), idx32(n);
+        d2h(off32.data(), b + o_off, (C + 1) * 4, st);
+        d2h(idx32.data(), b + o_idx, n * 4, st);
+        sync(c);
+        for (uint64_t i = 0; i <= C; ++i) off[i] = off32[i];
+        for (uint64_t i = 0; i < n; ++i) idx[i] = idx32[i];
+    });
+}
+
+int saap_rope_remove(saap_ctx* c, const float* x, uint64_t rows, uint64_t d,
+                     const uint64_t* positions, double base, float* out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        if (d == 0 || d % 2)
+            invalid("RopeConfig: dim must be even and positive, got " + std::to_string(d));
+        if (!(base > 0.0)) invalid("RopeConfig: base_theta must be positive");
+        if (rows == 0) return;
+        const cudaStream_t st = c->stream;
+        std::vector<double> cs = rope_table(positions, rows, d, base);
+        float* dx = (float*)ensure(c, c->qr, rows * d * 4);
+        float* dy = (float*)ensure(c, c->out, rows * d * 4);
+        double* dcs = (double*)ensure(c, c->misc, cs.size() * 8);
+        h2d(dx, x, rows * d * 4, st);
+        h2d(dcs, cs.data(), cs.size() * 8, st);
+        launch_derope(dx, dcs, rows, (uint32_t)d, dy, st);
+        c->launches++;
+        d2h(out, dy, rows * d * 4, st);
+        sync(c);
+    });
+}
+
+// ============================================================ layers (context stores)
+int saap_layer_create(saap_ctx* c, uint64_t n_groups, uint64_t d, uint64_t C,
+                      const uint64_t* n_keys, uint64_t sink, uint64_t recent_hint,
+                      saap_layer** out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(n_keys, "saap_layer_create: n_keys");
+        if (n_groups == 0) invalid("saap_layer_create: no groups");
+        if (!supported_dim(d)) unsupported("store: unsupported head dim " + std::to_string(d));
+        if (C == 0) invalid("Partition: empty centroid block");
+        if (C > 16384) unsupported("store: more than 16384 buckets per head");
+        auto* L = new saap_layer;
+        L->ctx = c;
+        L->n_groups = n_groups;
+        L->d = d;
+        L->C = C;
+        L->sink = sink;
+        L->recent_hint = recent_hint;
+        uint64_t rows = 0, ns = 0;
+        for (uint64_t g = 0; g < n_groups; ++g) {
+            const uint64_t n = n_keys[g];
+            if (n <= sink) {
+                delete L;
+                invalid("build_context_store: no keys left to index after " + std::to_string(sink) +
+                        " sink keys");
+            }
+            if (n >= (1ull << 30)) {
+                delete L;
+                unsupported("store: context longer than 2^30 keys");
+            }
+            const uint64_t T = n > sink + recent_hint ? n - recent_hint : sink;
+            L->h_meta.push_back(GroupMeta{rows, ns, (uint32_t)n, (uint32_t)sink, (uint32_t)T, 0});
+            rows += n;
+            ns += n - sink;
+        }
+        L->total_rows = rows;
+        L->total_ns = ns;
+        L->meta = dmalloc<GroupMeta>(n_groups);
+        L->row_base = dmalloc<uint64_t>(n_groups);
+        L->K = dmalloc<uint16_t>(rows * d);
+        L->V = dmalloc<uint16_t>(rows * d);
+        L->assign = dmalloc<uint32_t>(ns);
+        L->idx = dmalloc<uint32_t>(ns);
+        L->invA = dmalloc<uint32_t>(ns);
+        L->list = dmalloc<uint32_t>(ns);
+        L->off = dmalloc<uint32_t>(n_groups * (C + 1));
+        L->offA = dmalloc<uint32_t>(n_groups * (C + 1));
+        std::vector<TileDesc> tiles;
+        std::vector<uint32_t> first;
+        build_tiles(L->h_meta, tiles, first);
+        L->n_tiles = (uint32_t)tiles.size();
+        L->tiles = dmalloc<TileDesc>(tiles.size());
+        L->tile_first = dmalloc<uint32_t>(first.size());
+        L->hist = dmalloc<uint32_t>(tiles.size() * C);
+        L->countA = dmalloc<uint32_t>(n_groups * C);
+        L->d_cent64 = (const double**)(dmalloc<void*>(n_groups));
+        std::vector<uint64_t> rb(n_groups);
+        for (uint64_t g = 0; g < n_groups; ++g) rb[g] = L->h_meta[g].row_base;
+        SAAP_CUDA(cudaMemcpy(L->meta, L->h_meta.data(), n_groups * sizeof(GroupMeta),
+                             cudaMemcpyHostToDevice));
+        SAAP_CUDA(cudaMemcpy(L->row_base, rb.data(), n_groups * 8, cudaMemcpyHostToDevice));
+        SAAP_CUDA(cudaMemcpy(L->tiles, tiles.data(), tiles.size() * sizeof(TileDesc),
+                             cudaMemcpyHostToDevice));
+        SAAP_CUDA(cudaMemcpy(L->tile_first, first.data(), first.size() * 4, cudaMemcpyHostToDevice));
+        *out = L;
+    });
+}
+
+int saap_layer_destroy(saap_layer* L) {
+    return guard([&] {
+        if (!L) return;
+        cudaSetDevice(L->ctx->device);
+        cudaStreamSynchronize(L->ctx->stream);
+        dfree(L->meta);
+        dfree(L->row_base);
+        dfree(L->K);
+        dfree(L->V);
+        dfree(L->assign);
+        dfree(L->idx);
+        dfree(L->invA);
+        dfree(L->list);
+        dfree(L->off);
+        dfree(L->offA);
+        dfree(L->tiles);
+        dfree(L->tile_first);
+        dfree(L->hist);
+        dfree(L->countA);
+        dfree(L->d_cent64);
+        dfree(L->d_centT);
+        dfree(L->d_qm);
+        delete L;
+    });
+}
+
+static void bind_parts(saap_layer* L, const saap_partition* const* parts) {
+    need(parts, "build_context_store: partitions");
+    std::vector<const double*> p(L->n_groups);
+    L->parts.assign(parts, parts + L->n_groups);
+    for (uint64_t g = 0; g < L->n_groups; ++g) {
+        need(parts[g], "build_context_store: partition");
+        if (parts[g]->d != L->d)
+            invalid("assign_key: key dim " + std::to_string(L->d) + " does not match centroids " +
+                    std::to_string(parts[g]->C) + "x" + std::to_string(parts[g]->d));
+        if (parts[g]->C != L->C)
+            invalid("build_context_store: partition has " + std::to_string(parts[g]->C) +
+                    " buckets, store expects " + std::to_string(L->C));
+        p[g] = parts[g]->cent64;
+    }
+    SAAP_CUDA(cudaMemcpy(L->d_cent64, p.data(), p.size() * sizeof(void*), cudaMemcpyHostToDevice));
+}
+
+// assignment + pack from device bf16 sources laid out like the layer rows
+static void build_from_device(saap_layer* L, const uint16_t* Ksrc, const uint16_t* Vsrc,
+                              const void* keys_assign, bool assign_bf16) {
+    saap_ctx* c = L->ctx;
+    const cudaStream_t st = c->stream;
+    // assignment keys: rows sink + lid of each group (key_row0 = row_base + sink)
+    std::vector<uint64_t> kr0(L->n_groups), ob(L->n_groups);
+    for (uint64_t g = 0; g < L->n_groups; ++g) {
+        kr0[g] = L->h_meta[g].row_base + L->h_meta[g].sink;
+        ob[g] = L->h_meta[g].ivf_base;
+    }
+    uint64_t* d_kr0 = (uint64_t*)ensure(c, c->zeros, L->n_groups * 16);
+    uint64_t* d_ob = d_kr0 + L->n_groups;
+    h2d(d_kr0, kr0.data(), L->n_groups * 8, st);
+    h2d(d_ob, ob.data(), L->n_groups * 8, st);
+    launch_assign_exact((int)L->d, assign_bf16, L->tiles, L->n_tiles, keys_assign, d_kr0,
+                        L->d_cent64, (uint32_t)L->C, L->assign, d_ob, st);
+    c->launches++;
+    launch_pack((int)L->d, L->tiles, L->n_tiles, L->tile_first, (uint32_t)L->n_groups, L->meta,
+                L->assign, (uint32_t)L->C, L->hist, L->countA, L->off, L->offA, L->idx, L->invA,
+                Ksrc, Vsrc, L->row_base, L->K, L->V, st);
+    c->launches += 5;
+    L->built = true;
+}
+
+int saap_layer_build(saap_ctx* c, saap_layer* L, const saap_partition* const* parts,
+                     const float* keys_roped, const float* values, const float* keys_assign,
+                     double rope_base) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(L, "layer");
+        need(keys_roped, "build_context_store: keys");
+        need(values, "build_context_store: values");
+        bind_parts(L, parts);
+        const cudaStream_t st = c->stream;
+        const uint64_t elems = L->total_rows * L->d;
+        float* f32 = dmalloc<float>(elems);
+        uint16_t* Ks = dmalloc<uint16_t>(elems);
+        uint16_t* Vs = dmalloc<uint16_t>(elems);
+        try {
+            h2d(f32, keys_roped, elems * 4, st);
+            launch_f32_to_bf16(f32, Ks, elems, st);
+            h2d(f32, values, elems * 4, st);
+            launch_f32_to_bf16(f32, Vs, elems, st);
+            c->launches += 2;
+            // assignment keys (f32): caller's pre-RoPE keys, or de-rope on device
+            if (keys_assign) {
+                h2d(f32, keys_assign, elems * 4, st);
+            } else {
+                if (!(rope_base > 0.0)) invalid("RopeConfig: base_theta must be positive");
+                h2d(f32, keys_roped, elems * 4, st);
+                std::vector<uint64_t> pos(L->total_rows);
+                for (auto& gm : L->h_meta)
+                    for (uint32_t i = 0; i < gm.n; ++i) pos[gm.row_base + i] = i;
+                std::vector<double> cs = rope_table(pos.data(), L->total_rows, L->d, rope_base);
+                double* dcs = dmalloc<double>(cs.size());
+                float* der = dmalloc<float>(elems);
+                h2d(dcs, cs.data(), cs.size() * 8, st);
+                launch_derope(f32, dcs, L->total_rows, (uint32_t)L->d, der, st);
+                c->launches++;
+                sync(c);
+                cudaFree(dcs);
+                cudaFree(f32);
+                f32 = der;
+            }
+            build_from_device(L, Ks, Vs, f32, false);
+            sync(c);
+        } catch (...) {
+            cudaFree(f32);
+            cudaFree(Ks);
+            cudaFree(Vs);
+            throw;
+        }
+        cudaFree(f32);
+        cudaFree(Ks);
+        cudaFree(Vs);
+    });
+}
+
+int saap_layer_build_dev(saap_ctx* c, saap_layer* L, const saap_partition* const* parts,
+                         const void* keys_roped_bf16, const void* values_bf16,
+                         const void* keys_assign_bf16) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(L, "layer");
+        need(keys_roped_bf16, "build: keys");
+        need(values_bf16, "build: values");
+        need(keys_assign_bf16, "build: assignment keys");
+        bind_parts(L, parts);
+        build_from_device(L, (const uint16_t*)keys_roped_bf16, (const uint16_t*)values_bf16,
+                          keys_assign_bf16, true);
+    });
+}
+
+int saap_layer_read_index(saap_ctx* c, const saap_layer* L, uint64_t g, uint32_t* assignment,
+                          uint64_t* off, uint64_t* idx) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(L, "layer");
+        if (!L->built) invalid("store not built");
+        if (g >= L->n_groups) invalid("group out of range");
+        const GroupMeta& gm = L->h_meta[g];
+        const uint64_t ns = gm.n - gm.sink;
+        const cudaStream_t st = c->stream;
+        std::vector<uint32_t> off32(L->C + 1), idx32(ns);
+        if (assignment) d2h(assignment, L->assign + gm.ivf_base, ns * 4, st);
+        d2h(off32.data(), L->off + g * (L->C + 1), (L->C + 1) * 4, st);
+        d2h(idx32.data(), L->idx + gm.ivf_base, ns * 4, st);
+        sync(c);
+        if (off)
+            for (uint64_t i = 0; i <= L->C; ++i) off[i] = off32[i];
+        if (idx)
+            for (uint64_t i = 0; i < ns; ++i) idx[i] = idx32[i];
+    });
+}
+
+int saap_layer_packed_rows(const saap_layer* L, void** k, void** v, uint64_t* rows) {
+    return guard([&] {
+        need(L, "layer");
+        if (k) *k = L->K;
+        if (v) *v = L->V;
+        if (rows) *rows = L->total_rows;
+    });
+}
+
+static void validate_cfg(const saap_layer* L, const saap_sparse_cfg* cfg) {
+    need(cfg, "sparse_attention: cfg");
+    if (cfg->probes > L->C)
+        invalid("sparse_attention: probes " + std::to_string(cfg->probes) +
+                " exceed bucket count " + std::to_string(L->C));
+    if (cfg->block_size < 1) invalid("sparse_attention: block_size must be >= 1");
+    if (cfg->sink_count != L->sink)
+        invalid("sparse_attention: window sinks " + std::to_string(cfg->sink_count) +
+                " keys but the store indexes from id " + std::to_string(L->sink));
+}
+
+static uint64_t max_keys(const saap_layer* L) {
+    uint64_t m = 0;
+    for (auto& gm : L->h_meta) m = std::max<uint64_t>(m, gm.n);
+    return m;
+}
+
+static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* const* routers,
+                       const float* qr, const float* qd, uint64_t G, const saap_sparse_cfg* cfg,
+                       float* out, saap_attn_stats* stats, uint32_t* selected) {
+    saap_layer* L = const_cast<saap_layer*>(Lc);
+    if (!L->built) invalid("store not built");
+    validate_cfg(L, cfg);
+    int mode = 3, use_deroped = 1;
+    const uint64_t maxn = max_keys(L);
+    // routers only run when some group's context exceeds the window (attention.cpp:336-351)
+    bool any_route = false;
+    for (auto& gm : L->h_meta) any_route |= gm.n > cfg->sink_count + cfg->recent_count;
+    if (cfg->probes > 0 && any_route) {
+        need(routers, "sparse_attention: routers");
+        bind_routers(L, routers, mode, use_deroped);
+        for (uint64_t g = 0; g < L->n_groups; ++g) check_router_dims(routers[g], L->d, L->C, cfg->probes);
+    }
+    const float* q_route = (mode == 2 || (mode == 1 && use_deroped)) ? qd : qr;
+    if (mode != 3) need(q_route, "sparse_attention: routing queries");
+    uint64_t hq = 0;
+    if (mode == 2) hq = L->cached_routers[0]->model->h;
+    // Q-model hidden width must be uniform (kernel reads it from args)
+    if (mode == 2)
+        for (auto* r : L->cached_routers)
+            if (r->model->h != hq) unsupported("sparse_attention: Q-models with different widths");
+    enqueue_decode(c, L->n_groups, L->d, L->C, L->meta, L->row_base, maxn, L->off, L->offA, L->idx,
+                   L->assign, L->invA, L->list, L->K, L->V, mode, L->d_centT, L->d_qm, qr, q_route,
+                   G, cfg->probes, cfg->recent_count, out, stats, selected, kItemKeysSparse,
+                   (uint32_t)hq);
+}
+
+int saap_sparse_attention_dev(saap_ctx* c, const saap_layer* L, const saap_router* const* routers,
+                              const float* qr, const float* qd, uint64_t G,
+                              const saap_sparse_cfg* cfg, float* out, saap_attn_stats* stats,
+                              uint32_t* selected) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(L, "layer");
+        need(qr, "sparse_attention: queries");
+        need(out, "sparse_attention: out");
+        if (G == 0) return;
+        sparse_dev(c, L, routers, qr, qd, G, cfg, out, stats, selected);
+    });
+}
+
+int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* const* routers,
+                          const float* q_roped, const float* q_deroped, uint64_t G,
+                          const saap_sparse_cfg* cfg, float* out, saap_attn_stats* stats,
+                          uint32_t* selected) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(L, "layer");
+        need(q_roped, "sparse_attention: queries");
+        need(out, "sparse_attention: out");
+        if (G == 0) return;
+        validate_cfg(L, cfg);
+        const cudaStream_t st = c->stream;
+        const uint64_t qn = L->n_groups * G * L->d;
+        float* dqr = (float*)ensure(c, c->qr, qn * 4);
+        float* dqd = nullptr;
+        h2d(dqr, q_roped, qn * 4, st);
+        if (q_deroped) {
+            dqd = (float*)ensure(c, c->qd, qn * 4);
+            h2d(dqd, q_deroped, qn * 4, st);
+        }
+        float* dout = (float*)ensure(c, c->out, qn * 4);
+        saap_attn_stats* dst = (saap_attn_stats*)ensure(c, c->stats, L->n_groups * sizeof(saap_attn_stats));
+        uint32_t* dsel = selected ? (uint32_t*)ensure(c, c->sel, L->n_groups * std::max<uint64_t>(cfg->probes, 1) * 4) : nullptr;
+        sparse_dev(c, L, routers, dqr, dqd, G, cfg, dout, dst, dsel);
+        d2h(out, dout, qn * 4, st);
+        if (stats) d2h(stats, dst, L->n_groups * sizeof(saap_attn_stats), st);
+        if (selected && cfg->probes) d2h(selected, dsel, L->n_groups * cfg->probes * 4, st);
+        sync(c);
+    });
+}
+
+int saap_layer_full_attention(saap_ctx* c, const saap_layer* L, const float* q, uint64_t G,
+                              float* out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(L, "layer");
+        if (!L->built) invalid("store not built");
+        if (G == 0) return;
+        const cudaStream_t st = c->stream;
+        const uint64_t qn = L->n_groups * G * L->d;
+        float* dq = (float*)ensure(c, c->qr, qn * 4);
+        float* dout = (float*)ensure(c, c->out, qn * 4);
+        h2d(dq, q, qn * 4, st);
+        enqueue_decode(c, L->n_groups, L->d, L->C, L->meta, L->row_base, max_keys(L), L->off,
+                       L->offA, L->idx, L->assign, L->invA, L->list, L->K, L->V, 0, nullptr,
+                       nullptr, dq, nullptr, G, 0, 0, dout, nullptr, nullptr, kItemKeysDense);
+        d2h(out, dout, qn * 4, st);
+        sync(c);
+    });
+}
+
+int saap_full_attention(saap_ctx* c, const float* q, uint64_t G, const float* keys,
+                        const float* values, uint64_t n, uint64_t d, float* out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        if (n == 0) invalid("full_attention: empty key set");
+        if (!supported_dim(d)) unsupported("full_attention: unsupported head dim " + std::to_string(d));
+        if (n >= (1ull << 30)) unsupported("full_attention: more than 2^30 keys");
+        if (G == 0) return;
+        const cudaStream_t st = c->stream;
+        float* f32 = dmalloc<float>(n * d);
+        uint16_t* Kb = dmalloc<uint16_t>(n * d);
+        uint16_t* Vb = dmalloc<uint16_t>(n * d);
+        h2d(f32, keys, n * d * 4, st);
+        launch_f32_to_bf16(f32, Kb, n * d, st);
+        h2d(f32, values, n * d * 4, st);
+        launch_f32_to_bf16(f32, Vb, n * d, st);
+        c->launches += 2;
+        GroupMeta gm{0, 0, (uint32_t)n, 0, 0, 0};
+        char* b = (char*)ensure(c, c->misc, 256 + 64);
+        GroupMeta* dm = (GroupMeta*)b;
+        uint64_t* drb = (uint64_t*)(b + 256);
+        const uint64_t z = 0;
+        h2d(dm, &gm, sizeof gm, st);
+        h2d(drb, &z, 8, st);
+        float* dq = (float*)ensure(c, c->qr, G * d * 4);
+        float* dout = (float*)ensure(c, c->out, G * d * 4);
+        h2d(dq, q, G * d * 4, st);
+        enqueue_decode(c, 1, d, 1, dm, drb, n, nullptr, nullptr, nullptr, nullptr, nullptr,
+                       nullptr, Kb, Vb, 0, nullptr, nullptr, dq, nullptr, G, 0, 0, dout, nullptr,
+                       nullptr, kItemKeysDense);
+        d2h(out, dout, G * d * 4, st);
+        sync(c);
+        cudaFree(f32);
+        cudaFree(Kb);
+        cudaFree(Vb);
+    });
+}
+
+// ============================================================ dense baseline cache
+int saap_kvcache_create(saap_ctx* c, uint64_t n_groups, uint64_t d, const void* K, const void* V,
+                        const uint64_t* row_base, const uint64_t* n_keys, saap_kvcache** out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        if (!supported_dim(d)) unsupported("kvcache: unsupported head dim " + std::to_string(d));
+        need(K, "kvcache: keys");
+        need(V, "kvcache: values");
+        auto* kc = new saap_kvcache;
+        kc->ctx = c;
+        kc->n_groups = n_groups;
+        kc->d = d;
+        kc->K = (const uint16_t*)K;
+        kc->V = (const uint16_t*)V;
+        std::vector<GroupMeta> m(n_groups);
+        for (uint64_t g = 0; g < n_groups; ++g) {
+            if (n_keys[g] == 0) {
+                delete kc;
+                invalid("full_attention: empty key set");
+            }
+            m[g] = GroupMeta{row_base[g], 0, (uint32_t)n_keys[g], 0, 0, 0};
+            kc->max_n = std::max<uint64_t>(kc->max_n, n_keys[g]);
+        }
+        kc->meta = dmalloc<GroupMeta>(n_groups);
+        kc->row_base = dmalloc<uint64_t>(n_groups);
+        SAAP_CUDA(cudaMemcpy(kc->meta, m.data(), n_groups * sizeof(GroupMeta), cudaMemcpyHostToDevice));
+        SAAP_CUDA(cudaMemcpy(kc->row_base, row_base, n_groups * 8, cudaMemcpyHostToDevice));
+        *out = kc;
+    });
+}
+
+int saap_kvcache_destroy(saap_kvcache* kc) {
+    return guard([&] {
+        if (!kc) return;
+        cudaSetDevice(kc->ctx->device);
+        dfree(kc->meta);
+        dfree(kc->row_base);
+        delete kc;
+    });
+}
+
+int saap_dense_attention_dev(saap_ctx* c, const saap_kvcache* kc, const float* q, uint64_t G,
+                             float* out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(kc, "kvcache");
+        if (G == 0) return;
+        enqueue_decode(c, kc->n_groups, kc->d, 1, kc->meta, kc->row_base, kc->max_n, nullptr,
+                       nullptr, nullptr, nullptr, nullptr, nullptr, kc->K, kc->V, 0, nullptr,
+                       nullptr, q, nullptr, G, 0, 0, out, nullptr, nullptr, kItemKeysDense);
+    });
+}
+
+// ============================================================ graphs
+int saap_graph_begin(saap_ctx* c) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        SAAP_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        c->capturing = true;
+    });
+}
+
+int saap_graph_end(saap_ctx* c, saap_graph** out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        c->capturing = false;
+        auto* g = new saap_graph;
+        SAAP_CUDA(cudaStreamEndCapture(c->stream, &g->graph));
+        SAAP_CUDA(cudaGraphInstantiate(&g->exec, g->graph, 0));
+        *out = g;
+    });
+}
+
+int saap_graph_launch(saap_ctx* c, saap_graph* g) {
+    return guard([&] {
+        need(g, "graph");
+        SAAP_CUDA(cudaGraphLaunch(g->exec, c->stream));
+    });
+}
+
+int saap_graph_destroy(saap_graph* g) {
+    return guard([&] {
+        if (!g) return;
+        if (g->exec) cudaGraphExecDestroy(g->exec);
+        if (g->graph) cudaGraphDestroy(g->graph);
+        delete g;
+    });
+}
+
+// ============================================================ diagnostics
+int saap_debug_exp(saap_ctx* c, const double* x, uint64_t n, double* out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        if (!n) return;
+        double* dx = (double*)ensure(c, c->misc, n * 16);
+        h2d(dx, x, n * 8, c->stream);
+        launch_debug_exp(dx, n, dx + n, c->stream);
+        c->launches++;
+        d2h(out, dx + n, n * 8, c->stream);
+        sync(c);
+    });
+}
+
+// ============================================================ synthetic data
+int saap_synth_fill_dev(saap_ctx* c, void* out, uint64_t rows, uint64_t d, uint64_t seed, int kind,
+                        const float* centers, uint64_t n_centers, float center_scale, float noise) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(out, "synth: out");
+        if (kind == 1 && (!centers || n_centers == 0)) invalid("synth: clustered keys need centers");
+        launch_synth((uint16_t*)out, rows, (uint32_t)d, seed, kind, centers, n_centers, center_scale,
+                     noise, c->stream);
+        c->launches++;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,228 @@
+// Shared device helpers and internal types of libsaap_b200 (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "saap_b200.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libsaap_b200 is written for sm_100a (B200) only"
+#endif
+
+namespace saap_b200 {
+
+// ---------------------------------------------------------------- errors
+struct Error {
+    int code;
+    std::string msg;
+};
+void set_error(const std::string& m);
+[[noreturn]] void fail(int code, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what);
+#define SAAP_CUDA(x) ::saap_b200::check_cuda((x), #x)
+
+// ---------------------------------------------------------------- layout
+// One (sequence, KV head) context of a layer.
+struct GroupMeta {
+    uint64_t row_base;  // first packed K/V row of this group
+    uint64_t ivf_base;  // first entry of this group in assign/idx/invA (sum of N_s before)
+    uint32_t n;         // keys incl. the sink span
+    uint32_t sink;      // id_offset
+    uint32_t T;         // rows [sink,T) bucket-packed, [T,n) position order
+    uint32_t pad;
+};
+
+// A unit of decode work: up to item_keys consecutive keys of one segment,
+// for one query slot (group, chunk of <= 4 query heads).
+struct Item {
+    uint32_t qslot;
+    uint32_t n_kind;  // n (low 30 bits) | kind << 30
+    uint64_t start;   // kind 0: first row (group-relative); kind 1/2: list index (absolute)
+};
+enum : uint32_t { KIND_ROWS = 0, KIND_INVA = 1, KIND_LIST = 2 };
+
+constexpr uint32_t kPackTile = 2048;  // local ids per histogram / assignment tile
+
+struct TileDesc {
+    uint32_t group;
+    uint32_t first;  // first local id (0-based, after the sink span)
+    uint32_t count;
+    uint32_t pad;
+};
+
+struct QSlot {
+    uint32_t base;   // first item
+    uint32_t count;  // items
+};
+
+// Per-step device counters (zeroed with one memset at the start of a step).
+struct StepCounters {
+    uint32_t n_items;
+    uint32_t work;
+    uint32_t pad[30];
+};
+
+constexpr int kHeadsPerSlot = 4;  // query heads processed together (GQA group)
+constexpr int kTileKeys = 64;     // keys per smem stage
+constexpr int kComputeWarps = 8;
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ float bf16lo(uint32_t x) { return __uint_as_float(x << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t x) { return __uint_as_float(x & 0xFFFF0000u); }
+
+__device__ __forceinline__ uint16_t f32_to_bf16_rne(float f) {
+    uint32_t u = __float_as_uint(f);
+    uint32_t lsb = (u >> 16) & 1u;
+    return (uint16_t)((u + 0x7FFFu + lsb) >> 16);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+// 1-D bulk copy global -> shared (TMA engine), completes tx bytes on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];" ::"r"(smem_u32(dst)),
+            "l"(src), "r"(bytes), "r"(smem_u32(bar))
+            : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// ---------------------------------------------------------------- host side
+struct LaunchCounter {
+    uint64_t n = 0;
+};
+
+}  // namespace saap_b200
+
+// ---------------------------------------------------------------- handles
+struct saap_scratch {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+struct saap_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    uint64_t launches = 0;
+    // growable device scratch (sized by uncaptured calls; graphs reuse it)
+    saap_scratch items, qslots, part_O, part_ml, probs, stats, sel, qr, qd, out, misc, zeros;
+    saap_b200::StepCounters* counters = nullptr;  // persistent, 128 B
+    uint32_t* done = nullptr;                     // per query slot completion counters
+    size_t done_cap = 0;
+    // capture state
+    bool capturing = false;
+};
+
+struct saap_partition {
+    saap_ctx* ctx = nullptr;
+    uint64_t C = 0, d = 0;
+    float* cent = nullptr;     // C x d f32 (device)
+    float* centT = nullptr;    // d x C f32 (device, routing reads coalesced)
+    double* cent64 = nullptr;  // C x d fp64 (device, exact assignment)
+    std::vector<float> host;   // kept for validation / read-back
+};
+
+struct saap_qmodel {
+    saap_ctx* ctx = nullptr;
+    uint64_t d = 0, h = 0, C = 0;
+    double* w1 = nullptr;  // d x h
+    double* w2 = nullptr;  // h x C
+    double* vec = nullptr; // b1, gamma, beta, mean, var (5 x h) then b2 (C)
+};
+
+struct saap_router {
+    int kind = 0;  // 0 centroid, 1 qmodel
+    int use_deroped = 1;
+    const saap_partition* part = nullptr;
+    const saap_qmodel* model = nullptr;
+};
+
+struct saap_layer {
+    saap_ctx* ctx = nullptr;
+    uint64_t n_groups = 0, d = 0, C = 0, sink = 0, recent_hint = 0;
+    uint64_t total_rows = 0, total_ns = 0;
+    std::vector<saap_b200::GroupMeta> h_meta;
+    saap_b200::GroupMeta* meta = nullptr;
+    uint64_t* row_base = nullptr;  // device copy of h_meta[].row_base
+    uint16_t* K = nullptr;         // packed bf16 rows
+    uint16_t* V = nullptr;
+    uint32_t* assign = nullptr;  // total_ns
+    uint32_t* idx = nullptr;     // total_ns (local ids, ascending within bucket)
+    uint32_t* invA = nullptr;    // total_ns: position-sink -> packed row (region A)
+    uint32_t* list = nullptr;    // total_ns scratch for filtered window lists
+    uint32_t* off = nullptr;     // n_groups x (C+1)
+    uint32_t* offA = nullptr;    // n_groups x (C+1)
+    bool built = false;
+    // prefill work decomposition
+    saap_b200::TileDesc* tiles = nullptr;
+    uint32_t n_tiles = 0;
+    uint32_t* tile_first = nullptr;  // n_groups + 1
+    uint32_t* hist = nullptr;        // n_tiles x C
+    uint32_t* countA = nullptr;      // n_groups x C
+    const double** d_cent64 = nullptr;  // per group partition (exact assignment)
+    std::vector<const saap_partition*> parts;
+    // routing parameter table cache (device arrays of per-group pointers)
+    std::vector<const saap_router*> cached_routers;
+    const float** d_centT = nullptr;
+    const double** d_qm = nullptr;  // per group: w1, w2, vec (3 pointers)
+};
+
+struct saap_kvcache {
+    saap_ctx* ctx = nullptr;
+    uint64_t n_groups = 0, d = 0, max_n = 0;
+    const uint16_t* K = nullptr;  // borrowed
+    const uint16_t* V = nullptr;
+    saap_b200::GroupMeta* meta = nullptr;
+    uint64_t* row_base = nullptr;
+};
+
+struct saap_graph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+};

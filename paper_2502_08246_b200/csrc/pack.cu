@@ -1,0 +1,375 @@
+// Prefill side of SAAP: key assignment and the bucket-contiguous KV layout.
+//
+// Reference semantics (/root/reference/proj/core/src):
+//   best_bucket / assign_keys  partition.cpp:38-48, 181-198
+//   build_ivf                  partition.cpp:200-223  (stable counting sort)
+//   derope_indexed             attention.cpp:207-222, rotate_with rope.cpp:29-41
+#include "common.cuh"
+
+namespace saap_b200 {
+
+// ------------------------------------------------------------ exact assignment
+// argmax_c sum_j k_j c_cj with the sum in fp64 in index order; products of
+// f32 (or bf16) by f32 are exact in fp64, so each DFMA equals the reference's
+// mulsd+addsd pair.  Strict '>' in ascending c => lowest id
+// wins ties; the all-zero key stays on bucket 0.
+template <typename KT, int D>
+__global__ void __launch_bounds__(128) assign_exact_kernel(
+        const TileDesc* tiles, const KT* keys, const uint64_t* key_row0,
+        const double* const* cent64, uint32_t C, uint32_t* out, const uint64_t* out_base,
+        const uint32_t* sel_list, uint32_t sel_count) {
+    constexpr int CB = 32;  // centroids per smem chunk
+    __shared__ double sc[CB][D];
+    uint32_t lid, g;
+    bool active;
+    if (sel_list) {  // refine mode: explicit (group, local id) list
+        const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+        active = e < sel_count;
+        const uint32_t v = active ? sel_list[e] : 0;
+        g = tiles[0].group;  // refine lists are per single-group launch
+        lid = v;
+    } else {
+        const TileDesc td = tiles[blockIdx.x];
+        g = td.group;
+        lid = td.first + blockIdx.y * blockDim.x + threadIdx.x;
+        active = (blockIdx.y * blockDim.x + threadIdx.x) < td.count;
+    }
+    float k[D];
+    if (active) {
+        const KT* kp = keys + (key_row0[g] + lid) * D;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            if constexpr (sizeof(KT) == 2) k[j] = __uint_as_float(((uint32_t)kp[j]) << 16);
+            else k[j] = kp[j];
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j) k[j] = 0.f;
+    }
+    const double* cg = cent64[g];
+    double best = -INFINITY;
+    uint32_t best_id = 0;
+    for (uint32_t c0 = 0; c0 < C; c0 += CB) {
+        __syncthreads();
+        for (uint32_t e = threadIdx.x; e < CB * D; e += blockDim.x) {
+            const uint32_t cc = c0 + e / D;
+            sc[e / D][e % D] = cc < C ? cg[(size_t)cc * D + e % D] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int cc = 0; cc < CB; cc += 8) {
+            double s[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s[u] = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const double kd = (double)k[j];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) s[u] = fma(kd, sc[cc + u][j], s[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t c = c0 + cc + u;
+                if (c < C && s[u] > best) {
+                    best = s[u];
+                    best_id = c;
+                }
+            }
+        }
+    }
+    if (active) out[out_base[g] + lid] = best_id;
+}
+
+// ------------------------------------------------------------ histograms
+// hist[tile][c] = #keys of bucket c in the tile; countA[g][c] += #keys of
+// bucket c with position < T (region A).
+__global__ void __launch_bounds__(512) hist_kernel(const TileDesc* tiles, const GroupMeta* meta,
+                                                   const uint32_t* assign, uint32_t C,
+                                                   uint32_t* hist, uint32_t* countA) {
+    extern __shared__ uint32_t hs[];  // 2*C
+    uint32_t* h = hs;
+    uint32_t* hA = hs + C;
+    const TileDesc td = tiles[blockIdx.x];
+    const GroupMeta gm = meta[td.group];
+    for (uint32_t c = threadIdx.x; c < 2 * C; c += blockDim.x) hs[c] = 0;
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < td.count; e += blockDim.x) {
+        const uint32_t lid = td.first + e;
+        const uint32_t c = assign[gm.ivf_base + lid];
+        if (c >= C) continue;  // validated on the host for host inputs
+        atomicAdd(&h[c], 1u);
+        if (gm.sink + lid < gm.T) atomicAdd(&hA[c], 1u);
+    }
+    __syncthreads();
+    uint32_t* ht = hist + (size_t)blockIdx.x * C;
+    for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
+        ht[c] = h[c];
+        if (hA[c]) atomicAdd(&countA[(size_t)td.group * C + c], hA[c]);
+    }
+}
+
+// Per group: tile bases within each bucket (exclusive over tiles), then the
+// exclusive scans over buckets -> off (all keys) and offA (region A).
+__global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* tile_first, uint32_t C,
+                                                    uint32_t* hist, const uint32_t* countA,
+                                                    uint32_t* off, uint32_t* offA) {
+    extern __shared__ uint32_t tot[];  // 2*C
+    __shared__ uint32_t wsum[2][32];
+    const uint32_t g = blockIdx.x;
+    const uint32_t t0 = tile_first[g], t1 = tile_first[g + 1];
+    for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
+        uint32_t run = 0;
+        for (uint32_t t = t0; t < t1; ++t) {
+            uint32_t* p = hist + (size_t)t * C + c;
+            const uint32_t v = *p;
+            *p = run;
+            run += v;
+        }
+        tot[c] = run;
+        tot[C + c] = countA[(size_t)g * C + c];
+    }
+    __syncthreads();
+    // block exclusive scan of tot[0..C) and tot[C..2C): thread owns a chunk
+    const uint32_t per = (C + blockDim.x - 1) / blockDim.x;
+    const uint32_t lo = threadIdx.x * per, hi = min(C, lo + per);
+    uint32_t s0 = 0, s1 = 0;
+    for (uint32_t c = lo; c < hi; ++c) {
+        s0 += tot[c];
+        s1 += tot[C + c];
+    }
+    // warp inclusive scans
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t i0 = s0, i1 = s1;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t a0 = __shfl_up_sync(0xFFFFFFFFu, i0, o);
+        const uint32_t a1 = __shfl_up_sync(0xFFFFFFFFu, i1, o);
+        if (lane >= (uint32_t)o) {
+            i0 += a0;
+            i1 += a1;
+        }
+    }
+    if (lane == 31) {
+        wsum[0][warp] = i0;
+        wsum[1][warp] = i1;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w0 = lane < blockDim.x / 32 ? wsum[0][lane] : 0;
+        uint32_t w1 = lane < blockDim.x / 32 ? wsum[1][lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t a0 = __shfl_up_sync(0xFFFFFFFFu, w0, o);
+            const uint32_t a1 = __shfl_up_sync(0xFFFFFFFFu, w1, o);
+            if (lane >= (uint32_t)o) {
+                w0 += a0;
+                w1 += a1;
+            }
+        }
+        wsum[0][lane] = w0;
+        wsum[1][lane] = w1;
+    }
+    __syncthreads();
+    uint32_t e0 = i0 - s0 + (warp ? wsum[0][warp - 1] : 0);
+    uint32_t e1 = i1 - s1 + (warp ? wsum[1][warp - 1] : 0);
+    uint32_t* og = off + (size_t)g * (C + 1);
+    uint32_t* oAg = offA + (size_t)g * (C + 1);
+    for (uint32_t c = lo; c < hi; ++c) {
+        og[c] = e0;
+        oAg[c] = e1;
+        e0 += tot[c];
+        e1 += tot[C + c];
+    }
+    if (hi == C && lo < hi) {
+        og[C] = e0;
+        oAg[C] = e1;
+    }
+    if (C == 0 && threadIdx.x == 0) {
+        og[0] = 0;
+        oAg[0] = 0;
+    }
+}
+
+// ------------------------------------------------------------ rank + scatter
+// One warp per tile, 32 keys per step in id order: match_any groups equal
+// buckets, the leader bumps the tile's running base -> stable ranks, so idx
+// ascends within each bucket exactly as the reference's forward scatter.
+// Then the warp moves the 32 K/V rows to their packed rows.
+template <int D>
+__global__ void __launch_bounds__(128) scatter_kernel(
+        const TileDesc* tiles, uint32_t n_tiles, const GroupMeta* meta, const uint32_t* assign,
+        uint32_t C, uint32_t* hist, const uint32_t* off, const uint32_t* offA, uint32_t* idx,
+        uint32_t* invA, const uint16_t* Ksrc, const uint16_t* Vsrc, const uint64_t* src_row0,
+        uint16_t* Kdst, uint16_t* Vdst) {
+    const uint32_t warp_g = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const uint32_t lane = threadIdx.x & 31;
+    if (warp_g >= n_tiles) return;
+    const TileDesc td = tiles[warp_g];
+    const GroupMeta gm = meta[td.group];
+    uint32_t* ht = hist + (size_t)warp_g * C;
+    const uint32_t* og = off + (size_t)td.group * (C + 1);
+    const uint32_t* oAg = offA + (size_t)td.group * (C + 1);
+    constexpr int CH = D / 8;           // 16-byte chunks per row
+    constexpr int KPS = 32 / (2 * CH);  // keys per copy step (K and V chunks)
+    for (uint32_t e0 = 0; e0 < td.count; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        const bool act = e < td.count;
+        const uint32_t lid = td.first + e;
+        const uint32_t c = act ? assign[gm.ivf_base + lid] : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, c);
+        const uint32_t leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (act && lane == leader) {
+            base = ht[c];
+            ht[c] = base + __popc(peers);
+        }
+        base = __shfl_sync(0xFFFFFFFFu, base, leader);
+        const uint32_t r = base + __popc(peers & ((1u << lane) - 1));
+        uint32_t row = 0;
+        if (act) {
+            idx[gm.ivf_base + og[c] + r] = lid;
+            const uint32_t pos = gm.sink + lid;
+            if (pos < gm.T) {
+                row = gm.sink + oAg[c] + r;
+                invA[gm.ivf_base + lid] = row;
+            } else {
+                row = pos;
+            }
+        }
+        __syncwarp();
+        if (Ksrc) {
+            const uint32_t nk = min(32u, td.count - e0);
+            const uint64_t sbase = src_row0[td.group] + gm.sink + td.first + e0;
+            const uint64_t dbase = gm.row_base;
+            const int sub = lane / (2 * CH), ch = lane % (2 * CH);
+            const bool isv = ch >= CH;
+            const int cc = isv ? ch - CH : ch;
+#pragma unroll 4
+            for (uint32_t k0 = 0; k0 < 32; k0 += KPS) {
+                const uint32_t k = k0 + sub;
+                const uint32_t drow = __shfl_sync(0xFFFFFFFFu, row, k & 31);
+                if (k < nk) {
+                    const uint16_t* src = (isv ? Vsrc : Ksrc) + (sbase + k) * D + cc * 8;
+                    uint16_t* dst = (isv ? Vdst : Kdst) + (dbase + drow) * D + cc * 8;
+                    *reinterpret_cast<uint4*>(dst) = __ldcs(reinterpret_cast<const uint4*>(src));
+                }
+            }
+        }
+    }
+}
+
+// sink rows [0, sink) keep their position
+template <int D>
+__global__ void copy_sink_kernel(const GroupMeta* meta, uint32_t n_groups, const uint16_t* Ksrc,
+                                 const uint16_t* Vsrc, const uint64_t* src_row0, uint16_t* Kdst,
+                                 uint16_t* Vdst) {
+    const uint32_t g = blockIdx.x;
+    const GroupMeta gm = meta[g];
+    constexpr int CH = D / 8;
+    for (uint32_t e = threadIdx.x; e < gm.sink * CH; e += blockDim.x) {
+        const uint32_t r = e / CH, cc = e % CH;
+        const uint64_t s = (src_row0[g] + r) * D + cc * 8, d = (gm.row_base + r) * D + cc * 8;
+        *reinterpret_cast<uint4*>(Kdst + d) = *reinterpret_cast<const uint4*>(Ksrc + s);
+        *reinterpret_cast<uint4*>(Vdst + d) = *reinterpret_cast<const uint4*>(Vsrc + s);
+    }
+}
+
+// ------------------------------------------------------------ dtype + rope
+__global__ void f32_to_bf16_kernel(const float* in, uint16_t* out, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = f32_to_bf16_rne(in[i]);
+}
+
+// x' = (x0 c - x1 s, x0 s + x1 c) in fp64 with the products rounded before
+// the add (rope.cpp:32-39); (c, s) come from a host table computed with the
+// same libm calls as the reference, so the result is bit-identical.
+__global__ void derope_kernel(const float* x, const double* cs, uint64_t rows, uint32_t D,
+                              float* out) {
+    const uint64_t half = D / 2;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < rows * half;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = e / half, j = e % half;
+        const double c = cs[e * 2], s = cs[e * 2 + 1];
+        const double x0 = x[i * D + 2 * j], x1 = x[i * D + 2 * j + 1];
+        out[i * D + 2 * j] = (float)__dadd_rn(__dmul_rn(x0, c), -__dmul_rn(x1, s));
+        out[i * D + 2 * j + 1] = (float)__dadd_rn(__dmul_rn(x0, s), __dmul_rn(x1, c));
+    }
+}
+
+// ------------------------------------------------------------ launchers
+void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t n_tiles,
+                         const void* keys, const uint64_t* key_row0, const double* const* cent64,
+                         uint32_t C, uint32_t* out, const uint64_t* out_base, cudaStream_t st) {
+    dim3 grid(n_tiles, kPackTile / 128);
+#define SAAP_ASSIGN(DD)                                                                       \
+    if (bf16_keys)                                                                            \
+        assign_exact_kernel<uint16_t, DD><<<grid, 128, 0, st>>>(                              \
+                tiles, (const uint16_t*)keys, key_row0, cent64, C, out, out_base, nullptr, 0); \
+    else                                                                                      \
+        assign_exact_kernel<float, DD><<<grid, 128, 0, st>>>(                                 \
+                tiles, (const float*)keys, key_row0, cent64, C, out, out_base, nullptr, 0);
+    switch (D) {
+        case 128: SAAP_ASSIGN(128); break;
+        case 64: SAAP_ASSIGN(64); break;
+        case 32: SAAP_ASSIGN(32); break;
+        default: fail(SAAP_ERR_UNSUPPORTED, "assign_keys: unsupported key dim " + std::to_string(D));
+    }
+#undef SAAP_ASSIGN
+    SAAP_CUDA(cudaGetLastError());
+}
+
+void launch_pack(int D, const TileDesc* tiles, uint32_t n_tiles, const uint32_t* tile_first,
+                 uint32_t n_groups, const GroupMeta* meta, const uint32_t* assign, uint32_t C,
+                 uint32_t* hist, uint32_t* countA, uint32_t* off, uint32_t* offA, uint32_t* idx,
+                 uint32_t* invA, const uint16_t* Ksrc, const uint16_t* Vsrc,
+                 const uint64_t* src_row0, uint16_t* Kdst, uint16_t* Vdst, cudaStream_t st) {
+    const size_t hsm = (size_t)2 * C * 4;
+    static size_t cfg_h = 0, cfg_s = 0;
+    if (hsm > 48 * 1024 && hsm > cfg_h) {
+        SAAP_CUDA(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)hsm));
+        cfg_h = hsm;
+    }
+    if (hsm > 48 * 1024 && hsm > cfg_s) {
+        SAAP_CUDA(cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)hsm));
+        cfg_s = hsm;
+    }
+    SAAP_CUDA(cudaMemsetAsync(countA, 0, (size_t)n_groups * C * 4, st));
+    if (n_tiles) hist_kernel<<<n_tiles, 512, hsm, st>>>(tiles, meta, assign, C, hist, countA);
+    scan_kernel<<<n_groups, 1024, hsm, st>>>(tile_first, C, hist, countA, off, offA);
+    const uint32_t wpb = 4;
+    const uint32_t sgrid = (n_tiles + wpb - 1) / wpb;
+#define SAAP_SCATTER(DD)                                                                         \
+    if (sgrid)                                                                                   \
+        scatter_kernel<DD><<<sgrid, wpb * 32, 0, st>>>(tiles, n_tiles, meta, assign, C, hist, off, \
+                                                       offA, idx, invA, Ksrc, Vsrc, src_row0,    \
+                                                       Kdst, Vdst);                              \
+    if (Ksrc) copy_sink_kernel<DD><<<n_groups, 128, 0, st>>>(meta, n_groups, Ksrc, Vsrc, src_row0, \
+                                                             Kdst, Vdst);
+    switch (D) {
+        case 128: SAAP_SCATTER(128); break;
+        case 64: SAAP_SCATTER(64); break;
+        case 32: SAAP_SCATTER(32); break;
+        default: fail(SAAP_ERR_UNSUPPORTED, "pack: unsupported head dim " + std::to_string(D));
+    }
+#undef SAAP_SCATTER
+    SAAP_CUDA(cudaGetLastError());
+}
+
+void launch_f32_to_bf16(const float* in, uint16_t* out, uint64_t n, cudaStream_t st) {
+    if (!n) return;
+    const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 65535);
+    f32_to_bf16_kernel<<<(unsigned)blocks, 256, 0, st>>>(in, out, n);
+    SAAP_CUDA(cudaGetLastError());
+}
+
+void launch_derope(const float* x, const double* cs, uint64_t rows, uint32_t D, float* out,
+                   cudaStream_t st) {
+    const uint64_t n = rows * (D / 2);
+    if (!n) return;
+    const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 65535);
+    derope_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, cs, rows, D, out);
+    SAAP_CUDA(cudaGetLastError());
+}
+
+}  // namespace saap_b200
