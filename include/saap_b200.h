@@ -150,6 +150,15 @@ SAAP_API int saap_layer_build_dev(saap_ctx* ctx, saap_layer* L, const saap_parti
                          const void* keys_roped_bf16, const void* values_bf16,
                          const void* keys_assign_bf16);
 
+/* Assignment engine: 0 (default) = tcgen05 bf16 two-term-split GEMM with an
+ * fp64 re-check of near-tie keys (device bf16 keys, d = 128); 1 = fp64
+ * CUDA-core kernel only.  Both are bit-exact with assign_keys. */
+SAAP_API int saap_ctx_set_assign_mode(saap_ctx* ctx, int mode);
+/* After a build: whether the tensor-core path ran, and how many keys the
+ * fp64 re-check re-scored. */
+SAAP_API int saap_layer_assign_info(saap_ctx* ctx, const saap_layer* L, int* used_tensor_cores,
+                                    uint64_t* refined_keys);
+
 /* Read back ContextStore.assignment / index for group g (host). */
 SAAP_API int saap_layer_read_index(saap_ctx* ctx, const saap_layer* L, uint64_t group,
                           uint32_t* assignment, uint64_t* off, uint64_t* idx);
@@ -199,6 +208,14 @@ SAAP_API int saap_graph_begin(saap_ctx* ctx);
 SAAP_API int saap_graph_end(saap_ctx* ctx, saap_graph** out);
 SAAP_API int saap_graph_launch(saap_ctx* ctx, saap_graph* g);
 SAAP_API int saap_graph_destroy(saap_graph* g);
+
+/* Per-kernel device timing of decode steps issued while enabled (eager
+ * launches only): CUDA events bracket the route/plan kernel and the attention
+ * kernel on the context stream.  saap_ctx_timing synchronizes, returns the
+ * summed milliseconds and the number of steps, and clears the record. */
+SAAP_API int saap_ctx_enable_timing(saap_ctx* ctx, int on);
+SAAP_API int saap_ctx_timing(saap_ctx* ctx, double* route_plan_ms, double* attention_ms,
+                             uint64_t* steps);
 
 /* Kernel launches issued by this context so far (bench "gpu_launches"). */
 SAAP_API int saap_ctx_launch_count(saap_ctx* ctx, uint64_t* out);

@@ -208,6 +208,19 @@ class Context:
         _check(lib().saap_ctx_launch_count(self.h, C.byref(v)))
         return v.value
 
+    def set_assign_mode(self, mode: int):
+        """0: tcgen05 assignment (bf16 device keys, d=128) + fp64 re-check; 1: fp64 only."""
+        _check(lib().saap_ctx_set_assign_mode(self.h, C.c_int(mode)))
+
+    def enable_timing(self, on=True):
+        _check(lib().saap_ctx_enable_timing(self.h, C.c_int(1 if on else 0)))
+
+    def timing(self):
+        """(route_plan_ms, attention_ms, steps) summed since the last call."""
+        a, b, n = C.c_double(), C.c_double(), C.c_uint64()
+        _check(lib().saap_ctx_timing(self.h, C.byref(a), C.byref(b), C.byref(n)))
+        return a.value, b.value, n.value
+
     def graph_begin(self):
         _check(lib().saap_graph_begin(self.h))
 
@@ -420,6 +433,12 @@ class Layer:
         _check(lib().saap_layer_build_dev(self.ctx.h, self.h, arr, _dptr(keys_roped_bf16),
                                           _dptr(values_bf16), _dptr(keys_assign_bf16)))
         return self
+
+    def assign_info(self):
+        """(used_tensor_cores, keys re-scored in fp64) of the last build."""
+        u, n = C.c_int(), C.c_uint64()
+        _check(lib().saap_layer_assign_info(self.ctx.h, self.h, C.byref(u), C.byref(n)))
+        return bool(u.value), n.value
 
     def read_index(self, group: int):
         n = int(self.n_keys[group]) - self.sink

@@ -1,8 +1,33 @@
 // Argument blocks of the decode-side kernels (shared by the .cu files).
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace saap_b200 {
+
+constexpr int kTileRows = 128;   // smem rows per decode tile (8 warps x 16 keys)
+constexpr int kMaxPieces = 4;    // contiguous row runs per tile
+constexpr int kPlanThreads = 1024;
+
+// A contiguous run of cache rows placed at smem row `srow` of a tile.
+struct PieceRec {
+    uint32_t len;    // rows (<= 128), loaded rounded up to 8
+    uint32_t srow;   // first smem row (multiple of 8)
+    uint64_t row;    // first row in its tensor (layer cache or gather buffer)
+};
+struct TileRec {
+    uint32_t npieces;
+    uint32_t gather;  // 1: rows come from the gather buffer
+    uint32_t pad[2];
+    PieceRec p[kMaxPieces];
+};
+struct ItemRec {
+    uint32_t qslot;
+    uint32_t tile_first;
+    uint32_t ntiles;
+    uint32_t pad;
+};
 
 struct PlanArgs {
     const GroupMeta* meta;
@@ -10,33 +35,37 @@ struct PlanArgs {
     const uint32_t* offA;
     const uint32_t* idx;
     const uint32_t* assign;
-    uint32_t* list;
+    const uint32_t* invA;
     uint32_t C;
-    int mode;                   // 0 dense, 1 centroid, 2 precomputed scores, 3 window only
-    const float* const* centT;  // per group, d x C (mode 1)
-    const float* q_route;       // [groups][G][D]
-    const double* scores;       // [groups][G][C] per-row probabilities (mode 2)
+    int mode;                    // 0 dense, 1 centroid, 2 precomputed scores, 3 window only
+    const double* const* cent64T;  // per group, d x C fp64 (mode 1)
+    const float* q_route;        // [groups][G][D]
+    const double* scores;        // [groups][G][C] per-row probabilities (mode 2)
     uint32_t G, D, n_hchunks;
     uint32_t probes, recent;
-    uint32_t item_keys;
-    uint32_t P2;  // pow2 >= C (mode 1/2)
-    int route_only;  // BucketRouter::select: write `selected`, plan nothing
-    Item* items;
-    StepCounters* ctr;
+    uint32_t item_tiles;
+    uint32_t P2;                 // pow2 >= C (mode 1/2)
+    int route_only;              // BucketRouter::select: write `selected`, plan nothing
+    // general-window rows are gathered into a contiguous buffer
+    const uint16_t* K;
+    const uint16_t* V;
+    uint16_t* gK;
+    uint16_t* gV;
+    uint64_t gather_cap;         // rows per group in the gather buffer
+    // outputs
+    TileRec* tiles;
+    ItemRec* items;
+    StepCounters* ctr;           // n_items, work, n_tiles (pad[0])
     QSlot* qslots;
     saap_attn_stats* stats;
-    uint32_t* selected;  // nullable [groups][probes]
-    float* out;          // [groups][G][D]
+    uint32_t* selected;          // nullable [groups][probes]
+    float* out;                  // [groups][G][D]
 };
 
 struct DecodeArgs {
-    const Item* items;
+    const ItemRec* items;
+    const TileRec* tiles;
     StepCounters* ctr;
-    const uint16_t* K;
-    const uint16_t* V;
-    const uint64_t* row_base;
-    const uint32_t* invA;
-    const uint32_t* list;
     const float* q;
     uint32_t G;
     uint32_t n_hchunks;
@@ -48,11 +77,20 @@ struct DecodeArgs {
     float* out;
 };
 
+struct DecodeMaps {
+    CUtensorMap k64, k8, v64, v8;    // layer (or dense) cache, boxes of 64 / 8 rows
+    CUtensorMap gk64, gk8, gv64, gv8;  // gather buffer
+};
+
 struct QModelArgs {
     const float* q;            // [groups][G][d] de-roped queries
     const double* const* prm;  // per group: w1, w2, vec (3 pointers)
     uint32_t G, d, h, C;
     double* probs;             // [groups][G][C]
 };
+
+// host: TMA descriptor for a [rows x D] bf16 row-major tensor, boxes of
+// (min(D,64) elements x box_rows rows) with the matching swizzle.
+CUtensorMap make_row_map(const void* base, uint64_t rows, uint32_t D, uint32_t box_rows);
 
 }  // namespace saap_b200

@@ -1,0 +1,414 @@
+// Key assignment on the 5th-gen tensor cores (tcgen05 + TMEM + TMA), exact.
+//
+// Reference: best_bucket / assign_keys, partition.cpp:38-48, 191-198:
+//   argmax_c sum_j k_j c_cj (fp64, index order), strict '>' (lowest id wins).
+//
+// Scores S = K (C_hi + C_mid)^T with bf16 keys and a two-term bf16 split of
+// the f32 centroids, fp32 accumulation in TMEM.  Per key the epilogue keeps
+// the best and second-best approximate score.  With
+//   B = 2^-14 * |k|_2 * max_c |c|_2
+// bounding |approx - exact| (split residual <= 2^-18 |c| per element, fp32
+// accumulation of 256 exact products <= 256 * 2^-23 * sum|k_j c_j|), a key
+// whose margin best - second exceeds 2B has the reference's argmax; every
+// other key (incl. exact ties and all-zero keys) is re-scored in fp64 with the
+// reference's operation order by refine_kernel.  Result: bit-exact.
+//
+// CTA: 2 tiles of 128 keys (M=128 each) share every 128-centroid B chunk;
+// warp 4 issues TMA, warp 5 issues tcgen05.mma (one thread), warps 0-3 drain
+// TMEM (lane = key row) while the next chunk accumulates in the other half of
+// TMEM (2 x 256 columns).
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace saap_b200 {
+
+namespace tc {
+constexpr int TM = 128;       // keys per tile (UMMA M)
+constexpr int NT = 2;         // key tiles per CTA
+constexpr int CN = 128;       // centroids per chunk (UMMA N)
+constexpr int KD = 128;       // key dim (UMMA K total per term)
+constexpr int NSTAGE = 2;     // B ring depth
+constexpr int BOX = 64;       // bf16 elements per 128-byte swizzle row
+constexpr uint32_t A_TILE_BYTES = TM * KD * 2;         // 32 KB
+constexpr uint32_t B_TERM_BYTES = CN * KD * 2;         // 32 KB
+constexpr uint32_t B_STAGE_BYTES = 2 * B_TERM_BYTES;   // hi + mid
+constexpr uint32_t TMEM_COLS = 512;
+constexpr int THREADS = 192;
+}  // namespace tc
+
+struct TcTile {
+    uint32_t group;
+    uint32_t lid0;   // first local id of the tile
+    uint32_t count;  // valid keys (0 = padding tile)
+    uint32_t part;   // partition slot (rows part*Cpad.. in the split arrays)
+};
+
+struct TcAssignArgs {
+    const TcTile* tiles;
+    const uint64_t* key_row0;  // per group: row of local id 0 in the key tensor map
+    const uint64_t* out_base;  // per group: assignment base (ivf_base)
+    const float* cmax;         // per partition slot: max centroid norm
+    uint32_t C;                // buckets
+    uint32_t Cpad;             // C rounded up to CN
+    uint32_t* out;
+    uint32_t* refine;          // pairs (group, lid)
+    uint32_t* refine_count;
+    const uint16_t* keys;      // same tensor the map covers (for |k|)
+};
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1 << 16;    // LBO (unused for swizzled K-major) = 1
+    d |= (uint64_t)64 << 32;   // SBO = 1024 B between 8-row groups
+    d |= (uint64_t)1 << 46;    // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;    // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+    asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+            "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+            : "memory");
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+            "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+            "%28, %29, %30, %31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+              "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+              "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+              "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+              "=r"(r[31])
+            : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct __align__(1024) TcSmem {
+    uint8_t A[tc::NT][tc::A_TILE_BYTES];          // [tile][box(2)][128 rows][128 B]
+    uint8_t B[tc::NSTAGE][tc::B_STAGE_BYTES];     // [stage][term(2)][box(2)][CN rows][128 B]
+    uint64_t a_full;
+    uint64_t b_full[tc::NSTAGE];
+    uint64_t b_empty[tc::NSTAGE];
+    uint64_t t_full[2];
+    uint64_t t_empty[2];
+    uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(tc::THREADS, 1)
+        assign_tc_kernel(const __grid_constant__ CUtensorMap map_k,
+                         const __grid_constant__ CUtensorMap map_hi,
+                         const __grid_constant__ CUtensorMap map_mid, TcAssignArgs a) {
+    using namespace tc;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    TcSmem& s = *reinterpret_cast<TcSmem*>(
+            (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const TcTile t0 = a.tiles[blockIdx.x * NT];
+    const uint32_t nchunks = a.Cpad / CN;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&s.a_full, 1);
+        for (int i = 0; i < NSTAGE; ++i) {
+            mbar_init(&s.b_full[i], 1);
+            mbar_init(&s.b_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s.t_full[i], 1);
+            mbar_init(&s.t_empty[i], 4);  // one arrive per epilogue warp
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(&s.tmem_base)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = s.tmem_base;
+
+    if (warp == 4) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&map_k) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&map_hi) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&map_mid) : "memory");
+            mbar_arrive_expect_tx(&s.a_full, NT * A_TILE_BYTES);
+            for (int t = 0; t < NT; ++t) {
+                const TcTile tt = a.tiles[blockIdx.x * NT + t];
+                const int y = (int)(a.key_row0[tt.group] + tt.lid0);
+                for (int b = 0; b < 2; ++b)
+                    tma_load_2d(&s.A[t][b * TM * 128], &map_k, b * BOX, y, &s.a_full);
+            }
+            const int ybase = (int)(t0.part * a.Cpad);
+            for (uint32_t j = 0; j < nchunks; ++j) {
+                const uint32_t st = j % NSTAGE, ph = (j / NSTAGE) & 1;
+                mbar_wait(&s.b_empty[st], ph ^ 1);
+                mbar_arrive_expect_tx(&s.b_full[st], B_STAGE_BYTES);
+                for (int term = 0; term < 2; ++term)
+                    for (int b = 0; b < 2; ++b)
+                        tma_load_2d(&s.B[st][term * B_TERM_BYTES + b * CN * 128],
+                                    term ? &map_mid : &map_hi, b * BOX, ybase + (int)(j * CN),
+                                    &s.b_full[st]);
+            }
+        }
+    } else if (warp == 5) {
+        // ------------------------------------------------ MMA issuer (one thread)
+        if (lane == 0) {
+            constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
+                                       ((uint32_t)(CN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+            mbar_wait(&s.a_full, 0);
+            for (uint32_t j = 0; j < nchunks; ++j) {
+                const uint32_t st = j % NSTAGE, ph = (j / NSTAGE) & 1;
+                const uint32_t buf = j & 1, bph = (j >> 1) & 1;
+                mbar_wait(&s.b_full[st], ph);
+                mbar_wait(&s.t_empty[buf], bph ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int t = 0; t < NT; ++t) {
+                    const uint32_t dcol = tmem + buf * (NT * CN) + t * CN;
+                    for (int term = 0; term < 2; ++term) {
+#pragma unroll
+                        for (int kk = 0; kk < KD / 16; ++kk) {
+                            const uint32_t aoff = (kk >> 2) * TM * 128 + (kk & 3) * 32;
+                            const uint32_t boff = term * B_TERM_BYTES + (kk >> 2) * CN * 128 + (kk & 3) * 32;
+                            umma_bf16(dcol, umma_desc_sw128(smem_u32(&s.A[t][0]) + aoff),
+                                      umma_desc_sw128(smem_u32(&s.B[st][0]) + boff), idesc,
+                                      (term | kk) != 0);
+                        }
+                    }
+                }
+                umma_commit(&s.b_empty[st]);
+                umma_commit(&s.t_full[buf]);
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue: lane = key row
+        const int row = warp * 32 + lane;
+        float best[NT], second[NT], bound[NT];
+        uint32_t bidx[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            best[t] = -INFINITY;
+            second[t] = -INFINITY;
+            bidx[t] = 0;
+            const TcTile tt = a.tiles[blockIdx.x * NT + t];
+            float n2 = 0.f;
+            if ((uint32_t)row < tt.count) {
+                const uint4* kp = reinterpret_cast<const uint4*>(
+                        a.keys + (a.key_row0[tt.group] + tt.lid0 + row) * KD);
+#pragma unroll
+                for (int q = 0; q < KD / 8; ++q) {
+                    const uint4 u = kp[q];
+                    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float lo = bf16lo(w[e]), hi = bf16hi(w[e]);
+                        n2 = fmaf(lo, lo, fmaf(hi, hi, n2));
+                    }
+                }
+            }
+            bound[t] = 0x1p-14f * 1.0001f * sqrtf(n2) * a.cmax[tt.part];
+        }
+        for (uint32_t j = 0; j < nchunks; ++j) {
+            const uint32_t buf = j & 1, bph = (j >> 1) & 1;
+            mbar_wait(&s.t_full[buf], bph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+#pragma unroll 1
+                for (int q = 0; q < CN / 32; ++q) {
+                    float v[32];
+                    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + buf * (NT * CN) + t * CN + q * 32, v);
+                    const uint32_t c0 = j * CN + q * 32;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float x = v[i];
+                        if (c0 + i < a.C) {
+                            if (x > best[t]) {
+                                second[t] = best[t];
+                                best[t] = x;
+                                bidx[t] = c0 + i;
+                            } else if (x > second[t]) {
+                                second[t] = x;
+                            }
+                        }
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.t_empty[buf]);
+        }
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const TcTile tt = a.tiles[blockIdx.x * NT + t];
+            if ((uint32_t)row >= tt.count) continue;
+            const uint32_t lid = tt.lid0 + row;
+            if (best[t] - second[t] > 2.f * bound[t]) {
+                a.out[a.out_base[tt.group] + lid] = bidx[t];
+            } else {
+                const uint32_t slot = atomicAdd(a.refine_count, 1u);
+                a.refine[2 * slot] = tt.group;
+                a.refine[2 * slot + 1] = lid;
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(TMEM_COLS));
+    }
+}
+
+// fp64 re-score of ambiguous keys in the reference's exact operation order.
+template <int D>
+__global__ void __launch_bounds__(128) refine_kernel(const uint32_t* list, const uint32_t* count,
+                                                     const uint16_t* keys,
+                                                     const uint64_t* key_row0,
+                                                     const double* const* cent64,
+                                                     const uint64_t* out_base, uint32_t C,
+                                                     uint32_t* out) {
+    const uint32_t n = *count;
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+        const uint32_t g = list[2 * e], lid = list[2 * e + 1];
+        const uint16_t* kp = keys + (key_row0[g] + lid) * D;
+        const double* cg = cent64[g];
+        double best = -INFINITY;
+        uint32_t bid = 0;
+        for (uint32_t c = 0; c < C; ++c) {
+            double s = 0.0;
+            const double* cr = cg + (size_t)c * D;
+#pragma unroll 8
+            for (int j = 0; j < D; ++j) s = fma((double)__uint_as_float(((uint32_t)kp[j]) << 16), cr[j], s);
+            if (s > best) {
+                best = s;
+                bid = c;
+            }
+        }
+        out[out_base[g] + lid] = bid;
+    }
+}
+
+// f32 centroids -> (hi, mid) bf16 terms, rows padded to Cpad with zeros.
+__global__ void split_centroids_kernel(const float* cent, uint32_t C, uint32_t Cpad, uint32_t D,
+                                       uint16_t* hi, uint16_t* mid) {
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < Cpad * D; e += gridDim.x * blockDim.x) {
+        const uint32_t c = e / D;
+        float x = c < C ? cent[e] : 0.f;
+        const uint16_t h = f32_to_bf16_rne(x);
+        const float r = x - __uint_as_float((uint32_t)h << 16);
+        hi[e] = h;
+        mid[e] = f32_to_bf16_rne(r);
+    }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        SAAP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p)
+            fail(SAAP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = (EncodeTiledFn)p;
+    }
+    return fn;
+}
+
+static CUtensorMap make_map(const void* base, uint64_t rows, uint32_t box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)tc::KD, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)tc::KD * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)tc::BOX, box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(SAAP_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+uint32_t tc_cpad(uint32_t C) { return (C + tc::CN - 1) / tc::CN * tc::CN; }
+
+void launch_split_centroids(const float* cent, uint32_t C, uint32_t D, uint16_t* hi, uint16_t* mid,
+                            cudaStream_t st) {
+    const uint32_t Cpad = tc_cpad(C);
+    split_centroids_kernel<<<(Cpad * D + 255) / 256, 256, 0, st>>>(cent, C, Cpad, D, hi, mid);
+    SAAP_CUDA(cudaGetLastError());
+}
+
+// Host tile list: per group, 128-key tiles padded to an even count so the
+// two tiles of a CTA share one partition.
+void build_tc_tiles(const std::vector<GroupMeta>& meta, const std::vector<uint32_t>& part_slot,
+                    std::vector<TcTile>& tiles) {
+    tiles.clear();
+    for (size_t g = 0; g < meta.size(); ++g) {
+        const uint32_t ns = meta[g].n - meta[g].sink;
+        const size_t first = tiles.size();
+        for (uint32_t f = 0; f < ns; f += tc::TM)
+            tiles.push_back(TcTile{(uint32_t)g, f, std::min<uint32_t>(tc::TM, ns - f), part_slot[g]});
+        if ((tiles.size() - first) % tc::NT) tiles.push_back(TcTile{(uint32_t)g, 0, 0, part_slot[g]});
+    }
+}
+
+void launch_assign_tc(const uint16_t* keys, uint64_t key_rows, const uint16_t* hi,
+                      const uint16_t* mid, uint32_t n_parts, const TcAssignArgs& args,
+                      uint32_t n_tiles, cudaStream_t st) {
+    const CUtensorMap mk = make_map(keys, key_rows, tc::TM);
+    const CUtensorMap mh = make_map(hi, (uint64_t)n_parts * args.Cpad, tc::CN);
+    const CUtensorMap mm = make_map(mid, (uint64_t)n_parts * args.Cpad, tc::CN);
+    const size_t smem = sizeof(TcSmem) + 1024;
+    static bool configured = false;
+    if (!configured) {
+        SAAP_CUDA(cudaFuncSetAttribute(assign_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        configured = true;
+    }
+    assign_tc_kernel<<<n_tiles / tc::NT, tc::THREADS, smem, st>>>(mk, mh, mm, args);
+    SAAP_CUDA(cudaGetLastError());
+}
+
+void launch_refine(const uint32_t* list, const uint32_t* count, const uint16_t* keys,
+                   const uint64_t* key_row0, const double* const* cent64, const uint64_t* out_base,
+                   uint32_t C, uint32_t* out, int sm_count, cudaStream_t st) {
+    refine_kernel<128><<<sm_count * 4, 128, 0, st>>>(list, count, keys, key_row0, cent64, out_base, C,
+                                                     out);
+    SAAP_CUDA(cudaGetLastError());
+}
+
+}  // namespace saap_b200

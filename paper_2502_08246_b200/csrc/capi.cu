@@ -27,6 +27,32 @@ void launch_f32_to_bf16(const float* in, uint16_t* out, uint64_t n, cudaStream_t
 void launch_derope(const float* x, const double* cs, uint64_t rows, uint32_t D, float* out,
                    cudaStream_t st);
 void launch_debug_exp(const double* x, uint64_t n, double* y, cudaStream_t st);
+struct TcTile {
+    uint32_t group, lid0, count, part;
+};
+struct TcAssignArgs {
+    const TcTile* tiles;
+    const uint64_t* key_row0;
+    const uint64_t* out_base;
+    const float* cmax;
+    uint32_t C;
+    uint32_t Cpad;
+    uint32_t* out;
+    uint32_t* refine;
+    uint32_t* refine_count;
+    const uint16_t* keys;
+};
+uint32_t tc_cpad(uint32_t C);
+void launch_split_centroids(const float* cent, uint32_t C, uint32_t D, uint16_t* hi, uint16_t* mid,
+                            cudaStream_t st);
+void build_tc_tiles(const std::vector<GroupMeta>& meta, const std::vector<uint32_t>& part_slot,
+                    std::vector<TcTile>& tiles);
+void launch_assign_tc(const uint16_t* keys, uint64_t key_rows, const uint16_t* hi,
+                      const uint16_t* mid, uint32_t n_parts, const TcAssignArgs& args,
+                      uint32_t n_tiles, cudaStream_t st);
+void launch_refine(const uint32_t* list, const uint32_t* count, const uint16_t* keys,
+                   const uint64_t* key_row0, const double* const* cent64, const uint64_t* out_base,
+                   uint32_t C, uint32_t* out, int sm_count, cudaStream_t st);
 void launch_synth(uint16_t* out, uint64_t rows, uint32_t D, uint64_t seed, int kind,
                   const float* centers, uint64_t n_centers, float center_scale, float noise,
                   cudaStream_t st);
@@ -287,8 +313,14 @@ void enqueue_decode(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
     pa.stats = stats;
     pa.selected = selected;
     pa.out = out;
+    cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+    if (c->timing && !c->capturing) {
+        for (cudaEvent_t* e : {&e0, &e1, &e2}) SAAP_CUDA(cudaEventCreate(e));
+        SAAP_CUDA(cudaEventRecord(e0, st));
+    }
     launch_route_plan(pa, (uint32_t)n_groups, st);
     c->launches++;
+    if (e1) SAAP_CUDA(cudaEventRecord(e1, st));
 
     DecodeArgs da{};
     da.items = items;
@@ -310,6 +342,10 @@ void enqueue_decode(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
     const int grid = (int)std::min<uint64_t>((uint64_t)c->sm_count, max_items);
     launch_decode((int)D, da, std::max(grid, 1), st);
     c->launches++;
+    if (e2) {
+        SAAP_CUDA(cudaEventRecord(e2, st));
+        c->ev.insert(c->ev.end(), {e0, e1, e2});
+    }
 }
 
 }  // namespace
@@ -405,6 +441,33 @@ int saap_ctx_sm_count(saap_ctx* c, int* out) {
     return guard([&] {
         need(c, "ctx");
         *out = c->sm_count;
+    });
+}
+
+int saap_ctx_enable_timing(saap_ctx* c, int on) {
+    return guard([&] {
+        need(c, "ctx");
+        c->timing = on != 0;
+    });
+}
+
+int saap_ctx_timing(saap_ctx* c, double* plan_ms, double* attn_ms, uint64_t* steps) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        sync(c);
+        double a = 0, b = 0;
+        for (size_t i = 0; i + 2 < c->ev.size(); i += 3) {
+            float x = 0, y = 0;
+            SAAP_CUDA(cudaEventElapsedTime(&x, c->ev[i], c->ev[i + 1]));
+            SAAP_CUDA(cudaEventElapsedTime(&y, c->ev[i + 1], c->ev[i + 2]));
+            a += x;
+            b += y;
+        }
+        if (plan_ms) *plan_ms = a;
+        if (attn_ms) *attn_ms = b;
+        if (steps) *steps = c->ev.size() / 3;
+        for (auto e : c->ev) cudaEventDestroy(e);
+        c->ev.clear();
     });
 }
 
@@ -773,8 +836,16 @@ int saap_layer_create(saap_ctx* c, uint64_t n_groups, uint64_t d, uint64_t C,
         L->hist = dmalloc<uint32_t>(tiles.size() * C);
         L->countA = dmalloc<uint32_t>(n_groups * C);
         L->d_cent64 = (const double**)(dmalloc<void*>(n_groups));
-        std::vector<uint64_t> rb(n_groups);
-        for (uint64_t g = 0; g < n_groups; ++g) rb[g] = L->h_meta[g].row_base;
+        std::vector<uint64_t> rb(n_groups), kr0(n_groups), ib(n_groups);
+        for (uint64_t g = 0; g < n_groups; ++g) {
+            rb[g] = L->h_meta[g].row_base;
+            kr0[g] = L->h_meta[g].row_base + L->h_meta[g].sink;
+            ib[g] = L->h_meta[g].ivf_base;
+        }
+        L->key_row0 = dmalloc<uint64_t>(n_groups);
+        L->ivf_base = dmalloc<uint64_t>(n_groups);
+        SAAP_CUDA(cudaMemcpy(L->key_row0, kr0.data(), n_groups * 8, cudaMemcpyHostToDevice));
+        SAAP_CUDA(cudaMemcpy(L->ivf_base, ib.data(), n_groups * 8, cudaMemcpyHostToDevice));
         SAAP_CUDA(cudaMemcpy(L->meta, L->h_meta.data(), n_groups * sizeof(GroupMeta),
                              cudaMemcpyHostToDevice));
         SAAP_CUDA(cudaMemcpy(L->row_base, rb.data(), n_groups * 8, cudaMemcpyHostToDevice));
@@ -805,6 +876,14 @@ int saap_layer_destroy(saap_layer* L) {
         dfree(L->hist);
         dfree(L->countA);
         dfree(L->d_cent64);
+        dfree(L->key_row0);
+        dfree(L->ivf_base);
+        dfree(L->tc_hi);
+        dfree(L->tc_mid);
+        dfree(L->tc_cmax);
+        dfree(L->tc_refine);
+        dfree(L->tc_refine_count);
+        if (L->tc_tiles) cudaFree(L->tc_tiles);
         dfree(L->d_centT);
         dfree(L->d_qm);
         delete L;
@@ -829,23 +908,89 @@ static void bind_parts(saap_layer* L, const saap_partition* const* parts) {
 }
 
 // assignment + pack from device bf16 sources laid out like the layer rows
+static void assign_tc_path(saap_layer* L, const uint16_t* keys) {
+    saap_ctx* c = L->ctx;
+    const cudaStream_t st = c->stream;
+    // distinct partitions -> slots of the concatenated (hi, mid) split arrays
+    std::vector<const saap_partition*> slots;
+    std::vector<uint32_t> slot_of(L->n_groups);
+    for (uint64_t g = 0; g < L->n_groups; ++g) {
+        auto it = std::find(slots.begin(), slots.end(), L->parts[g]);
+        slot_of[g] = (uint32_t)(it - slots.begin());
+        if (it == slots.end()) slots.push_back(L->parts[g]);
+    }
+    const uint32_t Cpad = tc_cpad((uint32_t)L->C);
+    const size_t elems = slots.size() * (size_t)Cpad * L->d;
+    if (elems > L->tc_split_elems) {
+        dfree(L->tc_hi);
+        dfree(L->tc_mid);
+        L->tc_hi = dmalloc<uint16_t>(elems);
+        L->tc_mid = dmalloc<uint16_t>(elems);
+        L->tc_split_elems = elems;
+    }
+    std::vector<float> cmax(slots.size());
+    for (size_t i = 0; i < slots.size(); ++i) {
+        launch_split_centroids(slots[i]->cent, (uint32_t)L->C, (uint32_t)L->d,
+                               L->tc_hi + i * (size_t)Cpad * L->d, L->tc_mid + i * (size_t)Cpad * L->d, st);
+        c->launches++;
+        double m = 0;
+        for (uint64_t r = 0; r < L->C; ++r) {
+            double n2 = 0;
+            for (uint64_t j = 0; j < L->d; ++j) {
+                const double v = slots[i]->host[r * L->d + j];
+                n2 += v * v;
+            }
+            m = std::max(m, std::sqrt(n2));
+        }
+        cmax[i] = (float)(m * (1 + 1e-6));
+    }
+    std::vector<TcTile> tiles;
+    build_tc_tiles(L->h_meta, slot_of, tiles);
+    dfree(L->tc_cmax);
+    L->tc_cmax = dmalloc<float>(slots.size());
+    SAAP_CUDA(cudaMemcpy(L->tc_cmax, cmax.data(), cmax.size() * 4, cudaMemcpyHostToDevice));
+    if (L->tc_n_tiles != tiles.size()) {
+        if (L->tc_tiles) cudaFree(L->tc_tiles);
+        L->tc_tiles = dmalloc<TcTile>(tiles.size());
+        L->tc_n_tiles = (uint32_t)tiles.size();
+    }
+    SAAP_CUDA(cudaMemcpy(L->tc_tiles, tiles.data(), tiles.size() * sizeof(TcTile), cudaMemcpyHostToDevice));
+    if (!L->tc_refine) {
+        L->tc_refine = dmalloc<uint32_t>(2 * L->total_ns);
+        L->tc_refine_count = dmalloc<uint32_t>(1);
+    }
+    SAAP_CUDA(cudaMemsetAsync(L->tc_refine_count, 0, 4, st));
+    TcAssignArgs args{};
+    args.tiles = (const TcTile*)L->tc_tiles;
+    args.key_row0 = L->key_row0;
+    args.out_base = L->ivf_base;
+    args.cmax = L->tc_cmax;
+    args.C = (uint32_t)L->C;
+    args.Cpad = Cpad;
+    args.out = L->assign;
+    args.refine = L->tc_refine;
+    args.refine_count = L->tc_refine_count;
+    args.keys = keys;
+    launch_assign_tc(keys, L->total_rows, L->tc_hi, L->tc_mid, (uint32_t)slots.size(), args,
+                     (uint32_t)tiles.size(), st);
+    launch_refine(L->tc_refine, L->tc_refine_count, keys, L->key_row0, L->d_cent64, L->ivf_base,
+                  (uint32_t)L->C, L->assign, c->sm_count, st);
+    c->launches += 2;
+    L->last_tc = true;
+}
+
 static void build_from_device(saap_layer* L, const uint16_t* Ksrc, const uint16_t* Vsrc,
                               const void* keys_assign, bool assign_bf16) {
     saap_ctx* c = L->ctx;
     const cudaStream_t st = c->stream;
-    // assignment keys: rows sink + lid of each group (key_row0 = row_base + sink)
-    std::vector<uint64_t> kr0(L->n_groups), ob(L->n_groups);
-    for (uint64_t g = 0; g < L->n_groups; ++g) {
-        kr0[g] = L->h_meta[g].row_base + L->h_meta[g].sink;
-        ob[g] = L->h_meta[g].ivf_base;
+    L->last_tc = false;
+    if (assign_bf16 && L->d == 128 && c->assign_mode == 0) {
+        assign_tc_path(L, (const uint16_t*)keys_assign);
+    } else {
+        launch_assign_exact((int)L->d, assign_bf16, L->tiles, L->n_tiles, keys_assign, L->key_row0,
+                            L->d_cent64, (uint32_t)L->C, L->assign, L->ivf_base, st);
+        c->launches++;
     }
-    uint64_t* d_kr0 = (uint64_t*)ensure(c, c->zeros, L->n_groups * 16);
-    uint64_t* d_ob = d_kr0 + L->n_groups;
-    h2d(d_kr0, kr0.data(), L->n_groups * 8, st);
-    h2d(d_ob, ob.data(), L->n_groups * 8, st);
-    launch_assign_exact((int)L->d, assign_bf16, L->tiles, L->n_tiles, keys_assign, d_kr0,
-                        L->d_cent64, (uint32_t)L->C, L->assign, d_ob, st);
-    c->launches++;
     launch_pack((int)L->d, L->tiles, L->n_tiles, L->tile_first, (uint32_t)L->n_groups, L->meta,
                 L->assign, (uint32_t)L->C, L->hist, L->countA, L->off, L->offA, L->idx, L->invA,
                 Ksrc, Vsrc, L->row_base, L->K, L->V, st);
@@ -919,6 +1064,29 @@ int saap_layer_build_dev(saap_ctx* c, saap_layer* L, const saap_partition* const
         bind_parts(L, parts);
         build_from_device(L, (const uint16_t*)keys_roped_bf16, (const uint16_t*)values_bf16,
                           keys_assign_bf16, true);
+    });
+}
+
+int saap_ctx_set_assign_mode(saap_ctx* c, int mode) {
+    return guard([&] {
+        need(c, "ctx");
+        if (mode != 0 && mode != 1) invalid("assign mode must be 0 (tensor cores) or 1 (exact fp64)");
+        c->assign_mode = mode;
+    });
+}
+
+int saap_layer_assign_info(saap_ctx* c, const saap_layer* L, int* used_tensor_cores,
+                           uint64_t* refined_keys) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(L, "layer");
+        uint32_t n = 0;
+        if (L->last_tc) {
+            SAAP_CUDA(cudaMemcpyAsync(&n, L->tc_refine_count, 4, cudaMemcpyDeviceToHost, c->stream));
+            sync(c);
+        }
+        if (used_tensor_cores) *used_tensor_cores = L->last_tc ? 1 : 0;
+        if (refined_keys) *refined_keys = n;
     });
 }
 

@@ -157,6 +157,10 @@ struct saap_ctx {
     size_t done_cap = 0;
     // capture state
     bool capturing = false;
+    int assign_mode = 0;  // 0: tcgen05 path where applicable, 1: exact CUDA-core only
+    // optional per-kernel timing (eager steps)
+    bool timing = false;
+    std::vector<cudaEvent_t> ev;  // triples: before plan, before attention, after
 };
 
 struct saap_partition {
@@ -207,6 +211,19 @@ struct saap_layer {
     uint32_t* countA = nullptr;      // n_groups x C
     const double** d_cent64 = nullptr;  // per group partition (exact assignment)
     std::vector<const saap_partition*> parts;
+    // tcgen05 assignment resources
+    void* tc_tiles = nullptr;
+    uint32_t tc_n_tiles = 0;
+    uint16_t* tc_hi = nullptr;
+    uint16_t* tc_mid = nullptr;
+    size_t tc_split_elems = 0;
+    float* tc_cmax = nullptr;
+    uint32_t* tc_refine = nullptr;   // 2 * total_ns
+    uint32_t* tc_refine_count = nullptr;
+    uint64_t* key_row0 = nullptr;    // per group: row_base + sink
+    uint64_t* ivf_base = nullptr;    // per group
+    uint64_t last_refined = 0;
+    bool last_tc = false;
     // routing parameter table cache (device arrays of per-group pointers)
     std::vector<const saap_router*> cached_routers;
     const float** d_centT = nullptr;

@@ -527,11 +527,13 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1) decode_kernel(Dec
 
             const QSlot qs = a.qslots[cur_qslot];
             const uint32_t g = cur_qslot / a.n_hchunks, hc = cur_qslot % a.n_hchunks;
-            constexpr int PER = 4 * D / (kComputeWarps * 32);
+            constexpr int NOUT = 4 * D;
+            constexpr int PER = (NOUT + kComputeWarps * 32 - 1) / (kComputeWarps * 32);
             if (qs.count == 1) {
 #pragma unroll
                 for (int e0 = 0; e0 < PER; ++e0) {
                     const int e = tid + e0 * kComputeWarps * 32;
+                    if (e >= NOUT) break;
                     const int h = e / D, d = e % D;
                     float o = 0.f, lsum = 0.f;
 #pragma unroll
@@ -547,6 +549,7 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1) decode_kernel(Dec
 #pragma unroll
                 for (int e0 = 0; e0 < PER; ++e0) {
                     const int e = tid + e0 * kComputeWarps * 32;
+                    if (e >= NOUT) break;
                     const int h = e / D, d = e % D;
                     float o = 0.f;
 #pragma unroll
@@ -573,6 +576,7 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1) decode_kernel(Dec
 #pragma unroll
                     for (int e0 = 0; e0 < PER; ++e0) {
                         const int e = tid + e0 * kComputeWarps * 32;
+                        if (e >= NOUT) break;
                         const int h = e / D;
                         float M = -INFINITY;
                         for (uint32_t i = 0; i < qs.count; ++i)
