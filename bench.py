@@ -253,13 +253,12 @@ def ours(a):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if a.kv_heads % world:
-        raise SystemExit("kv heads must divide evenly over ranks")
-    heads_local = a.kv_heads // world
-    h0 = rank * heads_local
+    from paper_2502_08246_b200.shard import HeadShard, gather_outputs
+    sh = HeadShard(rank, world, a.kv_heads, a.batch)
+    heads_local, h0 = sh.heads_local, sh.head0
     G = a.q_heads // a.kv_heads
     d, C, N = a.dim, a.buckets, a.ctx_len
-    n_groups = a.batch * heads_local  # group = (sequence, local KV head)
+    n_groups = sh.n_groups  # group = (sequence, local KV head)
 
     stream = torch.cuda.Stream()
     ctx = sb.Context(local)
@@ -310,7 +309,6 @@ def ours(a):
     out = torch.empty(n_groups, G, d, device=dev)
     out_dense = torch.empty_like(out)
     stats = torch.zeros(n_groups, 3, dtype=torch.int64, device=dev)
-    out_full = torch.empty(world * n_groups, G, d, device=dev) if world > 1 else None
     cfg = sb.SparseAttnConfig(a.probes, 128, sb.DenseWindow(a.sink, a.recent))
 
     def sparse_step(li):
@@ -323,7 +321,7 @@ def ours(a):
     def gather():
         if world > 1:
             with torch.cuda.stream(stream):
-                dist.all_gather_into_tensor(out_full, out)
+                gather_outputs(out, sh, dist)
 
     # eager warm-up sizes the scratch, then capture one graph per layer
     for li in range(a.layers):

@@ -1,0 +1,251 @@
+// saap_b200.hpp — header-only C++ host API over the C ABI, mirroring the
+// reference's hot-path interface (/root/reference/proj/core/include/saap/
+// {partition,attention,qmodel}.hpp): same function names, argument meaning
+// and error behaviour (std::invalid_argument with the reference's message).
+//
+// The reference's own structs can be passed directly: every function is a
+// template over any type with the reference's field names (TensorBlock
+// {rows, dim, data}, Partition{centroids}, KeyAssignment{bucket_of},
+// SparseAttnConfig{probes, block_size, dense{sink_count, recent_count}}), so
+// a maintainer swaps `saap::sparse_attention(...)` for
+// `saap_b200::sparse_attention(...)` without touching call sites
+// (INTEGRATION.md).  Light-weight stand-in types are provided for callers
+// without the reference headers.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "saap_b200.h"
+
+namespace saap_b200 {
+
+class Error : public std::runtime_error {
+public:
+    Error(int code, const std::string& m) : std::runtime_error(m), code(code) {}
+    int code;
+};
+
+inline void check(int rc) {
+    if (rc == SAAP_OK) return;
+    const std::string msg = saap_last_error();
+    if (rc == SAAP_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+    throw Error(rc, msg);
+}
+
+// ---------------------------------------------------------------- stand-ins
+struct TensorBlock {
+    std::size_t rows = 0, dim = 0;
+    std::vector<float> data;
+    TensorBlock() = default;
+    TensorBlock(std::size_t r, std::size_t d) : rows(r), dim(d), data(r * d, 0.f) {}
+    const float* row(std::size_t i) const { return data.data() + i * dim; }
+};
+struct Partition {
+    TensorBlock centroids;
+};
+struct KeyAssignment {
+    std::vector<std::uint32_t> bucket_of;
+};
+struct IVFIndex {
+    std::vector<std::uint64_t> off, idx;
+};
+struct DenseWindow {
+    std::size_t sink_count = 1, recent_count = 2047;
+};
+struct SparseAttnConfig {
+    std::size_t probes = 16, block_size = 128;
+    DenseWindow dense;
+};
+struct AttnResult {
+    TensorBlock output;
+    std::size_t keys_scored = 0, max_visited_bucket = 0;
+    bool empty_attention = false;
+};
+
+// ---------------------------------------------------------------- device state
+class Context {
+public:
+    explicit Context(int device = 0) {
+        saap_ctx* c = nullptr;
+        check(saap_ctx_create(device, &c));
+        h_.reset(c);
+    }
+    saap_ctx* get() const { return h_.get(); }
+    static Context& current() {
+        static Context ctx(0);
+        return ctx;
+    }
+
+private:
+    struct Del {
+        void operator()(saap_ctx* c) const { saap_ctx_destroy(c); }
+    };
+    std::unique_ptr<saap_ctx, Del> h_;
+};
+
+class DevicePartition {
+public:
+    template <typename P>
+    explicit DevicePartition(const P& p, Context& ctx = Context::current()) : ctx_(&ctx) {
+        saap_partition* h = nullptr;
+        check(saap_partition_create(ctx.get(), p.centroids.data.data(), p.centroids.rows,
+                                    p.centroids.dim, &h));
+        h_.reset(h);
+        C_ = p.centroids.rows;
+        d_ = p.centroids.dim;
+    }
+    saap_partition* get() const { return h_.get(); }
+    Context& ctx() const { return *ctx_; }
+    std::size_t n_buckets() const { return C_; }
+    std::size_t dim() const { return d_; }
+
+private:
+    struct Del {
+        void operator()(saap_partition* p) const { saap_partition_destroy(p); }
+    };
+    Context* ctx_;
+    std::unique_ptr<saap_partition, Del> h_;
+    std::size_t C_, d_;
+};
+
+// BucketRouter plugin (attention.hpp:102-108)
+class BucketRouter {
+public:
+    virtual ~BucketRouter() { saap_router_destroy(h_); }
+    template <typename TB>
+    std::vector<std::uint32_t> select(const TB& q_roped, const TB& q_deroped, std::size_t l) const {
+        std::vector<std::uint32_t> out(l);
+        check(saap_router_select(ctx_->get(), h_, q_roped.data.data(), q_deroped.data.data(),
+                                 q_roped.rows, q_roped.dim, l, out.data()));
+        return out;
+    }
+    saap_router* get() const { return h_; }
+
+protected:
+    Context* ctx_ = nullptr;
+    saap_router* h_ = nullptr;
+};
+
+class CentroidRouter : public BucketRouter {
+public:
+    template <typename P>
+    CentroidRouter(const P& partition, bool use_deroped, Context& ctx = Context::current())
+            : part_(partition, ctx) {
+        ctx_ = &ctx;
+        check(saap_router_create_centroid(ctx.get(), part_.get(), use_deroped ? 1 : 0, &h_));
+    }
+
+private:
+    DevicePartition part_;
+};
+
+// ---------------------------------------------------------------- functions
+template <typename TB, typename P>
+KeyAssignment assign_keys(const TB& keys, const P& p) {
+    DevicePartition dp(p);
+    KeyAssignment a;
+    a.bucket_of.resize(keys.rows);
+    check(saap_assign_keys(dp.ctx().get(), dp.get(), keys.data.data(), keys.rows, keys.dim,
+                           a.bucket_of.data()));
+    return a;
+}
+
+template <typename KA>
+IVFIndex build_ivf(const KA& assignment, std::size_t n_buckets) {
+    IVFIndex ix;
+    ix.off.resize(n_buckets + 1);
+    ix.idx.resize(assignment.bucket_of.size());
+    check(saap_build_ivf(Context::current().get(), assignment.bucket_of.data(),
+                         assignment.bucket_of.size(), n_buckets, ix.off.data(), ix.idx.data()));
+    return ix;
+}
+
+template <typename TB>
+TensorBlock full_attention(const TB& q, const TB& keys, const TB& values) {
+    if (keys.rows != values.rows)
+        throw std::invalid_argument("attention: " + std::to_string(keys.rows) + " keys vs " +
+                                    std::to_string(values.rows) + " values");
+    TensorBlock out(q.rows, values.dim);
+    check(saap_full_attention(Context::current().get(), q.data.data(), q.rows, keys.data.data(),
+                              values.data.data(), keys.rows, keys.dim, out.data.data()));
+    return out;
+}
+
+// One ContextStore on the device (attention.hpp:76-86).
+class ContextStore {
+public:
+    // build_context_store(keys_roped, values, rope, partition, sink), with the
+    // partition's pre-RoPE keys passed explicitly (or nullptr: de-rope on device)
+    template <typename TB, typename P>
+    ContextStore(const TB& keys_roped, const TB& values, double rope_base, const P& partition,
+                 std::size_t sink, const TB* keys_deroped = nullptr, std::size_t recent_hint = 2047,
+                 Context& ctx = Context::current())
+            : ctx_(&ctx), part_(partition, ctx), sink_(sink), n_(keys_roped.rows) {
+        if (keys_roped.rows != values.rows)
+            throw std::invalid_argument("attention: " + std::to_string(keys_roped.rows) +
+                                        " keys vs " + std::to_string(values.rows) + " values");
+        const std::uint64_t n = keys_roped.rows;
+        saap_layer* L = nullptr;
+        check(saap_layer_create(ctx.get(), 1, keys_roped.dim, part_.n_buckets(), &n, sink,
+                                recent_hint, &L));
+        h_.reset(L);
+        const saap_partition* pp = part_.get();
+        check(saap_layer_build(ctx.get(), L, &pp, keys_roped.data.data(), values.data.data(),
+                               keys_deroped ? keys_deroped->data.data() : nullptr, rope_base));
+    }
+    std::size_t n_keys() const { return n_; }
+    std::size_t id_offset() const { return sink_; }
+    saap_layer* get() const { return h_.get(); }
+    Context& ctx() const { return *ctx_; }
+    KeyAssignment assignment() const {
+        KeyAssignment a;
+        a.bucket_of.resize(n_ - sink_);
+        check(saap_layer_read_index(ctx_->get(), h_.get(), 0, a.bucket_of.data(), nullptr, nullptr));
+        return a;
+    }
+    IVFIndex index() const {
+        IVFIndex ix;
+        ix.off.resize(part_.n_buckets() + 1);
+        ix.idx.resize(n_ - sink_);
+        check(saap_layer_read_index(ctx_->get(), h_.get(), 0, nullptr, ix.off.data(), ix.idx.data()));
+        return ix;
+    }
+
+private:
+    struct Del {
+        void operator()(saap_layer* L) const { saap_layer_destroy(L); }
+    };
+    Context* ctx_;
+    DevicePartition part_;
+    std::size_t sink_, n_;
+    std::unique_ptr<saap_layer, Del> h_;
+};
+
+// sparse_attention(q_roped, q_deroped, store, router, cfg) attention.cpp:317-376
+template <typename TB, typename CFG>
+AttnResult sparse_attention(const TB& q_roped, const TB& q_deroped, const ContextStore& store,
+                            const BucketRouter& router, const CFG& cfg) {
+    AttnResult r;
+    r.output = TensorBlock(q_roped.rows, q_roped.dim);
+    saap_sparse_cfg c{cfg.probes, cfg.block_size, cfg.dense.sink_count, cfg.dense.recent_count};
+    saap_attn_stats st{};
+    const saap_router* rt = router.get();
+    check(saap_sparse_attention(store.ctx().get(), store.get(), &rt, q_roped.data.data(),
+                                q_deroped.data.data(), q_roped.rows, &c, r.output.data.data(), &st,
+                                nullptr));
+    r.keys_scored = st.keys_scored;
+    r.max_visited_bucket = st.max_visited_bucket;
+    r.empty_attention = st.empty_attention != 0;
+    return r;
+}
+
+inline double selectivity(const AttnResult& r, std::size_t n_keys) {
+    if (n_keys == 0) throw std::invalid_argument("selectivity: empty context");
+    return static_cast<double>(r.keys_scored) / static_cast<double>(n_keys);
+}
+
+}  // namespace saap_b200

@@ -7,20 +7,34 @@
 namespace saap_b200 {
 
 constexpr int kTileRows = 128;   // smem rows per decode tile (8 warps x 16 keys)
-constexpr int kMaxPieces = 4;    // contiguous row runs per tile
+constexpr int kMaxPieces = 16;   // contiguous row runs per tile (each >= 8 virtual rows)
+constexpr int kSliceMax = 1024;  // centroids scored by one routing CTA
 constexpr int kPlanThreads = 1024;
 
 // A contiguous run of cache rows placed at smem row `srow` of a tile.
 struct PieceRec {
-    uint32_t len;    // rows (<= 128), loaded rounded up to 8
+    uint32_t len;    // rows (<= 128; loaded rounded up to 8) | 0x80000000 if gather buffer
     uint32_t srow;   // first smem row (multiple of 8)
     uint64_t row;    // first row in its tensor (layer cache or gather buffer)
 };
 struct TileRec {
     uint32_t npieces;
-    uint32_t gather;  // 1: rows come from the gather buffer
-    uint32_t pad[2];
+    uint32_t pad[3];
     PieceRec p[kMaxPieces];
+};
+constexpr uint32_t kPieceGather = 0x80000000u;
+
+// Routing, stage 1: one CTA scores a slice of <= kSliceMax centroids and
+// keeps its top-min(l, slice) (score, id) pairs in reference order.
+struct RouteArgs {
+    int mode;                      // 1 centroid, 2 precomputed Q-model probabilities
+    const double* const* cent64T;  // per group, d x C fp64
+    const float* q_route;          // [groups][G][D]
+    const double* scores;          // [groups][G][C]
+    uint32_t G, D, C, probes;
+    uint32_t slice, n_slices, keep;  // keep = min(probes, slice)
+    double* cand_s;                // [groups][n_slices][keep]
+    uint32_t* cand_i;
 };
 struct ItemRec {
     uint32_t qslot;
@@ -44,7 +58,10 @@ struct PlanArgs {
     uint32_t G, D, n_hchunks;
     uint32_t probes, recent;
     uint32_t item_tiles;
-    uint32_t P2;                 // pow2 >= C (mode 1/2)
+    uint32_t P2;                 // pow2 >= n_slices * keep (candidates to merge)
+    uint32_t n_cand;             // n_slices * keep
+    const double* cand_s;        // routing candidates from route_score_kernel
+    const uint32_t* cand_i;
     int route_only;              // BucketRouter::select: write `selected`, plan nothing
     // general-window rows are gathered into a contiguous buffer
     const uint16_t* K;

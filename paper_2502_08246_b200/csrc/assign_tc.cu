@@ -19,7 +19,7 @@
 // TMEM (2 x 256 columns).
 #include <cuda.h>
 
-#include "common.cuh"
+#include "args.cuh"
 
 namespace saap_b200 {
 
@@ -360,6 +360,24 @@ static CUtensorMap make_map(const void* base, uint64_t rows, uint32_t box_rows) 
                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(SAAP_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+// [rows x D] bf16 row-major tensor, boxes of min(D,64) elements x box_rows;
+// 128-byte swizzle for D >= 64 (per 64-element half), 64-byte for D = 32.
+CUtensorMap make_row_map(const void* base, uint64_t rows, uint32_t D, uint32_t box_rows) {
+    CUtensorMap m;
+    const uint32_t inner = D >= 64 ? 64 : D;
+    const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)(rows ? rows : 1)};
+    const cuuint64_t strides[1] = {(cuuint64_t)D * 2};
+    const cuuint32_t box[2] = {inner, box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             inner == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        fail(SAAP_ERR_CUDA, "cuTensorMapEncodeTiled (rows) failed: " + std::to_string((int)r));
     return m;
 }
 

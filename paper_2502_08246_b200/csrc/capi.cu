@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -13,7 +14,8 @@ namespace saap_b200 {
 
 // ---- kernels (decode.cu / pack.cu / route.cu / synth.cu)
 void launch_route_plan(const PlanArgs& a, uint32_t n_groups, cudaStream_t st);
-void launch_decode(int D, const DecodeArgs& a, int grid, cudaStream_t st);
+void launch_route_score(const RouteArgs& a, uint32_t n_groups, cudaStream_t st);
+void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st);
 void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st);
 void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t n_tiles,
                          const void* keys, const uint64_t* key_row0, const double* const* cent64,
@@ -211,9 +213,9 @@ void bind_routers(saap_layer* L, const saap_router* const* routers, int& mode, i
     if (rs == L->cached_routers) return;
     if (L->ctx->capturing) invalid("router set changed during graph capture");
     if (kind == 0) {
-        std::vector<const float*> p(L->n_groups);
-        for (size_t g = 0; g < p.size(); ++g) p[g] = rs[g]->part->centT;
-        if (!L->d_centT) L->d_centT = (const float**)(dmalloc<void*>(L->n_groups));
+        std::vector<const double*> p(L->n_groups);
+        for (size_t g = 0; g < p.size(); ++g) p[g] = rs[g]->part->cent64T;
+        if (!L->d_centT) L->d_centT = (const double**)(dmalloc<void*>(L->n_groups));
         SAAP_CUDA(cudaMemcpy(L->d_centT, p.data(), p.size() * sizeof(void*), cudaMemcpyHostToDevice));
     } else {
         std::vector<const double*> p(3 * L->n_groups);
@@ -246,26 +248,99 @@ void check_router_dims(const saap_router* r, uint64_t d, uint64_t C, uint64_t l)
     }
 }
 
-constexpr uint32_t kItemKeysSparse = 512;
-constexpr uint32_t kItemKeysDense = 2048;
+// Routing is split over ceil(C / slice) CTAs per context; each keeps its
+// top-min(l, slice) candidates, which route_plan_kernel merges.
+struct RouteGeo {
+    uint32_t slice, n_slices, keep, n_cand, P2;
+};
+RouteGeo route_geo(uint64_t C, uint64_t probes) {
+    RouteGeo r;
+    r.slice = C <= 256 ? (uint32_t)C : (C <= 4096 ? 256u : 1024u);
+    r.n_slices = (uint32_t)((C + r.slice - 1) / r.slice);
+    r.keep = (uint32_t)std::min<uint64_t>(probes, r.slice);
+    r.n_cand = r.n_slices * r.keep;
+    r.P2 = next_pow2(std::max<uint32_t>(r.n_cand, 1));
+    return r;
+}
+
+// stage-1 routing launch for n groups (mode 1 centroid / 2 Q-model scores)
+void enqueue_route_score(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C, uint64_t G,
+                         uint64_t probes, int mode, const double* const* cent64T,
+                         const float* q_route, const double* probs, PlanArgs& pa) {
+    const RouteGeo geo = route_geo(C, probes);
+    double* cs = (double*)ensure(c, c->cand_s, n_groups * geo.n_cand * sizeof(double));
+    uint32_t* ci = (uint32_t*)ensure(c, c->cand_i, n_groups * geo.n_cand * sizeof(uint32_t));
+    RouteArgs ra{};
+    ra.mode = mode;
+    ra.cent64T = cent64T;
+    ra.q_route = q_route;
+    ra.scores = probs;
+    ra.G = (uint32_t)G;
+    ra.D = (uint32_t)D;
+    ra.C = (uint32_t)C;
+    ra.probes = (uint32_t)probes;
+    ra.slice = geo.slice;
+    ra.n_slices = geo.n_slices;
+    ra.keep = geo.keep;
+    ra.cand_s = cs;
+    ra.cand_i = ci;
+    launch_route_score(ra, (uint32_t)n_groups, c->stream);
+    c->launches++;
+    pa.P2 = geo.P2;
+    pa.n_cand = geo.n_cand;
+    pa.cand_s = cs;
+    pa.cand_i = ci;
+}
+
+constexpr uint32_t kItemTilesSparse = 2;   // 128-row tiles per work item
+constexpr uint32_t kItemTilesDense = 16;
+
+// Everything a decode step reads about its cache.
+struct DecodeSrc {
+    uint64_t n_groups = 0, D = 0, C = 1, max_n = 0, rows = 0;
+    const GroupMeta* meta = nullptr;
+    const uint32_t *off = nullptr, *offA = nullptr, *idx = nullptr, *assign = nullptr,
+                   *invA = nullptr;
+    const uint16_t *K = nullptr, *V = nullptr;
+    uint16_t *gK = nullptr, *gV = nullptr;
+    uint64_t gather_cap = 0;
+    const DecodeMaps* maps = nullptr;
+};
+
+DecodeMaps* build_maps(const void* K, const void* V, uint64_t rows, uint32_t D, const void* gK,
+                       const void* gV, uint64_t grows) {
+    auto* m = new DecodeMaps;
+    m->k64 = make_row_map(K, rows, D, 64);
+    m->k8 = make_row_map(K, rows, D, 8);
+    m->v64 = make_row_map(V, rows, D, 64);
+    m->v8 = make_row_map(V, rows, D, 8);
+    const void* a = gK ? gK : K;
+    const void* b = gV ? gV : V;
+    const uint64_t r = gK ? grows : rows;
+    m->gk64 = make_row_map(a, r, D, 64);
+    m->gk8 = make_row_map(a, r, D, 8);
+    m->gv64 = make_row_map(b, r, D, 64);
+    m->gv8 = make_row_map(b, r, D, 8);
+    return m;
+}
 
 // Enqueue one decode step (routing, planning, attention, combine) on the
 // context stream.  mode: 0 dense/full, 1 centroid, 2 Q-model, 3 window only.
-void enqueue_decode(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
-                    const GroupMeta* meta, const uint64_t* row_base, uint64_t max_n,
-                    const uint32_t* off, const uint32_t* offA, const uint32_t* idx,
-                    const uint32_t* assign, const uint32_t* invA, uint32_t* list,
-                    const uint16_t* K, const uint16_t* V, int mode, const float* const* centT,
+void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const double* const* cent64T,
                     const double* const* qm, const float* q_roped, const float* q_route,
                     uint64_t G, uint64_t probes, uint64_t recent, float* out,
-                    saap_attn_stats* stats, uint32_t* selected, uint32_t item_keys,
+                    saap_attn_stats* stats, uint32_t* selected, uint32_t item_tiles,
                     uint32_t qm_hidden = 0) {
     const cudaStream_t st = c->stream;
+    const uint64_t n_groups = src.n_groups, D = src.D, C = src.C;
     const uint64_t n_hchunks = (G + kHeadsPerSlot - 1) / kHeadsPerSlot;
     const uint64_t qslots = n_groups * n_hchunks;
-    const uint64_t per_group_items = (max_n + item_keys - 1) / item_keys + probes + 8;
-    const uint64_t max_items = n_groups * per_group_items * n_hchunks;
-    Item* items = (Item*)ensure(c, c->items, max_items * sizeof(Item));
+    const uint64_t nseg = probes + 4;
+    const uint64_t per_group_tiles = (src.max_n + 8 * nseg) / kTileRows + nseg + 2;
+    const uint64_t max_tiles = n_groups * per_group_tiles;
+    const uint64_t max_items = max_tiles * n_hchunks;
+    TileRec* tiles = (TileRec*)ensure(c, c->tiles, max_tiles * sizeof(TileRec));
+    ItemRec* items = (ItemRec*)ensure(c, c->items, max_items * sizeof(ItemRec));
     QSlot* qs = (QSlot*)ensure(c, c->qslots, qslots * sizeof(QSlot));
     float* pO = (float*)ensure(c, c->part_O, max_items * kHeadsPerSlot * D * sizeof(float));
     float* pml = (float*)ensure(c, c->part_ml, max_items * 8 * sizeof(float));
@@ -288,15 +363,15 @@ void enqueue_decode(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
         c->launches++;
     }
     PlanArgs pa{};
-    pa.meta = meta;
-    pa.off = off;
-    pa.offA = offA;
-    pa.idx = idx;
-    pa.assign = assign;
-    pa.list = list;
+    pa.meta = src.meta;
+    pa.off = src.off;
+    pa.offA = src.offA;
+    pa.idx = src.idx;
+    pa.assign = src.assign;
+    pa.invA = src.invA;
     pa.C = (uint32_t)C;
     pa.mode = mode;
-    pa.centT = centT;
+    pa.cent64T = cent64T;
     pa.q_route = q_route;
     pa.scores = probs;
     pa.G = (uint32_t)G;
@@ -304,9 +379,14 @@ void enqueue_decode(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
     pa.n_hchunks = (uint32_t)n_hchunks;
     pa.probes = (uint32_t)probes;
     pa.recent = (uint32_t)std::min<uint64_t>(recent, 0xFFFFFFFFull);
-    pa.item_keys = item_keys;
-    pa.P2 = (mode == 1 || mode == 2) ? next_pow2((uint32_t)C) : 0;
+    pa.item_tiles = item_tiles;
     pa.route_only = 0;
+    pa.K = src.K;
+    pa.V = src.V;
+    pa.gK = src.gK;
+    pa.gV = src.gV;
+    pa.gather_cap = src.gather_cap;
+    pa.tiles = tiles;
     pa.items = items;
     pa.ctr = c->counters;
     pa.qslots = qs;
@@ -318,18 +398,16 @@ void enqueue_decode(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
         for (cudaEvent_t* e : {&e0, &e1, &e2}) SAAP_CUDA(cudaEventCreate(e));
         SAAP_CUDA(cudaEventRecord(e0, st));
     }
+    if ((mode == 1 || mode == 2) && probes > 0)
+        enqueue_route_score(c, n_groups, D, C, G, probes, mode, cent64T, q_route, probs, pa);
     launch_route_plan(pa, (uint32_t)n_groups, st);
     c->launches++;
     if (e1) SAAP_CUDA(cudaEventRecord(e1, st));
 
     DecodeArgs da{};
     da.items = items;
+    da.tiles = tiles;
     da.ctr = c->counters;
-    da.K = K;
-    da.V = V;
-    da.row_base = row_base;
-    da.invA = invA;
-    da.list = list;
     da.q = q_roped;
     da.G = (uint32_t)G;
     da.n_hchunks = (uint32_t)n_hchunks;
@@ -340,12 +418,57 @@ void enqueue_decode(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
     da.done = c->done;
     da.out = out;
     const int grid = (int)std::min<uint64_t>((uint64_t)c->sm_count, max_items);
-    launch_decode((int)D, da, std::max(grid, 1), st);
+    launch_decode((int)D, *src.maps, da, std::max(grid, 1), st);
     c->launches++;
     if (e2) {
         SAAP_CUDA(cudaEventRecord(e2, st));
         c->ev.insert(c->ev.end(), {e0, e1, e2});
     }
+}
+
+// The layer's decode view (maps built once; gather buffer sized on demand).
+DecodeSrc layer_src(saap_layer* L, uint64_t recent, bool need_gather) {
+    if (need_gather) {
+        uint64_t cap = 0;
+        for (auto& gm : L->h_meta) {
+            const uint64_t ns = gm.n - gm.sink;
+            const uint64_t d = recent > L->recent_hint ? recent - L->recent_hint : L->recent_hint - recent;
+            cap = std::max<uint64_t>(cap, std::min<uint64_t>(ns, d));
+        }
+        if (cap > L->gather_cap) {
+            if (L->ctx->capturing) invalid("gather buffer grows during graph capture");
+            SAAP_CUDA(cudaStreamSynchronize(L->ctx->stream));
+            dfree(L->gK);
+            dfree(L->gV);
+            L->gK = dmalloc<uint16_t>(L->n_groups * cap * L->d);
+            L->gV = dmalloc<uint16_t>(L->n_groups * cap * L->d);
+            L->gather_cap = cap;
+            delete (DecodeMaps*)L->maps;
+            L->maps = nullptr;
+        }
+    }
+    if (!L->maps)
+        L->maps = build_maps(L->K, L->V, L->total_rows, (uint32_t)L->d, L->gK, L->gV,
+                             L->n_groups * L->gather_cap);
+    DecodeSrc s;
+    s.n_groups = L->n_groups;
+    s.D = L->d;
+    s.C = L->C;
+    for (auto& gm : L->h_meta) s.max_n = std::max<uint64_t>(s.max_n, gm.n);
+    s.rows = L->total_rows;
+    s.meta = L->meta;
+    s.off = L->off;
+    s.offA = L->offA;
+    s.idx = L->idx;
+    s.assign = L->assign;
+    s.invA = L->invA;
+    s.K = L->K;
+    s.V = L->V;
+    s.gK = L->gK;
+    s.gV = L->gV;
+    s.gather_cap = L->gather_cap;
+    s.maps = (const DecodeMaps*)L->maps;
+    return s;
 }
 
 }  // namespace
@@ -490,18 +613,18 @@ int saap_partition_create(saap_ctx* c, const float* cent, uint64_t C, uint64_t d
         p->C = C;
         p->d = d;
         p->host.assign(cent, cent + C * d);
-        std::vector<float> t(C * d);
+        std::vector<double> t(C * d);
         std::vector<double> d64(C * d);
         for (uint64_t i = 0; i < C; ++i)
             for (uint64_t j = 0; j < d; ++j) {
-                t[j * C + i] = cent[i * d + j];
+                t[j * C + i] = (double)cent[i * d + j];
                 d64[i * d + j] = (double)cent[i * d + j];
             }
         p->cent = dmalloc<float>(C * d);
-        p->centT = dmalloc<float>(C * d);
+        p->cent64T = dmalloc<double>(C * d);
         p->cent64 = dmalloc<double>(C * d);
         SAAP_CUDA(cudaMemcpy(p->cent, cent, C * d * 4, cudaMemcpyHostToDevice));
-        SAAP_CUDA(cudaMemcpy(p->centT, t.data(), C * d * 4, cudaMemcpyHostToDevice));
+        SAAP_CUDA(cudaMemcpy(p->cent64T, t.data(), C * d * 8, cudaMemcpyHostToDevice));
         SAAP_CUDA(cudaMemcpy(p->cent64, d64.data(), C * d * 8, cudaMemcpyHostToDevice));
         *out = p;
     });
@@ -512,7 +635,7 @@ int saap_partition_destroy(saap_partition* p) {
         if (!p) return;
         cudaSetDevice(p->ctx->device);
         dfree(p->cent);
-        dfree(p->centT);
+        dfree(p->cent64T);
         dfree(p->cent64);
         delete p;
     });
@@ -602,7 +725,7 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
     int mode;
     double* probs = nullptr;
     if (r->kind == 0) {
-        ptrs[0] = (void*)r->part->centT;
+        ptrs[0] = (void*)r->part->cent64T;
         mode = 1;
     } else {
         ptrs[0] = (void*)r->model->w1;
@@ -629,7 +752,7 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
     pa.meta = dmeta;
     pa.C = (uint32_t)C;
     pa.mode = mode;
-    pa.centT = (const float* const*)dptr;
+    pa.cent64T = (const double* const*)dptr;
     pa.q_route = dq;
     pa.scores = probs;
     pa.G = (uint32_t)G;
@@ -637,10 +760,10 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
     pa.n_hchunks = 1;
     pa.probes = (uint32_t)l;
     pa.recent = 0;
-    pa.item_keys = kItemKeysSparse;
-    pa.P2 = next_pow2((uint32_t)C);
+    pa.item_tiles = kItemTilesSparse;
     pa.route_only = 1;
     pa.selected = dsel;
+    enqueue_route_score(c, 1, d, C, G, l, mode, (const double* const*)dptr, dq, probs, pa);
     launch_route_plan(pa, 1, st);
     c->launches++;
     d2h(out, dsel, l * 4, st);
@@ -824,7 +947,6 @@ int saap_layer_create(saap_ctx* c, uint64_t n_groups, uint64_t d, uint64_t C,
         L->assign = dmalloc<uint32_t>(ns);
         L->idx = dmalloc<uint32_t>(ns);
         L->invA = dmalloc<uint32_t>(ns);
-        L->list = dmalloc<uint32_t>(ns);
         L->off = dmalloc<uint32_t>(n_groups * (C + 1));
         L->offA = dmalloc<uint32_t>(n_groups * (C + 1));
         std::vector<TileDesc> tiles;
@@ -868,7 +990,9 @@ int saap_layer_destroy(saap_layer* L) {
         dfree(L->assign);
         dfree(L->idx);
         dfree(L->invA);
-        dfree(L->list);
+        dfree(L->gK);
+        dfree(L->gV);
+        delete (DecodeMaps*)L->maps;
         dfree(L->off);
         dfree(L->offA);
         dfree(L->tiles);
@@ -1162,10 +1286,15 @@ static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* con
     if (mode == 2)
         for (auto* r : L->cached_routers)
             if (r->model->h != hq) unsupported("sparse_attention: Q-models with different widths");
-    enqueue_decode(c, L->n_groups, L->d, L->C, L->meta, L->row_base, maxn, L->off, L->offA, L->idx,
-                   L->assign, L->invA, L->list, L->K, L->V, mode, L->d_centT, L->d_qm, qr, q_route,
-                   G, cfg->probes, cfg->recent_count, out, stats, selected, kItemKeysSparse,
-                   (uint32_t)hq);
+    (void)maxn;
+    bool need_gather = false;
+    if (cfg->recent_count != L->recent_hint)
+        for (auto& gm : L->h_meta)
+            need_gather |= gm.n > cfg->sink_count + cfg->recent_count &&
+                           (cfg->recent_count > L->recent_hint || (mode != 3 && cfg->probes > 0));
+    const DecodeSrc src = layer_src(L, cfg->recent_count, need_gather);
+    enqueue_decode(c, src, mode, L->d_centT, L->d_qm, qr, q_route, G, cfg->probes,
+                   cfg->recent_count, out, stats, selected, kItemTilesSparse, (uint32_t)hq);
 }
 
 int saap_sparse_attention_dev(saap_ctx* c, const saap_layer* L, const saap_router* const* routers,
@@ -1225,9 +1354,9 @@ int saap_layer_full_attention(saap_ctx* c, const saap_layer* L, const float* q, 
         float* dq = (float*)ensure(c, c->qr, qn * 4);
         float* dout = (float*)ensure(c, c->out, qn * 4);
         h2d(dq, q, qn * 4, st);
-        enqueue_decode(c, L->n_groups, L->d, L->C, L->meta, L->row_base, max_keys(L), L->off,
-                       L->offA, L->idx, L->assign, L->invA, L->list, L->K, L->V, 0, nullptr,
-                       nullptr, dq, nullptr, G, 0, 0, dout, nullptr, nullptr, kItemKeysDense);
+        const DecodeSrc src = layer_src(const_cast<saap_layer*>(L), L->recent_hint, false);
+        enqueue_decode(c, src, 0, nullptr, nullptr, dq, nullptr, G, 0, 0, dout, nullptr, nullptr,
+                       kItemTilesDense);
         d2h(out, dout, qn * 4, st);
         sync(c);
     });
@@ -1260,9 +1389,19 @@ int saap_full_attention(saap_ctx* c, const float* q, uint64_t G, const float* ke
         float* dq = (float*)ensure(c, c->qr, G * d * 4);
         float* dout = (float*)ensure(c, c->out, G * d * 4);
         h2d(dq, q, G * d * 4, st);
-        enqueue_decode(c, 1, d, 1, dm, drb, n, nullptr, nullptr, nullptr, nullptr, nullptr,
-                       nullptr, Kb, Vb, 0, nullptr, nullptr, dq, nullptr, G, 0, 0, dout, nullptr,
-                       nullptr, kItemKeysDense);
+        (void)drb;
+        DecodeSrc src;
+        src.n_groups = 1;
+        src.D = d;
+        src.max_n = n;
+        src.rows = n;
+        src.meta = dm;
+        src.K = Kb;
+        src.V = Vb;
+        std::unique_ptr<DecodeMaps> maps(build_maps(Kb, Vb, n, (uint32_t)d, nullptr, nullptr, 0));
+        src.maps = maps.get();
+        enqueue_decode(c, src, 0, nullptr, nullptr, dq, nullptr, G, 0, 0, dout, nullptr, nullptr,
+                       kItemTilesDense);
         d2h(out, dout, G * d * 4, st);
         sync(c);
         cudaFree(f32);
@@ -1293,7 +1432,9 @@ int saap_kvcache_create(saap_ctx* c, uint64_t n_groups, uint64_t d, const void* 
             }
             m[g] = GroupMeta{row_base[g], 0, (uint32_t)n_keys[g], 0, 0, 0};
             kc->max_n = std::max<uint64_t>(kc->max_n, n_keys[g]);
+            kc->rows = std::max<uint64_t>(kc->rows, row_base[g] + n_keys[g]);
         }
+        kc->maps = build_maps(K, V, kc->rows, (uint32_t)d, nullptr, nullptr, 0);
         kc->meta = dmalloc<GroupMeta>(n_groups);
         kc->row_base = dmalloc<uint64_t>(n_groups);
         SAAP_CUDA(cudaMemcpy(kc->meta, m.data(), n_groups * sizeof(GroupMeta), cudaMemcpyHostToDevice));
@@ -1308,6 +1449,7 @@ int saap_kvcache_destroy(saap_kvcache* kc) {
         cudaSetDevice(kc->ctx->device);
         dfree(kc->meta);
         dfree(kc->row_base);
+        delete (DecodeMaps*)kc->maps;
         delete kc;
     });
 }
@@ -1318,9 +1460,17 @@ int saap_dense_attention_dev(saap_ctx* c, const saap_kvcache* kc, const float* q
         DeviceGuard dg(c);
         need(kc, "kvcache");
         if (G == 0) return;
-        enqueue_decode(c, kc->n_groups, kc->d, 1, kc->meta, kc->row_base, kc->max_n, nullptr,
-                       nullptr, nullptr, nullptr, nullptr, nullptr, kc->K, kc->V, 0, nullptr,
-                       nullptr, q, nullptr, G, 0, 0, out, nullptr, nullptr, kItemKeysDense);
+        DecodeSrc src;
+        src.n_groups = kc->n_groups;
+        src.D = kc->d;
+        src.max_n = kc->max_n;
+        src.rows = kc->rows;
+        src.meta = kc->meta;
+        src.K = kc->K;
+        src.V = kc->V;
+        src.maps = (const DecodeMaps*)kc->maps;
+        enqueue_decode(c, src, 0, nullptr, nullptr, q, nullptr, G, 0, 0, out, nullptr, nullptr,
+                       kItemTilesDense);
     });
 }
 

@@ -151,7 +151,7 @@ struct saap_ctx {
     bool own_stream = false;
     uint64_t launches = 0;
     // growable device scratch (sized by uncaptured calls; graphs reuse it)
-    saap_scratch items, qslots, part_O, part_ml, probs, stats, sel, qr, qd, out, misc, zeros;
+    saap_scratch cand_s, cand_i, items, tiles, qslots, part_O, part_ml, probs, stats, sel, qr, qd, out, misc, zeros;
     saap_b200::StepCounters* counters = nullptr;  // persistent, 128 B
     uint32_t* done = nullptr;                     // per query slot completion counters
     size_t done_cap = 0;
@@ -167,8 +167,8 @@ struct saap_partition {
     saap_ctx* ctx = nullptr;
     uint64_t C = 0, d = 0;
     float* cent = nullptr;     // C x d f32 (device)
-    float* centT = nullptr;    // d x C f32 (device, routing reads coalesced)
     double* cent64 = nullptr;  // C x d fp64 (device, exact assignment)
+    double* cent64T = nullptr; // d x C fp64 (device, routing: coalesced, no converts)
     std::vector<float> host;   // kept for validation / read-back
 };
 
@@ -199,7 +199,6 @@ struct saap_layer {
     uint32_t* assign = nullptr;  // total_ns
     uint32_t* idx = nullptr;     // total_ns (local ids, ascending within bucket)
     uint32_t* invA = nullptr;    // total_ns: position-sink -> packed row (region A)
-    uint32_t* list = nullptr;    // total_ns scratch for filtered window lists
     uint32_t* off = nullptr;     // n_groups x (C+1)
     uint32_t* offA = nullptr;    // n_groups x (C+1)
     bool built = false;
@@ -226,17 +225,23 @@ struct saap_layer {
     bool last_tc = false;
     // routing parameter table cache (device arrays of per-group pointers)
     std::vector<const saap_router*> cached_routers;
-    const float** d_centT = nullptr;
-    const double** d_qm = nullptr;  // per group: w1, w2, vec (3 pointers)
+    const double** d_centT = nullptr;  // per group cent64T
+    const double** d_qm = nullptr;     // per group: w1, w2, vec (3 pointers)
+    // decode: TMA maps over the packed cache (+ gather buffer), built lazily
+    void* maps = nullptr;              // DecodeMaps (host copy)
+    uint16_t* gK = nullptr;            // gather buffer for general windows
+    uint16_t* gV = nullptr;
+    uint64_t gather_cap = 0;           // rows per group
 };
 
 struct saap_kvcache {
     saap_ctx* ctx = nullptr;
-    uint64_t n_groups = 0, d = 0, max_n = 0;
+    uint64_t n_groups = 0, d = 0, max_n = 0, rows = 0;
     const uint16_t* K = nullptr;  // borrowed
     const uint16_t* V = nullptr;
     saap_b200::GroupMeta* meta = nullptr;
     uint64_t* row_base = nullptr;
+    void* maps = nullptr;  // DecodeMaps
 };
 
 struct saap_graph {

@@ -15,32 +15,64 @@
 namespace saap_b200 {
 
 // ============================================================ route + plan
-
-
 struct Seg {
-    uint32_t kind;
+    uint32_t kind;  // KIND_ROWS (layer rows) or KIND_LIST (gather buffer rows)
     uint32_t len;
-    uint64_t start;
+    uint64_t start;  // ROWS: group-relative row; LIST: gather-buffer row
 };
 
 __device__ __forceinline__ bool precedes(double sa, uint32_t ia, double sb, uint32_t ib) {
     return sa > sb || (sa == sb && ia < ib);
 }
 
-// Bitonic sort of (score, id) pairs in shared memory: the comparator is the
-// reference's total order (attention.cpp:263-268), so the prefix equals the
-// std::partial_sort result bit for bit.
-__device__ void block_bitonic(double* ss, uint32_t* si, uint32_t n) {
+// Bitonic sort of (score, id) pairs under the reference's total order
+// (score desc, id asc; attention.cpp:263-268), so the prefix is exactly
+// std::partial_sort's.  n <= blockDim.x: one element per thread in registers,
+// distances < 32 through shuffles, larger ones through shared memory.
+__device__ void bitonic_regs(double& s, uint32_t& id, uint32_t n, double* xs, uint32_t* xi) {
+    const uint32_t t = threadIdx.x;
+    for (uint32_t k = 2; k <= n; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            double ps = 0.0;
+            uint32_t pi = 0;
+            if (j >= 32) {
+                if (t < n) {
+                    xs[t] = s;
+                    xi[t] = id;
+                }
+                __syncthreads();
+                if (t < n) {
+                    ps = xs[t ^ j];
+                    pi = xi[t ^ j];
+                }
+                __syncthreads();
+            } else {
+                ps = __shfl_xor_sync(0xFFFFFFFFu, s, j);
+                pi = __shfl_xor_sync(0xFFFFFFFFu, id, j);
+            }
+            if (t < n) {
+                const bool dir = (t & k) == 0;    // this block sorts in "precedes" order
+                const bool lower = (t & j) == 0;  // lower index of the pair
+                const bool p_first = precedes(ps, pi, s, id);
+                if ((lower == dir) ? p_first : !p_first) {
+                    s = ps;
+                    id = pi;
+                }
+            }
+        }
+    }
+}
+
+__device__ void bitonic_smem(double* ss, uint32_t* si, uint32_t n) {
     for (uint32_t k = 2; k <= n; k <<= 1) {
         for (uint32_t j = k >> 1; j > 0; j >>= 1) {
             for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-                uint32_t ixj = i ^ j;
+                const uint32_t ixj = i ^ j;
                 if (ixj > i) {
-                    bool asc = (i & k) == 0;  // "ascending" = precedes-order
-                    double a = ss[i], b = ss[ixj];
-                    uint32_t ia = si[i], ib = si[ixj];
-                    bool swap = asc ? precedes(b, ib, a, ia) : precedes(a, ia, b, ib);
-                    if (swap) {
+                    const bool asc = (i & k) == 0;
+                    const double a = ss[i], b = ss[ixj];
+                    const uint32_t ia = si[i], ib = si[ixj];
+                    if (asc ? precedes(b, ib, a, ia) : precedes(a, ia, b, ib)) {
                         ss[i] = b;
                         ss[ixj] = a;
                         si[i] = ib;
@@ -53,10 +85,56 @@ __device__ void block_bitonic(double* ss, uint32_t* si, uint32_t n) {
     }
 }
 
-__global__ void __launch_bounds__(512) route_plan_kernel(PlanArgs a) {
+// Stage 1: score a slice of centroids (one thread per centroid) and keep the
+// slice's top-`keep` in reference order.
+__global__ void __launch_bounds__(kSliceMax) route_score_kernel(RouteArgs a) {
+    __shared__ double pooled[128];
+    __shared__ double xs[kSliceMax];
+    __shared__ uint32_t xi[kSliceMax];
+    const uint32_t g = blockIdx.x, sl = blockIdx.y, tid = threadIdx.x;
+    if (a.mode == 1) {
+        // pooled_j = sum_i q_ij (fp64, rows in order)   attention.cpp:289-295
+        const float* q = a.q_route + (size_t)g * a.G * a.D;
+        for (uint32_t j = tid; j < a.D; j += blockDim.x) {
+            double s = 0.0;
+            for (uint32_t i = 0; i < a.G; ++i) s = __dadd_rn(s, (double)q[(size_t)i * a.D + j]);
+            pooled[j] = s;
+        }
+        __syncthreads();
+    }
+    const uint32_t c = sl * a.slice + tid;
+    double sc = -INFINITY;
+    uint32_t id = 0xFFFFFFFFu;
+    if (tid < a.slice && c < a.C) {
+        double s = 0.0;
+        if (a.mode == 1) {
+            // s_c = sum_j pooled_j * c_cj, mul rounded before add  attention.cpp:296-304
+            const double* cT = a.cent64T[g];
+#pragma unroll 16
+            for (uint32_t j = 0; j < a.D; ++j)
+                s = __dadd_rn(s, __dmul_rn(pooled[j], cT[(size_t)j * a.C + c]));
+        } else {
+            // Q-model: score_c = sum_i p_ic over the group rows   qmodel.cpp:493-499
+            const double* p = a.scores + (size_t)g * a.G * a.C;
+            for (uint32_t i = 0; i < a.G; ++i) s = __dadd_rn(s, p[(size_t)i * a.C + c]);
+        }
+        sc = s;
+        id = c;
+    }
+    bitonic_regs(sc, id, blockDim.x, xs, xi);
+    if (tid < a.keep) {
+        const size_t o = ((size_t)g * a.n_slices + sl) * a.keep + tid;
+        a.cand_s[o] = sc;
+        a.cand_i[o] = id;
+    }
+}
+
+// Stage 2 (one CTA per context): merge the slices' candidates into the top-l
+// list, build the visited set and cut it into tiles and work items.
+__global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t g = blockIdx.x;
-    const uint32_t tid = threadIdx.x;
+    const uint32_t tid = threadIdx.x, nth = blockDim.x;
     const GroupMeta gm = a.meta[g];
     const uint32_t n = gm.n, sink = gm.sink, T = gm.T;
     const uint32_t Cb = a.C;
@@ -64,71 +142,50 @@ __global__ void __launch_bounds__(512) route_plan_kernel(PlanArgs a) {
     const bool route = !fallback && a.probes > 0 && (a.mode == 1 || a.mode == 2);
     const uint32_t L = route ? a.probes : 0;
 
-    // smem carve: [sort scores P2 f64][sort ids P2 u32][bitmap C/32][segs L+4][misc]
+    // smem carve: [cand scores P2 f64][cand ids P2 u32][bitmap C/32][segs L+4][seg prefix]
     double* ss = reinterpret_cast<double*>(smem);
     uint32_t* si = reinterpret_cast<uint32_t*>(ss + (route ? a.P2 : 0));
     uint32_t* bitmap = si + (route ? a.P2 : 0);
     const uint32_t bm_words = route ? (Cb + 31) / 32 : 0;
     Seg* segs = reinterpret_cast<Seg*>(
             (reinterpret_cast<uintptr_t>(bitmap + bm_words) + 15) & ~uintptr_t(15));
-    __shared__ double pooled[128];
+    uint32_t* vpre = reinterpret_cast<uint32_t*>(segs + L + 4);  // virtual-row prefix per seg
     __shared__ unsigned long long s_keys;
-    __shared__ uint32_t s_maxv, s_nseg, s_base, s_total, s_wcnt[16], s_filtered;
+    __shared__ uint32_t s_maxv, s_wcnt[32], s_filtered, s_gbase, s_nseg, s_vrows;
+    __shared__ uint32_t s_tile0, s_ntiles, s_item0, s_nitems;
 
     if (tid == 0) {
         s_keys = 0;
         s_maxv = 0;
         s_filtered = 0;
+        s_gbase = 0;
     }
 
-    // ---------------- routing: scores -> (score desc, id asc) order
+    // ---------------- routing: merge candidates -> top-L in reference order
     if (route) {
-        if (a.mode == 1) {
-            // pooled_j = sum_i q_ij (fp64, rows in order)   attention.cpp:289-295
-            const float* q = a.q_route + (size_t)g * a.G * a.D;
-            for (uint32_t j = tid; j < a.D; j += blockDim.x) {
-                double s = 0.0;
-                for (uint32_t i = 0; i < a.G; ++i) s = __dadd_rn(s, (double)q[(size_t)i * a.D + j]);
-                pooled[j] = s;
+        const double* cs = a.cand_s + (size_t)g * a.n_cand;
+        const uint32_t* ci = a.cand_i + (size_t)g * a.n_cand;
+        if (a.P2 <= nth) {
+            double sc = -INFINITY;
+            uint32_t id = 0xFFFFFFFFu;
+            if (tid < a.n_cand) {
+                sc = cs[tid];
+                id = ci[tid];
+            }
+            bitonic_regs(sc, id, a.P2, ss, si);
+            __syncthreads();
+            if (tid < L) si[tid] = id;
+        } else {
+            for (uint32_t c = tid; c < a.P2; c += nth) {
+                ss[c] = c < a.n_cand ? cs[c] : -INFINITY;
+                si[c] = c < a.n_cand ? ci[c] : 0xFFFFFFFFu;
             }
             __syncthreads();
-            // s_c = sum_j pooled_j * c_cj, mul rounded before add (no FMA)
-            //                                              attention.cpp:296-304
-            const float* cT = a.centT[g];
-            for (uint32_t c = tid; c < a.P2; c += blockDim.x) {
-                if (c < Cb) {
-                    double s = 0.0;
-#pragma unroll 8
-                    for (uint32_t j = 0; j < a.D; ++j)
-                        s = __dadd_rn(s, __dmul_rn(pooled[j], (double)cT[(size_t)j * Cb + c]));
-                    ss[c] = s;
-                    si[c] = c;
-                } else {
-                    ss[c] = -INFINITY;
-                    si[c] = 0xFFFFFFFFu;
-                }
-            }
-        } else {
-            // Q-model: score_c = sum_i p_ic over the group rows in order
-            //                                              qmodel.cpp:493-499
-            const double* p = a.scores + (size_t)g * a.G * Cb;
-            for (uint32_t c = tid; c < a.P2; c += blockDim.x) {
-                if (c < Cb) {
-                    double s = 0.0;
-                    for (uint32_t i = 0; i < a.G; ++i) s = __dadd_rn(s, p[(size_t)i * Cb + c]);
-                    ss[c] = s;
-                    si[c] = c;
-                } else {
-                    ss[c] = -INFINITY;
-                    si[c] = 0xFFFFFFFFu;
-                }
-            }
+            bitonic_smem(ss, si, a.P2);
         }
+        for (uint32_t w = tid; w < bm_words; w += nth) bitmap[w] = 0;
         __syncthreads();
-        block_bitonic(ss, si, a.P2);
-        for (uint32_t w = tid; w < bm_words; w += blockDim.x) bitmap[w] = 0;
-        __syncthreads();
-        for (uint32_t b = tid; b < L; b += blockDim.x) {
+        for (uint32_t b = tid; b < L; b += nth) {
             atomicOr(&bitmap[si[b] >> 5], 1u << (si[b] & 31));
             if (a.selected) a.selected[(size_t)g * a.probes + b] = si[b];
         }
@@ -141,24 +198,11 @@ __global__ void __launch_bounds__(512) route_plan_kernel(PlanArgs a) {
     const uint32_t* offg = a.off + (size_t)g * (Cb + 1);
     const uint32_t* offAg = a.offA + (size_t)g * (Cb + 1);
     const uint32_t* idxg = a.idx + gm.ivf_base;
-    uint32_t nfixed = 0;  // window segments live after the L bucket segments
-    if (tid == 0) {
-        Seg* w = segs + L;
-        if (fallback) {
-            w[nfixed++] = Seg{KIND_ROWS, n, 0};
-        } else {
-            if (sink) w[nfixed++] = Seg{KIND_ROWS, sink, 0};
-            const uint32_t tail0 = rb > T ? rb : T;
-            if (n > tail0) w[nfixed++] = Seg{KIND_ROWS, n - tail0, tail0};
-            if (rb < T)  // region-A keys inside the recent window, via pos -> row map
-                w[nfixed++] = Seg{KIND_INVA, T - rb, gm.ivf_base + (rb - sink)};
-        }
-        s_nseg = L + nfixed;
-    }
+    const uint64_t gbuf = (uint64_t)g * a.gather_cap;  // this group's gather rows
     // bucket segments: region-A prefix of each selected bucket, cut at rb
     unsigned long long my_keys = 0;
     uint32_t my_max = 0;
-    for (uint32_t b = tid; b < L; b += blockDim.x) {
+    for (uint32_t b = tid; b < L; b += nth) {
         const uint32_t c = si[b];
         const uint32_t raw = offg[c + 1] - offg[c];
         uint32_t lenA = offAg[c + 1] - offAg[c];
@@ -167,7 +211,7 @@ __global__ void __launch_bounds__(512) route_plan_kernel(PlanArgs a) {
             const uint32_t lim = rb - sink;
             const uint32_t* seg = idxg + offg[c];
             while (lo < hi) {
-                uint32_t mid = (lo + hi) >> 1;
+                const uint32_t mid = (lo + hi) >> 1;
                 if (seg[mid] < lim) lo = mid + 1;
                 else hi = mid;
             }
@@ -181,11 +225,27 @@ __global__ void __launch_bounds__(512) route_plan_kernel(PlanArgs a) {
     if (my_max) atomicMax(&s_maxv, my_max);
     __syncthreads();
 
-    // region-B keys (positions [T, rb)) of selected buckets: compact a row list
+    // general windows: materialise the out-of-order rows in the gather buffer
+    //   recent > hint (rb < T): region-A rows with position in [rb, T) (pos -> row map)
+    //   recent < hint (rb > T): region-B rows in [T, rb) of selected buckets
+    auto gather_row = [&](uint32_t src_row, uint32_t dst) {
+        const uint32_t chunks = a.D / 8;  // 16-byte chunks per row
+        for (uint32_t e = 0; e < chunks; ++e) {
+            const uint64_t so = (gm.row_base + src_row) * a.D + e * 8;
+            const uint64_t d = (gbuf + dst) * a.D + e * 8;
+            *reinterpret_cast<uint4*>(a.gK + d) = *reinterpret_cast<const uint4*>(a.K + so);
+            *reinterpret_cast<uint4*>(a.gV + d) = *reinterpret_cast<const uint4*>(a.V + so);
+        }
+    };
+    if (!fallback && rb < T) {
+        for (uint32_t p = tid; p < T - rb; p += nth)
+            gather_row(a.invA[gm.ivf_base + (rb + p - sink)], p);
+        if (tid == 0) s_gbase = T - rb;
+    }
     if (route && rb > T) {
         uint32_t base = 0;
         const uint32_t warp = tid >> 5, lane = tid & 31;
-        for (uint32_t p0 = T; p0 < rb; p0 += blockDim.x) {
+        for (uint32_t p0 = T; p0 < rb; p0 += nth) {
             const uint32_t pos = p0 + tid;
             bool f = false;
             if (pos < rb) {
@@ -196,28 +256,70 @@ __global__ void __launch_bounds__(512) route_plan_kernel(PlanArgs a) {
             if (lane == 0) s_wcnt[warp] = __popc(bal);
             __syncthreads();
             uint32_t wex = 0, tot = 0;
-            for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+            for (uint32_t w = 0; w < nth / 32; ++w) {
                 if (w < warp) wex += s_wcnt[w];
                 tot += s_wcnt[w];
             }
-            if (f) a.list[gm.ivf_base + base + wex + __popc(bal & ((1u << lane) - 1))] = pos;
+            if (f) gather_row(pos, base + wex + __popc(bal & ((1u << lane) - 1)));
             base += tot;
             __syncthreads();
         }
-        if (tid == 0 && base) {
-            segs[L + nfixed] = Seg{KIND_LIST, base, gm.ivf_base};
-            s_nseg = L + nfixed + 1;
+        if (tid == 0) {
             s_filtered = base;
+            s_gbase = base;
         }
-        __syncthreads();
     }
-
-    // ---------------- items: segments cut into item_keys chunks
+    __syncthreads();
     if (tid == 0) {
-        uint32_t total = 0;
-        for (uint32_t s = 0; s < s_nseg; ++s) total += (segs[s].len + a.item_keys - 1) / a.item_keys;
-        s_total = total;
-        s_base = total ? atomicAdd(&a.ctr->n_items, total * a.n_hchunks) : 0;
+        uint32_t nseg = L;
+        if (fallback) {
+            segs[nseg++] = Seg{KIND_ROWS, n, 0};
+        } else {
+            if (sink) segs[nseg++] = Seg{KIND_ROWS, sink, 0};
+            const uint32_t tail0 = rb > T ? rb : T;
+            if (n > tail0) segs[nseg++] = Seg{KIND_ROWS, n - tail0, tail0};
+            if (s_gbase) segs[nseg++] = Seg{KIND_LIST, s_gbase, gbuf};
+        }
+        s_nseg = nseg;
+    }
+    __syncthreads();
+
+    // ---------------- virtual row layout: segment s occupies 8-aligned rows
+    // [vpre[s], vpre[s] + ceil8(len_s)); tile t = virtual rows [128t, 128t+128)
+    const uint32_t nseg = s_nseg;
+    {
+        const uint32_t per = (nseg + nth - 1) / nth;
+        const uint32_t lo = min(nseg, tid * per), hi = min(nseg, lo + per);
+        uint32_t sum = 0;
+        for (uint32_t s2 = lo; s2 < hi; ++s2) sum += (segs[s2].len + 7) & ~7u;
+        const uint32_t lane = tid & 31, warp = tid >> 5;
+        uint32_t incl = sum;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += v;
+        }
+        if (lane == 31) s_wcnt[warp] = incl;
+        __syncthreads();
+        uint32_t wbase = 0, tot = 0;
+        for (uint32_t w = 0; w < nth / 32; ++w) {
+            if (w < warp) wbase += s_wcnt[w];
+            tot += s_wcnt[w];
+        }
+        uint32_t run = wbase + incl - sum;
+        for (uint32_t s2 = lo; s2 < hi; ++s2) {
+            vpre[s2] = run;
+            run += (segs[s2].len + 7) & ~7u;
+        }
+        if (tid == 0) s_vrows = tot;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const uint32_t ntiles = (s_vrows + kTileRows - 1) / kTileRows;
+        const uint32_t nitems = (ntiles + a.item_tiles - 1) / a.item_tiles;
+        s_ntiles = ntiles;
+        s_nitems = nitems;
+        s_tile0 = ntiles ? atomicAdd(&a.ctr->pad[0], ntiles) : 0;
+        s_item0 = nitems ? atomicAdd(&a.ctr->n_items, nitems * a.n_hchunks) : 0;
         unsigned long long keys;
         if (fallback) keys = n;
         else keys = (unsigned long long)sink + (n - rb) + s_keys + s_filtered;
@@ -228,96 +330,163 @@ __global__ void __launch_bounds__(512) route_plan_kernel(PlanArgs a) {
         st.reserved = 0;
         a.stats[g] = st;
         for (uint32_t hc = 0; hc < a.n_hchunks; ++hc)
-            a.qslots[g * a.n_hchunks + hc] = QSlot{s_base + hc * total, total};
+            a.qslots[g * a.n_hchunks + hc] = QSlot{s_item0 + hc * nitems, nitems};
     }
     __syncthreads();
-    const uint32_t total = s_total, base = s_base;
-    if (total == 0) {  // nothing visited: zero rows, empty_attention (attention.cpp:147-152)
-        for (uint32_t e = tid; e < a.G * a.D; e += blockDim.x) a.out[(size_t)g * a.G * a.D + e] = 0.f;
+    const uint32_t ntiles = s_ntiles, nitems = s_nitems, tile0 = s_tile0;
+    if (nitems == 0) {  // nothing visited: zero rows, empty_attention (attention.cpp:147-152)
+        for (uint32_t e = tid; e < a.G * a.D; e += nth) a.out[(size_t)g * a.G * a.D + e] = 0.f;
         return;
     }
-    // chunk prefix per segment (serial over <= L+4 segments, then parallel write)
-    __shared__ uint32_t s_pref[1];
-    (void)s_pref;
-    for (uint32_t s = tid; s < s_nseg; s += blockDim.x) {
-        uint32_t before = 0;
-        for (uint32_t t = 0; t < s; ++t) before += (segs[t].len + a.item_keys - 1) / a.item_keys;
-        const Seg sg = segs[s];
-        const uint32_t nch = (sg.len + a.item_keys - 1) / a.item_keys;
-        for (uint32_t k = 0; k < nch; ++k) {
-            const uint32_t len = min(a.item_keys, sg.len - k * a.item_keys);
-            for (uint32_t hc = 0; hc < a.n_hchunks; ++hc) {
-                Item it;
-                it.qslot = g * a.n_hchunks + hc;
-                it.n_kind = len | (sg.kind << 30);
-                it.start = sg.start + (uint64_t)k * a.item_keys;
-                a.items[base + hc * total + before + k] = it;
-            }
+    for (uint32_t t = tid; t < ntiles; t += nth) a.tiles[tile0 + t].npieces = 0;
+    __syncthreads();
+    // pieces: one per (segment, overlapped tile); slot order inside a tile is free
+    for (uint32_t s2 = tid; s2 < nseg; s2 += nth) {
+        const Seg sg = segs[s2];
+        if (sg.len == 0) continue;
+        const uint32_t v0 = vpre[s2], v8 = v0 + ((sg.len + 7) & ~7u), vend = v0 + sg.len;
+        for (uint32_t t = v0 / kTileRows; t * kTileRows < v8; ++t) {
+            const uint32_t a0 = max(v0, t * kTileRows), b0 = min(v8, (t + 1) * kTileRows);
+            const uint32_t keys_end = min(b0, vend);
+            if (keys_end <= a0) continue;
+            PieceRec pr;
+            pr.len = (keys_end - a0) | (sg.kind == KIND_LIST ? kPieceGather : 0u);
+            pr.srow = a0 - t * kTileRows;
+            pr.row = (sg.kind == KIND_LIST ? 0 : gm.row_base) + sg.start + (a0 - v0);
+            TileRec* tr = a.tiles + tile0 + t;
+            const uint32_t slot = atomicAdd(&tr->npieces, 1u);
+            tr->p[slot] = pr;
         }
+    }
+    for (uint32_t e = tid; e < nitems * a.n_hchunks; e += nth) {
+        const uint32_t hc = e / nitems, k = e % nitems;
+        ItemRec it;
+        it.qslot = g * a.n_hchunks + hc;
+        it.tile_first = tile0 + k * a.item_tiles;
+        it.ntiles = min(a.item_tiles, ntiles - k * a.item_tiles);
+        it.pad = 0;
+        a.items[s_item0 + e] = it;
     }
 }
 
 // ============================================================ attention
-
-
-template <int D, int NS>
-struct DecodeSmem {
-    uint16_t K[NS][kTileKeys][D];
-    uint16_t V[NS][kTileKeys][D];
-    float red[kComputeWarps][kHeadsPerSlot][D];
-    float P[kTileKeys][kHeadsPerSlot];
-    float wmax[kComputeWarps][kHeadsPerSlot];
-    float wl[kComputeWarps][kHeadsPerSlot];
-    uint64_t full[NS];
-    uint64_t empty[NS];
-    int4 meta[NS];  // item, tile, nt, last
-    int flag;
+// One CTA per SM.  Warp 8 produces: TMA (cp.async.bulk.tensor, 128B/64B
+// swizzle) loads of 128-row K and V tiles into an NS-deep ring; the 8
+// compute warps each own 16 rows of a tile and run QK^T and PV on the tensor
+// cores (mma.sync m16n8k16, fp32 accumulation):
+//   S: A = [q1; q2; q3] (3-term bf16 split of q, fp32-exact), B = K rows
+//   O: A = [p1; p2; p3] (3-term bf16 split of the fp32 softmax weights,
+//      ~fp32-exact), B = V rows (ldmatrix.trans)
+// with a per-warp online softmax (lazy rescaling), merged across warps at
+// the end of an item and across items by the last CTA of a query slot.
+template <int D>
+struct DecodeCfg {
+    static constexpr int RB = 2 * D;                   // bytes per row
+    static constexpr int HALF = RB >= 128 ? 128 : RB;  // swizzle row bytes
+    static constexpr int HALVES = RB / HALF;
+    static constexpr int TILE_BYTES = kTileRows * RB;  // K (or V) bytes per tile
+    static constexpr int NS = D == 128 ? 3 : (D == 64 ? 6 : 8);
+    static constexpr int KSTEPS = D / 16;
+    static constexpr int NT = D / 8;  // PV n-tiles
 };
 
 template <int D>
-__device__ __forceinline__ void load_v(const uint16_t* row, int lane, float* v) {
-    constexpr int DPL = D / 32;
-    if constexpr (DPL == 4) {
-        uint2 x = *reinterpret_cast<const uint2*>(row + lane * 4);
-        v[0] = bf16lo(x.x);
-        v[1] = bf16hi(x.x);
-        v[2] = bf16lo(x.y);
-        v[3] = bf16hi(x.y);
-    } else if constexpr (DPL == 2) {
-        uint32_t x = *reinterpret_cast<const uint32_t*>(row + lane * 2);
-        v[0] = bf16lo(x);
-        v[1] = bf16hi(x);
-    } else {
-        v[0] = __uint_as_float(((uint32_t)row[lane]) << 16);
-    }
+struct DecodeSmem2 {
+    using CF = DecodeCfg<D>;
+    uint8_t K[CF::NS][CF::TILE_BYTES];
+    uint8_t V[CF::NS][CF::TILE_BYTES];
+    float q[CF::NS][kHeadsPerSlot][D];
+    float redO[kComputeWarps][kHeadsPerSlot][D];
+    float redm[kComputeWarps][kHeadsPerSlot];
+    float redl[kComputeWarps][kHeadsPerSlot];
+    uint64_t full[CF::NS];
+    uint64_t empty[CF::NS];
+    int4 meta[CF::NS];    // item, tile-in-item | last<<31, qslot, nq (q heads loaded)
+    uint4 valid[CF::NS];  // 128-bit row validity mask
+    int flag;
+};
+
+// swizzled byte offset of (row, 16-byte chunk) inside one tile half
+template <int D>
+__device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
+    using CF = DecodeCfg<D>;
+    if constexpr (CF::HALF == 128) return row * 128 + ((chunk ^ (row & 7)) << 4);
+    else return row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4);
 }
 
-// Warp roles: warps 0..7 compute, warp 8 produces (TMA bulk copies of 64-key
-// K/V tiles into an NS-deep ring; contiguous bucket segments are one copy
-// per tile, row lists one copy per row).  Items are fetched dynamically.
-template <int D, int NS>
-__global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1) decode_kernel(DecodeArgs a) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    auto& s = *reinterpret_cast<DecodeSmem<D, NS>*>(smem_raw);
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int x, int y,
+                                      uint64_t* bar) {
+    asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+            "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+            : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, "
+            "{%4, %5, %6, %7}, {%8, %9}, {%0, %1, %2, %3};"
+            : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    return (uint32_t)f32_to_bf16_rne(lo) | ((uint32_t)f32_to_bf16_rne(hi) << 16);
+}
+__device__ __forceinline__ float bf16_round(float x) {
+    return __uint_as_float((uint32_t)f32_to_bf16_rne(x) << 16);
+}
+
+template <int D>
+__global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
+        decode_kernel(const __grid_constant__ DecodeMaps maps, DecodeArgs a) {
+    using CF = DecodeCfg<D>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    auto& s = *reinterpret_cast<DecodeSmem2<D>*>(
+            (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < NS; ++i) {
+        for (int i = 0; i < CF::NS; ++i) {
             mbar_init(&s.full[i], 1);
             mbar_init(&s.empty[i], kComputeWarps);
         }
         fence_mbar_init();
     }
+    // gap rows of a tile are masked (p = 0) but still enter the PV MMA: start
+    // from zeroed V so 0 * stale never meets a non-finite value
+    for (uint32_t e = threadIdx.x; e < sizeof(s.V) / 16; e += blockDim.x)
+        reinterpret_cast<uint4*>(&s.V[0][0])[e] = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
 
     const uint32_t n_items = *reinterpret_cast<volatile uint32_t*>(&a.ctr->n_items);
 
     if (warp == kComputeWarps) {
         // ------------------------------------------------ producer
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.k64) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.k8) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.v64) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.v8) : "memory");
+        }
         uint32_t stage = 0, phase = 0;
+        uint32_t it = 0;
+        if (lane == 0) it = atomicAdd(&a.ctr->work, 1u);
         for (;;) {
-            uint32_t it = 0;
-            if (lane == 0) it = atomicAdd(&a.ctr->work, 1u);
             it = __shfl_sync(0xFFFFFFFFu, it, 0);
             if (it >= n_items) {
                 if (lane == 0) {
@@ -327,252 +496,305 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1) decode_kernel(Dec
                 }
                 break;
             }
-            const Item itm = a.items[it];
-            const uint32_t n = itm.n_kind & 0x3FFFFFFFu, kind = itm.n_kind >> 30;
-            const uint32_t g = itm.qslot / a.n_hchunks;
-            const uint64_t rbase = a.row_base[g];
-            const uint32_t ntiles = (n + kTileKeys - 1) / kTileKeys;
-            for (uint32_t t = 0; t < ntiles; ++t) {
-                const uint32_t nt = min((uint32_t)kTileKeys, n - t * kTileKeys);
+            const ItemRec itm = a.items[it];
+            uint32_t next = 0;
+            if (lane == 0) next = atomicAdd(&a.ctr->work, 1u);  // prefetch the next item id
+            const uint32_t g = itm.qslot / a.n_hchunks, hc = itm.qslot % a.n_hchunks;
+            const uint32_t nq = min((uint32_t)kHeadsPerSlot, a.G - hc * kHeadsPerSlot);
+            for (uint32_t t = 0; t < itm.ntiles; ++t) {
+                // lane p owns piece p of the tile: boxes, bytes and validity bits
+                const TileRec* tr = a.tiles + itm.tile_first + t;
+                const uint32_t np = tr->npieces;
+                uint32_t len = 0, srow = 0, gat = 0;
+                uint64_t row = 0;
+                if ((uint32_t)lane < np) {
+                    const PieceRec pr = tr->p[lane];
+                    len = pr.len & ~kPieceGather;
+                    gat = pr.len & kPieceGather;
+                    srow = pr.srow;
+                    row = pr.row;
+                }
+                const uint32_t r8 = (len + 7) & ~7u;
+                uint32_t bytes = r8 * CF::RB * 2;
+                uint32_t vm[4];
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    const uint32_t lo = max(srow, (uint32_t)w * 32), hi = min(srow + len, (uint32_t)w * 32 + 32);
+                    uint32_t m = 0;
+                    if (hi > lo) m = (hi - lo == 32 ? 0xFFFFFFFFu : ((1u << (hi - lo)) - 1u)) << (lo - w * 32);
+                    vm[w] = m;
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    bytes += __shfl_xor_sync(0xFFFFFFFFu, bytes, o);
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) vm[w] |= __shfl_xor_sync(0xFFFFFFFFu, vm[w], o);
+                }
                 if (lane == 0) {
                     mbar_wait(&s.empty[stage], phase ^ 1);
-                    s.meta[stage] = make_int4((int)it, (int)t, (int)nt, t + 1 == ntiles);
-                    mbar_arrive_expect_tx(&s.full[stage], nt * D * 2 * 2);
+                    s.valid[stage] = make_uint4(vm[0], vm[1], vm[2], vm[3]);
+                    s.meta[stage] = make_int4((int)it, (int)(t | ((t + 1 == itm.ntiles) ? 0x80000000u : 0u)),
+                                              (int)itm.qslot, (int)nq);
+                    mbar_arrive_expect_tx(&s.full[stage], bytes + (t == 0 ? nq * D * 4 : 0));
+                    if (t == 0)
+                        bulk_g2s(&s.q[stage][0][0], a.q + ((size_t)g * a.G + hc * kHeadsPerSlot) * D,
+                                 nq * D * 4, &s.full[stage]);
                 }
                 __syncwarp();
-                if (kind == KIND_ROWS) {
-                    if (lane == 0) {
-                        const uint64_t r0 = rbase + itm.start + (uint64_t)t * kTileKeys;
-                        bulk_g2s(&s.K[stage][0][0], a.K + r0 * D, nt * D * 2, &s.full[stage]);
-                        bulk_g2s(&s.V[stage][0][0], a.V + r0 * D, nt * D * 2, &s.full[stage]);
-                    }
-                } else {
-                    const uint32_t* lst = kind == KIND_INVA ? a.invA : a.list;
-                    for (uint32_t j = lane; j < nt; j += 32) {
-                        const uint64_t r = rbase + lst[itm.start + (uint64_t)t * kTileKeys + j];
-                        bulk_g2s(&s.K[stage][j][0], a.K + r * D, D * 2, &s.full[stage]);
-                        bulk_g2s(&s.V[stage][j][0], a.V + r * D, D * 2, &s.full[stage]);
+                if (len) {
+                    const CUtensorMap* mk64 = gat ? &maps.gk64 : &maps.k64;
+                    const CUtensorMap* mk8 = gat ? &maps.gk8 : &maps.k8;
+                    const CUtensorMap* mv64 = gat ? &maps.gv64 : &maps.v64;
+                    const CUtensorMap* mv8 = gat ? &maps.gv8 : &maps.v8;
+                    uint32_t rem = r8, sr = srow;
+                    int y = (int)row;
+                    while (rem) {
+                        const bool big = rem >= 64;
+#pragma unroll
+                        for (int h = 0; h < CF::HALVES; ++h) {
+                            const uint32_t off = h * kTileRows * CF::HALF + sr * CF::HALF;
+                            tma2d(&s.K[stage][off], big ? mk64 : mk8, h * (CF::HALF / 2), y, &s.full[stage]);
+                            tma2d(&s.V[stage][off], big ? mv64 : mv8, h * (CF::HALF / 2), y, &s.full[stage]);
+                        }
+                        const uint32_t step = big ? 64 : 8;
+                        rem -= step;
+                        sr += step;
+                        y += (int)step;
                     }
                 }
-                if (++stage == NS) {
+                __syncwarp();
+                if (++stage == CF::NS) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
+            it = next;
         }
         return;
     }
 
     // ---------------------------------------------------- consumers
-    constexpr int LPK = D / 8;    // lanes per key row in QK (8 dims each)
-    constexpr int KPI = 32 / LPK; // keys per warp instruction
-    constexpr int STEPS = 8 / KPI;
-    constexpr int DPL = D / 32;   // dims per lane in PV
-    const int tid = threadIdx.x;  // 0..255
-    const int hl = lane & 3;      // head of the score this lane ends up holding
-    const int idx = lane & (LPK - 1);
-    const int key_local = (idx >> 2) * KPI + lane / LPK;
+    const int gid = lane >> 2, tig = lane & 3;
+    const bool upper = lane >= 16;  // rows g+4: q_lo / p2
+    const int hq = gid & 3;         // head of this lane's score rows
+    const int row0 = warp * 16;     // this warp's 16 rows of the tile
+    const int mtx = lane >> 3, r8 = lane & 7;
 
-    float qr[4][8];
-    float m_run[4];
-    float acc[4][DPL];
-    float l_lane = 0.f;
-    uint32_t cur_qslot = 0, cur_item = 0;
+    uint32_t qa[CF::KSTEPS][4];  // A fragments of [q1; q2; q3; 0]
+    float o[CF::NT][4];
+    float m_run = -INFINITY, l_run = 0.f;
+    uint32_t cur_item = 0, cur_qslot = 0;
 
     uint32_t stage = 0, phase = 0;
     for (;;) {
         mbar_wait(&s.full[stage], phase);
         const int4 mt = s.meta[stage];
         if (mt.x < 0) break;
-        const int nt = mt.z;
-        if (mt.y == 0) {  // item start: load the query slot's 4 heads, reset state
+        const uint32_t tile_in_item = (uint32_t)mt.y & 0x7FFFFFFFu;
+        const bool last = ((uint32_t)mt.y >> 31) != 0;
+        if (tile_in_item == 0) {
             cur_item = (uint32_t)mt.x;
-            cur_qslot = a.items[cur_item].qslot;
-            const uint32_t g = cur_qslot / a.n_hchunks, hc = cur_qslot % a.n_hchunks;
+            cur_qslot = (uint32_t)mt.z;
+            const int nq = mt.w;
+            // q -> 3-term bf16 split as A rows: q1 (rows 0-3, lanes < 16),
+            // q2 (rows 4-7, lanes >= 16), q3 (rows 8-11, lanes < 16); scaled
+            // by log2(e)/sqrt(d) after the MMA, so bf16 queries stay exact
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const uint32_t head = hc * 4 + h;
-                if (head < a.G) {
-                    const float4* qp = reinterpret_cast<const float4*>(
-                            a.q + ((size_t)g * a.G + head) * D + (lane % LPK) * 8);
-                    float4 x0 = qp[0], x1 = qp[1];
-                    qr[h][0] = x0.x * a.qscale;
-                    qr[h][1] = x0.y * a.qscale;
-                    qr[h][2] = x0.z * a.qscale;
-                    qr[h][3] = x0.w * a.qscale;
-                    qr[h][4] = x1.x * a.qscale;
-                    qr[h][5] = x1.y * a.qscale;
-                    qr[h][6] = x1.z * a.qscale;
-                    qr[h][7] = x1.w * a.qscale;
+            for (int k = 0; k < CF::KSTEPS; ++k) {
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    const int d0 = k * 16 + half * 8 + tig * 2;
+                    float x[2] = {0.f, 0.f};
+                    if (hq < nq) {
+                        x[0] = s.q[stage][hq][d0];
+                        x[1] = s.q[stage][hq][d0 + 1];
+                    }
+                    float t1[2], t2[2], t3[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        t1[e] = bf16_round(x[e]);
+                        const float r1 = x[e] - t1[e];
+                        t2[e] = bf16_round(r1);
+                        t3[e] = r1 - t2[e];
+                    }
+                    // half 0 -> a0a1 (row g) / a2a3 (row g+8); half 1 -> a4a5 / a6a7
+                    qa[k][2 * half] = upper ? pack_bf16(t2[0], t2[1]) : pack_bf16(t1[0], t1[1]);
+                    qa[k][2 * half + 1] = upper ? 0u : pack_bf16(t3[0], t3[1]);
+                }
+            }
+#pragma unroll
+            for (int n = 0; n < CF::NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+            m_run = -INFINITY;
+            l_run = 0.f;
+        }
+        const uint32_t vbits = ((&s.valid[stage].x)[warp >> 1] >> ((warp & 1) * 16)) & 0xFFFFu;
+        if (vbits) {
+            // ---- S = [q_hi; q_lo] K^T for this warp's 16 rows
+            const uint32_t kbase = smem_u32(&s.K[stage][0]);
+            float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
+            const uint32_t krow = row0 + (mtx >> 1) * 8 + r8;
+#pragma unroll
+            for (int k = 0; k < CF::KSTEPS; ++k) {
+                const uint32_t chunk = 2 * k + (mtx & 1);  // 16-byte chunk within the row
+                const uint32_t h = chunk / (CF::HALF / 16), cc = chunk % (CF::HALF / 16);
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(kbase + h * kTileRows * CF::HALF + swz<D>(krow, cc), b0, b1, b2, b3);
+                mma16816(c0, qa[k][0], qa[k][1], qa[k][2], qa[k][3], b0, b1);
+                mma16816(c1, qa[k][0], qa[k][1], qa[k][2], qa[k][3], b2, b3);
+            }
+            // scores for head hq; keys c0 -> row0 + 2*tig + {0,1}, c1 -> row0 + 8 + 2*tig + {0,1}
+            // rows g + g+8 here, g+4 (+ zero row g+12) on lane ^ 16
+            float sc[4] = {c0[0] + c0[2], c0[1] + c0[3], c1[0] + c1[2], c1[1] + c1[3]};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) sc[i] = (sc[i] + __shfl_xor_sync(0xFFFFFFFFu, sc[i], 16)) * a.qscale;
+            const uint32_t kb = 2 * tig;
+            if (!((vbits >> kb) & 1)) sc[0] = -INFINITY;
+            if (!((vbits >> (kb + 1)) & 1)) sc[1] = -INFINITY;
+            if (!((vbits >> (kb + 8)) & 1)) sc[2] = -INFINITY;
+            if (!((vbits >> (kb + 9)) & 1)) sc[3] = -INFINITY;
+            float mx = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
+            mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, 2));
+            // lazy rescale: keep the running max unless this tile exceeds it by 2^8
+            const bool grow = mx > m_run + 8.f;
+            if (__any_sync(0xFFFFFFFFu, grow)) {
+                const float mnew = grow ? mx : m_run;
+                const float alpha = fast_exp2(m_run - mnew);
+                m_run = mnew;
+                l_run *= alpha;
+#pragma unroll
+                for (int n = 0; n < CF::NT; ++n) {
+                    o[n][0] *= alpha;
+                    o[n][1] *= alpha;
+                    o[n][2] *= alpha;
+                    o[n][3] *= alpha;
+                }
+            }
+            float p[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) p[i] = fast_exp2(sc[i] - m_run);  // -inf -> 0
+            if (!upper) l_run += (p[0] + p[1]) + (p[2] + p[3]);
+            // 3-term bf16 split: lanes < 16 carry p1 (rows g) and p3 (rows g+8),
+            // lanes >= 16 carry p2 (rows g+4) and zeros (rows g+12)
+            uint32_t pa0, pa1, pa2, pa3;
+            {
+                float t1[4], t2[4], t3[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    t1[i] = bf16_round(p[i]);
+                    const float r1 = p[i] - t1[i];
+                    t2[i] = bf16_round(r1);
+                    t3[i] = r1 - t2[i];
+                }
+                if (!upper) {
+                    pa0 = pack_bf16(t1[0], t1[1]);
+                    pa2 = pack_bf16(t1[2], t1[3]);
+                    pa1 = pack_bf16(t3[0], t3[1]);
+                    pa3 = pack_bf16(t3[2], t3[3]);
                 } else {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) qr[h][j] = 0.f;
+                    pa0 = pack_bf16(t2[0], t2[1]);
+                    pa2 = pack_bf16(t2[2], t2[3]);
+                    pa1 = 0u;
+                    pa3 = 0u;
                 }
-                m_run[h] = -INFINITY;
-#pragma unroll
-                for (int j = 0; j < DPL; ++j) acc[h][j] = 0.f;
             }
-            l_lane = 0.f;
-        }
-
-        // ---- S = q . k for this warp's 8 keys (lane owns 8 dims of a key)
-        float part[LPK];
-        const uint16_t* Ks = &s.K[stage][0][0];
+            // ---- O += P V   (B = V rows via ldmatrix.trans)
+            const uint32_t vbase = smem_u32(&s.V[stage][0]);
+            const uint32_t vrow = row0 + (mtx & 1) * 8 + r8;
 #pragma unroll
-        for (int st = 0; st < STEPS; ++st) {
-            const int key = warp * 8 + st * KPI + lane / LPK;
-            const uint4 kv = *reinterpret_cast<const uint4*>(Ks + key * D + (lane % LPK) * 8);
-            const float k0 = bf16lo(kv.x), k1 = bf16hi(kv.x), k2 = bf16lo(kv.y), k3 = bf16hi(kv.y);
-            const float k4 = bf16lo(kv.z), k5 = bf16hi(kv.z), k6 = bf16lo(kv.w), k7 = bf16hi(kv.w);
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                float x = qr[h][0] * k0;
-                x = fmaf(qr[h][1], k1, x);
-                x = fmaf(qr[h][2], k2, x);
-                x = fmaf(qr[h][3], k3, x);
-                x = fmaf(qr[h][4], k4, x);
-                x = fmaf(qr[h][5], k5, x);
-                x = fmaf(qr[h][6], k6, x);
-                x = fmaf(qr[h][7], k7, x);
-                part[st * 4 + h] = x;
-            }
-        }
-        // transpose-reduce across the LPK lanes of each key: lane keeps value #idx
-#pragma unroll
-        for (int m = LPK / 2; m >= 1; m >>= 1) {
-            const bool up = (lane & m) != 0;
-#pragma unroll
-            for (int i = 0; i < m; ++i) {
-                const float send = up ? part[i] : part[i + m];
-                const float keep = up ? part[i + m] : part[i];
-                part[i] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, m);
-            }
-        }
-        const int key = warp * 8 + key_local;
-        const bool valid = key < nt;
-        const float sc = valid ? part[0] : -INFINITY;
-
-        // ---- online softmax over the tile (Alg. 1)
-        float v = sc;
-        v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, 4));
-        v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, 8));
-        v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, 16));
-        if (lane < 4) s.wmax[warp][lane] = v;
-        named_bar_sync(1, kComputeWarps * 32);
-        float alpha[4], mnew[4];
-        {
-            float4 t = *reinterpret_cast<const float4*>(s.wmax[0]);
-#pragma unroll
-            for (int w = 1; w < kComputeWarps; ++w) {
-                const float4 u = *reinterpret_cast<const float4*>(s.wmax[w]);
-                t.x = fmaxf(t.x, u.x);
-                t.y = fmaxf(t.y, u.y);
-                t.z = fmaxf(t.z, u.z);
-                t.w = fmaxf(t.w, u.w);
-            }
-            mnew[0] = fmaxf(m_run[0], t.x);
-            mnew[1] = fmaxf(m_run[1], t.y);
-            mnew[2] = fmaxf(m_run[2], t.z);
-            mnew[3] = fmaxf(m_run[3], t.w);
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                alpha[h] = fast_exp2(m_run[h] - mnew[h]);
-                m_run[h] = mnew[h];
-            }
-        }
-        const float m_h = hl == 0 ? mnew[0] : hl == 1 ? mnew[1] : hl == 2 ? mnew[2] : mnew[3];
-        const float a_h = hl == 0 ? alpha[0] : hl == 1 ? alpha[1] : hl == 2 ? alpha[2] : alpha[3];
-        const float p = valid ? fast_exp2(sc - m_h) : 0.f;
-        l_lane = l_lane * a_h + p;
-        s.P[key][hl] = p;
-        named_bar_sync(1, kComputeWarps * 32);
-
-        // ---- O += P V (lane owns DPL dims x 4 heads; warp owns keys w, w+8, ..)
-#pragma unroll
-        for (int h = 0; h < 4; ++h)
-#pragma unroll
-            for (int j = 0; j < DPL; ++j) acc[h][j] *= alpha[h];
-        const uint16_t* Vs = &s.V[stage][0][0];
-#pragma unroll 4
-        for (int i = 0; i < 8; ++i) {
-            const int k = warp + 8 * i;
-            if (k < nt) {
-                const float4 pk = *reinterpret_cast<const float4*>(s.P[k]);
-                float vv[DPL];
-                load_v<D>(Vs + k * D, lane, vv);
-#pragma unroll
-                for (int j = 0; j < DPL; ++j) {
-                    acc[0][j] = fmaf(pk.x, vv[j], acc[0][j]);
-                    acc[1][j] = fmaf(pk.y, vv[j], acc[1][j]);
-                    acc[2][j] = fmaf(pk.z, vv[j], acc[2][j]);
-                    acc[3][j] = fmaf(pk.w, vv[j], acc[3][j]);
-                }
+            for (int j = 0; j < CF::NT / 2; ++j) {
+                const uint32_t chunk = 2 * j + (mtx >> 1);
+                const uint32_t h = chunk / (CF::HALF / 16), cc = chunk % (CF::HALF / 16);
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_t(vbase + h * kTileRows * CF::HALF + swz<D>(vrow, cc), b0, b1, b2, b3);
+                mma16816(o[2 * j], pa0, pa1, pa2, pa3, b0, b1);
+                mma16816(o[2 * j + 1], pa0, pa1, pa2, pa3, b2, b3);
             }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&s.empty[stage]);
 
-        if (mt.w) {
-            // ---- item done: reduce the 8 warps' partials (m is shared)
-            float lw = l_lane;
-            lw += __shfl_xor_sync(0xFFFFFFFFu, lw, 4);
-            lw += __shfl_xor_sync(0xFFFFFFFFu, lw, 8);
-            lw += __shfl_xor_sync(0xFFFFFFFFu, lw, 16);
-            if (lane < 4) s.wl[warp][lane] = lw;
+        if (last) {
+            // ---- item done: merge the 8 warps' (m, l, O) states
+            float lw = l_run;
+            lw += __shfl_xor_sync(0xFFFFFFFFu, lw, 1);
+            lw += __shfl_xor_sync(0xFFFFFFFFu, lw, 2);
+            // O rows: lanes < 16 hold p1 (c[0..1]) + p3 (c[2..3]); lanes >= 16 hold p2
 #pragma unroll
-            for (int h = 0; h < 4; ++h)
-#pragma unroll
-                for (int j = 0; j < DPL; ++j) s.red[warp][h][lane * DPL + j] = acc[h][j];
+            for (int n = 0; n < CF::NT; ++n) {
+                float x0 = o[n][0] + (upper ? 0.f : o[n][2]);
+                float x1 = o[n][1] + (upper ? 0.f : o[n][3]);
+                x0 += __shfl_xor_sync(0xFFFFFFFFu, x0, 16);
+                x1 += __shfl_xor_sync(0xFFFFFFFFu, x1, 16);
+                if (!upper) {
+                    s.redO[warp][hq][n * 8 + 2 * tig] = x0;
+                    s.redO[warp][hq][n * 8 + 2 * tig + 1] = x1;
+                }
+            }
+            if (!upper && tig == 0) {
+                s.redm[warp][hq] = m_run;
+                s.redl[warp][hq] = lw;
+            }
             named_bar_sync(1, kComputeWarps * 32);
 
             const QSlot qs = a.qslots[cur_qslot];
             const uint32_t g = cur_qslot / a.n_hchunks, hc = cur_qslot % a.n_hchunks;
-            constexpr int NOUT = 4 * D;
+            const int tid = threadIdx.x;
+            constexpr int NOUT = kHeadsPerSlot * D;
             constexpr int PER = (NOUT + kComputeWarps * 32 - 1) / (kComputeWarps * 32);
+            float resO[PER], resM[PER], resL[PER];
+#pragma unroll
+            for (int e0 = 0; e0 < PER; ++e0) {
+                const int e = tid + e0 * kComputeWarps * 32;
+                resO[e0] = 0.f;
+                resM[e0] = -INFINITY;
+                resL[e0] = 0.f;
+                if (e >= NOUT) continue;
+                const int h = e / D, d = e % D;
+                float M = -INFINITY;
+#pragma unroll
+                for (int w = 0; w < kComputeWarps; ++w) M = fmaxf(M, s.redm[w][h]);
+                float O = 0.f, Ls = 0.f;
+#pragma unroll
+                for (int w = 0; w < kComputeWarps; ++w) {
+                    const float wt = fast_exp2(s.redm[w][h] - M);
+                    O = fmaf(s.redO[w][h][d], wt, O);
+                    Ls = fmaf(s.redl[w][h], wt, Ls);
+                }
+                resO[e0] = O;
+                resM[e0] = M;
+                resL[e0] = Ls;
+            }
             if (qs.count == 1) {
 #pragma unroll
                 for (int e0 = 0; e0 < PER; ++e0) {
                     const int e = tid + e0 * kComputeWarps * 32;
                     if (e >= NOUT) break;
-                    const int h = e / D, d = e % D;
-                    float o = 0.f, lsum = 0.f;
-#pragma unroll
-                    for (int w = 0; w < kComputeWarps; ++w) {
-                        o += s.red[w][h][d];
-                        lsum += s.wl[w][h];
-                    }
-                    const uint32_t head = hc * 4 + h;
-                    if (head < a.G) a.out[((size_t)g * a.G + head) * D + d] = o / lsum;
+                    const uint32_t head = hc * kHeadsPerSlot + e / D;
+                    if (head < a.G) a.out[((size_t)g * a.G + head) * D + e % D] = resO[e0] / resL[e0];
                 }
             } else {
-                float* pO = a.part_O + (size_t)cur_item * 4 * D;
+                float* pO = a.part_O + (size_t)cur_item * NOUT;
 #pragma unroll
                 for (int e0 = 0; e0 < PER; ++e0) {
                     const int e = tid + e0 * kComputeWarps * 32;
                     if (e >= NOUT) break;
-                    const int h = e / D, d = e % D;
-                    float o = 0.f;
-#pragma unroll
-                    for (int w = 0; w < kComputeWarps; ++w) o += s.red[w][h][d];
-                    pO[e] = o;
+                    pO[e] = resO[e0];
+                    if (e % D == 0) {
+                        a.part_ml[(size_t)cur_item * 8 + e / D] = resM[e0];
+                        a.part_ml[(size_t)cur_item * 8 + 4 + e / D] = resL[e0];
+                    }
                 }
-                if (tid < 4) {
-                    float lsum = 0.f;
-#pragma unroll
-                    for (int w = 0; w < kComputeWarps; ++w) lsum += s.wl[w][tid];
-                    a.part_ml[(size_t)cur_item * 8 + tid] = m_run[tid];
-                    a.part_ml[(size_t)cur_item * 8 + 4 + tid] = lsum;
-                }
-                __threadfence();
                 named_bar_sync(1, kComputeWarps * 32);
                 if (tid == 0) {
+                    __threadfence();  // cumulative: publishes the CTA's partial writes
                     const uint32_t prev = atomicAdd(&a.done[cur_qslot], 1u);
                     s.flag = (prev + 1 == qs.count);
+                    if (s.flag) __threadfence();
                 }
                 named_bar_sync(1, kComputeWarps * 32);
                 if (s.flag) {
                     // last partial of this query slot: LSE combine (Alg. 2)
-                    __threadfence();
 #pragma unroll
                     for (int e0 = 0; e0 < PER; ++e0) {
                         const int e = tid + e0 * kComputeWarps * 32;
@@ -581,22 +803,22 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1) decode_kernel(Dec
                         float M = -INFINITY;
                         for (uint32_t i = 0; i < qs.count; ++i)
                             M = fmaxf(M, __ldcg(a.part_ml + (size_t)(qs.base + i) * 8 + h));
-                        float o = 0.f, lsum = 0.f;
+                        float O = 0.f, Ls = 0.f;
                         for (uint32_t i = 0; i < qs.count; ++i) {
-                            const size_t it = qs.base + i;
-                            const float wgt = fast_exp2(__ldcg(a.part_ml + it * 8 + h) - M);
-                            o = fmaf(__ldcg(a.part_O + it * 4 * D + e), wgt, o);
-                            lsum = fmaf(__ldcg(a.part_ml + it * 8 + 4 + h), wgt, lsum);
+                            const size_t iti = qs.base + i;
+                            const float wt = fast_exp2(__ldcg(a.part_ml + iti * 8 + h) - M);
+                            O = fmaf(__ldcg(a.part_O + iti * NOUT + e), wt, O);
+                            Ls = fmaf(__ldcg(a.part_ml + iti * 8 + 4 + h), wt, Ls);
                         }
-                        const uint32_t head = hc * 4 + h;
-                        if (head < a.G) a.out[((size_t)g * a.G + head) * D + (e % D)] = o / lsum;
+                        const uint32_t head = hc * kHeadsPerSlot + h;
+                        if (head < a.G) a.out[((size_t)g * a.G + head) * D + (e % D)] = O / Ls;
                     }
                     if (tid == 0) a.done[cur_qslot] = 0;
                 }
             }
             named_bar_sync(1, kComputeWarps * 32);
         }
-        if (++stage == NS) {
+        if (++stage == CF::NS) {
             stage = 0;
             phase ^= 1;
         }
@@ -604,40 +826,47 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1) decode_kernel(Dec
 }
 
 // ============================================================ launchers
-template <int D, int NS>
-static void launch_decode_t(const DecodeArgs& a, int grid, cudaStream_t st) {
-    const size_t smem = sizeof(DecodeSmem<D, NS>);
+template <int D>
+static void launch_decode_t(const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st) {
+    const size_t smem = sizeof(DecodeSmem2<D>) + 1024;
     static bool configured = false;
     if (!configured) {
-        SAAP_CUDA(cudaFuncSetAttribute(decode_kernel<D, NS>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SAAP_CUDA(cudaFuncSetAttribute(decode_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
         configured = true;
     }
-    decode_kernel<D, NS><<<grid, (kComputeWarps + 1) * 32, smem, st>>>(a);
+    decode_kernel<D><<<grid, (kComputeWarps + 1) * 32, smem, st>>>(m, a);
     SAAP_CUDA(cudaGetLastError());
 }
 
-void launch_decode(int D, const DecodeArgs& a, int grid, cudaStream_t st) {
+void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st) {
     switch (D) {
-        case 128: launch_decode_t<128, 4>(a, grid, st); break;
-        case 64: launch_decode_t<64, 6>(a, grid, st); break;
-        case 32: launch_decode_t<32, 8>(a, grid, st); break;
+        case 128: launch_decode_t<128>(m, a, grid, st); break;
+        case 64: launch_decode_t<64>(m, a, grid, st); break;
+        case 32: launch_decode_t<32>(m, a, grid, st); break;
         default: fail(SAAP_ERR_UNSUPPORTED, "decode: unsupported head dim " + std::to_string(D));
     }
+}
+
+void launch_route_score(const RouteArgs& a, uint32_t n_groups, cudaStream_t st) {
+    uint32_t threads = 32;
+    while (threads < a.slice) threads <<= 1;
+    route_score_kernel<<<dim3(n_groups, a.n_slices), threads, 0, st>>>(a);
+    SAAP_CUDA(cudaGetLastError());
 }
 
 void launch_route_plan(const PlanArgs& a, uint32_t n_groups, cudaStream_t st) {
     const bool route = a.mode == 1 || a.mode == 2;
     size_t smem = 0;
-    if (route) smem = (size_t)a.P2 * 12 + ((a.C + 31) / 32) * 4 + 16;
-    smem += (size_t)(a.probes + 8) * sizeof(Seg);
+    if (route) smem = (size_t)std::max<uint32_t>(a.P2, kPlanThreads) * 12 + ((a.C + 31) / 32) * 4 + 16;
+    smem += (size_t)(a.probes + 8) * (sizeof(Seg) + 4);
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
         SAAP_CUDA(cudaFuncSetAttribute(route_plan_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
-    route_plan_kernel<<<n_groups, 512, smem, st>>>(a);
+    route_plan_kernel<<<n_groups, kPlanThreads, smem, st>>>(a);
     SAAP_CUDA(cudaGetLastError());
 }
 
