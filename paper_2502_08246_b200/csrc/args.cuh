@@ -69,6 +69,8 @@ struct PlanArgs {
     uint16_t* gK;
     uint16_t* gV;
     uint64_t gather_cap;         // rows per group in the gather buffer
+    const float* q_attn;         // [groups][G][D] queries the attention uses (roped)
+    uint16_t* qA;                // out: [qslots][16][D] bf16 A operand (3-term split, swizzled)
     // outputs
     TileRec* tiles;
     ItemRec* items;
@@ -83,7 +85,7 @@ struct DecodeArgs {
     const ItemRec* items;
     const TileRec* tiles;
     StepCounters* ctr;
-    const float* q;
+    const uint16_t* qA;  // [qslots][16][D] prepared by route_plan_kernel
     uint32_t G;
     uint32_t n_hchunks;
     float qscale;  // log2(e)/sqrt(d): scores live in the exp2 domain

@@ -2,6 +2,7 @@
 // reference's C++ API (see include/saap_b200.h for the interface map).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -292,8 +293,13 @@ void enqueue_route_score(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
     pa.cand_i = ci;
 }
 
-constexpr uint32_t kItemTilesSparse = 2;   // 128-row tiles per work item
-constexpr uint32_t kItemTilesDense = 16;
+// 128-row tiles per work item (SAAP_ITEM_TILES / SAAP_ITEM_TILES_DENSE override, tuning only)
+uint32_t env_u32(const char* name, uint32_t dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? (uint32_t)std::max(1, std::atoi(v)) : dflt;
+}
+const uint32_t kItemTilesSparse = env_u32("SAAP_ITEM_TILES", 2);
+const uint32_t kItemTilesDense = env_u32("SAAP_ITEM_TILES_DENSE", 16);
 
 // Everything a decode step reads about its cache.
 struct DecodeSrc {
@@ -342,6 +348,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const double* c
     TileRec* tiles = (TileRec*)ensure(c, c->tiles, max_tiles * sizeof(TileRec));
     ItemRec* items = (ItemRec*)ensure(c, c->items, max_items * sizeof(ItemRec));
     QSlot* qs = (QSlot*)ensure(c, c->qslots, qslots * sizeof(QSlot));
+    uint16_t* qA = (uint16_t*)ensure(c, c->qA, qslots * 16 * D * sizeof(uint16_t));
     float* pO = (float*)ensure(c, c->part_O, max_items * kHeadsPerSlot * D * sizeof(float));
     float* pml = (float*)ensure(c, c->part_ml, max_items * 8 * sizeof(float));
     if (!stats) stats = (saap_attn_stats*)ensure(c, c->stats, n_groups * sizeof(saap_attn_stats));
@@ -386,6 +393,8 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const double* c
     pa.gK = src.gK;
     pa.gV = src.gV;
     pa.gather_cap = src.gather_cap;
+    pa.q_attn = q_roped;
+    pa.qA = qA;
     pa.tiles = tiles;
     pa.items = items;
     pa.ctr = c->counters;
@@ -408,7 +417,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const double* c
     da.items = items;
     da.tiles = tiles;
     da.ctr = c->counters;
-    da.q = q_roped;
+    da.qA = qA;
     da.G = (uint32_t)G;
     da.n_hchunks = (uint32_t)n_hchunks;
     da.qscale = (float)(1.4426950408889634 / std::sqrt((double)D));

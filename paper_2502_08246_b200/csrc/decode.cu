@@ -14,6 +14,28 @@
 
 namespace saap_b200 {
 
+// ============================================================ shared layout helpers
+// Row-major bf16 tiles are kept in smem as [half][rows][HALF bytes] with the
+// TMA swizzle (128-byte rows: chunk ^ (row & 7); 64-byte rows (d=32):
+// chunk ^ ((row >> 1) & 3)), so ldmatrix row fetches are conflict-free.
+__host__ __device__ __forceinline__ uint32_t swz_bytes(uint32_t D, uint32_t row, uint32_t chunk) {
+    const uint32_t half = 2 * D >= 128 ? 128 : 2 * D;
+    if (half == 128) return row * 128 + ((chunk ^ (row & 7)) << 4);
+    return row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4);
+}
+// byte offset of element (row, d) in a rows-tall swizzled bf16 tile
+__host__ __device__ __forceinline__ uint32_t swz_elem(uint32_t D, uint32_t rows, uint32_t row, uint32_t d) {
+    const uint32_t half = 2 * D >= 128 ? 128 : 2 * D;
+    const uint32_t per_half = half / 2;  // elements per swizzle row
+    const uint32_t h = d / per_half, dd = d % per_half;
+    return h * rows * half + swz_bytes(D, row, dd / 8) + (dd % 8) * 2;
+}
+__device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
 // ============================================================ route + plan
 struct Seg {
     uint32_t kind;  // KIND_ROWS (layer rows) or KIND_LIST (gather buffer rows)
@@ -338,25 +360,51 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         for (uint32_t e = tid; e < a.G * a.D; e += nth) a.out[(size_t)g * a.G * a.D + e] = 0.f;
         return;
     }
+    // query slots' A operands for QK^T: rows 0-3 q1, 4-7 q2, 8-11 q3 (3-term
+    // bf16 split of the f32 queries, ~fp32-exact), rows 12-15 zero
+    for (uint32_t e = tid; e < a.n_hchunks * 16 * a.D; e += nth) {
+        const uint32_t hc = e / (16 * a.D), r = (e / a.D) % 16, d = e % a.D;
+        const uint32_t head = hc * kHeadsPerSlot + (r & 3);
+        float v = 0.f;
+        if (r < 12 && head < a.G) {
+            const float x = a.q_attn[((size_t)g * a.G + head) * a.D + d];
+            const float t1 = __uint_as_float((uint32_t)f32_to_bf16_rne(x) << 16);
+            const float r1 = x - t1;
+            const float t2 = __uint_as_float((uint32_t)f32_to_bf16_rne(r1) << 16);
+            v = r < 4 ? t1 : (r < 8 ? t2 : r1 - t2);
+        }
+        uint16_t* dst = a.qA + (size_t)(g * a.n_hchunks + hc) * 16 * a.D;
+        *reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(dst) + swz_elem(a.D, 16, r, d)) =
+                f32_to_bf16_rne(v);
+    }
     for (uint32_t t = tid; t < ntiles; t += nth) a.tiles[tile0 + t].npieces = 0;
     __syncthreads();
-    // pieces: one per (segment, overlapped tile); slot order inside a tile is free
+    // pieces: one per (segment, overlapped tile); slot order inside a tile is
+    // free.  Short segments: one thread each; long ones: tiles spread over the CTA.
+    auto emit = [&](const Seg& sg, uint32_t v0, uint32_t t) {
+        const uint32_t v8 = v0 + ((sg.len + 7) & ~7u), vend = v0 + sg.len;
+        const uint32_t a0 = max(v0, t * kTileRows), b0 = min(v8, (t + 1) * kTileRows);
+        const uint32_t keys_end = min(b0, vend);
+        if (keys_end <= a0) return;
+        PieceRec pr;
+        pr.len = (keys_end - a0) | (sg.kind == KIND_LIST ? kPieceGather : 0u);
+        pr.srow = a0 - t * kTileRows;
+        pr.row = (sg.kind == KIND_LIST ? 0 : gm.row_base) + sg.start + (a0 - v0);
+        TileRec* tr = a.tiles + tile0 + t;
+        const uint32_t slot = atomicAdd(&tr->npieces, 1u);
+        tr->p[slot] = pr;
+    };
     for (uint32_t s2 = tid; s2 < nseg; s2 += nth) {
         const Seg sg = segs[s2];
-        if (sg.len == 0) continue;
-        const uint32_t v0 = vpre[s2], v8 = v0 + ((sg.len + 7) & ~7u), vend = v0 + sg.len;
-        for (uint32_t t = v0 / kTileRows; t * kTileRows < v8; ++t) {
-            const uint32_t a0 = max(v0, t * kTileRows), b0 = min(v8, (t + 1) * kTileRows);
-            const uint32_t keys_end = min(b0, vend);
-            if (keys_end <= a0) continue;
-            PieceRec pr;
-            pr.len = (keys_end - a0) | (sg.kind == KIND_LIST ? kPieceGather : 0u);
-            pr.srow = a0 - t * kTileRows;
-            pr.row = (sg.kind == KIND_LIST ? 0 : gm.row_base) + sg.start + (a0 - v0);
-            TileRec* tr = a.tiles + tile0 + t;
-            const uint32_t slot = atomicAdd(&tr->npieces, 1u);
-            tr->p[slot] = pr;
-        }
+        if (sg.len == 0 || sg.len > 4 * kTileRows) continue;
+        const uint32_t v0 = vpre[s2], v8 = v0 + ((sg.len + 7) & ~7u);
+        for (uint32_t t = v0 / kTileRows; t * kTileRows < v8; ++t) emit(sg, v0, t);
+    }
+    for (uint32_t s2 = 0; s2 < nseg; ++s2) {
+        const Seg sg = segs[s2];
+        if (sg.len <= 4 * kTileRows) continue;
+        const uint32_t v0 = vpre[s2], v8 = v0 + ((sg.len + 7) & ~7u);
+        for (uint32_t t = v0 / kTileRows + tid; t * kTileRows < v8; t += nth) emit(sg, v0, t);
     }
     for (uint32_t e = tid; e < nitems * a.n_hchunks; e += nth) {
         const uint32_t hc = e / nitems, k = e % nitems;
@@ -395,7 +443,7 @@ struct DecodeSmem2 {
     using CF = DecodeCfg<D>;
     uint8_t K[CF::NS][CF::TILE_BYTES];
     uint8_t V[CF::NS][CF::TILE_BYTES];
-    float q[CF::NS][kHeadsPerSlot][D];
+    uint16_t qA[CF::NS][16][D];  // swizzled bf16 A operand of the item's query slot
     float redO[kComputeWarps][kHeadsPerSlot][D];
     float redm[kComputeWarps][kHeadsPerSlot];
     float redl[kComputeWarps][kHeadsPerSlot];
@@ -455,8 +503,7 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
         decode_kernel(const __grid_constant__ DecodeMaps maps, DecodeArgs a) {
     using CF = DecodeCfg<D>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    auto& s = *reinterpret_cast<DecodeSmem2<D>*>(
-            (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    auto& s = *reinterpret_cast<DecodeSmem2<D>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -535,10 +582,10 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
                     s.valid[stage] = make_uint4(vm[0], vm[1], vm[2], vm[3]);
                     s.meta[stage] = make_int4((int)it, (int)(t | ((t + 1 == itm.ntiles) ? 0x80000000u : 0u)),
                                               (int)itm.qslot, (int)nq);
-                    mbar_arrive_expect_tx(&s.full[stage], bytes + (t == 0 ? nq * D * 4 : 0));
+                    mbar_arrive_expect_tx(&s.full[stage], bytes + (t == 0 ? 16 * D * 2 : 0));
                     if (t == 0)
-                        bulk_g2s(&s.q[stage][0][0], a.q + ((size_t)g * a.G + hc * kHeadsPerSlot) * D,
-                                 nq * D * 4, &s.full[stage]);
+                        bulk_g2s(&s.qA[stage][0][0], a.qA + (size_t)itm.qslot * 16 * D, 16 * D * 2,
+                                 &s.full[stage]);
                 }
                 __syncwarp();
                 if (len) {
@@ -579,6 +626,7 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
     const int hq = gid & 3;         // head of this lane's score rows
     const int row0 = warp * 16;     // this warp's 16 rows of the tile
     const int mtx = lane >> 3, r8 = lane & 7;
+    (void)gid;
 
     uint32_t qa[CF::KSTEPS][4];  // A fragments of [q1; q2; q3; 0]
     float o[CF::NT][4];
@@ -596,30 +644,16 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
             cur_item = (uint32_t)mt.x;
             cur_qslot = (uint32_t)mt.z;
             const int nq = mt.w;
-            // q -> 3-term bf16 split as A rows: q1 (rows 0-3, lanes < 16),
-            // q2 (rows 4-7, lanes >= 16), q3 (rows 8-11, lanes < 16); scaled
-            // by log2(e)/sqrt(d) after the MMA, so bf16 queries stay exact
+            // A operand [q1; q2; q3; 0] (prepared by route_plan_kernel) via ldmatrix
+            {
+                const uint32_t qbase = smem_u32(&s.qA[stage][0][0]);
+                const uint32_t qrow = (mtx & 1) * 8 + r8;
 #pragma unroll
-            for (int k = 0; k < CF::KSTEPS; ++k) {
-#pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    const int d0 = k * 16 + half * 8 + tig * 2;
-                    float x[2] = {0.f, 0.f};
-                    if (hq < nq) {
-                        x[0] = s.q[stage][hq][d0];
-                        x[1] = s.q[stage][hq][d0 + 1];
-                    }
-                    float t1[2], t2[2], t3[2];
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        t1[e] = bf16_round(x[e]);
-                        const float r1 = x[e] - t1[e];
-                        t2[e] = bf16_round(r1);
-                        t3[e] = r1 - t2[e];
-                    }
-                    // half 0 -> a0a1 (row g) / a2a3 (row g+8); half 1 -> a4a5 / a6a7
-                    qa[k][2 * half] = upper ? pack_bf16(t2[0], t2[1]) : pack_bf16(t1[0], t1[1]);
-                    qa[k][2 * half + 1] = upper ? 0u : pack_bf16(t3[0], t3[1]);
+                for (int k = 0; k < CF::KSTEPS; ++k) {
+                    const uint32_t chunk = 2 * k + (mtx >> 1);
+                    const uint32_t h = chunk / (CF::HALF / 16), cc = chunk % (CF::HALF / 16);
+                    ldsm_x4(qbase + h * 16 * CF::HALF + swz<D>(qrow, cc), qa[k][0], qa[k][1],
+                            qa[k][2], qa[k][3]);
                 }
             }
 #pragma unroll
@@ -678,22 +712,18 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
             // lanes >= 16 carry p2 (rows g+4) and zeros (rows g+12)
             uint32_t pa0, pa1, pa2, pa3;
             {
-                float t1[4], t2[4], t3[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    t1[i] = bf16_round(p[i]);
-                    const float r1 = p[i] - t1[i];
-                    t2[i] = bf16_round(r1);
-                    t3[i] = r1 - t2[i];
-                }
+                const uint32_t h01 = bf16x2_rn(p[0], p[1]), h23 = bf16x2_rn(p[2], p[3]);
+                const float r0 = p[0] - bf16lo(h01), r1 = p[1] - bf16hi(h01);
+                const float r2 = p[2] - bf16lo(h23), r3 = p[3] - bf16hi(h23);
+                const uint32_t m01 = bf16x2_rn(r0, r1), m23 = bf16x2_rn(r2, r3);
                 if (!upper) {
-                    pa0 = pack_bf16(t1[0], t1[1]);
-                    pa2 = pack_bf16(t1[2], t1[3]);
-                    pa1 = pack_bf16(t3[0], t3[1]);
-                    pa3 = pack_bf16(t3[2], t3[3]);
+                    pa0 = h01;
+                    pa2 = h23;
+                    pa1 = bf16x2_rn(r0 - bf16lo(m01), r1 - bf16hi(m01));
+                    pa3 = bf16x2_rn(r2 - bf16lo(m23), r3 - bf16hi(m23));
                 } else {
-                    pa0 = pack_bf16(t2[0], t2[1]);
-                    pa2 = pack_bf16(t2[2], t2[3]);
+                    pa0 = m01;
+                    pa2 = m23;
                     pa1 = 0u;
                     pa3 = 0u;
                 }
