@@ -298,6 +298,24 @@ def ours(a):
         kv = sb.KVCache(ctx, n_groups, d, K, V, [gi * N for gi in range(n_groups)], [N] * n_groups)
         layers.append(dict(L=L, K=K, V=V, routers=routers, parts=parts_h, kv=kv, cents=cents))
 
+    peak_early, _ = measured_peaks()
+    # ---- prefill (C4-style): rebuild layer 0 with device timing per phase
+    ctx.enable_timing(True)
+    pre_a, pre_p = [], []
+    lay0 = layers[0]
+    parts0 = [lay0["parts"][gi % heads_local] for gi in range(n_groups)]
+    for _ in range(3):
+        lay0["L"].build_dev(parts0, lay0["K"], lay0["V"], lay0["K"])
+        ta, tp = lay0["L"].build_timing()
+        pre_a.append(ta)
+        pre_p.append(tp)
+    ctx.timing()  # clear decode records
+    ctx.enable_timing(False)
+    used_tc, refined = lay0["L"].assign_info()
+    n_keys_prefill = n_groups * (N - a.sink)
+    assign_ms, pack_ms = float(np.median(pre_a)), float(np.median(pre_p))
+    pack_bytes = n_keys_prefill * (8 * d + 16)
+
     # ---- queries: each group's 4 heads look for one cluster of its KV head
     gq = torch.Generator(device=dev)
     gq.manual_seed(4242 + rank)
@@ -481,6 +499,16 @@ def ours(a):
         "clocks": clk,
         "gpu_launches": 2 * a.steps,
         "prefill_build_ms_per_layer": round(float(np.mean(t_build)), 2),
+        "prefill": {
+            "keys": n_keys_prefill, "assign_ms": round(assign_ms, 3), "pack_ms": round(pack_ms, 3),
+            "keys_per_s": round(n_keys_prefill / ((assign_ms + pack_ms) * 1e-3), 1),
+            "assign_engine": "tcgen05" if used_tc else "fp64", "refined_keys": refined,
+            "assign_tflops": round(2 * n_keys_prefill * C * d / (assign_ms * 1e-3) / 1e12, 1),
+            "assign_frac_of_bf16_sustained": round(2 * n_keys_prefill * C * d / (assign_ms * 1e-3) / 1e12
+                                                   / 1389.8, 4),
+            "pack_gbs": round(pack_bytes / (pack_ms * 1e-3) / 1e9, 1),
+            "pack_frac": round(pack_bytes / (pack_ms * 1e-3) / 1e9 / peak_early, 4),
+        },
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -159,6 +159,11 @@ SAAP_API int saap_ctx_set_assign_mode(saap_ctx* ctx, int mode);
 SAAP_API int saap_layer_assign_info(saap_ctx* ctx, const saap_layer* L, int* used_tensor_cores,
                                     uint64_t* refined_keys);
 
+/* Device time of the last build issued while context timing was enabled:
+ * assignment (incl. fp64 re-check) and packing (histogram/scan/scatter). */
+SAAP_API int saap_layer_build_timing(saap_ctx* ctx, const saap_layer* L, double* assign_ms,
+                                     double* pack_ms);
+
 /* Read back ContextStore.assignment / index for group g (host). */
 SAAP_API int saap_layer_read_index(saap_ctx* ctx, const saap_layer* L, uint64_t group,
                           uint32_t* assignment, uint64_t* off, uint64_t* idx);

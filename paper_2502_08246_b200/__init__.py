@@ -440,6 +440,12 @@ class Layer:
         _check(lib().saap_layer_assign_info(self.ctx.h, self.h, C.byref(u), C.byref(n)))
         return bool(u.value), n.value
 
+    def build_timing(self):
+        """(assign_ms, pack_ms) of the last build issued with ctx timing enabled."""
+        a, b = C.c_double(), C.c_double()
+        _check(lib().saap_layer_build_timing(self.ctx.h, self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def read_index(self, group: int):
         n = int(self.n_keys[group]) - self.sink
         a = np.empty(n, np.uint32)

@@ -28,7 +28,7 @@ constexpr uint32_t kPieceGather = 0x80000000u;
 // keeps its top-min(l, slice) (score, id) pairs in reference order.
 struct RouteArgs {
     int mode;                      // 1 centroid, 2 precomputed Q-model probabilities
-    const double* const* cent64T;  // per group, d x C fp64
+    const float* const* centT;     // per group, d x C f32 (exact in fp64)
     const float* q_route;          // [groups][G][D]
     const double* scores;          // [groups][G][C]
     uint32_t G, D, C, probes;
@@ -52,7 +52,6 @@ struct PlanArgs {
     const uint32_t* invA;
     uint32_t C;
     int mode;                    // 0 dense, 1 centroid, 2 precomputed scores, 3 window only
-    const double* const* cent64T;  // per group, d x C fp64 (mode 1)
     const float* q_route;        // [groups][G][D]
     const double* scores;        // [groups][G][C] per-row probabilities (mode 2)
     uint32_t G, D, n_hchunks;

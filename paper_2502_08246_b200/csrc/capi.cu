@@ -214,9 +214,9 @@ void bind_routers(saap_layer* L, const saap_router* const* routers, int& mode, i
     if (rs == L->cached_routers) return;
     if (L->ctx->capturing) invalid("router set changed during graph capture");
     if (kind == 0) {
-        std::vector<const double*> p(L->n_groups);
-        for (size_t g = 0; g < p.size(); ++g) p[g] = rs[g]->part->cent64T;
-        if (!L->d_centT) L->d_centT = (const double**)(dmalloc<void*>(L->n_groups));
+        std::vector<const float*> p(L->n_groups);
+        for (size_t g = 0; g < p.size(); ++g) p[g] = rs[g]->part->centT;
+        if (!L->d_centT) L->d_centT = (const float**)(dmalloc<void*>(L->n_groups));
         SAAP_CUDA(cudaMemcpy(L->d_centT, p.data(), p.size() * sizeof(void*), cudaMemcpyHostToDevice));
     } else {
         std::vector<const double*> p(3 * L->n_groups);
@@ -256,7 +256,7 @@ struct RouteGeo {
 };
 RouteGeo route_geo(uint64_t C, uint64_t probes) {
     RouteGeo r;
-    r.slice = C <= 256 ? (uint32_t)C : (C <= 4096 ? 256u : 1024u);
+    r.slice = C <= 256 ? (uint32_t)C : 256u;  // slab = D x slice f32 in shared memory
     r.n_slices = (uint32_t)((C + r.slice - 1) / r.slice);
     r.keep = (uint32_t)std::min<uint64_t>(probes, r.slice);
     r.n_cand = r.n_slices * r.keep;
@@ -266,14 +266,14 @@ RouteGeo route_geo(uint64_t C, uint64_t probes) {
 
 // stage-1 routing launch for n groups (mode 1 centroid / 2 Q-model scores)
 void enqueue_route_score(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C, uint64_t G,
-                         uint64_t probes, int mode, const double* const* cent64T,
+                         uint64_t probes, int mode, const float* const* centT,
                          const float* q_route, const double* probs, PlanArgs& pa) {
     const RouteGeo geo = route_geo(C, probes);
     double* cs = (double*)ensure(c, c->cand_s, n_groups * geo.n_cand * sizeof(double));
     uint32_t* ci = (uint32_t*)ensure(c, c->cand_i, n_groups * geo.n_cand * sizeof(uint32_t));
     RouteArgs ra{};
     ra.mode = mode;
-    ra.cent64T = cent64T;
+    ra.centT = centT;
     ra.q_route = q_route;
     ra.scores = probs;
     ra.G = (uint32_t)G;
@@ -298,7 +298,7 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
     const char* v = std::getenv(name);
     return v && *v ? (uint32_t)std::max(1, std::atoi(v)) : dflt;
 }
-const uint32_t kItemTilesSparse = env_u32("SAAP_ITEM_TILES", 2);
+const uint32_t kItemTilesSparse = env_u32("SAAP_ITEM_TILES", 4);
 const uint32_t kItemTilesDense = env_u32("SAAP_ITEM_TILES_DENSE", 16);
 
 // Everything a decode step reads about its cache.
@@ -332,7 +332,7 @@ DecodeMaps* build_maps(const void* K, const void* V, uint64_t rows, uint32_t D, 
 
 // Enqueue one decode step (routing, planning, attention, combine) on the
 // context stream.  mode: 0 dense/full, 1 centroid, 2 Q-model, 3 window only.
-void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const double* const* cent64T,
+void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const float* const* centT,
                     const double* const* qm, const float* q_roped, const float* q_route,
                     uint64_t G, uint64_t probes, uint64_t recent, float* out,
                     saap_attn_stats* stats, uint32_t* selected, uint32_t item_tiles,
@@ -378,7 +378,6 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const double* c
     pa.invA = src.invA;
     pa.C = (uint32_t)C;
     pa.mode = mode;
-    pa.cent64T = cent64T;
     pa.q_route = q_route;
     pa.scores = probs;
     pa.G = (uint32_t)G;
@@ -408,7 +407,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const double* c
         SAAP_CUDA(cudaEventRecord(e0, st));
     }
     if ((mode == 1 || mode == 2) && probes > 0)
-        enqueue_route_score(c, n_groups, D, C, G, probes, mode, cent64T, q_route, probs, pa);
+        enqueue_route_score(c, n_groups, D, C, G, probes, mode, centT, q_route, probs, pa);
     launch_route_plan(pa, (uint32_t)n_groups, st);
     c->launches++;
     if (e1) SAAP_CUDA(cudaEventRecord(e1, st));
@@ -622,18 +621,18 @@ int saap_partition_create(saap_ctx* c, const float* cent, uint64_t C, uint64_t d
         p->C = C;
         p->d = d;
         p->host.assign(cent, cent + C * d);
-        std::vector<double> t(C * d);
+        std::vector<float> t(C * d);
         std::vector<double> d64(C * d);
         for (uint64_t i = 0; i < C; ++i)
             for (uint64_t j = 0; j < d; ++j) {
-                t[j * C + i] = (double)cent[i * d + j];
+                t[j * C + i] = cent[i * d + j];
                 d64[i * d + j] = (double)cent[i * d + j];
             }
         p->cent = dmalloc<float>(C * d);
-        p->cent64T = dmalloc<double>(C * d);
+        p->centT = dmalloc<float>(C * d);
         p->cent64 = dmalloc<double>(C * d);
         SAAP_CUDA(cudaMemcpy(p->cent, cent, C * d * 4, cudaMemcpyHostToDevice));
-        SAAP_CUDA(cudaMemcpy(p->cent64T, t.data(), C * d * 8, cudaMemcpyHostToDevice));
+        SAAP_CUDA(cudaMemcpy(p->centT, t.data(), C * d * 4, cudaMemcpyHostToDevice));
         SAAP_CUDA(cudaMemcpy(p->cent64, d64.data(), C * d * 8, cudaMemcpyHostToDevice));
         *out = p;
     });
@@ -644,7 +643,7 @@ int saap_partition_destroy(saap_partition* p) {
         if (!p) return;
         cudaSetDevice(p->ctx->device);
         dfree(p->cent);
-        dfree(p->cent64T);
+        dfree(p->centT);
         dfree(p->cent64);
         delete p;
     });
@@ -734,7 +733,7 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
     int mode;
     double* probs = nullptr;
     if (r->kind == 0) {
-        ptrs[0] = (void*)r->part->cent64T;
+        ptrs[0] = (void*)r->part->centT;
         mode = 1;
     } else {
         ptrs[0] = (void*)r->model->w1;
@@ -761,7 +760,6 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
     pa.meta = dmeta;
     pa.C = (uint32_t)C;
     pa.mode = mode;
-    pa.cent64T = (const double* const*)dptr;
     pa.q_route = dq;
     pa.scores = probs;
     pa.G = (uint32_t)G;
@@ -772,7 +770,7 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
     pa.item_tiles = kItemTilesSparse;
     pa.route_only = 1;
     pa.selected = dsel;
-    enqueue_route_score(c, 1, d, C, G, l, mode, (const double* const*)dptr, dq, probs, pa);
+    enqueue_route_score(c, 1, d, C, G, l, mode, (const float* const*)dptr, dq, probs, pa);
     launch_route_plan(pa, 1, st);
     c->launches++;
     d2h(out, dsel, l * 4, st);
@@ -1008,6 +1006,8 @@ int saap_layer_destroy(saap_layer* L) {
         dfree(L->tile_first);
         dfree(L->hist);
         dfree(L->countA);
+        for (auto e : L->bev)
+            if (e) cudaEventDestroy(e);
         dfree(L->d_cent64);
         dfree(L->key_row0);
         dfree(L->ivf_base);
@@ -1044,50 +1044,56 @@ static void bind_parts(saap_layer* L, const saap_partition* const* parts) {
 static void assign_tc_path(saap_layer* L, const uint16_t* keys) {
     saap_ctx* c = L->ctx;
     const cudaStream_t st = c->stream;
-    // distinct partitions -> slots of the concatenated (hi, mid) split arrays
-    std::vector<const saap_partition*> slots;
-    std::vector<uint32_t> slot_of(L->n_groups);
-    for (uint64_t g = 0; g < L->n_groups; ++g) {
-        auto it = std::find(slots.begin(), slots.end(), L->parts[g]);
-        slot_of[g] = (uint32_t)(it - slots.begin());
-        if (it == slots.end()) slots.push_back(L->parts[g]);
-    }
     const uint32_t Cpad = tc_cpad((uint32_t)L->C);
-    const size_t elems = slots.size() * (size_t)Cpad * L->d;
-    if (elems > L->tc_split_elems) {
-        dfree(L->tc_hi);
-        dfree(L->tc_mid);
-        L->tc_hi = dmalloc<uint16_t>(elems);
-        L->tc_mid = dmalloc<uint16_t>(elems);
-        L->tc_split_elems = elems;
-    }
-    std::vector<float> cmax(slots.size());
-    for (size_t i = 0; i < slots.size(); ++i) {
-        launch_split_centroids(slots[i]->cent, (uint32_t)L->C, (uint32_t)L->d,
-                               L->tc_hi + i * (size_t)Cpad * L->d, L->tc_mid + i * (size_t)Cpad * L->d, st);
-        c->launches++;
-        double m = 0;
-        for (uint64_t r = 0; r < L->C; ++r) {
-            double n2 = 0;
-            for (uint64_t j = 0; j < L->d; ++j) {
-                const double v = slots[i]->host[r * L->d + j];
-                n2 += v * v;
-            }
-            m = std::max(m, std::sqrt(n2));
+    if (L->tc_parts != L->parts) {
+        // distinct partitions -> slots of the concatenated (hi, mid) split arrays
+        std::vector<const saap_partition*> slots;
+        std::vector<uint32_t> slot_of(L->n_groups);
+        for (uint64_t g = 0; g < L->n_groups; ++g) {
+            auto it = std::find(slots.begin(), slots.end(), L->parts[g]);
+            slot_of[g] = (uint32_t)(it - slots.begin());
+            if (it == slots.end()) slots.push_back(L->parts[g]);
         }
-        cmax[i] = (float)(m * (1 + 1e-6));
+        const size_t elems = slots.size() * (size_t)Cpad * L->d;
+        if (elems > L->tc_split_elems) {
+            dfree(L->tc_hi);
+            dfree(L->tc_mid);
+            L->tc_hi = dmalloc<uint16_t>(elems);
+            L->tc_mid = dmalloc<uint16_t>(elems);
+            L->tc_split_elems = elems;
+        }
+        std::vector<float> cmax(slots.size());
+        for (size_t i = 0; i < slots.size(); ++i) {
+            launch_split_centroids(slots[i]->cent, (uint32_t)L->C, (uint32_t)L->d,
+                                   L->tc_hi + i * (size_t)Cpad * L->d,
+                                   L->tc_mid + i * (size_t)Cpad * L->d, st);
+            c->launches++;
+            double m = 0;
+            for (uint64_t r = 0; r < L->C; ++r) {
+                double n2 = 0;
+                for (uint64_t j = 0; j < L->d; ++j) {
+                    const double v = slots[i]->host[r * L->d + j];
+                    n2 += v * v;
+                }
+                m = std::max(m, std::sqrt(n2));
+            }
+            cmax[i] = (float)(m * (1 + 1e-6));
+        }
+        std::vector<TcTile> tiles;
+        build_tc_tiles(L->h_meta, slot_of, tiles);
+        dfree(L->tc_cmax);
+        L->tc_cmax = dmalloc<float>(slots.size());
+        SAAP_CUDA(cudaMemcpy(L->tc_cmax, cmax.data(), cmax.size() * 4, cudaMemcpyHostToDevice));
+        if (L->tc_n_tiles != tiles.size()) {
+            if (L->tc_tiles) cudaFree(L->tc_tiles);
+            L->tc_tiles = dmalloc<TcTile>(tiles.size());
+            L->tc_n_tiles = (uint32_t)tiles.size();
+        }
+        SAAP_CUDA(cudaMemcpy(L->tc_tiles, tiles.data(), tiles.size() * sizeof(TcTile),
+                             cudaMemcpyHostToDevice));
+        L->tc_parts = L->parts;
+        L->tc_nslots = (uint32_t)slots.size();
     }
-    std::vector<TcTile> tiles;
-    build_tc_tiles(L->h_meta, slot_of, tiles);
-    dfree(L->tc_cmax);
-    L->tc_cmax = dmalloc<float>(slots.size());
-    SAAP_CUDA(cudaMemcpy(L->tc_cmax, cmax.data(), cmax.size() * 4, cudaMemcpyHostToDevice));
-    if (L->tc_n_tiles != tiles.size()) {
-        if (L->tc_tiles) cudaFree(L->tc_tiles);
-        L->tc_tiles = dmalloc<TcTile>(tiles.size());
-        L->tc_n_tiles = (uint32_t)tiles.size();
-    }
-    SAAP_CUDA(cudaMemcpy(L->tc_tiles, tiles.data(), tiles.size() * sizeof(TcTile), cudaMemcpyHostToDevice));
     if (!L->tc_refine) {
         L->tc_refine = dmalloc<uint32_t>(2 * L->total_ns);
         L->tc_refine_count = dmalloc<uint32_t>(1);
@@ -1104,8 +1110,8 @@ static void assign_tc_path(saap_layer* L, const uint16_t* keys) {
     args.refine = L->tc_refine;
     args.refine_count = L->tc_refine_count;
     args.keys = keys;
-    launch_assign_tc(keys, L->total_rows, L->tc_hi, L->tc_mid, (uint32_t)slots.size(), args,
-                     (uint32_t)tiles.size(), st);
+    launch_assign_tc(keys, L->total_rows, L->tc_hi, L->tc_mid, L->tc_nslots, args, L->tc_n_tiles,
+                     st);
     launch_refine(L->tc_refine, L->tc_refine_count, keys, L->key_row0, L->d_cent64, L->ivf_base,
                   (uint32_t)L->C, L->assign, c->sm_count, st);
     c->launches += 2;
@@ -1117,6 +1123,12 @@ static void build_from_device(saap_layer* L, const uint16_t* Ksrc, const uint16_
     saap_ctx* c = L->ctx;
     const cudaStream_t st = c->stream;
     L->last_tc = false;
+    const bool timed = c->timing && !c->capturing;
+    if (timed) {
+        for (auto& e : L->bev)
+            if (!e) SAAP_CUDA(cudaEventCreate(&e));
+        SAAP_CUDA(cudaEventRecord(L->bev[0], st));
+    }
     if (assign_bf16 && L->d == 128 && c->assign_mode == 0) {
         assign_tc_path(L, (const uint16_t*)keys_assign);
     } else {
@@ -1124,10 +1136,12 @@ static void build_from_device(saap_layer* L, const uint16_t* Ksrc, const uint16_
                             L->d_cent64, (uint32_t)L->C, L->assign, L->ivf_base, st);
         c->launches++;
     }
+    if (timed) SAAP_CUDA(cudaEventRecord(L->bev[1], st));
     launch_pack((int)L->d, L->tiles, L->n_tiles, L->tile_first, (uint32_t)L->n_groups, L->meta,
                 L->assign, (uint32_t)L->C, L->hist, L->countA, L->off, L->offA, L->idx, L->invA,
                 Ksrc, Vsrc, L->row_base, L->K, L->V, st);
     c->launches += 5;
+    if (timed) SAAP_CUDA(cudaEventRecord(L->bev[2], st));
     L->built = true;
 }
 
@@ -1205,6 +1219,20 @@ int saap_ctx_set_assign_mode(saap_ctx* c, int mode) {
         need(c, "ctx");
         if (mode != 0 && mode != 1) invalid("assign mode must be 0 (tensor cores) or 1 (exact fp64)");
         c->assign_mode = mode;
+    });
+}
+
+int saap_layer_build_timing(saap_ctx* c, const saap_layer* L, double* assign_ms, double* pack_ms) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(L, "layer");
+        if (!L->bev[2]) invalid("no timed build: enable timing before saap_layer_build_dev");
+        sync(c);
+        float a = 0, b = 0;
+        SAAP_CUDA(cudaEventElapsedTime(&a, L->bev[0], L->bev[1]));
+        SAAP_CUDA(cudaEventElapsedTime(&b, L->bev[1], L->bev[2]));
+        if (assign_ms) *assign_ms = a;
+        if (pack_ms) *pack_ms = b;
     });
 }
 

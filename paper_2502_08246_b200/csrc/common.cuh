@@ -168,7 +168,7 @@ struct saap_partition {
     uint64_t C = 0, d = 0;
     float* cent = nullptr;     // C x d f32 (device)
     double* cent64 = nullptr;  // C x d fp64 (device, exact assignment)
-    double* cent64T = nullptr; // d x C fp64 (device, routing: coalesced, no converts)
+    float* centT = nullptr;    // d x C f32 (device, routing slabs; exact in fp64)
     std::vector<float> host;   // kept for validation / read-back
 };
 
@@ -223,9 +223,12 @@ struct saap_layer {
     uint64_t* ivf_base = nullptr;    // per group
     uint64_t last_refined = 0;
     bool last_tc = false;
+    std::vector<const saap_partition*> tc_parts;  // partitions the tc resources were built for
+    uint32_t tc_nslots = 0;
+    cudaEvent_t bev[3] = {nullptr, nullptr, nullptr};  // last build: start, after assign, after pack
     // routing parameter table cache (device arrays of per-group pointers)
     std::vector<const saap_router*> cached_routers;
-    const double** d_centT = nullptr;  // per group cent64T
+    const float** d_centT = nullptr;   // per group centT
     const double** d_qm = nullptr;     // per group: w1, w2, vec (3 pointers)
     // decode: TMA maps over the packed cache (+ gather buffer), built lazily
     void* maps = nullptr;              // DecodeMaps (host copy)

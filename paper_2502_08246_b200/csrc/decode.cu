@@ -108,13 +108,36 @@ __device__ void bitonic_smem(double* ss, uint32_t* si, uint32_t n) {
 }
 
 // Stage 1: score a slice of centroids (one thread per centroid) and keep the
-// slice's top-`keep` in reference order.
+// slice's top-`keep` in reference order.  The slice's transposed f32
+// centroids [D x slice] are staged in shared memory by bulk copies, so the
+// sequential fp64 chains read shared memory, not L2.
 __global__ void __launch_bounds__(kSliceMax) route_score_kernel(RouteArgs a) {
+    extern __shared__ __align__(16) float slab[];  // [D][slice]
     __shared__ double pooled[128];
     __shared__ double xs[kSliceMax];
     __shared__ uint32_t xi[kSliceMax];
+    __shared__ __align__(8) uint64_t bar;
     const uint32_t g = blockIdx.x, sl = blockIdx.y, tid = threadIdx.x;
+    const uint32_t c0 = sl * a.slice, nsl = min(a.slice, a.C - c0);
     if (a.mode == 1) {
+        const float* cT = a.centT[g];
+        const bool bulk = (a.C % 4 == 0) && (c0 % 4 == 0) && (nsl % 4 == 0) && (a.slice % 4 == 0);
+        if (bulk) {
+            if (tid == 0) {
+                mbar_init(&bar, 1);
+                fence_mbar_init();
+            }
+            __syncthreads();
+            if (tid == 0) mbar_arrive_expect_tx(&bar, a.D * nsl * 4);
+            __syncthreads();
+            for (uint32_t j = tid; j < a.D; j += blockDim.x)
+                bulk_g2s(slab + j * a.slice, cT + (size_t)j * a.C + c0, nsl * 4, &bar);
+        } else {
+            for (uint32_t e = tid; e < a.D * nsl; e += blockDim.x) {
+                const uint32_t j = e / nsl, c = e % nsl;
+                slab[j * a.slice + c] = cT[(size_t)j * a.C + c0 + c];
+            }
+        }
         // pooled_j = sum_i q_ij (fp64, rows in order)   attention.cpp:289-295
         const float* q = a.q_route + (size_t)g * a.G * a.D;
         for (uint32_t j = tid; j < a.D; j += blockDim.x) {
@@ -122,19 +145,19 @@ __global__ void __launch_bounds__(kSliceMax) route_score_kernel(RouteArgs a) {
             for (uint32_t i = 0; i < a.G; ++i) s = __dadd_rn(s, (double)q[(size_t)i * a.D + j]);
             pooled[j] = s;
         }
+        if (bulk) mbar_wait(&bar, 0);
         __syncthreads();
     }
-    const uint32_t c = sl * a.slice + tid;
     double sc = -INFINITY;
     uint32_t id = 0xFFFFFFFFu;
-    if (tid < a.slice && c < a.C) {
+    if (tid < nsl) {
+        const uint32_t c = c0 + tid;
         double s = 0.0;
         if (a.mode == 1) {
             // s_c = sum_j pooled_j * c_cj, mul rounded before add  attention.cpp:296-304
-            const double* cT = a.cent64T[g];
-#pragma unroll 16
+#pragma unroll 8
             for (uint32_t j = 0; j < a.D; ++j)
-                s = __dadd_rn(s, __dmul_rn(pooled[j], cT[(size_t)j * a.C + c]));
+                s = __dadd_rn(s, __dmul_rn(pooled[j], (double)slab[j * a.slice + tid]));
         } else {
             // Q-model: score_c = sum_i p_ic over the group rows   qmodel.cpp:493-499
             const double* p = a.scores + (size_t)g * a.G * a.C;
@@ -531,10 +554,27 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
             asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.v8) : "memory");
         }
         uint32_t stage = 0, phase = 0;
-        uint32_t it = 0;
+        // software-pipelined: the next tile's records are loaded before this
+        // tile waits for a free ring slot
+        auto fetch_item = [&](uint32_t id) {
+            ItemRec r{0, 0, 0, 0};
+            if (id < n_items) r = a.items[id];
+            return r;
+        };
+        uint32_t it = 0, next_it = 0;
         if (lane == 0) it = atomicAdd(&a.ctr->work, 1u);
+        it = __shfl_sync(0xFFFFFFFFu, it, 0);
+        ItemRec itm = fetch_item(it);
+        if (lane == 0) next_it = atomicAdd(&a.ctr->work, 1u);
+        uint32_t t = 0;
+        uint32_t np = 0;
+        PieceRec pr{0, 0, 0};
+        if (it < n_items) {
+            const TileRec* tr = a.tiles + itm.tile_first;
+            np = tr->npieces;
+            if (lane < kMaxPieces) pr = tr->p[lane];
+        }
         for (;;) {
-            it = __shfl_sync(0xFFFFFFFFu, it, 0);
             if (it >= n_items) {
                 if (lane == 0) {
                     mbar_wait(&s.empty[stage], phase ^ 1);
@@ -543,79 +583,91 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
                 }
                 break;
             }
-            const ItemRec itm = a.items[it];
-            uint32_t next = 0;
-            if (lane == 0) next = atomicAdd(&a.ctr->work, 1u);  // prefetch the next item id
-            const uint32_t g = itm.qslot / a.n_hchunks, hc = itm.qslot % a.n_hchunks;
-            const uint32_t nq = min((uint32_t)kHeadsPerSlot, a.G - hc * kHeadsPerSlot);
-            for (uint32_t t = 0; t < itm.ntiles; ++t) {
-                // lane p owns piece p of the tile: boxes, bytes and validity bits
-                const TileRec* tr = a.tiles + itm.tile_first + t;
-                const uint32_t np = tr->npieces;
-                uint32_t len = 0, srow = 0, gat = 0;
-                uint64_t row = 0;
-                if ((uint32_t)lane < np) {
-                    const PieceRec pr = tr->p[lane];
-                    len = pr.len & ~kPieceGather;
-                    gat = pr.len & kPieceGather;
-                    srow = pr.srow;
-                    row = pr.row;
-                }
-                const uint32_t r8 = (len + 7) & ~7u;
-                uint32_t bytes = r8 * CF::RB * 2;
-                uint32_t vm[4];
+            // ---- prefetch the successor tile
+            const bool last_tile = t + 1 == itm.ntiles;
+            uint32_t it2 = it, t2 = t + 1;
+            ItemRec itm2 = itm;
+            if (last_tile) {
+                it2 = __shfl_sync(0xFFFFFFFFu, next_it, 0);
+                itm2 = fetch_item(it2);
+                t2 = 0;
+            }
+            uint32_t np2 = 0;
+            PieceRec pr2{0, 0, 0};
+            if (it2 < n_items) {
+                const TileRec* tr2 = a.tiles + itm2.tile_first + t2;
+                np2 = tr2->npieces;
+                if (lane < kMaxPieces) pr2 = tr2->p[lane];
+            }
+            // ---- issue this tile: lane p owns piece p
+            uint32_t len = 0, srow = 0, gat = 0;
+            uint64_t row = 0;
+            if ((uint32_t)lane < np) {
+                len = pr.len & ~kPieceGather;
+                gat = pr.len & kPieceGather;
+                srow = pr.srow;
+                row = pr.row;
+            }
+            const uint32_t r8 = (len + 7) & ~7u;
+            uint32_t bytes = r8 * CF::RB * 2;
+            uint32_t vm[4];
 #pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                    const uint32_t lo = max(srow, (uint32_t)w * 32), hi = min(srow + len, (uint32_t)w * 32 + 32);
-                    uint32_t m = 0;
-                    if (hi > lo) m = (hi - lo == 32 ? 0xFFFFFFFFu : ((1u << (hi - lo)) - 1u)) << (lo - w * 32);
-                    vm[w] = m;
-                }
+            for (int w = 0; w < 4; ++w) {
+                const uint32_t lo = max(srow, (uint32_t)w * 32), hi = min(srow + len, (uint32_t)w * 32 + 32);
+                uint32_t m = 0;
+                if (hi > lo) m = (hi - lo == 32 ? 0xFFFFFFFFu : ((1u << (hi - lo)) - 1u)) << (lo - w * 32);
+                vm[w] = m;
+            }
 #pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    bytes += __shfl_xor_sync(0xFFFFFFFFu, bytes, o);
+            for (int o = 16; o; o >>= 1) {
+                bytes += __shfl_xor_sync(0xFFFFFFFFu, bytes, o);
 #pragma unroll
-                    for (int w = 0; w < 4; ++w) vm[w] |= __shfl_xor_sync(0xFFFFFFFFu, vm[w], o);
-                }
-                if (lane == 0) {
-                    mbar_wait(&s.empty[stage], phase ^ 1);
-                    s.valid[stage] = make_uint4(vm[0], vm[1], vm[2], vm[3]);
-                    s.meta[stage] = make_int4((int)it, (int)(t | ((t + 1 == itm.ntiles) ? 0x80000000u : 0u)),
-                                              (int)itm.qslot, (int)nq);
-                    mbar_arrive_expect_tx(&s.full[stage], bytes + (t == 0 ? 16 * D * 2 : 0));
-                    if (t == 0)
-                        bulk_g2s(&s.qA[stage][0][0], a.qA + (size_t)itm.qslot * 16 * D, 16 * D * 2,
-                                 &s.full[stage]);
-                }
-                __syncwarp();
-                if (len) {
-                    const CUtensorMap* mk64 = gat ? &maps.gk64 : &maps.k64;
-                    const CUtensorMap* mk8 = gat ? &maps.gk8 : &maps.k8;
-                    const CUtensorMap* mv64 = gat ? &maps.gv64 : &maps.v64;
-                    const CUtensorMap* mv8 = gat ? &maps.gv8 : &maps.v8;
-                    uint32_t rem = r8, sr = srow;
-                    int y = (int)row;
-                    while (rem) {
-                        const bool big = rem >= 64;
+                for (int w = 0; w < 4; ++w) vm[w] |= __shfl_xor_sync(0xFFFFFFFFu, vm[w], o);
+            }
+            if (lane == 0) {
+                mbar_wait(&s.empty[stage], phase ^ 1);
+                s.valid[stage] = make_uint4(vm[0], vm[1], vm[2], vm[3]);
+                s.meta[stage] = make_int4((int)it, (int)(t | (last_tile ? 0x80000000u : 0u)),
+                                          (int)itm.qslot, 0);
+                mbar_arrive_expect_tx(&s.full[stage], bytes + (t == 0 ? 16 * D * 2 : 0));
+                if (t == 0)
+                    bulk_g2s(&s.qA[stage][0][0], a.qA + (size_t)itm.qslot * 16 * D, 16 * D * 2,
+                             &s.full[stage]);
+            }
+            __syncwarp();
+            if (len) {
+                const CUtensorMap* mk64 = gat ? &maps.gk64 : &maps.k64;
+                const CUtensorMap* mk8 = gat ? &maps.gk8 : &maps.k8;
+                const CUtensorMap* mv64 = gat ? &maps.gv64 : &maps.v64;
+                const CUtensorMap* mv8 = gat ? &maps.gv8 : &maps.v8;
+                uint32_t rem = r8, sr = srow;
+                int y = (int)row;
+                while (rem) {
+                    const bool big = rem >= 64;
 #pragma unroll
-                        for (int h = 0; h < CF::HALVES; ++h) {
-                            const uint32_t off = h * kTileRows * CF::HALF + sr * CF::HALF;
-                            tma2d(&s.K[stage][off], big ? mk64 : mk8, h * (CF::HALF / 2), y, &s.full[stage]);
-                            tma2d(&s.V[stage][off], big ? mv64 : mv8, h * (CF::HALF / 2), y, &s.full[stage]);
-                        }
-                        const uint32_t step = big ? 64 : 8;
-                        rem -= step;
-                        sr += step;
-                        y += (int)step;
+                    for (int h = 0; h < CF::HALVES; ++h) {
+                        const uint32_t off = h * kTileRows * CF::HALF + sr * CF::HALF;
+                        tma2d(&s.K[stage][off], big ? mk64 : mk8, h * (CF::HALF / 2), y, &s.full[stage]);
+                        tma2d(&s.V[stage][off], big ? mv64 : mv8, h * (CF::HALF / 2), y, &s.full[stage]);
                     }
-                }
-                __syncwarp();
-                if (++stage == CF::NS) {
-                    stage = 0;
-                    phase ^= 1;
+                    const uint32_t step = big ? 64 : 8;
+                    rem -= step;
+                    sr += step;
+                    y += (int)step;
                 }
             }
-            it = next;
+            __syncwarp();
+            if (++stage == CF::NS) {
+                stage = 0;
+                phase ^= 1;
+            }
+            // ---- advance
+            if (last_tile && lane == 0 && it2 < n_items) next_it = atomicAdd(&a.ctr->work, 1u);
+            it = it2;
+            itm = itm2;
+            t = t2;
+            np = np2;
+            pr = pr2;
         }
         return;
     }
@@ -881,7 +933,14 @@ void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cu
 void launch_route_score(const RouteArgs& a, uint32_t n_groups, cudaStream_t st) {
     uint32_t threads = 32;
     while (threads < a.slice) threads <<= 1;
-    route_score_kernel<<<dim3(n_groups, a.n_slices), threads, 0, st>>>(a);
+    const size_t smem = a.mode == 1 ? (size_t)a.D * a.slice * 4 : 0;
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        SAAP_CUDA(cudaFuncSetAttribute(route_score_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
+    route_score_kernel<<<dim3(n_groups, a.n_slices), threads, smem, st>>>(a);
     SAAP_CUDA(cudaGetLastError());
 }
 
