@@ -425,7 +425,7 @@ def ours(a):
     dense_bytes = n_groups * N * d * 2 * 2
 
     # ---- end to end through the public host API (pinned host buffers)
-    import ctypes as C
+    import ctypes as ct
     qh = torch.empty(n_groups, G, d, pin_memory=True)
     qh.copy_(q.cpu())
     oh = torch.empty(n_groups, G, d, pin_memory=True)
@@ -436,8 +436,8 @@ def ours(a):
     def e2e_step(i):
         lay = layers[i % a.layers]
         sb._check(lib.saap_sparse_attention(
-            ctx.h, lay["L"].h, lay["L"]._routers(lay["routers"]), C.c_void_p(qh.data_ptr()),
-            C.c_void_p(qh.data_ptr()), C.c_uint64(G), C.byref(ccfg), C.c_void_p(oh.data_ptr()),
+            ctx.h, lay["L"].h, lay["L"]._routers(lay["routers"]), ct.c_void_p(qh.data_ptr()),
+            ct.c_void_p(qh.data_ptr()), ct.c_uint64(G), ct.byref(ccfg), ct.c_void_p(oh.data_ptr()),
             st_h, None))
 
     ms_e2e = timed(e2e_step, a.steps, a.warmup)

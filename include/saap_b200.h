@@ -230,6 +230,10 @@ SAAP_API int saap_ctx_launch_count(saap_ctx* ctx, uint64_t* out);
  * softmax (host arrays); lets tests pin it against the host libm. */
 SAAP_API int saap_debug_exp(saap_ctx* ctx, const double* x, uint64_t n, double* out);
 
+/* With SAAP_PLAN_TRACE set: clock64 offsets of the planner's phases for
+ * context 0 of the last decode step (8 x u64). */
+SAAP_API int saap_debug_plan_trace(saap_ctx* ctx, uint64_t* out);
+
 /* ---- synthetic data (bench tooling; counter-based, reproducible) ------- */
 /* Fills a device bf16 [rows x dim] buffer with clustered keys / values. */
 SAAP_API int saap_synth_fill_dev(saap_ctx* ctx, void* out_bf16, uint64_t rows, uint64_t dim,

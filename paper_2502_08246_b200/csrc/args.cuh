@@ -35,6 +35,7 @@ struct RouteArgs {
     uint32_t slice, n_slices, keep;  // keep = min(probes, slice)
     double* cand_s;                // [groups][n_slices][keep]
     uint32_t* cand_i;
+    float* approx;                 // approx mode: [groups][C] fp32 scores, no selection here
 };
 struct ItemRec {
     uint32_t qslot;
@@ -61,6 +62,10 @@ struct PlanArgs {
     uint32_t n_cand;             // n_slices * keep
     const double* cand_s;        // routing candidates from route_score_kernel
     const uint32_t* cand_i;
+    const float* approx;         // centroid router, C <= 1024: fp32 scores [groups][C]
+    const float* const* centT;   // per group d x C f32 centroids (exact re-scoring)
+    const float* cmax;           // per group max centroid norm
+    unsigned long long* trace;   // debug: clock64 per planning phase (CTA 0)
     int route_only;              // BucketRouter::select: write `selected`, plan nothing
     // general-window rows are gathered into a contiguous buffer
     const uint16_t* K;

@@ -34,7 +34,7 @@ constexpr uint32_t A_TILE_BYTES = TM * KD * 2;         // 32 KB
 constexpr uint32_t B_TERM_BYTES = CN * KD * 2;         // 32 KB
 constexpr uint32_t B_STAGE_BYTES = 2 * B_TERM_BYTES;   // hi + mid
 constexpr uint32_t TMEM_COLS = 512;
-constexpr int THREADS = 192;
+constexpr int THREADS = 320;  // warps 0-7 epilogue, 8 TMA, 9 MMA
 }  // namespace tc
 
 struct TcTile {
@@ -52,7 +52,7 @@ struct TcAssignArgs {
     uint32_t C;                // buckets
     uint32_t Cpad;             // C rounded up to CN
     uint32_t* out;
-    uint32_t* refine;          // pairs (group, lid)
+    uint32_t* refine;          // (group, lid, best id, second id | ~0 for a full re-scan)
     uint32_t* refine_count;
     const uint16_t* keys;      // same tensor the map covers (for |k|)
 };
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s.t_full[i], 1);
-            mbar_init(&s.t_empty[i], 4);  // one arrive per epilogue warp
+            mbar_init(&s.t_empty[i], 8);  // one arrive per epilogue warp
         }
         fence_mbar_init();
     }
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = s.tmem_base;
 
-    if (warp == 4) {
+    if (warp == 8) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(&map_k) : "memory");
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                                     &s.b_full[st]);
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == 9) {
         // ------------------------------------------------ MMA issuer (one thread)
         if (lane == 0) {
             constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
@@ -209,74 +209,67 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             }
         }
     } else {
-        // ------------------------------------------------ epilogue: lane = key row
-        const int row = warp * 32 + lane;
-        float best[NT], second[NT], bound[NT];
-        uint32_t bidx[NT];
+        // ------------------------------------------------ epilogue: warp w drains
+        // tile w/4, TMEM lanes 32*(w%4).. (lane = key row); branchless top-3
+        const int t = warp >> 2, q4 = warp & 3;
+        const int row = q4 * 32 + lane;
+        const TcTile tt = a.tiles[blockIdx.x * NT + t];
+        float b1 = -INFINITY, b2 = -INFINITY, b3 = -INFINITY;
+        uint32_t i1 = 0, i2 = 0;
+        float n2 = 0.f;
+        if ((uint32_t)row < tt.count) {
+            const uint4* kp = reinterpret_cast<const uint4*>(a.keys + (a.key_row0[tt.group] + tt.lid0 + row) * KD);
 #pragma unroll
-        for (int t = 0; t < NT; ++t) {
-            best[t] = -INFINITY;
-            second[t] = -INFINITY;
-            bidx[t] = 0;
-            const TcTile tt = a.tiles[blockIdx.x * NT + t];
-            float n2 = 0.f;
-            if ((uint32_t)row < tt.count) {
-                const uint4* kp = reinterpret_cast<const uint4*>(
-                        a.keys + (a.key_row0[tt.group] + tt.lid0 + row) * KD);
+            for (int q = 0; q < KD / 8; ++q) {
+                const uint4 u = kp[q];
+                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-                for (int q = 0; q < KD / 8; ++q) {
-                    const uint4 u = kp[q];
-                    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float lo = bf16lo(w[e]), hi = bf16hi(w[e]);
-                        n2 = fmaf(lo, lo, fmaf(hi, hi, n2));
-                    }
+                for (int e = 0; e < 4; ++e) {
+                    const float lo = bf16lo(w4[e]), hi = bf16hi(w4[e]);
+                    n2 = fmaf(lo, lo, fmaf(hi, hi, n2));
                 }
             }
-            bound[t] = 0x1p-14f * 1.0001f * sqrtf(n2) * a.cmax[tt.part];
         }
+        const float bound = 0x1p-14f * 1.0001f * sqrtf(n2) * a.cmax[tt.part];
+        const uint32_t taddr0 = tmem + ((uint32_t)(q4 * 32) << 16) + t * CN;
         for (uint32_t j = 0; j < nchunks; ++j) {
             const uint32_t buf = j & 1, bph = (j >> 1) & 1;
             mbar_wait(&s.t_full[buf], bph);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-            for (int t = 0; t < NT; ++t) {
+            const bool tail = (j + 1) * CN > a.C;
 #pragma unroll 1
-                for (int q = 0; q < CN / 32; ++q) {
-                    float v[32];
-                    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + buf * (NT * CN) + t * CN + q * 32, v);
-                    const uint32_t c0 = j * CN + q * 32;
+            for (int q = 0; q < CN / 32; ++q) {
+                float v[32];
+                tmem_ld32(taddr0 + buf * (NT * CN) + q * 32, v);
+                const uint32_t c0 = j * CN + q * 32;
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const float x = v[i];
-                        if (c0 + i < a.C) {
-                            if (x > best[t]) {
-                                second[t] = best[t];
-                                best[t] = x;
-                                bidx[t] = c0 + i;
-                            } else if (x > second[t]) {
-                                second[t] = x;
-                            }
-                        }
-                    }
+                for (int i = 0; i < 32; ++i) {
+                    const float x = (tail && c0 + i >= a.C) ? -INFINITY : v[i];
+                    const bool g1 = x > b1, g2 = x > b2;
+                    b3 = fmaxf(b3, fminf(x, b2));
+                    const float nb2 = g1 ? b1 : (g2 ? x : b2);
+                    i2 = g1 ? i1 : (g2 ? c0 + i : i2);
+                    b2 = nb2;
+                    b1 = g1 ? x : b1;
+                    i1 = g1 ? c0 + i : i1;
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.t_empty[buf]);
         }
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-            const TcTile tt = a.tiles[blockIdx.x * NT + t];
-            if ((uint32_t)row >= tt.count) continue;
+        if ((uint32_t)row < tt.count) {
             const uint32_t lid = tt.lid0 + row;
-            if (best[t] - second[t] > 2.f * bound[t]) {
-                a.out[a.out_base[tt.group] + lid] = bidx[t];
+            if (b1 - b2 > 2.f * bound) {
+                a.out[a.out_base[tt.group] + lid] = i1;
             } else {
+                // ambiguous: the exact argmax is i1 or i2 when the third-best is
+                // out of range, else any centroid (full fp64 re-scan)
                 const uint32_t slot = atomicAdd(a.refine_count, 1u);
-                a.refine[2 * slot] = tt.group;
-                a.refine[2 * slot + 1] = lid;
+                a.refine[4 * slot] = tt.group;
+                a.refine[4 * slot + 1] = lid;
+                a.refine[4 * slot + 2] = i1;
+                a.refine[4 * slot + 3] = (b1 - b3 > 2.f * bound) ? i2 : 0xFFFFFFFFu;
             }
         }
     }
@@ -288,32 +281,59 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     }
 }
 
-// fp64 re-score of ambiguous keys in the reference's exact operation order.
+// fp64 re-score of ambiguous keys in the reference's exact operation order
+// (sequential over d; products of bf16 keys and f32 centroids are exact, so
+// DFMA == mulsd+addsd).  One warp per key: two candidates -> lanes 0/1; full
+// re-scan -> lanes split the centroids, then a (score desc, id asc) reduction.
 template <int D>
-__global__ void __launch_bounds__(128) refine_kernel(const uint32_t* list, const uint32_t* count,
+__device__ __forceinline__ double exact_dot(const uint16_t* kp, const double* cr) {
+    double s = 0.0;
+#pragma unroll 8
+    for (int j = 0; j < D; ++j) s = fma((double)__uint_as_float(((uint32_t)kp[j]) << 16), cr[j], s);
+    return s;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) refine_kernel(const uint32_t* list, const uint32_t* count,
                                                      const uint16_t* keys,
                                                      const uint64_t* key_row0,
                                                      const double* const* cent64,
                                                      const uint64_t* out_base, uint32_t C,
                                                      uint32_t* out) {
     const uint32_t n = *count;
-    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
-        const uint32_t g = list[2 * e], lid = list[2 * e + 1];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t e = wid; e < n; e += nw) {
+        const uint32_t g = list[4 * e], lid = list[4 * e + 1], c1 = list[4 * e + 2], c2 = list[4 * e + 3];
         const uint16_t* kp = keys + (key_row0[g] + lid) * D;
         const double* cg = cent64[g];
         double best = -INFINITY;
-        uint32_t bid = 0;
-        for (uint32_t c = 0; c < C; ++c) {
-            double s = 0.0;
-            const double* cr = cg + (size_t)c * D;
-#pragma unroll 8
-            for (int j = 0; j < D; ++j) s = fma((double)__uint_as_float(((uint32_t)kp[j]) << 16), cr[j], s);
-            if (s > best) {
-                best = s;
+        uint32_t bid = 0xFFFFFFFFu;
+        if (c2 != 0xFFFFFFFFu) {
+            if (lane < 2) {
+                const uint32_t c = lane ? c2 : c1;
+                best = exact_dot<D>(kp, cg + (size_t)c * D);
                 bid = c;
             }
+        } else {
+            for (uint32_t c = lane; c < C; c += 32) {
+                const double sc = exact_dot<D>(kp, cg + (size_t)c * D);
+                if (sc > best) {  // ascending c per lane: strict > keeps the lowest id
+                    best = sc;
+                    bid = c;
+                }
+            }
         }
-        out[out_base[g] + lid] = bid;
+        for (int o = 16; o; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+            const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, bid, o);
+            if (ob > best || (ob == best && oi < bid)) {
+                best = ob;
+                bid = oi;
+            }
+        }
+        if (lane == 0) out[out_base[g] + lid] = bid;
     }
 }
 
@@ -424,7 +444,7 @@ void launch_assign_tc(const uint16_t* keys, uint64_t key_rows, const uint16_t* h
 void launch_refine(const uint32_t* list, const uint32_t* count, const uint16_t* keys,
                    const uint64_t* key_row0, const double* const* cent64, const uint64_t* out_base,
                    uint32_t C, uint32_t* out, int sm_count, cudaStream_t st) {
-    refine_kernel<128><<<sm_count * 4, 128, 0, st>>>(list, count, keys, key_row0, cent64, out_base, C,
+    refine_kernel<128><<<sm_count * 4, 256, 0, st>>>(list, count, keys, key_row0, cent64, out_base, C,
                                                      out);
     SAAP_CUDA(cudaGetLastError());
 }

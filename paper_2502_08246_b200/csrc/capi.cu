@@ -215,9 +215,15 @@ void bind_routers(saap_layer* L, const saap_router* const* routers, int& mode, i
     if (L->ctx->capturing) invalid("router set changed during graph capture");
     if (kind == 0) {
         std::vector<const float*> p(L->n_groups);
-        for (size_t g = 0; g < p.size(); ++g) p[g] = rs[g]->part->centT;
+        std::vector<float> cm(L->n_groups);
+        for (size_t g = 0; g < p.size(); ++g) {
+            p[g] = rs[g]->part->centT;
+            cm[g] = rs[g]->part->cmax;
+        }
         if (!L->d_centT) L->d_centT = (const float**)(dmalloc<void*>(L->n_groups));
+        if (!L->d_cmax) L->d_cmax = dmalloc<float>(L->n_groups);
         SAAP_CUDA(cudaMemcpy(L->d_centT, p.data(), p.size() * sizeof(void*), cudaMemcpyHostToDevice));
+        SAAP_CUDA(cudaMemcpy(L->d_cmax, cm.data(), cm.size() * 4, cudaMemcpyHostToDevice));
     } else {
         std::vector<const double*> p(3 * L->n_groups);
         for (size_t g = 0; g < L->n_groups; ++g) {
@@ -264,11 +270,15 @@ RouteGeo route_geo(uint64_t C, uint64_t probes) {
     return r;
 }
 
-// stage-1 routing launch for n groups (mode 1 centroid / 2 Q-model scores)
+// stage-1 routing launch for n groups (mode 1 centroid / 2 Q-model scores).
+// Centroid routing with C <= 1024 uses fp32 scores + exact re-scoring of the
+// boundary candidates in the planner; otherwise every score is exact fp64.
 void enqueue_route_score(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C, uint64_t G,
                          uint64_t probes, int mode, const float* const* centT,
-                         const float* q_route, const double* probs, PlanArgs& pa) {
+                         const float* q_route, const double* probs, PlanArgs& pa,
+                         const float* cmax = nullptr) {
     const RouteGeo geo = route_geo(C, probes);
+    const bool approx = mode == 1 && C <= kPlanThreads && cmax != nullptr;
     double* cs = (double*)ensure(c, c->cand_s, n_groups * geo.n_cand * sizeof(double));
     uint32_t* ci = (uint32_t*)ensure(c, c->cand_i, n_groups * geo.n_cand * sizeof(uint32_t));
     RouteArgs ra{};
@@ -285,9 +295,15 @@ void enqueue_route_score(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
     ra.keep = geo.keep;
     ra.cand_s = cs;
     ra.cand_i = ci;
+    if (approx) {
+        ra.approx = (float*)ensure(c, c->approx, n_groups * C * sizeof(float));
+        pa.approx = ra.approx;
+        pa.centT = centT;
+        pa.cmax = cmax;
+    }
     launch_route_score(ra, (uint32_t)n_groups, c->stream);
     c->launches++;
-    pa.P2 = geo.P2;
+    pa.P2 = approx ? next_pow2((uint32_t)C) : geo.P2;
     pa.n_cand = geo.n_cand;
     pa.cand_s = cs;
     pa.cand_i = ci;
@@ -336,7 +352,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const float* co
                     const double* const* qm, const float* q_roped, const float* q_route,
                     uint64_t G, uint64_t probes, uint64_t recent, float* out,
                     saap_attn_stats* stats, uint32_t* selected, uint32_t item_tiles,
-                    uint32_t qm_hidden = 0) {
+                    uint32_t qm_hidden = 0, const float* cmax = nullptr) {
     const cudaStream_t st = c->stream;
     const uint64_t n_groups = src.n_groups, D = src.D, C = src.C;
     const uint64_t n_hchunks = (G + kHeadsPerSlot - 1) / kHeadsPerSlot;
@@ -407,7 +423,9 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const float* co
         SAAP_CUDA(cudaEventRecord(e0, st));
     }
     if ((mode == 1 || mode == 2) && probes > 0)
-        enqueue_route_score(c, n_groups, D, C, G, probes, mode, centT, q_route, probs, pa);
+        enqueue_route_score(c, n_groups, D, C, G, probes, mode, centT, q_route, probs, pa, cmax);
+    static const bool trace_on = std::getenv("SAAP_PLAN_TRACE") != nullptr;
+    if (trace_on) pa.trace = (unsigned long long*)ensure(c, c->trace, 64);
     launch_route_plan(pa, (uint32_t)n_groups, st);
     c->launches++;
     if (e1) SAAP_CUDA(cudaEventRecord(e1, st));
@@ -628,6 +646,13 @@ int saap_partition_create(saap_ctx* c, const float* cent, uint64_t C, uint64_t d
                 t[j * C + i] = cent[i * d + j];
                 d64[i * d + j] = (double)cent[i * d + j];
             }
+        double cm = 0;
+        for (uint64_t i = 0; i < C; ++i) {
+            double n2 = 0;
+            for (uint64_t j = 0; j < d; ++j) n2 += (double)cent[i * d + j] * cent[i * d + j];
+            cm = std::max(cm, std::sqrt(n2));
+        }
+        p->cmax = (float)(cm * (1 + 1e-6));
         p->cent = dmalloc<float>(C * d);
         p->centT = dmalloc<float>(C * d);
         p->cent64 = dmalloc<double>(C * d);
@@ -727,8 +752,9 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
     h2d(dq, q_route, G * d * 4, st);
     uint32_t* dsel = (uint32_t*)ensure(c, c->sel, l * 4);
     GroupMeta gm{0, 0, 2, 0, 0, 0};  // n > sink + recent so routing runs
-    GroupMeta* dmeta = (GroupMeta*)ensure(c, c->misc, sizeof(GroupMeta) + 2 * sizeof(void*) * 3);
+    GroupMeta* dmeta = (GroupMeta*)ensure(c, c->misc, sizeof(GroupMeta) + 2 * sizeof(void*) * 3 + 16);
     void** dptr = reinterpret_cast<void**>(reinterpret_cast<char*>(dmeta) + sizeof(GroupMeta));
+    float* dcmax = reinterpret_cast<float*>(dptr + 3);
     void* ptrs[3];
     int mode;
     double* probs = nullptr;
@@ -744,6 +770,7 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
     }
     h2d(dmeta, &gm, sizeof gm, st);
     h2d(dptr, ptrs, sizeof(void*) * 3, st);
+    if (r->kind == 0) h2d(dcmax, &r->part->cmax, 4, st);
     if (mode == 2) {
         QModelArgs qa{};
         qa.q = dq;
@@ -770,7 +797,8 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
     pa.item_tiles = kItemTilesSparse;
     pa.route_only = 1;
     pa.selected = dsel;
-    enqueue_route_score(c, 1, d, C, G, l, mode, (const float* const*)dptr, dq, probs, pa);
+    enqueue_route_score(c, 1, d, C, G, l, mode, (const float* const*)dptr, dq, probs, pa,
+                        r->kind == 0 ? dcmax : nullptr);
     launch_route_plan(pa, 1, st);
     c->launches++;
     d2h(out, dsel, l * 4, st);
@@ -1018,6 +1046,7 @@ int saap_layer_destroy(saap_layer* L) {
         dfree(L->tc_refine_count);
         if (L->tc_tiles) cudaFree(L->tc_tiles);
         dfree(L->d_centT);
+        dfree(L->d_cmax);
         dfree(L->d_qm);
         delete L;
     });
@@ -1095,7 +1124,7 @@ static void assign_tc_path(saap_layer* L, const uint16_t* keys) {
         L->tc_nslots = (uint32_t)slots.size();
     }
     if (!L->tc_refine) {
-        L->tc_refine = dmalloc<uint32_t>(2 * L->total_ns);
+        L->tc_refine = dmalloc<uint32_t>(4 * L->total_ns);
         L->tc_refine_count = dmalloc<uint32_t>(1);
     }
     SAAP_CUDA(cudaMemsetAsync(L->tc_refine_count, 0, 4, st));
@@ -1331,7 +1360,8 @@ static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* con
                            (cfg->recent_count > L->recent_hint || (mode != 3 && cfg->probes > 0));
     const DecodeSrc src = layer_src(L, cfg->recent_count, need_gather);
     enqueue_decode(c, src, mode, L->d_centT, L->d_qm, qr, q_route, G, cfg->probes,
-                   cfg->recent_count, out, stats, selected, kItemTilesSparse, (uint32_t)hq);
+                   cfg->recent_count, out, stats, selected, kItemTilesSparse, (uint32_t)hq,
+                   mode == 1 ? L->d_cmax : nullptr);
 }
 
 int saap_sparse_attention_dev(saap_ctx* c, const saap_layer* L, const saap_router* const* routers,
@@ -1557,6 +1587,15 @@ int saap_debug_exp(saap_ctx* c, const double* x, uint64_t n, double* out) {
         launch_debug_exp(dx, n, dx + n, c->stream);
         c->launches++;
         d2h(out, dx + n, n * 8, c->stream);
+        sync(c);
+    });
+}
+
+int saap_debug_plan_trace(saap_ctx* c, uint64_t* out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        if (!c->trace.p) invalid("plan tracing off: set SAAP_PLAN_TRACE before the first decode");
+        d2h(out, c->trace.p, 64, c->stream);
         sync(c);
     });
 }

@@ -151,7 +151,7 @@ struct saap_ctx {
     bool own_stream = false;
     uint64_t launches = 0;
     // growable device scratch (sized by uncaptured calls; graphs reuse it)
-    saap_scratch qA, cand_s, cand_i, items, tiles, qslots, part_O, part_ml, probs, stats, sel, qr, qd, out, misc, zeros;
+    saap_scratch approx, trace, qA, cand_s, cand_i, items, tiles, qslots, part_O, part_ml, probs, stats, sel, qr, qd, out, misc, zeros;
     saap_b200::StepCounters* counters = nullptr;  // persistent, 128 B
     uint32_t* done = nullptr;                     // per query slot completion counters
     size_t done_cap = 0;
@@ -169,6 +169,7 @@ struct saap_partition {
     float* cent = nullptr;     // C x d f32 (device)
     double* cent64 = nullptr;  // C x d fp64 (device, exact assignment)
     float* centT = nullptr;    // d x C f32 (device, routing slabs; exact in fp64)
+    float cmax = 0.f;          // max centroid L2 norm (routing error bound)
     std::vector<float> host;   // kept for validation / read-back
 };
 
@@ -217,7 +218,7 @@ struct saap_layer {
     uint16_t* tc_mid = nullptr;
     size_t tc_split_elems = 0;
     float* tc_cmax = nullptr;
-    uint32_t* tc_refine = nullptr;   // 2 * total_ns
+    uint32_t* tc_refine = nullptr;   // 4 * total_ns
     uint32_t* tc_refine_count = nullptr;
     uint64_t* key_row0 = nullptr;    // per group: row_base + sink
     uint64_t* ivf_base = nullptr;    // per group
@@ -229,6 +230,7 @@ struct saap_layer {
     // routing parameter table cache (device arrays of per-group pointers)
     std::vector<const saap_router*> cached_routers;
     const float** d_centT = nullptr;   // per group centT
+    float* d_cmax = nullptr;           // per group partition cmax
     const double** d_qm = nullptr;     // per group: w1, w2, vec (3 pointers)
     // decode: TMA maps over the packed cache (+ gather buffer), built lazily
     void* maps = nullptr;              // DecodeMaps (host copy)

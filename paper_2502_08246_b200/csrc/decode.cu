@@ -85,6 +85,41 @@ __device__ void bitonic_regs(double& s, uint32_t& id, uint32_t n, double* xs, ui
     }
 }
 
+// fp32 variant (approximate scores; same total order)
+__device__ void bitonic_regs_f(float& s, uint32_t& id, uint32_t n, float* xs, uint32_t* xi) {
+    const uint32_t t = threadIdx.x;
+    for (uint32_t k = 2; k <= n; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            float ps = 0.f;
+            uint32_t pi = 0;
+            if (j >= 32) {
+                if (t < n) {
+                    xs[t] = s;
+                    xi[t] = id;
+                }
+                __syncthreads();
+                if (t < n) {
+                    ps = xs[t ^ j];
+                    pi = xi[t ^ j];
+                }
+                __syncthreads();
+            } else {
+                ps = __shfl_xor_sync(0xFFFFFFFFu, s, j);
+                pi = __shfl_xor_sync(0xFFFFFFFFu, id, j);
+            }
+            if (t < n) {
+                const bool dir = (t & k) == 0;
+                const bool lower = (t & j) == 0;
+                const bool p_first = ps > s || (ps == s && pi < id);
+                if ((lower == dir) ? p_first : !p_first) {
+                    s = ps;
+                    id = pi;
+                }
+            }
+        }
+    }
+}
+
 __device__ void bitonic_smem(double* ss, uint32_t* si, uint32_t n) {
     for (uint32_t k = 2; k <= n; k <<= 1) {
         for (uint32_t j = k >> 1; j > 0; j >>= 1) {
@@ -147,6 +182,17 @@ __global__ void __launch_bounds__(kSliceMax) route_score_kernel(RouteArgs a) {
         }
         if (bulk) mbar_wait(&bar, 0);
         __syncthreads();
+        if (a.approx) {
+            // fp32 scores with the rounded pooled vector; route_plan_kernel bounds
+            // their error and re-scores the boundary candidates exactly
+            if (tid < nsl) {
+                float x = 0.f;
+#pragma unroll 8
+                for (uint32_t j = 0; j < a.D; ++j) x = fmaf((float)pooled[j], slab[j * a.slice + tid], x);
+                a.approx[(size_t)g * a.C + c0 + tid] = x;
+            }
+            return;
+        }
     }
     double sc = -INFINITY;
     uint32_t id = 0xFFFFFFFFu;
@@ -206,8 +252,73 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         s_gbase = 0;
     }
 
-    // ---------------- routing: merge candidates -> top-L in reference order
-    if (route) {
+    unsigned long long t0 = 0;
+    auto trace = [&](int k) {
+        if (a.trace && g == 0 && tid == 0) a.trace[k] = clock64() - t0;
+    };
+    if (a.trace && g == 0 && tid == 0) t0 = clock64();
+    // ---------------- routing: candidates -> top-L in reference order
+    if (route && a.approx) {
+        // centroid router, C <= blockDim: exact top-L from fp32 scores.  With
+        // B = 2^-16 |pooled|_2 max|c|_2 >= |approx - exact| (pooled rounded to
+        // f32: 2^-24 rel; fp32 accumulation of D products: D * 2^-24 rel), every
+        // centroid whose approx score is below t_L - 2B (t_L = L-th largest
+        // approx) ranks below L others exactly; the rest are re-scored with
+        // the reference's fp64 chain (attention.cpp:296-304) and sorted exactly.
+        __shared__ double pooled[128];
+        __shared__ float s_thr;
+        __shared__ double s_n2[32];
+        const float* q = a.q_route + (size_t)g * a.G * a.D;
+        double part = 0.0;
+        for (uint32_t j = tid; j < a.D; j += nth) {
+            double sj = 0.0;
+            for (uint32_t i = 0; i < a.G; ++i) sj = __dadd_rn(sj, (double)q[(size_t)i * a.D + j]);
+            pooled[j] = sj;
+            part += sj * sj;
+        }
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, o);
+        if ((tid & 31) == 0) s_n2[tid >> 5] = part;
+        float av = -INFINITY;
+        uint32_t aid = 0xFFFFFFFFu;
+        if (tid < Cb) {
+            av = a.approx[(size_t)g * Cb + tid];
+            aid = tid;
+        }
+        bitonic_regs_f(av, aid, a.P2, reinterpret_cast<float*>(ss), si);
+        trace(1);
+        if (tid == L - 1) s_thr = av;
+        __syncthreads();
+        double n2 = 0.0;
+        for (uint32_t w = 0; w < nth / 32; ++w) n2 += s_n2[w];
+        const float B2 = (float)(2.0 * 0x1p-16 * sqrt(n2) * (double)a.cmax[g]) * 1.0001f;
+        const bool cand = tid < Cb && av >= s_thr - B2;
+        const uint32_t nS = __syncthreads_count(cand);
+        double ex = -INFINITY;
+        uint32_t eid = 0xFFFFFFFFu;
+        if (tid < nS) {
+            const float* cT = a.centT[g];
+            double sx = 0.0;
+#pragma unroll 8
+            for (uint32_t j = 0; j < a.D; ++j)
+                sx = __dadd_rn(sx, __dmul_rn(pooled[j], (double)cT[(size_t)j * Cb + aid]));
+            ex = sx;
+            eid = aid;
+        }
+        uint32_t p2s = 1;
+        while (p2s < nS) p2s <<= 1;
+        trace(2);
+        bitonic_regs(ex, eid, p2s, ss, si);
+        __syncthreads();
+        if (tid < L) si[tid] = eid;
+        for (uint32_t w = tid; w < bm_words; w += nth) bitmap[w] = 0;
+        __syncthreads();
+        for (uint32_t b = tid; b < L; b += nth) {
+            atomicOr(&bitmap[si[b] >> 5], 1u << (si[b] & 31));
+            if (a.selected) a.selected[(size_t)g * a.probes + b] = si[b];
+        }
+        __syncthreads();
+        trace(3);
+    } else if (route) {
         const double* cs = a.cand_s + (size_t)g * a.n_cand;
         const uint32_t* ci = a.cand_i + (size_t)g * a.n_cand;
         if (a.P2 <= nth) {
@@ -269,6 +380,7 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
     if (my_keys) atomicAdd(&s_keys, my_keys);
     if (my_max) atomicMax(&s_maxv, my_max);
     __syncthreads();
+    trace(4);
 
     // general windows: materialise the out-of-order rows in the gather buffer
     //   recent > hint (rb < T): region-A rows with position in [rb, T) (pos -> row map)
@@ -378,6 +490,7 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
             a.qslots[g * a.n_hchunks + hc] = QSlot{s_item0 + hc * nitems, nitems};
     }
     __syncthreads();
+    trace(5);
     const uint32_t ntiles = s_ntiles, nitems = s_nitems, tile0 = s_tile0;
     if (nitems == 0) {  // nothing visited: zero rows, empty_attention (attention.cpp:147-152)
         for (uint32_t e = tid; e < a.G * a.D; e += nth) a.out[(size_t)g * a.G * a.D + e] = 0.f;
@@ -402,6 +515,7 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
     }
     for (uint32_t t = tid; t < ntiles; t += nth) a.tiles[tile0 + t].npieces = 0;
     __syncthreads();
+    trace(6);
     // pieces: one per (segment, overlapped tile); slot order inside a tile is
     // free.  Short segments: one thread each; long ones: tiles spread over the CTA.
     auto emit = [&](const Seg& sg, uint32_t v0, uint32_t t) {
@@ -438,6 +552,7 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         it.pad = 0;
         a.items[s_item0 + e] = it;
     }
+    trace(7);
 }
 
 // ============================================================ attention
@@ -474,7 +589,8 @@ struct DecodeSmem2 {
     uint64_t empty[CF::NS];
     int4 meta[CF::NS];    // item, tile-in-item | last<<31, qslot, nq (q heads loaded)
     uint4 valid[CF::NS];  // 128-bit row validity mask
-    int flag;
+    uint32_t mcnt;  // warps that deposited their state for the current item
+    uint32_t mgen;  // items merged so far
 };
 
 // swizzled byte offset of (row, 16-byte chunk) inside one tile half
@@ -534,6 +650,8 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
             mbar_init(&s.full[i], 1);
             mbar_init(&s.empty[i], kComputeWarps);
         }
+        s.mcnt = 0;
+        s.mgen = 0;
         fence_mbar_init();
     }
     // gap rows of a tile are masked (p = 0) but still enter the PV MMA: start
@@ -683,7 +801,7 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
     uint32_t qa[CF::KSTEPS][4];  // A fragments of [q1; q2; q3; 0]
     float o[CF::NT][4];
     float m_run = -INFINITY, l_run = 0.f;
-    uint32_t cur_item = 0, cur_qslot = 0;
+    uint32_t cur_item = 0, cur_qslot = 0, item_seq = 0;
 
     uint32_t stage = 0, phase = 0;
     for (;;) {
@@ -797,7 +915,16 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
         if (lane == 0) mbar_arrive(&s.empty[stage]);
 
         if (last) {
-            // ---- item done: merge the 8 warps' (m, l, O) states
+            // ---- item done.  Each warp deposits its (m, l, O) state; the last
+            // warp to arrive merges the eight states and publishes the item
+            // while the other warps stream on.  s.mgen counts merged items, so
+            // a warp never overwrites a state buffer that is still being read.
+            ++item_seq;
+            if (item_seq > 1) {
+                if (lane == 0)
+                    while (*reinterpret_cast<volatile uint32_t*>(&s.mgen) < item_seq - 1) __nanosleep(32);
+                __syncwarp();
+            }
             float lw = l_run;
             lw += __shfl_xor_sync(0xFFFFFFFFu, lw, 1);
             lw += __shfl_xor_sync(0xFFFFFFFFu, lw, 2);
@@ -817,88 +944,103 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
                 s.redm[warp][hq] = m_run;
                 s.redl[warp][hq] = lw;
             }
-            named_bar_sync(1, kComputeWarps * 32);
-
-            const QSlot qs = a.qslots[cur_qslot];
-            const uint32_t g = cur_qslot / a.n_hchunks, hc = cur_qslot % a.n_hchunks;
-            const int tid = threadIdx.x;
-            constexpr int NOUT = kHeadsPerSlot * D;
-            constexpr int PER = (NOUT + kComputeWarps * 32 - 1) / (kComputeWarps * 32);
-            float resO[PER], resM[PER], resL[PER];
-#pragma unroll
-            for (int e0 = 0; e0 < PER; ++e0) {
-                const int e = tid + e0 * kComputeWarps * 32;
-                resO[e0] = 0.f;
-                resM[e0] = -INFINITY;
-                resL[e0] = 0.f;
-                if (e >= NOUT) continue;
-                const int h = e / D, d = e % D;
-                float M = -INFINITY;
-#pragma unroll
-                for (int w = 0; w < kComputeWarps; ++w) M = fmaxf(M, s.redm[w][h]);
-                float O = 0.f, Ls = 0.f;
-#pragma unroll
-                for (int w = 0; w < kComputeWarps; ++w) {
-                    const float wt = fast_exp2(s.redm[w][h] - M);
-                    O = fmaf(s.redO[w][h][d], wt, O);
-                    Ls = fmaf(s.redl[w][h], wt, Ls);
-                }
-                resO[e0] = O;
-                resM[e0] = M;
-                resL[e0] = Ls;
+            __syncwarp();
+            uint32_t merger = 0;
+            if (lane == 0) {
+                __threadfence_block();
+                merger = atomicAdd(&s.mcnt, 1u) == kComputeWarps - 1;
+                if (merger) __threadfence_block();
             }
-            if (qs.count == 1) {
+            merger = __shfl_sync(0xFFFFFFFFu, merger, 0);
+            if (merger) {
+                const QSlot qs = a.qslots[cur_qslot];
+                const uint32_t g = cur_qslot / a.n_hchunks, hc = cur_qslot % a.n_hchunks;
+                constexpr int NOUT = kHeadsPerSlot * D;
+                constexpr int PER = NOUT / 32;
+                float resO[PER];
+                float mh[4], lh[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    float M = -INFINITY;
+#pragma unroll
+                    for (int w = 0; w < kComputeWarps; ++w) M = fmaxf(M, s.redm[w][h]);
+                    float Ls = 0.f;
+#pragma unroll
+                    for (int w = 0; w < kComputeWarps; ++w) Ls = fmaf(s.redl[w][h], fast_exp2(s.redm[w][h] - M), Ls);
+                    mh[h] = M;
+                    lh[h] = Ls;
+                }
 #pragma unroll
                 for (int e0 = 0; e0 < PER; ++e0) {
-                    const int e = tid + e0 * kComputeWarps * 32;
-                    if (e >= NOUT) break;
-                    const uint32_t head = hc * kHeadsPerSlot + e / D;
-                    if (head < a.G) a.out[((size_t)g * a.G + head) * D + e % D] = resO[e0] / resL[e0];
-                }
-            } else {
-                float* pO = a.part_O + (size_t)cur_item * NOUT;
+                    const int e = lane + 32 * e0, h = e / D, d = e % D;
+                    const float M = h == 0 ? mh[0] : h == 1 ? mh[1] : h == 2 ? mh[2] : mh[3];
+                    float O = 0.f;
 #pragma unroll
-                for (int e0 = 0; e0 < PER; ++e0) {
-                    const int e = tid + e0 * kComputeWarps * 32;
-                    if (e >= NOUT) break;
-                    pO[e] = resO[e0];
-                    if (e % D == 0) {
-                        a.part_ml[(size_t)cur_item * 8 + e / D] = resM[e0];
-                        a.part_ml[(size_t)cur_item * 8 + 4 + e / D] = resL[e0];
-                    }
+                    for (int w = 0; w < kComputeWarps; ++w)
+                        O = fmaf(s.redO[w][h][d], fast_exp2(s.redm[w][h] - M), O);
+                    resO[e0] = O;
                 }
-                named_bar_sync(1, kComputeWarps * 32);
-                if (tid == 0) {
-                    __threadfence();  // cumulative: publishes the CTA's partial writes
-                    const uint32_t prev = atomicAdd(&a.done[cur_qslot], 1u);
-                    s.flag = (prev + 1 == qs.count);
-                    if (s.flag) __threadfence();
+                // the state buffer is free again
+                __syncwarp();
+                if (lane == 0) {
+                    s.mcnt = 0;
+                    __threadfence_block();
+                    *reinterpret_cast<volatile uint32_t*>(&s.mgen) = item_seq;
                 }
-                named_bar_sync(1, kComputeWarps * 32);
-                if (s.flag) {
-                    // last partial of this query slot: LSE combine (Alg. 2)
+                if (qs.count == 1) {
 #pragma unroll
                     for (int e0 = 0; e0 < PER; ++e0) {
-                        const int e = tid + e0 * kComputeWarps * 32;
-                        if (e >= NOUT) break;
-                        const int h = e / D;
-                        float M = -INFINITY;
-                        for (uint32_t i = 0; i < qs.count; ++i)
-                            M = fmaxf(M, __ldcg(a.part_ml + (size_t)(qs.base + i) * 8 + h));
-                        float O = 0.f, Ls = 0.f;
-                        for (uint32_t i = 0; i < qs.count; ++i) {
-                            const size_t iti = qs.base + i;
-                            const float wt = fast_exp2(__ldcg(a.part_ml + iti * 8 + h) - M);
-                            O = fmaf(__ldcg(a.part_O + iti * NOUT + e), wt, O);
-                            Ls = fmaf(__ldcg(a.part_ml + iti * 8 + 4 + h), wt, Ls);
-                        }
+                        const int e = lane + 32 * e0, h = e / D;
+                        const float L = h == 0 ? lh[0] : h == 1 ? lh[1] : h == 2 ? lh[2] : lh[3];
                         const uint32_t head = hc * kHeadsPerSlot + h;
-                        if (head < a.G) a.out[((size_t)g * a.G + head) * D + (e % D)] = O / Ls;
+                        if (head < a.G) a.out[((size_t)g * a.G + head) * D + e % D] = resO[e0] / L;
                     }
-                    if (tid == 0) a.done[cur_qslot] = 0;
+                } else {
+                    float* pO = a.part_O + (size_t)cur_item * NOUT;
+#pragma unroll
+                    for (int e0 = 0; e0 < PER; ++e0) pO[lane + 32 * e0] = resO[e0];
+                    if (lane < 4) {
+                        a.part_ml[(size_t)cur_item * 8 + lane] = lane == 0 ? mh[0] : lane == 1 ? mh[1] : lane == 2 ? mh[2] : mh[3];
+                        a.part_ml[(size_t)cur_item * 8 + 4 + lane] = lane == 0 ? lh[0] : lane == 1 ? lh[1] : lane == 2 ? lh[2] : lh[3];
+                    }
+                    __syncwarp();
+                    uint32_t lastp = 0;
+                    if (lane == 0) {
+                        __threadfence();  // cumulative: publishes the warp's partial writes
+                        lastp = atomicAdd(&a.done[cur_qslot], 1u) + 1 == qs.count;
+                        if (lastp) __threadfence();
+                    }
+                    lastp = __shfl_sync(0xFFFFFFFFu, lastp, 0);
+                    if (lastp) {
+                        // last partial of this query slot: LSE combine (Alg. 2)
+                        float M4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, L4[4] = {0.f, 0.f, 0.f, 0.f};
+                        for (uint32_t i = 0; i < qs.count; ++i)
+#pragma unroll
+                            for (int h = 0; h < 4; ++h)
+                                M4[h] = fmaxf(M4[h], __ldcg(a.part_ml + (size_t)(qs.base + i) * 8 + h));
+                        for (uint32_t i = 0; i < qs.count; ++i)
+#pragma unroll
+                            for (int h = 0; h < 4; ++h)
+                                L4[h] = fmaf(__ldcg(a.part_ml + (size_t)(qs.base + i) * 8 + 4 + h),
+                                             fast_exp2(__ldcg(a.part_ml + (size_t)(qs.base + i) * 8 + h) - M4[h]), L4[h]);
+#pragma unroll
+                        for (int e0 = 0; e0 < PER; ++e0) {
+                            const int e = lane + 32 * e0, h = e / D;
+                            const float M = h == 0 ? M4[0] : h == 1 ? M4[1] : h == 2 ? M4[2] : M4[3];
+                            const float L = h == 0 ? L4[0] : h == 1 ? L4[1] : h == 2 ? L4[2] : L4[3];
+                            float O = 0.f;
+                            for (uint32_t i = 0; i < qs.count; ++i) {
+                                const size_t iti = qs.base + i;
+                                O = fmaf(__ldcg(a.part_O + iti * NOUT + e),
+                                         fast_exp2(__ldcg(a.part_ml + iti * 8 + h) - M), O);
+                            }
+                            const uint32_t head = hc * kHeadsPerSlot + h;
+                            if (head < a.G) a.out[((size_t)g * a.G + head) * D + (e % D)] = O / L;
+                        }
+                        if (lane == 0) a.done[cur_qslot] = 0;
+                    }
                 }
             }
-            named_bar_sync(1, kComputeWarps * 32);
         }
         if (++stage == CF::NS) {
             stage = 0;
