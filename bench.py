@@ -410,6 +410,12 @@ def ours(a):
         _, dms, dn = ctx.timing()
         dense_attn_ms = dms / max(dn, 1)
     ctx.enable_timing(False)
+    plan_trace = None
+    if os.environ.get("SAAP_PLAN_TRACE"):
+        import ctypes as ct
+        buf = (ct.c_uint64 * 8)()
+        if sb.lib().saap_debug_plan_trace(ctx.h, buf) == 0:
+            plan_trace = list(buf)
 
     # ---- counters, quality vs dense
     keys_scored = []
@@ -499,6 +505,7 @@ def ours(a):
         "clocks": clk,
         "gpu_launches": 2 * a.steps,
         "prefill_build_ms_per_layer": round(float(np.mean(t_build)), 2),
+        "plan_trace_cycles": plan_trace,
         "prefill": {
             "keys": n_keys_prefill, "assign_ms": round(assign_ms, 3), "pack_ms": round(pack_ms, 3),
             "keys_per_s": round(n_keys_prefill / ((assign_ms + pack_ms) * 1e-3), 1),

@@ -187,6 +187,14 @@ SAAP_API int saap_sparse_attention_dev(saap_ctx* ctx, const saap_layer* L,
                               const saap_sparse_cfg* cfg, float* out_dev,
                               saap_attn_stats* stats_dev, uint32_t* selected_dev);
 
+/* attention_mass_coverage(q_roped, store, selected, dense) for every group
+ *                                            attention.cpp:427-462
+ * q [n_groups x G x dim] f32, selected [n_groups x l]; out[n_groups] (key
+ * recall of the routed buckets: share of the non-window softmax mass). */
+SAAP_API int saap_attention_mass_coverage(saap_ctx* ctx, const saap_layer* L, const float* q_roped,
+                                          uint64_t G, const uint32_t* selected, uint64_t l,
+                                          uint64_t sink, uint64_t recent, double* out);
+
 /* full_attention(q, keys, values) over each group's whole context, from the
  * layer's packed cache (permutation-invariant)     attention.cpp:163-195 */
 SAAP_API int saap_layer_full_attention(saap_ctx* ctx, const saap_layer* L, const float* q,

@@ -487,6 +487,17 @@ class Layer:
                                                C.byref(c), _dptr(out), _dptr(stats),
                                                _dptr(selected)))
 
+    def coverage(self, q_roped, selected, dense: DenseWindow):
+        """attention_mass_coverage per group (attention.cpp:427-462)."""
+        q = _f32(q_roped)
+        sel = np.ascontiguousarray(selected, np.uint32).reshape(self.n_groups, -1)
+        out = np.empty(self.n_groups, np.float64)
+        _check(lib().saap_attention_mass_coverage(self.ctx.h, self.h, _p(q), _u64(q.shape[1]),
+                                                  _p(sel), _u64(sel.shape[1]),
+                                                  _u64(dense.sink_count), _u64(dense.recent_count),
+                                                  _p(out)))
+        return out
+
     def full_attention(self, q):
         q = _f32(q)
         out = np.empty_like(q)
@@ -556,6 +567,14 @@ def full_attention(q_group, keys, values, ctx: Optional[Context] = None) -> np.n
     _check(lib().saap_full_attention(ctx.h, _p(q), _u64(q.shape[0]), _p(k), _p(v),
                                      _u64(k.shape[0]), _u64(k.shape[1]), _p(out)))
     return out
+
+
+def attention_mass_coverage(q_group_roped, store: ContextStore, selected_buckets,
+                            dense: DenseWindow) -> float:
+    """Share of non-window softmax mass in the selected buckets, mean over
+    rows (attention.cpp:427-462) — the key recall of a routing decision."""
+    return float(store.coverage(_f32(q_group_roped)[None], np.asarray(selected_buckets,
+                                                                      np.uint32)[None], dense)[0])
 
 
 def selectivity(result: AttnResult, n_keys: int) -> float:

@@ -64,6 +64,7 @@ struct PlanArgs {
     const uint32_t* cand_i;
     const float* approx;         // centroid router, C <= 1024: fp32 scores [groups][C]
     const float* const* centT;   // per group d x C f32 centroids (exact re-scoring)
+    const float* const* centR;   // per group C x d f32 centroids (row-major)
     const float* cmax;           // per group max centroid norm
     unsigned long long* trace;   // debug: clock64 per planning phase (CTA 0)
     int route_only;              // BucketRouter::select: write `selected`, plan nothing

@@ -24,8 +24,12 @@ void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t 
 void launch_pack(int D, const TileDesc* tiles, uint32_t n_tiles, const uint32_t* tile_first,
                  uint32_t n_groups, const GroupMeta* meta, const uint32_t* assign, uint32_t C,
                  uint32_t* hist, uint32_t* countA, uint32_t* off, uint32_t* offA, uint32_t* idx,
-                 uint32_t* invA, const uint16_t* Ksrc, const uint16_t* Vsrc,
+                 uint32_t* invA, uint32_t* posA, const uint16_t* Ksrc, const uint16_t* Vsrc,
                  const uint64_t* src_row0, uint16_t* Kdst, uint16_t* Vdst, cudaStream_t st);
+void launch_coverage(const GroupMeta* meta, uint32_t n_groups, const uint16_t* K,
+                     const uint32_t* posA, const uint32_t* assign, const float* q, uint32_t G,
+                     uint32_t D, const uint32_t* sel, uint32_t l, uint32_t C, uint32_t recent,
+                     double* out, cudaStream_t st);
 void launch_f32_to_bf16(const float* in, uint16_t* out, uint64_t n, cudaStream_t st);
 void launch_derope(const float* x, const double* cs, uint64_t rows, uint32_t D, float* out,
                    cudaStream_t st);
@@ -214,15 +218,18 @@ void bind_routers(saap_layer* L, const saap_router* const* routers, int& mode, i
     if (rs == L->cached_routers) return;
     if (L->ctx->capturing) invalid("router set changed during graph capture");
     if (kind == 0) {
-        std::vector<const float*> p(L->n_groups);
+        std::vector<const float*> p(L->n_groups), pr(L->n_groups);
         std::vector<float> cm(L->n_groups);
         for (size_t g = 0; g < p.size(); ++g) {
             p[g] = rs[g]->part->centT;
+            pr[g] = rs[g]->part->cent;
             cm[g] = rs[g]->part->cmax;
         }
         if (!L->d_centT) L->d_centT = (const float**)(dmalloc<void*>(L->n_groups));
+        if (!L->d_centR) L->d_centR = (const float**)(dmalloc<void*>(L->n_groups));
         if (!L->d_cmax) L->d_cmax = dmalloc<float>(L->n_groups);
         SAAP_CUDA(cudaMemcpy(L->d_centT, p.data(), p.size() * sizeof(void*), cudaMemcpyHostToDevice));
+        SAAP_CUDA(cudaMemcpy(L->d_centR, pr.data(), pr.size() * sizeof(void*), cudaMemcpyHostToDevice));
         SAAP_CUDA(cudaMemcpy(L->d_cmax, cm.data(), cm.size() * 4, cudaMemcpyHostToDevice));
     } else {
         std::vector<const double*> p(3 * L->n_groups);
@@ -276,9 +283,9 @@ RouteGeo route_geo(uint64_t C, uint64_t probes) {
 void enqueue_route_score(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C, uint64_t G,
                          uint64_t probes, int mode, const float* const* centT,
                          const float* q_route, const double* probs, PlanArgs& pa,
-                         const float* cmax = nullptr) {
+                         const float* cmax = nullptr, const float* const* centR = nullptr) {
     const RouteGeo geo = route_geo(C, probes);
-    const bool approx = mode == 1 && C <= kPlanThreads && cmax != nullptr;
+    const bool approx = mode == 1 && C <= kPlanThreads && cmax != nullptr && centR != nullptr;
     double* cs = (double*)ensure(c, c->cand_s, n_groups * geo.n_cand * sizeof(double));
     uint32_t* ci = (uint32_t*)ensure(c, c->cand_i, n_groups * geo.n_cand * sizeof(uint32_t));
     RouteArgs ra{};
@@ -299,6 +306,7 @@ void enqueue_route_score(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
         ra.approx = (float*)ensure(c, c->approx, n_groups * C * sizeof(float));
         pa.approx = ra.approx;
         pa.centT = centT;
+        pa.centR = centR;
         pa.cmax = cmax;
     }
     launch_route_score(ra, (uint32_t)n_groups, c->stream);
@@ -352,7 +360,8 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const float* co
                     const double* const* qm, const float* q_roped, const float* q_route,
                     uint64_t G, uint64_t probes, uint64_t recent, float* out,
                     saap_attn_stats* stats, uint32_t* selected, uint32_t item_tiles,
-                    uint32_t qm_hidden = 0, const float* cmax = nullptr) {
+                    uint32_t qm_hidden = 0, const float* cmax = nullptr,
+                    const float* const* centR = nullptr) {
     const cudaStream_t st = c->stream;
     const uint64_t n_groups = src.n_groups, D = src.D, C = src.C;
     const uint64_t n_hchunks = (G + kHeadsPerSlot - 1) / kHeadsPerSlot;
@@ -423,7 +432,8 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const float* co
         SAAP_CUDA(cudaEventRecord(e0, st));
     }
     if ((mode == 1 || mode == 2) && probes > 0)
-        enqueue_route_score(c, n_groups, D, C, G, probes, mode, centT, q_route, probs, pa, cmax);
+        enqueue_route_score(c, n_groups, D, C, G, probes, mode, centT, q_route, probs, pa, cmax,
+                            centR);
     static const bool trace_on = std::getenv("SAAP_PLAN_TRACE") != nullptr;
     if (trace_on) pa.trace = (unsigned long long*)ensure(c, c->trace, 64);
     launch_route_plan(pa, (uint32_t)n_groups, st);
@@ -752,14 +762,15 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
     h2d(dq, q_route, G * d * 4, st);
     uint32_t* dsel = (uint32_t*)ensure(c, c->sel, l * 4);
     GroupMeta gm{0, 0, 2, 0, 0, 0};  // n > sink + recent so routing runs
-    GroupMeta* dmeta = (GroupMeta*)ensure(c, c->misc, sizeof(GroupMeta) + 2 * sizeof(void*) * 3 + 16);
+    GroupMeta* dmeta = (GroupMeta*)ensure(c, c->misc, sizeof(GroupMeta) + sizeof(void*) * 4 + 16);
     void** dptr = reinterpret_cast<void**>(reinterpret_cast<char*>(dmeta) + sizeof(GroupMeta));
-    float* dcmax = reinterpret_cast<float*>(dptr + 3);
-    void* ptrs[3];
+    float* dcmax = reinterpret_cast<float*>(dptr + 4);
+    void* ptrs[4] = {nullptr, nullptr, nullptr, nullptr};
     int mode;
     double* probs = nullptr;
     if (r->kind == 0) {
         ptrs[0] = (void*)r->part->centT;
+        ptrs[3] = (void*)r->part->cent;
         mode = 1;
     } else {
         ptrs[0] = (void*)r->model->w1;
@@ -769,7 +780,7 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
         probs = (double*)ensure(c, c->probs, G * C * 8);
     }
     h2d(dmeta, &gm, sizeof gm, st);
-    h2d(dptr, ptrs, sizeof(void*) * 3, st);
+    h2d(dptr, ptrs, sizeof(void*) * 4, st);
     if (r->kind == 0) h2d(dcmax, &r->part->cmax, 4, st);
     if (mode == 2) {
         QModelArgs qa{};
@@ -798,7 +809,8 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
     pa.route_only = 1;
     pa.selected = dsel;
     enqueue_route_score(c, 1, d, C, G, l, mode, (const float* const*)dptr, dq, probs, pa,
-                        r->kind == 0 ? dcmax : nullptr);
+                        r->kind == 0 ? dcmax : nullptr,
+                        r->kind == 0 ? (const float* const*)(dptr + 3) : nullptr);
     launch_route_plan(pa, 1, st);
     c->launches++;
     d2h(out, dsel, l * 4, st);
@@ -905,7 +917,7 @@ int saap_build_ivf(saap_ctx* c, const uint32_t* assignment, uint64_t n, uint64_t
                     (GroupMeta*)(b + o_meta), (uint32_t*)(b + o_as), (uint32_t)C,
                     (uint32_t*)(b + o_hist), (uint32_t*)(b + o_cA), (uint32_t*)(b + o_off),
                     (uint32_t*)(b + o_offA), (uint32_t*)(b + o_idx), (uint32_t*)(b + o_inv),
-                    nullptr, nullptr, nullptr, nullptr, nullptr, st);
+                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st);
         c->launches += 3;
         std::vector<uint32_t> off32(C + 1), idx32(n);
         d2h(off32.data(), b + o_off, (C + 1) * 4, st);
@@ -982,6 +994,7 @@ int saap_layer_create(saap_ctx* c, uint64_t n_groups, uint64_t d, uint64_t C,
         L->assign = dmalloc<uint32_t>(ns);
         L->idx = dmalloc<uint32_t>(ns);
         L->invA = dmalloc<uint32_t>(ns);
+        L->posA = dmalloc<uint32_t>(ns);
         L->off = dmalloc<uint32_t>(n_groups * (C + 1));
         L->offA = dmalloc<uint32_t>(n_groups * (C + 1));
         std::vector<TileDesc> tiles;
@@ -1025,6 +1038,7 @@ int saap_layer_destroy(saap_layer* L) {
         dfree(L->assign);
         dfree(L->idx);
         dfree(L->invA);
+        dfree(L->posA);
         dfree(L->gK);
         dfree(L->gV);
         delete (DecodeMaps*)L->maps;
@@ -1046,6 +1060,7 @@ int saap_layer_destroy(saap_layer* L) {
         dfree(L->tc_refine_count);
         if (L->tc_tiles) cudaFree(L->tc_tiles);
         dfree(L->d_centT);
+        dfree(L->d_centR);
         dfree(L->d_cmax);
         dfree(L->d_qm);
         delete L;
@@ -1168,7 +1183,7 @@ static void build_from_device(saap_layer* L, const uint16_t* Ksrc, const uint16_
     if (timed) SAAP_CUDA(cudaEventRecord(L->bev[1], st));
     launch_pack((int)L->d, L->tiles, L->n_tiles, L->tile_first, (uint32_t)L->n_groups, L->meta,
                 L->assign, (uint32_t)L->C, L->hist, L->countA, L->off, L->offA, L->idx, L->invA,
-                Ksrc, Vsrc, L->row_base, L->K, L->V, st);
+                L->posA, Ksrc, Vsrc, L->row_base, L->K, L->V, st);
     c->launches += 5;
     if (timed) SAAP_CUDA(cudaEventRecord(L->bev[2], st));
     L->built = true;
@@ -1361,7 +1376,7 @@ static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* con
     const DecodeSrc src = layer_src(L, cfg->recent_count, need_gather);
     enqueue_decode(c, src, mode, L->d_centT, L->d_qm, qr, q_route, G, cfg->probes,
                    cfg->recent_count, out, stats, selected, kItemTilesSparse, (uint32_t)hq,
-                   mode == 1 ? L->d_cmax : nullptr);
+                   mode == 1 ? L->d_cmax : nullptr, mode == 1 ? L->d_centR : nullptr);
 }
 
 int saap_sparse_attention_dev(saap_ctx* c, const saap_layer* L, const saap_router* const* routers,
@@ -1405,6 +1420,35 @@ int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* c
         d2h(out, dout, qn * 4, st);
         if (stats) d2h(stats, dst, L->n_groups * sizeof(saap_attn_stats), st);
         if (selected && cfg->probes) d2h(selected, dsel, L->n_groups * cfg->probes * 4, st);
+        sync(c);
+    });
+}
+
+int saap_attention_mass_coverage(saap_ctx* c, const saap_layer* L, const float* q_roped,
+                                 uint64_t G, const uint32_t* selected, uint64_t l, uint64_t sink,
+                                 uint64_t recent, double* out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(L, "layer");
+        if (!L->built) invalid("store not built");
+        if (sink != L->sink)
+            invalid("coverage: window sinks " + std::to_string(sink) +
+                    " keys but the store indexes from id " + std::to_string(L->sink));
+        for (uint64_t i = 0; i < L->n_groups * l; ++i)
+            if (selected[i] >= L->C) invalid("coverage: bucket id out of range");
+        if (G == 0) invalid("coverage: empty query group");
+        const cudaStream_t st = c->stream;
+        const uint64_t qn = L->n_groups * G * L->d;
+        float* dq = (float*)ensure(c, c->qr, qn * 4);
+        uint32_t* dsel = (uint32_t*)ensure(c, c->sel, std::max<uint64_t>(L->n_groups * l, 1) * 4);
+        double* dout = (double*)ensure(c, c->out, L->n_groups * 8);
+        h2d(dq, q_roped, qn * 4, st);
+        h2d(dsel, selected, L->n_groups * l * 4, st);
+        launch_coverage(L->meta, (uint32_t)L->n_groups, L->K, L->posA, L->assign, dq, (uint32_t)G,
+                        (uint32_t)L->d, dsel, (uint32_t)l, (uint32_t)L->C,
+                        (uint32_t)std::min<uint64_t>(recent, 0xFFFFFFFFull), dout, st);
+        c->launches++;
+        d2h(out, dout, L->n_groups * 8, st);
         sync(c);
     });
 }

@@ -200,6 +200,7 @@ struct saap_layer {
     uint32_t* assign = nullptr;  // total_ns
     uint32_t* idx = nullptr;     // total_ns (local ids, ascending within bucket)
     uint32_t* invA = nullptr;    // total_ns: position-sink -> packed row (region A)
+    uint32_t* posA = nullptr;    // total_ns: packed row-sink -> position (region A)
     uint32_t* off = nullptr;     // n_groups x (C+1)
     uint32_t* offA = nullptr;    // n_groups x (C+1)
     bool built = false;
@@ -230,6 +231,7 @@ struct saap_layer {
     // routing parameter table cache (device arrays of per-group pointers)
     std::vector<const saap_router*> cached_routers;
     const float** d_centT = nullptr;   // per group centT
+    const float** d_centR = nullptr;   // per group row-major centroids
     float* d_cmax = nullptr;           // per group partition cmax
     const double** d_qm = nullptr;     // per group: w1, w2, vec (3 pointers)
     // decode: TMA maps over the packed cache (+ gather buffer), built lazily

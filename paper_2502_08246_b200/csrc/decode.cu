@@ -266,8 +266,12 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         // approx) ranks below L others exactly; the rest are re-scored with
         // the reference's fp64 chain (attention.cpp:296-304) and sorted exactly.
         __shared__ double pooled[128];
-        __shared__ float s_thr;
+        __shared__ uint32_t hist[256];
+        __shared__ uint32_t s_pref, s_need, s_ncand;
         __shared__ double s_n2[32];
+        constexpr uint32_t kMaxCand = 64;
+        __shared__ float crow[kMaxCand][129];  // candidate centroid rows (padded)
+        __shared__ uint32_t cand_id[kMaxCand];
         const float* q = a.q_route + (size_t)g * a.G * a.D;
         double part = 0.0;
         for (uint32_t j = tid; j < a.D; j += nth) {
@@ -278,36 +282,100 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         }
         for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, o);
         if ((tid & 31) == 0) s_n2[tid >> 5] = part;
-        float av = -INFINITY;
-        uint32_t aid = 0xFFFFFFFFu;
-        if (tid < Cb) {
-            av = a.approx[(size_t)g * Cb + tid];
-            aid = tid;
+        const float av = tid < Cb ? a.approx[(size_t)g * Cb + tid] : -INFINITY;
+        const uint32_t u = __float_as_uint(av);
+        const uint32_t key = (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // order-preserving
+        // radix select (MSB first, 8-bit digits): the L-th largest key
+        if (tid == 0) {
+            s_pref = 0;
+            s_need = L;
         }
-        bitonic_regs_f(av, aid, a.P2, reinterpret_cast<float*>(ss), si);
-        trace(1);
-        if (tid == L - 1) s_thr = av;
-        __syncthreads();
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            if (tid < 256) hist[tid] = 0;
+            __syncthreads();
+            const uint32_t pref = s_pref;
+            const uint32_t hmask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
+            if (tid < Cb && (key & hmask) == (pref & hmask)) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+            __syncthreads();
+            if (tid < 32) {
+                // bins high -> low: lane owns bins 255-8*lane .. 248-8*lane
+                uint32_t cnt[8], tot = 0;
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    cnt[b] = hist[255 - 8 * tid - b];
+                    tot += cnt[b];
+                }
+                uint32_t incl = tot;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (tid >= (uint32_t)o) incl += v;
+                }
+                const uint32_t need = s_need, before = incl - tot;
+                if (before < need && incl >= need) {
+                    uint32_t run = before;
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        if (run + cnt[b] >= need) {
+                            s_pref = pref | ((uint32_t)(255 - 8 * tid - b) << shift);
+                            s_need = need - run;
+                            break;
+                        }
+                        run += cnt[b];
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        const uint32_t tk = s_pref;
+        const float t_l = __uint_as_float((tk & 0x80000000u) ? (tk & 0x7FFFFFFFu) : ~tk);
         double n2 = 0.0;
         for (uint32_t w = 0; w < nth / 32; ++w) n2 += s_n2[w];
         const float B2 = (float)(2.0 * 0x1p-16 * sqrt(n2) * (double)a.cmax[g]) * 1.0001f;
-        const bool cand = tid < Cb && av >= s_thr - B2;
-        const uint32_t nS = __syncthreads_count(cand);
+        // candidates: approx >= t_L - 2B (a superset of the exact top-L)
+        if (tid == 0) s_ncand = 0;
+        __syncthreads();
+        const bool cand = tid < Cb && av >= t_l - B2;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, cand);
+        uint32_t wbase = 0;
+        if ((tid & 31) == 0 && bal) wbase = atomicAdd(&s_ncand, __popc(bal));
+        wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
+        const uint32_t slot = wbase + __popc(bal & ((1u << (tid & 31)) - 1));
+        if (cand && slot < kMaxCand) cand_id[slot] = tid;
+        __syncthreads();
+        const uint32_t nS = s_ncand;
+        trace(1);
         double ex = -INFINITY;
         uint32_t eid = 0xFFFFFFFFu;
-        if (tid < nS) {
-            const float* cT = a.centT[g];
-            double sx = 0.0;
+        if (nS <= kMaxCand) {
+            // stage the candidates' centroid rows (coalesced) and run the chains from smem
+            const float* cr = a.centR[g];
+            for (uint32_t e = tid; e < nS * a.D; e += nth) {
+                const uint32_t r = e / a.D, jj = e % a.D;
+                crow[r][jj] = cr[(size_t)cand_id[r] * a.D + jj];
+            }
+            __syncthreads();
+            if (tid < nS) {
+                double sx = 0.0;
 #pragma unroll 8
-            for (uint32_t j = 0; j < a.D; ++j)
-                sx = __dadd_rn(sx, __dmul_rn(pooled[j], (double)cT[(size_t)j * Cb + aid]));
-            ex = sx;
-            eid = aid;
+                for (uint32_t j = 0; j < a.D; ++j) sx = __dadd_rn(sx, __dmul_rn(pooled[j], (double)crow[tid][j]));
+                ex = sx;
+                eid = cand_id[tid];
+            }
+        } else {
+            // degenerate (many near-ties): exact chains for every candidate, rank by position
+            if (cand) {
+                const float* cT = a.centT[g];
+                double sx = 0.0;
+#pragma unroll 8
+                for (uint32_t j = 0; j < a.D; ++j) sx = __dadd_rn(sx, __dmul_rn(pooled[j], (double)cT[(size_t)j * Cb + tid]));
+                ex = sx;
+                eid = tid;
+            }
         }
         uint32_t p2s = 1;
-        while (p2s < nS) p2s <<= 1;
+        while (p2s < (nS <= kMaxCand ? nS : Cb)) p2s <<= 1;
         trace(2);
-        bitonic_regs(ex, eid, p2s, ss, si);
+        bitonic_regs(ex, eid, nS <= kMaxCand ? p2s : a.P2, ss, si);
         __syncthreads();
         if (tid < L) si[tid] = eid;
         for (uint32_t w = tid; w < bm_words; w += nth) bitmap[w] = 0;
@@ -589,8 +657,9 @@ struct DecodeSmem2 {
     uint64_t empty[CF::NS];
     int4 meta[CF::NS];    // item, tile-in-item | last<<31, qslot, nq (q heads loaded)
     uint4 valid[CF::NS];  // 128-bit row validity mask
-    uint32_t mcnt;  // warps that deposited their state for the current item
-    uint32_t mgen;  // items merged so far
+    uint64_t st_full;   // 8 consumer warps deposited an item's (m, l, O) states
+    uint64_t st_empty;  // merge warp has read them
+    uint32_t st_item, st_qslot;
 };
 
 // swizzled byte offset of (row, 16-byte chunk) inside one tile half
@@ -638,7 +707,7 @@ __device__ __forceinline__ float bf16_round(float x) {
 }
 
 template <int D>
-__global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
+__global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
         decode_kernel(const __grid_constant__ DecodeMaps maps, DecodeArgs a) {
     using CF = DecodeCfg<D>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -650,8 +719,8 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
             mbar_init(&s.full[i], 1);
             mbar_init(&s.empty[i], kComputeWarps);
         }
-        s.mcnt = 0;
-        s.mgen = 0;
+        mbar_init(&s.st_full, kComputeWarps);
+        mbar_init(&s.st_empty, 1);
         fence_mbar_init();
     }
     // gap rows of a tile are masked (p = 0) but still enter the PV MMA: start
@@ -662,6 +731,99 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
     __syncthreads();
 
     const uint32_t n_items = *reinterpret_cast<volatile uint32_t*>(&a.ctr->n_items);
+
+    if (warp == kComputeWarps + 1) {
+        // ------------------------------------------------ merge warp
+        // LSE-merges the 8 consumer warps' states of each finished item and
+        // publishes it (output row, or a partial + the query slot's combine),
+        // off the consumers' critical path.
+        constexpr int NOUT = kHeadsPerSlot * D;
+        constexpr int PER = NOUT / 32;
+        uint32_t ph = 0;
+        for (;;) {
+            mbar_wait(&s.st_full, ph);
+            const uint32_t cur_item = s.st_item, cur_qslot = s.st_qslot;
+            if (cur_item == 0xFFFFFFFFu) break;
+            const QSlot qs = a.qslots[cur_qslot];
+            const uint32_t g = cur_qslot / a.n_hchunks, hc = cur_qslot % a.n_hchunks;
+            float mh[4], lh[4], resO[PER];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                float M = -INFINITY;
+#pragma unroll
+                for (int w = 0; w < kComputeWarps; ++w) M = fmaxf(M, s.redm[w][h]);
+                float Ls = 0.f;
+#pragma unroll
+                for (int w = 0; w < kComputeWarps; ++w)
+                    Ls = fmaf(s.redl[w][h], fast_exp2(s.redm[w][h] - M), Ls);
+                mh[h] = M;
+                lh[h] = Ls;
+            }
+#pragma unroll
+            for (int e0 = 0; e0 < PER; ++e0) {
+                const int e = lane + 32 * e0, h = e / D, d = e % D;
+                const float M = h == 0 ? mh[0] : h == 1 ? mh[1] : h == 2 ? mh[2] : mh[3];
+                float O = 0.f;
+#pragma unroll
+                for (int w = 0; w < kComputeWarps; ++w) O = fmaf(s.redO[w][h][d], fast_exp2(s.redm[w][h] - M), O);
+                resO[e0] = O;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.st_empty);  // state buffer free
+            ph ^= 1;
+            if (qs.count == 1) {
+#pragma unroll
+                for (int e0 = 0; e0 < PER; ++e0) {
+                    const int e = lane + 32 * e0, h = e / D;
+                    const float Lh = h == 0 ? lh[0] : h == 1 ? lh[1] : h == 2 ? lh[2] : lh[3];
+                    const uint32_t head = hc * kHeadsPerSlot + h;
+                    if (head < a.G) a.out[((size_t)g * a.G + head) * D + e % D] = resO[e0] / Lh;
+                }
+                continue;
+            }
+            float* pO = a.part_O + (size_t)cur_item * NOUT;
+#pragma unroll
+            for (int e0 = 0; e0 < PER; ++e0) pO[lane + 32 * e0] = resO[e0];
+            if (lane < 4) {
+                a.part_ml[(size_t)cur_item * 8 + lane] = lane == 0 ? mh[0] : lane == 1 ? mh[1] : lane == 2 ? mh[2] : mh[3];
+                a.part_ml[(size_t)cur_item * 8 + 4 + lane] = lane == 0 ? lh[0] : lane == 1 ? lh[1] : lane == 2 ? lh[2] : lh[3];
+            }
+            __syncwarp();
+            uint32_t lastp = 0;
+            if (lane == 0) {
+                __threadfence();  // cumulative: publishes the warp's partial writes
+                lastp = atomicAdd(&a.done[cur_qslot], 1u) + 1 == qs.count;
+                if (lastp) __threadfence();
+            }
+            lastp = __shfl_sync(0xFFFFFFFFu, lastp, 0);
+            if (!lastp) continue;
+            // last partial of this query slot: LSE combine (Alg. 2)
+            float M4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, L4[4] = {0.f, 0.f, 0.f, 0.f};
+            for (uint32_t i = 0; i < qs.count; ++i)
+#pragma unroll
+                for (int h = 0; h < 4; ++h) M4[h] = fmaxf(M4[h], __ldcg(a.part_ml + (size_t)(qs.base + i) * 8 + h));
+            for (uint32_t i = 0; i < qs.count; ++i)
+#pragma unroll
+                for (int h = 0; h < 4; ++h)
+                    L4[h] = fmaf(__ldcg(a.part_ml + (size_t)(qs.base + i) * 8 + 4 + h),
+                                 fast_exp2(__ldcg(a.part_ml + (size_t)(qs.base + i) * 8 + h) - M4[h]), L4[h]);
+#pragma unroll
+            for (int e0 = 0; e0 < PER; ++e0) {
+                const int e = lane + 32 * e0, h = e / D;
+                const float M = h == 0 ? M4[0] : h == 1 ? M4[1] : h == 2 ? M4[2] : M4[3];
+                const float Lh = h == 0 ? L4[0] : h == 1 ? L4[1] : h == 2 ? L4[2] : L4[3];
+                float O = 0.f;
+                for (uint32_t i = 0; i < qs.count; ++i) {
+                    const size_t iti = qs.base + i;
+                    O = fmaf(__ldcg(a.part_O + iti * NOUT + e), fast_exp2(__ldcg(a.part_ml + iti * 8 + h) - M), O);
+                }
+                const uint32_t head = hc * kHeadsPerSlot + h;
+                if (head < a.G) a.out[((size_t)g * a.G + head) * D + (e % D)] = O / Lh;
+            }
+            if (lane == 0) a.done[cur_qslot] = 0;
+        }
+        return;
+    }
 
     if (warp == kComputeWarps) {
         // ------------------------------------------------ producer
@@ -801,13 +963,20 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
     uint32_t qa[CF::KSTEPS][4];  // A fragments of [q1; q2; q3; 0]
     float o[CF::NT][4];
     float m_run = -INFINITY, l_run = 0.f;
-    uint32_t cur_item = 0, cur_qslot = 0, item_seq = 0;
+    uint32_t cur_item = 0, cur_qslot = 0, st_ph = 0;
 
     uint32_t stage = 0, phase = 0;
     for (;;) {
         mbar_wait(&s.full[stage], phase);
         const int4 mt = s.meta[stage];
-        if (mt.x < 0) break;
+        if (mt.x < 0) {
+            // stop the merge warp once it has drained the last item
+            mbar_wait(&s.st_empty, st_ph ^ 1);
+            if (warp == 0 && lane == 0) s.st_item = 0xFFFFFFFFu;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.st_full);
+            break;
+        }
         const uint32_t tile_in_item = (uint32_t)mt.y & 0x7FFFFFFFu;
         const bool last = ((uint32_t)mt.y >> 31) != 0;
         if (tile_in_item == 0) {
@@ -915,132 +1084,36 @@ __global__ void __launch_bounds__((kComputeWarps + 1) * 32, 1)
         if (lane == 0) mbar_arrive(&s.empty[stage]);
 
         if (last) {
-            // ---- item done.  Each warp deposits its (m, l, O) state; the last
-            // warp to arrive merges the eight states and publishes the item
-            // while the other warps stream on.  s.mgen counts merged items, so
-            // a warp never overwrites a state buffer that is still being read.
-            ++item_seq;
-            if (item_seq > 1) {
-                if (lane == 0)
-                    while (*reinterpret_cast<volatile uint32_t*>(&s.mgen) < item_seq - 1) __nanosleep(32);
-                __syncwarp();
-            }
+            // ---- item done: deposit this warp's (m, l, O) state for the merge warp
             float lw = l_run;
             lw += __shfl_xor_sync(0xFFFFFFFFu, lw, 1);
             lw += __shfl_xor_sync(0xFFFFFFFFu, lw, 2);
-            // O rows: lanes < 16 hold p1 (c[0..1]) + p3 (c[2..3]); lanes >= 16 hold p2
+            float xo[CF::NT][2];
 #pragma unroll
             for (int n = 0; n < CF::NT; ++n) {
+                // lanes < 16 hold p1 (c[0..1]) + p3 (c[2..3]); lanes >= 16 hold p2
                 float x0 = o[n][0] + (upper ? 0.f : o[n][2]);
                 float x1 = o[n][1] + (upper ? 0.f : o[n][3]);
-                x0 += __shfl_xor_sync(0xFFFFFFFFu, x0, 16);
-                x1 += __shfl_xor_sync(0xFFFFFFFFu, x1, 16);
-                if (!upper) {
-                    s.redO[warp][hq][n * 8 + 2 * tig] = x0;
-                    s.redO[warp][hq][n * 8 + 2 * tig + 1] = x1;
+                xo[n][0] = x0 + __shfl_xor_sync(0xFFFFFFFFu, x0, 16);
+                xo[n][1] = x1 + __shfl_xor_sync(0xFFFFFFFFu, x1, 16);
+            }
+            mbar_wait(&s.st_empty, st_ph ^ 1);  // previous item's states consumed
+            if (!upper) {
+#pragma unroll
+                for (int n = 0; n < CF::NT; ++n)
+                    *reinterpret_cast<float2*>(&s.redO[warp][hq][n * 8 + 2 * tig]) = make_float2(xo[n][0], xo[n][1]);
+                if (tig == 0) {
+                    s.redm[warp][hq] = m_run;
+                    s.redl[warp][hq] = lw;
                 }
             }
-            if (!upper && tig == 0) {
-                s.redm[warp][hq] = m_run;
-                s.redl[warp][hq] = lw;
+            if (warp == 0 && lane == 0) {
+                s.st_item = cur_item;
+                s.st_qslot = cur_qslot;
             }
             __syncwarp();
-            uint32_t merger = 0;
-            if (lane == 0) {
-                __threadfence_block();
-                merger = atomicAdd(&s.mcnt, 1u) == kComputeWarps - 1;
-                if (merger) __threadfence_block();
-            }
-            merger = __shfl_sync(0xFFFFFFFFu, merger, 0);
-            if (merger) {
-                const QSlot qs = a.qslots[cur_qslot];
-                const uint32_t g = cur_qslot / a.n_hchunks, hc = cur_qslot % a.n_hchunks;
-                constexpr int NOUT = kHeadsPerSlot * D;
-                constexpr int PER = NOUT / 32;
-                float resO[PER];
-                float mh[4], lh[4];
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    float M = -INFINITY;
-#pragma unroll
-                    for (int w = 0; w < kComputeWarps; ++w) M = fmaxf(M, s.redm[w][h]);
-                    float Ls = 0.f;
-#pragma unroll
-                    for (int w = 0; w < kComputeWarps; ++w) Ls = fmaf(s.redl[w][h], fast_exp2(s.redm[w][h] - M), Ls);
-                    mh[h] = M;
-                    lh[h] = Ls;
-                }
-#pragma unroll
-                for (int e0 = 0; e0 < PER; ++e0) {
-                    const int e = lane + 32 * e0, h = e / D, d = e % D;
-                    const float M = h == 0 ? mh[0] : h == 1 ? mh[1] : h == 2 ? mh[2] : mh[3];
-                    float O = 0.f;
-#pragma unroll
-                    for (int w = 0; w < kComputeWarps; ++w)
-                        O = fmaf(s.redO[w][h][d], fast_exp2(s.redm[w][h] - M), O);
-                    resO[e0] = O;
-                }
-                // the state buffer is free again
-                __syncwarp();
-                if (lane == 0) {
-                    s.mcnt = 0;
-                    __threadfence_block();
-                    *reinterpret_cast<volatile uint32_t*>(&s.mgen) = item_seq;
-                }
-                if (qs.count == 1) {
-#pragma unroll
-                    for (int e0 = 0; e0 < PER; ++e0) {
-                        const int e = lane + 32 * e0, h = e / D;
-                        const float L = h == 0 ? lh[0] : h == 1 ? lh[1] : h == 2 ? lh[2] : lh[3];
-                        const uint32_t head = hc * kHeadsPerSlot + h;
-                        if (head < a.G) a.out[((size_t)g * a.G + head) * D + e % D] = resO[e0] / L;
-                    }
-                } else {
-                    float* pO = a.part_O + (size_t)cur_item * NOUT;
-#pragma unroll
-                    for (int e0 = 0; e0 < PER; ++e0) pO[lane + 32 * e0] = resO[e0];
-                    if (lane < 4) {
-                        a.part_ml[(size_t)cur_item * 8 + lane] = lane == 0 ? mh[0] : lane == 1 ? mh[1] : lane == 2 ? mh[2] : mh[3];
-                        a.part_ml[(size_t)cur_item * 8 + 4 + lane] = lane == 0 ? lh[0] : lane == 1 ? lh[1] : lane == 2 ? lh[2] : lh[3];
-                    }
-                    __syncwarp();
-                    uint32_t lastp = 0;
-                    if (lane == 0) {
-                        __threadfence();  // cumulative: publishes the warp's partial writes
-                        lastp = atomicAdd(&a.done[cur_qslot], 1u) + 1 == qs.count;
-                        if (lastp) __threadfence();
-                    }
-                    lastp = __shfl_sync(0xFFFFFFFFu, lastp, 0);
-                    if (lastp) {
-                        // last partial of this query slot: LSE combine (Alg. 2)
-                        float M4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, L4[4] = {0.f, 0.f, 0.f, 0.f};
-                        for (uint32_t i = 0; i < qs.count; ++i)
-#pragma unroll
-                            for (int h = 0; h < 4; ++h)
-                                M4[h] = fmaxf(M4[h], __ldcg(a.part_ml + (size_t)(qs.base + i) * 8 + h));
-                        for (uint32_t i = 0; i < qs.count; ++i)
-#pragma unroll
-                            for (int h = 0; h < 4; ++h)
-                                L4[h] = fmaf(__ldcg(a.part_ml + (size_t)(qs.base + i) * 8 + 4 + h),
-                                             fast_exp2(__ldcg(a.part_ml + (size_t)(qs.base + i) * 8 + h) - M4[h]), L4[h]);
-#pragma unroll
-                        for (int e0 = 0; e0 < PER; ++e0) {
-                            const int e = lane + 32 * e0, h = e / D;
-                            const float M = h == 0 ? M4[0] : h == 1 ? M4[1] : h == 2 ? M4[2] : M4[3];
-                            const float L = h == 0 ? L4[0] : h == 1 ? L4[1] : h == 2 ? L4[2] : L4[3];
-                            float O = 0.f;
-                            for (uint32_t i = 0; i < qs.count; ++i) {
-                                const size_t iti = qs.base + i;
-                                O = fmaf(__ldcg(a.part_O + iti * NOUT + e),
-                                         fast_exp2(__ldcg(a.part_ml + iti * 8 + h) - M), O);
-                            }
-                            const uint32_t head = hc * kHeadsPerSlot + h;
-                            if (head < a.G) a.out[((size_t)g * a.G + head) * D + (e % D)] = O / L;
-                        }
-                        if (lane == 0) a.done[cur_qslot] = 0;
-                    }
-                }
-            }
+            if (lane == 0) mbar_arrive(&s.st_full);
+            st_ph ^= 1;
         }
         if (++stage == CF::NS) {
             stage = 0;
@@ -1059,7 +1132,7 @@ static void launch_decode_t(const DecodeMaps& m, const DecodeArgs& a, int grid, 
                                        (int)smem));
         configured = true;
     }
-    decode_kernel<D><<<grid, (kComputeWarps + 1) * 32, smem, st>>>(m, a);
+    decode_kernel<D><<<grid, (kComputeWarps + 2) * 32, smem, st>>>(m, a);
     SAAP_CUDA(cudaGetLastError());
 }
 
@@ -1091,12 +1164,13 @@ void launch_route_plan(const PlanArgs& a, uint32_t n_groups, cudaStream_t st) {
     size_t smem = 0;
     if (route) smem = (size_t)std::max<uint32_t>(a.P2, kPlanThreads) * 12 + ((a.C + 31) / 32) * 4 + 16;
     smem += (size_t)(a.probes + 8) * (sizeof(Seg) + 4);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
+    static bool configured = false;  // static smem (~36 KB) + dynamic can exceed 48 KB
+    if (!configured) {
         SAAP_CUDA(cudaFuncSetAttribute(route_plan_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024));
+        configured = true;
     }
+    if (smem > 180 * 1024) fail(SAAP_ERR_UNSUPPORTED, "route_plan: too many buckets/probes for one CTA");
     route_plan_kernel<<<n_groups, kPlanThreads, smem, st>>>(a);
     SAAP_CUDA(cudaGetLastError());
 }

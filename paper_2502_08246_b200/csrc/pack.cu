@@ -197,8 +197,8 @@ template <int D>
 __global__ void __launch_bounds__(128) scatter_kernel(
         const TileDesc* tiles, uint32_t n_tiles, const GroupMeta* meta, const uint32_t* assign,
         uint32_t C, uint32_t* hist, const uint32_t* off, const uint32_t* offA, uint32_t* idx,
-        uint32_t* invA, const uint16_t* Ksrc, const uint16_t* Vsrc, const uint64_t* src_row0,
-        uint16_t* Kdst, uint16_t* Vdst) {
+        uint32_t* invA, uint32_t* posA, const uint16_t* Ksrc, const uint16_t* Vsrc,
+        const uint64_t* src_row0, uint16_t* Kdst, uint16_t* Vdst) {
     const uint32_t warp_g = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const uint32_t lane = threadIdx.x & 31;
     if (warp_g >= n_tiles) return;
@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(128) scatter_kernel(
             if (pos < gm.T) {
                 row = gm.sink + oAg[c] + r;
                 invA[gm.ivf_base + lid] = row;
+                if (posA) posA[gm.ivf_base + (row - gm.sink)] = pos;
             } else {
                 row = pos;
             }
@@ -295,6 +296,116 @@ __global__ void derope_kernel(const float* x, const double* cs, uint64_t rows, u
     }
 }
 
+// ------------------------------------------------------------ coverage
+// attention_mass_coverage (attention.cpp:427-462): per query row, the share of
+// softmax(q k / sqrt(d)) mass over non-window keys [lo, hi) that falls in the
+// selected buckets; mean over the rows.  One CTA per context walks its packed
+// rows once (positions via posA / identity) with an online (max, denom, hit)
+// per row, merged across threads in shared memory.
+constexpr int kCovRows = 8;  // query rows per pass
+__global__ void __launch_bounds__(256) coverage_kernel(const GroupMeta* meta, const uint16_t* K,
+                                                       const uint32_t* posA, const uint32_t* assign,
+                                                       const float* q, uint32_t G, uint32_t D,
+                                                       const uint32_t* sel, uint32_t l, uint32_t C,
+                                                       uint32_t recent, double* out) {
+    extern __shared__ float csm[];  // q rows (kCovRows x D) then bitmap (C/32 words)
+    __shared__ float red[3][kCovRows][8];
+    const uint32_t g = blockIdx.x, tid = threadIdx.x;
+    const GroupMeta gm = meta[g];
+    const uint32_t lo = min(gm.sink, gm.n);
+    uint32_t hi = gm.n > recent ? gm.n - recent : 0;
+    if (hi < lo) hi = lo;
+    if (lo == hi) {
+        if (tid == 0) out[g] = 1.0;  // nothing outside the window
+        return;
+    }
+    uint32_t* bitmap = reinterpret_cast<uint32_t*>(csm + kCovRows * D);
+    for (uint32_t w = tid; w < (C + 31) / 32; w += blockDim.x) bitmap[w] = 0;
+    __syncthreads();
+    for (uint32_t b = tid; b < l; b += blockDim.x) {
+        const uint32_t c = sel[(size_t)g * l + b];
+        atomicOr(&bitmap[c >> 5], 1u << (c & 31));
+    }
+    const float scale = 1.4426950408889634f / sqrtf((float)D);  // exp2 domain
+    double total = 0.0;
+    for (uint32_t r0 = 0; r0 < G; r0 += kCovRows) {
+        const uint32_t nr = min((uint32_t)kCovRows, G - r0);
+        __syncthreads();
+        for (uint32_t e = tid; e < nr * D; e += blockDim.x)
+            csm[e] = q[((size_t)g * G + r0) * D + e] * scale;
+        __syncthreads();
+        float m[kCovRows], den[kCovRows], hit[kCovRows];
+#pragma unroll
+        for (int i = 0; i < kCovRows; ++i) {
+            m[i] = -INFINITY;
+            den[i] = 0.f;
+            hit[i] = 0.f;
+        }
+        for (uint32_t r = gm.sink + tid; r < gm.n; r += blockDim.x) {
+            const uint32_t pos = r < gm.T ? posA[gm.ivf_base + (r - gm.sink)] : r;
+            if (pos < lo || pos >= hi) continue;
+            const uint32_t c = assign[gm.ivf_base + (pos - gm.sink)];
+            const bool picked = (bitmap[c >> 5] >> (c & 31)) & 1u;
+            const uint16_t* kr = K + (gm.row_base + r) * D;
+#pragma unroll
+            for (int i = 0; i < kCovRows; ++i) {
+                if ((uint32_t)i >= nr) break;
+                float sc = 0.f;
+                for (uint32_t j = 0; j < D; j += 2) {
+                    const uint32_t kk = *reinterpret_cast<const uint32_t*>(kr + j);
+                    sc = fmaf(csm[i * D + j], bf16lo(kk), sc);
+                    sc = fmaf(csm[i * D + j + 1], bf16hi(kk), sc);
+                }
+                if (sc > m[i]) {
+                    const float a = exp2f(m[i] - sc);
+                    den[i] *= a;
+                    hit[i] *= a;
+                    m[i] = sc;
+                }
+                const float p = exp2f(sc - m[i]);
+                den[i] += p;
+                if (picked) hit[i] += p;
+            }
+        }
+        // block merge of (m, den, hit) per row: warp shuffles then shared memory
+        const uint32_t lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+        for (int i = 0; i < kCovRows; ++i) {
+            for (int o = 16; o; o >>= 1) {
+                const float om = __shfl_xor_sync(0xFFFFFFFFu, m[i], o);
+                const float od = __shfl_xor_sync(0xFFFFFFFFu, den[i], o);
+                const float oh = __shfl_xor_sync(0xFFFFFFFFu, hit[i], o);
+                const float M = fmaxf(m[i], om);
+                const float a = M == -INFINITY ? 0.f : exp2f(m[i] - M), b = M == -INFINITY ? 0.f : exp2f(om - M);
+                den[i] = den[i] * a + od * b;
+                hit[i] = hit[i] * a + oh * b;
+                m[i] = M;
+            }
+            if (lane == 0) {
+                red[0][i][warp] = m[i];
+                red[1][i][warp] = den[i];
+                red[2][i][warp] = hit[i];
+            }
+        }
+        __syncthreads();
+        if (tid < nr) {
+            float M = -INFINITY;
+            for (uint32_t w = 0; w < blockDim.x / 32; ++w) M = fmaxf(M, red[0][tid][w]);
+            double dn = 0.0, ht = 0.0;
+            for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+                const double a = red[0][tid][w] == -INFINITY ? 0.0 : exp2((double)red[0][tid][w] - M);
+                dn += red[1][tid][w] * a;
+                ht += red[2][tid][w] * a;
+            }
+            red[0][tid][0] = (float)(ht / dn);
+        }
+        __syncthreads();
+        if (tid == 0)
+            for (uint32_t i = 0; i < nr; ++i) total += red[0][i][0];
+    }
+    if (tid == 0) out[g] = total / (double)G;
+}
+
 // ------------------------------------------------------------ launchers
 void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t n_tiles,
                          const void* keys, const uint64_t* key_row0, const double* const* cent64,
@@ -320,7 +431,7 @@ void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t 
 void launch_pack(int D, const TileDesc* tiles, uint32_t n_tiles, const uint32_t* tile_first,
                  uint32_t n_groups, const GroupMeta* meta, const uint32_t* assign, uint32_t C,
                  uint32_t* hist, uint32_t* countA, uint32_t* off, uint32_t* offA, uint32_t* idx,
-                 uint32_t* invA, const uint16_t* Ksrc, const uint16_t* Vsrc,
+                 uint32_t* invA, uint32_t* posA, const uint16_t* Ksrc, const uint16_t* Vsrc,
                  const uint64_t* src_row0, uint16_t* Kdst, uint16_t* Vdst, cudaStream_t st) {
     const size_t hsm = (size_t)2 * C * 4;
     static size_t cfg_h = 0, cfg_s = 0;
@@ -342,8 +453,8 @@ void launch_pack(int D, const TileDesc* tiles, uint32_t n_tiles, const uint32_t*
 #define SAAP_SCATTER(DD)                                                                         \
     if (sgrid)                                                                                   \
         scatter_kernel<DD><<<sgrid, wpb * 32, 0, st>>>(tiles, n_tiles, meta, assign, C, hist, off, \
-                                                       offA, idx, invA, Ksrc, Vsrc, src_row0,    \
-                                                       Kdst, Vdst);                              \
+                                                       offA, idx, invA, posA, Ksrc, Vsrc,        \
+                                                       src_row0, Kdst, Vdst);                    \
     if (Ksrc) copy_sink_kernel<DD><<<n_groups, 128, 0, st>>>(meta, n_groups, Ksrc, Vsrc, src_row0, \
                                                              Kdst, Vdst);
     switch (D) {
@@ -353,6 +464,15 @@ void launch_pack(int D, const TileDesc* tiles, uint32_t n_tiles, const uint32_t*
         default: fail(SAAP_ERR_UNSUPPORTED, "pack: unsupported head dim " + std::to_string(D));
     }
 #undef SAAP_SCATTER
+    SAAP_CUDA(cudaGetLastError());
+}
+
+void launch_coverage(const GroupMeta* meta, uint32_t n_groups, const uint16_t* K,
+                     const uint32_t* posA, const uint32_t* assign, const float* q, uint32_t G,
+                     uint32_t D, const uint32_t* sel, uint32_t l, uint32_t C, uint32_t recent,
+                     double* out, cudaStream_t st) {
+    const size_t smem = (size_t)kCovRows * D * 4 + ((C + 31) / 32) * 4;
+    coverage_kernel<<<n_groups, 256, smem, st>>>(meta, K, posA, assign, q, G, D, sel, l, C, recent, out);
     SAAP_CUDA(cudaGetLastError());
 }
 

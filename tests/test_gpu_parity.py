@@ -321,3 +321,28 @@ def test_long_context_128k(ctx, port):
                                  2047)
     _check_sparse(res, want)
     assert res.keys_scored < n // 5
+
+
+# ------------------------------------------------------------------ key recall
+@pytest.mark.parametrize("hint", [2047, 64, 5])
+def test_coverage_golden(ctx, g, hint):
+    part = sb.Partition(g["cent"], ctx)
+    st = sb.build_context_store(g["K"], g["V"], 5e5, part, 1, keys_deroped=g["Kd"], recent_hint=hint)
+    dense = sb.DenseWindow(1, 64)
+    got = [sb.attention_mass_coverage(g["qr"][:4], st, s, dense) for s in ([3, 7, 11], [], list(range(16)))]
+    assert np.allclose(got, g["cov"], rtol=1e-4, atol=1e-6)
+    with pytest.raises(sb.InvalidArgument, match="coverage: bucket id out of range"):
+        sb.attention_mass_coverage(g["qr"][:4], st, [16], dense)
+
+
+@pytest.mark.parametrize("hint,recent", [(2047, 2047), (300, 2047), (2047, 100), (0, 10**6)])
+def test_coverage_matches_oracle(ctx, port, hint, recent):
+    case = make_case(d=128, n=7000, C=128, seed=11)
+    a, off, idx = port_index(port, case, 128)
+    part = sb.Partition(case["cent"], ctx)
+    st = sb.build_context_store(case["K"], case["V"], 5e5, part, 1, keys_deroped=case["Kd"],
+                                recent_hint=hint)
+    sel = port.centroid_select(case["cent"], case["qd"][:4], 16)
+    got = sb.attention_mass_coverage(case["qr"][:4], st, sel, sb.DenseWindow(1, recent))
+    want = port.coverage(case["qr"][:4], case["K"], 1, a, 128, sel, recent)
+    assert abs(got - want) <= 1e-4 * max(1.0, abs(want))
