@@ -214,8 +214,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         const int t = warp >> 2, q4 = warp & 3;
         const int row = q4 * 32 + lane;
         const TcTile tt = a.tiles[blockIdx.x * NT + t];
-        float b1 = -INFINITY, b2 = -INFINITY, b3 = -INFINITY;
-        uint32_t i1 = 0, i2 = 0;
+        float b1 = -INFINITY, b2 = -INFINITY;
+        uint32_t i1 = 0;
         float n2 = 0.f;
         if ((uint32_t)row < tt.count) {
             const uint4* kp = reinterpret_cast<const uint4*>(a.keys + (a.key_row0[tt.group] + tt.lid0 + row) * KD);
@@ -236,20 +236,23 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             const uint32_t buf = j & 1, bph = (j >> 1) & 1;
             mbar_wait(&s.t_full[buf], bph);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const bool tail = (j + 1) * CN > a.C;
+            const uint32_t lim = (j + 1) * CN > a.C ? a.C - j * CN : CN;  // valid columns
 #pragma unroll 1
             for (int q = 0; q < CN / 32; ++q) {
                 float v[32];
                 tmem_ld32(taddr0 + buf * (NT * CN) + q * 32, v);
                 const uint32_t c0 = j * CN + q * 32;
+                if ((uint32_t)(q * 32 + 32) > lim) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if ((uint32_t)(q * 32 + i) >= lim) v[i] = -INFINITY;
+                }
+                // running best (value, lowest id) and second-best value
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                    const float x = (tail && c0 + i >= a.C) ? -INFINITY : v[i];
-                    const bool g1 = x > b1, g2 = x > b2;
-                    b3 = fmaxf(b3, fminf(x, b2));
-                    const float nb2 = g1 ? b1 : (g2 ? x : b2);
-                    i2 = g1 ? i1 : (g2 ? c0 + i : i2);
-                    b2 = nb2;
+                    const float x = v[i];
+                    b2 = fmaxf(b2, fminf(x, b1));
+                    const bool g1 = x > b1;
                     b1 = g1 ? x : b1;
                     i1 = g1 ? c0 + i : i1;
                 }
@@ -262,14 +265,12 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             const uint32_t lid = tt.lid0 + row;
             if (b1 - b2 > 2.f * bound) {
                 a.out[a.out_base[tt.group] + lid] = i1;
-            } else {
-                // ambiguous: the exact argmax is i1 or i2 when the third-best is
-                // out of range, else any centroid (full fp64 re-scan)
+            } else {  // ambiguous (near tie, exact tie, zero key): full fp64 re-scan
                 const uint32_t slot = atomicAdd(a.refine_count, 1u);
                 a.refine[4 * slot] = tt.group;
                 a.refine[4 * slot + 1] = lid;
                 a.refine[4 * slot + 2] = i1;
-                a.refine[4 * slot + 3] = (b1 - b3 > 2.f * bound) ? i2 : 0xFFFFFFFFu;
+                a.refine[4 * slot + 3] = 0xFFFFFFFFu;
             }
         }
     }

@@ -17,6 +17,8 @@ namespace saap_b200 {
 void launch_route_plan(const PlanArgs& a, uint32_t n_groups, cudaStream_t st);
 void launch_route_score(const RouteArgs& a, uint32_t n_groups, cudaStream_t st);
 void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st);
+void launch_combine(int D, const QSlot* qs, uint32_t n_qslots, uint32_t G, uint32_t n_hchunks,
+                    const float* pO, const float* pml, float* out, cudaStream_t st);
 void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st);
 void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t n_tiles,
                          const void* keys, const uint64_t* key_row0, const double* const* cent64,
@@ -24,8 +26,9 @@ void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t 
 void launch_pack(int D, const TileDesc* tiles, uint32_t n_tiles, const uint32_t* tile_first,
                  uint32_t n_groups, const GroupMeta* meta, const uint32_t* assign, uint32_t C,
                  uint32_t* hist, uint32_t* countA, uint32_t* off, uint32_t* offA, uint32_t* idx,
-                 uint32_t* invA, uint32_t* posA, const uint16_t* Ksrc, const uint16_t* Vsrc,
-                 const uint64_t* src_row0, uint16_t* Kdst, uint16_t* Vdst, cudaStream_t st);
+                 uint32_t* invA, uint32_t* posA, uint32_t* dst_row, uint64_t total_ns,
+                 const uint16_t* Ksrc, const uint16_t* Vsrc, const uint64_t* src_row0,
+                 uint16_t* Kdst, uint16_t* Vdst, cudaStream_t st);
 void launch_coverage(const GroupMeta* meta, uint32_t n_groups, const uint16_t* K,
                      const uint32_t* posA, const uint32_t* assign, const float* q, uint32_t G,
                      uint32_t D, const uint32_t* sel, uint32_t l, uint32_t C, uint32_t recent,
@@ -455,7 +458,8 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const float* co
     da.out = out;
     const int grid = (int)std::min<uint64_t>((uint64_t)c->sm_count, max_items);
     launch_decode((int)D, *src.maps, da, std::max(grid, 1), st);
-    c->launches++;
+    launch_combine((int)D, qs, (uint32_t)qslots, (uint32_t)G, (uint32_t)n_hchunks, pO, pml, out, st);
+    c->launches += 2;
     if (e2) {
         SAAP_CUDA(cudaEventRecord(e2, st));
         c->ev.insert(c->ev.end(), {e0, e1, e2});
@@ -917,7 +921,7 @@ int saap_build_ivf(saap_ctx* c, const uint32_t* assignment, uint64_t n, uint64_t
                     (GroupMeta*)(b + o_meta), (uint32_t*)(b + o_as), (uint32_t)C,
                     (uint32_t*)(b + o_hist), (uint32_t*)(b + o_cA), (uint32_t*)(b + o_off),
                     (uint32_t*)(b + o_offA), (uint32_t*)(b + o_idx), (uint32_t*)(b + o_inv),
-                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st);
+                    nullptr, nullptr, n, nullptr, nullptr, nullptr, nullptr, nullptr, st);
         c->launches += 3;
         std::vector<uint32_t> off32(C + 1), idx32(n);
         d2h(off32.data(), b + o_off, (C + 1) * 4, st);
@@ -995,6 +999,7 @@ int saap_layer_create(saap_ctx* c, uint64_t n_groups, uint64_t d, uint64_t C,
         L->idx = dmalloc<uint32_t>(ns);
         L->invA = dmalloc<uint32_t>(ns);
         L->posA = dmalloc<uint32_t>(ns);
+        L->list = dmalloc<uint32_t>(ns);  // per-key destination row (pack scratch)
         L->off = dmalloc<uint32_t>(n_groups * (C + 1));
         L->offA = dmalloc<uint32_t>(n_groups * (C + 1));
         std::vector<TileDesc> tiles;
@@ -1039,6 +1044,7 @@ int saap_layer_destroy(saap_layer* L) {
         dfree(L->idx);
         dfree(L->invA);
         dfree(L->posA);
+        dfree(L->list);
         dfree(L->gK);
         dfree(L->gV);
         delete (DecodeMaps*)L->maps;
@@ -1183,8 +1189,8 @@ static void build_from_device(saap_layer* L, const uint16_t* Ksrc, const uint16_
     if (timed) SAAP_CUDA(cudaEventRecord(L->bev[1], st));
     launch_pack((int)L->d, L->tiles, L->n_tiles, L->tile_first, (uint32_t)L->n_groups, L->meta,
                 L->assign, (uint32_t)L->C, L->hist, L->countA, L->off, L->offA, L->idx, L->invA,
-                L->posA, Ksrc, Vsrc, L->row_base, L->K, L->V, st);
-    c->launches += 5;
+                L->posA, L->list, L->total_ns, Ksrc, Vsrc, L->row_base, L->K, L->V, st);
+    c->launches += 6;
     if (timed) SAAP_CUDA(cudaEventRecord(L->bev[2], st));
     L->built = true;
 }

@@ -201,6 +201,7 @@ struct saap_layer {
     uint32_t* idx = nullptr;     // total_ns (local ids, ascending within bucket)
     uint32_t* invA = nullptr;    // total_ns: position-sink -> packed row (region A)
     uint32_t* posA = nullptr;    // total_ns: packed row-sink -> position (region A)
+    uint32_t* list = nullptr;    // total_ns: packing scratch (destination row per key)
     uint32_t* off = nullptr;     // n_groups x (C+1)
     uint32_t* offA = nullptr;    // n_groups x (C+1)
     bool built = false;

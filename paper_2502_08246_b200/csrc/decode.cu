@@ -788,39 +788,7 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
                 a.part_ml[(size_t)cur_item * 8 + lane] = lane == 0 ? mh[0] : lane == 1 ? mh[1] : lane == 2 ? mh[2] : mh[3];
                 a.part_ml[(size_t)cur_item * 8 + 4 + lane] = lane == 0 ? lh[0] : lane == 1 ? lh[1] : lane == 2 ? lh[2] : lh[3];
             }
-            __syncwarp();
-            uint32_t lastp = 0;
-            if (lane == 0) {
-                __threadfence();  // cumulative: publishes the warp's partial writes
-                lastp = atomicAdd(&a.done[cur_qslot], 1u) + 1 == qs.count;
-                if (lastp) __threadfence();
-            }
-            lastp = __shfl_sync(0xFFFFFFFFu, lastp, 0);
-            if (!lastp) continue;
-            // last partial of this query slot: LSE combine (Alg. 2)
-            float M4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, L4[4] = {0.f, 0.f, 0.f, 0.f};
-            for (uint32_t i = 0; i < qs.count; ++i)
-#pragma unroll
-                for (int h = 0; h < 4; ++h) M4[h] = fmaxf(M4[h], __ldcg(a.part_ml + (size_t)(qs.base + i) * 8 + h));
-            for (uint32_t i = 0; i < qs.count; ++i)
-#pragma unroll
-                for (int h = 0; h < 4; ++h)
-                    L4[h] = fmaf(__ldcg(a.part_ml + (size_t)(qs.base + i) * 8 + 4 + h),
-                                 fast_exp2(__ldcg(a.part_ml + (size_t)(qs.base + i) * 8 + h) - M4[h]), L4[h]);
-#pragma unroll
-            for (int e0 = 0; e0 < PER; ++e0) {
-                const int e = lane + 32 * e0, h = e / D;
-                const float M = h == 0 ? M4[0] : h == 1 ? M4[1] : h == 2 ? M4[2] : M4[3];
-                const float Lh = h == 0 ? L4[0] : h == 1 ? L4[1] : h == 2 ? L4[2] : L4[3];
-                float O = 0.f;
-                for (uint32_t i = 0; i < qs.count; ++i) {
-                    const size_t iti = qs.base + i;
-                    O = fmaf(__ldcg(a.part_O + iti * NOUT + e), fast_exp2(__ldcg(a.part_ml + iti * 8 + h) - M), O);
-                }
-                const uint32_t head = hc * kHeadsPerSlot + h;
-                if (head < a.G) a.out[((size_t)g * a.G + head) * D + (e % D)] = O / Lh;
-            }
-            if (lane == 0) a.done[cur_qslot] = 0;
+            // multi-item query slots are combined by combine_kernel after this launch
         }
         return;
     }
@@ -1122,7 +1090,46 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
     }
 }
 
+// ============================================================ LSE combine (Alg. 2)
+// One CTA per query slot with > 1 item: O = sum_i O_i 2^(m_i - M) / sum_i l_i 2^(m_i - M)
+// (merge_into / pattn_finalize, attention.cpp:102-161; Alg. 2).
+template <int D>
+__global__ void __launch_bounds__(kHeadsPerSlot * D) combine_kernel(const QSlot* qslots, uint32_t n_qslots,
+                                                                    uint32_t G, uint32_t n_hchunks,
+                                                                    const float* part_O, const float* part_ml,
+                                                                    float* out) {
+    constexpr int NOUT = kHeadsPerSlot * D;
+    const uint32_t qsi = blockIdx.x;
+    const QSlot qs = qslots[qsi];
+    if (qs.count <= 1) return;  // written directly by the decode kernel
+    const uint32_t e = threadIdx.x, h = e / D;
+    const uint32_t g = qsi / n_hchunks, hc = qsi % n_hchunks;
+    const uint32_t head = hc * kHeadsPerSlot + h;
+    float M = -INFINITY;
+    for (uint32_t i = 0; i < qs.count; ++i) M = fmaxf(M, part_ml[(size_t)(qs.base + i) * 8 + h]);
+    float O = 0.f, L = 0.f;
+#pragma unroll 4
+    for (uint32_t i = 0; i < qs.count; ++i) {
+        const size_t it = qs.base + i;
+        const float w = fast_exp2(part_ml[it * 8 + h] - M);
+        O = fmaf(part_O[it * NOUT + e], w, O);
+        L = fmaf(part_ml[it * 8 + 4 + h], w, L);
+    }
+    if (head < G) out[((size_t)g * G + head) * D + (e % D)] = O / L;
+}
+
 // ============================================================ launchers
+void launch_combine(int D, const QSlot* qs, uint32_t n_qslots, uint32_t G, uint32_t n_hchunks,
+                    const float* pO, const float* pml, float* out, cudaStream_t st) {
+    switch (D) {
+        case 128: combine_kernel<128><<<n_qslots, 4 * 128, 0, st>>>(qs, n_qslots, G, n_hchunks, pO, pml, out); break;
+        case 64: combine_kernel<64><<<n_qslots, 4 * 64, 0, st>>>(qs, n_qslots, G, n_hchunks, pO, pml, out); break;
+        case 32: combine_kernel<32><<<n_qslots, 4 * 32, 0, st>>>(qs, n_qslots, G, n_hchunks, pO, pml, out); break;
+        default: fail(SAAP_ERR_UNSUPPORTED, "combine: unsupported head dim");
+    }
+    SAAP_CUDA(cudaGetLastError());
+}
+
 template <int D>
 static void launch_decode_t(const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st) {
     const size_t smem = sizeof(DecodeSmem2<D>) + 1024;

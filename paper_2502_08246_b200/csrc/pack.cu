@@ -197,8 +197,7 @@ template <int D>
 __global__ void __launch_bounds__(128) scatter_kernel(
         const TileDesc* tiles, uint32_t n_tiles, const GroupMeta* meta, const uint32_t* assign,
         uint32_t C, uint32_t* hist, const uint32_t* off, const uint32_t* offA, uint32_t* idx,
-        uint32_t* invA, uint32_t* posA, const uint16_t* Ksrc, const uint16_t* Vsrc,
-        const uint64_t* src_row0, uint16_t* Kdst, uint16_t* Vdst) {
+        uint32_t* invA, uint32_t* posA, uint32_t* dst_row) {
     const uint32_t warp_g = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const uint32_t lane = threadIdx.x & 31;
     if (warp_g >= n_tiles) return;
@@ -207,8 +206,6 @@ __global__ void __launch_bounds__(128) scatter_kernel(
     uint32_t* ht = hist + (size_t)warp_g * C;
     const uint32_t* og = off + (size_t)td.group * (C + 1);
     const uint32_t* oAg = offA + (size_t)td.group * (C + 1);
-    constexpr int CH = D / 8;           // 16-byte chunks per row
-    constexpr int KPS = 32 / (2 * CH);  // keys per copy step (K and V chunks)
     for (uint32_t e0 = 0; e0 < td.count; e0 += 32) {
         const uint32_t e = e0 + lane;
         const bool act = e < td.count;
@@ -235,25 +232,51 @@ __global__ void __launch_bounds__(128) scatter_kernel(
                 row = pos;
             }
         }
+        if (act && dst_row) dst_row[gm.ivf_base + lid] = row;
         __syncwarp();
-        if (Ksrc) {
-            const uint32_t nk = min(32u, td.count - e0);
-            const uint64_t sbase = src_row0[td.group] + gm.sink + td.first + e0;
-            const uint64_t dbase = gm.row_base;
-            const int sub = lane / (2 * CH), ch = lane % (2 * CH);
-            const bool isv = ch >= CH;
-            const int cc = isv ? ch - CH : ch;
-#pragma unroll 4
-            for (uint32_t k0 = 0; k0 < 32; k0 += KPS) {
-                const uint32_t k = k0 + sub;
-                const uint32_t drow = __shfl_sync(0xFFFFFFFFu, row, k & 31);
-                if (k < nk) {
-                    const uint16_t* src = (isv ? Vsrc : Ksrc) + (sbase + k) * D + cc * 8;
-                    uint16_t* dst = (isv ? Vdst : Kdst) + (dbase + drow) * D + cc * 8;
-                    *reinterpret_cast<uint4*>(dst) = __ldcs(reinterpret_cast<const uint4*>(src));
-                }
+    }
+}
+
+// Streams K/V rows to their packed rows: consecutive threads move consecutive
+// 16-byte chunks of a row (coalesced 256-byte reads and writes), 4 chunks in
+// flight per thread.  dst_row comes from scatter_kernel.
+template <int D>
+__global__ void __launch_bounds__(256) move_rows_kernel(const GroupMeta* meta, const uint32_t* n_tile_group,
+                                                        uint32_t n_groups, uint64_t total_ns,
+                                                        const uint32_t* dst_row, const uint16_t* Ksrc,
+                                                        const uint16_t* Vsrc, const uint64_t* src_row0,
+                                                        uint16_t* Kdst, uint16_t* Vdst) {
+    constexpr uint32_t CH = D / 8;  // 16-byte chunks per row
+    const uint64_t n_chunks = total_ns * 2 * CH;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e0 < n_chunks; e0 += 4 * stride) {
+        uint4 v[4];
+        uint16_t* dst[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint64_t e = e0 + u * stride;
+            dst[u] = nullptr;
+            if (e >= n_chunks) continue;
+            const uint64_t key = e / (2 * CH);       // global ivf index
+            const uint32_t part = (uint32_t)(e % (2 * CH));
+            // group of this key: binary search over ivf_base (n_groups small)
+            uint32_t lo = 0, hi = n_groups;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (meta[mid].ivf_base <= key) lo = mid;
+                else hi = mid;
             }
+            const GroupMeta gm = meta[lo];
+            const uint64_t lid = key - gm.ivf_base;
+            const bool isv = part >= CH;
+            const uint32_t cc = isv ? part - CH : part;
+            const uint16_t* src = (isv ? Vsrc : Ksrc) + (src_row0[lo] + gm.sink + lid) * D + cc * 8;
+            v[u] = __ldcs(reinterpret_cast<const uint4*>(src));
+            dst[u] = (isv ? Vdst : Kdst) + (gm.row_base + dst_row[key]) * D + cc * 8;
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (dst[u]) __stcs(reinterpret_cast<uint4*>(dst[u]), v[u]);
     }
 }
 
@@ -431,8 +454,9 @@ void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t 
 void launch_pack(int D, const TileDesc* tiles, uint32_t n_tiles, const uint32_t* tile_first,
                  uint32_t n_groups, const GroupMeta* meta, const uint32_t* assign, uint32_t C,
                  uint32_t* hist, uint32_t* countA, uint32_t* off, uint32_t* offA, uint32_t* idx,
-                 uint32_t* invA, uint32_t* posA, const uint16_t* Ksrc, const uint16_t* Vsrc,
-                 const uint64_t* src_row0, uint16_t* Kdst, uint16_t* Vdst, cudaStream_t st) {
+                 uint32_t* invA, uint32_t* posA, uint32_t* dst_row, uint64_t total_ns,
+                 const uint16_t* Ksrc, const uint16_t* Vsrc, const uint64_t* src_row0,
+                 uint16_t* Kdst, uint16_t* Vdst, cudaStream_t st) {
     const size_t hsm = (size_t)2 * C * 4;
     static size_t cfg_h = 0, cfg_s = 0;
     if (hsm > 48 * 1024 && hsm > cfg_h) {
@@ -453,16 +477,13 @@ void launch_pack(int D, const TileDesc* tiles, uint32_t n_tiles, const uint32_t*
 #define SAAP_SCATTER(DD)                                                                         \
     if (sgrid)                                                                                   \
         scatter_kernel<DD><<<sgrid, wpb * 32, 0, st>>>(tiles, n_tiles, meta, assign, C, hist, off, \
-                                                       offA, idx, invA, posA, Ksrc, Vsrc,        \
-                                                       src_row0, Kdst, Vdst);                    \
+                                                       offA, idx, invA, posA,                    \
+                                                       Ksrc ? dst_row : nullptr);                \
+    if (Ksrc && total_ns)                                                                        \
+        move_rows_kernel<DD><<<148 * 16, 256, 0, st>>>(meta, nullptr, n_groups, total_ns, dst_row,  \
+                                                       Ksrc, Vsrc, src_row0, Kdst, Vdst);        \
     if (Ksrc) copy_sink_kernel<DD><<<n_groups, 128, 0, st>>>(meta, n_groups, Ksrc, Vsrc, src_row0, \
                                                              Kdst, Vdst);
-    switch (D) {
-        case 128: SAAP_SCATTER(128); break;
-        case 64: SAAP_SCATTER(64); break;
-        case 32: SAAP_SCATTER(32); break;
-        default: fail(SAAP_ERR_UNSUPPORTED, "pack: unsupported head dim " + std::to_string(D));
-    }
 #undef SAAP_SCATTER
     SAAP_CUDA(cudaGetLastError());
 }

@@ -31,7 +31,8 @@ METRICS = {
     "sm__cycles_elapsed.avg.per_second": "sm_clock_hz",
 }
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9,
-              "usecond": 1e-6, "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6}
+              "usecond": 1e-6, "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
+              "s": 1.0}
 
 
 def raw_rows(rep):
