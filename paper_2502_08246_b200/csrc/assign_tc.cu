@@ -14,9 +14,9 @@
 // reference's operation order by refine_kernel.  Result: bit-exact.
 //
 // CTA: 2 tiles of 128 keys (M=128 each) share every 128-centroid B chunk;
-// warp 4 issues TMA, warp 5 issues tcgen05.mma (one thread), warps 0-3 drain
-// TMEM (lane = key row) while the next chunk accumulates in the other half of
-// TMEM (2 x 256 columns).
+// warp 8 issues TMA, warp 9 issues tcgen05.mma (one thread), warps 0-7 drain
+// TMEM (warp w: tile w/4, lanes 32*(w%4).., lane = key row) while the next
+// chunk accumulates in the other half of TMEM (2 x 256 columns).
 #include <cuda.h>
 
 #include "args.cuh"
@@ -52,8 +52,8 @@ struct TcAssignArgs {
     uint32_t C;                // buckets
     uint32_t Cpad;             // C rounded up to CN
     uint32_t* out;
-    uint32_t* refine;          // (group, lid, best id, second id | ~0 for a full re-scan)
-    uint32_t* refine_count;
+    uint32_t* refine;          // per group (at out_base): local ids of ambiguous keys
+    uint32_t* refine_count;    // per group
     const uint16_t* keys;      // same tensor the map covers (for |k|)
 };
 
@@ -265,12 +265,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             const uint32_t lid = tt.lid0 + row;
             if (b1 - b2 > 2.f * bound) {
                 a.out[a.out_base[tt.group] + lid] = i1;
-            } else {  // ambiguous (near tie, exact tie, zero key): full fp64 re-scan
-                const uint32_t slot = atomicAdd(a.refine_count, 1u);
-                a.refine[4 * slot] = tt.group;
-                a.refine[4 * slot + 1] = lid;
-                a.refine[4 * slot + 2] = i1;
-                a.refine[4 * slot + 3] = 0xFFFFFFFFu;
+            } else {  // ambiguous (near tie, exact tie, zero key): fp64 re-scan
+                const uint32_t slot = atomicAdd(&a.refine_count[tt.group], 1u);
+                a.refine[a.out_base[tt.group] + slot] = lid;
             }
         }
     }
@@ -284,57 +281,89 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 
 // fp64 re-score of ambiguous keys in the reference's exact operation order
 // (sequential over d; products of bf16 keys and f32 centroids are exact, so
-// DFMA == mulsd+addsd).  One warp per key: two candidates -> lanes 0/1; full
-// re-scan -> lanes split the centroids, then a (score desc, id asc) reduction.
-template <int D>
-__device__ __forceinline__ double exact_dot(const uint16_t* kp, const double* cr) {
-    double s = 0.0;
-#pragma unroll 8
-    for (int j = 0; j < D; ++j) s = fma((double)__uint_as_float(((uint32_t)kp[j]) << 16), cr[j], s);
-    return s;
-}
+// DFMA == mulsd+addsd), batched per group so each centroid chunk staged in
+// shared memory serves RB keys.  CTA (y, g) takes batches y, y+Y, ... of
+// group g's list; thread t scores key t%RB against centroids t/RB + 8i of
+// each chunk (RC centroids), then a (score desc, id asc) reduction.
+namespace rf {
+constexpr int RB = 32;    // keys per batch
+constexpr int RC = 64;    // centroids per staged chunk
+constexpr int THREADS = 256;
+constexpr int PER = RC * RB / THREADS;  // chains per thread
+}  // namespace rf
 
 template <int D>
-__global__ void __launch_bounds__(256) refine_kernel(const uint32_t* list, const uint32_t* count,
-                                                     const uint16_t* keys,
-                                                     const uint64_t* key_row0,
-                                                     const double* const* cent64,
-                                                     const uint64_t* out_base, uint32_t C,
-                                                     uint32_t* out) {
-    const uint32_t n = *count;
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t e = wid; e < n; e += nw) {
-        const uint32_t g = list[4 * e], lid = list[4 * e + 1], c1 = list[4 * e + 2], c2 = list[4 * e + 3];
-        const uint16_t* kp = keys + (key_row0[g] + lid) * D;
-        const double* cg = cent64[g];
+__global__ void __launch_bounds__(rf::THREADS) refine_kernel(const uint32_t* list,
+                                                             const uint32_t* count,
+                                                             const uint16_t* keys,
+                                                             const uint64_t* key_row0,
+                                                             const double* const* cent64,
+                                                             const uint64_t* out_base, uint32_t C,
+                                                             uint32_t* out) {
+    using namespace rf;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    double* ks = reinterpret_cast<double*>(smem_raw);  // [RB][D+1]
+    double* cs = ks + RB * (D + 1);                     // [RC][D]
+    __shared__ double red_s[THREADS / RB][RB];
+    __shared__ uint32_t red_i[THREADS / RB][RB];
+    const uint32_t g = blockIdx.y;
+    const uint32_t n = count[g];
+    const uint32_t tid = threadIdx.x, kq = tid % RB, cw = tid / RB;
+    const double* cg = cent64[g];
+    const uint32_t* lg = list + out_base[g];
+    for (uint32_t b0 = blockIdx.x * RB; b0 < n; b0 += gridDim.x * RB) {
+        const uint32_t nb = min((uint32_t)RB, n - b0);
+        __syncthreads();
+        for (uint32_t e = tid; e < RB * D; e += THREADS) {
+            const uint32_t r = e / D, j = e % D;
+            double v = 0.0;
+            if (r < nb)
+                v = (double)__uint_as_float(((uint32_t)keys[(key_row0[g] + lg[b0 + r]) * D + j]) << 16);
+            ks[r * (D + 1) + j] = v;
+        }
         double best = -INFINITY;
         uint32_t bid = 0xFFFFFFFFu;
-        if (c2 != 0xFFFFFFFFu) {
-            if (lane < 2) {
-                const uint32_t c = lane ? c2 : c1;
-                best = exact_dot<D>(kp, cg + (size_t)c * D);
-                bid = c;
+        for (uint32_t c0 = 0; c0 < C; c0 += RC) {
+            const uint32_t nc = min((uint32_t)RC, C - c0);
+            __syncthreads();
+            for (uint32_t e = tid; e < (uint32_t)RC * D; e += THREADS)
+                cs[e] = e < nc * D ? cg[(size_t)c0 * D + e] : 0.0;
+            __syncthreads();
+            double acc[PER];
+#pragma unroll
+            for (int i = 0; i < PER; ++i) acc[i] = 0.0;
+            const double* kr = ks + kq * (D + 1);
+#pragma unroll 4
+            for (int j = 0; j < D; ++j) {
+                const double kv = kr[j];
+#pragma unroll
+                for (int i = 0; i < PER; ++i) acc[i] = fma(kv, cs[(cw + (THREADS / RB) * i) * D + j], acc[i]);
             }
-        } else {
-            for (uint32_t c = lane; c < C; c += 32) {
-                const double sc = exact_dot<D>(kp, cg + (size_t)c * D);
-                if (sc > best) {  // ascending c per lane: strict > keeps the lowest id
-                    best = sc;
-                    bid = c;
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {  // ascending centroid ids: strict > keeps the lowest
+                const uint32_t c = cw + (THREADS / RB) * i;
+                if (c < nc && acc[i] > best) {
+                    best = acc[i];
+                    bid = c0 + c;
                 }
             }
         }
-        for (int o = 16; o; o >>= 1) {
-            const double ob = __shfl_xor_sync(0xFFFFFFFFu, best, o);
-            const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, bid, o);
-            if (ob > best || (ob == best && oi < bid)) {
-                best = ob;
-                bid = oi;
+        red_s[cw][kq] = best;
+        red_i[cw][kq] = bid;
+        __syncthreads();
+        if (tid < nb) {
+            double bs = red_s[0][tid];
+            uint32_t bi = red_i[0][tid];
+            for (int w = 1; w < THREADS / RB; ++w) {
+                const double o = red_s[w][tid];
+                const uint32_t oi = red_i[w][tid];
+                if (o > bs || (o == bs && oi < bi)) {
+                    bs = o;
+                    bi = oi;
+                }
             }
+            out[out_base[g] + lg[b0 + tid]] = bi == 0xFFFFFFFFu ? 0u : bi;
         }
-        if (lane == 0) out[out_base[g] + lid] = bid;
     }
 }
 
@@ -444,9 +473,18 @@ void launch_assign_tc(const uint16_t* keys, uint64_t key_rows, const uint16_t* h
 
 void launch_refine(const uint32_t* list, const uint32_t* count, const uint16_t* keys,
                    const uint64_t* key_row0, const double* const* cent64, const uint64_t* out_base,
-                   uint32_t C, uint32_t* out, int sm_count, cudaStream_t st) {
-    refine_kernel<128><<<sm_count * 4, 256, 0, st>>>(list, count, keys, key_row0, cent64, out_base, C,
-                                                     out);
+                   uint32_t C, uint32_t* out, uint32_t n_groups, int sm_count, cudaStream_t st) {
+    using namespace rf;
+    const size_t smem = (size_t)(RB * (tc::KD + 1) + RC * tc::KD) * sizeof(double);
+    static bool configured = false;
+    if (!configured) {
+        SAAP_CUDA(cudaFuncSetAttribute(refine_kernel<tc::KD>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = true;
+    }
+    const uint32_t y = std::max<uint32_t>(1, (uint32_t)(2 * sm_count) / std::max<uint32_t>(n_groups, 1));
+    refine_kernel<tc::KD><<<dim3(y, n_groups), THREADS, smem, st>>>(list, count, keys, key_row0, cent64,
+                                                                 out_base, C, out);
     SAAP_CUDA(cudaGetLastError());
 }
 

@@ -62,7 +62,7 @@ void launch_assign_tc(const uint16_t* keys, uint64_t key_rows, const uint16_t* h
                       uint32_t n_tiles, cudaStream_t st);
 void launch_refine(const uint32_t* list, const uint32_t* count, const uint16_t* keys,
                    const uint64_t* key_row0, const double* const* cent64, const uint64_t* out_base,
-                   uint32_t C, uint32_t* out, int sm_count, cudaStream_t st);
+                   uint32_t C, uint32_t* out, uint32_t n_groups, int sm_count, cudaStream_t st);
 void launch_synth(uint16_t* out, uint64_t rows, uint32_t D, uint64_t seed, int kind,
                   const float* centers, uint64_t n_centers, float center_scale, float noise,
                   cudaStream_t st);
@@ -1145,10 +1145,10 @@ static void assign_tc_path(saap_layer* L, const uint16_t* keys) {
         L->tc_nslots = (uint32_t)slots.size();
     }
     if (!L->tc_refine) {
-        L->tc_refine = dmalloc<uint32_t>(4 * L->total_ns);
-        L->tc_refine_count = dmalloc<uint32_t>(1);
+        L->tc_refine = dmalloc<uint32_t>(std::max<uint64_t>(L->total_ns, 1));
+        L->tc_refine_count = dmalloc<uint32_t>(L->n_groups);
     }
-    SAAP_CUDA(cudaMemsetAsync(L->tc_refine_count, 0, 4, st));
+    SAAP_CUDA(cudaMemsetAsync(L->tc_refine_count, 0, L->n_groups * 4, st));
     TcAssignArgs args{};
     args.tiles = (const TcTile*)L->tc_tiles;
     args.key_row0 = L->key_row0;
@@ -1163,7 +1163,7 @@ static void assign_tc_path(saap_layer* L, const uint16_t* keys) {
     launch_assign_tc(keys, L->total_rows, L->tc_hi, L->tc_mid, L->tc_nslots, args, L->tc_n_tiles,
                      st);
     launch_refine(L->tc_refine, L->tc_refine_count, keys, L->key_row0, L->d_cent64, L->ivf_base,
-                  (uint32_t)L->C, L->assign, c->sm_count, st);
+                  (uint32_t)L->C, L->assign, (uint32_t)L->n_groups, c->sm_count, st);
     c->launches += 2;
     L->last_tc = true;
 }
@@ -1291,10 +1291,13 @@ int saap_layer_assign_info(saap_ctx* c, const saap_layer* L, int* used_tensor_co
     return guard([&] {
         DeviceGuard dg(c);
         need(L, "layer");
-        uint32_t n = 0;
+        uint64_t n = 0;
         if (L->last_tc) {
-            SAAP_CUDA(cudaMemcpyAsync(&n, L->tc_refine_count, 4, cudaMemcpyDeviceToHost, c->stream));
+            std::vector<uint32_t> cnt(L->n_groups);
+            SAAP_CUDA(cudaMemcpyAsync(cnt.data(), L->tc_refine_count, L->n_groups * 4,
+                                      cudaMemcpyDeviceToHost, c->stream));
             sync(c);
+            for (uint32_t x : cnt) n += x;
         }
         if (used_tensor_cores) *used_tensor_cores = L->last_tc ? 1 : 0;
         if (refined_keys) *refined_keys = n;

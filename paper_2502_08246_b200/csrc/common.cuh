@@ -220,8 +220,8 @@ struct saap_layer {
     uint16_t* tc_mid = nullptr;
     size_t tc_split_elems = 0;
     float* tc_cmax = nullptr;
-    uint32_t* tc_refine = nullptr;   // 4 * total_ns
-    uint32_t* tc_refine_count = nullptr;
+    uint32_t* tc_refine = nullptr;   // total_ns: per-group lists of ambiguous keys
+    uint32_t* tc_refine_count = nullptr;  // n_groups
     uint64_t* key_row0 = nullptr;    // per group: row_base + sink
     uint64_t* ivf_base = nullptr;    // per group
     uint64_t last_refined = 0;

@@ -484,6 +484,12 @@ void launch_pack(int D, const TileDesc* tiles, uint32_t n_tiles, const uint32_t*
                                                        Ksrc, Vsrc, src_row0, Kdst, Vdst);        \
     if (Ksrc) copy_sink_kernel<DD><<<n_groups, 128, 0, st>>>(meta, n_groups, Ksrc, Vsrc, src_row0, \
                                                              Kdst, Vdst);
+    switch (D) {
+        case 128: SAAP_SCATTER(128); break;
+        case 64: SAAP_SCATTER(64); break;
+        case 32: SAAP_SCATTER(32); break;
+        default: fail(SAAP_ERR_UNSUPPORTED, "pack: unsupported head dim " + std::to_string(D));
+    }
 #undef SAAP_SCATTER
     SAAP_CUDA(cudaGetLastError());
 }
