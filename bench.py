@@ -413,7 +413,7 @@ def ours(a):
     plan_trace = None
     if os.environ.get("SAAP_PLAN_TRACE"):
         import ctypes as ct
-        buf = (ct.c_uint64 * 8)()
+        buf = (ct.c_uint64 * 16)()
         if sb.lib().saap_debug_plan_trace(ctx.h, buf) == 0:
             plan_trace = list(buf)
 

@@ -35,7 +35,18 @@ struct RouteArgs {
     uint32_t slice, n_slices, keep;  // keep = min(probes, slice)
     double* cand_s;                // [groups][n_slices][keep]
     uint32_t* cand_i;
-    float* approx;                 // approx mode: [groups][C] fp32 scores, no selection here
+};
+// Routing, approximate stage (centroid router, C <= kPlanThreads): fp32
+// scores of every centroid for every context.  Contexts sharing one
+// partition (same KV head, different sequences) form a slot and share each
+// centroid load.
+struct ApproxArgs {
+    const float* const* centT;     // per group, d x C f32
+    const float* q_route;          // [groups][G][D]
+    const uint32_t* slot_off;      // [n_slots + 1] into slot_list; null: slot s = group s
+    const uint32_t* slot_list;     // groups by slot
+    uint32_t G, C;
+    float* approx;                 // [groups][C]
 };
 struct ItemRec {
     uint32_t qslot;

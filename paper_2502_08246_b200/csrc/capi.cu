@@ -14,7 +14,8 @@
 namespace saap_b200 {
 
 // ---- kernels (decode.cu / pack.cu / route.cu / synth.cu)
-void launch_route_plan(const PlanArgs& a, uint32_t n_groups, cudaStream_t st);
+void launch_route_plan(const PlanArgs& a, uint32_t n_groups, bool pdl, cudaStream_t st);
+void launch_route_approx(int D, const ApproxArgs& a, uint32_t n_slots, cudaStream_t st);
 void launch_route_score(const RouteArgs& a, uint32_t n_groups, cudaStream_t st);
 void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st);
 void launch_combine(int D, const QSlot* qs, uint32_t n_qslots, uint32_t G, uint32_t n_hchunks,
@@ -234,6 +235,24 @@ void bind_routers(saap_layer* L, const saap_router* const* routers, int& mode, i
         SAAP_CUDA(cudaMemcpy(L->d_centT, p.data(), p.size() * sizeof(void*), cudaMemcpyHostToDevice));
         SAAP_CUDA(cudaMemcpy(L->d_centR, pr.data(), pr.size() * sizeof(void*), cudaMemcpyHostToDevice));
         SAAP_CUDA(cudaMemcpy(L->d_cmax, cm.data(), cm.size() * 4, cudaMemcpyHostToDevice));
+        // slots: groups sharing one partition share the approximate scoring loads
+        std::vector<const saap_partition*> uniq;
+        std::vector<std::vector<uint32_t>> members;
+        for (size_t g = 0; g < rs.size(); ++g) {
+            auto it = std::find(uniq.begin(), uniq.end(), rs[g]->part);
+            if (it == uniq.end()) {
+                uniq.push_back(rs[g]->part);
+                members.emplace_back();
+                it = uniq.end() - 1;
+            }
+            members[it - uniq.begin()].push_back((uint32_t)g);
+        }
+        std::vector<uint32_t> tab{0};
+        for (auto& m : members) tab.push_back(tab.back() + (uint32_t)m.size());
+        for (auto& m : members) tab.insert(tab.end(), m.begin(), m.end());
+        if (!L->d_route_slots) L->d_route_slots = dmalloc<uint32_t>(2 * L->n_groups + 1);
+        SAAP_CUDA(cudaMemcpy(L->d_route_slots, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+        L->n_route_slots = (uint32_t)uniq.size();
     } else {
         std::vector<const double*> p(3 * L->n_groups);
         for (size_t g = 0; g < L->n_groups; ++g) {
@@ -286,7 +305,8 @@ RouteGeo route_geo(uint64_t C, uint64_t probes) {
 void enqueue_route_score(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C, uint64_t G,
                          uint64_t probes, int mode, const float* const* centT,
                          const float* q_route, const double* probs, PlanArgs& pa,
-                         const float* cmax = nullptr, const float* const* centR = nullptr) {
+                         const float* cmax = nullptr, const float* const* centR = nullptr,
+                         const uint32_t* slots = nullptr, uint32_t n_slots = 0) {
     const RouteGeo geo = route_geo(C, probes);
     const bool approx = mode == 1 && C <= kPlanThreads && cmax != nullptr && centR != nullptr;
     double* cs = (double*)ensure(c, c->cand_s, n_groups * geo.n_cand * sizeof(double));
@@ -306,13 +326,23 @@ void enqueue_route_score(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
     ra.cand_s = cs;
     ra.cand_i = ci;
     if (approx) {
-        ra.approx = (float*)ensure(c, c->approx, n_groups * C * sizeof(float));
-        pa.approx = ra.approx;
+        // fp32 scores of every centroid; the planner re-scores the boundary exactly
+        ApproxArgs aa{};
+        aa.centT = centT;
+        aa.q_route = q_route;
+        aa.slot_off = slots;
+        aa.slot_list = slots ? slots + n_slots + 1 : nullptr;
+        aa.G = (uint32_t)G;
+        aa.C = (uint32_t)C;
+        aa.approx = (float*)ensure(c, c->approx, n_groups * C * sizeof(float));
+        launch_route_approx((int)D, aa, slots ? n_slots : (uint32_t)n_groups, c->stream);
+        pa.approx = aa.approx;
         pa.centT = centT;
         pa.centR = centR;
         pa.cmax = cmax;
+    } else {
+        launch_route_score(ra, (uint32_t)n_groups, c->stream);
     }
-    launch_route_score(ra, (uint32_t)n_groups, c->stream);
     c->launches++;
     pa.P2 = approx ? next_pow2((uint32_t)C) : geo.P2;
     pa.n_cand = geo.n_cand;
@@ -364,7 +394,8 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const float* co
                     uint64_t G, uint64_t probes, uint64_t recent, float* out,
                     saap_attn_stats* stats, uint32_t* selected, uint32_t item_tiles,
                     uint32_t qm_hidden = 0, const float* cmax = nullptr,
-                    const float* const* centR = nullptr) {
+                    const float* const* centR = nullptr, const uint32_t* slots = nullptr,
+                    uint32_t n_slots = 0) {
     const cudaStream_t st = c->stream;
     const uint64_t n_groups = src.n_groups, D = src.D, C = src.C;
     const uint64_t n_hchunks = (G + kHeadsPerSlot - 1) / kHeadsPerSlot;
@@ -434,12 +465,13 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const float* co
         for (cudaEvent_t* e : {&e0, &e1, &e2}) SAAP_CUDA(cudaEventCreate(e));
         SAAP_CUDA(cudaEventRecord(e0, st));
     }
-    if ((mode == 1 || mode == 2) && probes > 0)
+    const bool routed = (mode == 1 || mode == 2) && probes > 0;
+    if (routed)
         enqueue_route_score(c, n_groups, D, C, G, probes, mode, centT, q_route, probs, pa, cmax,
-                            centR);
+                            centR, slots, n_slots);
     static const bool trace_on = std::getenv("SAAP_PLAN_TRACE") != nullptr;
-    if (trace_on) pa.trace = (unsigned long long*)ensure(c, c->trace, 64);
-    launch_route_plan(pa, (uint32_t)n_groups, st);
+    if (trace_on) pa.trace = (unsigned long long*)ensure(c, c->trace, 128);
+    launch_route_plan(pa, (uint32_t)n_groups, routed, st);
     c->launches++;
     if (e1) SAAP_CUDA(cudaEventRecord(e1, st));
 
@@ -815,7 +847,7 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
     enqueue_route_score(c, 1, d, C, G, l, mode, (const float* const*)dptr, dq, probs, pa,
                         r->kind == 0 ? dcmax : nullptr,
                         r->kind == 0 ? (const float* const*)(dptr + 3) : nullptr);
-    launch_route_plan(pa, 1, st);
+    launch_route_plan(pa, 1, true, st);
     c->launches++;
     d2h(out, dsel, l * 4, st);
     sync(c);
@@ -1068,6 +1100,7 @@ int saap_layer_destroy(saap_layer* L) {
         dfree(L->d_centT);
         dfree(L->d_centR);
         dfree(L->d_cmax);
+        dfree(L->d_route_slots);
         dfree(L->d_qm);
         delete L;
     });
@@ -1385,7 +1418,8 @@ static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* con
     const DecodeSrc src = layer_src(L, cfg->recent_count, need_gather);
     enqueue_decode(c, src, mode, L->d_centT, L->d_qm, qr, q_route, G, cfg->probes,
                    cfg->recent_count, out, stats, selected, kItemTilesSparse, (uint32_t)hq,
-                   mode == 1 ? L->d_cmax : nullptr, mode == 1 ? L->d_centR : nullptr);
+                   mode == 1 ? L->d_cmax : nullptr, mode == 1 ? L->d_centR : nullptr,
+                   mode == 1 ? L->d_route_slots : nullptr, mode == 1 ? L->n_route_slots : 0);
 }
 
 int saap_sparse_attention_dev(saap_ctx* c, const saap_layer* L, const saap_router* const* routers,
@@ -1648,7 +1682,7 @@ int saap_debug_plan_trace(saap_ctx* c, uint64_t* out) {
     return guard([&] {
         DeviceGuard dg(c);
         if (!c->trace.p) invalid("plan tracing off: set SAAP_PLAN_TRACE before the first decode");
-        d2h(out, c->trace.p, 64, c->stream);
+        d2h(out, c->trace.p, 128, c->stream);
         sync(c);
     });
 }

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "saap_b200.h"
@@ -24,6 +25,26 @@ void set_error(const std::string& m);
 [[noreturn]] void fail(int code, const std::string& msg);
 void check_cuda(cudaError_t e, const char* what);
 #define SAAP_CUDA(x) ::saap_b200::check_cuda((x), #x)
+
+// Launch with programmatic stream serialization (PDL): the kernel may be
+// scheduled while the previous kernel on the stream drains; it must call
+// pdl_wait() before touching that kernel's outputs.  Captured into graphs as
+// programmatic edges.
+template <typename... KArgs, typename... Args>
+void launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    check_cuda(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+}
 
 // ---------------------------------------------------------------- layout
 // One (sequence, KV head) context of a layer.
@@ -121,6 +142,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
             "[%3];" ::"r"(smem_u32(dst)),
             "l"(src), "r"(bytes), "r"(smem_u32(bar))
             : "memory");
+}
+// Programmatic dependent launch: a kernel launched with launch_pdl() may start
+// while its predecessor drains; pdl_wait() blocks until the predecessor grid
+// has completed and its writes are visible (no-op without the attribute).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
@@ -234,6 +262,8 @@ struct saap_layer {
     const float** d_centT = nullptr;   // per group centT
     const float** d_centR = nullptr;   // per group row-major centroids
     float* d_cmax = nullptr;           // per group partition cmax
+    uint32_t* d_route_slots = nullptr;  // [n_slots+1] offsets, then groups by partition
+    uint32_t n_route_slots = 0;
     const double** d_qm = nullptr;     // per group: w1, w2, vec (3 pointers)
     // decode: TMA maps over the packed cache (+ gather buffer), built lazily
     void* maps = nullptr;              // DecodeMaps (host copy)

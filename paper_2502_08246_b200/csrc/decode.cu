@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kSliceMax) route_score_kernel(RouteArgs a) {
     __shared__ double xs[kSliceMax];
     __shared__ uint32_t xi[kSliceMax];
     __shared__ __align__(8) uint64_t bar;
+    pdl_trigger();
     const uint32_t g = blockIdx.x, sl = blockIdx.y, tid = threadIdx.x;
     const uint32_t c0 = sl * a.slice, nsl = min(a.slice, a.C - c0);
     if (a.mode == 1) {
@@ -182,17 +183,6 @@ __global__ void __launch_bounds__(kSliceMax) route_score_kernel(RouteArgs a) {
         }
         if (bulk) mbar_wait(&bar, 0);
         __syncthreads();
-        if (a.approx) {
-            // fp32 scores with the rounded pooled vector; route_plan_kernel bounds
-            // their error and re-scores the boundary candidates exactly
-            if (tid < nsl) {
-                float x = 0.f;
-#pragma unroll 8
-                for (uint32_t j = 0; j < a.D; ++j) x = fmaf((float)pooled[j], slab[j * a.slice + tid], x);
-                a.approx[(size_t)g * a.C + c0 + tid] = x;
-            }
-            return;
-        }
     }
     double sc = -INFINITY;
     uint32_t id = 0xFFFFFFFFu;
@@ -220,10 +210,62 @@ __global__ void __launch_bounds__(kSliceMax) route_score_kernel(RouteArgs a) {
     }
 }
 
+// Approximate routing scores.  CTA (slot, 32 centroids): warp w owns dims
+// [w*D/8, (w+1)*D/8) and lane the centroid, so every centroid value is loaded
+// once (coalesced rows of the transposed centroids) and reused by all the
+// slot's contexts; the 8 warps' partial dot products are summed in shared
+// memory.  pooled = fp64 row sum of the group's queries rounded to f32
+// (route_plan_kernel bounds the resulting error).
+constexpr int kApproxGroups = 16;  // contexts per pass
+template <int D>
+__global__ void __launch_bounds__(256) route_approx_kernel(ApproxArgs a) {
+    constexpr int DW = D / 8;
+    __shared__ float pf[kApproxGroups][D];
+    __shared__ float red[8][kApproxGroups][33];
+    pdl_trigger();
+    const uint32_t s = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t gb = a.slot_off ? a.slot_off[s] : s;
+    const uint32_t ng = a.slot_off ? a.slot_off[s + 1] - gb : 1;
+    auto group = [&](uint32_t k) { return a.slot_off ? a.slot_list[gb + k] : gb + k; };
+    const float* cT = a.centT[group(0)];
+    const uint32_t c = blockIdx.y * 32 + lane;
+    float cv[DW];
+#pragma unroll
+    for (int jj = 0; jj < DW; ++jj) cv[jj] = c < a.C ? cT[(size_t)(warp * DW + jj) * a.C + c] : 0.f;
+    for (uint32_t k0 = 0; k0 < ng; k0 += kApproxGroups) {
+        const uint32_t nk = min((uint32_t)kApproxGroups, ng - k0);
+        for (uint32_t e = tid; e < nk * D; e += blockDim.x) {
+            const uint32_t k = e / D, j = e % D;
+            const float* q = a.q_route + (size_t)group(k0 + k) * a.G * D + j;
+            double sj = 0.0;
+            for (uint32_t i = 0; i < a.G; ++i) sj = __dadd_rn(sj, (double)q[(size_t)i * D]);
+            pf[k][j] = (float)sj;
+        }
+        __syncthreads();
+        for (uint32_t k = 0; k < nk; ++k) {
+            float x = 0.f;
+#pragma unroll
+            for (int jj = 0; jj < DW; ++jj) x = fmaf(pf[k][warp * DW + jj], cv[jj], x);
+            red[warp][k][lane] = x;
+        }
+        __syncthreads();
+        for (uint32_t e = tid; e < nk * 32; e += blockDim.x) {
+            const uint32_t k = e / 32, l = e % 32, cc = blockIdx.y * 32 + l;
+            float x = 0.f;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) x += red[w][k][l];
+            if (cc < a.C) a.approx[(size_t)group(k0 + k) * a.C + cc] = x;
+        }
+        __syncthreads();
+    }
+}
+
 // Stage 2 (one CTA per context): merge the slices' candidates into the top-l
 // list, build the visited set and cut it into tiles and work items.
 __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
+    pdl_trigger();
+    pdl_wait();
     const uint32_t g = blockIdx.x;
     const uint32_t tid = threadIdx.x, nth = blockDim.x;
     const GroupMeta gm = a.meta[g];
@@ -254,7 +296,7 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
 
     unsigned long long t0 = 0;
     auto trace = [&](int k) {
-        if (a.trace && g == 0 && tid == 0) a.trace[k] = clock64() - t0;
+        if (a.trace && route && g == 0 && tid == 0) a.trace[k] = clock64() - t0;
     };
     if (a.trace && g == 0 && tid == 0) t0 = clock64();
     // ---------------- routing: candidates -> top-L in reference order
@@ -283,6 +325,10 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xFFFFFFFFu, part, o);
         if ((tid & 31) == 0) s_n2[tid >> 5] = part;
         const float av = tid < Cb ? a.approx[(size_t)g * Cb + tid] : -INFINITY;
+        if (a.trace && g == 0) {
+            __syncthreads();
+            trace(8);
+        }
         const uint32_t u = __float_as_uint(av);
         const uint32_t key = (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // order-preserving
         // radix select (MSB first, 8-bit digits): the L-th largest key
@@ -326,6 +372,7 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
             }
             __syncthreads();
         }
+        trace(9);
         const uint32_t tk = s_pref;
         const float t_l = __uint_as_float((tk & 0x80000000u) ? (tk & 0x7FFFFFFFu) : ~tk);
         double n2 = 0.0;
@@ -354,6 +401,7 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
                 crow[r][jj] = cr[(size_t)cand_id[r] * a.D + jj];
             }
             __syncthreads();
+            trace(10);
             if (tid < nS) {
                 double sx = 0.0;
 #pragma unroll 8
@@ -729,6 +777,8 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
         reinterpret_cast<uint4*>(&s.V[0][0])[e] = make_uint4(0, 0, 0, 0);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
+    pdl_trigger();
+    pdl_wait();  // everything above overlaps the planner's tail
 
     const uint32_t n_items = *reinterpret_cast<volatile uint32_t*>(&a.ctr->n_items);
 
@@ -1099,6 +1149,7 @@ __global__ void __launch_bounds__(kHeadsPerSlot * D) combine_kernel(const QSlot*
                                                                     const float* part_O, const float* part_ml,
                                                                     float* out) {
     constexpr int NOUT = kHeadsPerSlot * D;
+    pdl_wait();
     const uint32_t qsi = blockIdx.x;
     const QSlot qs = qslots[qsi];
     if (qs.count <= 1) return;  // written directly by the decode kernel
@@ -1121,13 +1172,16 @@ __global__ void __launch_bounds__(kHeadsPerSlot * D) combine_kernel(const QSlot*
 // ============================================================ launchers
 void launch_combine(int D, const QSlot* qs, uint32_t n_qslots, uint32_t G, uint32_t n_hchunks,
                     const float* pO, const float* pml, float* out, cudaStream_t st) {
+#define SAAP_COMBINE(DD)                                                                        \
+    launch_pdl(true, combine_kernel<DD>, dim3(n_qslots), dim3(kHeadsPerSlot * DD), 0, st, qs,   \
+               n_qslots, G, n_hchunks, pO, pml, out)
     switch (D) {
-        case 128: combine_kernel<128><<<n_qslots, 4 * 128, 0, st>>>(qs, n_qslots, G, n_hchunks, pO, pml, out); break;
-        case 64: combine_kernel<64><<<n_qslots, 4 * 64, 0, st>>>(qs, n_qslots, G, n_hchunks, pO, pml, out); break;
-        case 32: combine_kernel<32><<<n_qslots, 4 * 32, 0, st>>>(qs, n_qslots, G, n_hchunks, pO, pml, out); break;
+        case 128: SAAP_COMBINE(128); break;
+        case 64: SAAP_COMBINE(64); break;
+        case 32: SAAP_COMBINE(32); break;
         default: fail(SAAP_ERR_UNSUPPORTED, "combine: unsupported head dim");
     }
-    SAAP_CUDA(cudaGetLastError());
+#undef SAAP_COMBINE
 }
 
 template <int D>
@@ -1139,8 +1193,7 @@ static void launch_decode_t(const DecodeMaps& m, const DecodeArgs& a, int grid, 
                                        (int)smem));
         configured = true;
     }
-    decode_kernel<D><<<grid, (kComputeWarps + 2) * 32, smem, st>>>(m, a);
-    SAAP_CUDA(cudaGetLastError());
+    launch_pdl(true, decode_kernel<D>, dim3(grid), dim3((kComputeWarps + 2) * 32), smem, st, m, a);
 }
 
 void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st) {
@@ -1166,7 +1219,18 @@ void launch_route_score(const RouteArgs& a, uint32_t n_groups, cudaStream_t st) 
     SAAP_CUDA(cudaGetLastError());
 }
 
-void launch_route_plan(const PlanArgs& a, uint32_t n_groups, cudaStream_t st) {
+void launch_route_approx(int D, const ApproxArgs& a, uint32_t n_slots, cudaStream_t st) {
+    const dim3 grid(n_slots, (a.C + 31) / 32);
+    switch (D) {
+        case 128: route_approx_kernel<128><<<grid, 256, 0, st>>>(a); break;
+        case 64: route_approx_kernel<64><<<grid, 256, 0, st>>>(a); break;
+        case 32: route_approx_kernel<32><<<grid, 256, 0, st>>>(a); break;
+        default: fail(SAAP_ERR_UNSUPPORTED, "route: unsupported head dim " + std::to_string(D));
+    }
+    SAAP_CUDA(cudaGetLastError());
+}
+
+void launch_route_plan(const PlanArgs& a, uint32_t n_groups, bool pdl, cudaStream_t st) {
     const bool route = a.mode == 1 || a.mode == 2;
     size_t smem = 0;
     if (route) smem = (size_t)std::max<uint32_t>(a.P2, kPlanThreads) * 12 + ((a.C + 31) / 32) * 4 + 16;
@@ -1178,8 +1242,7 @@ void launch_route_plan(const PlanArgs& a, uint32_t n_groups, cudaStream_t st) {
         configured = true;
     }
     if (smem > 180 * 1024) fail(SAAP_ERR_UNSUPPORTED, "route_plan: too many buckets/probes for one CTA");
-    route_plan_kernel<<<n_groups, kPlanThreads, smem, st>>>(a);
-    SAAP_CUDA(cudaGetLastError());
+    launch_pdl(pdl, route_plan_kernel, dim3(n_groups), dim3(kPlanThreads), smem, st, a);
 }
 
 }  // namespace saap_b200
