@@ -416,6 +416,18 @@ def ours(a):
         buf = (ct.c_uint64 * 16)()
         if sb.lib().saap_debug_plan_trace(ctx.h, buf) == 0:
             plan_trace = list(buf)
+    decode_trace = None
+    if os.environ.get("SAAP_DECODE_TRACE"):
+        import ctypes as ct
+        nc = ctx.sm_count()
+        buf = (ct.c_uint64 * (4 * nc))()
+        if sb.lib().saap_debug_decode_trace(ctx.h, buf, ct.c_uint64(nc)) == 0:
+            t = np.array(list(buf), dtype=np.float64).reshape(nc, 4)
+            t0 = t[:, 0].min()
+            rel = lambda x: [round(float(v), 2) for v in np.percentile((x - t0) / 1e3, [0, 50, 100])]
+            decode_trace = {"start_us": rel(t[:, 0]), "first_tile_us": rel(t[:, 1]),
+                            "end_us": rel(t[:, 2]),
+                            "tiles_per_cta": [int(v) for v in np.percentile(t[:, 3], [0, 50, 100])]}
 
     # ---- counters, quality vs dense
     keys_scored = []
@@ -506,6 +518,7 @@ def ours(a):
         "gpu_launches": 2 * a.steps,
         "prefill_build_ms_per_layer": round(float(np.mean(t_build)), 2),
         "plan_trace_cycles": plan_trace,
+        "decode_trace": decode_trace,
         "prefill": {
             "keys": n_keys_prefill, "assign_ms": round(assign_ms, 3), "pack_ms": round(pack_ms, 3),
             "keys_per_s": round(n_keys_prefill / ((assign_ms + pack_ms) * 1e-3), 1),

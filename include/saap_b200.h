@@ -242,6 +242,10 @@ SAAP_API int saap_debug_exp(saap_ctx* ctx, const double* x, uint64_t n, double* 
  * context 0 of the last routed decode step (16 x u64). */
 SAAP_API int saap_debug_plan_trace(saap_ctx* ctx, uint64_t* out);
 
+/* With SAAP_DECODE_TRACE set: per attention CTA of the last decode step
+ * {start, first tile, end (globaltimer ns), tiles consumed} (4 x u64 each). */
+SAAP_API int saap_debug_decode_trace(saap_ctx* ctx, uint64_t* out, uint64_t n_ctas);
+
 /* ---- synthetic data (bench tooling; counter-based, reproducible) ------- */
 /* Fills a device bf16 [rows x dim] buffer with clustered keys / values. */
 SAAP_API int saap_synth_fill_dev(saap_ctx* ctx, void* out_bf16, uint64_t rows, uint64_t dim,

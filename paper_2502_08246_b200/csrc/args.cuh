@@ -110,6 +110,7 @@ struct DecodeArgs {
     const QSlot* qslots;
     uint32_t* done;
     float* out;
+    unsigned long long* dtrace;  // debug: per CTA {start, first tile, end (globaltimer ns), tiles}
 };
 
 struct DecodeMaps {

@@ -283,13 +283,15 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 // (sequential over d; products of bf16 keys and f32 centroids are exact, so
 // DFMA == mulsd+addsd), batched per group so each centroid chunk staged in
 // shared memory serves RB keys.  CTA (y, g) takes batches y, y+Y, ... of
-// group g's list; thread t scores key t%RB against centroids t/RB + 8i of
-// each chunk (RC centroids), then a (score desc, id asc) reduction.
+// group g's list; lane = key (bf16 pairs in shared memory), warp w scores
+// centroids w + 8i of each chunk reading (j, j+1) centroid pairs as one
+// 16-byte broadcast, then a (score desc, id asc) reduction over warps.
 namespace rf {
-constexpr int RB = 32;    // keys per batch
+constexpr int RB = 32;    // keys per batch (one per lane)
 constexpr int RC = 64;    // centroids per staged chunk
 constexpr int THREADS = 256;
-constexpr int PER = RC * RB / THREADS;  // chains per thread
+constexpr int NW = THREADS / 32;
+constexpr int PER = RC / NW;  // chains per thread
 }  // namespace rf
 
 template <int D>
@@ -302,61 +304,68 @@ __global__ void __launch_bounds__(rf::THREADS) refine_kernel(const uint32_t* lis
                                                              uint32_t* out) {
     using namespace rf;
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    double* ks = reinterpret_cast<double*>(smem_raw);  // [RB][D+1]
-    double* cs = ks + RB * (D + 1);                     // [RC][D]
-    __shared__ double red_s[THREADS / RB][RB];
-    __shared__ uint32_t red_i[THREADS / RB][RB];
+    double* cs = reinterpret_cast<double*>(smem_raw);  // [RC][D]
+    __shared__ uint32_t ks[RB * (D / 2 + 1)];           // keys as bf16 pairs (padded rows)
+    __shared__ double red_s[NW][RB];
+    __shared__ uint32_t red_i[NW][RB];
     const uint32_t g = blockIdx.y;
     const uint32_t n = count[g];
-    const uint32_t tid = threadIdx.x, kq = tid % RB, cw = tid / RB;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const double* cg = cent64[g];
     const uint32_t* lg = list + out_base[g];
     for (uint32_t b0 = blockIdx.x * RB; b0 < n; b0 += gridDim.x * RB) {
         const uint32_t nb = min((uint32_t)RB, n - b0);
         __syncthreads();
-        for (uint32_t e = tid; e < RB * D; e += THREADS) {
-            const uint32_t r = e / D, j = e % D;
-            double v = 0.0;
-            if (r < nb)
-                v = (double)__uint_as_float(((uint32_t)keys[(key_row0[g] + lg[b0 + r]) * D + j]) << 16);
-            ks[r * (D + 1) + j] = v;
+        for (uint32_t e = tid; e < (uint32_t)RB * (D / 2); e += THREADS) {  // bf16 pairs
+            const uint32_t r = e / (D / 2), j2 = e % (D / 2);
+            ks[r * (D / 2 + 1) + j2] = reinterpret_cast<const uint32_t*>(
+                    keys + (key_row0[g] + lg[b0 + min(r, nb - 1)]) * D)[j2];
         }
+        const uint32_t* kw = ks + lane * (D / 2 + 1);
         double best = -INFINITY;
         uint32_t bid = 0xFFFFFFFFu;
         for (uint32_t c0 = 0; c0 < C; c0 += RC) {
             const uint32_t nc = min((uint32_t)RC, C - c0);
             __syncthreads();
-            for (uint32_t e = tid; e < (uint32_t)RC * D; e += THREADS)
-                cs[e] = e < nc * D ? cg[(size_t)c0 * D + e] : 0.0;
+            for (uint32_t e = tid; e < (uint32_t)RC * D / 2; e += THREADS)
+                reinterpret_cast<double2*>(cs)[e] = 2 * e < nc * D
+                        ? reinterpret_cast<const double2*>(cg + (size_t)c0 * D)[e]
+                        : make_double2(0.0, 0.0);
             __syncthreads();
-            double acc[PER];
+#pragma unroll 1
+            for (int i0 = 0; i0 < PER; i0 += 4) {
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                const double* cw = cs + (w + NW * i0) * D;
+#pragma unroll 8
+                for (int j2 = 0; j2 < D / 2; ++j2) {
+                    const double k0 = (double)__uint_as_float(kw[j2] << 16);
+                    const double k1 = (double)__uint_as_float(kw[j2] & 0xFFFF0000u);
 #pragma unroll
-            for (int i = 0; i < PER; ++i) acc[i] = 0.0;
-            const double* kr = ks + kq * (D + 1);
-#pragma unroll 4
-            for (int j = 0; j < D; ++j) {
-                const double kv = kr[j];
+                    for (int i = 0; i < 4; ++i) {
+                        const double2 cv = reinterpret_cast<const double2*>(cw + NW * i * D)[j2];
+                        acc[i] = fma(k0, cv.x, acc[i]);
+                        acc[i] = fma(k1, cv.y, acc[i]);
+                    }
+                }
 #pragma unroll
-                for (int i = 0; i < PER; ++i) acc[i] = fma(kv, cs[(cw + (THREADS / RB) * i) * D + j], acc[i]);
-            }
-#pragma unroll
-            for (int i = 0; i < PER; ++i) {  // ascending centroid ids: strict > keeps the lowest
-                const uint32_t c = cw + (THREADS / RB) * i;
-                if (c < nc && acc[i] > best) {
-                    best = acc[i];
-                    bid = c0 + c;
+                for (int i = 0; i < 4; ++i) {  // ascending centroid ids: strict > keeps the lowest
+                    const uint32_t c = w + NW * (i0 + i);
+                    if (c < nc && acc[i] > best) {
+                        best = acc[i];
+                        bid = c0 + c;
+                    }
                 }
             }
         }
-        red_s[cw][kq] = best;
-        red_i[cw][kq] = bid;
+        red_s[w][lane] = best;
+        red_i[w][lane] = bid;
         __syncthreads();
         if (tid < nb) {
             double bs = red_s[0][tid];
             uint32_t bi = red_i[0][tid];
-            for (int w = 1; w < THREADS / RB; ++w) {
-                const double o = red_s[w][tid];
-                const uint32_t oi = red_i[w][tid];
+            for (int v = 1; v < NW; ++v) {
+                const double o = red_s[v][tid];
+                const uint32_t oi = red_i[v][tid];
                 if (o > bs || (o == bs && oi < bi)) {
                     bs = o;
                     bi = oi;
@@ -475,7 +484,7 @@ void launch_refine(const uint32_t* list, const uint32_t* count, const uint16_t* 
                    const uint64_t* key_row0, const double* const* cent64, const uint64_t* out_base,
                    uint32_t C, uint32_t* out, uint32_t n_groups, int sm_count, cudaStream_t st) {
     using namespace rf;
-    const size_t smem = (size_t)(RB * (tc::KD + 1) + RC * tc::KD) * sizeof(double);
+    const size_t smem = (size_t)RC * tc::KD * sizeof(double);
     static bool configured = false;
     if (!configured) {
         SAAP_CUDA(cudaFuncSetAttribute(refine_kernel<tc::KD>,

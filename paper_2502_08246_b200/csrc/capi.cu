@@ -489,6 +489,8 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const float* co
     da.done = c->done;
     da.out = out;
     const int grid = (int)std::min<uint64_t>((uint64_t)c->sm_count, max_items);
+    static const bool dtrace_on = std::getenv("SAAP_DECODE_TRACE") != nullptr;
+    if (dtrace_on) da.dtrace = (unsigned long long*)ensure(c, c->dtrace, (size_t)c->sm_count * 32);
     launch_decode((int)D, *src.maps, da, std::max(grid, 1), st);
     launch_combine((int)D, qs, (uint32_t)qslots, (uint32_t)G, (uint32_t)n_hchunks, pO, pml, out, st);
     c->launches += 2;
@@ -595,8 +597,9 @@ int saap_ctx_destroy(saap_ctx* c) {
         if (!c) return;
         cudaSetDevice(c->device);
         cudaStreamSynchronize(c->stream);
-        for (saap_scratch* s : {&c->items, &c->qslots, &c->part_O, &c->part_ml, &c->probs, &c->stats,
-                                &c->sel, &c->qr, &c->qd, &c->out, &c->misc, &c->zeros})
+        for (saap_scratch* s : {&c->approx, &c->trace, &c->dtrace, &c->qA, &c->cand_s, &c->cand_i,
+                                &c->items, &c->tiles, &c->qslots, &c->part_O, &c->part_ml, &c->probs,
+                                &c->stats, &c->sel, &c->qr, &c->qd, &c->out, &c->misc, &c->zeros})
             if (s->p) cudaFree(s->p);
         dfree(c->counters);
         dfree(c->done);
@@ -942,7 +945,7 @@ int saap_build_ivf(saap_ctx* c, const uint32_t* assignment, uint64_t n, uint64_t
         };
         const size_t o_meta = take(sizeof(GroupMeta)), o_tiles = take(nt * sizeof(TileDesc)),
                      o_first = take(first.size() * 4), o_hist = take(nt * C * 4),
-                     o_cA = take(C * 4), o_off = take((C + 1) * 4), o_offA = take((C + 1) * 4),
+                     o_cA = take(2 * C * 4), o_off = take((C + 1) * 4), o_offA = take((C + 1) * 4),
                      o_as = take(n * 4), o_idx = take(n * 4), o_inv = take(n * 4);
         char* b = (char*)ensure(c, c->misc, o);
         h2d(b + o_meta, meta.data(), sizeof(GroupMeta), st);
@@ -954,7 +957,7 @@ int saap_build_ivf(saap_ctx* c, const uint32_t* assignment, uint64_t n, uint64_t
                     (uint32_t*)(b + o_hist), (uint32_t*)(b + o_cA), (uint32_t*)(b + o_off),
                     (uint32_t*)(b + o_offA), (uint32_t*)(b + o_idx), (uint32_t*)(b + o_inv),
                     nullptr, nullptr, n, nullptr, nullptr, nullptr, nullptr, nullptr, st);
-        c->launches += 3;
+        c->launches += 4;
         std::vector<uint32_t> off32(C + 1), idx32(n);
         d2h(off32.data(), b + o_off, (C + 1) * 4, st);
         d2h(idx32.data(), b + o_idx, n * 4, st);
@@ -1041,7 +1044,7 @@ int saap_layer_create(saap_ctx* c, uint64_t n_groups, uint64_t d, uint64_t C,
         L->tiles = dmalloc<TileDesc>(tiles.size());
         L->tile_first = dmalloc<uint32_t>(first.size());
         L->hist = dmalloc<uint32_t>(tiles.size() * C);
-        L->countA = dmalloc<uint32_t>(n_groups * C);
+        L->countA = dmalloc<uint32_t>(2 * n_groups * C);  // countA | per-bucket totals
         L->d_cent64 = (const double**)(dmalloc<void*>(n_groups));
         std::vector<uint64_t> rb(n_groups), kr0(n_groups), ib(n_groups);
         for (uint64_t g = 0; g < n_groups; ++g) {
@@ -1683,6 +1686,16 @@ int saap_debug_plan_trace(saap_ctx* c, uint64_t* out) {
         DeviceGuard dg(c);
         if (!c->trace.p) invalid("plan tracing off: set SAAP_PLAN_TRACE before the first decode");
         d2h(out, c->trace.p, 128, c->stream);
+        sync(c);
+    });
+}
+
+int saap_debug_decode_trace(saap_ctx* c, uint64_t* out, uint64_t n_ctas) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        if (!c->dtrace.p) invalid("decode tracing off: set SAAP_DECODE_TRACE before the first decode");
+        if (n_ctas > (uint64_t)c->sm_count) invalid("decode trace: more CTAs than SMs");
+        d2h(out, c->dtrace.p, n_ctas * 32, c->stream);
         sync(c);
     });
 }

@@ -179,7 +179,7 @@ struct saap_ctx {
     bool own_stream = false;
     uint64_t launches = 0;
     // growable device scratch (sized by uncaptured calls; graphs reuse it)
-    saap_scratch approx, trace, qA, cand_s, cand_i, items, tiles, qslots, part_O, part_ml, probs, stats, sel, qr, qd, out, misc, zeros;
+    saap_scratch approx, trace, dtrace, qA, cand_s, cand_i, items, tiles, qslots, part_O, part_ml, probs, stats, sel, qr, qd, out, misc, zeros;
     saap_b200::StepCounters* counters = nullptr;  // persistent, 128 B
     uint32_t* done = nullptr;                     // per query slot completion counters
     size_t done_cap = 0;

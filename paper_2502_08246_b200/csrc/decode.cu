@@ -142,6 +142,22 @@ __device__ void bitonic_smem(double* ss, uint32_t* si, uint32_t n) {
     }
 }
 
+// pooled_j = sum_i q_ij in fp64, rows in order (attention.cpp:289-295); the
+// row loads are issued 8 at a time so the chain waits on one round trip.
+template <typename T>
+__device__ __forceinline__ double pooled_sum(const T* q, uint32_t G, size_t stride) {
+    double s = 0.0;
+    for (uint32_t i0 = 0; i0 < G; i0 += 8) {
+        T v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = i0 + u < G ? q[(size_t)(i0 + u) * stride] : (T)0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (i0 + u < G) s = __dadd_rn(s, (double)v[u]);
+    }
+    return s;
+}
+
 // Stage 1: score a slice of centroids (one thread per centroid) and keep the
 // slice's top-`keep` in reference order.  The slice's transposed f32
 // centroids [D x slice] are staged in shared memory by bulk copies, so the
@@ -177,9 +193,7 @@ __global__ void __launch_bounds__(kSliceMax) route_score_kernel(RouteArgs a) {
         // pooled_j = sum_i q_ij (fp64, rows in order)   attention.cpp:289-295
         const float* q = a.q_route + (size_t)g * a.G * a.D;
         for (uint32_t j = tid; j < a.D; j += blockDim.x) {
-            double s = 0.0;
-            for (uint32_t i = 0; i < a.G; ++i) s = __dadd_rn(s, (double)q[(size_t)i * a.D + j]);
-            pooled[j] = s;
+            pooled[j] = pooled_sum(q + j, a.G, a.D);
         }
         if (bulk) mbar_wait(&bar, 0);
         __syncthreads();
@@ -196,8 +210,7 @@ __global__ void __launch_bounds__(kSliceMax) route_score_kernel(RouteArgs a) {
                 s = __dadd_rn(s, __dmul_rn(pooled[j], (double)slab[j * a.slice + tid]));
         } else {
             // Q-model: score_c = sum_i p_ic over the group rows   qmodel.cpp:493-499
-            const double* p = a.scores + (size_t)g * a.G * a.C;
-            for (uint32_t i = 0; i < a.G; ++i) s = __dadd_rn(s, p[(size_t)i * a.C + c]);
+            s = pooled_sum(a.scores + (size_t)g * a.G * a.C + c, a.G, a.C);
         }
         sc = s;
         id = c;
@@ -217,6 +230,10 @@ __global__ void __launch_bounds__(kSliceMax) route_score_kernel(RouteArgs a) {
 // memory.  pooled = fp64 row sum of the group's queries rounded to f32
 // (route_plan_kernel bounds the resulting error).
 constexpr int kApproxGroups = 16;  // contexts per pass
+constexpr uint32_t kStageOff = 2049;  // planner stages off/offA in shared memory up to C = 2048
+constexpr int kPlanTileCnt = 1024;    // planner keeps per-tile piece counts in shared memory
+
+
 template <int D>
 __global__ void __launch_bounds__(256) route_approx_kernel(ApproxArgs a) {
     constexpr int DW = D / 8;
@@ -236,10 +253,7 @@ __global__ void __launch_bounds__(256) route_approx_kernel(ApproxArgs a) {
         const uint32_t nk = min((uint32_t)kApproxGroups, ng - k0);
         for (uint32_t e = tid; e < nk * D; e += blockDim.x) {
             const uint32_t k = e / D, j = e % D;
-            const float* q = a.q_route + (size_t)group(k0 + k) * a.G * D + j;
-            double sj = 0.0;
-            for (uint32_t i = 0; i < a.G; ++i) sj = __dadd_rn(sj, (double)q[(size_t)i * D]);
-            pf[k][j] = (float)sj;
+            pf[k][j] = (float)pooled_sum(a.q_route + (size_t)group(k0 + k) * a.G * D + j, a.G, D);
         }
         __syncthreads();
         for (uint32_t k = 0; k < nk; ++k) {
@@ -299,6 +313,36 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         if (a.trace && route && g == 0 && tid == 0) a.trace[k] = clock64() - t0;
     };
     if (a.trace && g == 0 && tid == 0) t0 = clock64();
+    // query slots' A operands for QK^T: rows 0-3 q1, 4-7 q2, 8-11 q3 (3-term
+    // bf16 split of the f32 queries, ~fp32-exact), rows 12-15 zero.  Independent
+    // of routing: issued first so its loads overlap the routing phases.
+    for (uint32_t e = tid; a.qA && !a.route_only && e < a.n_hchunks * 16 * a.D; e += nth) {
+        const uint32_t hc = e / (16 * a.D), r = (e / a.D) % 16, d = e % a.D;
+        const uint32_t head = hc * kHeadsPerSlot + (r & 3);
+        float v = 0.f;
+        if (r < 12 && head < a.G) {
+            const float x = a.q_attn[((size_t)g * a.G + head) * a.D + d];
+            const float t1 = __uint_as_float((uint32_t)f32_to_bf16_rne(x) << 16);
+            const float r1 = x - t1;
+            const float t2 = __uint_as_float((uint32_t)f32_to_bf16_rne(r1) << 16);
+            v = r < 4 ? t1 : (r < 8 ? t2 : r1 - t2);
+        }
+        uint16_t* dst = a.qA + (size_t)(g * a.n_hchunks + hc) * 16 * a.D;
+        *reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(dst) + swz_elem(a.D, 16, r, d)) =
+                f32_to_bf16_rne(v);
+    }
+    // the group's bucket offsets, staged while routing runs (C <= kStageOff)
+    const bool stage_off = route && Cb + 1 <= kStageOff;
+    uint32_t* s_off = vpre + L + 4;
+    uint32_t* s_offA = s_off + (stage_off ? Cb + 1 : 0);
+    if (stage_off) {
+        const uint32_t* og = a.off + (size_t)g * (Cb + 1);
+        const uint32_t* oAg = a.offA + (size_t)g * (Cb + 1);
+        for (uint32_t c = tid; c <= Cb; c += nth) {
+            s_off[c] = og[c];
+            s_offA[c] = oAg[c];
+        }
+    }
     // ---------------- routing: candidates -> top-L in reference order
     if (route && a.approx) {
         // centroid router, C <= blockDim: exact top-L from fp32 scores.  With
@@ -317,8 +361,7 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         const float* q = a.q_route + (size_t)g * a.G * a.D;
         double part = 0.0;
         for (uint32_t j = tid; j < a.D; j += nth) {
-            double sj = 0.0;
-            for (uint32_t i = 0; i < a.G; ++i) sj = __dadd_rn(sj, (double)q[(size_t)i * a.D + j]);
+            const double sj = pooled_sum(q + j, a.G, a.D);
             pooled[j] = sj;
             part += sj * sj;
         }
@@ -467,8 +510,8 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
 
     // ---------------- segments of the visited set      attention.cpp:342-372
     const uint32_t rb = fallback ? 0 : n - a.recent;  // recent_begin
-    const uint32_t* offg = a.off + (size_t)g * (Cb + 1);
-    const uint32_t* offAg = a.offA + (size_t)g * (Cb + 1);
+    const uint32_t* offg = stage_off ? s_off : a.off + (size_t)g * (Cb + 1);
+    const uint32_t* offAg = stage_off ? s_offA : a.offA + (size_t)g * (Cb + 1);
     const uint32_t* idxg = a.idx + gm.ivf_base;
     const uint64_t gbuf = (uint64_t)g * a.gather_cap;  // this group's gather rows
     // bucket segments: region-A prefix of each selected bucket, cut at rb
@@ -612,24 +655,13 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         for (uint32_t e = tid; e < a.G * a.D; e += nth) a.out[(size_t)g * a.G * a.D + e] = 0.f;
         return;
     }
-    // query slots' A operands for QK^T: rows 0-3 q1, 4-7 q2, 8-11 q3 (3-term
-    // bf16 split of the f32 queries, ~fp32-exact), rows 12-15 zero
-    for (uint32_t e = tid; e < a.n_hchunks * 16 * a.D; e += nth) {
-        const uint32_t hc = e / (16 * a.D), r = (e / a.D) % 16, d = e % a.D;
-        const uint32_t head = hc * kHeadsPerSlot + (r & 3);
-        float v = 0.f;
-        if (r < 12 && head < a.G) {
-            const float x = a.q_attn[((size_t)g * a.G + head) * a.D + d];
-            const float t1 = __uint_as_float((uint32_t)f32_to_bf16_rne(x) << 16);
-            const float r1 = x - t1;
-            const float t2 = __uint_as_float((uint32_t)f32_to_bf16_rne(r1) << 16);
-            v = r < 4 ? t1 : (r < 8 ? t2 : r1 - t2);
-        }
-        uint16_t* dst = a.qA + (size_t)(g * a.n_hchunks + hc) * 16 * a.D;
-        *reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(dst) + swz_elem(a.D, 16, r, d)) =
-                f32_to_bf16_rne(v);
+    // piece counters: shared memory when the group's tiles fit, else in place
+    __shared__ uint32_t s_np[kPlanTileCnt];
+    const bool np_smem = ntiles <= (uint32_t)kPlanTileCnt;
+    for (uint32_t t = tid; t < ntiles; t += nth) {
+        if (np_smem) s_np[t] = 0;
+        else a.tiles[tile0 + t].npieces = 0;
     }
-    for (uint32_t t = tid; t < ntiles; t += nth) a.tiles[tile0 + t].npieces = 0;
     __syncthreads();
     trace(6);
     // pieces: one per (segment, overlapped tile); slot order inside a tile is
@@ -644,7 +676,7 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         pr.srow = a0 - t * kTileRows;
         pr.row = (sg.kind == KIND_LIST ? 0 : gm.row_base) + sg.start + (a0 - v0);
         TileRec* tr = a.tiles + tile0 + t;
-        const uint32_t slot = atomicAdd(&tr->npieces, 1u);
+        const uint32_t slot = atomicAdd(np_smem ? &s_np[t] : &tr->npieces, 1u);
         tr->p[slot] = pr;
     };
     for (uint32_t s2 = tid; s2 < nseg; s2 += nth) {
@@ -667,6 +699,10 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         it.ntiles = min(a.item_tiles, ntiles - k * a.item_tiles);
         it.pad = 0;
         a.items[s_item0 + e] = it;
+    }
+    if (np_smem) {
+        __syncthreads();
+        for (uint32_t t = tid; t < ntiles; t += nth) a.tiles[tile0 + t].npieces = s_np[t];
     }
     trace(7);
 }
@@ -762,6 +798,12 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
     auto& s = *reinterpret_cast<DecodeSmem2<D>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+    auto gtime = []() {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        return t;
+    };
+    if (a.dtrace && threadIdx.x == 0) a.dtrace[4 * blockIdx.x] = gtime();
     if (threadIdx.x == 0) {
         for (int i = 0; i < CF::NS; ++i) {
             mbar_init(&s.full[i], 1);
@@ -984,9 +1026,18 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
     uint32_t cur_item = 0, cur_qslot = 0, st_ph = 0;
 
     uint32_t stage = 0, phase = 0;
+    uint32_t n_tiles_done = 0;
     for (;;) {
         mbar_wait(&s.full[stage], phase);
         const int4 mt = s.meta[stage];
+        if (a.dtrace && threadIdx.x == 0) {
+            if (n_tiles_done == 0) a.dtrace[4 * blockIdx.x + 1] = gtime();
+            if (mt.x < 0) {
+                a.dtrace[4 * blockIdx.x + 2] = gtime();
+                a.dtrace[4 * blockIdx.x + 3] = n_tiles_done;
+            }
+        }
+        ++n_tiles_done;
         if (mt.x < 0) {
             // stop the merge warp once it has drained the last item
             mbar_wait(&s.st_empty, st_ph ^ 1);
@@ -1149,6 +1200,8 @@ __global__ void __launch_bounds__(kHeadsPerSlot * D) combine_kernel(const QSlot*
                                                                     const float* part_O, const float* part_ml,
                                                                     float* out) {
     constexpr int NOUT = kHeadsPerSlot * D;
+    constexpr int kMaxStage = 256;  // items whose (m, l) are staged in shared memory
+    __shared__ float sml[kMaxStage][8];
     pdl_wait();
     const uint32_t qsi = blockIdx.x;
     const QSlot qs = qslots[qsi];
@@ -1156,15 +1209,29 @@ __global__ void __launch_bounds__(kHeadsPerSlot * D) combine_kernel(const QSlot*
     const uint32_t e = threadIdx.x, h = e / D;
     const uint32_t g = qsi / n_hchunks, hc = qsi % n_hchunks;
     const uint32_t head = hc * kHeadsPerSlot + h;
+    const uint32_t ns = min(qs.count, (uint32_t)kMaxStage);
+    for (uint32_t i = e; i < ns * 8; i += blockDim.x) sml[i / 8][i % 8] = part_ml[(size_t)qs.base * 8 + i];
+    __syncthreads();
+    auto ml = [&](uint32_t i, uint32_t k) {
+        return i < kMaxStage ? sml[i][k] : part_ml[(size_t)(qs.base + i) * 8 + k];
+    };
     float M = -INFINITY;
-    for (uint32_t i = 0; i < qs.count; ++i) M = fmaxf(M, part_ml[(size_t)(qs.base + i) * 8 + h]);
+    for (uint32_t i = 0; i < qs.count; ++i) M = fmaxf(M, ml(i, h));
     float O = 0.f, L = 0.f;
-#pragma unroll 4
-    for (uint32_t i = 0; i < qs.count; ++i) {
-        const size_t it = qs.base + i;
-        const float w = fast_exp2(part_ml[it * 8 + h] - M);
-        O = fmaf(part_O[it * NOUT + e], w, O);
-        L = fmaf(part_ml[it * 8 + 4 + h], w, L);
+    constexpr int U = 8;  // partial rows in flight
+    for (uint32_t i0 = 0; i0 < qs.count; i0 += U) {
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            v[u] = i0 + u < qs.count ? part_O[(size_t)(qs.base + i0 + u) * NOUT + e] : 0.f;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (i0 + u < qs.count) {
+                const float w = fast_exp2(ml(i0 + u, h) - M);
+                O = fmaf(v[u], w, O);
+                L = fmaf(ml(i0 + u, 4 + h), w, L);
+            }
+        }
     }
     if (head < G) out[((size_t)g * G + head) * D + (e % D)] = O / L;
 }
@@ -1235,6 +1302,7 @@ void launch_route_plan(const PlanArgs& a, uint32_t n_groups, bool pdl, cudaStrea
     size_t smem = 0;
     if (route) smem = (size_t)std::max<uint32_t>(a.P2, kPlanThreads) * 12 + ((a.C + 31) / 32) * 4 + 16;
     smem += (size_t)(a.probes + 8) * (sizeof(Seg) + 4);
+    if (route && a.C + 1 <= kStageOff) smem += (size_t)2 * (a.C + 1) * 4;  // staged off/offA
     static bool configured = false;  // static smem (~36 KB) + dynamic can exceed 48 KB
     if (!configured) {
         SAAP_CUDA(cudaFuncSetAttribute(route_plan_kernel,

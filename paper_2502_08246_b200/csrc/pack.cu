@@ -110,32 +110,65 @@ __global__ void __launch_bounds__(512) hist_kernel(const TileDesc* tiles, const 
 
 // Per group: tile bases within each bucket (exclusive over tiles), then the
 // exclusive scans over buckets -> off (all keys) and offA (region A).
-__global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* tile_first, uint32_t C,
-                                                    uint32_t* hist, const uint32_t* countA,
-                                                    uint32_t* off, uint32_t* offA) {
-    extern __shared__ uint32_t tot[];  // 2*C
+// Stage 1, CTA (group, 32 buckets): thread (chunk k, bucket b) sums a run of
+// tiles with all loads in flight, the 32 chunk sums are scanned in shared
+// memory, then each thread rewrites its run as exclusive prefixes.
+constexpr int kScanChunks = 32;
+__global__ void __launch_bounds__(1024) scan_tiles_kernel(const uint32_t* tile_first, uint32_t C,
+                                                          uint32_t* hist, uint32_t* tot) {
+    __shared__ uint32_t part[kScanChunks][33];
+    const uint32_t g = blockIdx.x, b = threadIdx.x & 31, k = threadIdx.x >> 5;
+    const uint32_t c = blockIdx.y * 32 + b;
+    const uint32_t t0 = tile_first[g], nt = tile_first[g + 1] - t0;
+    const uint32_t per = (nt + kScanChunks - 1) / kScanChunks;
+    const uint32_t lo = t0 + min(nt, k * per), hi = t0 + min(nt, (k + 1) * per);
+    constexpr int U = 16;
+    uint32_t sum = 0;
+    if (c < C) {
+        for (uint32_t t = lo; t < hi; t += U) {
+            uint32_t v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = t + u < hi ? hist[(size_t)(t + u) * C + c] : 0u;
+#pragma unroll
+            for (int u = 0; u < U; ++u) sum += v[u];
+        }
+    }
+    part[k][b] = sum;
+    __syncthreads();
+    uint32_t run = 0;
+    for (uint32_t j = 0; j < k; ++j) run += part[j][b];
+    if (k == kScanChunks - 1 && c < C) tot[(size_t)g * C + c] = run + sum;
+    if (c < C) {
+        for (uint32_t t = lo; t < hi; t += U) {
+            uint32_t v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = t + u < hi ? hist[(size_t)(t + u) * C + c] : 0u;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (t + u < hi) {
+                    hist[(size_t)(t + u) * C + c] = run;
+                    run += v[u];
+                }
+        }
+    }
+}
+
+// Stage 2, one CTA per group: exclusive scans of tot (all keys) and countA
+// (region A) over buckets.
+__global__ void __launch_bounds__(1024) scan_buckets_kernel(uint32_t C, const uint32_t* totg,
+                                                            const uint32_t* countA, uint32_t* off,
+                                                            uint32_t* offA) {
     __shared__ uint32_t wsum[2][32];
     const uint32_t g = blockIdx.x;
-    const uint32_t t0 = tile_first[g], t1 = tile_first[g + 1];
-    for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
-        uint32_t run = 0;
-        for (uint32_t t = t0; t < t1; ++t) {
-            uint32_t* p = hist + (size_t)t * C + c;
-            const uint32_t v = *p;
-            *p = run;
-            run += v;
-        }
-        tot[c] = run;
-        tot[C + c] = countA[(size_t)g * C + c];
-    }
-    __syncthreads();
-    // block exclusive scan of tot[0..C) and tot[C..2C): thread owns a chunk
+    const uint32_t* t_all = totg + (size_t)g * C;
+    const uint32_t* t_A = countA + (size_t)g * C;
+    // thread owns a chunk of buckets
     const uint32_t per = (C + blockDim.x - 1) / blockDim.x;
-    const uint32_t lo = threadIdx.x * per, hi = min(C, lo + per);
+    const uint32_t lo = min(C, threadIdx.x * per), hi = min(C, lo + per);
     uint32_t s0 = 0, s1 = 0;
     for (uint32_t c = lo; c < hi; ++c) {
-        s0 += tot[c];
-        s1 += tot[C + c];
+        s0 += t_all[c];
+        s1 += t_A[c];
     }
     // warp inclusive scans
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -175,8 +208,8 @@ __global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* tile_first, 
     for (uint32_t c = lo; c < hi; ++c) {
         og[c] = e0;
         oAg[c] = e1;
-        e0 += tot[c];
-        e1 += tot[C + c];
+        e0 += t_all[c];
+        e1 += t_A[c];
     }
     if (hi == C && lo < hi) {
         og[C] = e0;
@@ -190,49 +223,59 @@ __global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* tile_first, 
 
 // ------------------------------------------------------------ rank + scatter
 // One warp per tile, 32 keys per step in id order: match_any groups equal
-// buckets, the leader bumps the tile's running base -> stable ranks, so idx
-// ascends within each bucket exactly as the reference's forward scatter.
-// Then the warp moves the 32 K/V rows to their packed rows.
-template <int D>
-__global__ void __launch_bounds__(128) scatter_kernel(
-        const TileDesc* tiles, uint32_t n_tiles, const GroupMeta* meta, const uint32_t* assign,
-        uint32_t C, uint32_t* hist, const uint32_t* off, const uint32_t* offA, uint32_t* idx,
+// buckets, the leader bumps the bucket's running position -> stable ranks, so
+// idx ascends within each bucket exactly as the reference's forward scatter.
+// The running positions (off + tile base) and the region-A shift (offA - off)
+// live in shared memory, so the only global loads in the loop are the
+// (prefetched) assignments.  Writes idx/invA/posA and each key's destination
+// row for move_rows_kernel.
+__global__ void __launch_bounds__(32) scatter_kernel(
+        const TileDesc* tiles, const GroupMeta* meta, const uint32_t* assign, uint32_t C,
+        const uint32_t* hist, const uint32_t* off, const uint32_t* offA, uint32_t* idx,
         uint32_t* invA, uint32_t* posA, uint32_t* dst_row) {
-    const uint32_t warp_g = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    const uint32_t lane = threadIdx.x & 31;
-    if (warp_g >= n_tiles) return;
-    const TileDesc td = tiles[warp_g];
+    extern __shared__ uint32_t sm[];  // run[C], shiftA[C]
+    uint32_t* run = sm;
+    uint32_t* shA = sm + C;
+    const uint32_t lane = threadIdx.x;
+    const TileDesc td = tiles[blockIdx.x];
     const GroupMeta gm = meta[td.group];
-    uint32_t* ht = hist + (size_t)warp_g * C;
+    const uint32_t* ht = hist + (size_t)blockIdx.x * C;
     const uint32_t* og = off + (size_t)td.group * (C + 1);
     const uint32_t* oAg = offA + (size_t)td.group * (C + 1);
+    for (uint32_t c = lane; c < C; c += 32) {
+        const uint32_t o = og[c];
+        run[c] = o + ht[c];
+        shA[c] = oAg[c] - o;
+    }
+    const uint32_t* as = assign + gm.ivf_base + td.first;
+    uint32_t cn = lane < td.count ? as[lane] : 0xFFFFFFFFu;
+    __syncwarp();
     for (uint32_t e0 = 0; e0 < td.count; e0 += 32) {
         const uint32_t e = e0 + lane;
         const bool act = e < td.count;
+        const uint32_t c = cn;
+        cn = e + 32 < td.count ? as[e + 32] : 0xFFFFFFFFu;  // next step's bucket in flight
         const uint32_t lid = td.first + e;
-        const uint32_t c = act ? assign[gm.ivf_base + lid] : 0xFFFFFFFFu;
         const uint32_t peers = __match_any_sync(0xFFFFFFFFu, c);
         const uint32_t leader = __ffs(peers) - 1;
         uint32_t base = 0;
         if (act && lane == leader) {
-            base = ht[c];
-            ht[c] = base + __popc(peers);
+            base = run[c];
+            run[c] = base + __popc(peers);
         }
         base = __shfl_sync(0xFFFFFFFFu, base, leader);
-        const uint32_t r = base + __popc(peers & ((1u << lane) - 1));
-        uint32_t row = 0;
         if (act) {
-            idx[gm.ivf_base + og[c] + r] = lid;
+            const uint32_t q = base + __popc(peers & ((1u << lane) - 1));  // position in group idx
+            idx[gm.ivf_base + q] = lid;
             const uint32_t pos = gm.sink + lid;
+            uint32_t row = pos;
             if (pos < gm.T) {
-                row = gm.sink + oAg[c] + r;
+                row = gm.sink + q + shA[c];
                 invA[gm.ivf_base + lid] = row;
                 if (posA) posA[gm.ivf_base + (row - gm.sink)] = pos;
-            } else {
-                row = pos;
             }
+            if (dst_row) dst_row[gm.ivf_base + lid] = row;
         }
-        if (act && dst_row) dst_row[gm.ivf_base + lid] = row;
         __syncwarp();
     }
 }
@@ -464,27 +507,26 @@ void launch_pack(int D, const TileDesc* tiles, uint32_t n_tiles, const uint32_t*
                                        (int)hsm));
         cfg_h = hsm;
     }
-    if (hsm > 48 * 1024 && hsm > cfg_s) {
-        SAAP_CUDA(cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)hsm));
-        cfg_s = hsm;
-    }
     SAAP_CUDA(cudaMemsetAsync(countA, 0, (size_t)n_groups * C * 4, st));
+    uint32_t* tot = countA + (size_t)n_groups * C;  // per-bucket totals (second half)
     if (n_tiles) hist_kernel<<<n_tiles, 512, hsm, st>>>(tiles, meta, assign, C, hist, countA);
-    scan_kernel<<<n_groups, 1024, hsm, st>>>(tile_first, C, hist, countA, off, offA);
-    const uint32_t wpb = 4;
-    const uint32_t sgrid = (n_tiles + wpb - 1) / wpb;
+    if (C) scan_tiles_kernel<<<dim3(n_groups, (C + 31) / 32), 1024, 0, st>>>(tile_first, C, hist, tot);
+    scan_buckets_kernel<<<n_groups, 1024, 0, st>>>(C, tot, countA, off, offA);
+    const size_t ssm = (size_t)2 * C * 4;
+    if (ssm > 48 * 1024 && ssm > cfg_s) {
+        SAAP_CUDA(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)ssm));
+        cfg_s = ssm;
+    }
+    if (n_tiles)
+        scatter_kernel<<<n_tiles, 32, ssm, st>>>(tiles, meta, assign, C, hist, off, offA, idx, invA,
+                                                 posA, Ksrc ? dst_row : nullptr);
 #define SAAP_SCATTER(DD)                                                                         \
-    if (sgrid)                                                                                   \
-        scatter_kernel<DD><<<sgrid, wpb * 32, 0, st>>>(tiles, n_tiles, meta, assign, C, hist, off, \
-                                                       offA, idx, invA, posA,                    \
-                                                       Ksrc ? dst_row : nullptr);                \
-    if (Ksrc && total_ns)                                                                        \
+    if (total_ns)                                                                                \
         move_rows_kernel<DD><<<148 * 16, 256, 0, st>>>(meta, nullptr, n_groups, total_ns, dst_row,  \
                                                        Ksrc, Vsrc, src_row0, Kdst, Vdst);        \
-    if (Ksrc) copy_sink_kernel<DD><<<n_groups, 128, 0, st>>>(meta, n_groups, Ksrc, Vsrc, src_row0, \
-                                                             Kdst, Vdst);
-    switch (D) {
+    copy_sink_kernel<DD><<<n_groups, 128, 0, st>>>(meta, n_groups, Ksrc, Vsrc, src_row0, Kdst, Vdst);
+    if (Ksrc) switch (D) {
         case 128: SAAP_SCATTER(128); break;
         case 64: SAAP_SCATTER(64); break;
         case 32: SAAP_SCATTER(32); break;
