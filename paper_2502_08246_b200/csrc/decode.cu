@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
                 f32_to_bf16_rne(v);
     }
     // the group's bucket offsets, staged while routing runs (C <= kStageOff)
-    const bool stage_off = route && Cb + 1 <= kStageOff;
+    const bool stage_off = route && !a.route_only && Cb + 1 <= kStageOff;
     uint32_t* s_off = vpre + L + 4;
     uint32_t* s_offA = s_off + (stage_off ? Cb + 1 : 0);
     if (stage_off) {
