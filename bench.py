@@ -419,15 +419,24 @@ def ours(a):
     decode_trace = None
     if os.environ.get("SAAP_DECODE_TRACE"):
         import ctypes as ct
-        nc = ctx.sm_count()
-        buf = (ct.c_uint64 * (4 * nc))()
+        graphs[0].launch()  # trace the sparse step (the eager loop above ended on dense)
+        ctx.synchronize()
+        nc = ctx.sm_count
+        buf = (ct.c_uint64 * (16 * nc))()
         if sb.lib().saap_debug_decode_trace(ctx.h, buf, ct.c_uint64(nc)) == 0:
-            t = np.array(list(buf), dtype=np.float64).reshape(nc, 4)
+            t = np.array(list(buf), dtype=np.float64).reshape(nc, 16)
             t0 = t[:, 0].min()
+            os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+            np.save(os.path.join(ROOT, "gpurun_out", "decode_trace.npy"), t)
             rel = lambda x: [round(float(v), 2) for v in np.percentile((x - t0) / 1e3, [0, 50, 100])]
             decode_trace = {"start_us": rel(t[:, 0]), "first_tile_us": rel(t[:, 1]),
                             "end_us": rel(t[:, 2]),
-                            "tiles_per_cta": [int(v) for v in np.percentile(t[:, 3], [0, 50, 100])]}
+                            "tiles_per_cta": [int(v) for v in np.percentile(t[:, 3], [0, 50, 100])],
+                            "producer_empty_wait_frac": round(float(np.median(t[:, 4] / np.maximum(t[:, 5], 1))), 3),
+                            "consumer_full_wait_frac": round(float(np.median(t[:, 6] / np.maximum(t[:, 5], 1))), 3),
+                            "producer_feed_frac": round(float(np.median(t[:, 7] / np.maximum(t[:, 5], 1))), 3),
+                            "producer_record_wait_frac": round(float(np.median(t[:, 8] / np.maximum(t[:, 5], 1))), 3),
+                            "producer_tma_issue_frac": round(float(np.median(t[:, 9] / np.maximum(t[:, 5], 1))), 3)}
 
     # ---- counters, quality vs dense
     keys_scored = []

@@ -243,7 +243,10 @@ SAAP_API int saap_debug_exp(saap_ctx* ctx, const double* x, uint64_t n, double* 
 SAAP_API int saap_debug_plan_trace(saap_ctx* ctx, uint64_t* out);
 
 /* With SAAP_DECODE_TRACE set: per attention CTA of the last decode step
- * {start, first tile, end (globaltimer ns), tiles consumed} (4 x u64 each). */
+ * {start, first tile, end (globaltimer ns), tiles consumed, producer cycles
+ * waiting for a free stage, producer cycles total, consumer cycles waiting
+ * for data, producer cycles feeding work records, producer cycles waiting for
+ * a record, 0 x 7} (16 x u64 each). */
 SAAP_API int saap_debug_decode_trace(saap_ctx* ctx, uint64_t* out, uint64_t n_ctas);
 
 /* ---- synthetic data (bench tooling; counter-based, reproducible) ------- */

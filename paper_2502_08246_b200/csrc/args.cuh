@@ -17,9 +17,17 @@ struct PieceRec {
     uint32_t srow;   // first smem row (multiple of 8)
     uint64_t row;    // first row in its tensor (layer cache or gather buffer)
 };
-struct TileRec {
+// One 128-row tile of decode work for one query slot.  The decode work
+// stream is [static tiles | dynamic tiles]: static tiles (the dense window:
+// sink + recent tail, or every row for full attention) are planned on the host
+// once per (cache, window, heads) and are ready when the step starts; dynamic
+// tiles (selected buckets, general-window gathers) are appended by the
+// planner and published through `ready` (the decode producer clears it).
+struct alignas(16) TileRec {
     uint32_t npieces;
-    uint32_t pad[3];
+    uint32_t qslot;  // group * n_hchunks + head chunk
+    uint32_t ready;  // dynamic tiles: 1 = published
+    uint32_t end;    // 1: last tile of its slot's contiguous range (a run ends here)
     PieceRec p[kMaxPieces];
 };
 constexpr uint32_t kPieceGather = 0x80000000u;
@@ -48,13 +56,6 @@ struct ApproxArgs {
     uint32_t G, C;
     float* approx;                 // [groups][C]
 };
-struct ItemRec {
-    uint32_t qslot;
-    uint32_t tile_first;
-    uint32_t ntiles;
-    uint32_t pad;
-};
-
 struct PlanArgs {
     const GroupMeta* meta;
     const uint32_t* off;
@@ -68,7 +69,6 @@ struct PlanArgs {
     const double* scores;        // [groups][G][C] per-row probabilities (mode 2)
     uint32_t G, D, n_hchunks;
     uint32_t probes, recent;
-    uint32_t item_tiles;
     uint32_t P2;                 // pow2 >= n_slices * keep (candidates to merge)
     uint32_t n_cand;             // n_slices * keep
     const double* cand_s;        // routing candidates from route_score_kernel
@@ -85,37 +85,56 @@ struct PlanArgs {
     uint16_t* gK;
     uint16_t* gV;
     uint64_t gather_cap;         // rows per group in the gather buffer
-    const float* q_attn;         // [groups][G][D] queries the attention uses (roped)
-    uint16_t* qA;                // out: [qslots][16][D] bf16 A operand (3-term split, swizzled)
     // outputs
-    TileRec* tiles;
-    ItemRec* items;
-    StepCounters* ctr;           // n_items, work, n_tiles (pad[0])
-    QSlot* qslots;
+    TileRec* dyn_tiles;          // dynamic part of the work stream
+    StepCounters* ctr;           // dyn (tiles reserved), groups_done
+    uint32_t* dyn_cnt;           // [qslots] dynamic tiles | kCntValid
     saap_attn_stats* stats;
     uint32_t* selected;          // nullable [groups][probes]
-    float* out;                  // [groups][G][D]
 };
+constexpr uint32_t kCntValid = 0x80000000u;
 
 struct DecodeArgs {
-    const ItemRec* items;
-    const TileRec* tiles;
+    const TileRec* st_tiles;   // static part of the work stream [n_static]
+    TileRec* dyn_tiles;        // dynamic part (ready flags cleared after use)
+    uint32_t n_static;
+    uint32_t n_plan_groups;    // planner CTAs that publish dynamic tiles (0: static only)
+    uint32_t chunk;            // work-stream tiles per ticket
+    uint32_t tail;             // the stream's last `tail` tiles go out one per ticket
     StepCounters* ctr;
-    const uint16_t* qA;  // [qslots][16][D] prepared by route_plan_kernel
+    const float* q;            // [groups][G][D] attention queries (f32)
     uint32_t G;
     uint32_t n_hchunks;
     float qscale;  // log2(e)/sqrt(d): scores live in the exp2 domain
-    float* part_O;
-    float* part_ml;  // [items][2][4]: m then l
-    const QSlot* qslots;
-    uint32_t* done;
-    float* out;
+    float* part_O;   // [qslots][run_cap][4][D] unnormalised run partials
+    float* part_ml;  // [qslots][run_cap][8]: m then l
+    uint32_t run_cap;
+    uint32_t* runs;  // [qslots] runs reserved
+    uint32_t* done;  // [qslots] tiles published
     unsigned long long* dtrace;  // debug: per CTA {start, first tile, end (globaltimer ns), tiles}
 };
 
+struct CombineArgs {
+    const uint32_t* st_cnt;  // [qslots] static tiles
+    uint32_t* dyn_cnt;       // [qslots] dynamic tiles | kCntValid (null: static only)
+    uint32_t* runs;
+    uint32_t* done;
+    const float* part_O;
+    const float* part_ml;
+    uint32_t run_cap;
+    uint32_t G, n_hchunks;
+    float* out;
+};
+
+// Decode tiles live in shared memory as 8-row groups [group][half][8 rows][HALF
+// bytes] (HALF = min(row bytes, 128), TMA-swizzled).  One 4-D TMA request
+// moves 8*2^i rows (i = 0..4) of both halves of K (or V) straight into that
+// layout: dims {HALF elems, rows, halves, 16 groups} with strides {row, HALF,
+// 8 rows} (the group dimension overlaps the row dimension on purpose).
+constexpr int kBoxSizes = 5;  // boxes of 8, 16, 32, 64, 128 rows
 struct DecodeMaps {
-    CUtensorMap k64, k8, v64, v8;    // layer (or dense) cache, boxes of 64 / 8 rows
-    CUtensorMap gk64, gk8, gv64, gv8;  // gather buffer
+    CUtensorMap k[kBoxSizes], v[kBoxSizes];    // layer (or dense) cache
+    CUtensorMap gk[kBoxSizes], gv[kBoxSizes];  // gather buffer
 };
 
 struct QModelArgs {
@@ -128,5 +147,7 @@ struct QModelArgs {
 // host: TMA descriptor for a [rows x D] bf16 row-major tensor, boxes of
 // (min(D,64) elements x box_rows rows) with the matching swizzle.
 CUtensorMap make_row_map(const void* base, uint64_t rows, uint32_t D, uint32_t box_rows);
+// host: the 4-D grouped view above, boxes of 8 * groups rows
+CUtensorMap make_group_map(const void* base, uint64_t rows, uint32_t D, uint32_t groups);
 
 }  // namespace saap_b200

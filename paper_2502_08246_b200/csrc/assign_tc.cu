@@ -440,6 +440,23 @@ CUtensorMap make_row_map(const void* base, uint64_t rows, uint32_t D, uint32_t b
     return m;
 }
 
+CUtensorMap make_group_map(const void* base, uint64_t rows, uint32_t D, uint32_t groups) {
+    CUtensorMap m;
+    const uint32_t inner = D >= 64 ? 64 : D;   // elements per swizzle row (128 or 64 bytes)
+    const uint32_t halves = D / inner;
+    const cuuint64_t dims[4] = {(cuuint64_t)inner, (cuuint64_t)(rows ? rows : 1), (cuuint64_t)halves, 16};
+    const cuuint64_t strides[3] = {(cuuint64_t)D * 2, (cuuint64_t)inner * 2, (cuuint64_t)D * 2 * 8};
+    const cuuint32_t box[4] = {inner, 8, halves, groups};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
+                             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             inner == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        fail(SAAP_ERR_CUDA, "cuTensorMapEncodeTiled (grouped rows) failed: " + std::to_string((int)r));
+    return m;
+}
+
 uint32_t tc_cpad(uint32_t C) { return (C + tc::CN - 1) / tc::CN * tc::CN; }
 
 void launch_split_centroids(const float* cent, uint32_t C, uint32_t D, uint16_t* hi, uint16_t* mid,

@@ -18,8 +18,7 @@ void launch_route_plan(const PlanArgs& a, uint32_t n_groups, bool pdl, cudaStrea
 void launch_route_approx(int D, const ApproxArgs& a, uint32_t n_slots, cudaStream_t st);
 void launch_route_score(const RouteArgs& a, uint32_t n_groups, cudaStream_t st);
 void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st);
-void launch_combine(int D, const QSlot* qs, uint32_t n_qslots, uint32_t G, uint32_t n_hchunks,
-                    const float* pO, const float* pml, float* out, cudaStream_t st);
+void launch_combine(int D, const CombineArgs& ca, uint32_t n_qslots, cudaStream_t st);
 void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st);
 void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t n_tiles,
                          const void* keys, const uint64_t* key_row0, const double* const* cent64,
@@ -148,6 +147,14 @@ void ensure_done(saap_ctx* c, size_t n) {
     SAAP_CUDA(cudaMalloc(&c->done, cap * 4));
     SAAP_CUDA(cudaMemset(c->done, 0, cap * 4));
     c->done_cap = cap;
+}
+
+// scratch whose contents must start at zero (per-slot step counters)
+void* ensure_zero(saap_ctx* c, saap_scratch& s, size_t bytes) {
+    if (bytes <= s.cap) return s.p;
+    void* p = ensure(c, s, bytes);
+    SAAP_CUDA(cudaMemset(p, 0, s.cap));
+    return p;
 }
 
 struct DeviceGuard {
@@ -350,13 +357,13 @@ void enqueue_route_score(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
     pa.cand_i = ci;
 }
 
-// 128-row tiles per work item (SAAP_ITEM_TILES / SAAP_ITEM_TILES_DENSE override, tuning only)
+// work-stream tiles per decode ticket (SAAP_CHUNK / SAAP_CHUNK_DENSE override, tuning only)
 uint32_t env_u32(const char* name, uint32_t dflt) {
     const char* v = std::getenv(name);
-    return v && *v ? (uint32_t)std::max(1, std::atoi(v)) : dflt;
+    return v && *v ? (uint32_t)std::min(32, std::max(1, std::atoi(v))) : dflt;
 }
-const uint32_t kItemTilesSparse = env_u32("SAAP_ITEM_TILES", 4);
-const uint32_t kItemTilesDense = env_u32("SAAP_ITEM_TILES_DENSE", 16);
+const uint32_t kChunkSparse = env_u32("SAAP_CHUNK", 4);
+const uint32_t kChunkDense = env_u32("SAAP_CHUNK_DENSE", 16);
 
 // Everything a decode step reads about its cache.
 struct DecodeSrc {
@@ -373,26 +380,113 @@ struct DecodeSrc {
 DecodeMaps* build_maps(const void* K, const void* V, uint64_t rows, uint32_t D, const void* gK,
                        const void* gV, uint64_t grows) {
     auto* m = new DecodeMaps;
-    m->k64 = make_row_map(K, rows, D, 64);
-    m->k8 = make_row_map(K, rows, D, 8);
-    m->v64 = make_row_map(V, rows, D, 64);
-    m->v8 = make_row_map(V, rows, D, 8);
     const void* a = gK ? gK : K;
     const void* b = gV ? gV : V;
     const uint64_t r = gK ? grows : rows;
-    m->gk64 = make_row_map(a, r, D, 64);
-    m->gk8 = make_row_map(a, r, D, 8);
-    m->gv64 = make_row_map(b, r, D, 64);
-    m->gv8 = make_row_map(b, r, D, 8);
+    for (int i = 0; i < kBoxSizes; ++i) {
+        m->k[i] = make_group_map(K, rows, D, 1u << i);
+        m->v[i] = make_group_map(V, rows, D, 1u << i);
+        m->gk[i] = make_group_map(a, r, D, 1u << i);
+        m->gv[i] = make_group_map(b, r, D, 1u << i);
+    }
     return m;
 }
 
-// Enqueue one decode step (routing, planning, attention, combine) on the
-// context stream.  mode: 0 dense/full, 1 centroid, 2 Q-model, 3 window only.
-void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const float* const* centT,
-                    const double* const* qm, const float* q_roped, const float* q_route,
-                    uint64_t G, uint64_t probes, uint64_t recent, float* out,
-                    saap_attn_stats* stats, uint32_t* selected, uint32_t item_tiles,
+// Static part of a decode work stream, planned on the host: per group the
+// dense window (sink span [0, sink) and the recent tail [max(n - recent, T), n)
+// of the packed layout), or every row when the window covers the context or
+// for full attention (mode 0).  Segments take 8-aligned virtual rows and are
+// cut into 128-row tiles (attention.cpp:342-347: the window is absorbed
+// before any bucket).
+saap_static_plan* build_static_plan(const std::vector<GroupMeta>& meta, int mode, uint64_t recent,
+                                    uint32_t nh) {
+    auto* sp = new saap_static_plan;
+    sp->mode = mode;
+    sp->recent = recent;
+    sp->n_hchunks = nh;
+    std::vector<TileRec> tiles;
+    std::vector<uint32_t> cnt(meta.size() * nh, 0);
+    for (size_t g = 0; g < meta.size(); ++g) {
+        const GroupMeta& gm = meta[g];
+        const uint64_t n = gm.n, sink = gm.sink, T = gm.T;
+        std::vector<std::pair<uint64_t, uint64_t>> segs;  // (first row, rows)
+        if (mode == 0 || n <= sink + recent) {
+            segs.push_back({0, n});
+        } else {
+            const uint64_t rb = n - recent, tail0 = std::max(rb, T);
+            if (sink) segs.push_back({0, sink});
+            if (n > tail0) segs.push_back({tail0, n - tail0});
+        }
+        std::vector<uint64_t> v0(segs.size());
+        uint64_t v = 0;
+        for (size_t i = 0; i < segs.size(); ++i) {
+            v0[i] = v;
+            v += (segs[i].second + 7) & ~7ull;
+        }
+        const uint64_t ntiles = (v + kTileRows - 1) / kTileRows;
+        std::vector<TileRec> gt(ntiles);
+        for (auto& t : gt) std::memset(&t, 0, sizeof t);
+        for (size_t i = 0; i < segs.size(); ++i) {
+            const uint64_t s0 = v0[i], s8 = s0 + ((segs[i].second + 7) & ~7ull), send = s0 + segs[i].second;
+            for (uint64_t t = s0 / kTileRows; t * kTileRows < s8; ++t) {
+                const uint64_t a0 = std::max(s0, t * kTileRows), b0 = std::min(s8, (t + 1) * kTileRows);
+                const uint64_t kend = std::min(b0, send);
+                if (kend <= a0) continue;
+                TileRec& tr = gt[t];
+                PieceRec& pr = tr.p[tr.npieces++];
+                pr.len = (uint32_t)(kend - a0);
+                pr.srow = (uint32_t)(a0 - t * kTileRows);
+                pr.row = gm.row_base + segs[i].first + (a0 - s0);
+            }
+        }
+        for (uint32_t hc = 0; hc < nh; ++hc) {
+            for (size_t i = 0; i < gt.size(); ++i) {
+                TileRec t = gt[i];
+                t.qslot = (uint32_t)(g * nh + hc);
+                t.ready = 0;
+                t.end = i + 1 == gt.size() ? 1u : 0u;
+                tiles.push_back(t);
+            }
+            cnt[g * nh + hc] = (uint32_t)ntiles;
+        }
+        sp->max_slot_tiles = std::max<uint32_t>(sp->max_slot_tiles, (uint32_t)ntiles);
+    }
+    sp->n_tiles = (uint32_t)tiles.size();
+    sp->tiles = dmalloc<TileRec>(std::max<size_t>(tiles.size(), 1));
+    sp->cnt = dmalloc<uint32_t>(std::max<size_t>(cnt.size(), 1));
+    if (!tiles.empty())
+        SAAP_CUDA(cudaMemcpy(sp->tiles, tiles.data(), tiles.size() * sizeof(TileRec), cudaMemcpyHostToDevice));
+    if (!cnt.empty())
+        SAAP_CUDA(cudaMemcpy(sp->cnt, cnt.data(), cnt.size() * 4, cudaMemcpyHostToDevice));
+    return sp;
+}
+
+void free_static_plan(saap_static_plan* sp) {
+    if (!sp) return;
+    if (sp->tiles) cudaFree(sp->tiles);
+    if (sp->cnt) cudaFree(sp->cnt);
+    delete sp;
+}
+
+// cached per handle: plans depend only on the (immutable) group layout
+const saap_static_plan* static_plan(saap_ctx* c, std::vector<saap_static_plan*>& cache,
+                                    const std::vector<GroupMeta>& meta, int mode, uint64_t recent,
+                                    uint32_t nh) {
+    const uint64_t rkey = mode == 0 ? 0 : recent;
+    for (auto* p : cache)
+        if (p->mode == mode && p->recent == rkey && p->n_hchunks == nh) return p;
+    if (c->capturing) invalid("decode plan for a new window/head count during graph capture: run once uncaptured first");
+    cache.push_back(build_static_plan(meta, mode, rkey, nh));
+    return cache.back();
+}
+
+// Enqueue one decode step on the context stream: [Q-model] -> [routing] ->
+// planner (dynamic tiles) -> decode (static + dynamic work stream) -> combine.
+// mode: 0 dense/full (no planner), 1 centroid, 2 Q-model, 3 window only.
+void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* sp, int mode,
+                    const float* const* centT, const double* const* qm, const float* q_attn,
+                    const float* q_route, uint64_t G, uint64_t probes, uint64_t recent, float* out,
+                    saap_attn_stats* stats, uint32_t* selected, uint32_t chunk,
                     uint32_t qm_hidden = 0, const float* cmax = nullptr,
                     const float* const* centR = nullptr, const uint32_t* slots = nullptr,
                     uint32_t n_slots = 0) {
@@ -400,99 +494,114 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, int mode, const float* co
     const uint64_t n_groups = src.n_groups, D = src.D, C = src.C;
     const uint64_t n_hchunks = (G + kHeadsPerSlot - 1) / kHeadsPerSlot;
     const uint64_t qslots = n_groups * n_hchunks;
-    const uint64_t nseg = probes + 4;
-    const uint64_t per_group_tiles = (src.max_n + 8 * nseg) / kTileRows + nseg + 2;
-    const uint64_t max_tiles = n_groups * per_group_tiles;
-    const uint64_t max_items = max_tiles * n_hchunks;
-    TileRec* tiles = (TileRec*)ensure(c, c->tiles, max_tiles * sizeof(TileRec));
-    ItemRec* items = (ItemRec*)ensure(c, c->items, max_items * sizeof(ItemRec));
-    QSlot* qs = (QSlot*)ensure(c, c->qslots, qslots * sizeof(QSlot));
-    uint16_t* qA = (uint16_t*)ensure(c, c->qA, qslots * 16 * D * sizeof(uint16_t));
-    float* pO = (float*)ensure(c, c->part_O, max_items * kHeadsPerSlot * D * sizeof(float));
-    float* pml = (float*)ensure(c, c->part_ml, max_items * 8 * sizeof(float));
-    if (!stats) stats = (saap_attn_stats*)ensure(c, c->stats, n_groups * sizeof(saap_attn_stats));
+    if (reinterpret_cast<uintptr_t>(q_attn) & 15) invalid("decode: queries must be 16-byte aligned");
+    const bool plan = mode != 0;
+    const uint64_t nseg = probes + 2;
+    const uint64_t dyn_per_group = plan ? (src.max_n + 8 * nseg) / kTileRows + nseg + 2 : 0;
+    // a run is >= 1 tile of one slot (the stream's tail goes out tile by tile)
+    const uint64_t run_cap = sp->max_slot_tiles + dyn_per_group + 2;
+    TileRec* dyn = plan ? (TileRec*)ensure_zero(c, c->tiles, n_groups * dyn_per_group * n_hchunks * sizeof(TileRec))
+                        : nullptr;
+    float* pO = (float*)ensure(c, c->part_O, qslots * run_cap * kHeadsPerSlot * D * sizeof(float));
+    float* pml = (float*)ensure(c, c->part_ml, qslots * run_cap * 8 * sizeof(float));
+    uint32_t* runs = (uint32_t*)ensure_zero(c, c->runs, qslots * 4);
+    uint32_t* dcnt = plan ? (uint32_t*)ensure_zero(c, c->dyn_cnt, qslots * 4) : nullptr;
     ensure_done(c, qslots);
+    if (plan && !stats) stats = (saap_attn_stats*)ensure(c, c->stats, n_groups * sizeof(saap_attn_stats));
     double* probs = nullptr;
     if (mode == 2) probs = (double*)ensure(c, c->probs, n_groups * G * C * sizeof(double));
 
-    SAAP_CUDA(cudaMemsetAsync(c->counters, 0, sizeof(StepCounters), st));
-    if (mode == 2) {
-        QModelArgs qa{};
-        qa.q = q_route;
-        qa.prm = qm;
-        qa.G = (uint32_t)G;
-        qa.d = (uint32_t)D;
-        qa.h = qm_hidden;
-        qa.C = (uint32_t)C;
-        qa.probs = probs;
-        launch_qmodel_probs(qa, (uint32_t)n_groups, st);
-        c->launches++;
-    }
-    PlanArgs pa{};
-    pa.meta = src.meta;
-    pa.off = src.off;
-    pa.offA = src.offA;
-    pa.idx = src.idx;
-    pa.assign = src.assign;
-    pa.invA = src.invA;
-    pa.C = (uint32_t)C;
-    pa.mode = mode;
-    pa.q_route = q_route;
-    pa.scores = probs;
-    pa.G = (uint32_t)G;
-    pa.D = (uint32_t)D;
-    pa.n_hchunks = (uint32_t)n_hchunks;
-    pa.probes = (uint32_t)probes;
-    pa.recent = (uint32_t)std::min<uint64_t>(recent, 0xFFFFFFFFull);
-    pa.item_tiles = item_tiles;
-    pa.route_only = 0;
-    pa.K = src.K;
-    pa.V = src.V;
-    pa.gK = src.gK;
-    pa.gV = src.gV;
-    pa.gather_cap = src.gather_cap;
-    pa.q_attn = q_roped;
-    pa.qA = qA;
-    pa.tiles = tiles;
-    pa.items = items;
-    pa.ctr = c->counters;
-    pa.qslots = qs;
-    pa.stats = stats;
-    pa.selected = selected;
-    pa.out = out;
     cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
     if (c->timing && !c->capturing) {
         for (cudaEvent_t* e : {&e0, &e1, &e2}) SAAP_CUDA(cudaEventCreate(e));
         SAAP_CUDA(cudaEventRecord(e0, st));
     }
-    const bool routed = (mode == 1 || mode == 2) && probes > 0;
-    if (routed)
-        enqueue_route_score(c, n_groups, D, C, G, probes, mode, centT, q_route, probs, pa, cmax,
-                            centR, slots, n_slots);
-    static const bool trace_on = std::getenv("SAAP_PLAN_TRACE") != nullptr;
-    if (trace_on) pa.trace = (unsigned long long*)ensure(c, c->trace, 128);
-    launch_route_plan(pa, (uint32_t)n_groups, routed, st);
-    c->launches++;
+    if (plan) {
+        if (mode == 2) {
+            QModelArgs qa{};
+            qa.q = q_route;
+            qa.prm = qm;
+            qa.G = (uint32_t)G;
+            qa.d = (uint32_t)D;
+            qa.h = qm_hidden;
+            qa.C = (uint32_t)C;
+            qa.probs = probs;
+            launch_qmodel_probs(qa, (uint32_t)n_groups, st);
+            c->launches++;
+        }
+        PlanArgs pa{};
+        pa.meta = src.meta;
+        pa.off = src.off;
+        pa.offA = src.offA;
+        pa.idx = src.idx;
+        pa.assign = src.assign;
+        pa.invA = src.invA;
+        pa.C = (uint32_t)C;
+        pa.mode = mode;
+        pa.q_route = q_route;
+        pa.scores = probs;
+        pa.G = (uint32_t)G;
+        pa.D = (uint32_t)D;
+        pa.n_hchunks = (uint32_t)n_hchunks;
+        pa.probes = (uint32_t)probes;
+        pa.recent = (uint32_t)std::min<uint64_t>(recent, 0xFFFFFFFFull);
+        pa.route_only = 0;
+        pa.K = src.K;
+        pa.V = src.V;
+        pa.gK = src.gK;
+        pa.gV = src.gV;
+        pa.gather_cap = src.gather_cap;
+        pa.dyn_tiles = dyn;
+        pa.ctr = c->counters;
+        pa.dyn_cnt = dcnt;
+        pa.stats = stats;
+        pa.selected = selected;
+        const bool routed = (mode == 1 || mode == 2) && probes > 0;
+        if (routed)
+            enqueue_route_score(c, n_groups, D, C, G, probes, mode, centT, q_route, probs, pa, cmax,
+                                centR, slots, n_slots);
+        static const bool trace_on = std::getenv("SAAP_PLAN_TRACE") != nullptr;
+        if (trace_on) pa.trace = (unsigned long long*)ensure(c, c->trace, 128);
+        launch_route_plan(pa, (uint32_t)n_groups, routed, st);
+        c->launches++;
+    }
     if (e1) SAAP_CUDA(cudaEventRecord(e1, st));
 
     DecodeArgs da{};
-    da.items = items;
-    da.tiles = tiles;
+    da.st_tiles = (const TileRec*)sp->tiles;
+    da.dyn_tiles = dyn;
+    da.n_static = sp->n_tiles;
+    da.n_plan_groups = plan ? (uint32_t)n_groups : 0u;
+    da.chunk = chunk;
     da.ctr = c->counters;
-    da.qA = qA;
+    da.q = q_attn;
     da.G = (uint32_t)G;
     da.n_hchunks = (uint32_t)n_hchunks;
     da.qscale = (float)(1.4426950408889634 / std::sqrt((double)D));
     da.part_O = pO;
     da.part_ml = pml;
-    da.qslots = qs;
+    da.run_cap = (uint32_t)run_cap;
+    da.runs = runs;
     da.done = c->done;
-    da.out = out;
-    const int grid = (int)std::min<uint64_t>((uint64_t)c->sm_count, max_items);
+    const uint64_t max_stream = sp->n_tiles + n_groups * dyn_per_group * n_hchunks;
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->sm_count,
+                                                                    (max_stream + chunk - 1) / chunk));
+    da.tail = env_u32("SAAP_TAIL_PER_CTA", 2) * (uint32_t)grid;
     static const bool dtrace_on = std::getenv("SAAP_DECODE_TRACE") != nullptr;
-    if (dtrace_on) da.dtrace = (unsigned long long*)ensure(c, c->dtrace, (size_t)c->sm_count * 32);
-    launch_decode((int)D, *src.maps, da, std::max(grid, 1), st);
-    launch_combine((int)D, qs, (uint32_t)qslots, (uint32_t)G, (uint32_t)n_hchunks, pO, pml, out, st);
+    if (dtrace_on) da.dtrace = (unsigned long long*)ensure(c, c->dtrace, (size_t)c->sm_count * 128);
+    launch_decode((int)D, *src.maps, da, grid, st);
+    CombineArgs ca{};
+    ca.st_cnt = sp->cnt;
+    ca.dyn_cnt = dcnt;
+    ca.runs = runs;
+    ca.done = c->done;
+    ca.part_O = pO;
+    ca.part_ml = pml;
+    ca.run_cap = (uint32_t)run_cap;
+    ca.G = (uint32_t)G;
+    ca.n_hchunks = (uint32_t)n_hchunks;
+    ca.out = out;
+    launch_combine((int)D, ca, (uint32_t)qslots, st);
     c->launches += 2;
     if (e2) {
         SAAP_CUDA(cudaEventRecord(e2, st));
@@ -597,9 +706,9 @@ int saap_ctx_destroy(saap_ctx* c) {
         if (!c) return;
         cudaSetDevice(c->device);
         cudaStreamSynchronize(c->stream);
-        for (saap_scratch* s : {&c->approx, &c->trace, &c->dtrace, &c->qA, &c->cand_s, &c->cand_i,
-                                &c->items, &c->tiles, &c->qslots, &c->part_O, &c->part_ml, &c->probs,
-                                &c->stats, &c->sel, &c->qr, &c->qd, &c->out, &c->misc, &c->zeros})
+        for (saap_scratch* s : {&c->approx, &c->trace, &c->dtrace, &c->cand_s, &c->cand_i,
+                                &c->tiles, &c->part_O, &c->part_ml, &c->probs, &c->stats, &c->sel,
+                                &c->qr, &c->qd, &c->out, &c->misc, &c->zeros, &c->runs, &c->dyn_cnt})
             if (s->p) cudaFree(s->p);
         dfree(c->counters);
         dfree(c->done);
@@ -844,7 +953,6 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
     pa.n_hchunks = 1;
     pa.probes = (uint32_t)l;
     pa.recent = 0;
-    pa.item_tiles = kItemTilesSparse;
     pa.route_only = 1;
     pa.selected = dsel;
     enqueue_route_score(c, 1, d, C, G, l, mode, (const float* const*)dptr, dq, probs, pa,
@@ -1083,6 +1191,7 @@ int saap_layer_destroy(saap_layer* L) {
         dfree(L->gK);
         dfree(L->gV);
         delete (DecodeMaps*)L->maps;
+        for (auto* p : L->plans) free_static_plan(p);
         dfree(L->off);
         dfree(L->offA);
         dfree(L->tiles);
@@ -1419,8 +1528,10 @@ static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* con
             need_gather |= gm.n > cfg->sink_count + cfg->recent_count &&
                            (cfg->recent_count > L->recent_hint || (mode != 3 && cfg->probes > 0));
     const DecodeSrc src = layer_src(L, cfg->recent_count, need_gather);
-    enqueue_decode(c, src, mode, L->d_centT, L->d_qm, qr, q_route, G, cfg->probes,
-                   cfg->recent_count, out, stats, selected, kItemTilesSparse, (uint32_t)hq,
+    const uint32_t nh = (uint32_t)((G + kHeadsPerSlot - 1) / kHeadsPerSlot);
+    const saap_static_plan* sp = static_plan(c, L->plans, L->h_meta, 1, cfg->recent_count, nh);
+    enqueue_decode(c, src, sp, mode, L->d_centT, L->d_qm, qr, q_route, G, cfg->probes,
+                   cfg->recent_count, out, stats, selected, kChunkSparse, (uint32_t)hq,
                    mode == 1 ? L->d_cmax : nullptr, mode == 1 ? L->d_centR : nullptr,
                    mode == 1 ? L->d_route_slots : nullptr, mode == 1 ? L->n_route_slots : 0);
 }
@@ -1512,8 +1623,10 @@ int saap_layer_full_attention(saap_ctx* c, const saap_layer* L, const float* q, 
         float* dout = (float*)ensure(c, c->out, qn * 4);
         h2d(dq, q, qn * 4, st);
         const DecodeSrc src = layer_src(const_cast<saap_layer*>(L), L->recent_hint, false);
-        enqueue_decode(c, src, 0, nullptr, nullptr, dq, nullptr, G, 0, 0, dout, nullptr, nullptr,
-                       kItemTilesDense);
+        const uint32_t nh = (uint32_t)((G + kHeadsPerSlot - 1) / kHeadsPerSlot);
+        const saap_static_plan* sp = static_plan(c, const_cast<saap_layer*>(L)->plans, L->h_meta, 0, 0, nh);
+        enqueue_decode(c, src, sp, 0, nullptr, nullptr, dq, nullptr, G, 0, 0, dout, nullptr, nullptr,
+                       kChunkDense);
         d2h(out, dout, qn * 4, st);
         sync(c);
     });
@@ -1557,10 +1670,14 @@ int saap_full_attention(saap_ctx* c, const float* q, uint64_t G, const float* ke
         src.V = Vb;
         std::unique_ptr<DecodeMaps> maps(build_maps(Kb, Vb, n, (uint32_t)d, nullptr, nullptr, 0));
         src.maps = maps.get();
-        enqueue_decode(c, src, 0, nullptr, nullptr, dq, nullptr, G, 0, 0, dout, nullptr, nullptr,
-                       kItemTilesDense);
+        const uint32_t nh = (uint32_t)((G + kHeadsPerSlot - 1) / kHeadsPerSlot);
+        if (c->capturing) invalid("full_attention: not capturable (uploads its keys)");
+        saap_static_plan* sp = build_static_plan({gm}, 0, 0, nh);
+        enqueue_decode(c, src, sp, 0, nullptr, nullptr, dq, nullptr, G, 0, 0, dout, nullptr, nullptr,
+                       kChunkDense);
         d2h(out, dout, G * d * 4, st);
         sync(c);
+        free_static_plan(sp);
         cudaFree(f32);
         cudaFree(Kb);
         cudaFree(Vb);
@@ -1591,6 +1708,7 @@ int saap_kvcache_create(saap_ctx* c, uint64_t n_groups, uint64_t d, const void* 
             kc->max_n = std::max<uint64_t>(kc->max_n, n_keys[g]);
             kc->rows = std::max<uint64_t>(kc->rows, row_base[g] + n_keys[g]);
         }
+        kc->h_meta = m;
         kc->maps = build_maps(K, V, kc->rows, (uint32_t)d, nullptr, nullptr, 0);
         kc->meta = dmalloc<GroupMeta>(n_groups);
         kc->row_base = dmalloc<uint64_t>(n_groups);
@@ -1606,6 +1724,7 @@ int saap_kvcache_destroy(saap_kvcache* kc) {
         cudaSetDevice(kc->ctx->device);
         dfree(kc->meta);
         dfree(kc->row_base);
+        for (auto* p : kc->plans) free_static_plan(p);
         delete (DecodeMaps*)kc->maps;
         delete kc;
     });
@@ -1626,8 +1745,11 @@ int saap_dense_attention_dev(saap_ctx* c, const saap_kvcache* kc, const float* q
         src.K = kc->K;
         src.V = kc->V;
         src.maps = (const DecodeMaps*)kc->maps;
-        enqueue_decode(c, src, 0, nullptr, nullptr, q, nullptr, G, 0, 0, out, nullptr, nullptr,
-                       kItemTilesDense);
+        const uint32_t nh = (uint32_t)((G + kHeadsPerSlot - 1) / kHeadsPerSlot);
+        const saap_static_plan* sp =
+                static_plan(c, const_cast<saap_kvcache*>(kc)->plans, kc->h_meta, 0, 0, nh);
+        enqueue_decode(c, src, sp, 0, nullptr, nullptr, q, nullptr, G, 0, 0, out, nullptr, nullptr,
+                       kChunkDense);
     });
 }
 
@@ -1695,7 +1817,7 @@ int saap_debug_decode_trace(saap_ctx* c, uint64_t* out, uint64_t n_ctas) {
         DeviceGuard dg(c);
         if (!c->dtrace.p) invalid("decode tracing off: set SAAP_DECODE_TRACE before the first decode");
         if (n_ctas > (uint64_t)c->sm_count) invalid("decode trace: more CTAs than SMs");
-        d2h(out, c->dtrace.p, n_ctas * 32, c->stream);
+        d2h(out, c->dtrace.p, n_ctas * 128, c->stream);
         sync(c);
     });
 }

@@ -57,13 +57,6 @@ struct GroupMeta {
     uint32_t pad;
 };
 
-// A unit of decode work: up to item_keys consecutive keys of one segment,
-// for one query slot (group, chunk of <= 4 query heads).
-struct Item {
-    uint32_t qslot;
-    uint32_t n_kind;  // n (low 30 bits) | kind << 30
-    uint64_t start;   // kind 0: first row (group-relative); kind 1/2: list index (absolute)
-};
 enum : uint32_t { KIND_ROWS = 0, KIND_INVA = 1, KIND_LIST = 2 };
 
 constexpr uint32_t kPackTile = 2048;  // local ids per histogram / assignment tile
@@ -75,16 +68,14 @@ struct TileDesc {
     uint32_t pad;
 };
 
-struct QSlot {
-    uint32_t base;   // first item
-    uint32_t count;  // items
-};
-
-// Per-step device counters (zeroed with one memset at the start of a step).
+// Per-step device counters.  Zero at allocation; the last decode CTA of a
+// step resets them for the next step (every reader has finished by then).
 struct StepCounters {
-    uint32_t n_items;
-    uint32_t work;
-    uint32_t pad[30];
+    uint32_t tickets;      // work-stream chunks handed out beyond the first gridDim.x
+    uint32_t dyn;          // dynamic tiles reserved by the planner
+    uint32_t groups_done;  // planner CTAs that finished reserving
+    uint32_t exited;       // decode CTAs finished
+    uint32_t pad[28];
 };
 
 constexpr int kHeadsPerSlot = 4;  // query heads processed together (GQA group)
@@ -150,6 +141,14 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -179,7 +178,8 @@ struct saap_ctx {
     bool own_stream = false;
     uint64_t launches = 0;
     // growable device scratch (sized by uncaptured calls; graphs reuse it)
-    saap_scratch approx, trace, dtrace, qA, cand_s, cand_i, items, tiles, qslots, part_O, part_ml, probs, stats, sel, qr, qd, out, misc, zeros;
+    saap_scratch approx, trace, dtrace, cand_s, cand_i, tiles, part_O, part_ml, probs, stats, sel, qr, qd, out, misc, zeros;
+    saap_scratch runs, dyn_cnt;  // per query slot, zero between steps (the combine re-arms them)
     saap_b200::StepCounters* counters = nullptr;  // persistent, 128 B
     uint32_t* done = nullptr;                     // per query slot completion counters
     size_t done_cap = 0;
@@ -189,6 +189,18 @@ struct saap_ctx {
     // optional per-kernel timing (eager steps)
     bool timing = false;
     std::vector<cudaEvent_t> ev;  // triples: before plan, before attention, after
+};
+
+// Host-planned static part of a decode work stream (the dense window, or
+// every row for full attention) for one (cache, mode, recent, head chunks).
+struct saap_static_plan {
+    int mode = 0;
+    uint64_t recent = 0;
+    uint32_t n_hchunks = 0;
+    void* tiles = nullptr;      // TileRec[n_tiles] (device)
+    uint32_t n_tiles = 0;
+    uint32_t* cnt = nullptr;    // [qslots] static tiles per query slot (device)
+    uint32_t max_slot_tiles = 0;
 };
 
 struct saap_partition {
@@ -270,6 +282,7 @@ struct saap_layer {
     uint16_t* gK = nullptr;            // gather buffer for general windows
     uint16_t* gV = nullptr;
     uint64_t gather_cap = 0;           // rows per group
+    std::vector<saap_static_plan*> plans;  // static work streams by (mode, recent, head chunks)
 };
 
 struct saap_kvcache {
@@ -280,6 +293,8 @@ struct saap_kvcache {
     saap_b200::GroupMeta* meta = nullptr;
     uint64_t* row_base = nullptr;
     void* maps = nullptr;  // DecodeMaps
+    std::vector<saap_b200::GroupMeta> h_meta;
+    std::vector<saap_static_plan*> plans;
 };
 
 struct saap_graph {

@@ -313,24 +313,6 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         if (a.trace && route && g == 0 && tid == 0) a.trace[k] = clock64() - t0;
     };
     if (a.trace && g == 0 && tid == 0) t0 = clock64();
-    // query slots' A operands for QK^T: rows 0-3 q1, 4-7 q2, 8-11 q3 (3-term
-    // bf16 split of the f32 queries, ~fp32-exact), rows 12-15 zero.  Independent
-    // of routing: issued first so its loads overlap the routing phases.
-    for (uint32_t e = tid; a.qA && !a.route_only && e < a.n_hchunks * 16 * a.D; e += nth) {
-        const uint32_t hc = e / (16 * a.D), r = (e / a.D) % 16, d = e % a.D;
-        const uint32_t head = hc * kHeadsPerSlot + (r & 3);
-        float v = 0.f;
-        if (r < 12 && head < a.G) {
-            const float x = a.q_attn[((size_t)g * a.G + head) * a.D + d];
-            const float t1 = __uint_as_float((uint32_t)f32_to_bf16_rne(x) << 16);
-            const float r1 = x - t1;
-            const float t2 = __uint_as_float((uint32_t)f32_to_bf16_rne(r1) << 16);
-            v = r < 4 ? t1 : (r < 8 ? t2 : r1 - t2);
-        }
-        uint16_t* dst = a.qA + (size_t)(g * a.n_hchunks + hc) * 16 * a.D;
-        *reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(dst) + swz_elem(a.D, 16, r, d)) =
-                f32_to_bf16_rne(v);
-    }
     // the group's bucket offsets, staged while routing runs (C <= kStageOff)
     const bool stage_off = route && !a.route_only && Cb + 1 <= kStageOff;
     uint32_t* s_off = vpre + L + 4;
@@ -509,6 +491,9 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
     if (a.route_only) return;
 
     // ---------------- segments of the visited set      attention.cpp:342-372
+    // The dense window (sink span + recent tail) is static work planned on the
+    // host; this CTA appends the routed bucket segments and, for general
+    // windows, the gathered rows.
     const uint32_t rb = fallback ? 0 : n - a.recent;  // recent_begin
     const uint32_t* offg = stage_off ? s_off : a.off + (size_t)g * (Cb + 1);
     const uint32_t* offAg = stage_off ? s_offA : a.offA + (size_t)g * (Cb + 1);
@@ -588,14 +573,7 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
     __syncthreads();
     if (tid == 0) {
         uint32_t nseg = L;
-        if (fallback) {
-            segs[nseg++] = Seg{KIND_ROWS, n, 0};
-        } else {
-            if (sink) segs[nseg++] = Seg{KIND_ROWS, sink, 0};
-            const uint32_t tail0 = rb > T ? rb : T;
-            if (n > tail0) segs[nseg++] = Seg{KIND_ROWS, n - tail0, tail0};
-            if (s_gbase) segs[nseg++] = Seg{KIND_LIST, s_gbase, gbuf};
-        }
+        if (!fallback && s_gbase) segs[nseg++] = Seg{KIND_LIST, s_gbase, gbuf};
         s_nseg = nseg;
     }
     __syncthreads();
@@ -629,13 +607,16 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         if (tid == 0) s_vrows = tot;
     }
     __syncthreads();
+    const uint32_t nh = a.n_hchunks;
     if (tid == 0) {
         const uint32_t ntiles = (s_vrows + kTileRows - 1) / kTileRows;
-        const uint32_t nitems = (ntiles + a.item_tiles - 1) / a.item_tiles;
         s_ntiles = ntiles;
-        s_nitems = nitems;
-        s_tile0 = ntiles ? atomicAdd(&a.ctr->pad[0], ntiles) : 0;
-        s_item0 = nitems ? atomicAdd(&a.ctr->n_items, nitems * a.n_hchunks) : 0;
+        // reserve this group's dynamic tiles, then report the reservation:
+        // decode producers treat the stream as final once every group has
+        s_tile0 = ntiles ? atomicAdd(&a.ctr->dyn, ntiles * nh) : 0;
+        __threadfence();
+        atomicAdd(&a.ctr->groups_done, 1u);
+        for (uint32_t hc = 0; hc < nh; ++hc) a.dyn_cnt[g * nh + hc] = ntiles | kCntValid;
         unsigned long long keys;
         if (fallback) keys = n;
         else keys = (unsigned long long)sink + (n - rb) + s_keys + s_filtered;
@@ -645,27 +626,23 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         st.empty_attention = keys == 0 ? 1 : 0;
         st.reserved = 0;
         a.stats[g] = st;
-        for (uint32_t hc = 0; hc < a.n_hchunks; ++hc)
-            a.qslots[g * a.n_hchunks + hc] = QSlot{s_item0 + hc * nitems, nitems};
     }
     __syncthreads();
     trace(5);
-    const uint32_t ntiles = s_ntiles, nitems = s_nitems, tile0 = s_tile0;
-    if (nitems == 0) {  // nothing visited: zero rows, empty_attention (attention.cpp:147-152)
-        for (uint32_t e = tid; e < a.G * a.D; e += nth) a.out[(size_t)g * a.G * a.D + e] = 0.f;
-        return;
-    }
+    const uint32_t ntiles = s_ntiles, tile0 = s_tile0;
+    if (ntiles == 0) return;
     // piece counters: shared memory when the group's tiles fit, else in place
     __shared__ uint32_t s_np[kPlanTileCnt];
     const bool np_smem = ntiles <= (uint32_t)kPlanTileCnt;
     for (uint32_t t = tid; t < ntiles; t += nth) {
         if (np_smem) s_np[t] = 0;
-        else a.tiles[tile0 + t].npieces = 0;
+        else a.dyn_tiles[tile0 + t].npieces = 0;
     }
     __syncthreads();
     trace(6);
     // pieces: one per (segment, overlapped tile); slot order inside a tile is
-    // free.  Short segments: one thread each; long ones: tiles spread over the CTA.
+    // free.  Short segments: one thread each; long ones: tiles spread over the
+    // CTA.  Head chunks > 0 get copies of chunk 0's tiles.
     auto emit = [&](const Seg& sg, uint32_t v0, uint32_t t) {
         const uint32_t v8 = v0 + ((sg.len + 7) & ~7u), vend = v0 + sg.len;
         const uint32_t a0 = max(v0, t * kTileRows), b0 = min(v8, (t + 1) * kTileRows);
@@ -675,9 +652,9 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         pr.len = (keys_end - a0) | (sg.kind == KIND_LIST ? kPieceGather : 0u);
         pr.srow = a0 - t * kTileRows;
         pr.row = (sg.kind == KIND_LIST ? 0 : gm.row_base) + sg.start + (a0 - v0);
-        TileRec* tr = a.tiles + tile0 + t;
+        TileRec* tr = a.dyn_tiles + tile0 + t;
         const uint32_t slot = atomicAdd(np_smem ? &s_np[t] : &tr->npieces, 1u);
-        tr->p[slot] = pr;
+        for (uint32_t hc = 0; hc < nh; ++hc) tr[(size_t)hc * ntiles].p[slot] = pr;
     };
     for (uint32_t s2 = tid; s2 < nseg; s2 += nth) {
         const Seg sg = segs[s2];
@@ -691,18 +668,16 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         const uint32_t v0 = vpre[s2], v8 = v0 + ((sg.len + 7) & ~7u);
         for (uint32_t t = v0 / kTileRows + tid; t * kTileRows < v8; t += nth) emit(sg, v0, t);
     }
-    for (uint32_t e = tid; e < nitems * a.n_hchunks; e += nth) {
-        const uint32_t hc = e / nitems, k = e % nitems;
-        ItemRec it;
-        it.qslot = g * a.n_hchunks + hc;
-        it.tile_first = tile0 + k * a.item_tiles;
-        it.ntiles = min(a.item_tiles, ntiles - k * a.item_tiles);
-        it.pad = 0;
-        a.items[s_item0 + e] = it;
-    }
-    if (np_smem) {
-        __syncthreads();
-        for (uint32_t t = tid; t < ntiles; t += nth) a.tiles[tile0 + t].npieces = s_np[t];
+    __threadfence();  // pieces before the headers' ready flags (release)
+    __syncthreads();
+    for (uint32_t e = tid; e < ntiles * nh; e += nth) {
+        const uint32_t hc = e / ntiles, t = e % ntiles;
+        TileRec* tr = a.dyn_tiles + tile0 + e;
+        tr->npieces = np_smem ? s_np[t] : a.dyn_tiles[tile0 + t].npieces;
+        tr->qslot = g * nh + hc;
+        tr->end = t + 1 == ntiles ? 1u : 0u;
+        __threadfence();
+        st_release_u32(&tr->ready, 1u);
     }
     trace(7);
 }
@@ -728,39 +703,66 @@ struct DecodeCfg {
     static constexpr int NT = D / 8;  // PV n-tiles
 };
 
+constexpr int kRecRing = 8;  // work records in flight ahead of the TMA issue
+
 template <int D>
-struct DecodeSmem2 {
+struct DecodeSmem {
     using CF = DecodeCfg<D>;
     uint8_t K[CF::NS][CF::TILE_BYTES];
     uint8_t V[CF::NS][CF::TILE_BYTES];
-    uint16_t qA[CF::NS][16][D];  // swizzled bf16 A operand of the item's query slot
+    float qraw[CF::NS][kHeadsPerSlot][D];  // f32 queries of the run's slot (first tile of a run)
     float redO[kComputeWarps][kHeadsPerSlot][D];
     float redm[kComputeWarps][kHeadsPerSlot];
     float redl[kComputeWarps][kHeadsPerSlot];
     uint64_t full[CF::NS];
     uint64_t empty[CF::NS];
-    int4 meta[CF::NS];    // item, tile-in-item | last<<31, qslot, nq (q heads loaded)
+    int4 meta[CF::NS];    // qslot (-1: end), flags (1 first | 2 last | nq << 8), run index, run tiles
     uint4 valid[CF::NS];  // 128-bit row validity mask
-    uint64_t st_full;   // 8 consumer warps deposited an item's (m, l, O) states
-    uint64_t st_empty;  // merge warp has read them
-    uint32_t st_item, st_qslot;
+    uint64_t st_full;     // the 8 consumer warps deposited a run's (m, l, O) states
+    uint64_t st_empty;    // the merge warp has read them
+    uint32_t st_slot, st_tiles;
+    // producer's work-record ring: records of upcoming tiles, bulk-copied ahead
+    alignas(16) TileRec rec[kRecRing];
+    uint64_t rec_bar[kRecRing];
+    uint32_t rec_w[kRecRing];     // work-stream index of the record
+    uint32_t rec_last[kRecRing];  // last tile of its chunk
 };
 
-// swizzled byte offset of (row, 16-byte chunk) inside one tile half
+// byte offset of (row, 16-byte chunk of the row) in a tile laid out as 8-row
+// groups [group][half][8][HALF] with the TMA swizzle (128B: chunk ^ row;
+// 64B: chunk ^ (row >> 1)); ldmatrix reads of 8 rows are conflict-free
 template <int D>
-__device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
+__device__ __forceinline__ uint32_t toff(uint32_t row, uint32_t chunk) {
     using CF = DecodeCfg<D>;
-    if constexpr (CF::HALF == 128) return row * 128 + ((chunk ^ (row & 7)) << 4);
-    else return row * 64 + ((chunk ^ ((row >> 1) & 3)) << 4);
+    constexpr uint32_t CPH = CF::HALF / 16;  // chunks per half row
+    const uint32_t g = row >> 3, r = row & 7, h = chunk / CPH, cc = chunk % CPH;
+    const uint32_t base = g * 8 * CF::RB + h * 8 * CF::HALF;
+    if constexpr (CF::HALF == 128) return base + r * 128 + ((cc ^ r) << 4);
+    else return base + r * 64 + ((cc ^ ((r >> 1) & 3)) << 4);
 }
 
+// K/V rows are streamed once per step: loaded with an L2 evict_first policy so
+// the step's small hot data (work records, offsets, partials) stays in L2.
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int x, int y,
-                                      uint64_t* bar) {
+                                      uint64_t* bar, uint64_t policy) {
     asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
-            "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
-            "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+            "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+            "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
             : "memory");
+}
+__device__ __forceinline__ void tma4d(void* dst, const CUtensorMap* map, int y, uint64_t* bar,
+                                      uint64_t policy) {
+    asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+            "[%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+            "l"(map), "r"(0), "r"(y), "r"(0), "r"(0), "r"(smem_u32(bar)), "l"(policy)
+            : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
 }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
@@ -795,7 +797,7 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
         decode_kernel(const __grid_constant__ DecodeMaps maps, DecodeArgs a) {
     using CF = DecodeCfg<D>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    auto& s = *reinterpret_cast<DecodeSmem2<D>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    auto& s = *reinterpret_cast<DecodeSmem<D>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     auto gtime = []() {
@@ -803,7 +805,7 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
         return t;
     };
-    if (a.dtrace && threadIdx.x == 0) a.dtrace[4 * blockIdx.x] = gtime();
+    if (a.dtrace && threadIdx.x == 0) a.dtrace[16 * blockIdx.x] = gtime();
     if (threadIdx.x == 0) {
         for (int i = 0; i < CF::NS; ++i) {
             mbar_init(&s.full[i], 1);
@@ -811,6 +813,7 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
         }
         mbar_init(&s.st_full, kComputeWarps);
         mbar_init(&s.st_empty, 1);
+        for (int i = 0; i < kRecRing; ++i) mbar_init(&s.rec_bar[i], 1);
         fence_mbar_init();
     }
     // gap rows of a tile are masked (p = 0) but still enter the PV MMA: start
@@ -819,249 +822,346 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
         reinterpret_cast<uint4*>(&s.V[0][0])[e] = make_uint4(0, 0, 0, 0);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
+    // No grid wait: static tiles are ready now, dynamic tiles are published
+    // by the (resident) planner through ready flags.  The combine grid may
+    // launch once every decode CTA is resident.
     pdl_trigger();
-    pdl_wait();  // everything above overlaps the planner's tail
-
-    const uint32_t n_items = *reinterpret_cast<volatile uint32_t*>(&a.ctr->n_items);
 
     if (warp == kComputeWarps + 1) {
         // ------------------------------------------------ merge warp
-        // LSE-merges the 8 consumer warps' states of each finished item and
-        // publishes it (output row, or a partial + the query slot's combine),
-        // off the consumers' critical path.
+        // LSE-merges the 8 consumer warps' states of a finished run into the
+        // run's partial (Alg. 2, attention.cpp:102-128), publishes it at gpu
+        // scope and counts its tiles for the combine -- off the consumers' path.
         constexpr int NOUT = kHeadsPerSlot * D;
         constexpr int PER = NOUT / 32;
         uint32_t ph = 0;
         for (;;) {
             mbar_wait(&s.st_full, ph);
-            const uint32_t cur_item = s.st_item, cur_qslot = s.st_qslot;
-            if (cur_item == 0xFFFFFFFFu) break;
-            const QSlot qs = a.qslots[cur_qslot];
-            const uint32_t g = cur_qslot / a.n_hchunks, hc = cur_qslot % a.n_hchunks;
-            float mh[4], lh[4], resO[PER];
+            ph ^= 1;
+            const uint32_t slot = s.st_slot, tiles = s.st_tiles;
+            if (slot == 0xFFFFFFFFu) break;
+            uint32_t run = 0;  // the run's partial slot (off the consumers' path)
+            if (lane == 0) run = atomicAdd(&a.runs[slot], 1u);
+            // lane = (warp w, head h): per-head max and scale of every warp state
+            const int w = lane >> 2, h = lane & 3;
+            const float mw = s.redm[w][h];
+            float M = mw;
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                float M = -INFINITY;
+            for (int o = 4; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xFFFFFFFFu, M, o));
+            const float sc = M == -INFINITY ? 0.f : fast_exp2(mw - M);
+            float Lp = s.redl[w][h] * sc;
 #pragma unroll
-                for (int w = 0; w < kComputeWarps; ++w) M = fmaxf(M, s.redm[w][h]);
-                float Ls = 0.f;
-#pragma unroll
-                for (int w = 0; w < kComputeWarps; ++w)
-                    Ls = fmaf(s.redl[w][h], fast_exp2(s.redm[w][h] - M), Ls);
-                mh[h] = M;
-                lh[h] = Ls;
-            }
+            for (int o = 4; o < 32; o <<= 1) Lp += __shfl_xor_sync(0xFFFFFFFFu, Lp, o);
+            float res[PER];
 #pragma unroll
             for (int e0 = 0; e0 < PER; ++e0) {
-                const int e = lane + 32 * e0, h = e / D, d = e % D;
-                const float M = h == 0 ? mh[0] : h == 1 ? mh[1] : h == 2 ? mh[2] : mh[3];
+                const int e = lane + 32 * e0, hh = e / D, d = e % D;
                 float O = 0.f;
 #pragma unroll
-                for (int w = 0; w < kComputeWarps; ++w) O = fmaf(s.redO[w][h][d], fast_exp2(s.redm[w][h] - M), O);
-                resO[e0] = O;
+                for (int ww = 0; ww < kComputeWarps; ++ww)
+                    O = fmaf(s.redO[ww][hh][d], __shfl_sync(0xFFFFFFFFu, sc, ww * 4 + hh), O);
+                res[e0] = O;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.st_empty);  // state buffer free
-            ph ^= 1;
-            if (qs.count == 1) {
+            run = __shfl_sync(0xFFFFFFFFu, run, 0);
+            const size_t pidx = (size_t)slot * a.run_cap + run;
+            float* pO = a.part_O + pidx * NOUT;
 #pragma unroll
-                for (int e0 = 0; e0 < PER; ++e0) {
-                    const int e = lane + 32 * e0, h = e / D;
-                    const float Lh = h == 0 ? lh[0] : h == 1 ? lh[1] : h == 2 ? lh[2] : lh[3];
-                    const uint32_t head = hc * kHeadsPerSlot + h;
-                    if (head < a.G) a.out[((size_t)g * a.G + head) * D + e % D] = resO[e0] / Lh;
-                }
-                continue;
-            }
-            float* pO = a.part_O + (size_t)cur_item * NOUT;
-#pragma unroll
-            for (int e0 = 0; e0 < PER; ++e0) pO[lane + 32 * e0] = resO[e0];
+            for (int e0 = 0; e0 < PER; ++e0) pO[lane + 32 * e0] = res[e0];
             if (lane < 4) {
-                a.part_ml[(size_t)cur_item * 8 + lane] = lane == 0 ? mh[0] : lane == 1 ? mh[1] : lane == 2 ? mh[2] : mh[3];
-                a.part_ml[(size_t)cur_item * 8 + 4 + lane] = lane == 0 ? lh[0] : lane == 1 ? lh[1] : lane == 2 ? lh[2] : lh[3];
+                a.part_ml[pidx * 8 + lane] = M;  // lanes 0-3: w = 0, h = lane
+                a.part_ml[pidx * 8 + 4 + lane] = Lp;
             }
-            // multi-item query slots are combined by combine_kernel after this launch
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(&a.done[slot], tiles);
         }
         return;
     }
 
     if (warp == kComputeWarps) {
         // ------------------------------------------------ producer
-        if (lane == 0) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.k64) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.k8) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.v64) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.v8) : "memory");
+        // Work stream: [static tiles | dynamic tiles].  Tickets (the CTA index,
+        // then a global counter) map to chunks of `chunk` tiles; the last
+        // `tail` tiles of the stream are single-tile chunks so the CTAs finish
+        // together.  A feeder keeps up to kRecRing work records in flight
+        // (bulk copies into shared memory) ahead of the TMA issue.
+        if (lane < kBoxSizes) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.k[lane]) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.v[lane]) : "memory");
         }
-        uint32_t stage = 0, phase = 0;
-        // software-pipelined: the next tile's records are loaded before this
-        // tile waits for a free ring slot
-        auto fetch_item = [&](uint32_t id) {
-            ItemRec r{0, 0, 0, 0};
-            if (id < n_items) r = a.items[id];
-            return r;
-        };
-        uint32_t it = 0, next_it = 0;
-        if (lane == 0) it = atomicAdd(&a.ctr->work, 1u);
-        it = __shfl_sync(0xFFFFFFFFu, it, 0);
-        ItemRec itm = fetch_item(it);
-        if (lane == 0) next_it = atomicAdd(&a.ctr->work, 1u);
-        uint32_t t = 0;
-        uint32_t np = 0;
-        PieceRec pr{0, 0, 0};
-        if (it < n_items) {
-            const TileRec* tr = a.tiles + itm.tile_first;
-            np = tr->npieces;
-            if (lane < kMaxPieces) pr = tr->p[lane];
-        }
-        for (;;) {
-            if (it >= n_items) {
-                if (lane == 0) {
-                    mbar_wait(&s.empty[stage], phase ^ 1);
-                    s.meta[stage] = make_int4(-1, 0, 0, 0);
-                    mbar_arrive(&s.full[stage]);
+        const uint64_t pol = l2_evict_first_policy();
+        const uint32_t W = a.n_static, CH = a.chunk, M = a.tail;
+        // ticket j -> [b0, b1): 1 ok, 0 not yet reserved by the planner, -1 end
+        auto try_chunk = [&](uint32_t j, uint32_t& b0, uint32_t& b1) -> int {
+            const uint32_t gd = ld_acquire_u32(&a.ctr->groups_done);
+            const uint32_t dyn = ld_acquire_u32(&a.ctr->dyn);
+            const uint32_t tot = W + dyn;
+            if (gd >= a.n_plan_groups) {  // final: big chunks, then singles
+                const uint32_t B = tot > M ? (tot - M) / CH * CH : 0u, nb = B / CH;
+                if (j < nb) {
+                    b0 = j * CH;
+                    b1 = b0 + CH;
+                } else {
+                    b0 = B + (j - nb);
+                    if (b0 >= tot) return -1;
+                    b1 = b0 + 1;
                 }
-                break;
+                return 1;
             }
-            // ---- prefetch the successor tile
-            const bool last_tile = t + 1 == itm.ntiles;
-            uint32_t it2 = it, t2 = t + 1;
-            ItemRec itm2 = itm;
-            if (last_tile) {
-                it2 = __shfl_sync(0xFFFFFFFFu, next_it, 0);
-                itm2 = fetch_item(it2);
-                t2 = 0;
+            if ((j + 1) * CH + M <= tot) {  // big in any final mapping
+                b0 = j * CH;
+                b1 = b0 + CH;
+                return 1;
             }
-            uint32_t np2 = 0;
-            PieceRec pr2{0, 0, 0};
-            if (it2 < n_items) {
-                const TileRec* tr2 = a.tiles + itm2.tile_first + t2;
-                np2 = tr2->npieces;
-                if (lane < kMaxPieces) pr2 = tr2->p[lane];
+            return 0;
+        };
+        // dynamic records are published with release stores; every lane
+        // acquires one flag, the warp barrier orders them before lane 0's
+        // (async-proxy) record copies
+        auto dyn_ready = [&](uint32_t b0, uint32_t b1) -> bool {
+            bool ok = true;
+            const uint32_t i = max(b0, W) + lane;
+            if (i < b1) ok = ld_acquire_u32(&a.dyn_tiles[i - W].ready) != 0;
+            const bool all = __all_sync(0xFFFFFFFFu, ok);
+            __syncwarp();
+            return all;
+        };
+        uint32_t pc0 = 0, pc1 = 0;
+        bool pend = false, feeding = true;
+        uint32_t ticket = blockIdx.x, tk = 0;
+        bool have_ticket = true, tk_inflight = false;
+        uint32_t head = 0, tail = 0, cnt = 0, rph = 0;  // record ring (rph: phase bit per slot)
+        uint32_t stage = 0, phase = 0;
+        bool run_first = true;
+        uint32_t run_tiles = 0;
+        unsigned long long p_wait = 0;
+        const unsigned long long p_t0 = clock64();
+        unsigned long long p_feed = 0, p_rec = 0, p_tma = 0;
+        for (;;) {
+            // ---- feed records
+            const unsigned long long tf = clock64();
+            while (cnt < (uint32_t)kRecRing && feeding) {
+                if (!pend) {
+                    if (!have_ticket) {
+                        if (!tk_inflight && lane == 0) tk = atomicAdd(&a.ctr->tickets, 1u) + gridDim.x;
+                        tk_inflight = false;
+                        ticket = __shfl_sync(0xFFFFFFFFu, tk, 0);
+                        have_ticket = true;
+                    }
+                    uint32_t b0 = 0, b1 = 0;
+                    const int r = try_chunk(ticket, b0, b1);
+                    if (r < 0) {
+                        feeding = false;
+                        break;
+                    }
+                    if (r == 0 || (b1 > W && !dyn_ready(b0, b1))) break;  // retry after issuing
+                    // acquired generic-proxy data is read by the bulk copies (async proxy)
+                    if (b1 > W && lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+                    pc0 = b0;
+                    pc1 = b1;
+                    pend = true;
+                    have_ticket = false;  // the next ticket travels while this chunk feeds
+                    if (lane == 0) tk = atomicAdd(&a.ctr->tickets, 1u) + gridDim.x;
+                    tk_inflight = true;
+                }
+                if (lane == 0) {
+                    const TileRec* src = pc0 < W ? a.st_tiles + pc0 : a.dyn_tiles + (pc0 - W);
+                    s.rec_w[tail] = pc0;
+                    s.rec_last[tail] = pc0 + 1 == pc1 ? 1u : 0u;
+                    mbar_arrive_expect_tx(&s.rec_bar[tail], (uint32_t)sizeof(TileRec));
+                    bulk_g2s(&s.rec[tail], src, (uint32_t)sizeof(TileRec), &s.rec_bar[tail]);
+                }
+                ++pc0;
+                if (pc0 == pc1) pend = false;
+                tail = tail + 1 == (uint32_t)kRecRing ? 0u : tail + 1;
+                ++cnt;
             }
-            // ---- issue this tile: lane p owns piece p
+            p_feed += clock64() - tf;
+            if (cnt == 0) {
+                if (!feeding) break;
+                __nanosleep(100);  // waiting for the planner
+                continue;
+            }
+            // ---- issue the head tile
+            const unsigned long long tr = clock64();
+            mbar_wait(&s.rec_bar[head], (rph >> head) & 1u);
+            p_rec += clock64() - tr;
+            rph ^= 1u << head;
+            __syncwarp();
+            const uint32_t w = s.rec_w[head];
+            const bool last_in_chunk = s.rec_last[head] != 0;
+            const uint4 hdr = *reinterpret_cast<const uint4*>(&s.rec[head]);
+            const uint32_t np = hdr.x, qslot = hdr.y;
+            const bool last_of_run = last_in_chunk || hdr.w != 0;
             uint32_t len = 0, srow = 0, gat = 0;
             uint64_t row = 0;
             if ((uint32_t)lane < np) {
-                len = pr.len & ~kPieceGather;
-                gat = pr.len & kPieceGather;
-                srow = pr.srow;
-                row = pr.row;
+                const uint4 v = *reinterpret_cast<const uint4*>(&s.rec[head].p[lane]);
+                len = v.x & ~kPieceGather;
+                gat = v.x & kPieceGather;
+                srow = v.y;
+                row = ((uint64_t)v.w << 32) | v.z;
             }
+            ++run_tiles;
             const uint32_t r8 = (len + 7) & ~7u;
             uint32_t bytes = r8 * CF::RB * 2;
             uint32_t vm[4];
 #pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                const uint32_t lo = max(srow, (uint32_t)w * 32), hi = min(srow + len, (uint32_t)w * 32 + 32);
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t lo = max(srow, (uint32_t)q * 32), hi = min(srow + len, (uint32_t)q * 32 + 32);
                 uint32_t m = 0;
-                if (hi > lo) m = (hi - lo == 32 ? 0xFFFFFFFFu : ((1u << (hi - lo)) - 1u)) << (lo - w * 32);
-                vm[w] = m;
+                if (hi > lo) m = (hi - lo == 32 ? 0xFFFFFFFFu : ((1u << (hi - lo)) - 1u)) << (lo - q * 32);
+                vm[q] = m;
             }
 #pragma unroll
             for (int o = 16; o; o >>= 1) {
                 bytes += __shfl_xor_sync(0xFFFFFFFFu, bytes, o);
 #pragma unroll
-                for (int w = 0; w < 4; ++w) vm[w] |= __shfl_xor_sync(0xFFFFFFFFu, vm[w], o);
+                for (int q = 0; q < 4; ++q) vm[q] |= __shfl_xor_sync(0xFFFFFFFFu, vm[q], o);
             }
+            const uint32_t g = qslot / a.n_hchunks, hc = qslot % a.n_hchunks;
+            const uint32_t nq = min((uint32_t)kHeadsPerSlot, a.G - hc * kHeadsPerSlot);
             if (lane == 0) {
+                const unsigned long long tw = clock64();
                 mbar_wait(&s.empty[stage], phase ^ 1);
+                p_wait += clock64() - tw;
                 s.valid[stage] = make_uint4(vm[0], vm[1], vm[2], vm[3]);
-                s.meta[stage] = make_int4((int)it, (int)(t | (last_tile ? 0x80000000u : 0u)),
-                                          (int)itm.qslot, 0);
-                mbar_arrive_expect_tx(&s.full[stage], bytes + (t == 0 ? 16 * D * 2 : 0));
-                if (t == 0)
-                    bulk_g2s(&s.qA[stage][0][0], a.qA + (size_t)itm.qslot * 16 * D, 16 * D * 2,
-                             &s.full[stage]);
+                const uint32_t flags = (run_first ? 1u : 0u) | (last_of_run ? 2u : 0u) | (nq << 8);
+                s.meta[stage] = make_int4((int)qslot, (int)flags, 0, (int)run_tiles);
+                const uint32_t qbytes = nq * D * 4;
+                mbar_arrive_expect_tx(&s.full[stage], bytes + (run_first ? qbytes : 0));
+                if (run_first)
+                    bulk_g2s(&s.qraw[stage][0][0], a.q + ((size_t)g * a.G + hc * kHeadsPerSlot) * D,
+                             qbytes, &s.full[stage]);
             }
             __syncwarp();
+            const unsigned long long tt = clock64();
             if (len) {
-                const CUtensorMap* mk64 = gat ? &maps.gk64 : &maps.k64;
-                const CUtensorMap* mk8 = gat ? &maps.gk8 : &maps.k8;
-                const CUtensorMap* mv64 = gat ? &maps.gv64 : &maps.v64;
-                const CUtensorMap* mv8 = gat ? &maps.gv8 : &maps.v8;
-                uint32_t rem = r8, sr = srow;
+                // binary decomposition: boxes of 128..16 rows cover only rows of
+                // the piece (their group dimension is not bounds-checked), the
+                // 8-row box takes the rounded-up remainder (zero-filled past the end)
+                const CUtensorMap* mk = gat ? maps.gk : maps.k;
+                const CUtensorMap* mv = gat ? maps.gv : maps.v;
+                uint32_t full = len & ~7u, sr = srow, rem = r8;
                 int y = (int)row;
                 while (rem) {
-                    const bool big = rem >= 64;
-#pragma unroll
-                    for (int h = 0; h < CF::HALVES; ++h) {
-                        const uint32_t off = h * kTileRows * CF::HALF + sr * CF::HALF;
-                        tma2d(&s.K[stage][off], big ? mk64 : mk8, h * (CF::HALF / 2), y, &s.full[stage]);
-                        tma2d(&s.V[stage][off], big ? mv64 : mv8, h * (CF::HALF / 2), y, &s.full[stage]);
-                    }
-                    const uint32_t step = big ? 64 : 8;
-                    rem -= step;
-                    sr += step;
-                    y += (int)step;
+                    int i = 0;
+                    if (full >= 16) i = 31 - __clz((int)min(full, 128u) >> 3);  // largest 8*2^i <= full
+                    const uint32_t rows_i = 8u << i;
+                    const uint32_t off = (sr >> 3) * 8 * CF::RB;
+                    tma4d(&s.K[stage][off], mk + i, y, &s.full[stage], pol);
+                    tma4d(&s.V[stage][off], mv + i, y, &s.full[stage], pol);
+                    rem -= rows_i;
+                    full = full > rows_i ? full - rows_i : 0u;
+                    sr += rows_i;
+                    y += (int)rows_i;
                 }
             }
             __syncwarp();
+            p_tma += clock64() - tt;
+            // a dynamic record is re-armed for the next step once consumed
+            if (w >= W && lane == 0) a.dyn_tiles[w - W].ready = 0;
             if (++stage == CF::NS) {
                 stage = 0;
                 phase ^= 1;
             }
-            // ---- advance
-            if (last_tile && lane == 0 && it2 < n_items) next_it = atomicAdd(&a.ctr->work, 1u);
-            it = it2;
-            itm = itm2;
-            t = t2;
-            np = np2;
-            pr = pr2;
+            head = head + 1 == (uint32_t)kRecRing ? 0u : head + 1;
+            --cnt;
+            run_first = last_of_run;
+            if (last_of_run) run_tiles = 0;
+        }
+        if (lane == 0) {
+            if (a.dtrace) {
+                a.dtrace[16 * blockIdx.x + 4] = p_wait;
+                a.dtrace[16 * blockIdx.x + 5] = clock64() - p_t0;
+                a.dtrace[16 * blockIdx.x + 7] = p_feed;
+                a.dtrace[16 * blockIdx.x + 8] = p_rec;
+                a.dtrace[16 * blockIdx.x + 9] = p_tma;
+            }
+            mbar_wait(&s.empty[stage], phase ^ 1);
+            s.meta[stage] = make_int4(-1, 0, 0, 0);
+            mbar_arrive(&s.full[stage]);
+            // the last CTA out re-arms the step counters (every reader is done)
+            if (atomicAdd(&a.ctr->exited, 1u) == gridDim.x - 1) {
+                a.ctr->tickets = 0;
+                a.ctr->dyn = 0;
+                a.ctr->groups_done = 0;
+                a.ctr->exited = 0;
+                __threadfence();
+            }
         }
         return;
     }
 
     // ---------------------------------------------------- consumers
     const int gid = lane >> 2, tig = lane & 3;
-    const bool upper = lane >= 16;  // rows g+4: q_lo / p2
+    const bool upper = lane >= 16;  // rows g+4: q2 / p2
     const int hq = gid & 3;         // head of this lane's score rows
     const int row0 = warp * 16;     // this warp's 16 rows of the tile
     const int mtx = lane >> 3, r8 = lane & 7;
-    (void)gid;
 
     uint32_t qa[CF::KSTEPS][4];  // A fragments of [q1; q2; q3; 0]
     float o[CF::NT][4];
     float m_run = -INFINITY, l_run = 0.f;
-    uint32_t cur_item = 0, cur_qslot = 0, st_ph = 0;
+    uint32_t st_ph = 0;
 
     uint32_t stage = 0, phase = 0;
     uint32_t n_tiles_done = 0;
+    unsigned long long c_wait = 0;
     for (;;) {
-        mbar_wait(&s.full[stage], phase);
+        if (a.dtrace && threadIdx.x == 0) {
+            const unsigned long long t0 = clock64();
+            mbar_wait(&s.full[stage], phase);
+            c_wait += clock64() - t0;
+        } else {
+            mbar_wait(&s.full[stage], phase);
+        }
         const int4 mt = s.meta[stage];
         if (a.dtrace && threadIdx.x == 0) {
-            if (n_tiles_done == 0) a.dtrace[4 * blockIdx.x + 1] = gtime();
+            if (n_tiles_done == 0) a.dtrace[16 * blockIdx.x + 1] = gtime();
             if (mt.x < 0) {
-                a.dtrace[4 * blockIdx.x + 2] = gtime();
-                a.dtrace[4 * blockIdx.x + 3] = n_tiles_done;
+                a.dtrace[16 * blockIdx.x + 2] = gtime();
+                a.dtrace[16 * blockIdx.x + 3] = n_tiles_done;
+                a.dtrace[16 * blockIdx.x + 6] = c_wait;
             }
         }
         ++n_tiles_done;
         if (mt.x < 0) {
-            // stop the merge warp once it has drained the last item
+            // stop the merge warp once it has drained the last run
             mbar_wait(&s.st_empty, st_ph ^ 1);
-            if (warp == 0 && lane == 0) s.st_item = 0xFFFFFFFFu;
+            if (threadIdx.x == 0) s.st_slot = 0xFFFFFFFFu;
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.st_full);
             break;
         }
-        const uint32_t tile_in_item = (uint32_t)mt.y & 0x7FFFFFFFu;
-        const bool last = ((uint32_t)mt.y >> 31) != 0;
-        if (tile_in_item == 0) {
-            cur_item = (uint32_t)mt.x;
-            cur_qslot = (uint32_t)mt.z;
-            const int nq = mt.w;
-            // A operand [q1; q2; q3; 0] (prepared by route_plan_kernel) via ldmatrix
-            {
-                const uint32_t qbase = smem_u32(&s.qA[stage][0][0]);
-                const uint32_t qrow = (mtx & 1) * 8 + r8;
+        const uint32_t flags = (uint32_t)mt.y;
+        if (flags & 1u) {
+            // A operand [q1; q2; q3; 0]: 3-term bf16 split of the f32 queries
+            // (~fp32-exact).  Rows g (lanes < 16: q1, else q2) and g + 8 (q3 / 0).
+            const uint32_t nq = (flags >> 8) & 7u;
+            const float* qh = &s.qraw[stage][hq][0];
+            const bool live = (uint32_t)hq < nq;
 #pragma unroll
-                for (int k = 0; k < CF::KSTEPS; ++k) {
-                    const uint32_t chunk = 2 * k + (mtx >> 1);
-                    const uint32_t h = chunk / (CF::HALF / 16), cc = chunk % (CF::HALF / 16);
-                    ldsm_x4(qbase + h * 16 * CF::HALF + swz<D>(qrow, cc), qa[k][0], qa[k][1],
-                            qa[k][2], qa[k][3]);
+            for (int k = 0; k < CF::KSTEPS; ++k) {
+                const float2 lo2 = live ? *reinterpret_cast<const float2*>(qh + 16 * k + 2 * tig) : make_float2(0.f, 0.f);
+                const float2 hi2 = live ? *reinterpret_cast<const float2*>(qh + 16 * k + 8 + 2 * tig) : make_float2(0.f, 0.f);
+                // x = t1 + t2 + t3 (bf16 terms, hardware RNE conversions)
+                const uint32_t a1 = bf16x2_rn(lo2.x, lo2.y), b1 = bf16x2_rn(hi2.x, hi2.y);
+                const float ra0 = lo2.x - bf16lo(a1), ra1 = lo2.y - bf16hi(a1);
+                const float rb0 = hi2.x - bf16lo(b1), rb1 = hi2.y - bf16hi(b1);
+                const uint32_t a2 = bf16x2_rn(ra0, ra1), b2 = bf16x2_rn(rb0, rb1);
+                if (!upper) {
+                    qa[k][0] = a1;
+                    qa[k][1] = bf16x2_rn(ra0 - bf16lo(a2), ra1 - bf16hi(a2));
+                    qa[k][2] = b1;
+                    qa[k][3] = bf16x2_rn(rb0 - bf16lo(b2), rb1 - bf16hi(b2));
+                } else {
+                    qa[k][0] = a2;
+                    qa[k][1] = 0u;
+                    qa[k][2] = b2;
+                    qa[k][3] = 0u;
                 }
             }
 #pragma unroll
@@ -1071,16 +1171,15 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
         }
         const uint32_t vbits = ((&s.valid[stage].x)[warp >> 1] >> ((warp & 1) * 16)) & 0xFFFFu;
         if (vbits) {
-            // ---- S = [q_hi; q_lo] K^T for this warp's 16 rows
+            // ---- S = [q1; q2; q3] K^T for this warp's 16 rows
             const uint32_t kbase = smem_u32(&s.K[stage][0]);
             float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
             const uint32_t krow = row0 + (mtx >> 1) * 8 + r8;
 #pragma unroll
             for (int k = 0; k < CF::KSTEPS; ++k) {
                 const uint32_t chunk = 2 * k + (mtx & 1);  // 16-byte chunk within the row
-                const uint32_t h = chunk / (CF::HALF / 16), cc = chunk % (CF::HALF / 16);
                 uint32_t b0, b1, b2, b3;
-                ldsm_x4(kbase + h * kTileRows * CF::HALF + swz<D>(krow, cc), b0, b1, b2, b3);
+                ldsm_x4(kbase + toff<D>(krow, chunk), b0, b1, b2, b3);
                 mma16816(c0, qa[k][0], qa[k][1], qa[k][2], qa[k][3], b0, b1);
                 mma16816(c1, qa[k][0], qa[k][1], qa[k][2], qa[k][3], b2, b3);
             }
@@ -1142,9 +1241,8 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
 #pragma unroll
             for (int j = 0; j < CF::NT / 2; ++j) {
                 const uint32_t chunk = 2 * j + (mtx >> 1);
-                const uint32_t h = chunk / (CF::HALF / 16), cc = chunk % (CF::HALF / 16);
                 uint32_t b0, b1, b2, b3;
-                ldsm_x4_t(vbase + h * kTileRows * CF::HALF + swz<D>(vrow, cc), b0, b1, b2, b3);
+                ldsm_x4_t(vbase + toff<D>(vrow, chunk), b0, b1, b2, b3);
                 mma16816(o[2 * j], pa0, pa1, pa2, pa3, b0, b1);
                 mma16816(o[2 * j + 1], pa0, pa1, pa2, pa3, b2, b3);
             }
@@ -1152,8 +1250,9 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&s.empty[stage]);
 
-        if (last) {
-            // ---- item done: deposit this warp's (m, l, O) state for the merge warp
+        if (flags & 2u) {
+            // ---- run done: deposit this warp's (m, l, O) state for the merge warp
+            const uint32_t slot = (uint32_t)mt.x;
             float lw = l_run;
             lw += __shfl_xor_sync(0xFFFFFFFFu, lw, 1);
             lw += __shfl_xor_sync(0xFFFFFFFFu, lw, 2);
@@ -1166,7 +1265,7 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
                 xo[n][0] = x0 + __shfl_xor_sync(0xFFFFFFFFu, x0, 16);
                 xo[n][1] = x1 + __shfl_xor_sync(0xFFFFFFFFu, x1, 16);
             }
-            mbar_wait(&s.st_empty, st_ph ^ 1);  // previous item's states consumed
+            mbar_wait(&s.st_empty, st_ph ^ 1);  // previous run's states consumed
             if (!upper) {
 #pragma unroll
                 for (int n = 0; n < CF::NT; ++n)
@@ -1176,9 +1275,9 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
                     s.redl[warp][hq] = lw;
                 }
             }
-            if (warp == 0 && lane == 0) {
-                s.st_item = cur_item;
-                s.st_qslot = cur_qslot;
+            if (threadIdx.x == 0) {
+                s.st_slot = slot;
+                s.st_tiles = (uint32_t)mt.w;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.st_full);
@@ -1192,56 +1291,79 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
 }
 
 // ============================================================ LSE combine (Alg. 2)
-// One CTA per query slot with > 1 item: O = sum_i O_i 2^(m_i - M) / sum_i l_i 2^(m_i - M)
-// (merge_into / pattn_finalize, attention.cpp:102-161; Alg. 2).
+// One CTA per query slot: O = sum_r O_r 2^(m_r - M) / sum_r l_r 2^(m_r - M)
+// over the slot's run partials (merge_into / pattn_finalize,
+// attention.cpp:102-161; Alg. 2).  Launched (PDL) once every decode
+// CTA is resident; its CTAs become resident as decode CTAs retire and combine
+// a slot as soon as the slot's tiles are all published, so only the last
+// slots' combines trail the decode.  A slot with no visited key gets zero
+// rows (attention.cpp:147-152).
 template <int D>
-__global__ void __launch_bounds__(kHeadsPerSlot * D) combine_kernel(const QSlot* qslots, uint32_t n_qslots,
-                                                                    uint32_t G, uint32_t n_hchunks,
-                                                                    const float* part_O, const float* part_ml,
-                                                                    float* out) {
+__global__ void __launch_bounds__(kHeadsPerSlot * D) combine_kernel(CombineArgs a) {
     constexpr int NOUT = kHeadsPerSlot * D;
-    constexpr int kMaxStage = 256;  // items whose (m, l) are staged in shared memory
+    constexpr int kMaxStage = 256;  // runs whose (m, l) are staged in shared memory
     __shared__ float sml[kMaxStage][8];
-    pdl_wait();
+    __shared__ uint32_t s_total, s_runs;
     const uint32_t qsi = blockIdx.x;
-    const QSlot qs = qslots[qsi];
-    if (qs.count <= 1) return;  // written directly by the decode kernel
+    if (threadIdx.x == 0) {
+        uint32_t total = a.st_cnt[qsi];
+        if (a.dyn_cnt) {
+            uint32_t v;
+            while (!((v = ld_acquire_u32(a.dyn_cnt + qsi)) & kCntValid)) __nanosleep(128);
+            total += v & ~kCntValid;
+            a.dyn_cnt[qsi] = 0;
+        }
+        if (total)
+            while (ld_acquire_u32(a.done + qsi) < total) __nanosleep(128);
+        s_total = total;
+        s_runs = ld_acquire_u32(a.runs + qsi);
+        a.done[qsi] = 0;  // re-armed for the next step (this CTA is the only reader)
+        a.runs[qsi] = 0;
+    }
+    __syncthreads();
     const uint32_t e = threadIdx.x, h = e / D;
-    const uint32_t g = qsi / n_hchunks, hc = qsi % n_hchunks;
+    const uint32_t g = qsi / a.n_hchunks, hc = qsi % a.n_hchunks;
     const uint32_t head = hc * kHeadsPerSlot + h;
-    const uint32_t ns = min(qs.count, (uint32_t)kMaxStage);
-    for (uint32_t i = e; i < ns * 8; i += blockDim.x) sml[i / 8][i % 8] = part_ml[(size_t)qs.base * 8 + i];
+    float* out = a.out + ((size_t)g * a.G + head) * D + (e % D);
+    const uint32_t nr = s_runs;
+    if (s_total == 0 || nr == 0) {
+        if (head < a.G) *out = 0.f;
+        return;
+    }
+    const size_t base = (size_t)qsi * a.run_cap;
+    const uint32_t ns = min(nr, (uint32_t)kMaxStage);
+    for (uint32_t i = e; i < ns * 8; i += blockDim.x) sml[i / 8][i % 8] = __ldcg(a.part_ml + base * 8 + i);
     __syncthreads();
     auto ml = [&](uint32_t i, uint32_t k) {
-        return i < kMaxStage ? sml[i][k] : part_ml[(size_t)(qs.base + i) * 8 + k];
+        return i < kMaxStage ? sml[i][k] : __ldcg(a.part_ml + (base + i) * 8 + k);
     };
     float M = -INFINITY;
-    for (uint32_t i = 0; i < qs.count; ++i) M = fmaxf(M, ml(i, h));
+    for (uint32_t i = 0; i < nr; ++i) M = fmaxf(M, ml(i, h));
     float O = 0.f, L = 0.f;
-    constexpr int U = 8;  // partial rows in flight
-    for (uint32_t i0 = 0; i0 < qs.count; i0 += U) {
-        float v[U];
+    if (M != -INFINITY) {
+        constexpr int U = 8;  // partial rows in flight
+        for (uint32_t i0 = 0; i0 < nr; i0 += U) {
+            float v[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-            v[u] = i0 + u < qs.count ? part_O[(size_t)(qs.base + i0 + u) * NOUT + e] : 0.f;
+            for (int u = 0; u < U; ++u)
+                v[u] = i0 + u < nr ? __ldcg(a.part_O + (base + i0 + u) * NOUT + e) : 0.f;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (i0 + u < qs.count) {
-                const float w = fast_exp2(ml(i0 + u, h) - M);
-                O = fmaf(v[u], w, O);
-                L = fmaf(ml(i0 + u, 4 + h), w, L);
+            for (int u = 0; u < U; ++u) {
+                if (i0 + u < nr) {
+                    const float wgt = fast_exp2(ml(i0 + u, h) - M);
+                    O = fmaf(v[u], wgt, O);
+                    L = fmaf(ml(i0 + u, 4 + h), wgt, L);
+                }
             }
         }
     }
-    if (head < G) out[((size_t)g * G + head) * D + (e % D)] = O / L;
+    if (head < a.G) *out = L > 0.f ? O / L : 0.f;
 }
 
 // ============================================================ launchers
-void launch_combine(int D, const QSlot* qs, uint32_t n_qslots, uint32_t G, uint32_t n_hchunks,
-                    const float* pO, const float* pml, float* out, cudaStream_t st) {
-#define SAAP_COMBINE(DD)                                                                        \
-    launch_pdl(true, combine_kernel<DD>, dim3(n_qslots), dim3(kHeadsPerSlot * DD), 0, st, qs,   \
-               n_qslots, G, n_hchunks, pO, pml, out)
+void launch_combine(int D, const CombineArgs& ca, uint32_t n_qslots, cudaStream_t st) {
+#define SAAP_COMBINE(DD) \
+    launch_pdl(true, combine_kernel<DD>, dim3(n_qslots), dim3(kHeadsPerSlot * DD), 0, st, ca)
     switch (D) {
         case 128: SAAP_COMBINE(128); break;
         case 64: SAAP_COMBINE(64); break;
@@ -1253,7 +1375,7 @@ void launch_combine(int D, const QSlot* qs, uint32_t n_qslots, uint32_t G, uint3
 
 template <int D>
 static void launch_decode_t(const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st) {
-    const size_t smem = sizeof(DecodeSmem2<D>) + 1024;
+    const size_t smem = sizeof(DecodeSmem<D>) + 1024;
     static bool configured = false;
     if (!configured) {
         SAAP_CUDA(cudaFuncSetAttribute(decode_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
