@@ -48,11 +48,17 @@ struct RouteArgs {
 // scores of every centroid for every context.  Contexts sharing one
 // partition (same KV head, different sequences) form a slot and share each
 // centroid load.
+constexpr int kSlotGroups = 8;  // contexts per approximate-scoring slot
+struct ApproxSlot {
+    const float* centT;            // d x C f32 of the slot's partition
+    uint32_t count;                // member contexts (<= kSlotGroups)
+    uint32_t group[kSlotGroups];
+    uint32_t pad;
+};
 struct ApproxArgs {
-    const float* const* centT;     // per group, d x C f32
+    const float* const* centT;     // per group, d x C f32 (slots == null: slot s = group s)
+    const ApproxSlot* slots;       // one load gives the centroids and the members
     const float* q_route;          // [groups][G][D]
-    const uint32_t* slot_off;      // [n_slots + 1] into slot_list; null: slot s = group s
-    const uint32_t* slot_list;     // groups by slot
     uint32_t G, C;
     float* approx;                 // [groups][C]
 };
@@ -99,7 +105,8 @@ struct DecodeArgs {
     TileRec* dyn_tiles;        // dynamic part (ready flags cleared after use)
     uint32_t n_static;
     uint32_t n_plan_groups;    // planner CTAs that publish dynamic tiles (0: static only)
-    uint32_t chunk;            // work-stream tiles per ticket
+    uint32_t chunk;            // work-stream tiles per ticket (dynamic part)
+    uint32_t chunk_st;         // tiles per ticket in the static part
     uint32_t tail;             // the stream's last `tail` tiles go out one per ticket
     StepCounters* ctr;
     const float* q;            // [groups][G][D] attention queries (f32)

@@ -254,12 +254,19 @@ void bind_routers(saap_layer* L, const saap_router* const* routers, int& mode, i
             }
             members[it - uniq.begin()].push_back((uint32_t)g);
         }
-        std::vector<uint32_t> tab{0};
-        for (auto& m : members) tab.push_back(tab.back() + (uint32_t)m.size());
-        for (auto& m : members) tab.insert(tab.end(), m.begin(), m.end());
-        if (!L->d_route_slots) L->d_route_slots = dmalloc<uint32_t>(2 * L->n_groups + 1);
-        SAAP_CUDA(cudaMemcpy(L->d_route_slots, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
-        L->n_route_slots = (uint32_t)uniq.size();
+        std::vector<ApproxSlot> tab;
+        for (size_t u = 0; u < uniq.size(); ++u)
+            for (size_t k0 = 0; k0 < members[u].size(); k0 += kSlotGroups) {
+                ApproxSlot sl{};
+                sl.centT = uniq[u]->centT;
+                sl.count = (uint32_t)std::min<size_t>(kSlotGroups, members[u].size() - k0);
+                for (uint32_t k = 0; k < sl.count; ++k) sl.group[k] = members[u][k0 + k];
+                tab.push_back(sl);
+            }
+        if (!L->d_route_slots) L->d_route_slots = dmalloc<ApproxSlot>(L->n_groups);  // <= one slot per group
+        SAAP_CUDA(cudaMemcpy(L->d_route_slots, tab.data(), tab.size() * sizeof(ApproxSlot),
+                             cudaMemcpyHostToDevice));
+        L->n_route_slots = (uint32_t)tab.size();
     } else {
         std::vector<const double*> p(3 * L->n_groups);
         for (size_t g = 0; g < L->n_groups; ++g) {
@@ -313,7 +320,7 @@ void enqueue_route_score(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
                          uint64_t probes, int mode, const float* const* centT,
                          const float* q_route, const double* probs, PlanArgs& pa,
                          const float* cmax = nullptr, const float* const* centR = nullptr,
-                         const uint32_t* slots = nullptr, uint32_t n_slots = 0) {
+                         const ApproxSlot* slots = nullptr, uint32_t n_slots = 0) {
     const RouteGeo geo = route_geo(C, probes);
     const bool approx = mode == 1 && C <= kPlanThreads && cmax != nullptr && centR != nullptr;
     double* cs = (double*)ensure(c, c->cand_s, n_groups * geo.n_cand * sizeof(double));
@@ -337,8 +344,7 @@ void enqueue_route_score(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
         ApproxArgs aa{};
         aa.centT = centT;
         aa.q_route = q_route;
-        aa.slot_off = slots;
-        aa.slot_list = slots ? slots + n_slots + 1 : nullptr;
+        aa.slots = slots;
         aa.G = (uint32_t)G;
         aa.C = (uint32_t)C;
         aa.approx = (float*)ensure(c, c->approx, n_groups * C * sizeof(float));
@@ -488,7 +494,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
                     const float* q_route, uint64_t G, uint64_t probes, uint64_t recent, float* out,
                     saap_attn_stats* stats, uint32_t* selected, uint32_t chunk,
                     uint32_t qm_hidden = 0, const float* cmax = nullptr,
-                    const float* const* centR = nullptr, const uint32_t* slots = nullptr,
+                    const float* const* centR = nullptr, const ApproxSlot* slots = nullptr,
                     uint32_t n_slots = 0) {
     const cudaStream_t st = c->stream;
     const uint64_t n_groups = src.n_groups, D = src.D, C = src.C;
@@ -586,7 +592,9 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     const uint64_t max_stream = sp->n_tiles + n_groups * dyn_per_group * n_hchunks;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->sm_count,
                                                                     (max_stream + chunk - 1) / chunk));
-    da.tail = env_u32("SAAP_TAIL_PER_CTA", 2) * (uint32_t)grid;
+    da.tail = env_u32("SAAP_TAIL_PER_CTA", 1) * (uint32_t)grid;
+    // static tickets: enough to give every CTA a share of the window
+    da.chunk_st = plan ? std::max<uint32_t>(1u, std::min<uint32_t>(chunk, sp->n_tiles / (uint32_t)grid)) : chunk;
     static const bool dtrace_on = std::getenv("SAAP_DECODE_TRACE") != nullptr;
     if (dtrace_on) da.dtrace = (unsigned long long*)ensure(c, c->dtrace, (size_t)c->sm_count * 128);
     launch_decode((int)D, *src.maps, da, grid, st);
@@ -1533,7 +1541,7 @@ static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* con
     enqueue_decode(c, src, sp, mode, L->d_centT, L->d_qm, qr, q_route, G, cfg->probes,
                    cfg->recent_count, out, stats, selected, kChunkSparse, (uint32_t)hq,
                    mode == 1 ? L->d_cmax : nullptr, mode == 1 ? L->d_centR : nullptr,
-                   mode == 1 ? L->d_route_slots : nullptr, mode == 1 ? L->n_route_slots : 0);
+                   mode == 1 ? (const ApproxSlot*)L->d_route_slots : nullptr, mode == 1 ? L->n_route_slots : 0);
 }
 
 int saap_sparse_attention_dev(saap_ctx* c, const saap_layer* L, const saap_router* const* routers,

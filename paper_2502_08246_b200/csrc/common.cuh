@@ -71,11 +71,11 @@ struct TileDesc {
 // Per-step device counters.  Zero at allocation; the last decode CTA of a
 // step resets them for the next step (every reader has finished by then).
 struct StepCounters {
-    uint32_t tickets;      // work-stream chunks handed out beyond the first gridDim.x
-    uint32_t dyn;          // dynamic tiles reserved by the planner
-    uint32_t groups_done;  // planner CTAs that finished reserving
-    uint32_t exited;       // decode CTAs finished
-    uint32_t pad[28];
+    unsigned long long dynres;  // (planner CTAs that reserved << 32) | dynamic tiles reserved
+    uint32_t published;         // planner CTAs whose tiles are all published
+    uint32_t tickets;           // work-stream tickets handed out beyond the static first batch
+    uint32_t exited;            // decode CTAs finished
+    uint32_t pad[27];
 };
 
 constexpr int kHeadsPerSlot = 4;  // query heads processed together (GQA group)
@@ -144,6 +144,11 @@ __device__ __forceinline__ void pdl_trigger() {
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
@@ -274,7 +279,7 @@ struct saap_layer {
     const float** d_centT = nullptr;   // per group centT
     const float** d_centR = nullptr;   // per group row-major centroids
     float* d_cmax = nullptr;           // per group partition cmax
-    uint32_t* d_route_slots = nullptr;  // [n_slots+1] offsets, then groups by partition
+    void* d_route_slots = nullptr;     // ApproxSlot[]: approximate-scoring slots (<= 8 contexts of one partition)
     uint32_t n_route_slots = 0;
     const double** d_qm = nullptr;     // per group: w1, w2, vec (3 pointers)
     // decode: TMA maps over the packed cache (+ gather buffer), built lazily

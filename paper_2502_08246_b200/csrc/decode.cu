@@ -229,7 +229,6 @@ __global__ void __launch_bounds__(kSliceMax) route_score_kernel(RouteArgs a) {
 // slot's contexts; the 8 warps' partial dot products are summed in shared
 // memory.  pooled = fp64 row sum of the group's queries rounded to f32
 // (route_plan_kernel bounds the resulting error).
-constexpr int kApproxGroups = 16;  // contexts per pass
 constexpr uint32_t kStageOff = 2049;  // planner stages off/offA in shared memory up to C = 2048
 constexpr int kPlanTileCnt = 1024;    // planner keeps per-tile piece counts in shared memory
 
@@ -237,40 +236,43 @@ constexpr int kPlanTileCnt = 1024;    // planner keeps per-tile piece counts in 
 template <int D>
 __global__ void __launch_bounds__(256) route_approx_kernel(ApproxArgs a) {
     constexpr int DW = D / 8;
-    __shared__ float pf[kApproxGroups][D];
-    __shared__ float red[8][kApproxGroups][33];
+    __shared__ float pf[kSlotGroups][D];
+    __shared__ float red[8][kSlotGroups][33];
     pdl_trigger();
     const uint32_t s = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t gb = a.slot_off ? a.slot_off[s] : s;
-    const uint32_t ng = a.slot_off ? a.slot_off[s + 1] - gb : 1;
-    auto group = [&](uint32_t k) { return a.slot_off ? a.slot_list[gb + k] : gb + k; };
-    const float* cT = a.centT[group(0)];
+    ApproxSlot sl;
+    if (a.slots) {
+        sl = a.slots[s];
+    } else {
+        sl.centT = a.centT[s];
+        sl.count = 1;
+        sl.group[0] = s;
+    }
+    const uint32_t ng = sl.count;
+    const float* cT = sl.centT;
     const uint32_t c = blockIdx.y * 32 + lane;
+    // centroid slice and member queries are loaded together (one round trip)
     float cv[DW];
 #pragma unroll
     for (int jj = 0; jj < DW; ++jj) cv[jj] = c < a.C ? cT[(size_t)(warp * DW + jj) * a.C + c] : 0.f;
-    for (uint32_t k0 = 0; k0 < ng; k0 += kApproxGroups) {
-        const uint32_t nk = min((uint32_t)kApproxGroups, ng - k0);
-        for (uint32_t e = tid; e < nk * D; e += blockDim.x) {
-            const uint32_t k = e / D, j = e % D;
-            pf[k][j] = (float)pooled_sum(a.q_route + (size_t)group(k0 + k) * a.G * D + j, a.G, D);
-        }
-        __syncthreads();
-        for (uint32_t k = 0; k < nk; ++k) {
-            float x = 0.f;
+    for (uint32_t e = tid; e < ng * D; e += blockDim.x) {
+        const uint32_t k = e / D, j = e % D;
+        pf[k][j] = (float)pooled_sum(a.q_route + (size_t)sl.group[k] * a.G * D + j, a.G, D);
+    }
+    __syncthreads();
+    for (uint32_t k = 0; k < ng; ++k) {
+        float x = 0.f;
 #pragma unroll
-            for (int jj = 0; jj < DW; ++jj) x = fmaf(pf[k][warp * DW + jj], cv[jj], x);
-            red[warp][k][lane] = x;
-        }
-        __syncthreads();
-        for (uint32_t e = tid; e < nk * 32; e += blockDim.x) {
-            const uint32_t k = e / 32, l = e % 32, cc = blockIdx.y * 32 + l;
-            float x = 0.f;
+        for (int jj = 0; jj < DW; ++jj) x = fmaf(pf[k][warp * DW + jj], cv[jj], x);
+        red[warp][k][lane] = x;
+    }
+    __syncthreads();
+    for (uint32_t e = tid; e < ng * 32; e += blockDim.x) {
+        const uint32_t k = e / 32, l = e % 32, cc = blockIdx.y * 32 + l;
+        float x = 0.f;
 #pragma unroll
-            for (int w = 0; w < 8; ++w) x += red[w][k][l];
-            if (cc < a.C) a.approx[(size_t)group(k0 + k) * a.C + cc] = x;
-        }
-        __syncthreads();
+        for (int w = 0; w < 8; ++w) x += red[w][k][l];
+        if (cc < a.C) a.approx[(size_t)sl.group[k] * a.C + cc] = x;
     }
 }
 
@@ -416,9 +418,16 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         __syncthreads();
         const uint32_t nS = s_ncand;
         trace(1);
+        // The candidates are a superset of the exact top-L; when there are
+        // exactly L of them they ARE the exact set.  Attention does not depend
+        // on the bucket order, so without a `selected` output no fp64 chain
+        // is needed (the usual case: approx gaps >> 2B at the boundary).
+        const bool set_only = a.selected == nullptr && nS == L && L <= kMaxCand;
         double ex = -INFINITY;
         uint32_t eid = 0xFFFFFFFFu;
-        if (nS <= kMaxCand) {
+        if (set_only) {
+            if (tid < L) eid = cand_id[tid];
+        } else if (nS <= kMaxCand) {
             // stage the candidates' centroid rows (coalesced) and run the chains from smem
             const float* cr = a.centR[g];
             for (uint32_t e = tid; e < nS * a.D; e += nth) {
@@ -448,7 +457,7 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         uint32_t p2s = 1;
         while (p2s < (nS <= kMaxCand ? nS : Cb)) p2s <<= 1;
         trace(2);
-        bitonic_regs(ex, eid, nS <= kMaxCand ? p2s : a.P2, ss, si);
+        if (!set_only) bitonic_regs(ex, eid, nS <= kMaxCand ? p2s : a.P2, ss, si);
         __syncthreads();
         if (tid < L) si[tid] = eid;
         for (uint32_t w = tid; w < bm_words; w += nth) bitmap[w] = 0;
@@ -489,6 +498,115 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         __syncthreads();
     }
     if (a.route_only) return;
+
+    // ---------------- fast path (no general-window gathers): one warp plans
+    // the bucket segments with shuffles only -- sizes, counters, one tile
+    // reservation, pieces, publication                attention.cpp:342-372
+    {
+        const uint32_t rb0 = fallback ? 0 : n - a.recent;
+        const bool fast = fallback || rb0 == T || (rb0 > T && !route);
+        if (fast) {
+            if (tid >= 32) return;
+            const uint32_t lane = tid, nh = a.n_hchunks;
+            const uint32_t* offg = stage_off ? s_off : a.off + (size_t)g * (Cb + 1);
+            const uint32_t* offAg = stage_off ? s_offA : a.offA + (size_t)g * (Cb + 1);
+            unsigned long long keys = 0;
+            uint32_t mx = 0, vrows = 0;
+            for (uint32_t b0 = 0; b0 < L; b0 += 32) {
+                const uint32_t b = b0 + lane;
+                uint32_t lenA = 0, st = 0;
+                if (b < L) {
+                    const uint32_t c = si[b];
+                    mx = max(mx, offg[c + 1] - offg[c]);  // raw bucket size (attention.cpp:356)
+                    lenA = offAg[c + 1] - offAg[c];        // rb >= T: no in-window ids in region A
+                    st = sink + offAg[c];
+                }
+                keys += lenA;
+                const uint32_t v8 = (lenA + 7) & ~7u;
+                uint32_t incl = v8;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (lane >= (uint32_t)o) incl += v;
+                }
+                if (b < L) {
+                    segs[b] = Seg{KIND_ROWS, lenA, st};
+                    vpre[b] = vrows + incl - v8;
+                }
+                vrows += __shfl_sync(0xFFFFFFFFu, incl, 31);
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                keys += __shfl_xor_sync(0xFFFFFFFFu, keys, o);
+                mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+            }
+            const uint32_t ntiles = (vrows + kTileRows - 1) / kTileRows;
+            uint32_t tile0 = 0;
+            if (lane == 0) {
+                // one atomic reserves the tiles and reports this group
+                tile0 = (uint32_t)atomicAdd(&a.ctr->dynres, (1ull << 32) | (unsigned long long)(ntiles * nh));
+                for (uint32_t hc = 0; hc < nh; ++hc) a.dyn_cnt[g * nh + hc] = ntiles | kCntValid;
+                saap_attn_stats stt;
+                stt.keys_scored = fallback ? (unsigned long long)n : (unsigned long long)sink + (n - rb0) + keys;
+                stt.max_visited_bucket = fallback ? 0 : mx;
+                stt.empty_attention = stt.keys_scored == 0 ? 1 : 0;
+                stt.reserved = 0;
+                a.stats[g] = stt;
+            }
+            trace(5);
+            if (ntiles == 0) {
+                if (lane == 0) {
+                    __threadfence();
+                    atomicAdd(&a.ctr->published, 1u);
+                }
+                return;
+            }
+            tile0 = __shfl_sync(0xFFFFFFFFu, tile0, 0);
+            __shared__ uint32_t s_np1[kPlanTileCnt];
+            const bool np_smem = ntiles <= (uint32_t)kPlanTileCnt;
+            for (uint32_t t = lane; t < ntiles; t += 32) {
+                if (np_smem) s_np1[t] = 0;
+                else a.dyn_tiles[tile0 + t].npieces = 0;
+            }
+            __syncwarp();
+            if (!np_smem) __threadfence_block();
+            for (uint32_t b = lane; b < L; b += 32) {
+                const Seg sg = segs[b];
+                const uint32_t v0 = vpre[b], v8 = v0 + ((sg.len + 7) & ~7u), vend = v0 + sg.len;
+                for (uint32_t t = v0 / kTileRows; t * kTileRows < v8; ++t) {
+                    const uint32_t a0 = max(v0, t * kTileRows), b1 = min(v8, (t + 1) * kTileRows);
+                    const uint32_t kend = min(b1, vend);
+                    if (kend <= a0) continue;
+                    PieceRec pr;
+                    pr.len = kend - a0;
+                    pr.srow = a0 - t * kTileRows;
+                    pr.row = gm.row_base + sg.start + (a0 - v0);
+                    TileRec* tr = a.dyn_tiles + tile0 + t;
+                    const uint32_t slot = atomicAdd(np_smem ? &s_np1[t] : &tr->npieces, 1u);
+                    for (uint32_t hc = 0; hc < nh; ++hc) tr[(size_t)hc * ntiles].p[slot] = pr;
+                }
+            }
+            __syncwarp();
+            // publish: header + release flag per tile (the release is cumulative
+            // over the pieces the warp wrote before the warp barrier)
+            for (uint32_t e = lane; e < ntiles * nh; e += 32) {
+                const uint32_t hc = e / ntiles, t = e % ntiles;
+                TileRec* tr = a.dyn_tiles + tile0 + e;
+                tr->npieces = np_smem ? s_np1[t] : a.dyn_tiles[tile0 + t].npieces;
+                tr->qslot = g * nh + hc;
+                tr->end = t + 1 == ntiles ? 1u : 0u;
+                __threadfence();
+                st_release_u32(&tr->ready, 1u);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                atomicAdd(&a.ctr->published, 1u);
+            }
+            trace(7);
+            return;
+        }
+    }
 
     // ---------------- segments of the visited set      attention.cpp:342-372
     // The dense window (sink span + recent tail) is static work planned on the
@@ -613,9 +731,7 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         s_ntiles = ntiles;
         // reserve this group's dynamic tiles, then report the reservation:
         // decode producers treat the stream as final once every group has
-        s_tile0 = ntiles ? atomicAdd(&a.ctr->dyn, ntiles * nh) : 0;
-        __threadfence();
-        atomicAdd(&a.ctr->groups_done, 1u);
+        s_tile0 = (uint32_t)atomicAdd(&a.ctr->dynres, (1ull << 32) | (unsigned long long)(ntiles * nh));
         for (uint32_t hc = 0; hc < nh; ++hc) a.dyn_cnt[g * nh + hc] = ntiles | kCntValid;
         unsigned long long keys;
         if (fallback) keys = n;
@@ -630,7 +746,13 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
     __syncthreads();
     trace(5);
     const uint32_t ntiles = s_ntiles, tile0 = s_tile0;
-    if (ntiles == 0) return;
+    if (ntiles == 0) {
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(&a.ctr->published, 1u);
+        }
+        return;
+    }
     // piece counters: shared memory when the group's tiles fit, else in place
     __shared__ uint32_t s_np[kPlanTileCnt];
     const bool np_smem = ntiles <= (uint32_t)kPlanTileCnt;
@@ -679,6 +801,11 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         __threadfence();
         st_release_u32(&tr->ready, 1u);
     }
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        atomicAdd(&a.ctr->published, 1u);
+    }
     trace(7);
 }
 
@@ -703,7 +830,7 @@ struct DecodeCfg {
     static constexpr int NT = D / 8;  // PV n-tiles
 };
 
-constexpr int kRecRing = 8;  // work records in flight ahead of the TMA issue
+constexpr int kRecRing = 6;  // work records in flight ahead of the TMA issue
 
 template <int D>
 struct DecodeSmem {
@@ -893,34 +1020,70 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
         }
         const uint64_t pol = l2_evict_first_policy();
         const uint32_t W = a.n_static, CH = a.chunk, M = a.tail;
-        // ticket j -> [b0, b1): 1 ok, 0 not yet reserved by the planner, -1 end
+        constexpr uint32_t TB = 1;  // tickets per grab (the next grab travels while these feed)
+        uint32_t fin_tot = 0;       // stream length once final (0: not yet)
+        bool fin = false, all_pub = a.n_plan_groups == 0;
+        // Ticket j -> work-stream tiles [b0, b1); 1 ok, 0 not yet reserved by
+        // the planner, -1 end.  Static tickets first (chunk_st tiles each, spread
+        // over the CTAs; for a static-only stream its last M tiles go out one
+        // per ticket), then the dynamic part: CH-tile chunks, its last M tiles
+        // one per ticket.
+        const uint32_t CS = a.chunk_st;
+        const uint32_t Bs = a.n_plan_groups == 0 && W > M ? (W - M) / CS * CS : (a.n_plan_groups ? W : 0u);
+        const uint32_t ks = (Bs + CS - 1) / CS + (W - min(W, Bs));  // static tickets
         auto try_chunk = [&](uint32_t j, uint32_t& b0, uint32_t& b1) -> int {
-            const uint32_t gd = ld_acquire_u32(&a.ctr->groups_done);
-            const uint32_t dyn = ld_acquire_u32(&a.ctr->dyn);
-            const uint32_t tot = W + dyn;
-            if (gd >= a.n_plan_groups) {  // final: big chunks, then singles
-                const uint32_t B = tot > M ? (tot - M) / CH * CH : 0u, nb = B / CH;
+            if (j < ks) {
+                const uint32_t nb = (Bs + CS - 1) / CS;
                 if (j < nb) {
-                    b0 = j * CH;
-                    b1 = b0 + CH;
+                    b0 = j * CS;
+                    b1 = min(Bs, b0 + CS);
                 } else {
-                    b0 = B + (j - nb);
-                    if (b0 >= tot) return -1;
+                    b0 = Bs + (j - nb);
                     b1 = b0 + 1;
                 }
                 return 1;
             }
-            if ((j + 1) * CH + M <= tot) {  // big in any final mapping
-                b0 = j * CH;
+            if (a.n_plan_groups == 0) return -1;
+            const uint32_t d = j - ks;
+            uint32_t D = fin_tot;
+            if (!fin) {
+                const unsigned long long dr = ld_acquire_u64(&a.ctr->dynres);
+                D = (uint32_t)dr;
+                if ((uint32_t)(dr >> 32) >= a.n_plan_groups) {
+                    fin = true;
+                    fin_tot = D;
+                }
+            }
+            if (fin) {
+                const uint32_t B = D > M ? (D - M) / CH * CH : 0u, nb = B / CH;
+                if (d < nb) {
+                    b0 = W + d * CH;
+                    b1 = b0 + CH;
+                } else {
+                    b0 = W + B + (d - nb);
+                    if (b0 >= W + D) return -1;
+                    b1 = b0 + 1;
+                }
+                return 1;
+            }
+            if ((d + 1) * CH + M <= D) {  // big in any final mapping
+                b0 = W + d * CH;
                 b1 = b0 + CH;
                 return 1;
             }
             return 0;
         };
-        // dynamic records are published with release stores; every lane
-        // acquires one flag, the warp barrier orders them before lane 0's
-        // (async-proxy) record copies
+        // dynamic records are published with release stores: once every
+        // planner CTA reported (one acquire) no per-record check is needed;
+        // before that every lane acquires one flag of the chunk, and the warp
+        // barrier orders them before lane 0's (async-proxy) record copies
         auto dyn_ready = [&](uint32_t b0, uint32_t b1) -> bool {
+            if (all_pub) return true;
+            if (ld_acquire_u32(&a.ctr->published) >= a.n_plan_groups) {
+                all_pub = true;
+                __syncwarp();
+                return true;
+            }
             bool ok = true;
             const uint32_t i = max(b0, W) + lane;
             if (i < b1) ok = ld_acquire_u32(&a.dyn_tiles[i - W].ready) != 0;
@@ -929,9 +1092,11 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
             return all;
         };
         uint32_t pc0 = 0, pc1 = 0;
-        bool pend = false, feeding = true;
-        uint32_t ticket = blockIdx.x, tk = 0;
-        bool have_ticket = true, tk_inflight = false;
+        bool pend = false, feeding = true, poll_wait = false;
+        // first batch: tickets b and b + grid (the static part spreads over all
+        // CTAs); later batches of TB consecutive tickets from the counter
+        uint32_t ticket = blockIdx.x, ticket_end = 0xFFFFFFFFu, tk = 0, tk_first = blockIdx.x + gridDim.x;
+        if (lane == 0) tk = atomicAdd(&a.ctr->tickets, TB) + 2 * gridDim.x;
         uint32_t head = 0, tail = 0, cnt = 0, rph = 0;  // record ring (rph: phase bit per slot)
         uint32_t stage = 0, phase = 0;
         bool run_first = true;
@@ -943,12 +1108,17 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
             // ---- feed records
             const unsigned long long tf = clock64();
             while (cnt < (uint32_t)kRecRing && feeding) {
+                // waiting for the planner: re-poll only when the ring runs low
+                // (each poll is a round trip on the producer's path)
+                if (!pend && poll_wait && cnt > 1) break;
                 if (!pend) {
-                    if (!have_ticket) {
-                        if (!tk_inflight && lane == 0) tk = atomicAdd(&a.ctr->tickets, 1u) + gridDim.x;
-                        tk_inflight = false;
+                    if (ticket_end == 0xFFFFFFFFu && ticket != blockIdx.x) {  // second ticket of the first batch
+                        ticket = tk_first;
+                        ticket_end = tk_first + 1;
+                    } else if (ticket == ticket_end) {  // next batch (reserved one batch ahead)
                         ticket = __shfl_sync(0xFFFFFFFFu, tk, 0);
-                        have_ticket = true;
+                        ticket_end = ticket + TB;
+                        if (lane == 0) tk = atomicAdd(&a.ctr->tickets, TB) + 2 * gridDim.x;
                     }
                     uint32_t b0 = 0, b1 = 0;
                     const int r = try_chunk(ticket, b0, b1);
@@ -956,15 +1126,17 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
                         feeding = false;
                         break;
                     }
-                    if (r == 0 || (b1 > W && !dyn_ready(b0, b1))) break;  // retry after issuing
+                    if (r == 0 || (b1 > W && !dyn_ready(b0, b1))) {  // retry after issuing
+                        poll_wait = true;
+                        break;
+                    }
+                    poll_wait = false;
                     // acquired generic-proxy data is read by the bulk copies (async proxy)
                     if (b1 > W && lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
                     pc0 = b0;
                     pc1 = b1;
                     pend = true;
-                    have_ticket = false;  // the next ticket travels while this chunk feeds
-                    if (lane == 0) tk = atomicAdd(&a.ctr->tickets, 1u) + gridDim.x;
-                    tk_inflight = true;
+                    ++ticket;
                 }
                 if (lane == 0) {
                     const TileRec* src = pc0 < W ? a.st_tiles + pc0 : a.dyn_tiles + (pc0 - W);
@@ -1086,8 +1258,8 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
             // the last CTA out re-arms the step counters (every reader is done)
             if (atomicAdd(&a.ctr->exited, 1u) == gridDim.x - 1) {
                 a.ctr->tickets = 0;
-                a.ctr->dyn = 0;
-                a.ctr->groups_done = 0;
+                a.ctr->dynres = 0;
+                a.ctr->published = 0;
                 a.ctr->exited = 0;
                 __threadfence();
             }
