@@ -416,6 +416,20 @@ def ours(a):
         buf = (ct.c_uint64 * 16)()
         if sb.lib().saap_debug_plan_trace(ctx.h, buf) == 0:
             plan_trace = list(buf)
+    step_trace = None
+    if os.environ.get("SAAP_STEP_TRACE"):
+        import ctypes as ct
+        buf = (ct.c_uint64 * 8)()
+        sb._check(sb.lib().saap_debug_step_trace(ctx.h, buf, 1))
+        graphs[0].launch()
+        ctx.synchronize()
+        sb._check(sb.lib().saap_debug_step_trace(ctx.h, buf, 0))
+        v = list(buf)
+        t0 = min(x for x in v[0::2] if x)
+        names = ["approx", "plan", "decode", "combine"]
+        step_trace = {n: [round((v[2 * k] - t0) / 1e3, 2) if v[2 * k] != 2**64 - 1 else None,
+                          round((v[2 * k + 1] - t0) / 1e3, 2) if v[2 * k + 1] else None]
+                      for k, n in enumerate(names)}
     decode_trace = None
     if os.environ.get("SAAP_DECODE_TRACE"):
         import ctypes as ct
@@ -528,6 +542,7 @@ def ours(a):
         "prefill_build_ms_per_layer": round(float(np.mean(t_build)), 2),
         "plan_trace_cycles": plan_trace,
         "decode_trace": decode_trace,
+        "step_trace_us": step_trace,
         "prefill": {
             "keys": n_keys_prefill, "assign_ms": round(assign_ms, 3), "pack_ms": round(pack_ms, 3),
             "keys_per_s": round(n_keys_prefill / ((assign_ms + pack_ms) * 1e-3), 1),

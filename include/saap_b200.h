@@ -242,6 +242,11 @@ SAAP_API int saap_debug_exp(saap_ctx* ctx, const double* x, uint64_t n, double* 
  * context 0 of the last routed decode step (16 x u64). */
 SAAP_API int saap_debug_plan_trace(saap_ctx* ctx, uint64_t* out);
 
+/* With SAAP_STEP_TRACE set when the context was created: reset (reset=1) or
+ * read (reset=0) the step timeline: first start / last end (globaltimer ns)
+ * of {approximate routing, planner, decode, combine} (8 x u64). */
+SAAP_API int saap_debug_step_trace(saap_ctx* ctx, uint64_t* out, int reset);
+
 /* With SAAP_DECODE_TRACE set: per attention CTA of the last decode step
  * {start, first tile, end (globaltimer ns), tiles consumed, producer cycles
  * waiting for a free stage, producer cycles total, consumer cycles waiting

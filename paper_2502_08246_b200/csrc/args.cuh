@@ -61,6 +61,7 @@ struct ApproxArgs {
     const float* q_route;          // [groups][G][D]
     uint32_t G, C;
     float* approx;                 // [groups][C]
+    unsigned long long* tl;        // debug step timeline (null: off)
 };
 struct PlanArgs {
     const GroupMeta* meta;
@@ -84,6 +85,7 @@ struct PlanArgs {
     const float* const* centR;   // per group C x d f32 centroids (row-major)
     const float* cmax;           // per group max centroid norm
     unsigned long long* trace;   // debug: clock64 per planning phase (CTA 0)
+    unsigned long long* tl;      // debug step timeline (null: off)
     int route_only;              // BucketRouter::select: write `selected`, plan nothing
     // general-window rows are gathered into a contiguous buffer
     const uint16_t* K;
@@ -119,6 +121,7 @@ struct DecodeArgs {
     uint32_t* runs;  // [qslots] runs reserved
     uint32_t* done;  // [qslots] tiles published
     unsigned long long* dtrace;  // debug: per CTA {start, first tile, end (globaltimer ns), tiles}
+    unsigned long long* tl;      // debug step timeline (null: off)
 };
 
 struct CombineArgs {
@@ -131,6 +134,7 @@ struct CombineArgs {
     uint32_t run_cap;
     uint32_t G, n_hchunks;
     float* out;
+    unsigned long long* tl;  // debug step timeline (null: off)
 };
 
 // Decode tiles live in shared memory as 8-row groups [group][half][8 rows][HALF

@@ -348,6 +348,7 @@ void enqueue_route_score(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
         aa.G = (uint32_t)G;
         aa.C = (uint32_t)C;
         aa.approx = (float*)ensure(c, c->approx, n_groups * C * sizeof(float));
+        aa.tl = c->tl;
         launch_route_approx((int)D, aa, slots ? n_slots : (uint32_t)n_groups, c->stream);
         pa.approx = aa.approx;
         pa.centT = centT;
@@ -566,6 +567,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
         if (routed)
             enqueue_route_score(c, n_groups, D, C, G, probes, mode, centT, q_route, probs, pa, cmax,
                                 centR, slots, n_slots);
+        pa.tl = c->tl;
         static const bool trace_on = std::getenv("SAAP_PLAN_TRACE") != nullptr;
         if (trace_on) pa.trace = (unsigned long long*)ensure(c, c->trace, 128);
         launch_route_plan(pa, (uint32_t)n_groups, routed, st);
@@ -593,6 +595,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->sm_count,
                                                                     (max_stream + chunk - 1) / chunk));
     da.tail = env_u32("SAAP_TAIL_PER_CTA", 1) * (uint32_t)grid;
+    da.tl = c->tl;
     // static tickets: enough to give every CTA a share of the window
     da.chunk_st = plan ? std::max<uint32_t>(1u, std::min<uint32_t>(chunk, sp->n_tiles / (uint32_t)grid)) : chunk;
     static const bool dtrace_on = std::getenv("SAAP_DECODE_TRACE") != nullptr;
@@ -609,6 +612,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     ca.G = (uint32_t)G;
     ca.n_hchunks = (uint32_t)n_hchunks;
     ca.out = out;
+    ca.tl = c->tl;
     launch_combine((int)D, ca, (uint32_t)qslots, st);
     c->launches += 2;
     if (e2) {
@@ -703,6 +707,10 @@ int saap_ctx_create(int device, saap_ctx** out) {
         SAAP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = true;
         c->counters = dmalloc<StepCounters>(1);
+        if (std::getenv("SAAP_STEP_TRACE")) {
+            c->tl = dmalloc<unsigned long long>(8);
+            SAAP_CUDA(cudaMemset(c->tl, 0, 64));
+        }
         SAAP_CUDA(cudaMemset(c->counters, 0, sizeof(StepCounters)));
         ensure_done(c, 4096);
         *out = c;
@@ -720,6 +728,7 @@ int saap_ctx_destroy(saap_ctx* c) {
             if (s->p) cudaFree(s->p);
         dfree(c->counters);
         dfree(c->done);
+        dfree(c->tl);
         if (c->own_stream) cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -1816,6 +1825,24 @@ int saap_debug_plan_trace(saap_ctx* c, uint64_t* out) {
         DeviceGuard dg(c);
         if (!c->trace.p) invalid("plan tracing off: set SAAP_PLAN_TRACE before the first decode");
         d2h(out, c->trace.p, 128, c->stream);
+        sync(c);
+    });
+}
+
+int saap_debug_step_trace(saap_ctx* c, uint64_t* out, int reset) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        if (!c->tl) invalid("step tracing off: set SAAP_STEP_TRACE before creating the context");
+        if (reset) {
+            uint64_t init[8];
+            for (int k = 0; k < 4; ++k) {
+                init[2 * k] = ~0ull;
+                init[2 * k + 1] = 0;
+            }
+            h2d(c->tl, init, 64, c->stream);
+        } else {
+            d2h(out, c->tl, 64, c->stream);
+        }
         sync(c);
     });
 }

@@ -154,6 +154,14 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// debug step timeline: kernel k's first start / last end (globaltimer ns)
+__device__ __forceinline__ void tl_mark(unsigned long long* tl, int k, bool start) {
+    if (!tl) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    if (start) atomicMin(tl + 2 * k, t);
+    else atomicMax(tl + 2 * k + 1, t);
+}
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
@@ -185,6 +193,7 @@ struct saap_ctx {
     // growable device scratch (sized by uncaptured calls; graphs reuse it)
     saap_scratch approx, trace, dtrace, cand_s, cand_i, tiles, part_O, part_ml, probs, stats, sel, qr, qd, out, misc, zeros;
     saap_scratch runs, dyn_cnt;  // per query slot, zero between steps (the combine re-arms them)
+    unsigned long long* tl = nullptr;  // debug step timeline (SAAP_STEP_TRACE)
     saap_b200::StepCounters* counters = nullptr;  // persistent, 128 B
     uint32_t* done = nullptr;                     // per query slot completion counters
     size_t done_cap = 0;

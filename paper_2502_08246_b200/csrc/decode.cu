@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(256) route_approx_kernel(ApproxArgs a) {
     __shared__ float red[8][kSlotGroups][33];
     pdl_trigger();
     const uint32_t s = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) tl_mark(a.tl, 0, true);
     ApproxSlot sl;
     if (a.slots) {
         sl = a.slots[s];
@@ -274,6 +275,7 @@ __global__ void __launch_bounds__(256) route_approx_kernel(ApproxArgs a) {
         for (int w = 0; w < 8; ++w) x += red[w][k][l];
         if (cc < a.C) a.approx[(size_t)sl.group[k] * a.C + cc] = x;
     }
+    if (tid == 0) tl_mark(a.tl, 0, false);
 }
 
 // Stage 2 (one CTA per context): merge the slices' candidates into the top-l
@@ -281,6 +283,7 @@ __global__ void __launch_bounds__(256) route_approx_kernel(ApproxArgs a) {
 __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     pdl_trigger();
+    if (threadIdx.x == 0) tl_mark(a.tl, 1, true);
     pdl_wait();
     const uint32_t g = blockIdx.x;
     const uint32_t tid = threadIdx.x, nth = blockDim.x;
@@ -602,6 +605,7 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
             if (lane == 0) {
                 __threadfence();
                 atomicAdd(&a.ctr->published, 1u);
+                tl_mark(a.tl, 1, false);
             }
             trace(7);
             return;
@@ -920,7 +924,7 @@ __device__ __forceinline__ float bf16_round(float x) {
 }
 
 template <int D>
-__global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
+__global__ void __maxnreg__(144)
         decode_kernel(const __grid_constant__ DecodeMaps maps, DecodeArgs a) {
     using CF = DecodeCfg<D>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -933,6 +937,7 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
         return t;
     };
     if (a.dtrace && threadIdx.x == 0) a.dtrace[16 * blockIdx.x] = gtime();
+    if (threadIdx.x == 0) tl_mark(a.tl, 2, true);
     if (threadIdx.x == 0) {
         for (int i = 0; i < CF::NS; ++i) {
             mbar_init(&s.full[i], 1);
@@ -1301,6 +1306,7 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
         }
         ++n_tiles_done;
         if (mt.x < 0) {
+            if (threadIdx.x == 0) tl_mark(a.tl, 2, false);
             // stop the merge warp once it has drained the last run
             mbar_wait(&s.st_empty, st_ph ^ 1);
             if (threadIdx.x == 0) s.st_slot = 0xFFFFFFFFu;
@@ -1470,72 +1476,99 @@ __global__ void __launch_bounds__((kComputeWarps + 2) * 32, 1)
 // a slot as soon as the slot's tiles are all published, so only the last
 // slots' combines trail the decode.  A slot with no visited key gets zero
 // rows (attention.cpp:147-152).
+// D threads (one float4 of the slot's 4 x D outputs each): small enough to
+// sit next to a decode CTA
 template <int D>
-__global__ void __launch_bounds__(kHeadsPerSlot * D) combine_kernel(CombineArgs a) {
+__global__ void __maxnreg__(80) combine_kernel(CombineArgs a) {
     constexpr int NOUT = kHeadsPerSlot * D;
-    constexpr int kMaxStage = 256;  // runs whose (m, l) are staged in shared memory
-    __shared__ float sml[kMaxStage][8];
+    constexpr int PER = 4;  // consecutive outputs per thread (one head)
+    constexpr int U = 8;  // runs in flight
     __shared__ uint32_t s_total, s_runs;
     const uint32_t qsi = blockIdx.x;
     if (threadIdx.x == 0) {
+        tl_mark(a.tl, 3, true);
         uint32_t total = a.st_cnt[qsi];
         if (a.dyn_cnt) {
             uint32_t v;
-            while (!((v = ld_acquire_u32(a.dyn_cnt + qsi)) & kCntValid)) __nanosleep(128);
+            while (!((v = ld_acquire_u32(a.dyn_cnt + qsi)) & kCntValid)) __nanosleep(256);
             total += v & ~kCntValid;
             a.dyn_cnt[qsi] = 0;
         }
         if (total)
-            while (ld_acquire_u32(a.done + qsi) < total) __nanosleep(128);
+            while (ld_acquire_u32(a.done + qsi) < total) __nanosleep(256);
         s_total = total;
         s_runs = ld_acquire_u32(a.runs + qsi);
         a.done[qsi] = 0;  // re-armed for the next step (this CTA is the only reader)
         a.runs[qsi] = 0;
     }
     __syncthreads();
-    const uint32_t e = threadIdx.x, h = e / D;
+    const uint32_t e0 = threadIdx.x * PER, h = e0 / D;
     const uint32_t g = qsi / a.n_hchunks, hc = qsi % a.n_hchunks;
     const uint32_t head = hc * kHeadsPerSlot + h;
-    float* out = a.out + ((size_t)g * a.G + head) * D + (e % D);
+    float* out = a.out + ((size_t)g * a.G + head) * D + (e0 % D);
     const uint32_t nr = s_runs;
     if (s_total == 0 || nr == 0) {
-        if (head < a.G) *out = 0.f;
+        if (head < a.G)
+#pragma unroll
+            for (int i = 0; i < PER; ++i) out[i] = 0.f;
         return;
     }
+    // one pass, U runs per round with all their loads in flight, online
+    // rescaling to the running max (Alg. 2)
     const size_t base = (size_t)qsi * a.run_cap;
-    const uint32_t ns = min(nr, (uint32_t)kMaxStage);
-    for (uint32_t i = e; i < ns * 8; i += blockDim.x) sml[i / 8][i % 8] = __ldcg(a.part_ml + base * 8 + i);
-    __syncthreads();
-    auto ml = [&](uint32_t i, uint32_t k) {
-        return i < kMaxStage ? sml[i][k] : __ldcg(a.part_ml + (base + i) * 8 + k);
-    };
-    float M = -INFINITY;
-    for (uint32_t i = 0; i < nr; ++i) M = fmaxf(M, ml(i, h));
-    float O = 0.f, L = 0.f;
-    if (M != -INFINITY) {
-        constexpr int U = 8;  // partial rows in flight
-        for (uint32_t i0 = 0; i0 < nr; i0 += U) {
-            float v[U];
+    float M = -INFINITY, O[PER], L = 0.f;
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-                v[u] = i0 + u < nr ? __ldcg(a.part_O + (base + i0 + u) * NOUT + e) : 0.f;
+    for (int i = 0; i < PER; ++i) O[i] = 0.f;
+    for (uint32_t i0 = 0; i0 < nr; i0 += U) {
+        float4 v[U];
+        float mu[U], lu[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (i0 + u < nr) {
-                    const float wgt = fast_exp2(ml(i0 + u, h) - M);
-                    O = fmaf(v[u], wgt, O);
-                    L = fmaf(ml(i0 + u, 4 + h), wgt, L);
-                }
-            }
+        for (int u = 0; u < U; ++u) {
+            const bool ok = i0 + u < nr;
+            v[u] = ok ? __ldcg(reinterpret_cast<const float4*>(a.part_O + (base + i0 + u) * NOUT + e0))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+            mu[u] = ok ? __ldcg(a.part_ml + (base + i0 + u) * 8 + h) : -INFINITY;
+            lu[u] = ok ? __ldcg(a.part_ml + (base + i0 + u) * 8 + 4 + h) : 0.f;
         }
+        float Mn = M;
+#pragma unroll
+        for (int u = 0; u < U; ++u) Mn = fmaxf(Mn, mu[u]);
+        if (Mn == -INFINITY) continue;
+        const float sc = fast_exp2(M - Mn);  // M = -inf -> 0
+#pragma unroll
+        for (int i = 0; i < PER; ++i) O[i] *= sc;
+        L *= sc;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float wgt = fast_exp2(mu[u] - Mn);  // empty run -> 0
+            O[0] = fmaf(v[u].x, wgt, O[0]);
+            O[1] = fmaf(v[u].y, wgt, O[1]);
+            O[2] = fmaf(v[u].z, wgt, O[2]);
+            O[3] = fmaf(v[u].w, wgt, O[3]);
+            L = fmaf(lu[u], wgt, L);
+        }
+        M = Mn;
     }
-    if (head < a.G) *out = L > 0.f ? O / L : 0.f;
+    if (head < a.G)
+#pragma unroll
+        for (int i = 0; i < PER; ++i) out[i] = L > 0.f ? O[i] / L : 0.f;
+    if (threadIdx.x == 0) tl_mark(a.tl, 3, false);
 }
 
 // ============================================================ launchers
 void launch_combine(int D, const CombineArgs& ca, uint32_t n_qslots, cudaStream_t st) {
+    // same shared-memory carveout as the decode kernel, so combine CTAs can sit
+    // next to decode CTAs and combine each slot as soon as it completes
+    static bool configured = false;
+    if (!configured) {
+        for (const void* f : {(const void*)combine_kernel<128>, (const void*)combine_kernel<64>,
+                              (const void*)combine_kernel<32>})
+            SAAP_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                           (int)cudaSharedmemCarveoutMaxShared));
+        configured = true;
+    }
 #define SAAP_COMBINE(DD) \
-    launch_pdl(true, combine_kernel<DD>, dim3(n_qslots), dim3(kHeadsPerSlot * DD), 0, st, ca)
+    launch_pdl(true, combine_kernel<DD>, dim3(n_qslots), dim3(DD), 0, st, ca)
     switch (D) {
         case 128: SAAP_COMBINE(128); break;
         case 64: SAAP_COMBINE(64); break;
@@ -1552,6 +1585,8 @@ static void launch_decode_t(const DecodeMaps& m, const DecodeArgs& a, int grid, 
     if (!configured) {
         SAAP_CUDA(cudaFuncSetAttribute(decode_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
+        SAAP_CUDA(cudaFuncSetAttribute(decode_kernel<D>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       (int)cudaSharedmemCarveoutMaxShared));
         configured = true;
     }
     launch_pdl(true, decode_kernel<D>, dim3(grid), dim3((kComputeWarps + 2) * 32), smem, st, m, a);
