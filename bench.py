@@ -413,9 +413,15 @@ def ours(a):
     plan_trace = None
     if os.environ.get("SAAP_PLAN_TRACE"):
         import ctypes as ct
-        buf = (ct.c_uint64 * 16)()
+        buf = (ct.c_uint64 * (16 + 3 * 1024))()
         if sb.lib().saap_debug_plan_trace(ctx.h, buf) == 0:
-            plan_trace = list(buf)
+            plan_trace = list(buf)[:16]
+            cta = np.array(list(buf)[16:], dtype=np.float64).reshape(1024, 3)
+            cta = cta[cta[:, 0] > 0]
+            if len(cta):
+                t0 = cta[:, 0].min()
+                plan_trace.append({k: [round(float(v), 2) for v in np.percentile((cta[:, i] - t0) / 1e3, [0, 50, 100])]
+                                   for i, k in enumerate(["start_us", "exchanged_us", "end_us"])})
     step_trace = None
     if os.environ.get("SAAP_STEP_TRACE"):
         import ctypes as ct

@@ -239,7 +239,8 @@ SAAP_API int saap_ctx_launch_count(saap_ctx* ctx, uint64_t* out);
 SAAP_API int saap_debug_exp(saap_ctx* ctx, const double* x, uint64_t n, double* out);
 
 /* With SAAP_PLAN_TRACE set: clock64 offsets of the planner's phases for
- * context 0 of the last routed decode step (16 x u64). */
+ * context 0 of the last routed decode step (16 x u64), then per routing CTA
+ * {start, scores exchanged, end} globaltimer ns (3 x 1024 x u64). */
 SAAP_API int saap_debug_plan_trace(saap_ctx* ctx, uint64_t* out);
 
 /* With SAAP_STEP_TRACE set when the context was created: reset (reset=1) or

@@ -63,6 +63,28 @@ struct ApproxArgs {
     float* approx;                 // [groups][C]
     unsigned long long* tl;        // debug step timeline (null: off)
 };
+// Fused routing + planning for the centroid router (C <= 1024, power of two):
+// one cluster of 8 CTAs per approximate-scoring slot.
+struct ClusterRouteArgs {
+    const ApproxSlot* slots;
+    const GroupMeta* meta;
+    const uint32_t* off;
+    const uint32_t* offA;
+    const float* q_route;        // [groups][G][D]
+    const float* const* centR;   // per group C x d f32 centroids (exact re-scoring)
+    const float* cmax;           // per group max centroid norm
+    uint32_t G, C, probes, recent, n_hchunks;
+    TileRec* dyn_tiles;
+    StepCounters* ctr;
+    uint32_t* dyn_cnt;
+    saap_attn_stats* stats;
+    uint32_t* selected;          // nullable [groups][probes]
+    unsigned long long* trace;   // debug: clock64 per phase (slot 0, rank 0)
+    unsigned long long* tl;      // debug step timeline (null: off)
+};
+constexpr int kClusterCtas = 8;
+constexpr int kClusterThreads = 512;
+
 struct PlanArgs {
     const GroupMeta* meta;
     const uint32_t* off;
@@ -110,6 +132,7 @@ struct DecodeArgs {
     uint32_t chunk;            // work-stream tiles per ticket (dynamic part)
     uint32_t chunk_st;         // tiles per ticket in the static part
     uint32_t tail;             // the stream's last `tail` tiles go out one per ticket
+    uint32_t wait_plan;        // 1: wait for the planner grid before streaming
     StepCounters* ctr;
     const float* q;            // [groups][G][D] attention queries (f32)
     uint32_t G;

@@ -15,6 +15,8 @@ namespace saap_b200 {
 
 // ---- kernels (decode.cu / pack.cu / route.cu / synth.cu)
 void launch_route_plan(const PlanArgs& a, uint32_t n_groups, bool pdl, cudaStream_t st);
+void launch_route_cluster(int D, const ClusterRouteArgs& a, uint32_t n_slots, cudaStream_t st);
+bool route_cluster_supported(int D, uint32_t C);
 void launch_route_approx(int D, const ApproxArgs& a, uint32_t n_slots, cudaStream_t st);
 void launch_route_score(const RouteArgs& a, uint32_t n_groups, cudaStream_t st);
 void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st);
@@ -381,6 +383,7 @@ struct DecodeSrc {
     const uint16_t *K = nullptr, *V = nullptr;
     uint16_t *gK = nullptr, *gV = nullptr;
     uint64_t gather_cap = 0;
+    uint64_t recent_hint = ~0ull;  // packed-layout window (layers only)
     const DecodeMaps* maps = nullptr;
 };
 
@@ -564,14 +567,45 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
         pa.stats = stats;
         pa.selected = selected;
         const bool routed = (mode == 1 || mode == 2) && probes > 0;
-        if (routed)
-            enqueue_route_score(c, n_groups, D, C, G, probes, mode, centT, q_route, probs, pa, cmax,
-                                centR, slots, n_slots);
-        pa.tl = c->tl;
         static const bool trace_on = std::getenv("SAAP_PLAN_TRACE") != nullptr;
-        if (trace_on) pa.trace = (unsigned long long*)ensure(c, c->trace, 128);
-        launch_route_plan(pa, (uint32_t)n_groups, routed, st);
-        c->launches++;
+        static const bool no_cluster = std::getenv("SAAP_NO_CLUSTER_ROUTE") != nullptr;
+        // fused cluster routing: centroid router, C a power of two <= 1024,
+        // the packed layout's window (every routed context has rb == T)
+        const bool fused = routed && mode == 1 && slots && cmax && centR && !no_cluster &&
+                           route_cluster_supported((int)D, (uint32_t)C) && probes <= C &&
+                           recent == src.recent_hint;
+        if (fused) {
+            ClusterRouteArgs ra{};
+            ra.slots = slots;
+            ra.meta = src.meta;
+            ra.off = src.off;
+            ra.offA = src.offA;
+            ra.q_route = q_route;
+            ra.centR = centR;
+            ra.cmax = cmax;
+            ra.G = (uint32_t)G;
+            ra.C = (uint32_t)C;
+            ra.probes = (uint32_t)probes;
+            ra.recent = (uint32_t)std::min<uint64_t>(recent, 0xFFFFFFFFull);
+            ra.n_hchunks = (uint32_t)n_hchunks;
+            ra.dyn_tiles = dyn;
+            ra.ctr = c->counters;
+            ra.dyn_cnt = dcnt;
+            ra.stats = stats;
+            ra.selected = selected;
+            ra.tl = c->tl;
+            if (trace_on) ra.trace = (unsigned long long*)ensure(c, c->trace, 128 + 24 * 1024);
+            launch_route_cluster((int)D, ra, n_slots, st);
+            c->launches++;
+        } else {
+            if (routed)
+                enqueue_route_score(c, n_groups, D, C, G, probes, mode, centT, q_route, probs, pa, cmax,
+                                    centR, slots, n_slots);
+            pa.tl = c->tl;
+            if (trace_on) pa.trace = (unsigned long long*)ensure(c, c->trace, 128 + 24 * 1024);
+            launch_route_plan(pa, (uint32_t)n_groups, routed, st);
+            c->launches++;
+        }
     }
     if (e1) SAAP_CUDA(cudaEventRecord(e1, st));
 
@@ -596,6 +630,8 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
                                                                     (max_stream + chunk - 1) / chunk));
     da.tail = env_u32("SAAP_TAIL_PER_CTA", 1) * (uint32_t)grid;
     da.tl = c->tl;
+    static const int wait_env = std::getenv("SAAP_DECODE_WAIT") ? std::atoi(std::getenv("SAAP_DECODE_WAIT")) : 0;
+    da.wait_plan = plan && wait_env ? 1u : 0u;
     // static tickets: enough to give every CTA a share of the window
     da.chunk_st = plan ? std::max<uint32_t>(1u, std::min<uint32_t>(chunk, sp->n_tiles / (uint32_t)grid)) : chunk;
     static const bool dtrace_on = std::getenv("SAAP_DECODE_TRACE") != nullptr;
@@ -662,6 +698,7 @@ DecodeSrc layer_src(saap_layer* L, uint64_t recent, bool need_gather) {
     s.gK = L->gK;
     s.gV = L->gV;
     s.gather_cap = L->gather_cap;
+    s.recent_hint = L->recent_hint;
     s.maps = (const DecodeMaps*)L->maps;
     return s;
 }
@@ -1824,7 +1861,7 @@ int saap_debug_plan_trace(saap_ctx* c, uint64_t* out) {
     return guard([&] {
         DeviceGuard dg(c);
         if (!c->trace.p) invalid("plan tracing off: set SAAP_PLAN_TRACE before the first decode");
-        d2h(out, c->trace.p, 128, c->stream);
+        d2h(out, c->trace.p, 128 + 24 * 1024, c->stream);
         sync(c);
     });
 }

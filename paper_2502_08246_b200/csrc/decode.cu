@@ -813,6 +813,409 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
     trace(7);
 }
 
+// ============================================================ fused cluster routing
+// Centroid router + planner in one launch (CentroidRouter::select
+// attention.cpp:275-306, top_l_ids :259-271, visited set :342-372).  A cluster
+// of 8 CTAs serves one slot (<= 8 contexts sharing a partition): CTA r scores
+// centroids [r*C/8, (r+1)*C/8) for every context of the slot in fp32 (its
+// centroid slice stays in registers) and stores context k's scores into CTA
+// k's shared memory (distributed shared memory).  After one cluster barrier
+// CTA k owns all C scores of context k and selects its top-l exactly: fp32
+// radix select, candidates within the error bound 2B of the l-th score, exact
+// fp64 chains (reference operation order) only when the boundary is
+// ambiguous or the ordered list is requested.  Warp 0 then plans and
+// publishes the context's bucket tiles.
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void dsmem_st_f32(float* local, uint32_t cta, float v) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(cta));
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int D, int S>
+__global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterRouteArgs a) {
+    constexpr uint32_t NT = kClusterThreads;
+    constexpr uint32_t TPC = NT / S, DPT = D / TPC;  // threads per centroid, dims per thread
+    static_assert(NT % S == 0 && D % TPC == 0 && DPT % 4 == 0, "slice geometry");
+    constexpr uint32_t kMaxC = 1024;
+    constexpr uint32_t kMaxCand = 64;
+    __shared__ float sc_all[kMaxC];            // this CTA's context: every centroid's fp32 score
+    __shared__ double pd[D];                   // own context: pooled query in fp64
+    __shared__ uint32_t s_off[kMaxC + 1], s_offA[kMaxC + 1];
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t cand_id[kMaxCand], sel[kMaxC];
+    __shared__ uint32_t s_np[kPlanTileCnt];
+    // phase-local buffers share one region: scoring | exact sort | planning
+    union Phase {
+        struct {
+            float pf[kSlotGroups][D];    // pooled queries (f32) of the slot's contexts
+            float red[kSlotGroups][NT];  // partial dot products
+        } score;
+        struct {
+            double xs[kMaxC];
+            uint32_t xi[kMaxC];
+        } sort;
+        struct {
+            Seg segs[kMaxC];
+            uint32_t vpre[kMaxC];
+        } plan;
+    };
+    __shared__ __align__(16) Phase ph;
+    auto& pf = ph.score.pf;
+    auto& red = ph.score.red;
+    auto& xs = ph.sort.xs;
+    auto& xi = ph.sort.xi;
+    auto& segs = ph.plan.segs;
+    auto& vpre = ph.plan.vpre;
+    __shared__ uint32_t s_pref, s_need, s_ncand;
+    __shared__ double s_n2[NT / 32];
+    pdl_trigger();
+    const uint32_t tid = threadIdx.x, lane = tid & 31;
+    const uint32_t rank = cluster_rank(), slot = blockIdx.x / kClusterCtas;
+    if (tid == 0) tl_mark(a.tl, 1, true);
+    auto gt = []() {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        return t;
+    };
+    if (a.trace && tid == 0) a.trace[16 + 3 * blockIdx.x] = gt();
+    unsigned long long t0 = 0;
+    const bool tr = a.trace && slot == 0 && rank == 0 && tid == 0;
+    if (tr) t0 = clock64();
+    auto trace = [&](int k) {
+        if (tr) a.trace[k] = clock64() - t0;
+    };
+    extern __shared__ __align__(16) float dyn_smem[];
+    float* slab = dyn_smem;                    // [D][S] this CTA's centroid slice (transposed)
+    const ApproxSlot sl = a.slots[slot];
+    const uint32_t ng = sl.count, C = a.C;  // C == 8 * S
+    float* qs = slab + (size_t)D * S;          // [ng][G][D] member queries
+    const bool own = rank < ng;
+    const uint32_t g = own ? sl.group[rank] : 0u;
+    // ---- loads, all in one round trip: the slice rows and the member query
+    // rows by bulk copies (TMA engine) onto one barrier, own offsets by loads
+    __shared__ __align__(8) uint64_t bar;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint32_t qbytes = a.G * D * 4;
+    if (tid == 0) mbar_arrive_expect_tx(&bar, D * S * 4 + ng * qbytes);
+    __syncthreads();
+    for (uint32_t j = tid; j < D; j += NT)
+        bulk_g2s(slab + (size_t)j * S, sl.centT + (size_t)j * C + rank * S, S * 4, &bar);
+    for (uint32_t k = tid; k < ng; k += NT)
+        bulk_g2s(qs + (size_t)k * a.G * D, a.q_route + (size_t)sl.group[k] * a.G * D, qbytes, &bar);
+    GroupMeta gm{};
+    if (own) {
+        gm = a.meta[g];
+        const uint32_t* og = a.off + (size_t)g * (C + 1);
+        const uint32_t* oAg = a.offA + (size_t)g * (C + 1);
+        for (uint32_t i = tid; i <= C; i += NT) {
+            s_off[i] = og[i];
+            s_offA[i] = oAg[i];
+        }
+    }
+    mbar_wait(&bar, 0);
+    // pooled_j = sum_i q_ij in fp64, rows in order   attention.cpp:289-295
+    for (uint32_t e = tid; e < ng * D; e += NT) {
+        const uint32_t k = e / D, j = e % D;
+        const double ps = pooled_sum(qs + (size_t)k * a.G * D + j, a.G, D);
+        pf[k][j] = (float)ps;
+        if (k == rank) pd[j] = ps;
+    }
+    __syncthreads();
+    trace(0);
+    // ---- fp32 scores of this CTA's slice for every member, to the owners
+    // the slice column stays in registers; pooled rows are float4 broadcasts
+    // (shared-memory traffic ~1/4 of an FMA each)
+    const uint32_t cl = tid % S, part = tid / S;
+    float cv[DPT];
+#pragma unroll
+    for (int jj = 0; jj < (int)DPT; ++jj) cv[jj] = slab[(part * DPT + jj) * S + cl];
+    // the slot's contexts are independent accumulation chains (ILP)
+    float x[kSlotGroups];
+#pragma unroll
+    for (int k = 0; k < kSlotGroups; ++k) x[k] = 0.f;
+#pragma unroll
+    for (int j4 = 0; j4 < (int)DPT / 4; ++j4) {
+#pragma unroll
+        for (int k = 0; k < kSlotGroups; ++k) {
+            if ((uint32_t)k < ng) {
+                const float4 p4 = reinterpret_cast<const float4*>(&pf[k][part * DPT])[j4];
+                x[k] = fmaf(p4.x, cv[4 * j4], x[k]);
+                x[k] = fmaf(p4.y, cv[4 * j4 + 1], x[k]);
+                x[k] = fmaf(p4.z, cv[4 * j4 + 2], x[k]);
+                x[k] = fmaf(p4.w, cv[4 * j4 + 3], x[k]);
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kSlotGroups; ++k)
+        if ((uint32_t)k < ng) red[k][tid] = x[k];
+    __syncthreads();
+    trace(6);
+    for (uint32_t e = tid; e < ng * S; e += NT) {
+        const uint32_t k = e / S, cc = e % S;
+        float x = 0.f;
+        for (uint32_t p = 0; p < TPC; ++p) x += red[k][p * S + cc];
+        dsmem_st_f32(&sc_all[rank * S + cc], k, x);
+    }
+    trace(7);
+    cluster_sync_all();  // every owner now holds all C scores of its context
+    trace(1);
+    if (a.trace && tid == 0) a.trace[16 + 3 * blockIdx.x + 1] = gt();
+    if (!own) {
+        if (tid == 0) tl_mark(a.tl, 1, false);
+        return;
+    }
+    const uint32_t n = gm.n, sink = gm.sink, T = gm.T;
+    const bool fallback = n <= sink + a.recent;
+    const bool route = !fallback && a.probes > 0;
+    const uint32_t L = route ? a.probes : 0u;
+    constexpr uint32_t PER = kMaxC / NT;  // scores per thread
+    if (route) {
+        // |pooled|_2 for the error bound
+        double part2 = 0.0;
+        for (uint32_t j = tid; j < D; j += NT) part2 += pd[j] * pd[j];
+        for (int o = 16; o; o >>= 1) part2 += __shfl_xor_sync(0xFFFFFFFFu, part2, o);
+        if (lane == 0) s_n2[tid >> 5] = part2;
+        // radix select (8-bit digits, MSB first): the L-th largest score
+        uint32_t key[PER];
+        float av[PER];
+#pragma unroll
+        for (uint32_t i = 0; i < PER; ++i) {
+            const uint32_t cc = tid + i * NT;
+            av[i] = cc < C ? sc_all[cc] : -INFINITY;
+            const uint32_t u = __float_as_uint(av[i]);
+            key[i] = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+        }
+        if (tid == 0) {
+            s_pref = 0;
+            s_need = L;
+        }
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            if (tid < 256) hist[tid] = 0;
+            __syncthreads();
+            const uint32_t pref = s_pref;
+            const uint32_t hmask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
+#pragma unroll
+            for (uint32_t i = 0; i < PER; ++i)
+                if (tid + i * NT < C && (key[i] & hmask) == (pref & hmask)) atomicAdd(&hist[(key[i] >> shift) & 255u], 1u);
+            __syncthreads();
+            if (tid < 32) {
+                uint32_t cnt[8], tot = 0;
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    cnt[b] = hist[255 - 8 * tid - b];
+                    tot += cnt[b];
+                }
+                uint32_t incl = tot;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (tid >= (uint32_t)o) incl += v;
+                }
+                const uint32_t need = s_need, before = incl - tot;
+                if (before < need && incl >= need) {
+                    uint32_t run = before;
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        if (run + cnt[b] >= need) {
+                            s_pref = pref | ((uint32_t)(255 - 8 * tid - b) << shift);
+                            s_need = need - run;
+                            break;
+                        }
+                        run += cnt[b];
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        trace(2);
+        const uint32_t tk = s_pref;
+        const float t_l = __uint_as_float((tk & 0x80000000u) ? (tk & 0x7FFFFFFFu) : ~tk);
+        double n2 = 0.0;
+        for (uint32_t w = 0; w < NT / 32; ++w) n2 += s_n2[w];
+        // |approx - exact| <= B = 2^-16 |pooled|_2 max|c|_2 (pooled rounded to
+        // f32: 2^-24 rel; fp32 accumulation of D products: D 2^-24 rel)
+        const float B2 = (float)(2.0 * 0x1p-16 * sqrt(n2) * (double)a.cmax[g]) * 1.0001f;
+        if (tid == 0) s_ncand = 0;
+        __syncthreads();
+#pragma unroll
+        for (uint32_t i = 0; i < PER; ++i) {
+            const uint32_t cc = tid + i * NT;
+            const bool cand = cc < C && av[i] >= t_l - B2;
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, cand);
+            uint32_t wbase = 0;
+            if (lane == 0 && bal) wbase = atomicAdd(&s_ncand, __popc(bal));
+            wbase = __shfl_sync(0xFFFFFFFFu, wbase, 0);
+            const uint32_t slotc = wbase + __popc(bal & ((1u << lane) - 1));
+            if (cand && slotc < kMaxCand) cand_id[slotc] = cc;
+        }
+        __syncthreads();
+        const uint32_t nS = s_ncand;
+        trace(3);
+        // the candidates are a superset of the exact top-L: exactly L of them
+        // are the exact set (attention does not depend on the order)
+        if (a.selected == nullptr && nS == L && L <= kMaxCand) {
+            if (tid < L) sel[tid] = cand_id[tid];
+        } else if (nS <= kMaxCand) {
+            // exact fp64 chains (attention.cpp:296-304: mul rounded before add)
+            // over the candidates' centroid rows, staged (coalesced) into the
+            // now free slice buffer
+            float* crow = slab;  // [nS][D + 1]
+            const float* cR = a.centR[g];
+            for (uint32_t e = tid; e < nS * D; e += NT) {
+                const uint32_t r = e / D, j = e % D;
+                crow[r * (D + 1) + j] = cR[(size_t)cand_id[r] * D + j];
+            }
+            __syncthreads();
+            double ex = -INFINITY;
+            uint32_t eid = 0xFFFFFFFFu;
+            if (tid < nS) {
+                const float* row = crow + tid * (D + 1);
+                double sx = 0.0;
+#pragma unroll 8
+                for (uint32_t j = 0; j < D; ++j) sx = __dadd_rn(sx, __dmul_rn(pd[j], (double)row[j]));
+                ex = sx;
+                eid = cand_id[tid];
+            }
+            uint32_t p2s = 1;
+            while (p2s < nS) p2s <<= 1;
+            bitonic_regs(ex, eid, p2s, xs, xi);  // (score desc, id asc): attention.cpp:263-268
+            __syncthreads();
+            if (tid < L) sel[tid] = eid;
+        } else {
+            // degenerate (many near-ties): exact chains for every candidate
+            uint32_t P2 = 1;
+            while (P2 < C) P2 <<= 1;
+            for (uint32_t cc = tid; cc < P2; cc += NT) {
+                double ex = -INFINITY;
+                uint32_t eid = 0xFFFFFFFFu;
+                if (cc < C && sc_all[cc] >= t_l - B2) {
+                    const float* row = a.centR[g] + (size_t)cc * D;
+                    double sx = 0.0;
+                    for (uint32_t j = 0; j < D; ++j) sx = __dadd_rn(sx, __dmul_rn(pd[j], (double)row[j]));
+                    ex = sx;
+                    eid = cc;
+                }
+                xs[cc] = ex;
+                xi[cc] = eid;
+            }
+            __syncthreads();
+            bitonic_smem(xs, xi, P2);
+            if (tid < L) sel[tid] = xi[tid];
+        }
+        __syncthreads();
+        if (a.selected)
+            for (uint32_t b = tid; b < L; b += NT) a.selected[(size_t)g * a.probes + b] = sel[b];
+        trace(4);
+    }
+    // ---- plan (one warp): bucket segments -> 8-aligned virtual rows -> tiles
+    if (tid >= 32) return;
+    const uint32_t nh = a.n_hchunks;
+    const uint32_t rb0 = fallback ? 0 : n - a.recent;  // == T (recent == the layer's hint)
+    unsigned long long keys = 0;
+    uint32_t mx = 0, vrows = 0;
+    for (uint32_t b0 = 0; b0 < L; b0 += 32) {
+        const uint32_t b = b0 + lane;
+        uint32_t lenA = 0, st = 0;
+        if (b < L) {
+            const uint32_t cc = sel[b];
+            mx = max(mx, s_off[cc + 1] - s_off[cc]);  // raw bucket size (attention.cpp:356)
+            lenA = s_offA[cc + 1] - s_offA[cc];
+            st = sink + s_offA[cc];
+        }
+        keys += lenA;
+        const uint32_t v8 = (lenA + 7) & ~7u;
+        uint32_t incl = v8;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += v;
+        }
+        if (b < L) {
+            segs[b] = Seg{KIND_ROWS, lenA, st};
+            vpre[b] = vrows + incl - v8;
+        }
+        vrows += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        keys += __shfl_xor_sync(0xFFFFFFFFu, keys, o);
+        mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    }
+    const uint32_t ntiles = (vrows + kTileRows - 1) / kTileRows;
+    uint32_t tile0 = 0;
+    if (lane == 0) {
+        tile0 = (uint32_t)atomicAdd(&a.ctr->dynres, (1ull << 32) | (unsigned long long)(ntiles * nh));
+        for (uint32_t hc = 0; hc < nh; ++hc) a.dyn_cnt[g * nh + hc] = ntiles | kCntValid;
+        saap_attn_stats stt;
+        stt.keys_scored = fallback ? (unsigned long long)n : (unsigned long long)sink + (n - rb0) + keys;
+        stt.max_visited_bucket = fallback ? 0 : mx;
+        stt.empty_attention = stt.keys_scored == 0 ? 1 : 0;
+        stt.reserved = 0;
+        a.stats[g] = stt;
+    }
+    (void)T;
+    tile0 = __shfl_sync(0xFFFFFFFFu, tile0, 0);
+    if (ntiles) {
+        const bool np_smem = ntiles <= (uint32_t)kPlanTileCnt;
+        for (uint32_t t = lane; t < ntiles; t += 32) {
+            if (np_smem) s_np[t] = 0;
+            else a.dyn_tiles[tile0 + t].npieces = 0;
+        }
+        __syncwarp();
+        if (!np_smem) __threadfence_block();
+        for (uint32_t b = lane; b < L; b += 32) {
+            const Seg sg = segs[b];
+            const uint32_t v0 = vpre[b], v8 = v0 + ((sg.len + 7) & ~7u), vend = v0 + sg.len;
+            for (uint32_t t = v0 / kTileRows; t * kTileRows < v8; ++t) {
+                const uint32_t a0 = max(v0, t * kTileRows), b1 = min(v8, (t + 1) * kTileRows);
+                const uint32_t kend = min(b1, vend);
+                if (kend <= a0) continue;
+                PieceRec pr;
+                pr.len = kend - a0;
+                pr.srow = a0 - t * kTileRows;
+                pr.row = gm.row_base + sg.start + (a0 - v0);
+                TileRec* trp = a.dyn_tiles + tile0 + t;
+                const uint32_t sl2 = atomicAdd(np_smem ? &s_np[t] : &trp->npieces, 1u);
+                for (uint32_t hc = 0; hc < nh; ++hc) trp[(size_t)hc * ntiles].p[sl2] = pr;
+            }
+        }
+        __syncwarp();
+        for (uint32_t e = lane; e < ntiles * nh; e += 32) {
+            const uint32_t hc = e / ntiles, t = e % ntiles;
+            TileRec* trp = a.dyn_tiles + tile0 + e;
+            trp->npieces = np_smem ? s_np[t] : a.dyn_tiles[tile0 + t].npieces;
+            trp->qslot = g * nh + hc;
+            trp->end = t + 1 == ntiles ? 1u : 0u;
+        }
+        // one fence per lane orders every record the warp wrote (the warp
+        // barrier makes the other lanes' writes cumulative) before the flags
+        __syncwarp();
+        __threadfence();
+        __syncwarp();
+        for (uint32_t e = lane; e < ntiles * nh; e += 32)
+            *reinterpret_cast<volatile uint32_t*>(&a.dyn_tiles[tile0 + e].ready) = 1u;
+    }
+    if (lane == 0) {
+        if (!ntiles) __threadfence();
+        atomicAdd(&a.ctr->published, 1u);
+        tl_mark(a.tl, 1, false);
+        if (a.trace) a.trace[16 + 3 * blockIdx.x + 2] = gt();
+    }
+    trace(5);
+}
+
 // ============================================================ attention
 // One CTA per SM.  Warp 8 produces: TMA (cp.async.bulk.tensor, 128B/64B
 // swizzle) loads of 128-row K and V tiles into an NS-deep ring; the 8
@@ -958,6 +1361,7 @@ __global__ void __maxnreg__(144)
     // by the (resident) planner through ready flags.  The combine grid may
     // launch once every decode CTA is resident.
     pdl_trigger();
+    if (a.wait_plan) pdl_wait();  // routing runs on an idle memory system first
 
     if (warp == kComputeWarps + 1) {
         // ------------------------------------------------ merge warp
@@ -1624,6 +2028,46 @@ void launch_route_approx(int D, const ApproxArgs& a, uint32_t n_slots, cudaStrea
         default: fail(SAAP_ERR_UNSUPPORTED, "route: unsupported head dim " + std::to_string(D));
     }
     SAAP_CUDA(cudaGetLastError());
+}
+
+bool route_cluster_supported(int D, uint32_t C) {
+    const uint32_t S = C / kClusterCtas;
+    if (C % kClusterCtas) return false;
+    return (D == 128 && (S == 128 || S == 64 || S == 32)) || (D == 64 && (S == 128 || S == 64)) ||
+           (D == 32 && S == 128);
+}
+
+void launch_route_cluster(int D, const ClusterRouteArgs& a, uint32_t n_slots, cudaStream_t st) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(n_slots * kClusterCtas);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kClusterCtas;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    // dynamic smem: centroid slice [D][C/8] + member queries [8][G][D] (f32)
+    cfg.dynamicSmemBytes = ((size_t)D * (a.C / kClusterCtas) + (size_t)kSlotGroups * a.G * D) * 4;
+    if (cfg.dynamicSmemBytes > 160 * 1024) fail(SAAP_ERR_UNSUPPORTED, "route: slice too large");
+    auto go = [&](auto kern) {
+        static bool configured = false;  // one per instantiation
+        if (!configured) {
+            SAAP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+            configured = true;
+        }
+        SAAP_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    };
+    const uint32_t S = a.C / kClusterCtas;
+    if (D == 128 && S == 128) go(route_cluster_kernel<128, 128>);
+    else if (D == 128 && S == 64) go(route_cluster_kernel<128, 64>);
+    else if (D == 128 && S == 32) go(route_cluster_kernel<128, 32>);
+    else if (D == 64 && S == 128) go(route_cluster_kernel<64, 128>);
+    else if (D == 64 && S == 64) go(route_cluster_kernel<64, 64>);
+    else if (D == 32 && S == 128) go(route_cluster_kernel<32, 128>);
+    else fail(SAAP_ERR_UNSUPPORTED, "route: no fused routing kernel for this geometry");
 }
 
 void launch_route_plan(const PlanArgs& a, uint32_t n_groups, bool pdl, cudaStream_t st) {
