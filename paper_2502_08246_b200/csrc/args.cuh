@@ -125,6 +125,8 @@ struct PlanArgs {
 constexpr uint32_t kCntValid = 0x80000000u;
 
 struct DecodeArgs {
+    const CUtensorMap* tmaps;  // DecodeMaps::dev
+    uint64_t rows, grows;      // rows of the cache / gather tensors (box bounds)
     const TileRec* st_tiles;   // static part of the work stream [n_static]
     TileRec* dyn_tiles;        // dynamic part (ready flags cleared after use)
     uint32_t n_static;
@@ -162,13 +164,16 @@ struct CombineArgs {
 
 // Decode tiles live in shared memory as 8-row groups [group][half][8 rows][HALF
 // bytes] (HALF = min(row bytes, 128), TMA-swizzled).  One 4-D TMA request
-// moves 8*2^i rows (i = 0..4) of both halves of K (or V) straight into that
+// moves 8*G rows (G = 1..16) of both halves of K (or V) straight into that
 // layout: dims {HALF elems, rows, halves, 16 groups} with strides {row, HALF,
-// 8 rows} (the group dimension overlaps the row dimension on purpose).
-constexpr int kBoxSizes = 5;  // boxes of 8, 16, 32, 64, 128 rows
+// 8 rows} (the group dimension overlaps the row dimension on purpose, so a
+// piece of any 8-row multiple is one request).  The 64 maps (K, V, gather K,
+// gather V) x 16 heights live in device memory.
+constexpr int kBoxSizes = 16;  // boxes of 8, 16, ..., 128 rows
 struct DecodeMaps {
-    CUtensorMap k[kBoxSizes], v[kBoxSizes];    // layer (or dense) cache
-    CUtensorMap gk[kBoxSizes], gv[kBoxSizes];  // gather buffer
+    CUtensorMap* dev = nullptr;  // [4][kBoxSizes] in device memory (64-B aligned)
+    uint64_t rows = 0, grows = 0;
+    ~DecodeMaps();
 };
 
 struct QModelArgs {

@@ -19,7 +19,7 @@ void launch_route_cluster(int D, const ClusterRouteArgs& a, uint32_t n_slots, cu
 bool route_cluster_supported(int D, uint32_t C);
 void launch_route_approx(int D, const ApproxArgs& a, uint32_t n_slots, cudaStream_t st);
 void launch_route_score(const RouteArgs& a, uint32_t n_groups, cudaStream_t st);
-void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st);
+void launch_decode(int D, const DecodeArgs& a, int grid, cudaStream_t st);
 void launch_combine(int D, const CombineArgs& ca, uint32_t n_qslots, cudaStream_t st);
 void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st);
 void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t n_tiles,
@@ -393,12 +393,17 @@ DecodeMaps* build_maps(const void* K, const void* V, uint64_t rows, uint32_t D, 
     const void* a = gK ? gK : K;
     const void* b = gV ? gV : V;
     const uint64_t r = gK ? grows : rows;
+    std::vector<CUtensorMap> h(4 * kBoxSizes);
     for (int i = 0; i < kBoxSizes; ++i) {
-        m->k[i] = make_group_map(K, rows, D, 1u << i);
-        m->v[i] = make_group_map(V, rows, D, 1u << i);
-        m->gk[i] = make_group_map(a, r, D, 1u << i);
-        m->gv[i] = make_group_map(b, r, D, 1u << i);
+        h[0 * kBoxSizes + i] = make_group_map(K, rows, D, (uint32_t)i + 1);
+        h[1 * kBoxSizes + i] = make_group_map(V, rows, D, (uint32_t)i + 1);
+        h[2 * kBoxSizes + i] = make_group_map(a, r, D, (uint32_t)i + 1);
+        h[3 * kBoxSizes + i] = make_group_map(b, r, D, (uint32_t)i + 1);
     }
+    m->dev = dmalloc<CUtensorMap>(h.size());
+    SAAP_CUDA(cudaMemcpy(m->dev, h.data(), h.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    m->rows = rows;
+    m->grows = r;
     return m;
 }
 
@@ -636,7 +641,10 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     da.chunk_st = plan ? std::max<uint32_t>(1u, std::min<uint32_t>(chunk, sp->n_tiles / (uint32_t)grid)) : chunk;
     static const bool dtrace_on = std::getenv("SAAP_DECODE_TRACE") != nullptr;
     if (dtrace_on) da.dtrace = (unsigned long long*)ensure(c, c->dtrace, (size_t)c->sm_count * 128);
-    launch_decode((int)D, *src.maps, da, grid, st);
+    da.tmaps = src.maps->dev;
+    da.rows = src.maps->rows;
+    da.grows = src.maps->grows;
+    launch_decode((int)D, da, grid, st);
     CombineArgs ca{};
     ca.st_cnt = sp->cnt;
     ca.dyn_cnt = dcnt;
@@ -706,6 +714,9 @@ DecodeSrc layer_src(saap_layer* L, uint64_t recent, bool need_gather) {
 }  // namespace
 
 namespace saap_b200 {
+DecodeMaps::~DecodeMaps() {
+    if (dev) cudaFree(dev);
+}
 void set_error(const std::string& m) { g_err = m; }
 [[noreturn]] void fail(int code, const std::string& msg) { throw Failure{code, msg}; }
 void check_cuda(cudaError_t e, const char* what) {

@@ -1237,7 +1237,7 @@ struct DecodeCfg {
     static constexpr int NT = D / 8;  // PV n-tiles
 };
 
-constexpr int kRecRing = 6;  // work records in flight ahead of the TMA issue
+constexpr int kRecRing = 3;  // work records in flight ahead of the TMA issue
 
 template <int D>
 struct DecodeSmem {
@@ -1328,7 +1328,7 @@ __device__ __forceinline__ float bf16_round(float x) {
 
 template <int D>
 __global__ void __maxnreg__(144)
-        decode_kernel(const __grid_constant__ DecodeMaps maps, DecodeArgs a) {
+        decode_kernel(const __grid_constant__ DecodeArgs a) {
     using CF = DecodeCfg<D>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     auto& s = *reinterpret_cast<DecodeSmem<D>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
@@ -1423,10 +1423,7 @@ __global__ void __maxnreg__(144)
         // `tail` tiles of the stream are single-tile chunks so the CTAs finish
         // together.  A feeder keeps up to kRecRing work records in flight
         // (bulk copies into shared memory) ahead of the TMA issue.
-        if (lane < kBoxSizes) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.k[lane]) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.v[lane]) : "memory");
-        }
+        if (lane < 2 * kBoxSizes) asm volatile("prefetch.tensormap [%0];" ::"l"(a.tmaps + lane) : "memory");
         const uint64_t pol = l2_evict_first_policy();
         const uint32_t W = a.n_static, CH = a.chunk, M = a.tail;
         constexpr uint32_t TB = 1;  // tickets per grab (the next grab travels while these feed)
@@ -1438,21 +1435,35 @@ __global__ void __maxnreg__(144)
         // per ticket), then the dynamic part: CH-tile chunks, its last M tiles
         // one per ticket.
         const uint32_t CS = a.chunk_st;
-        const uint32_t Bs = a.n_plan_groups == 0 && W > M ? (W - M) / CS * CS : (a.n_plan_groups ? W : 0u);
-        const uint32_t ks = (Bs + CS - 1) / CS + (W - min(W, Bs));  // static tickets
+        // Guided tail: a region of R tiles goes out in CH-tile chunks, then its
+        // last 3M tiles as 2M tiles in pairs and M singles, so CTAs finish
+        // within about a tile of each other.
+        auto guided = [&](uint32_t d, uint32_t R, uint32_t ch, uint32_t& b0, uint32_t& b1) -> bool {
+            const uint32_t tail = 3 * M;
+            const uint32_t B = R > tail ? (R - tail) / ch * ch : 0u, nb = B / ch;
+            if (d < nb) {
+                b0 = d * ch;
+                b1 = b0 + ch;
+                return true;
+            }
+            const uint32_t rest = R - B, S1 = rest > M ? (rest - M) / 2 * 2 : 0u, np = S1 / 2, e = d - nb;
+            if (e < np) {
+                b0 = B + 2 * e;
+                b1 = b0 + 2;
+                return true;
+            }
+            b0 = B + S1 + (e - np);
+            b1 = b0 + 1;
+            return b0 < R;
+        };
+        const uint32_t ks = a.n_plan_groups ? (W + CS - 1) / CS : 0xFFFFFFFFu;  // static tickets
         auto try_chunk = [&](uint32_t j, uint32_t& b0, uint32_t& b1) -> int {
+            if (a.n_plan_groups == 0) return guided(j, W, CS, b0, b1) ? 1 : -1;  // static stream
             if (j < ks) {
-                const uint32_t nb = (Bs + CS - 1) / CS;
-                if (j < nb) {
-                    b0 = j * CS;
-                    b1 = min(Bs, b0 + CS);
-                } else {
-                    b0 = Bs + (j - nb);
-                    b1 = b0 + 1;
-                }
+                b0 = j * CS;
+                b1 = min(W, b0 + CS);
                 return 1;
             }
-            if (a.n_plan_groups == 0) return -1;
             const uint32_t d = j - ks;
             uint32_t D = fin_tot;
             if (!fin) {
@@ -1464,18 +1475,12 @@ __global__ void __maxnreg__(144)
                 }
             }
             if (fin) {
-                const uint32_t B = D > M ? (D - M) / CH * CH : 0u, nb = B / CH;
-                if (d < nb) {
-                    b0 = W + d * CH;
-                    b1 = b0 + CH;
-                } else {
-                    b0 = W + B + (d - nb);
-                    if (b0 >= W + D) return -1;
-                    b1 = b0 + 1;
-                }
+                if (!guided(d, D, CH, b0, b1)) return -1;
+                b0 += W;
+                b1 += W;
                 return 1;
             }
-            if ((d + 1) * CH + M <= D) {  // big in any final mapping
+            if ((d + 2) * CH + 3 * M <= D) {  // big in any final mapping
                 b0 = W + d * CH;
                 b1 = b0 + CH;
                 return 1;
@@ -1620,24 +1625,27 @@ __global__ void __maxnreg__(144)
             __syncwarp();
             const unsigned long long tt = clock64();
             if (len) {
-                // binary decomposition: boxes of 128..16 rows cover only rows of
-                // the piece (their group dimension is not bounds-checked), the
-                // 8-row box takes the rounded-up remainder (zero-filled past the end)
-                const CUtensorMap* mk = gat ? maps.gk : maps.k;
-                const CUtensorMap* mv = gat ? maps.gv : maps.v;
-                uint32_t full = len & ~7u, sr = srow, rem = r8;
-                int y = (int)row;
-                while (rem) {
-                    int i = 0;
-                    if (full >= 16) i = 31 - __clz((int)min(full, 128u) >> 3);  // largest 8*2^i <= full
-                    const uint32_t rows_i = 8u << i;
-                    const uint32_t off = (sr >> 3) * 8 * CF::RB;
-                    tma4d(&s.K[stage][off], mk + i, y, &s.full[stage], pol);
-                    tma4d(&s.V[stage][off], mv + i, y, &s.full[stage], pol);
-                    rem -= rows_i;
-                    full = full > rows_i ? full - rows_i : 0u;
-                    sr += rows_i;
-                    y += (int)rows_i;
+                // one request per piece for K and one for V: a box of r8/8 groups
+                // when the rounded-up rows exist; else the piece's whole groups
+                // plus a bounds-checked 8-row box (zero fill past the end)
+                const CUtensorMap* mk = a.tmaps + (gat ? 2 : 0) * kBoxSizes;
+                const CUtensorMap* mv = mk + kBoxSizes;
+                const uint64_t lim = gat ? a.grows : a.rows;
+                const uint32_t off = (srow >> 3) * 8 * CF::RB;
+                if (row + r8 <= lim) {
+                    tma4d(&s.K[stage][off], mk + (r8 / 8 - 1), (int)row, &s.full[stage], pol);
+                    tma4d(&s.V[stage][off], mv + (r8 / 8 - 1), (int)row, &s.full[stage], pol);
+                } else {
+                    const uint32_t full = len & ~7u;
+                    if (full) {
+                        tma4d(&s.K[stage][off], mk + (full / 8 - 1), (int)row, &s.full[stage], pol);
+                        tma4d(&s.V[stage][off], mv + (full / 8 - 1), (int)row, &s.full[stage], pol);
+                    }
+                    if (r8 > full) {
+                        const uint32_t off2 = ((srow + full) >> 3) * 8 * CF::RB;
+                        tma4d(&s.K[stage][off2], mk, (int)(row + full), &s.full[stage], pol);
+                        tma4d(&s.V[stage][off2], mv, (int)(row + full), &s.full[stage], pol);
+                    }
                 }
             }
             __syncwarp();
@@ -1983,7 +1991,7 @@ void launch_combine(int D, const CombineArgs& ca, uint32_t n_qslots, cudaStream_
 }
 
 template <int D>
-static void launch_decode_t(const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st) {
+static void launch_decode_t(const DecodeArgs& a, int grid, cudaStream_t st) {
     const size_t smem = sizeof(DecodeSmem<D>) + 1024;
     static bool configured = false;
     if (!configured) {
@@ -1993,14 +2001,14 @@ static void launch_decode_t(const DecodeMaps& m, const DecodeArgs& a, int grid, 
                                        (int)cudaSharedmemCarveoutMaxShared));
         configured = true;
     }
-    launch_pdl(true, decode_kernel<D>, dim3(grid), dim3((kComputeWarps + 2) * 32), smem, st, m, a);
+    launch_pdl(true, decode_kernel<D>, dim3(grid), dim3((kComputeWarps + 2) * 32), smem, st, a);
 }
 
-void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st) {
+void launch_decode(int D, const DecodeArgs& a, int grid, cudaStream_t st) {
     switch (D) {
-        case 128: launch_decode_t<128>(m, a, grid, st); break;
-        case 64: launch_decode_t<64>(m, a, grid, st); break;
-        case 32: launch_decode_t<32>(m, a, grid, st); break;
+        case 128: launch_decode_t<128>(a, grid, st); break;
+        case 64: launch_decode_t<64>(a, grid, st); break;
+        case 32: launch_decode_t<32>(a, grid, st); break;
         default: fail(SAAP_ERR_UNSUPPORTED, "decode: unsupported head dim " + std::to_string(D));
     }
 }
@@ -2052,14 +2060,15 @@ void launch_route_cluster(int D, const ClusterRouteArgs& a, uint32_t n_slots, cu
     // dynamic smem: centroid slice [D][C/8] + member queries [8][G][D] (f32)
     cfg.dynamicSmemBytes = ((size_t)D * (a.C / kClusterCtas) + (size_t)kSlotGroups * a.G * D) * 4;
     if (cfg.dynamicSmemBytes > 160 * 1024) fail(SAAP_ERR_UNSUPPORTED, "route: slice too large");
-    auto go = [&](auto kern) {
-        static bool configured = false;  // one per instantiation
-        if (!configured) {
+    static bool configured = false;
+    if (!configured) {
+        for (auto kern : {route_cluster_kernel<128, 128>, route_cluster_kernel<128, 64>,
+                          route_cluster_kernel<128, 32>, route_cluster_kernel<64, 128>,
+                          route_cluster_kernel<64, 64>, route_cluster_kernel<32, 128>})
             SAAP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-            configured = true;
-        }
-        SAAP_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
-    };
+        configured = true;
+    }
+    auto go = [&](void (*kern)(ClusterRouteArgs)) { SAAP_CUDA(cudaLaunchKernelEx(&cfg, kern, a)); };
     const uint32_t S = a.C / kClusterCtas;
     if (D == 128 && S == 128) go(route_cluster_kernel<128, 128>);
     else if (D == 128 && S == 64) go(route_cluster_kernel<128, 64>);
