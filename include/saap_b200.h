@@ -243,6 +243,12 @@ SAAP_API int saap_debug_exp(saap_ctx* ctx, const double* x, uint64_t n, double* 
  * {start, scores exchanged, end} globaltimer ns (3 x 1024 x u64). */
 SAAP_API int saap_debug_plan_trace(saap_ctx* ctx, uint64_t* out);
 
+/* Debug invariant: after a decode step every per-step counter and flag is
+ * back at zero.  out[8]: {tickets, dynamic tiles reserved, planner CTAs,
+ * published, decode CTAs exited, nonzero run counters, nonzero done/dyn
+ * counters, nonzero partial/ready flags}. */
+SAAP_API int saap_debug_step_state(saap_ctx* ctx, uint64_t* out);
+
 /* With SAAP_STEP_TRACE set when the context was created: reset (reset=1) or
  * read (reset=0) the step timeline: first start / last end (globaltimer ns)
  * of {approximate routing, planner, decode, combine} (8 x u64). */

@@ -221,6 +221,14 @@ class Context:
         _check(lib().saap_ctx_timing(self.h, C.byref(a), C.byref(b), C.byref(n)))
         return a.value, b.value, n.value
 
+    def step_state(self):
+        """Debug invariant: per-step counters/flags after a step (all zero when clean)."""
+        out = (C.c_uint64 * 8)()
+        _check(lib().saap_debug_step_state(self.h, out))
+        names = ["tickets", "dyn_reserved", "planner_groups", "published", "exited",
+                 "runs_nonzero", "done_nonzero", "flags_nonzero"]
+        return dict(zip(names, [int(v) for v in out]))
+
     def graph_begin(self):
         _check(lib().saap_graph_begin(self.h))
 

@@ -125,8 +125,6 @@ struct PlanArgs {
 constexpr uint32_t kCntValid = 0x80000000u;
 
 struct DecodeArgs {
-    const CUtensorMap* tmaps;  // DecodeMaps::dev
-    uint64_t rows, grows;      // rows of the cache / gather tensors (box bounds)
     const TileRec* st_tiles;   // static part of the work stream [n_static]
     TileRec* dyn_tiles;        // dynamic part (ready flags cleared after use)
     uint32_t n_static;
@@ -142,6 +140,7 @@ struct DecodeArgs {
     float qscale;  // log2(e)/sqrt(d): scores live in the exp2 domain
     float* part_O;   // [qslots][run_cap][4][D] unnormalised run partials
     float* part_ml;  // [qslots][run_cap][8]: m then l
+    uint32_t* part_flag;  // [qslots][run_cap] run partial published
     uint32_t run_cap;
     uint32_t* runs;  // [qslots] runs reserved
     uint32_t* done;  // [qslots] tiles published
@@ -156,6 +155,7 @@ struct CombineArgs {
     uint32_t* done;
     const float* part_O;
     const float* part_ml;
+    uint32_t* part_flag;
     uint32_t run_cap;
     uint32_t G, n_hchunks;
     float* out;
@@ -170,10 +170,12 @@ struct CombineArgs {
 // piece of any 8-row multiple is one request).  The 64 maps (K, V, gather K,
 // gather V) x 16 heights live in device memory.
 constexpr int kBoxSizes = 16;  // boxes of 8, 16, ..., 128 rows
+// Passed by value as a __grid_constant__ kernel parameter (8 KB): descriptors
+// in parameter space are per launch, never served stale from the TMA
+// descriptor cache (device-memory maps at a reused address would be).
 struct DecodeMaps {
-    CUtensorMap* dev = nullptr;  // [4][kBoxSizes] in device memory (64-B aligned)
+    CUtensorMap map[4 * kBoxSizes];  // [K, V, gather K, gather V][height]
     uint64_t rows = 0, grows = 0;
-    ~DecodeMaps();
 };
 
 struct QModelArgs {

@@ -19,7 +19,7 @@ void launch_route_cluster(int D, const ClusterRouteArgs& a, uint32_t n_slots, cu
 bool route_cluster_supported(int D, uint32_t C);
 void launch_route_approx(int D, const ApproxArgs& a, uint32_t n_slots, cudaStream_t st);
 void launch_route_score(const RouteArgs& a, uint32_t n_groups, cudaStream_t st);
-void launch_decode(int D, const DecodeArgs& a, int grid, cudaStream_t st);
+void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st);
 void launch_combine(int D, const CombineArgs& ca, uint32_t n_qslots, cudaStream_t st);
 void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st);
 void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t n_tiles,
@@ -393,15 +393,12 @@ DecodeMaps* build_maps(const void* K, const void* V, uint64_t rows, uint32_t D, 
     const void* a = gK ? gK : K;
     const void* b = gV ? gV : V;
     const uint64_t r = gK ? grows : rows;
-    std::vector<CUtensorMap> h(4 * kBoxSizes);
     for (int i = 0; i < kBoxSizes; ++i) {
-        h[0 * kBoxSizes + i] = make_group_map(K, rows, D, (uint32_t)i + 1);
-        h[1 * kBoxSizes + i] = make_group_map(V, rows, D, (uint32_t)i + 1);
-        h[2 * kBoxSizes + i] = make_group_map(a, r, D, (uint32_t)i + 1);
-        h[3 * kBoxSizes + i] = make_group_map(b, r, D, (uint32_t)i + 1);
+        m->map[0 * kBoxSizes + i] = make_group_map(K, rows, D, (uint32_t)i + 1);
+        m->map[1 * kBoxSizes + i] = make_group_map(V, rows, D, (uint32_t)i + 1);
+        m->map[2 * kBoxSizes + i] = make_group_map(a, r, D, (uint32_t)i + 1);
+        m->map[3 * kBoxSizes + i] = make_group_map(b, r, D, (uint32_t)i + 1);
     }
-    m->dev = dmalloc<CUtensorMap>(h.size());
-    SAAP_CUDA(cudaMemcpy(m->dev, h.data(), h.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
     m->rows = rows;
     m->grows = r;
     return m;
@@ -520,6 +517,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     float* pO = (float*)ensure(c, c->part_O, qslots * run_cap * kHeadsPerSlot * D * sizeof(float));
     float* pml = (float*)ensure(c, c->part_ml, qslots * run_cap * 8 * sizeof(float));
     uint32_t* runs = (uint32_t*)ensure_zero(c, c->runs, qslots * 4);
+    uint32_t* pflag = (uint32_t*)ensure_zero(c, c->part_flag, qslots * run_cap * 4);
     uint32_t* dcnt = plan ? (uint32_t*)ensure_zero(c, c->dyn_cnt, qslots * 4) : nullptr;
     ensure_done(c, qslots);
     if (plan && !stats) stats = (saap_attn_stats*)ensure(c, c->stats, n_groups * sizeof(saap_attn_stats));
@@ -627,6 +625,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     da.qscale = (float)(1.4426950408889634 / std::sqrt((double)D));
     da.part_O = pO;
     da.part_ml = pml;
+    da.part_flag = pflag;
     da.run_cap = (uint32_t)run_cap;
     da.runs = runs;
     da.done = c->done;
@@ -641,10 +640,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     da.chunk_st = plan ? std::max<uint32_t>(1u, std::min<uint32_t>(chunk, sp->n_tiles / (uint32_t)grid)) : chunk;
     static const bool dtrace_on = std::getenv("SAAP_DECODE_TRACE") != nullptr;
     if (dtrace_on) da.dtrace = (unsigned long long*)ensure(c, c->dtrace, (size_t)c->sm_count * 128);
-    da.tmaps = src.maps->dev;
-    da.rows = src.maps->rows;
-    da.grows = src.maps->grows;
-    launch_decode((int)D, da, grid, st);
+    launch_decode((int)D, *src.maps, da, grid, st);
     CombineArgs ca{};
     ca.st_cnt = sp->cnt;
     ca.dyn_cnt = dcnt;
@@ -652,6 +648,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     ca.done = c->done;
     ca.part_O = pO;
     ca.part_ml = pml;
+    ca.part_flag = pflag;
     ca.run_cap = (uint32_t)run_cap;
     ca.G = (uint32_t)G;
     ca.n_hchunks = (uint32_t)n_hchunks;
@@ -714,9 +711,6 @@ DecodeSrc layer_src(saap_layer* L, uint64_t recent, bool need_gather) {
 }  // namespace
 
 namespace saap_b200 {
-DecodeMaps::~DecodeMaps() {
-    if (dev) cudaFree(dev);
-}
 void set_error(const std::string& m) { g_err = m; }
 [[noreturn]] void fail(int code, const std::string& msg) { throw Failure{code, msg}; }
 void check_cuda(cudaError_t e, const char* what) {
@@ -772,7 +766,7 @@ int saap_ctx_destroy(saap_ctx* c) {
         cudaStreamSynchronize(c->stream);
         for (saap_scratch* s : {&c->approx, &c->trace, &c->dtrace, &c->cand_s, &c->cand_i,
                                 &c->tiles, &c->part_O, &c->part_ml, &c->probs, &c->stats, &c->sel,
-                                &c->qr, &c->qd, &c->out, &c->misc, &c->zeros, &c->runs, &c->dyn_cnt})
+                                &c->qr, &c->qd, &c->out, &c->misc, &c->zeros, &c->runs, &c->dyn_cnt, &c->part_flag})
             if (s->p) cudaFree(s->p);
         dfree(c->counters);
         dfree(c->done);
@@ -1874,6 +1868,42 @@ int saap_debug_plan_trace(saap_ctx* c, uint64_t* out) {
         if (!c->trace.p) invalid("plan tracing off: set SAAP_PLAN_TRACE before the first decode");
         d2h(out, c->trace.p, 128 + 24 * 1024, c->stream);
         sync(c);
+    });
+}
+
+// Between decode steps every per-step counter and flag must be back at zero
+// (the last decode CTA, the combine and the producer re-arm them).  out[8]:
+// {tickets, dyn reserved, planner groups, published, exited, nonzero run
+// counters, nonzero done counters + dyn counts, nonzero part/ready flags}.
+int saap_debug_step_state(saap_ctx* c, uint64_t* out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(out, "out");
+        sync(c);
+        StepCounters h{};
+        SAAP_CUDA(cudaMemcpy(&h, c->counters, sizeof h, cudaMemcpyDeviceToHost));
+        out[0] = h.tickets;
+        out[1] = (uint32_t)h.dynres;
+        out[2] = (uint32_t)(h.dynres >> 32);
+        out[3] = h.published;
+        out[4] = h.exited;
+        auto nonzero = [](const void* d, size_t bytes) {
+            std::vector<uint32_t> v(bytes / 4);
+            if (!v.empty()) SAAP_CUDA(cudaMemcpy(v.data(), d, v.size() * 4, cudaMemcpyDeviceToHost));
+            uint64_t n = 0;
+            for (uint32_t x : v) n += x != 0;
+            return n;
+        };
+        out[5] = c->runs.p ? nonzero(c->runs.p, c->runs.cap) : 0;
+        out[6] = (c->done ? nonzero(c->done, c->done_cap * 4) : 0) +
+                 (c->dyn_cnt.p ? nonzero(c->dyn_cnt.p, c->dyn_cnt.cap) : 0);
+        uint64_t flags = c->part_flag.p ? nonzero(c->part_flag.p, c->part_flag.cap) : 0;
+        if (c->tiles.p) {
+            std::vector<TileRec> t(c->tiles.cap / sizeof(TileRec));
+            SAAP_CUDA(cudaMemcpy(t.data(), c->tiles.p, t.size() * sizeof(TileRec), cudaMemcpyDeviceToHost));
+            for (auto& r : t) flags += r.ready != 0;
+        }
+        out[7] = flags;
     });
 }
 

@@ -192,7 +192,7 @@ struct saap_ctx {
     uint64_t launches = 0;
     // growable device scratch (sized by uncaptured calls; graphs reuse it)
     saap_scratch approx, trace, dtrace, cand_s, cand_i, tiles, part_O, part_ml, probs, stats, sel, qr, qd, out, misc, zeros;
-    saap_scratch runs, dyn_cnt;  // per query slot, zero between steps (the combine re-arms them)
+    saap_scratch runs, dyn_cnt, part_flag;  // zero between steps (the combine re-arms them)
     unsigned long long* tl = nullptr;  // debug step timeline (SAAP_STEP_TRACE)
     saap_b200::StepCounters* counters = nullptr;  // persistent, 128 B
     uint32_t* done = nullptr;                     // per query slot completion counters

@@ -1328,7 +1328,7 @@ __device__ __forceinline__ float bf16_round(float x) {
 
 template <int D>
 __global__ void __maxnreg__(144)
-        decode_kernel(const __grid_constant__ DecodeArgs a) {
+        decode_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ DecodeMaps maps) {
     using CF = DecodeCfg<D>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     auto& s = *reinterpret_cast<DecodeSmem<D>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
@@ -1411,7 +1411,10 @@ __global__ void __maxnreg__(144)
             }
             __threadfence();
             __syncwarp();
-            if (lane == 0) atomicAdd(&a.done[slot], tiles);
+            if (lane == 0) {
+                st_release_u32(a.part_flag + pidx, 1u);  // the combine folds it in now
+                atomicAdd(&a.done[slot], tiles);
+            }
         }
         return;
     }
@@ -1423,7 +1426,7 @@ __global__ void __maxnreg__(144)
         // `tail` tiles of the stream are single-tile chunks so the CTAs finish
         // together.  A feeder keeps up to kRecRing work records in flight
         // (bulk copies into shared memory) ahead of the TMA issue.
-        if (lane < 2 * kBoxSizes) asm volatile("prefetch.tensormap [%0];" ::"l"(a.tmaps + lane) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.map[lane]) : "memory");
         const uint64_t pol = l2_evict_first_policy();
         const uint32_t W = a.n_static, CH = a.chunk, M = a.tail;
         constexpr uint32_t TB = 1;  // tickets per grab (the next grab travels while these feed)
@@ -1545,8 +1548,9 @@ __global__ void __maxnreg__(144)
                         break;
                     }
                     poll_wait = false;
-                    // acquired generic-proxy data is read by the bulk copies (async proxy)
-                    if (b1 > W && lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+                    // acquired generic-proxy data (records, gathered rows) is read by
+                    // every lane's bulk and tensor copies (async proxy)
+                    if (b1 > W) asm volatile("fence.proxy.async.global;" ::: "memory");
                     pc0 = b0;
                     pc1 = b1;
                     pend = true;
@@ -1628,9 +1632,9 @@ __global__ void __maxnreg__(144)
                 // one request per piece for K and one for V: a box of r8/8 groups
                 // when the rounded-up rows exist; else the piece's whole groups
                 // plus a bounds-checked 8-row box (zero fill past the end)
-                const CUtensorMap* mk = a.tmaps + (gat ? 2 : 0) * kBoxSizes;
+                const CUtensorMap* mk = &maps.map[(gat ? 2 : 0) * kBoxSizes];
                 const CUtensorMap* mv = mk + kBoxSizes;
-                const uint64_t lim = gat ? a.grows : a.rows;
+                const uint64_t lim = gat ? maps.grows : maps.rows;
                 const uint32_t off = (srow >> 3) * 8 * CF::RB;
                 if (row + r8 <= lim) {
                     tma4d(&s.K[stage][off], mk + (r8 / 8 - 1), (int)row, &s.full[stage], pol);
@@ -1895,71 +1899,96 @@ __global__ void __maxnreg__(80) combine_kernel(CombineArgs a) {
     constexpr int NOUT = kHeadsPerSlot * D;
     constexpr int PER = 4;  // consecutive outputs per thread (one head)
     constexpr int U = 8;  // runs in flight
-    __shared__ uint32_t s_total, s_runs;
     const uint32_t qsi = blockIdx.x;
-    if (threadIdx.x == 0) {
-        tl_mark(a.tl, 3, true);
-        uint32_t total = a.st_cnt[qsi];
-        if (a.dyn_cnt) {
-            uint32_t v;
-            while (!((v = ld_acquire_u32(a.dyn_cnt + qsi)) & kCntValid)) __nanosleep(256);
-            total += v & ~kCntValid;
-            a.dyn_cnt[qsi] = 0;
-        }
-        if (total)
-            while (ld_acquire_u32(a.done + qsi) < total) __nanosleep(256);
-        s_total = total;
-        s_runs = ld_acquire_u32(a.runs + qsi);
-        a.done[qsi] = 0;  // re-armed for the next step (this CTA is the only reader)
-        a.runs[qsi] = 0;
-    }
-    __syncthreads();
+    __shared__ uint32_t s_nr, s_fin;
     const uint32_t e0 = threadIdx.x * PER, h = e0 / D;
     const uint32_t g = qsi / a.n_hchunks, hc = qsi % a.n_hchunks;
     const uint32_t head = hc * kHeadsPerSlot + h;
     float* out = a.out + ((size_t)g * a.G + head) * D + (e0 % D);
-    const uint32_t nr = s_runs;
-    if (s_total == 0 || nr == 0) {
-        if (head < a.G)
-#pragma unroll
-            for (int i = 0; i < PER; ++i) out[i] = 0.f;
-        return;
-    }
-    // one pass, U runs per round with all their loads in flight, online
-    // rescaling to the running max (Alg. 2)
     const size_t base = (size_t)qsi * a.run_cap;
+    if (threadIdx.x == 0) tl_mark(a.tl, 3, true);
+    // Streaming fold: run partials are merged as the decode publishes them
+    // (per-run release flags), so only the last ones trail the decode.
     float M = -INFINITY, O[PER], L = 0.f;
 #pragma unroll
     for (int i = 0; i < PER; ++i) O[i] = 0.f;
-    for (uint32_t i0 = 0; i0 < nr; i0 += U) {
-        float4 v[U];
-        float mu[U], lu[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const bool ok = i0 + u < nr;
-            v[u] = ok ? __ldcg(reinterpret_cast<const float4*>(a.part_O + (base + i0 + u) * NOUT + e0))
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
-            mu[u] = ok ? __ldcg(a.part_ml + (base + i0 + u) * 8 + h) : -INFINITY;
-            lu[u] = ok ? __ldcg(a.part_ml + (base + i0 + u) * 8 + 4 + h) : 0.f;
+    uint32_t total = 0, have_total = 0, folded = 0;
+    __shared__ uint32_t s_res, s_first, s_dn;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            if (!have_total) {
+                total = a.st_cnt[qsi];
+                if (a.dyn_cnt) {
+                    const uint32_t v = ld_acquire_u32(a.dyn_cnt + qsi);
+                    if (v & kCntValid) {
+                        total += v & ~kCntValid;
+                        have_total = 1;
+                    }
+                } else {
+                    have_total = 1;
+                }
+            }
+            // done before runs: once every tile is counted, every run is
+            // reserved (each run is reserved, flagged, then counted)
+            s_dn = have_total && ld_acquire_u32(a.done + qsi) >= total;
+            s_res = ld_acquire_u32(a.runs + qsi);
+            s_first = 0xFFFFFFFFu;
         }
-        float Mn = M;
-#pragma unroll
-        for (int u = 0; u < U; ++u) Mn = fmaxf(Mn, mu[u]);
-        if (Mn == -INFINITY) continue;
-        const float sc = fast_exp2(M - Mn);  // M = -inf -> 0
-#pragma unroll
-        for (int i = 0; i < PER; ++i) O[i] *= sc;
-        L *= sc;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const float wgt = fast_exp2(mu[u] - Mn);  // empty run -> 0
-            O[0] = fmaf(v[u].x, wgt, O[0]);
-            O[1] = fmaf(v[u].y, wgt, O[1]);
-            O[2] = fmaf(v[u].z, wgt, O[2]);
-            O[3] = fmaf(v[u].w, wgt, O[3]);
-            L = fmaf(lu[u], wgt, L);
+        __syncthreads();
+        // the published prefix of the reserved runs: every thread checks one flag
+        const uint32_t res = s_res;
+        for (uint32_t r = folded + threadIdx.x; r < res; r += blockDim.x)
+            if (!ld_acquire_u32(a.part_flag + base + r)) atomicMin(&s_first, r);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t nr = min(res, s_first);
+            s_nr = nr;
+            s_fin = s_dn && nr == res;
         }
-        M = Mn;
+        __syncthreads();
+        const uint32_t nr = s_nr, fin = s_fin;
+        __syncthreads();
+        for (uint32_t i0 = folded; i0 < nr; i0 += U) {
+            float4 v[U];
+            float mu[U], lu[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool ok = i0 + u < nr;
+                v[u] = ok ? __ldcg(reinterpret_cast<const float4*>(a.part_O + (base + i0 + u) * NOUT + e0))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+                mu[u] = ok ? __ldcg(a.part_ml + (base + i0 + u) * 8 + h) : -INFINITY;
+                lu[u] = ok ? __ldcg(a.part_ml + (base + i0 + u) * 8 + 4 + h) : 0.f;
+            }
+            float Mn = M;
+#pragma unroll
+            for (int u = 0; u < U; ++u) Mn = fmaxf(Mn, mu[u]);
+            if (Mn == -INFINITY) continue;
+            const float sc = fast_exp2(M - Mn);  // M = -inf -> 0
+#pragma unroll
+            for (int i = 0; i < PER; ++i) O[i] *= sc;
+            L *= sc;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const float wgt = fast_exp2(mu[u] - Mn);  // empty run -> 0
+                O[0] = fmaf(v[u].x, wgt, O[0]);
+                O[1] = fmaf(v[u].y, wgt, O[1]);
+                O[2] = fmaf(v[u].z, wgt, O[2]);
+                O[3] = fmaf(v[u].w, wgt, O[3]);
+                L = fmaf(lu[u], wgt, L);
+            }
+            M = Mn;
+        }
+        const bool progress = nr > folded;
+        folded = nr;
+        if (fin) break;
+        if (threadIdx.x == 0 && !progress) __nanosleep(1000);  // light polling next to the decode
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // re-arm the slot for the next step (this CTA is the only reader)
+        for (uint32_t r = 0; r < folded; ++r) a.part_flag[base + r] = 0;
+        if (a.dyn_cnt) a.dyn_cnt[qsi] = 0;
+        a.done[qsi] = 0;
+        a.runs[qsi] = 0;
     }
     if (head < a.G)
 #pragma unroll
@@ -1991,7 +2020,7 @@ void launch_combine(int D, const CombineArgs& ca, uint32_t n_qslots, cudaStream_
 }
 
 template <int D>
-static void launch_decode_t(const DecodeArgs& a, int grid, cudaStream_t st) {
+static void launch_decode_t(const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st) {
     const size_t smem = sizeof(DecodeSmem<D>) + 1024;
     static bool configured = false;
     if (!configured) {
@@ -2001,14 +2030,14 @@ static void launch_decode_t(const DecodeArgs& a, int grid, cudaStream_t st) {
                                        (int)cudaSharedmemCarveoutMaxShared));
         configured = true;
     }
-    launch_pdl(true, decode_kernel<D>, dim3(grid), dim3((kComputeWarps + 2) * 32), smem, st, a);
+    launch_pdl(true, decode_kernel<D>, dim3(grid), dim3((kComputeWarps + 2) * 32), smem, st, a, m);
 }
 
-void launch_decode(int D, const DecodeArgs& a, int grid, cudaStream_t st) {
+void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st) {
     switch (D) {
-        case 128: launch_decode_t<128>(a, grid, st); break;
-        case 64: launch_decode_t<64>(a, grid, st); break;
-        case 32: launch_decode_t<32>(a, grid, st); break;
+        case 128: launch_decode_t<128>(m, a, grid, st); break;
+        case 64: launch_decode_t<64>(m, a, grid, st); break;
+        case 32: launch_decode_t<32>(m, a, grid, st); break;
         default: fail(SAAP_ERR_UNSUPPORTED, "decode: unsupported head dim " + std::to_string(D));
     }
 }

@@ -31,3 +31,17 @@ def ctx():
 def port():
     import oracle
     return oracle.port()
+
+
+@pytest.fixture(autouse=True)
+def _step_state_clean(request):
+    """After every GPU test the default context's per-step counters and flags
+    must be re-armed (zero): a leak would corrupt the next decode step."""
+    yield
+    if request.node.get_closest_marker("gpu") is None or not _has_gpu():
+        return
+    import paper_2502_08246_b200 as sb
+    if sb._default_ctx is None:
+        return
+    st = sb._default_ctx.step_state()
+    assert not any(st.values()), f"step state leaked: {st}"
