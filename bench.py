@@ -348,10 +348,13 @@ def ours(a):
             dense_step(li)
     ctx.synchronize()
     graphs, dgraphs = [], []
+    kernels_per_step = None
     for li in range(a.layers):
+        n0 = ctx.launch_count
         ctx.graph_begin()
         sparse_step(li)
         graphs.append(ctx.graph_end())
+        kernels_per_step = ctx.launch_count - n0  # our kernels captured in one step's graph
         if not a.no_dense:
             ctx.graph_begin()
             dense_step(li)
@@ -544,7 +547,8 @@ def ours(a):
                 "h2d_bytes_per_step": int(q.numel() * 4),
                 "d2h_bytes_per_step": int(out.numel() * 4 + n_groups * 24)},
         "clocks": clk,
-        "gpu_launches": 2 * a.steps,
+        "gpu_launches": int(kernels_per_step * a.steps),
+        "kernels_per_step": int(kernels_per_step),
         "prefill_build_ms_per_layer": round(float(np.mean(t_build)), 2),
         "plan_trace_cycles": plan_trace,
         "decode_trace": decode_trace,
