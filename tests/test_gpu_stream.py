@@ -131,7 +131,7 @@ def test_repeated_steps_are_consistent(ctx, port):
     ref = L.sparse_attention(routers, qr, qd, cfg)
     for _ in range(10):
         out, stats, _ = L.sparse_attention(routers, qr, qd, cfg)
-        assert max_rel_diff(out, ref[0]) <= 1e-5
+        assert max_rel_diff(out, ref[0]) <= 1e-4
         assert [s.keys_scored for s in stats] == [s.keys_scored for s in ref[1]]
 
 
