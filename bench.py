@@ -416,26 +416,40 @@ def ours(a):
     plan_trace = None
     if os.environ.get("SAAP_PLAN_TRACE"):
         import ctypes as ct
-        buf = (ct.c_uint64 * (16 + 3 * 1024))()
+        buf = (ct.c_uint64 * (16 + 6 * 1024))()
         if sb.lib().saap_debug_plan_trace(ctx.h, buf) == 0:
             plan_trace = list(buf)[:16]
-            cta = np.array(list(buf)[16:], dtype=np.float64).reshape(1024, 3)
+            cta = np.array(list(buf)[16:], dtype=np.float64).reshape(1024, 6)[:, :3]
             cta = cta[cta[:, 0] > 0]
             if len(cta):
                 t0 = cta[:, 0].min()
                 plan_trace.append({k: [round(float(v), 2) for v in np.percentile((cta[:, i] - t0) / 1e3, [0, 50, 100])]
                                    for i, k in enumerate(["start_us", "exchanged_us", "end_us"])})
     step_trace = None
+    graph_plan_trace = None
     if os.environ.get("SAAP_STEP_TRACE"):
         import ctypes as ct
-        buf = (ct.c_uint64 * 8)()
+        buf = (ct.c_uint64 * 16)()
         sb._check(sb.lib().saap_debug_step_trace(ctx.h, buf, 1))
         graphs[0].launch()
         ctx.synchronize()
         sb._check(sb.lib().saap_debug_step_trace(ctx.h, buf, 0))
+        if os.environ.get("SAAP_PLAN_TRACE"):  # routing phases of this (overlapped) step
+            pbuf = (ct.c_uint64 * (16 + 6 * 1024))()
+            if sb.lib().saap_debug_plan_trace(ctx.h, pbuf) == 0:
+                cta = np.array(list(pbuf)[16:], dtype=np.float64).reshape(1024, 6)
+                cta = cta[cta[:, 0] > 0]
+                tt0 = cta[:, 0].min() if len(cta) else 0
+                own = cta[cta[:, 3] > 0]
+                slow = own[np.argsort(own[:, 3])[-4:]] if len(own) else own
+                graph_plan_trace = [list(pbuf)[:8]] + [
+                    {k: [round(float(x), 2) for x in np.percentile((own[:, i] - tt0) / 1e3, [0, 50, 100])]
+                     for i, k in enumerate(["start_us", "exchanged_us", "selected_us", "end_us"])},
+                    {"slowest_owner_ctas_us_and_candidates": [[round(float((r[i] - tt0) / 1e3), 2) for i in range(4)] + [int(r[4])]
+                                                              for r in slow]}] if len(own) else None
         v = list(buf)
         t0 = min(x for x in v[0::2] if x)
-        names = ["approx", "plan", "decode", "combine"]
+        names = ["approx", "plan", "decode", "combine", "run_published", "slot_complete"]
         step_trace = {n: [round((v[2 * k] - t0) / 1e3, 2) if v[2 * k] != 2**64 - 1 else None,
                           round((v[2 * k + 1] - t0) / 1e3, 2) if v[2 * k + 1] else None]
                       for k, n in enumerate(names)}
@@ -553,6 +567,7 @@ def ours(a):
         "plan_trace_cycles": plan_trace,
         "decode_trace": decode_trace,
         "step_trace_us": step_trace,
+        "graph_plan_trace": graph_plan_trace,
         "prefill": {
             "keys": n_keys_prefill, "assign_ms": round(assign_ms, 3), "pack_ms": round(pack_ms, 3),
             "keys_per_s": round(n_keys_prefill / ((assign_ms + pack_ms) * 1e-3), 1),

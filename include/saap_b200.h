@@ -239,8 +239,9 @@ SAAP_API int saap_ctx_launch_count(saap_ctx* ctx, uint64_t* out);
 SAAP_API int saap_debug_exp(saap_ctx* ctx, const double* x, uint64_t n, double* out);
 
 /* With SAAP_PLAN_TRACE set: clock64 offsets of the planner's phases for
- * context 0 of the last routed decode step (16 x u64), then per routing CTA
- * {start, scores exchanged, end} globaltimer ns (3 x 1024 x u64). */
+ * context 0 of the last routed decode step (16 x u64), then per fused routing
+ * CTA {start, scores exchanged, selected, end (globaltimer ns), candidates,
+ * 0} (6 x 1024 x u64). */
 SAAP_API int saap_debug_plan_trace(saap_ctx* ctx, uint64_t* out);
 
 /* Debug invariant: after a decode step every per-step counter and flag is
@@ -251,7 +252,8 @@ SAAP_API int saap_debug_step_state(saap_ctx* ctx, uint64_t* out);
 
 /* With SAAP_STEP_TRACE set when the context was created: reset (reset=1) or
  * read (reset=0) the step timeline: first start / last end (globaltimer ns)
- * of {approximate routing, planner, decode, combine} (8 x u64). */
+ * of {approximate routing, planner, decode, combine, last run published,
+ * last slot complete, -, -} (16 x u64). */
 SAAP_API int saap_debug_step_trace(saap_ctx* ctx, uint64_t* out, int reset);
 
 /* With SAAP_DECODE_TRACE set: per attention CTA of the last decode step

@@ -158,6 +158,7 @@ struct CombineArgs {
     uint32_t* part_flag;
     uint32_t run_cap;
     uint32_t G, n_hchunks;
+    uint32_t poll_ns;        // sleep between polls without progress
     float* out;
     unsigned long long* tl;  // debug step timeline (null: off)
 };

@@ -597,7 +597,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
             ra.stats = stats;
             ra.selected = selected;
             ra.tl = c->tl;
-            if (trace_on) ra.trace = (unsigned long long*)ensure(c, c->trace, 128 + 24 * 1024);
+            if (trace_on) ra.trace = (unsigned long long*)ensure(c, c->trace, 128 + 48 * 1024);
             launch_route_cluster((int)D, ra, n_slots, st);
             c->launches++;
         } else {
@@ -605,7 +605,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
                 enqueue_route_score(c, n_groups, D, C, G, probes, mode, centT, q_route, probs, pa, cmax,
                                     centR, slots, n_slots);
             pa.tl = c->tl;
-            if (trace_on) pa.trace = (unsigned long long*)ensure(c, c->trace, 128 + 24 * 1024);
+            if (trace_on) pa.trace = (unsigned long long*)ensure(c, c->trace, 128 + 48 * 1024);
             launch_route_plan(pa, (uint32_t)n_groups, routed, st);
             c->launches++;
         }
@@ -654,6 +654,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     ca.n_hchunks = (uint32_t)n_hchunks;
     ca.out = out;
     ca.tl = c->tl;
+    ca.poll_ns = std::getenv("SAAP_POLL_NS") ? (uint32_t)std::atoi(std::getenv("SAAP_POLL_NS")) : 1000u;
     launch_combine((int)D, ca, (uint32_t)qslots, st);
     c->launches += 2;
     if (e2) {
@@ -750,8 +751,8 @@ int saap_ctx_create(int device, saap_ctx** out) {
         c->own_stream = true;
         c->counters = dmalloc<StepCounters>(1);
         if (std::getenv("SAAP_STEP_TRACE")) {
-            c->tl = dmalloc<unsigned long long>(8);
-            SAAP_CUDA(cudaMemset(c->tl, 0, 64));
+            c->tl = dmalloc<unsigned long long>(16);
+            SAAP_CUDA(cudaMemset(c->tl, 0, 128));
         }
         SAAP_CUDA(cudaMemset(c->counters, 0, sizeof(StepCounters)));
         ensure_done(c, 4096);
@@ -1866,7 +1867,7 @@ int saap_debug_plan_trace(saap_ctx* c, uint64_t* out) {
     return guard([&] {
         DeviceGuard dg(c);
         if (!c->trace.p) invalid("plan tracing off: set SAAP_PLAN_TRACE before the first decode");
-        d2h(out, c->trace.p, 128 + 24 * 1024, c->stream);
+        d2h(out, c->trace.p, 128 + 48 * 1024, c->stream);
         sync(c);
     });
 }
@@ -1912,14 +1913,14 @@ int saap_debug_step_trace(saap_ctx* c, uint64_t* out, int reset) {
         DeviceGuard dg(c);
         if (!c->tl) invalid("step tracing off: set SAAP_STEP_TRACE before creating the context");
         if (reset) {
-            uint64_t init[8];
-            for (int k = 0; k < 4; ++k) {
+            uint64_t init[16];
+            for (int k = 0; k < 8; ++k) {
                 init[2 * k] = ~0ull;
                 init[2 * k + 1] = 0;
             }
-            h2d(c->tl, init, 64, c->stream);
+            h2d(c->tl, init, 128, c->stream);
         } else {
-            d2h(out, c->tl, 64, c->stream);
+            d2h(out, c->tl, 128, c->stream);
         }
         sync(c);
     });

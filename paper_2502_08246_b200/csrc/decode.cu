@@ -885,7 +885,7 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
         return t;
     };
-    if (a.trace && tid == 0) a.trace[16 + 3 * blockIdx.x] = gt();
+    if (a.trace && tid == 0) a.trace[16 + 6 * blockIdx.x] = gt();
     unsigned long long t0 = 0;
     const bool tr = a.trace && slot == 0 && rank == 0 && tid == 0;
     if (tr) t0 = clock64();
@@ -972,7 +972,7 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     trace(7);
     cluster_sync_all();  // every owner now holds all C scores of its context
     trace(1);
-    if (a.trace && tid == 0) a.trace[16 + 3 * blockIdx.x + 1] = gt();
+    if (a.trace && tid == 0) a.trace[16 + 6 * blockIdx.x + 1] = gt();
     if (!own) {
         if (tid == 0) tl_mark(a.tl, 1, false);
         return;
@@ -1044,9 +1044,12 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
         const float t_l = __uint_as_float((tk & 0x80000000u) ? (tk & 0x7FFFFFFFu) : ~tk);
         double n2 = 0.0;
         for (uint32_t w = 0; w < NT / 32; ++w) n2 += s_n2[w];
-        // |approx - exact| <= B = 2^-16 |pooled|_2 max|c|_2 (pooled rounded to
-        // f32: 2^-24 rel; fp32 accumulation of D products: D 2^-24 rel)
-        const float B2 = (float)(2.0 * 0x1p-16 * sqrt(n2) * (double)a.cmax[g]) * 1.0001f;
+        // |approx - exact| <= B: pooled rounded to f32 (<= u sum|p_j c_j|) plus
+        // fp32 accumulation over a path of DPT chained FMAs and TPC partial
+        // sums (<= gamma_{DPT+TPC} sum|p_j c_j|), sum|p_j c_j| <= |p|_2 max|c|_2,
+        // u = 2^-24; doubled, then widened 1.5x for the f32 threshold arithmetic
+        const float B2 = (float)(2.0 * 1.5 * (double)(DPT + TPC + 1) * 0x1p-24 * sqrt(n2) *
+                                 (double)a.cmax[g]);
         if (tid == 0) s_ncand = 0;
         __syncthreads();
 #pragma unroll
@@ -1071,11 +1074,12 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
             // exact fp64 chains (attention.cpp:296-304: mul rounded before add)
             // over the candidates' centroid rows, staged (coalesced) into the
             // now free slice buffer
+            // (from the transposed centroids: the cluster just streamed them, so
+            // these reads hit L2 instead of queueing behind the decode in HBM)
             float* crow = slab;  // [nS][D + 1]
-            const float* cR = a.centR[g];
             for (uint32_t e = tid; e < nS * D; e += NT) {
-                const uint32_t r = e / D, j = e % D;
-                crow[r * (D + 1) + j] = cR[(size_t)cand_id[r] * D + j];
+                const uint32_t r = e % nS, j = e / nS;
+                crow[r * (D + 1) + j] = sl.centT[(size_t)j * C + cand_id[r]];
             }
             __syncthreads();
             double ex = -INFINITY;
@@ -1118,6 +1122,10 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
         if (a.selected)
             for (uint32_t b = tid; b < L; b += NT) a.selected[(size_t)g * a.probes + b] = sel[b];
         trace(4);
+        if (a.trace && tid == 0) {
+            a.trace[16 + 6 * blockIdx.x + 2] = gt();
+            a.trace[16 + 6 * blockIdx.x + 4] = nS;
+        }
     }
     // ---- plan (one warp): bucket segments -> 8-aligned virtual rows -> tiles
     if (tid >= 32) return;
@@ -1211,7 +1219,7 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
         if (!ntiles) __threadfence();
         atomicAdd(&a.ctr->published, 1u);
         tl_mark(a.tl, 1, false);
-        if (a.trace) a.trace[16 + 3 * blockIdx.x + 2] = gt();
+        if (a.trace) a.trace[16 + 6 * blockIdx.x + 3] = gt();
     }
     trace(5);
 }
@@ -1414,6 +1422,7 @@ __global__ void __maxnreg__(144)
             if (lane == 0) {
                 st_release_u32(a.part_flag + pidx, 1u);  // the combine folds it in now
                 atomicAdd(&a.done[slot], tiles);
+                tl_mark(a.tl, 4, false);  // last run published
             }
         }
         return;
@@ -1980,8 +1989,11 @@ __global__ void __maxnreg__(80) combine_kernel(CombineArgs a) {
         }
         const bool progress = nr > folded;
         folded = nr;
-        if (fin) break;
-        if (threadIdx.x == 0 && !progress) __nanosleep(1000);  // light polling next to the decode
+        if (fin) {
+            if (threadIdx.x == 0) tl_mark(a.tl, 5, false);  // slot complete
+            break;
+        }
+        if (threadIdx.x == 0 && !progress) __nanosleep(a.poll_ns);  // light polling next to the decode
     }
     __syncthreads();
     if (threadIdx.x == 0) {  // re-arm the slot for the next step (this CTA is the only reader)
