@@ -1262,7 +1262,7 @@ struct DecodeSmem {
     uint4 valid[CF::NS];  // 128-bit row validity mask
     uint64_t st_full;     // the 8 consumer warps deposited a run's (m, l, O) states
     uint64_t st_empty;    // the merge warp has read them
-    uint32_t st_slot, st_tiles;
+    uint32_t st_slot, st_tiles, st_run;
     // producer's work-record ring: records of upcoming tiles, bulk-copied ahead
     alignas(16) TileRec rec[kRecRing];
     uint64_t rec_bar[kRecRing];
@@ -1382,10 +1382,8 @@ __global__ void __maxnreg__(144)
         for (;;) {
             mbar_wait(&s.st_full, ph);
             ph ^= 1;
-            const uint32_t slot = s.st_slot, tiles = s.st_tiles;
+            const uint32_t slot = s.st_slot, tiles = s.st_tiles, run = s.st_run;
             if (slot == 0xFFFFFFFFu) break;
-            uint32_t run = 0;  // the run's partial slot (off the consumers' path)
-            if (lane == 0) run = atomicAdd(&a.runs[slot], 1u);
             // lane = (warp w, head h): per-head max and scale of every warp state
             const int w = lane >> 2, h = lane & 3;
             const float mw = s.redm[w][h];
@@ -1408,7 +1406,6 @@ __global__ void __maxnreg__(144)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.st_empty);  // state buffer free
-            run = __shfl_sync(0xFFFFFFFFu, run, 0);
             const size_t pidx = (size_t)slot * a.run_cap + run;
             float* pO = a.part_O + pidx * NOUT;
 #pragma unroll
@@ -1417,7 +1414,8 @@ __global__ void __maxnreg__(144)
                 a.part_ml[pidx * 8 + lane] = M;  // lanes 0-3: w = 0, h = lane
                 a.part_ml[pidx * 8 + 4 + lane] = Lp;
             }
-            __threadfence();
+            // the release store by lane 0 is cumulative over the partial (the
+            // warp barrier orders the other lanes' writes before it)
             __syncwarp();
             if (lane == 0) {
                 st_release_u32(a.part_flag + pidx, 1u);  // the combine folds it in now
@@ -1707,7 +1705,7 @@ __global__ void __maxnreg__(144)
     uint32_t qa[CF::KSTEPS][4];  // A fragments of [q1; q2; q3; 0]
     float o[CF::NT][4];
     float m_run = -INFINITY, l_run = 0.f;
-    uint32_t st_ph = 0;
+    uint32_t st_ph = 0, run_idx = 0;
 
     uint32_t stage = 0, phase = 0;
     uint32_t n_tiles_done = 0;
@@ -1740,6 +1738,8 @@ __global__ void __maxnreg__(144)
             break;
         }
         const uint32_t flags = (uint32_t)mt.y;
+        if ((flags & 1u) && threadIdx.x == 0)  // the run's partial slot, reserved early
+            run_idx = atomicAdd(&a.runs[(uint32_t)mt.x], 1u);
         if (flags & 1u) {
             // A operand [q1; q2; q3; 0]: 3-term bf16 split of the f32 queries
             // (~fp32-exact).  Rows g (lanes < 16: q1, else q2) and g + 8 (q3 / 0).
@@ -1881,6 +1881,7 @@ __global__ void __maxnreg__(144)
             if (threadIdx.x == 0) {
                 s.st_slot = slot;
                 s.st_tiles = (uint32_t)mt.w;
+                s.st_run = run_idx;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.st_full);
