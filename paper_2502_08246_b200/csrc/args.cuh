@@ -142,8 +142,7 @@ struct DecodeArgs {
     float* part_ml;  // [qslots][run_cap][8]: m then l
     uint32_t* part_flag;  // [qslots][run_cap] run partial published
     uint32_t run_cap;
-    uint32_t* runs;  // [qslots] runs reserved
-    uint32_t* done;  // [qslots] tiles published
+    unsigned long long* rd;  // [qslots] (runs reserved << 32) | tiles published
     unsigned long long* dtrace;  // debug: per CTA {start, first tile, end (globaltimer ns), tiles}
     unsigned long long* tl;      // debug step timeline (null: off)
 };
@@ -151,8 +150,7 @@ struct DecodeArgs {
 struct CombineArgs {
     const uint32_t* st_cnt;  // [qslots] static tiles
     uint32_t* dyn_cnt;       // [qslots] dynamic tiles | kCntValid (null: static only)
-    uint32_t* runs;
-    uint32_t* done;
+    unsigned long long* rd;  // [qslots] (runs reserved << 32) | tiles published
     const float* part_O;
     const float* part_ml;
     uint32_t* part_flag;

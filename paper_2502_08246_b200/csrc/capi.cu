@@ -138,18 +138,6 @@ void* ensure(saap_ctx* c, saap_scratch& s, size_t bytes) {
     return s.p;
 }
 
-void ensure_done(saap_ctx* c, size_t n) {
-    if (n <= c->done_cap) return;
-    if (c->capturing) invalid("scratch grows during graph capture: run the call once uncaptured first");
-    if (c->done) {
-        SAAP_CUDA(cudaStreamSynchronize(c->stream));
-        cudaFree(c->done);
-    }
-    const size_t cap = std::max<size_t>(n, 1024) * 2;
-    SAAP_CUDA(cudaMalloc(&c->done, cap * 4));
-    SAAP_CUDA(cudaMemset(c->done, 0, cap * 4));
-    c->done_cap = cap;
-}
 
 // scratch whose contents must start at zero (per-slot step counters)
 void* ensure_zero(saap_ctx* c, saap_scratch& s, size_t bytes) {
@@ -516,10 +504,9 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
                         : nullptr;
     float* pO = (float*)ensure(c, c->part_O, qslots * run_cap * kHeadsPerSlot * D * sizeof(float));
     float* pml = (float*)ensure(c, c->part_ml, qslots * run_cap * 8 * sizeof(float));
-    uint32_t* runs = (uint32_t*)ensure_zero(c, c->runs, qslots * 4);
+    unsigned long long* rd = (unsigned long long*)ensure_zero(c, c->runs, qslots * 8);
     uint32_t* pflag = (uint32_t*)ensure_zero(c, c->part_flag, qslots * run_cap * 4);
     uint32_t* dcnt = plan ? (uint32_t*)ensure_zero(c, c->dyn_cnt, qslots * 4) : nullptr;
-    ensure_done(c, qslots);
     if (plan && !stats) stats = (saap_attn_stats*)ensure(c, c->stats, n_groups * sizeof(saap_attn_stats));
     double* probs = nullptr;
     if (mode == 2) probs = (double*)ensure(c, c->probs, n_groups * G * C * sizeof(double));
@@ -627,8 +614,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     da.part_ml = pml;
     da.part_flag = pflag;
     da.run_cap = (uint32_t)run_cap;
-    da.runs = runs;
-    da.done = c->done;
+    da.rd = rd;
     const uint64_t max_stream = sp->n_tiles + n_groups * dyn_per_group * n_hchunks;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->sm_count,
                                                                     (max_stream + chunk - 1) / chunk));
@@ -644,8 +630,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     CombineArgs ca{};
     ca.st_cnt = sp->cnt;
     ca.dyn_cnt = dcnt;
-    ca.runs = runs;
-    ca.done = c->done;
+    ca.rd = rd;
     ca.part_O = pO;
     ca.part_ml = pml;
     ca.part_flag = pflag;
@@ -755,7 +740,6 @@ int saap_ctx_create(int device, saap_ctx** out) {
             SAAP_CUDA(cudaMemset(c->tl, 0, 128));
         }
         SAAP_CUDA(cudaMemset(c->counters, 0, sizeof(StepCounters)));
-        ensure_done(c, 4096);
         *out = c;
     });
 }
@@ -770,7 +754,6 @@ int saap_ctx_destroy(saap_ctx* c) {
                                 &c->qr, &c->qd, &c->out, &c->misc, &c->zeros, &c->runs, &c->dyn_cnt, &c->part_flag})
             if (s->p) cudaFree(s->p);
         dfree(c->counters);
-        dfree(c->done);
         dfree(c->tl);
         if (c->own_stream) cudaStreamDestroy(c->stream);
         delete c;
@@ -1896,8 +1879,7 @@ int saap_debug_step_state(saap_ctx* c, uint64_t* out) {
             return n;
         };
         out[5] = c->runs.p ? nonzero(c->runs.p, c->runs.cap) : 0;
-        out[6] = (c->done ? nonzero(c->done, c->done_cap * 4) : 0) +
-                 (c->dyn_cnt.p ? nonzero(c->dyn_cnt.p, c->dyn_cnt.cap) : 0);
+        out[6] = c->dyn_cnt.p ? nonzero(c->dyn_cnt.p, c->dyn_cnt.cap) : 0;
         uint64_t flags = c->part_flag.p ? nonzero(c->part_flag.p, c->part_flag.cap) : 0;
         if (c->tiles.p) {
             std::vector<TileRec> t(c->tiles.cap / sizeof(TileRec));

@@ -195,8 +195,6 @@ struct saap_ctx {
     saap_scratch runs, dyn_cnt, part_flag;  // zero between steps (the combine re-arms them)
     unsigned long long* tl = nullptr;  // debug step timeline (SAAP_STEP_TRACE)
     saap_b200::StepCounters* counters = nullptr;  // persistent, 128 B
-    uint32_t* done = nullptr;                     // per query slot completion counters
-    size_t done_cap = 0;
     // capture state
     bool capturing = false;
     int assign_mode = 0;  // 0: tcgen05 path where applicable, 1: exact CUDA-core only

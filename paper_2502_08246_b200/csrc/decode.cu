@@ -1419,7 +1419,7 @@ __global__ void __maxnreg__(144)
             __syncwarp();
             if (lane == 0) {
                 st_release_u32(a.part_flag + pidx, 1u);  // the combine folds it in now
-                atomicAdd(&a.done[slot], tiles);
+                atomicAdd(&a.rd[slot], (unsigned long long)tiles);  // tiles published (low word)
                 tl_mark(a.tl, 4, false);  // last run published
             }
         }
@@ -1739,7 +1739,7 @@ __global__ void __maxnreg__(144)
         }
         const uint32_t flags = (uint32_t)mt.y;
         if ((flags & 1u) && threadIdx.x == 0)  // the run's partial slot, reserved early
-            run_idx = atomicAdd(&a.runs[(uint32_t)mt.x], 1u);
+            run_idx = (uint32_t)(atomicAdd(&a.rd[(uint32_t)mt.x], 1ull << 32) >> 32);
         if (flags & 1u) {
             // A operand [q1; q2; q3; 0]: 3-term bf16 split of the f32 queries
             // (~fp32-exact).  Rows g (lanes < 16: q1, else q2) and g + 8 (q3 / 0).
@@ -1938,10 +1938,11 @@ __global__ void __maxnreg__(80) combine_kernel(CombineArgs a) {
                     have_total = 1;
                 }
             }
-            // done before runs: once every tile is counted, every run is
-            // reserved (each run is reserved, flagged, then counted)
-            s_dn = have_total && ld_acquire_u32(a.done + qsi) >= total;
-            s_res = ld_acquire_u32(a.runs + qsi);
+            // one load: (runs reserved << 32) | tiles published; once every
+            // tile is counted, every run is reserved (reserved, flagged, counted)
+            const unsigned long long v = ld_acquire_u64(a.rd + qsi);
+            s_dn = have_total && (uint32_t)v >= total;
+            s_res = (uint32_t)(v >> 32);
             s_first = 0xFFFFFFFFu;
         }
         __syncthreads();
@@ -1994,14 +1995,13 @@ __global__ void __maxnreg__(80) combine_kernel(CombineArgs a) {
             if (threadIdx.x == 0) tl_mark(a.tl, 5, false);  // slot complete
             break;
         }
-        if (threadIdx.x == 0 && !progress) __nanosleep(a.poll_ns);  // light polling next to the decode
+        if (threadIdx.x == 0 && !progress) __nanosleep(s_dn ? 32u : a.poll_ns);  // light polling next to the decode
     }
     __syncthreads();
     if (threadIdx.x == 0) {  // re-arm the slot for the next step (this CTA is the only reader)
         for (uint32_t r = 0; r < folded; ++r) a.part_flag[base + r] = 0;
         if (a.dyn_cnt) a.dyn_cnt[qsi] = 0;
-        a.done[qsi] = 0;
-        a.runs[qsi] = 0;
+        a.rd[qsi] = 0;
     }
     if (head < a.G)
 #pragma unroll
