@@ -431,7 +431,14 @@ def ours(a):
         import ctypes as ct
         buf = (ct.c_uint64 * 16)()
         sb._check(sb.lib().saap_debug_step_trace(ctx.h, buf, 1))
-        graphs[0].launch()
+        if os.environ.get("SAAP_STEP_TRACE_EAGER"):
+            ctx.enable_timing(True)  # the eager step with its timing events
+            sparse_step(0)
+            ctx.synchronize()
+            ctx.timing()
+            ctx.enable_timing(False)
+        else:
+            graphs[0].launch()
         ctx.synchronize()
         sb._check(sb.lib().saap_debug_step_trace(ctx.h, buf, 0))
         if os.environ.get("SAAP_PLAN_TRACE"):  # routing phases of this (overlapped) step
@@ -473,7 +480,8 @@ def ours(a):
                             "consumer_full_wait_frac": round(float(np.median(t[:, 6] / np.maximum(t[:, 5], 1))), 3),
                             "producer_feed_frac": round(float(np.median(t[:, 7] / np.maximum(t[:, 5], 1))), 3),
                             "producer_record_wait_frac": round(float(np.median(t[:, 8] / np.maximum(t[:, 5], 1))), 3),
-                            "producer_tma_issue_frac": round(float(np.median(t[:, 9] / np.maximum(t[:, 5], 1))), 3)}
+                            "producer_tma_issue_frac": round(float(np.median(t[:, 9] / np.maximum(t[:, 5], 1))), 3),
+                            "first_record_us": rel(t[:, 10]), "first_tma_us": rel(t[:, 11])}
 
     # ---- counters, quality vs dense
     keys_scored = []

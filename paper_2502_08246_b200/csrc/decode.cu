@@ -1347,7 +1347,11 @@ __global__ void __maxnreg__(144)
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
         return t;
     };
-    if (a.dtrace && threadIdx.x == 0) a.dtrace[16 * blockIdx.x] = gtime();
+    if (a.dtrace && threadIdx.x == 0) {
+        a.dtrace[16 * blockIdx.x] = gtime();
+        a.dtrace[16 * blockIdx.x + 10] = 0;
+        a.dtrace[16 * blockIdx.x + 11] = 0;
+    }
     if (threadIdx.x == 0) tl_mark(a.tl, 2, true);
     if (threadIdx.x == 0) {
         for (int i = 0; i < CF::NS; ++i) {
@@ -1359,11 +1363,8 @@ __global__ void __maxnreg__(144)
         for (int i = 0; i < kRecRing; ++i) mbar_init(&s.rec_bar[i], 1);
         fence_mbar_init();
     }
-    // gap rows of a tile are masked (p = 0) but still enter the PV MMA: start
-    // from zeroed V so 0 * stale never meets a non-finite value
-    for (uint32_t e = threadIdx.x; e < sizeof(s.V) / 16; e += blockDim.x)
-        reinterpret_cast<uint4*>(&s.V[0][0])[e] = make_uint4(0, 0, 0, 0);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // (gap rows of a tile hold stale shared memory: their V fragments are
+    // masked to zero before the PV MMA, their scores to -inf)
     __syncthreads();
     // No grid wait: static tiles are ready now, dynamic tiles are published
     // by the (resident) planner through ready flags.  The combine grid may
@@ -1585,6 +1586,7 @@ __global__ void __maxnreg__(144)
             const unsigned long long tr = clock64();
             mbar_wait(&s.rec_bar[head], (rph >> head) & 1u);
             p_rec += clock64() - tr;
+            if (a.dtrace && lane == 0 && a.dtrace[16 * blockIdx.x + 10] == 0) a.dtrace[16 * blockIdx.x + 10] = gtime();
             rph ^= 1u << head;
             __syncwarp();
             const uint32_t w = s.rec_w[head];
@@ -1661,6 +1663,7 @@ __global__ void __maxnreg__(144)
             }
             __syncwarp();
             p_tma += clock64() - tt;
+            if (a.dtrace && lane == 0 && a.dtrace[16 * blockIdx.x + 11] == 0) a.dtrace[16 * blockIdx.x + 11] = gtime();
             // a dynamic record is re-armed for the next step once consumed
             if (w >= W && lane == 0) a.dyn_tiles[w - W].ready = 0;
             if (++stage == CF::NS) {
@@ -1841,11 +1844,19 @@ __global__ void __maxnreg__(144)
             // ---- O += P V   (B = V rows via ldmatrix.trans)
             const uint32_t vbase = smem_u32(&s.V[stage][0]);
             const uint32_t vrow = row0 + (mtx & 1) * 8 + r8;
+            // this lane's B elements are rows 2tig, 2tig+1 (b0, b2) and 2tig+8,
+            // 2tig+9 (b1, b3): zero the invalid ones (stale smem may be NaN)
+            const uint32_t m_lo = (((vbits >> kb) & 1u) ? 0x0000FFFFu : 0u) | (((vbits >> (kb + 1)) & 1u) ? 0xFFFF0000u : 0u);
+            const uint32_t m_hi = (((vbits >> (kb + 8)) & 1u) ? 0x0000FFFFu : 0u) | (((vbits >> (kb + 9)) & 1u) ? 0xFFFF0000u : 0u);
 #pragma unroll
             for (int j = 0; j < CF::NT / 2; ++j) {
                 const uint32_t chunk = 2 * j + (mtx >> 1);
                 uint32_t b0, b1, b2, b3;
                 ldsm_x4_t(vbase + toff<D>(vrow, chunk), b0, b1, b2, b3);
+                b0 &= m_lo;
+                b1 &= m_hi;
+                b2 &= m_lo;
+                b3 &= m_hi;
                 mma16816(o[2 * j], pa0, pa1, pa2, pa3, b0, b1);
                 mma16816(o[2 * j + 1], pa0, pa1, pa2, pa3, b2, b3);
             }
