@@ -280,47 +280,64 @@ __global__ void __launch_bounds__(32) scatter_kernel(
     }
 }
 
-// Streams K/V rows to their packed rows: consecutive threads move consecutive
-// 16-byte chunks of a row (coalesced 256-byte reads and writes), 4 chunks in
-// flight per thread.  dst_row comes from scatter_kernel.
+// Streams K/V rows to their packed rows.  One warp moves one key per step:
+// the K row and the V row as 16-byte chunks across the lanes (coalesced
+// 2 x 256-byte reads and writes at d=128), U keys in flight per warp.  The
+// key's context is found once per run of keys (contexts are contiguous in the
+// key order); dst_row comes from scatter_kernel.
 template <int D>
 __global__ void __launch_bounds__(256) move_rows_kernel(const GroupMeta* meta, const uint32_t* n_tile_group,
                                                         uint32_t n_groups, uint64_t total_ns,
                                                         const uint32_t* dst_row, const uint16_t* Ksrc,
                                                         const uint16_t* Vsrc, const uint64_t* src_row0,
                                                         uint16_t* Kdst, uint16_t* Vdst) {
-    constexpr uint32_t CH = D / 8;  // 16-byte chunks per row
-    const uint64_t n_chunks = total_ns * 2 * CH;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t e0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e0 < n_chunks; e0 += 4 * stride) {
-        uint4 v[4];
-        uint16_t* dst[4];
+    constexpr uint32_t CH = D / 8;                 // 16-byte chunks per row
+    constexpr uint32_t KPW = 32 / (2 * CH);        // keys per warp step (1 at d=128, 2 at 64, 4 at 32)
+    constexpr int U = 4;                           // warp steps in flight
+    const uint32_t lane = threadIdx.x & 31, sub = lane / (2 * CH), part = lane % (2 * CH);
+    const bool isv = part >= CH;
+    const uint32_t cc = isv ? part - CH : part;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t step = n_warps * KPW;
+    uint64_t g_lo = 1, g_hi = 0;  // cached context key range [g_lo, g_hi)
+    uint32_t g = 0;
+    GroupMeta gm{};
+    uint64_t srow0 = 0;
+    auto locate = [&](uint64_t key) {
+        if (key >= g_lo && key < g_hi) return;
+        uint32_t lo = 0, hi = n_groups;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (meta[mid].ivf_base <= key) lo = mid;
+            else hi = mid;
+        }
+        g = lo;
+        gm = meta[lo];
+        srow0 = src_row0[lo];
+        g_lo = gm.ivf_base;
+        g_hi = gm.ivf_base + (gm.n - gm.sink);
+    };
+    for (uint64_t k0 = warp * KPW + sub; k0 < total_ns; k0 += U * step) {
+        uint4 v[U];
+        uint16_t* dst[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint64_t e = e0 + u * stride;
+        for (int u = 0; u < U; ++u) {
+            const uint64_t key = k0 + u * step;
             dst[u] = nullptr;
-            if (e >= n_chunks) continue;
-            const uint64_t key = e / (2 * CH);       // global ivf index
-            const uint32_t part = (uint32_t)(e % (2 * CH));
-            // group of this key: binary search over ivf_base (n_groups small)
-            uint32_t lo = 0, hi = n_groups;
-            while (hi - lo > 1) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (meta[mid].ivf_base <= key) lo = mid;
-                else hi = mid;
-            }
-            const GroupMeta gm = meta[lo];
+            if (key >= total_ns) continue;
+            locate(key);
             const uint64_t lid = key - gm.ivf_base;
-            const bool isv = part >= CH;
-            const uint32_t cc = isv ? part - CH : part;
-            const uint16_t* src = (isv ? Vsrc : Ksrc) + (src_row0[lo] + gm.sink + lid) * D + cc * 8;
+            const uint16_t* src = (isv ? Vsrc : Ksrc) + (srow0 + gm.sink + lid) * D + cc * 8;
             v[u] = __ldcs(reinterpret_cast<const uint4*>(src));
             dst[u] = (isv ? Vdst : Kdst) + (gm.row_base + dst_row[key]) * D + cc * 8;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < U; ++u)
             if (dst[u]) __stcs(reinterpret_cast<uint4*>(dst[u]), v[u]);
     }
+    (void)g;
+    (void)n_tile_group;
 }
 
 // sink rows [0, sink) keep their position
