@@ -427,6 +427,8 @@ def ours(a):
                                    for i, k in enumerate(["start_us", "exchanged_us", "end_us"])})
     step_trace = None
     graph_plan_trace = None
+    # SAAP_TRACE_DENSE=1: the step / decode traces follow the dense step instead
+    tgraphs = dgraphs if os.environ.get("SAAP_TRACE_DENSE") and dgraphs else graphs
     if os.environ.get("SAAP_STEP_TRACE"):
         import ctypes as ct
         buf = (ct.c_uint64 * 16)()
@@ -438,7 +440,7 @@ def ours(a):
             ctx.timing()
             ctx.enable_timing(False)
         else:
-            graphs[0].launch()
+            tgraphs[0].launch()
         ctx.synchronize()
         sb._check(sb.lib().saap_debug_step_trace(ctx.h, buf, 0))
         if os.environ.get("SAAP_PLAN_TRACE"):  # routing phases of this (overlapped) step
@@ -449,7 +451,7 @@ def ours(a):
                 tt0 = cta[:, 0].min() if len(cta) else 0
                 own = cta[cta[:, 3] > 0]
                 slow = own[np.argsort(own[:, 3])[-4:]] if len(own) else own
-                graph_plan_trace = [list(pbuf)[:8]] + [
+                graph_plan_trace = [list(pbuf)[:13]] + [
                     {k: [round(float(x), 2) for x in np.percentile((own[:, i] - tt0) / 1e3, [0, 50, 100])]
                      for i, k in enumerate(["start_us", "exchanged_us", "selected_us", "end_us"])},
                     {"slowest_owner_ctas_us_and_candidates": [[round(float((r[i] - tt0) / 1e3), 2) for i in range(4)] + [int(r[4])]
@@ -463,7 +465,7 @@ def ours(a):
     decode_trace = None
     if os.environ.get("SAAP_DECODE_TRACE"):
         import ctypes as ct
-        graphs[0].launch()  # trace the sparse step (the eager loop above ended on dense)
+        tgraphs[0].launch()  # trace the sparse (or dense) step
         ctx.synchronize()
         nc = ctx.sm_count
         buf = (ct.c_uint64 * (16 * nc))()

@@ -619,6 +619,8 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->sm_count,
                                                                     (max_stream + chunk - 1) / chunk));
     da.tail = env_u32("SAAP_TAIL_PER_CTA", 1) * (uint32_t)grid;
+    static const uint32_t dec_poll = env_u32("SAAP_DEC_POLL_NS", 100);
+    da.poll_ns = dec_poll;
     da.tl = c->tl;
     static const int wait_env = std::getenv("SAAP_DECODE_WAIT") ? std::atoi(std::getenv("SAAP_DECODE_WAIT")) : 0;
     da.wait_plan = plan && wait_env ? 1u : 0u;

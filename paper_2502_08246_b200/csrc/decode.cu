@@ -43,6 +43,49 @@ struct Seg {
     uint64_t start;  // ROWS: group-relative row; LIST: gather-buffer row
 };
 
+// Tile records of one group's dynamic tiles (attention.cpp:342-372 visited
+// set, laid out as tiles): segment s occupies the 8-aligned virtual rows
+// [vpre[s], vpre[s] + ceil8(len_s)), tile t the virtual rows [128t, 128t+128).
+// One thread per tile (threads first, first + stride, ...): a binary search
+// finds the segment holding the tile's first row, the overlapped segments
+// become its pieces in order.  No counters, no second pass: every record
+// (header with ready = 0, pieces) is written once; head chunks > 0 get copies.
+__device__ __forceinline__ void emit_tiles(TileRec* base, uint32_t ntiles, uint32_t nh, uint32_t qslot0,
+                                           const Seg* segs, const uint32_t* vpre, uint32_t ns,
+                                           uint64_t row_base, uint32_t first, uint32_t stride) {
+#pragma unroll 1
+    for (uint32_t t = first; t < ntiles; t += stride) {
+        const uint32_t v_lo = t * kTileRows, v_hi = v_lo + kTileRows;
+        uint32_t lo = 0, hi = ns;  // last segment with vpre <= v_lo (vpre[0] == 0)
+#pragma unroll 1
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (vpre[mid] <= v_lo) lo = mid;
+            else hi = mid;
+        }
+        uint32_t np = 0;
+#pragma unroll 1
+        for (uint32_t b = lo; b < ns; ++b) {
+            const uint32_t v0 = vpre[b];
+            if (v0 >= v_hi) break;
+            const Seg sg = segs[b];
+            const uint32_t a0 = max(v0, v_lo), kend = min(v0 + sg.len, v_hi);
+            if (kend <= a0) continue;
+            const uint64_t row = (sg.kind == KIND_LIST ? 0 : row_base) + sg.start + (a0 - v0);
+            const uint4 pr = make_uint4((kend - a0) | (sg.kind == KIND_LIST ? kPieceGather : 0u), a0 - v_lo,
+                                        (uint32_t)row, (uint32_t)(row >> 32));
+#pragma unroll 1
+            for (uint32_t hc = 0; hc < nh; ++hc)
+                *reinterpret_cast<uint4*>(&base[(size_t)hc * ntiles + t].p[np]) = pr;
+            ++np;
+        }
+#pragma unroll 1
+        for (uint32_t hc = 0; hc < nh; ++hc)
+            *reinterpret_cast<uint4*>(&base[(size_t)hc * ntiles + t]) =
+                make_uint4(np, qslot0 + hc, 0u, t + 1 == ntiles ? 1u : 0u);
+    }
+}
+
 __device__ __forceinline__ bool precedes(double sa, uint32_t ia, double sb, uint32_t ib) {
     return sa > sb || (sa == sb && ia < ib);
 }
@@ -565,42 +608,14 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
                 return;
             }
             tile0 = __shfl_sync(0xFFFFFFFFu, tile0, 0);
-            __shared__ uint32_t s_np1[kPlanTileCnt];
-            const bool np_smem = ntiles <= (uint32_t)kPlanTileCnt;
-            for (uint32_t t = lane; t < ntiles; t += 32) {
-                if (np_smem) s_np1[t] = 0;
-                else a.dyn_tiles[tile0 + t].npieces = 0;
-            }
+            emit_tiles(a.dyn_tiles + tile0, ntiles, nh, g * nh, segs, vpre, L, gm.row_base, lane, 32);
+            // one fence per lane orders every record the warp wrote (the warp
+            // barrier makes the other lanes' writes cumulative) before the flags
             __syncwarp();
-            if (!np_smem) __threadfence_block();
-            for (uint32_t b = lane; b < L; b += 32) {
-                const Seg sg = segs[b];
-                const uint32_t v0 = vpre[b], v8 = v0 + ((sg.len + 7) & ~7u), vend = v0 + sg.len;
-                for (uint32_t t = v0 / kTileRows; t * kTileRows < v8; ++t) {
-                    const uint32_t a0 = max(v0, t * kTileRows), b1 = min(v8, (t + 1) * kTileRows);
-                    const uint32_t kend = min(b1, vend);
-                    if (kend <= a0) continue;
-                    PieceRec pr;
-                    pr.len = kend - a0;
-                    pr.srow = a0 - t * kTileRows;
-                    pr.row = gm.row_base + sg.start + (a0 - v0);
-                    TileRec* tr = a.dyn_tiles + tile0 + t;
-                    const uint32_t slot = atomicAdd(np_smem ? &s_np1[t] : &tr->npieces, 1u);
-                    for (uint32_t hc = 0; hc < nh; ++hc) tr[(size_t)hc * ntiles].p[slot] = pr;
-                }
-            }
+            __threadfence();
             __syncwarp();
-            // publish: header + release flag per tile (the release is cumulative
-            // over the pieces the warp wrote before the warp barrier)
-            for (uint32_t e = lane; e < ntiles * nh; e += 32) {
-                const uint32_t hc = e / ntiles, t = e % ntiles;
-                TileRec* tr = a.dyn_tiles + tile0 + e;
-                tr->npieces = np_smem ? s_np1[t] : a.dyn_tiles[tile0 + t].npieces;
-                tr->qslot = g * nh + hc;
-                tr->end = t + 1 == ntiles ? 1u : 0u;
-                __threadfence();
-                st_release_u32(&tr->ready, 1u);
-            }
+            for (uint32_t e = lane; e < ntiles * nh; e += 32)
+                *reinterpret_cast<volatile uint32_t*>(&a.dyn_tiles[tile0 + e].ready) = 1u;
             __syncwarp();
             if (lane == 0) {
                 __threadfence();
@@ -757,54 +772,12 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         }
         return;
     }
-    // piece counters: shared memory when the group's tiles fit, else in place
-    __shared__ uint32_t s_np[kPlanTileCnt];
-    const bool np_smem = ntiles <= (uint32_t)kPlanTileCnt;
-    for (uint32_t t = tid; t < ntiles; t += nth) {
-        if (np_smem) s_np[t] = 0;
-        else a.dyn_tiles[tile0 + t].npieces = 0;
-    }
-    __syncthreads();
     trace(6);
-    // pieces: one per (segment, overlapped tile); slot order inside a tile is
-    // free.  Short segments: one thread each; long ones: tiles spread over the
-    // CTA.  Head chunks > 0 get copies of chunk 0's tiles.
-    auto emit = [&](const Seg& sg, uint32_t v0, uint32_t t) {
-        const uint32_t v8 = v0 + ((sg.len + 7) & ~7u), vend = v0 + sg.len;
-        const uint32_t a0 = max(v0, t * kTileRows), b0 = min(v8, (t + 1) * kTileRows);
-        const uint32_t keys_end = min(b0, vend);
-        if (keys_end <= a0) return;
-        PieceRec pr;
-        pr.len = (keys_end - a0) | (sg.kind == KIND_LIST ? kPieceGather : 0u);
-        pr.srow = a0 - t * kTileRows;
-        pr.row = (sg.kind == KIND_LIST ? 0 : gm.row_base) + sg.start + (a0 - v0);
-        TileRec* tr = a.dyn_tiles + tile0 + t;
-        const uint32_t slot = atomicAdd(np_smem ? &s_np[t] : &tr->npieces, 1u);
-        for (uint32_t hc = 0; hc < nh; ++hc) tr[(size_t)hc * ntiles].p[slot] = pr;
-    };
-    for (uint32_t s2 = tid; s2 < nseg; s2 += nth) {
-        const Seg sg = segs[s2];
-        if (sg.len == 0 || sg.len > 4 * kTileRows) continue;
-        const uint32_t v0 = vpre[s2], v8 = v0 + ((sg.len + 7) & ~7u);
-        for (uint32_t t = v0 / kTileRows; t * kTileRows < v8; ++t) emit(sg, v0, t);
-    }
-    for (uint32_t s2 = 0; s2 < nseg; ++s2) {
-        const Seg sg = segs[s2];
-        if (sg.len <= 4 * kTileRows) continue;
-        const uint32_t v0 = vpre[s2], v8 = v0 + ((sg.len + 7) & ~7u);
-        for (uint32_t t = v0 / kTileRows + tid; t * kTileRows < v8; t += nth) emit(sg, v0, t);
-    }
-    __threadfence();  // pieces before the headers' ready flags (release)
+    emit_tiles(a.dyn_tiles + tile0, ntiles, nh, g * nh, segs, vpre, nseg, gm.row_base, tid, nth);
+    __threadfence();  // records before the ready flags
     __syncthreads();
-    for (uint32_t e = tid; e < ntiles * nh; e += nth) {
-        const uint32_t hc = e / ntiles, t = e % ntiles;
-        TileRec* tr = a.dyn_tiles + tile0 + e;
-        tr->npieces = np_smem ? s_np[t] : a.dyn_tiles[tile0 + t].npieces;
-        tr->qslot = g * nh + hc;
-        tr->end = t + 1 == ntiles ? 1u : 0u;
-        __threadfence();
-        st_release_u32(&tr->ready, 1u);
-    }
+    for (uint32_t e = tid; e < ntiles * nh; e += nth)
+        *reinterpret_cast<volatile uint32_t*>(&a.dyn_tiles[tile0 + e].ready) = 1u;
     __syncthreads();
     if (tid == 0) {
         __threadfence();
@@ -851,7 +824,6 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     __shared__ uint32_t s_off[kMaxC + 1], s_offA[kMaxC + 1];
     __shared__ uint32_t hist[256];
     __shared__ uint32_t cand_id[kMaxCand], sel[kMaxC];
-    __shared__ uint32_t s_np[kPlanTileCnt];
     // phase-local buffers share one region: scoring | exact sort | planning
     union Phase {
         struct {
@@ -874,7 +846,8 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     auto& xi = ph.sort.xi;
     auto& segs = ph.plan.segs;
     auto& vpre = ph.plan.vpre;
-    __shared__ uint32_t s_pref, s_need, s_ncand;
+    __shared__ uint32_t s_pref, s_need, s_ncand, s_nb, s_bsel, s_bcnt;
+    __shared__ float s_mm[2][NT / 32], s_bnd[32];
     __shared__ double s_n2[NT / 32];
     pdl_trigger();
     const uint32_t tid = threadIdx.x, lane = tid & 31;
@@ -998,46 +971,142 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
             const uint32_t u = __float_as_uint(av[i]);
             key[i] = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
         }
-        if (tid == 0) {
-            s_pref = 0;
-            s_need = L;
-        }
-        for (int shift = 24; shift >= 0; shift -= 8) {
-            if (tid < 256) hist[tid] = 0;
-            __syncthreads();
-            const uint32_t pref = s_pref;
-            const uint32_t hmask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
+        // the L-th largest score.  Pass 1: 256 linear buckets over [min, max]
+        // (monotone in the score), suffix counts find the boundary bucket;
+        // pass 2: one warp ranks its (usually few) members.  Radix select
+        // (8-bit digits, MSB first) when the boundary bucket holds > 32.
+        {
+            float lmn = INFINITY, lmx = -INFINITY;
 #pragma unroll
             for (uint32_t i = 0; i < PER; ++i)
-                if (tid + i * NT < C && (key[i] & hmask) == (pref & hmask)) atomicAdd(&hist[(key[i] >> shift) & 255u], 1u);
-            __syncthreads();
-            if (tid < 32) {
-                uint32_t cnt[8], tot = 0;
+                if (tid + i * NT < C) {
+                    lmn = fminf(lmn, av[i]);
+                    lmx = fmaxf(lmx, av[i]);
+                }
 #pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    cnt[b] = hist[255 - 8 * tid - b];
-                    tot += cnt[b];
-                }
-                uint32_t incl = tot;
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                    if (tid >= (uint32_t)o) incl += v;
-                }
-                const uint32_t need = s_need, before = incl - tot;
-                if (before < need && incl >= need) {
-                    uint32_t run = before;
-#pragma unroll
-                    for (int b = 0; b < 8; ++b) {
-                        if (run + cnt[b] >= need) {
-                            s_pref = pref | ((uint32_t)(255 - 8 * tid - b) << shift);
-                            s_need = need - run;
-                            break;
-                        }
-                        run += cnt[b];
-                    }
-                }
+            for (int o = 16; o; o >>= 1) {
+                lmn = fminf(lmn, __shfl_xor_sync(0xFFFFFFFFu, lmn, o));
+                lmx = fmaxf(lmx, __shfl_xor_sync(0xFFFFFFFFu, lmx, o));
+            }
+            if (lane == 0) {
+                s_mm[0][tid >> 5] = lmn;
+                s_mm[1][tid >> 5] = lmx;
+            }
+            if (tid < 256) hist[tid] = 0;
+            if (tid == 0) {
+                s_nb = 0;
+                s_bcnt = 0xFFFFFFFFu;
             }
             __syncthreads();
+            float vmn = s_mm[0][0], vmx = s_mm[1][0];
+#pragma unroll
+            for (uint32_t w = 1; w < NT / 32; ++w) {
+                vmn = fminf(vmn, s_mm[0][w]);
+                vmx = fmaxf(vmx, s_mm[1][w]);
+            }
+            const float span = vmx - vmn, scale = 256.f / span;
+            const bool lin = span > 0.f && scale < INFINITY && vmx < INFINITY && vmn > -INFINITY;
+            uint32_t bk[PER];
+            if (lin) {
+#pragma unroll
+                for (uint32_t i = 0; i < PER; ++i) {
+                    bk[i] = min(255u, (uint32_t)((av[i] - vmn) * scale));
+                    if (tid + i * NT < C) atomicAdd(&hist[bk[i]], 1u);
+                }
+                __syncthreads();
+                if (tid < 32) {
+                    uint32_t cnt[8], tot = 0;
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        cnt[b] = hist[255 - 8 * tid - b];
+                        tot += cnt[b];
+                    }
+                    uint32_t incl = tot;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                        if (tid >= (uint32_t)o) incl += v;
+                    }
+                    const uint32_t before = incl - tot;
+                    if (before < L && incl >= L) {
+                        uint32_t run = before;
+#pragma unroll
+                        for (int b = 0; b < 8; ++b) {
+                            if (run + cnt[b] >= L) {
+                                s_bsel = 255 - 8 * tid - b;
+                                s_need = L - run;
+                                s_bcnt = cnt[b];
+                                break;
+                            }
+                            run += cnt[b];
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            if (lin && s_bcnt <= 32) {
+                const uint32_t bsel = s_bsel;
+#pragma unroll
+                for (uint32_t i = 0; i < PER; ++i)
+                    if (tid + i * NT < C && bk[i] == bsel) s_bnd[atomicAdd(&s_nb, 1u)] = av[i];
+                __syncthreads();
+                if (tid < 32) {
+                    const uint32_t nb = s_nb;
+                    const float v = tid < nb ? s_bnd[tid] : -INFINITY;
+                    uint32_t rank = 0;
+                    for (uint32_t k = 0; k < nb; ++k) {
+                        const float u = s_bnd[k];
+                        rank += (u > v || (u == v && k < tid)) ? 1u : 0u;
+                    }
+                    if (tid < nb && rank == s_need - 1) {
+                        const uint32_t u = __float_as_uint(v);
+                        s_pref = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+                    }
+                }
+                __syncthreads();
+            } else {
+            if (tid == 0) {
+                s_pref = 0;
+                s_need = L;
+            }
+            for (int shift = 24; shift >= 0; shift -= 8) {
+                if (tid < 256) hist[tid] = 0;
+                __syncthreads();
+                const uint32_t pref = s_pref;
+                const uint32_t hmask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
+    #pragma unroll
+                for (uint32_t i = 0; i < PER; ++i)
+                    if (tid + i * NT < C && (key[i] & hmask) == (pref & hmask)) atomicAdd(&hist[(key[i] >> shift) & 255u], 1u);
+                __syncthreads();
+                if (tid < 32) {
+                    uint32_t cnt[8], tot = 0;
+    #pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        cnt[b] = hist[255 - 8 * tid - b];
+                        tot += cnt[b];
+                    }
+                    uint32_t incl = tot;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                        if (tid >= (uint32_t)o) incl += v;
+                    }
+                    const uint32_t need = s_need, before = incl - tot;
+                    if (before < need && incl >= need) {
+                        uint32_t run = before;
+    #pragma unroll
+                        for (int b = 0; b < 8; ++b) {
+                            if (run + cnt[b] >= need) {
+                                s_pref = pref | ((uint32_t)(255 - 8 * tid - b) << shift);
+                                s_need = need - run;
+                                break;
+                            }
+                            run += cnt[b];
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            }
         }
         trace(2);
         const uint32_t tk = s_pref;
@@ -1076,10 +1145,19 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
             // now free slice buffer
             // (from the transposed centroids: the cluster just streamed them, so
             // these reads hit L2 instead of queueing behind the decode in HBM)
+            // (every load in flight before the first store: one L2 round trip)
             float* crow = slab;  // [nS][D + 1]
-            for (uint32_t e = tid; e < nS * D; e += NT) {
-                const uint32_t r = e % nS, j = e / nS;
-                crow[r * (D + 1) + j] = sl.centT[(size_t)j * C + cand_id[r]];
+            constexpr uint32_t PE = (kMaxCand * D + NT - 1) / NT;
+            float tv[PE];
+#pragma unroll
+            for (uint32_t i = 0; i < PE; ++i) {
+                const uint32_t e = tid + i * NT;
+                if (e < nS * D) tv[i] = __ldcg(sl.centT + (size_t)(e / nS) * C + cand_id[e % nS]);
+            }
+#pragma unroll
+            for (uint32_t i = 0; i < PE; ++i) {
+                const uint32_t e = tid + i * NT;
+                if (e < nS * D) crow[(e % nS) * (D + 1) + e / nS] = tv[i];
             }
             __syncthreads();
             double ex = -INFINITY;
@@ -1175,43 +1253,16 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     }
     (void)T;
     tile0 = __shfl_sync(0xFFFFFFFFu, tile0, 0);
+    trace(8);
     if (ntiles) {
-        const bool np_smem = ntiles <= (uint32_t)kPlanTileCnt;
-        for (uint32_t t = lane; t < ntiles; t += 32) {
-            if (np_smem) s_np[t] = 0;
-            else a.dyn_tiles[tile0 + t].npieces = 0;
-        }
-        __syncwarp();
-        if (!np_smem) __threadfence_block();
-        for (uint32_t b = lane; b < L; b += 32) {
-            const Seg sg = segs[b];
-            const uint32_t v0 = vpre[b], v8 = v0 + ((sg.len + 7) & ~7u), vend = v0 + sg.len;
-            for (uint32_t t = v0 / kTileRows; t * kTileRows < v8; ++t) {
-                const uint32_t a0 = max(v0, t * kTileRows), b1 = min(v8, (t + 1) * kTileRows);
-                const uint32_t kend = min(b1, vend);
-                if (kend <= a0) continue;
-                PieceRec pr;
-                pr.len = kend - a0;
-                pr.srow = a0 - t * kTileRows;
-                pr.row = gm.row_base + sg.start + (a0 - v0);
-                TileRec* trp = a.dyn_tiles + tile0 + t;
-                const uint32_t sl2 = atomicAdd(np_smem ? &s_np[t] : &trp->npieces, 1u);
-                for (uint32_t hc = 0; hc < nh; ++hc) trp[(size_t)hc * ntiles].p[sl2] = pr;
-            }
-        }
-        __syncwarp();
-        for (uint32_t e = lane; e < ntiles * nh; e += 32) {
-            const uint32_t hc = e / ntiles, t = e % ntiles;
-            TileRec* trp = a.dyn_tiles + tile0 + e;
-            trp->npieces = np_smem ? s_np[t] : a.dyn_tiles[tile0 + t].npieces;
-            trp->qslot = g * nh + hc;
-            trp->end = t + 1 == ntiles ? 1u : 0u;
-        }
+        emit_tiles(a.dyn_tiles + tile0, ntiles, nh, g * nh, segs, vpre, L, gm.row_base, lane, 32);
         // one fence per lane orders every record the warp wrote (the warp
         // barrier makes the other lanes' writes cumulative) before the flags
         __syncwarp();
+        trace(9);
         __threadfence();
         __syncwarp();
+        trace(10);
         for (uint32_t e = lane; e < ntiles * nh; e += 32)
             *reinterpret_cast<volatile uint32_t*>(&a.dyn_tiles[tile0 + e].ready) = 1u;
     }
@@ -1420,7 +1471,9 @@ __global__ void __maxnreg__(144)
             __syncwarp();
             if (lane == 0) {
                 st_release_u32(a.part_flag + pidx, 1u);  // the combine folds it in now
-                atomicAdd(&a.rd[slot], (unsigned long long)tiles);  // tiles published (low word)
+                // tiles published (low word), a release too: once the combine
+                // reads every tile counted, every partial is visible
+                red_release_add_u64(&a.rd[slot], (unsigned long long)tiles);
                 tl_mark(a.tl, 4, false);  // last run published
             }
         }
@@ -1449,9 +1502,11 @@ __global__ void __maxnreg__(144)
         // Guided tail: a region of R tiles goes out in CH-tile chunks, then its
         // last 3M tiles as 2M tiles in pairs and M singles, so CTAs finish
         // within about a tile of each other.
+        bool in_tail = false;  // the last ticket was a pair or a single
         auto guided = [&](uint32_t d, uint32_t R, uint32_t ch, uint32_t& b0, uint32_t& b1) -> bool {
             const uint32_t tail = 3 * M;
             const uint32_t B = R > tail ? (R - tail) / ch * ch : 0u, nb = B / ch;
+            in_tail = d >= nb;
             if (d < nb) {
                 b0 = d * ch;
                 b1 = b0 + ch;
@@ -1536,6 +1591,9 @@ __global__ void __maxnreg__(144)
                 // waiting for the planner: re-poll only when the ring runs low
                 // (each poll is a round trip on the producer's path)
                 if (!pend && poll_wait && cnt > 1) break;
+                // in the stream's tail a CTA holds at most one record beyond
+                // its tile ring, so the CTAs drain together
+                if (!pend && in_tail && cnt > 0) break;
                 if (!pend) {
                     if (ticket_end == 0xFFFFFFFFu && ticket != blockIdx.x) {  // second ticket of the first batch
                         ticket = tk_first;
@@ -1579,7 +1637,7 @@ __global__ void __maxnreg__(144)
             p_feed += clock64() - tf;
             if (cnt == 0) {
                 if (!feeding) break;
-                __nanosleep(100);  // waiting for the planner
+                __nanosleep(a.poll_ns);  // waiting for the planner
                 continue;
             }
             // ---- issue the head tile
@@ -1957,11 +2015,14 @@ __global__ void __maxnreg__(80) combine_kernel(CombineArgs a) {
             s_first = 0xFFFFFFFFu;
         }
         __syncthreads();
-        // the published prefix of the reserved runs: every thread checks one flag
+        // the published prefix of the reserved runs: every thread checks one
+        // flag (once every tile is counted, every reserved run is published)
         const uint32_t res = s_res;
-        for (uint32_t r = folded + threadIdx.x; r < res; r += blockDim.x)
-            if (!ld_acquire_u32(a.part_flag + base + r)) atomicMin(&s_first, r);
-        __syncthreads();
+        if (!s_dn) {
+            for (uint32_t r = folded + threadIdx.x; r < res; r += blockDim.x)
+                if (!ld_acquire_u32(a.part_flag + base + r)) atomicMin(&s_first, r);
+            __syncthreads();
+        }
         if (threadIdx.x == 0) {
             const uint32_t nr = min(res, s_first);
             s_nr = nr;
