@@ -122,6 +122,15 @@ SAAP_API int saap_assign_keys(saap_ctx* ctx, const saap_partition* p, const floa
 /* build_ivf(assignment, C) -> off[C+1], idx  partition.cpp:200-223 */
 SAAP_API int saap_build_ivf(saap_ctx* ctx, const uint32_t* assignment, uint64_t n, uint64_t n_buckets,
                    uint64_t* off, uint64_t* idx);
+/* kmeans_train(keys, C, iters, rng, stats)  partition.cpp:52-179 (spherical
+ * k-means, bit-exact).  seed_rows[C] are the caller's Rng draws in centroid
+ * order: rng.sample_without_replacement(n, C) then rng.shuffle(...)
+ * (partition.cpp:80-82).  objective_per_iter (iters entries), and the two
+ * counters (KMeansStats, partition.hpp:52-57) may be NULL.  d <= 128. */
+SAAP_API int saap_kmeans_train(saap_ctx* ctx, const float* keys, uint64_t n, uint64_t dim,
+                      uint64_t n_buckets, uint64_t iters, const uint64_t* seed_rows,
+                      float* centroids, double* objective_per_iter,
+                      uint64_t* zero_vector_keys, uint64_t* empty_cluster_repairs);
 /* rope_remove_block(keys, positions, {dim, base})  rope.cpp:87-90 */
 SAAP_API int saap_rope_remove(saap_ctx* ctx, const float* x, uint64_t rows, uint64_t dim,
                      const uint64_t* positions, double base, float* out);

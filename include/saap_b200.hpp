@@ -13,6 +13,7 @@
 // without the reference headers.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -152,6 +153,87 @@ KeyAssignment assign_keys(const TB& keys, const P& p) {
     check(saap_assign_keys(dp.ctx().get(), dp.get(), keys.data.data(), keys.rows, keys.dim,
                            a.bucket_of.data()));
     return a;
+}
+
+// Stand-in for saap::Rng (tensor.hpp:87-131): only the draws kmeans_train
+// makes.  With the reference headers, pass saap::Rng itself.
+class Rng {
+public:
+    explicit Rng(std::uint64_t seed) : seed_(seed), state_(seed) {}
+    std::uint64_t next_u64() {
+        std::uint64_t z = (state_ += 0x9E3779B97F4A7C15ull);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    }
+    std::uint64_t below(std::uint64_t n) {
+        if (n == 0) throw std::invalid_argument("Rng::below: n must be >= 1");
+        const std::uint64_t threshold = (0 - n) % n;
+        for (;;) {
+            const std::uint64_t r = next_u64();
+            if (r >= threshold) return r % n;
+        }
+    }
+    Rng child(std::uint64_t stream) const {
+        Rng mixer(seed_ ^ (0xD1342543DE82EF95ull * (stream + 1)));
+        return Rng(mixer.next_u64());
+    }
+    std::vector<std::uint64_t> sample_without_replacement(std::uint64_t n, std::uint64_t m) {
+        if (m > n) throw std::invalid_argument("sample_without_replacement: m > n");
+        std::vector<std::uint64_t> out;
+        out.reserve(m);
+        std::vector<bool> taken(n, false);
+        for (std::uint64_t j = n - m; j < n; ++j) {
+            std::uint64_t t = below(j + 1);
+            if (taken[t]) t = j;
+            taken[t] = true;
+            out.push_back(t);
+        }
+        std::sort(out.begin(), out.end());
+        return out;
+    }
+    template <typename T>
+    void shuffle(std::vector<T>& v) {
+        for (std::size_t i = v.size(); i > 1; --i) std::swap(v[i - 1], v[(std::size_t)below(i)]);
+    }
+
+private:
+    std::uint64_t seed_, state_;
+};
+
+struct KMeansStats {
+    std::vector<double> objective_per_iter;
+    std::size_t zero_vector_keys = 0;
+    std::size_t empty_cluster_repairs = 0;
+};
+
+// kmeans_train (partition.cpp:52-179), bit-exact on the device.  The caller's
+// Rng draws the seed rows here, as in the reference; any Rng/stats types with
+// the reference's member names work (saap::Rng, saap::KMeansStats).
+template <typename TB, typename RngT, typename StatsT = KMeansStats>
+Partition kmeans_train(const TB& keys, std::size_t n_buckets, std::size_t iters, RngT& rng,
+                       StatsT* stats = nullptr) {
+    if (n_buckets < 1) throw std::invalid_argument("kmeans_train: need at least 1 bucket");
+    if (keys.rows < n_buckets)
+        throw std::invalid_argument("kmeans_train: " + std::to_string(keys.rows) +
+                                    " keys cannot seed " + std::to_string(n_buckets) + " buckets");
+    if (iters < 1) throw std::invalid_argument("kmeans_train: iters must be >= 1");
+    auto seeds = rng.sample_without_replacement(keys.rows, n_buckets);
+    rng.shuffle(seeds);
+    std::vector<std::uint64_t> rows(seeds.begin(), seeds.end());
+    Partition p;
+    p.centroids = TensorBlock(n_buckets, keys.dim);
+    std::vector<double> obj(iters);
+    std::uint64_t zk = 0, rep = 0;
+    check(saap_kmeans_train(Context::current().get(), keys.data.data(), keys.rows, keys.dim,
+                            n_buckets, iters, rows.data(), p.centroids.data.data(), obj.data(),
+                            &zk, &rep));
+    if (stats) {
+        stats->objective_per_iter.assign(obj.begin(), obj.end());
+        stats->zero_vector_keys = zk;
+        stats->empty_cluster_repairs = rep;
+    }
+    return p;
 }
 
 template <typename KA>

@@ -274,6 +274,24 @@ class Ref:
                                             _u64(n_buckets), _u64(iters), _u64(seed), _p(out)))
         return out
 
+    def kmeans_train_stats(self, keys, n_buckets, iters, seed, stream=None):
+        """kmeans_train(keys, C, iters, Rng(seed)[.child(stream)], &stats) ->
+        (centroids, objective_per_iter, zero_vector_keys, repairs, next draw)."""
+        keys = _f32(keys)
+        out = np.empty((n_buckets, keys.shape[1]), np.float32)
+        obj = np.empty(iters, np.float64)
+        zk, rep, nxt = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        st = (1 << 64) - 1 if stream is None else stream
+        self._chk(self.lib.ref_kmeans_train_stats(
+            _p(keys), _u64(keys.shape[0]), _u64(keys.shape[1]), _u64(n_buckets), _u64(iters),
+            _u64(seed), _u64(st), _p(out), _p(obj), C.byref(zk), C.byref(rep), C.byref(nxt)))
+        return out, obj, zk.value, rep.value, nxt.value
+
+    def kmeans_seed_rows(self, seed, n, m):
+        out = np.empty(m, np.uint64)
+        self._chk(self.lib.ref_kmeans_seed_rows(_u64(seed), _u64(n), _u64(m), _p(out)))
+        return out
+
     def assign_keys(self, keys, cent, threads=1):
         keys, cent = _f32(keys), _f32(cent)
         out = np.empty(keys.shape[0], np.uint32)

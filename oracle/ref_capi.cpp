@@ -167,6 +167,37 @@ int ref_kmeans_train(const float* keys, std::uint64_t n, std::uint64_t d, std::u
     });
 }
 
+// kmeans_train with its KMeansStats; the Rng is Rng(seed), or
+// Rng(seed).child(stream) when stream != ~0 (train_head_partition's stream).
+// rng_state_after receives the Rng's next draw after training (stream check).
+int ref_kmeans_train_stats(const float* keys, std::uint64_t n, std::uint64_t d,
+                           std::uint64_t n_buckets, std::uint64_t iters, std::uint64_t seed,
+                           std::uint64_t stream, float* centroids, double* objective,
+                           std::uint64_t* zero_keys, std::uint64_t* repairs,
+                           std::uint64_t* next_draw) {
+    return guard([&] {
+        Rng rng = stream == ~0ull ? Rng(seed) : Rng(seed).child(stream);
+        KMeansStats st;
+        Partition p = kmeans_train(block(keys, n, d), n_buckets, iters, rng, &st);
+        put(p.centroids, centroids);
+        std::copy(st.objective_per_iter.begin(), st.objective_per_iter.end(), objective);
+        *zero_keys = st.zero_vector_keys;
+        *repairs = st.empty_cluster_repairs;
+        *next_draw = rng.next_u64();
+    });
+}
+
+// The seed rows kmeans_train draws (partition.cpp:80-82) for Rng(seed).
+int ref_kmeans_seed_rows(std::uint64_t seed, std::uint64_t n, std::uint64_t m,
+                         std::uint64_t* out) {
+    return guard([&] {
+        Rng rng(seed);
+        auto s = rng.sample_without_replacement(n, m);
+        rng.shuffle(s);
+        std::copy(s.begin(), s.end(), out);
+    });
+}
+
 int ref_assign_keys(const float* keys, std::uint64_t n, std::uint64_t d, const float* centroids,
                     std::uint64_t C, std::uint32_t* out) {
     return guard([&] {

@@ -9,6 +9,7 @@ and error behaviour (``std::invalid_argument`` -> :class:`InvalidArgument`, a
 =========================  ==================================================
 reference (proj/core)      here
 =========================  ==================================================
+kmeans_train / Rng         :func:`kmeans_train` / :class:`Rng` (partition.cpp:52-179)
 assign_keys                :func:`assign_keys`  (partition.cpp:191-198)
 build_ivf                  :func:`build_ivf`    (partition.cpp:200-223)
 rope_remove_block          :func:`rope_remove_block` (rope.cpp:87-90)
@@ -363,6 +364,97 @@ def batched_bucket_select(model: QModel, query_group, l) -> np.ndarray:
     _check(lib().saap_batched_bucket_select(model.ctx.h, model.h, _p(q), _u64(q.shape[0]),
                                             _u64(q.shape[1]), _u64(l), _p(out)))
     return out
+
+
+# --------------------------------------------------------------------------
+_M64 = (1 << 64) - 1
+
+
+class Rng:
+    """saap::Rng host stream (tensor.hpp:87-131, tensor.cpp:90-168): SplitMix64
+    with the reference's rejection sampling, Floyd sampling and Fisher-Yates
+    shuffle, so ``kmeans_train`` draws the same seed rows as the reference for
+    the same seed.  Host-side control state only (no arithmetic on keys)."""
+
+    def __init__(self, seed: int):
+        self.seed_ = int(seed) & _M64
+        self.state_ = self.seed_
+
+    def next_u64(self) -> int:
+        self.state_ = (self.state_ + 0x9E3779B97F4A7C15) & _M64
+        z = self.state_
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+        return z ^ (z >> 31)
+
+    def below(self, n: int) -> int:
+        if n == 0:
+            raise InvalidArgument("Rng::below: n must be >= 1")
+        threshold = ((1 << 64) - n) % n
+        while True:
+            r = self.next_u64()
+            if r >= threshold:
+                return r % n
+
+    def child(self, stream: int) -> "Rng":
+        mixer = Rng(self.seed_ ^ ((0xD1342543DE82EF95 * (int(stream) + 1)) & _M64))
+        return Rng(mixer.next_u64())
+
+    def sample_without_replacement(self, n: int, m: int) -> list:
+        if m > n:
+            raise InvalidArgument("sample_without_replacement: m > n")
+        taken, out = set(), []
+        for j in range(n - m, n):
+            t = self.below(j + 1)
+            if t in taken:
+                t = j
+            taken.add(t)
+            out.append(t)
+        return sorted(out)
+
+    def shuffle(self, v: list) -> None:
+        for i in range(len(v), 1, -1):
+            j = self.below(i)
+            v[i - 1], v[j] = v[j], v[i - 1]
+
+
+@dataclass
+class KMeansStats:
+    """saap::KMeansStats (partition.hpp:52-57)."""
+    objective_per_iter: list = field(default_factory=list)
+    zero_vector_keys: int = 0
+    empty_cluster_repairs: int = 0
+
+
+def kmeans_train(keys, n_buckets, iters, rng: Rng, stats: Optional[KMeansStats] = None,
+                 ctx: Optional[Context] = None) -> "Partition":
+    """Spherical k-means on the device (partition.cpp:52-179), bit-exact with
+    the reference for the same keys and Rng state.  The Rng draws the seed
+    rows on the host exactly where the reference does; seeding, assignment,
+    empty-cluster repair, member means and the objective run in kmeans.cu."""
+    k = _f32(keys)
+    n, d = (k.shape[0], k.shape[1]) if k.ndim == 2 else (0, 0)
+    C_, iters = int(n_buckets), int(iters)
+    if C_ < 1:
+        raise InvalidArgument("kmeans_train: need at least 1 bucket")
+    if n < C_:
+        raise InvalidArgument(f"kmeans_train: {n} keys cannot seed {C_} buckets")
+    if iters < 1:
+        raise InvalidArgument("kmeans_train: iters must be >= 1")
+    seeds = rng.sample_without_replacement(n, C_)
+    rng.shuffle(seeds)
+    ctx = ctx or default_context()
+    seeds = np.asarray(seeds, np.uint64)
+    cent = np.empty((C_, d), np.float32)
+    obj = np.empty(iters, np.float64)
+    zk, rep = C.c_uint64(0), C.c_uint64(0)
+    _check(lib().saap_kmeans_train(ctx.h, _p(k), _u64(n), _u64(d), _u64(C_), _u64(iters),
+                                   _p(seeds), _p(cent), _p(obj), C.byref(zk), C.byref(rep)))
+    if stats is not None:
+        stats.objective_per_iter = obj.tolist()
+        stats.zero_vector_keys = int(zk.value)
+        stats.empty_cluster_repairs = int(rep.value)
+    return Partition(cent, ctx)
 
 
 # --------------------------------------------------------------------------

@@ -39,6 +39,18 @@ void launch_f32_to_bf16(const float* in, uint16_t* out, uint64_t n, cudaStream_t
 void launch_derope(const float* x, const double* cs, uint64_t rows, uint32_t D, float* out,
                    cudaStream_t st);
 void launch_debug_exp(const double* x, uint64_t n, double* y, cudaStream_t st);
+uint32_t km_dim_max(uint32_t D);
+void launch_km_assign(const float* keys, uint32_t n, uint32_t D, const float* cent, uint32_t C,
+                      uint32_t* assign, double* score, unsigned long long* zero_keys,
+                      cudaStream_t st);
+void launch_km_iteration_tail(const float* keys, uint32_t n, uint32_t D, uint32_t* assign,
+                              double* score, uint32_t* counts, uint32_t C,
+                              unsigned long long* repairs, cudaStream_t st);
+void launch_km_objective(const double* score, uint32_t n, double* out, cudaStream_t st);
+void launch_km_seed(const float* keys, uint32_t D, const uint64_t* seed_rows, uint32_t C,
+                    float* cent, cudaStream_t st);
+void launch_km_update(const float* keys, uint32_t D, const uint32_t* off, const uint32_t* idx,
+                      uint32_t C, float* cent, cudaStream_t st);
 struct TcTile {
     uint32_t group, lid0, count, part;
 };
@@ -1117,6 +1129,94 @@ int saap_build_ivf(saap_ctx* c, const uint32_t* assignment, uint64_t n, uint64_t
         sync(c);
         for (uint64_t i = 0; i <= C; ++i) off[i] = off32[i];
         for (uint64_t i = 0; i < n; ++i) idx[i] = idx32[i];
+    });
+}
+
+// kmeans_train(keys, C, iters, rng, stats)   partition.cpp:52-179.  The
+// caller's Rng draws the seed rows (sample_without_replacement then shuffle,
+// :80-82); everything after that runs on the device (kmeans.cu).
+int saap_kmeans_train(saap_ctx* c, const float* keys, uint64_t n, uint64_t d, uint64_t C,
+                      uint64_t iters, const uint64_t* seed_rows, float* centroids,
+                      double* objective_per_iter, uint64_t* zero_vector_keys,
+                      uint64_t* empty_cluster_repairs) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        if (C < 1) invalid("kmeans_train: need at least 1 bucket");
+        if (n < C)
+            invalid("kmeans_train: " + std::to_string(n) + " keys cannot seed " +
+                    std::to_string(C) + " buckets");
+        if (iters < 1) invalid("kmeans_train: iters must be >= 1");
+        need(keys, "kmeans_train: keys");
+        need(seed_rows, "kmeans_train: seed rows");
+        need(centroids, "kmeans_train: centroids");
+        if (d == 0 || km_dim_max((uint32_t)d) == 0)
+            unsupported("kmeans_train: unsupported key dim " + std::to_string(d));
+        if (n >= 0xFFFFFFFFull) unsupported("kmeans_train: more than 2^32-1 keys");
+        for (uint64_t i = 0; i < C; ++i)
+            if (seed_rows[i] >= n) invalid("kmeans_train: seed row out of range");
+        const cudaStream_t st = c->stream;
+        std::vector<GroupMeta> meta{GroupMeta{0, 0, (uint32_t)n, 0, 0, 0}};
+        std::vector<TileDesc> tiles;
+        std::vector<uint32_t> first;
+        build_tiles(meta, tiles, first);
+        const size_t nt = tiles.size();
+        size_t o = 0;
+        auto take = [&](size_t bytes) {
+            size_t r = o;
+            o += (bytes + 255) & ~size_t(255);
+            return r;
+        };
+        const size_t o_keys = take(n * d * 4), o_cent = take(C * d * 4), o_seed = take(C * 8),
+                     o_as = take(n * 4), o_sc = take(n * 8), o_cnt = take(C * 4),
+                     o_meta = take(sizeof(GroupMeta)), o_tiles = take(nt * sizeof(TileDesc)),
+                     o_first = take(first.size() * 4), o_hist = take(nt * C * 4),
+                     o_cA = take(2 * C * 4), o_off = take((C + 1) * 4), o_offA = take((C + 1) * 4),
+                     o_idx = take(n * 4), o_inv = take(n * 4), o_obj = take(iters * 8),
+                     o_ctr = take(16);
+        char* b = nullptr;
+        SAAP_CUDA(cudaMalloc(&b, o));
+        std::unique_ptr<char, void (*)(char*)> hold(b, [](char* p) { cudaFree(p); });
+        const float* dk = (const float*)(b + o_keys);
+        float* dc = (float*)(b + o_cent);
+        uint32_t* das = (uint32_t*)(b + o_as);
+        double* dsc = (double*)(b + o_sc);
+        uint32_t* dcnt = (uint32_t*)(b + o_cnt);
+        double* dobj = (double*)(b + o_obj);
+        unsigned long long* ctr = (unsigned long long*)(b + o_ctr);
+        h2d(b + o_keys, keys, n * d * 4, st);
+        h2d(b + o_seed, seed_rows, C * 8, st);
+        h2d(b + o_meta, meta.data(), sizeof(GroupMeta), st);
+        h2d(b + o_tiles, tiles.data(), nt * sizeof(TileDesc), st);
+        h2d(b + o_first, first.data(), first.size() * 4, st);
+        SAAP_CUDA(cudaMemsetAsync(ctr, 0, 16, st));
+        const uint32_t N = (uint32_t)n, D = (uint32_t)d, CC = (uint32_t)C;
+        launch_km_seed(dk, D, (const uint64_t*)(b + o_seed), CC, dc, st);
+        c->launches++;
+        for (uint64_t it = 0; it < iters; ++it) {
+            launch_km_assign(dk, N, D, dc, CC, das, dsc, it == 0 ? ctr : nullptr, st);
+            if (it > 0 && objective_per_iter) launch_km_objective(dsc, N, dobj + it - 1, st);
+            launch_km_iteration_tail(dk, N, D, das, dsc, dcnt, CC, ctr + 1, st);
+            launch_pack(32, (TileDesc*)(b + o_tiles), (uint32_t)nt, (uint32_t*)(b + o_first), 1,
+                        (GroupMeta*)(b + o_meta), das, CC, (uint32_t*)(b + o_hist),
+                        (uint32_t*)(b + o_cA), (uint32_t*)(b + o_off), (uint32_t*)(b + o_offA),
+                        (uint32_t*)(b + o_idx), (uint32_t*)(b + o_inv), nullptr, nullptr, n,
+                        nullptr, nullptr, nullptr, nullptr, nullptr, st);
+            launch_km_update(dk, D, (const uint32_t*)(b + o_off), (const uint32_t*)(b + o_idx), CC,
+                             dc, st);
+            c->launches += 4 + 4 + (it > 0 && objective_per_iter ? 1 : 0);
+        }
+        if (objective_per_iter) {  // objective of the last update: one more scoring pass
+            launch_km_assign(dk, N, D, dc, CC, das, dsc, nullptr, st);
+            launch_km_objective(dsc, N, dobj + iters - 1, st);
+            c->launches += 2;
+        }
+        unsigned long long hc[2];
+        d2h(centroids, dc, C * d * 4, st);
+        d2h(hc, ctr, 16, st);
+        if (objective_per_iter) d2h(objective_per_iter, dobj, iters * 8, st);
+        sync(c);
+        if (zero_vector_keys) *zero_vector_keys = hc[0];
+        if (empty_cluster_repairs) *empty_cluster_repairs = hc[1];
     });
 }
 

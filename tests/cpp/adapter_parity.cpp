@@ -111,6 +111,28 @@ int main() {
     } catch (const std::invalid_argument& e) {
         check(std::string(e.what()).rfind("sparse_attention: probes", 0) == 0, "probes > C throws invalid_argument");
     }
+    // kmeans_train with the reference's own Rng and KMeansStats types
+    {
+        saap::TensorBlock tk = rows(p.keys_deroped, 1, 4097);
+        saap::Rng r1 = saap::Rng(spec.seed).child(2ull << 32), r2 = r1;
+        saap::KMeansStats s1, s2;
+        saap::Partition k1 = saap::kmeans_train(tk, 64, 4, r1, &s1);
+        auto k2 = saap_b200::kmeans_train(tk, 64, 4, r2, &s2);
+        check(std::memcmp(k1.centroids.data.data(), k2.centroids.data.data(),
+                          k1.centroids.data.size() * 4) == 0 &&
+                      s1.objective_per_iter == s2.objective_per_iter &&
+                      s1.empty_cluster_repairs == s2.empty_cluster_repairs &&
+                      r1.next_u64() == r2.next_u64(),
+              "kmeans_train bit-exact (saap::Rng, saap::KMeansStats)");
+        try {
+            saap::Rng r3(14);
+            saap_b200::kmeans_train(rows(tk, 0, 3), 4, 10, r3);
+            check(false, "kmeans_train throws with too few keys");
+        } catch (const std::invalid_argument& e) {
+            check(std::string(e.what()) == "kmeans_train: 3 keys cannot seed 4 buckets",
+                  "kmeans_train too few keys message");
+        }
+    }
     std::printf("%d failed\n", g_fail);
     return g_fail;
 }

@@ -109,3 +109,53 @@ def test_port_equals_live_reference_random():
             o1 = st.sparse_attention(rt, q, q, probes, 128, recent=recent)
             o2 = P.sparse_attention(q, keys, V, 1, off, idx, sel, probes, 128, recent)
             assert np.array_equal(o1[0], o2[0]) and o1[1:] == o2[1:]
+
+
+# ---------------------------------------------------------------- k-means host side
+KM_GOLD = os.path.join(os.path.dirname(__file__), "golden", "kmeans_small.npz")
+
+
+def test_rng_port_draws_reference_seed_rows():
+    """The host Rng mirror (paper_2502_08246_b200.Rng) draws exactly the seed
+    rows the reference's kmeans_train draws (tensor.cpp:90-168)."""
+    import paper_2502_08246_b200 as sb
+    g = np.load(KM_GOLD)
+    for name in g["names"]:
+        C, _, seed = (int(x) for x in g[f"{name}_cfg"])
+        n = g[f"{name}_keys"].shape[0]
+        rng = sb.Rng(seed)
+        s = rng.sample_without_replacement(n, C)
+        rng.shuffle(s)
+        assert s == g[f"{name}_seeds"].tolist(), name
+
+
+def test_rng_port_child_and_below():
+    import paper_2502_08246_b200 as sb
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    R = oracle.ref()
+    for seed, n, m in [(1, 10, 10), (99, 1 << 20, 7), (2 ** 63 + 5, 1000, 999)]:
+        rng = sb.Rng(seed)
+        s = rng.sample_without_replacement(n, m)
+        rng.shuffle(s)
+        assert s == R.kmeans_seed_rows(seed, n, m).tolist()
+    # train_head_partition's stream: Rng(seed).child(2 << 32)
+    keys = np.random.default_rng(0).normal(0, 1, (64, 8)).astype(np.float32)
+    _, _, _, _, nxt = R.kmeans_train_stats(keys, 4, 1, 5, stream=2 << 32)
+    rng = sb.Rng(5).child(2 << 32)
+    s = rng.sample_without_replacement(64, 4)
+    rng.shuffle(s)
+    assert rng.next_u64() == nxt
+
+
+def test_kmeans_golden_matches_live_reference():
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    R = oracle.ref()
+    g = np.load(KM_GOLD)
+    for name in g["names"]:
+        C, iters, seed = (int(x) for x in g[f"{name}_cfg"])
+        cent, obj, zk, rep, nxt = R.kmeans_train_stats(g[f"{name}_keys"], C, iters, seed)
+        assert np.array_equal(cent.view(np.uint32), g[f"{name}_cent"].view(np.uint32)), name
+        assert np.array_equal(obj.view(np.uint64), g[f"{name}_obj"].view(np.uint64)), name
+        assert [zk, rep, nxt] == g[f"{name}_stats"].tolist(), name
