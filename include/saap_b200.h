@@ -46,6 +46,7 @@ extern "C" {
 #define SAAP_ERR_CUDA 2             /* CUDA runtime / launch failure */
 #define SAAP_ERR_UNSUPPORTED 3      /* shape outside the kernels' envelope */
 #define SAAP_ERR_NO_DEVICE 4        /* no sm_100 device: no fallback exists */
+#define SAAP_ERR_IO 5               /* reference: saap::IoError; kind via saap_last_io_kind() */
 
 typedef struct saap_ctx saap_ctx;             /* device + stream + scratch */
 typedef struct saap_partition saap_partition; /* saap::Partition (partition.hpp:14-23) */
@@ -131,6 +132,33 @@ SAAP_API int saap_kmeans_train(saap_ctx* ctx, const float* keys, uint64_t n, uin
                       uint64_t n_buckets, uint64_t iters, const uint64_t* seed_rows,
                       float* centroids, double* objective_per_iter,
                       uint64_t* zero_vector_keys, uint64_t* empty_cluster_repairs);
+/* ---- SAAPTNS1 artifacts (tensor_io.hpp:14-47, partition.cpp:260-296,
+ * qmodel.cpp:530-589).  Host-only file I/O; loaded partitions / Q-models go
+ * straight to the device.  SAAP_ERR_IO carries the IoErrorKind
+ * (0 OpenFailed, 1 BadMagic, 2 BadVersion, 3 BadDtype, 4 BadShape,
+ * 5 Truncated); validation failures are SAAP_ERR_INVALID_ARGUMENT with the
+ * reference's message.  Readers take NULL outputs to query sizes. */
+SAAP_API int saap_last_io_kind(void);
+SAAP_API int saap_tensor_write(const char* path, const float* data, uint64_t rows, uint64_t dim);
+SAAP_API int saap_tensor_read(const char* path, float* out, uint64_t cap, uint64_t* rows,
+                              uint64_t* dim);
+SAAP_API int saap_u64_write(const char* path, const uint64_t* v, uint64_t n);
+SAAP_API int saap_u64_read(const char* path, uint64_t* out, uint64_t cap, uint64_t* n);
+/* partition_load(path): unit-norm check, then a device partition. */
+SAAP_API int saap_partition_load(saap_ctx* ctx, const char* path, saap_partition** out);
+/* ivf_load(off_path, idx_path): prefix-sum check. */
+SAAP_API int saap_ivf_load(const char* off_path, const char* idx_path, uint64_t* off,
+                           uint64_t off_cap, uint64_t* n_off, uint64_t* idx, uint64_t idx_cap,
+                           uint64_t* n_idx);
+/* qmodel_save / qmodel_load: params[8] in checkpoint order (w1 [d x h], b1,
+ * bn_gamma, bn_beta, bn_run_mean, bn_run_var [1 x h], w2 [h x C], b2 [1 x C]),
+ * fp64 in memory, f32 on disk.  saap_qmodel_read fills dims[3] = (d, h, C)
+ * and, when params (and its entries) are non-NULL, the widened parameters. */
+SAAP_API int saap_qmodel_save(const char* dir, uint64_t dim, uint64_t hidden, uint64_t n_buckets,
+                              const double* const* params);
+SAAP_API int saap_qmodel_read(const char* dir, uint64_t* dims, double* const* params);
+SAAP_API int saap_qmodel_load(saap_ctx* ctx, const char* dir, saap_qmodel** out);
+
 /* rope_remove_block(keys, positions, {dim, base})  rope.cpp:87-90 */
 SAAP_API int saap_rope_remove(saap_ctx* ctx, const float* x, uint64_t rows, uint64_t dim,
                      const uint64_t* positions, double base, float* out);

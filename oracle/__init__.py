@@ -292,6 +292,73 @@ class Ref:
         self._chk(self.lib.ref_kmeans_seed_rows(_u64(seed), _u64(n), _u64(m), _p(out)))
         return out
 
+    # ---- artifacts (tensor_io.cpp, partition.cpp:260-296, qmodel.cpp:530-589)
+    def _io(self, rc):
+        """-> None on success, else (status, io kind name or None, message)."""
+        if rc == 0:
+            return None
+        k = self.lib.ref_io_kind()
+        kinds = ("OpenFailed", "BadMagic", "BadVersion", "BadDtype", "BadShape", "Truncated")
+        return rc, (kinds[k] if k >= 0 else None), self.lib.ref_last_error().decode()
+
+    def tensor_write(self, t, path):
+        t = _f32(t)
+        return self._io(self.lib.ref_tensor_write(os.fspath(path).encode(), _p(t),
+                                                  _u64(t.shape[0]), _u64(t.shape[1])))
+
+    def tensor_read(self, path):
+        """-> (array or None, error or None)."""
+        r, d = C.c_uint64(), C.c_uint64()
+        e = self._io(self.lib.ref_tensor_read(os.fspath(path).encode(), None, _u64(0),
+                                              C.byref(r), C.byref(d)))
+        if e:
+            return None, e
+        out = np.empty((r.value, d.value), np.float32)
+        self.lib.ref_tensor_read(os.fspath(path).encode(), _p(out), _u64(out.size),
+                                 C.byref(r), C.byref(d))
+        return out, None
+
+    def u64_write(self, v, path):
+        v = np.ascontiguousarray(v, np.uint64)
+        return self._io(self.lib.ref_u64_write(os.fspath(path).encode(), _p(v), _u64(v.size)))
+
+    def u64_read(self, path):
+        n = C.c_uint64()
+        e = self._io(self.lib.ref_u64_read(os.fspath(path).encode(), None, _u64(0), C.byref(n)))
+        if e:
+            return None, e
+        out = np.empty(n.value, np.uint64)
+        self.lib.ref_u64_read(os.fspath(path).encode(), _p(out), _u64(out.size), C.byref(n))
+        return out, None
+
+    def partition_load(self, path):
+        Cb, d = C.c_uint64(), C.c_uint64()
+        e = self._io(self.lib.ref_partition_load(os.fspath(path).encode(), None, _u64(0),
+                                                 C.byref(Cb), C.byref(d)))
+        return e
+
+    def ivf_load(self, off_path, idx_path):
+        a, b = C.c_uint64(), C.c_uint64()
+        return self._io(self.lib.ref_ivf_load(os.fspath(off_path).encode(),
+                                              os.fspath(idx_path).encode(), C.byref(a), C.byref(b)))
+
+    def qmodel_save_init(self, dir_path, d, h, n_buckets, seed):
+        return self._io(self.lib.ref_qmodel_save_init(os.fspath(dir_path).encode(), _u64(d),
+                                                      _u64(h), _u64(n_buckets), _u64(seed)))
+
+    def qmodel_load(self, dir_path):
+        dims = (C.c_uint64 * 3)()
+        e = self._io(self.lib.ref_qmodel_load(os.fspath(dir_path).encode(), dims,
+                                              *([None] * 8)))
+        if e:
+            return None, e
+        d, h, Cb = dims
+        shapes = dict(w1=(d, h), w2=(h, Cb), b2=(1, Cb))
+        names = ("w1", "b1", "bn_gamma", "bn_beta", "bn_run_mean", "bn_run_var", "w2", "b2")
+        out = {k: np.empty(shapes.get(k, (1, h)), np.float64) for k in names}
+        self.lib.ref_qmodel_load(os.fspath(dir_path).encode(), dims, *[_p(out[k]) for k in names])
+        return out, None
+
     def assign_keys(self, keys, cent, threads=1):
         keys, cent = _f32(keys), _f32(cent)
         out = np.empty(keys.shape[0], np.uint32)

@@ -37,6 +37,7 @@
 #include "saap/rope.hpp"
 #include "saap/synthdata.hpp"
 #include "saap/tensor.hpp"
+#include "saap/tensor_io.hpp"
 
 using namespace saap;
 
@@ -475,3 +476,107 @@ int ref_sparse_attention_batch(std::uint64_t n_groups, void* const* stores,
 }
 
 } // extern "C"
+
+// ---------------------------------------------------------------- artifacts
+// tensor_io.cpp / partition.cpp:260-296 / qmodel.cpp:530-589.  ref_io_kind()
+// is the IoErrorKind of the last IoError (-1 otherwise).
+namespace {
+thread_local int g_io_kind = -1;
+template <typename F>
+int io_guard(F&& f) {
+    g_io_kind = -1;
+    try {
+        f();
+        return 0;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        g_io_kind = static_cast<int>(e.kind());
+        return 3;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+}  // namespace
+
+extern "C" {
+int ref_io_kind() { return g_io_kind; }
+
+int ref_tensor_write(const char* path, const float* data, std::uint64_t rows, std::uint64_t dim) {
+    return io_guard([&] { tensor_write(block(data, rows, dim), path); });
+}
+
+int ref_tensor_read(const char* path, float* out, std::uint64_t cap, std::uint64_t* rows,
+                    std::uint64_t* dim) {
+    return io_guard([&] {
+        TensorBlock t = tensor_read(path);
+        *rows = t.rows;
+        *dim = t.dim;
+        if (out && cap >= t.data.size()) put(t, out);
+    });
+}
+
+int ref_u64_write(const char* path, const std::uint64_t* v, std::uint64_t n) {
+    return io_guard([&] { u64_write(std::vector<std::uint64_t>(v, v + n), path); });
+}
+
+int ref_u64_read(const char* path, std::uint64_t* out, std::uint64_t cap, std::uint64_t* n) {
+    return io_guard([&] {
+        auto v = u64_read(path);
+        *n = v.size();
+        if (out && cap >= v.size()) std::copy(v.begin(), v.end(), out);
+    });
+}
+
+int ref_partition_load(const char* path, float* out, std::uint64_t cap, std::uint64_t* C,
+                       std::uint64_t* d) {
+    return io_guard([&] {
+        Partition p = partition_load(path);
+        *C = p.n_buckets();
+        *d = p.dim();
+        if (out && cap >= p.centroids.data.size()) put(p.centroids, out);
+    });
+}
+
+int ref_ivf_load(const char* off_path, const char* idx_path, std::uint64_t* n_off,
+                 std::uint64_t* n_idx) {
+    return io_guard([&] {
+        IVFIndex ix = ivf_load(off_path, idx_path);
+        *n_off = ix.off.size();
+        *n_idx = ix.idx.size();
+    });
+}
+
+// qmodel_save of qmodel_init(d, h, C, Rng(seed)) (the params come back via
+// ref_qmodel_init with the same seed).
+int ref_qmodel_save_init(const char* dir, std::uint64_t d, std::uint64_t h, std::uint64_t C,
+                         std::uint64_t seed) {
+    return io_guard([&] {
+        Rng rng(seed);
+        qmodel_save(qmodel_init(d, h, C, rng), dir);
+    });
+}
+
+int ref_qmodel_load(const char* dir, std::uint64_t* dims, double* w1, double* b1, double* gamma,
+                    double* beta, double* mean, double* var, double* w2, double* b2) {
+    return io_guard([&] {
+        QModel m = qmodel_load(dir);
+        dims[0] = m.dim();
+        dims[1] = m.hidden();
+        dims[2] = m.n_buckets();
+        if (!w1) return;
+        auto cp = [](const Mat& s, double* o) { std::copy(s.data.begin(), s.data.end(), o); };
+        cp(m.w1, w1);
+        cp(m.b1, b1);
+        cp(m.bn_gamma, gamma);
+        cp(m.bn_beta, beta);
+        cp(m.bn_run_mean, mean);
+        cp(m.bn_run_var, var);
+        cp(m.w2, w2);
+        cp(m.b2, b2);
+    });
+}
+}  // extern "C"

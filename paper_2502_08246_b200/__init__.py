@@ -10,6 +10,8 @@ and error behaviour (``std::invalid_argument`` -> :class:`InvalidArgument`, a
 reference (proj/core)      here
 =========================  ==================================================
 kmeans_train / Rng         :func:`kmeans_train` / :class:`Rng` (partition.cpp:52-179)
+tensor_read/_write, u64_*  :func:`tensor_read` ... (tensor_io.cpp:104-152)
+partition_/ivf_/qmodel_ load/save  (partition.cpp:260-296, qmodel.cpp:530-589)
 assign_keys                :func:`assign_keys`  (partition.cpp:191-198)
 build_ivf                  :func:`build_ivf`    (partition.cpp:200-223)
 rope_remove_block          :func:`rope_remove_block` (rope.cpp:87-90)
@@ -38,7 +40,8 @@ _DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_DIR, "libsaap_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_DIR), "include", "saap_b200.h")
 
-SAAP_OK, SAAP_ERR_INVALID_ARGUMENT, SAAP_ERR_CUDA, SAAP_ERR_UNSUPPORTED, SAAP_ERR_NO_DEVICE = range(5)
+(SAAP_OK, SAAP_ERR_INVALID_ARGUMENT, SAAP_ERR_CUDA, SAAP_ERR_UNSUPPORTED, SAAP_ERR_NO_DEVICE,
+ SAAP_ERR_IO) = range(6)
 
 
 class SaapError(RuntimeError):
@@ -56,6 +59,18 @@ class Unsupported(SaapError):
 
 class NoDevice(SaapError):
     code = SAAP_ERR_NO_DEVICE
+
+
+IO_KINDS = ("OpenFailed", "BadMagic", "BadVersion", "BadDtype", "BadShape", "Truncated")
+
+
+class IoError(RuntimeError):
+    """saap::IoError (tensor_io.hpp:18-38); ``kind`` is the IoErrorKind name."""
+    code = SAAP_ERR_IO
+
+    def __init__(self, msg, kind):
+        super().__init__(msg)
+        self.kind = kind
 
 
 _lib = None
@@ -84,6 +99,8 @@ def _check(rc):
         raise Unsupported(msg)
     if rc == SAAP_ERR_NO_DEVICE:
         raise NoDevice(msg)
+    if rc == SAAP_ERR_IO:
+        raise IoError(msg, IO_KINDS[lib().saap_last_io_kind()])
     raise SaapError(msg)
 
 
@@ -364,6 +381,93 @@ def batched_bucket_select(model: QModel, query_group, l) -> np.ndarray:
     _check(lib().saap_batched_bucket_select(model.ctx.h, model.h, _p(q), _u64(q.shape[0]),
                                             _u64(q.shape[1]), _u64(l), _p(out)))
     return out
+
+
+# --------------------------------------------------------------------------
+# SAAPTNS1 artifacts (tensor_io.hpp:14-47; partition.cpp:260-296;
+# qmodel.cpp:530-589) through the library's host-side readers/writers.
+def _path(p):
+    return os.fspath(p).encode()
+
+
+def tensor_write(t, path) -> None:
+    a = _f32(t)
+    if a.ndim != 2:
+        raise InvalidArgument("tensor_write: expected a 2-d block")
+    _check(lib().saap_tensor_write(_path(path), _p(a), _u64(a.shape[0]), _u64(a.shape[1])))
+
+
+def tensor_read(path) -> np.ndarray:
+    r, d = C.c_uint64(), C.c_uint64()
+    _check(lib().saap_tensor_read(_path(path), None, _u64(0), C.byref(r), C.byref(d)))
+    out = np.empty((r.value, d.value), np.float32)
+    _check(lib().saap_tensor_read(_path(path), _p(out), _u64(out.size), C.byref(r), C.byref(d)))
+    return out
+
+
+def u64_write(v, path) -> None:
+    a = np.ascontiguousarray(v, dtype=np.uint64)
+    _check(lib().saap_u64_write(_path(path), _p(a), _u64(a.size)))
+
+
+def u64_read(path) -> np.ndarray:
+    n = C.c_uint64()
+    _check(lib().saap_u64_read(_path(path), None, _u64(0), C.byref(n)))
+    out = np.empty(n.value, np.uint64)
+    _check(lib().saap_u64_read(_path(path), _p(out), _u64(out.size), C.byref(n)))
+    return out
+
+
+def partition_save(p, path) -> None:
+    tensor_write(p.centroids if isinstance(p, Partition) else p, path)
+
+
+def partition_load(path, ctx: Optional[Context] = None) -> "Partition":
+    """Unit-norm check (1e-5) in the library, then a device partition."""
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    _check(lib().saap_partition_load(ctx.h, _path(path), C.byref(h)))
+    p = Partition.__new__(Partition)
+    p.ctx, p.h, p.centroids = ctx, h, tensor_read(path)
+    return p
+
+
+def ivf_save(ix, off_path, idx_path) -> None:
+    u64_write(ix.off, off_path)
+    u64_write(ix.idx, idx_path)
+
+
+def ivf_load(off_path, idx_path) -> "IVFIndex":
+    no, ni = C.c_uint64(), C.c_uint64()
+    _check(lib().saap_ivf_load(_path(off_path), _path(idx_path), None, _u64(0), C.byref(no),
+                               None, _u64(0), C.byref(ni)))
+    off, idx = np.empty(no.value, np.uint64), np.empty(ni.value, np.uint64)
+    _check(lib().saap_ivf_load(_path(off_path), _path(idx_path), _p(off), _u64(off.size),
+                               C.byref(no), _p(idx), _u64(idx.size), C.byref(ni)))
+    return IVFIndex(off, idx)
+
+
+def qmodel_save(params, dir_path) -> None:
+    ps = params.params if isinstance(params, QModel) else {k: _f64(params[k]) for k in QMODEL_FIELDS}
+    d, h = ps["w1"].shape
+    arr = (C.c_void_p * 8)(*[_p(ps[k]).value for k in QMODEL_FIELDS])
+    _check(lib().saap_qmodel_save(_path(dir_path), _u64(d), _u64(h), _u64(ps["w2"].shape[1]), arr))
+
+
+def qmodel_read(dir_path) -> dict:
+    """The checkpoint's parameters, widened to fp64 (host only)."""
+    dims = (C.c_uint64 * 3)()
+    _check(lib().saap_qmodel_read(_path(dir_path), dims, None))
+    d, h, Cb = dims
+    shapes = dict(w1=(d, h), w2=(h, Cb), b2=(1, Cb))
+    out = {k: np.empty(shapes.get(k, (1, h)), np.float64) for k in QMODEL_FIELDS}
+    arr = (C.c_void_p * 8)(*[_p(out[k]).value for k in QMODEL_FIELDS])
+    _check(lib().saap_qmodel_read(_path(dir_path), dims, arr))
+    return out
+
+
+def qmodel_load(dir_path, ctx: Optional[Context] = None) -> "QModel":
+    return QModel(qmodel_read(dir_path), ctx)
 
 
 # --------------------------------------------------------------------------
