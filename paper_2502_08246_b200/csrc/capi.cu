@@ -1059,11 +1059,24 @@ int saap_assign_keys(saap_ctx* c, const saap_partition* p, const float* keys, ui
         if (d != p->d)
             invalid("assign_key: key dim " + std::to_string(d) + " does not match centroids " +
                     std::to_string(p->C) + "x" + std::to_string(p->d));
-        if (!supported_dim(d)) unsupported("assign_keys: unsupported key dim " + std::to_string(d));
+        if (!supported_dim(d) && km_dim_max((uint32_t)d) == 0)
+            unsupported("assign_keys: unsupported key dim " + std::to_string(d));
         if (n == 0) return;
         const cudaStream_t st = c->stream;
         float* dk = (float*)ensure(c, c->qr, n * d * 4);
         h2d(dk, keys, n * d * 4, st);
+        if (!supported_dim(d)) {  // other dims <= 128: the k-means scorer (same best_bucket)
+            if (n >= 0xFFFFFFFFull) unsupported("assign_keys: more than 2^32-1 keys");
+            char* b = (char*)ensure(c, c->misc, n * 12 + 256);
+            uint32_t* dout = (uint32_t*)b;
+            double* dsc = (double*)(b + ((n * 4 + 255) & ~size_t(255)));
+            launch_km_assign(dk, (uint32_t)n, (uint32_t)d, p->cent, (uint32_t)p->C, dout, dsc,
+                             nullptr, st);
+            c->launches++;
+            d2h(out, dout, n * 4, st);
+            sync(c);
+            return;
+        }
         std::vector<GroupMeta> meta{GroupMeta{0, 0, (uint32_t)n, 0, 0, 0}};
         std::vector<TileDesc> tiles;
         std::vector<uint32_t> first;

@@ -17,7 +17,9 @@ CASES = [(131071, 128, 1024, 10), (1048575, 128, 4096, 3), (1048575, 128, 16384,
 def main():
     ctx = sb.default_context()
     r = np.random.default_rng(0)
-    for n, d, C, iters in CASES:
+    sel = os.environ.get("KM_CASES")
+    cases = [CASES[int(i)] for i in sel.split(",")] if sel else CASES
+    for n, d, C, iters in cases:
         cen = r.normal(0, 1, (256, d)).astype(np.float32)
         keys = (cen[r.integers(0, 256, n)] * 2 + r.normal(0, 1, (n, d))).astype(np.float32)
         sb.kmeans_train(keys[:4096], 64, 1, sb.Rng(1), ctx=ctx)  # warm the module

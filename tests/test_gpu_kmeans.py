@@ -81,3 +81,19 @@ def test_kmeans_live_reference_head_keys(ctx, n, d, C, iters, drift):
     assert np.array_equal(_bits(np.array(st.objective_per_iter)), _bits(obj))
     assert (st.zero_vector_keys, st.empty_cluster_repairs) == (zk, rep)
     assert rng.next_u64() == nxt
+
+
+@pytest.mark.parametrize("d", [2, 3, 16, 100])
+def test_assign_keys_other_dims(ctx, d):
+    """assign_keys for head dims outside the decode kernels' {32, 64, 128}
+    (the reference's partition tests use d = 2..8): exact best_bucket."""
+    import paper_2502_08246_b200 as sb
+    r = np.random.default_rng(d)
+    cent = r.normal(0, 1, (37, d)).astype(np.float32)
+    cent /= np.linalg.norm(cent, axis=1, keepdims=True)
+    keys = r.normal(0, 1, (5000, d)).astype(np.float32)
+    keys[7] = 0.0
+    keys[11] = cent[5] * 2  # exact positive scaling: its own bucket
+    got = sb.assign_keys(keys, sb.Partition(cent, ctx))
+    assert np.array_equal(got, oracle.port().assign_keys(keys, cent))
+    assert got[7] == 0 and got[11] == 5
