@@ -54,6 +54,7 @@ typedef struct saap_qmodel saap_qmodel;       /* saap::QModel (qmodel.hpp:15-28)
 typedef struct saap_router saap_router;       /* saap::BucketRouter (attention.hpp:102-108) */
 typedef struct saap_layer saap_layer;         /* n_groups ContextStores (attention.hpp:76-86) */
 typedef struct saap_graph saap_graph;         /* captured decode step (CUDA graph) */
+typedef struct saap_qtrainer saap_qtrainer;   /* QModel + TrainerState (qmodel.hpp:66-75) */
 
 /* saap::SparseAttnConfig (attention.hpp:21-25) with DenseWindow (:16-19). */
 typedef struct {
@@ -158,6 +159,28 @@ SAAP_API int saap_qmodel_save(const char* dir, uint64_t dim, uint64_t hidden, ui
                               const double* const* params);
 SAAP_API int saap_qmodel_read(const char* dir, uint64_t* dims, double* const* params);
 SAAP_API int saap_qmodel_load(saap_ctx* ctx, const char* dir, saap_qmodel** out);
+
+/* ---- Q-model training on the device (qmodel.cpp:227-433), bit-exact
+ * parameters.  params[8] in checkpoint order (see saap_qmodel_save);
+ * hyper[5] = (lr, beta1, beta2, eps, bn_momentum) or NULL for the
+ * TrainerState defaults; Adam moments start at zero (state.m empty). */
+SAAP_API int saap_qtrainer_create(saap_ctx* ctx, uint64_t dim, uint64_t hidden, uint64_t n_buckets,
+                                  const double* const* params, const double* hyper, uint64_t step,
+                                  saap_qtrainer** out);
+SAAP_API int saap_qtrainer_destroy(saap_qtrainer* t);
+/* train_step_on_target(model, state, queries_deroped [n x dim] f32,
+ * target [n x C] fp64) -> pre-step loss (kl_loss with CUDA log: within
+ * 1e-12 relative of glibc's).  Throws (SAAP_ERR_CUDA, "train_step:
+ * non-finite loss at step k") before touching the state, like the reference. */
+SAAP_API int saap_qtrainer_step(saap_ctx* ctx, saap_qtrainer* t, const float* q, uint64_t n,
+                                uint64_t dim, const double* target, double* loss);
+SAAP_API int saap_qtrainer_read(saap_ctx* ctx, const saap_qtrainer* t, double* const* params,
+                                uint64_t* step);
+/* attention_target_rows(q_roped [n x dim], keys_roped [n_keys x dim],
+ * assignment, C) -> [n x C] fp64 (qmodel.cpp:384-407), bit-exact. */
+SAAP_API int saap_attention_target(saap_ctx* ctx, const float* q_roped, uint64_t n, uint64_t dim,
+                                   const float* keys_roped, uint64_t n_keys,
+                                   const uint32_t* assignment, uint64_t n_buckets, double* out);
 
 /* rope_remove_block(keys, positions, {dim, base})  rope.cpp:87-90 */
 SAAP_API int saap_rope_remove(saap_ctx* ctx, const float* x, uint64_t rows, uint64_t dim,

@@ -359,6 +359,30 @@ class Ref:
         self.lib.ref_qmodel_load(os.fspath(dir_path).encode(), dims, *[_p(out[k]) for k in names])
         return out, None
 
+    def qtrain_steps(self, params, lr, q_batches, targets):
+        """K reference train_step_on_target calls -> (new params, losses)."""
+        names = ("w1", "b1", "bn_gamma", "bn_beta", "bn_run_mean", "bn_run_var", "w2", "b2")
+        ps = {k: np.array(params[k], np.float64, copy=True) for k in names}
+        d, h = ps["w1"].shape
+        Cb = ps["w2"].shape[1]
+        q = _f32(q_batches)
+        t = _f64(targets)
+        K, n = q.shape[0], q.shape[1]
+        losses = np.empty(K, np.float64)
+        self._chk(self.lib.ref_qtrain_steps(_u64(d), _u64(h), _u64(Cb), *[_p(ps[k]) for k in names],
+                                            C.c_double(lr), _u64(K), _u64(n), _p(q), _p(t),
+                                            _p(losses)))
+        return ps, losses
+
+    def attention_target(self, q, keys, assignment, n_buckets):
+        q, keys = _f32(q), _f32(keys)
+        a = np.ascontiguousarray(assignment, np.uint32)
+        out = np.empty((q.shape[0], n_buckets), np.float64)
+        self._chk(self.lib.ref_attention_target(_p(q), _u64(q.shape[0]), _u64(q.shape[1]),
+                                                _p(keys), _u64(keys.shape[0]), _p(a),
+                                                _u64(n_buckets), _p(out)))
+        return out
+
     def assign_keys(self, keys, cent, threads=1):
         keys, cent = _f32(keys), _f32(cent)
         out = np.empty(keys.shape[0], np.uint32)

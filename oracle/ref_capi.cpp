@@ -580,3 +580,45 @@ int ref_qmodel_load(const char* dir, std::uint64_t* dims, double* w1, double* b1
     });
 }
 }  // extern "C"
+
+// ---------------------------------------------------------------- Q-model training
+extern "C" {
+// K train_step_on_target calls (qmodel.cpp:419-433) from the given params
+// (checkpoint order) with TrainerState{lr, ...defaults}; batches q [K][n x d]
+// f32 and targets [K][n x C] fp64.  Params are updated in place; losses [K].
+int ref_qtrain_steps(std::uint64_t d, std::uint64_t h, std::uint64_t C, double* w1, double* b1,
+                     double* gamma, double* beta, double* mean, double* var, double* w2,
+                     double* b2, double lr, std::uint64_t K, std::uint64_t n, const float* q,
+                     const double* targets, double* losses) {
+    return guard([&] {
+        QModel m = make_qmodel(d, h, C, w1, b1, gamma, beta, mean, var, w2, b2);
+        TrainerState st;
+        st.lr = lr;
+        for (std::uint64_t k = 0; k < K; ++k) {
+            TensorBlock qb = block(q + k * n * d, n, d);
+            Mat t = mat(targets + k * n * C, n, C);
+            losses[k] = train_step_on_target(m, st, qb, t);
+        }
+        auto cp = [](const Mat& s, double* o) { std::copy(s.data.begin(), s.data.end(), o); };
+        cp(m.w1, w1);
+        cp(m.b1, b1);
+        cp(m.bn_gamma, gamma);
+        cp(m.bn_beta, beta);
+        cp(m.bn_run_mean, mean);
+        cp(m.bn_run_var, var);
+        cp(m.w2, w2);
+        cp(m.b2, b2);
+    });
+}
+
+int ref_attention_target(const float* q, std::uint64_t n, std::uint64_t d, const float* keys,
+                         std::uint64_t n_keys, const std::uint32_t* assignment, std::uint64_t C,
+                         double* out) {
+    return guard([&] {
+        KeyAssignment a;
+        a.bucket_of.assign(assignment, assignment + n_keys);
+        Mat t = attention_target_rows(block(q, n, d), block(keys, n_keys, d), a, C);
+        std::copy(t.data.begin(), t.data.end(), out);
+    });
+}
+}  // extern "C"

@@ -11,6 +11,8 @@ reference (proj/core)      here
 =========================  ==================================================
 kmeans_train / Rng         :func:`kmeans_train` / :class:`Rng` (partition.cpp:52-179)
 tensor_read/_write, u64_*  :func:`tensor_read` ... (tensor_io.cpp:104-152)
+train_step_on_target       :class:`QModelTrainer` (qmodel.cpp:227-433)
+attention_target_rows      :func:`attention_target_rows` (qmodel.cpp:384-407)
 partition_/ivf_/qmodel_ load/save  (partition.cpp:260-296, qmodel.cpp:530-589)
 assign_keys                :func:`assign_keys`  (partition.cpp:191-198)
 build_ivf                  :func:`build_ivf`    (partition.cpp:200-223)
@@ -468,6 +470,86 @@ def qmodel_read(dir_path) -> dict:
 
 def qmodel_load(dir_path, ctx: Optional[Context] = None) -> "QModel":
     return QModel(qmodel_read(dir_path), ctx)
+
+
+# --------------------------------------------------------------------------
+@dataclass
+class TrainerState:
+    """saap::TrainerState hyper-parameters (qmodel.hpp:66-75)."""
+    lr: float = 1e-5
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    bn_momentum: float = 0.9
+    step: int = 0
+
+
+class QModelTrainer:
+    """QModel + TrainerState resident on the device (qtrain.cu).
+    ``train_step_on_target`` is the reference's (qmodel.cpp:419-433) with
+    bit-identical parameters after every step; ``params()`` reads them back
+    in checkpoint order; ``qmodel()`` hands them to the router."""
+
+    def __init__(self, params: dict, state: Optional[TrainerState] = None,
+                 ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.state = state or TrainerState()
+        ps = [_f64(params[k]) for k in QMODEL_FIELDS]
+        self.d, self.hidden = ps[0].shape
+        self.C = ps[6].shape[1]
+        arr = (C.c_void_p * 8)(*[_p(x).value for x in ps])
+        st = self.state
+        hyper = np.array([st.lr, st.beta1, st.beta2, st.eps, st.bn_momentum], np.float64)
+        h = C.c_void_p()
+        _check(lib().saap_qtrainer_create(self.ctx.h, _u64(self.d), _u64(self.hidden),
+                                          _u64(self.C), arr, _p(hyper), _u64(st.step),
+                                          C.byref(h)))
+        self.h = h
+
+    def train_step_on_target(self, queries_deroped, target) -> float:
+        q = _f32(queries_deroped)
+        t = _f64(target)
+        if t.shape != (q.shape[0], self.C):
+            raise InvalidArgument(f"kl_loss: pred {q.shape[0]}x{self.C} vs target "
+                                  f"{t.shape[0]}x{t.shape[1] if t.ndim > 1 else 0}")
+        loss = C.c_double()
+        _check(lib().saap_qtrainer_step(self.ctx.h, self.h, _p(q), _u64(q.shape[0]),
+                                        _u64(q.shape[1]), _p(t), C.byref(loss)))
+        self.state.step += 1
+        return loss.value
+
+    def params(self) -> dict:
+        out = {"w1": np.empty((self.d, self.hidden)), "w2": np.empty((self.hidden, self.C)),
+               "b2": np.empty((1, self.C))}
+        for k in QMODEL_FIELDS:
+            out.setdefault(k, np.empty((1, self.hidden)))
+        arr = (C.c_void_p * 8)(*[_p(out[k]).value for k in QMODEL_FIELDS])
+        step = C.c_uint64()
+        _check(lib().saap_qtrainer_read(self.ctx.h, self.h, arr, C.byref(step)))
+        return out
+
+    def qmodel(self) -> "QModel":
+        return QModel(self.params(), self.ctx)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().saap_qtrainer_destroy(self.h)
+            self.h = None
+
+
+def attention_target_rows(queries_roped, keys_roped, assignment, n_buckets,
+                          ctx: Optional[Context] = None) -> np.ndarray:
+    """Per-bucket attention mass (qmodel.cpp:384-407), fp64, bit-exact."""
+    ctx = ctx or default_context()
+    q, k = _f32(queries_roped), _f32(keys_roped)
+    a = np.ascontiguousarray(assignment, np.uint32)
+    if a.size != k.shape[0]:
+        raise InvalidArgument(f"attention_target: assignment covers {a.size} keys, block has "
+                              f"{k.shape[0]}")
+    out = np.empty((q.shape[0], int(n_buckets)), np.float64)
+    _check(lib().saap_attention_target(ctx.h, _p(q), _u64(q.shape[0]), _u64(q.shape[1]), _p(k),
+                                       _u64(k.shape[0]), _p(a), _u64(n_buckets), _p(out)))
+    return out
 
 
 # --------------------------------------------------------------------------

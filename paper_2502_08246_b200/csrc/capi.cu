@@ -40,6 +40,11 @@ void launch_derope(const float* x, const double* cs, uint64_t rows, uint32_t D, 
                    cudaStream_t st);
 void launch_debug_exp(const double* x, uint64_t n, double* y, cudaStream_t st);
 uint32_t km_dim_max(uint32_t D);
+void qtrain_forward(saap_qtrainer* t, uint32_t n, cudaStream_t st);
+void qtrain_update(saap_qtrainer* t, uint32_t n, cudaStream_t st);
+void launch_attention_target(const float* q, uint32_t n, uint32_t d, const float* K,
+                             uint32_t n_keys, const uint32_t* assign, uint32_t C, double* a,
+                             double* out, cudaStream_t st);
 void launch_km_assign(const float* keys, uint32_t n, uint32_t D, const float* cent, uint32_t C,
                       uint32_t* assign, double* score, unsigned long long* zero_keys,
                       cudaStream_t st);
@@ -1230,6 +1235,166 @@ int saap_kmeans_train(saap_ctx* c, const float* keys, uint64_t n, uint64_t d, ui
         sync(c);
         if (zero_vector_keys) *zero_vector_keys = hc[0];
         if (empty_cluster_repairs) *empty_cluster_repairs = hc[1];
+    });
+}
+
+// ---------------------------------------------------------------- Q-model training
+// TrainerState + QModel on the device (qmodel.hpp:66-75, qtrain.cu).
+int saap_qtrainer_create(saap_ctx* c, uint64_t d, uint64_t h, uint64_t C,
+                         const double* const* params, const double* hyper, uint64_t step,
+                         saap_qtrainer** out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(out, "qtrainer: out");
+        need(params, "qtrainer: params");
+        if (d == 0 || h == 0 || C == 0) invalid("qmodel_init: zero dimension");
+        auto* t = new saap_qtrainer();
+        std::unique_ptr<saap_qtrainer> hold(t);
+        t->ctx = c;
+        t->d = d;
+        t->h = h;
+        t->C = C;
+        if (hyper) {
+            t->lr = hyper[0];
+            t->beta1 = hyper[1];
+            t->beta2 = hyper[2];
+            t->eps = hyper[3];
+            t->bn_momentum = hyper[4];
+        }
+        t->step = step;
+        const uint64_t cnt[8] = {d * h, h, h, h, h, h, h * C, C};
+        for (int k = 0; k < 8; ++k) {
+            need(params[k], "qtrainer: parameter");
+            t->p[k] = dmalloc<double>(cnt[k]);
+            t->m[k] = dmalloc<double>(cnt[k]);
+            t->v[k] = dmalloc<double>(cnt[k]);
+            t->g[k] = dmalloc<double>(cnt[k]);
+            SAAP_CUDA(cudaMemcpy(t->p[k], params[k], cnt[k] * 8, cudaMemcpyHostToDevice));
+            SAAP_CUDA(cudaMemset(t->m[k], 0, cnt[k] * 8));
+            SAAP_CUDA(cudaMemset(t->v[k], 0, cnt[k] * 8));
+        }
+        t->mean = dmalloc<double>(h);
+        t->var = dmalloc<double>(h);
+        t->w2T = dmalloc<double>(h * C);
+        t->loss = dmalloc<double>(1);
+        *out = hold.release();
+    });
+}
+
+static void qtrainer_free_acts(saap_qtrainer* t) {
+    for (double** a : {&t->x, &t->z, &t->xhat, &t->y, &t->r, &t->pr, &t->tgt, &t->dl, &t->dy,
+                       &t->dz, &t->loss_rows})
+        dfree(*a);
+    dfree(t->q32);
+    t->n_cap = 0;
+}
+
+int saap_qtrainer_destroy(saap_qtrainer* t) {
+    return guard([&] {
+        if (!t) return;
+        cudaSetDevice(t->ctx->device);
+        qtrainer_free_acts(t);
+        for (int k = 0; k < 8; ++k) {
+            dfree(t->p[k]);
+            dfree(t->m[k]);
+            dfree(t->v[k]);
+            dfree(t->g[k]);
+        }
+        dfree(t->mean);
+        dfree(t->var);
+        dfree(t->w2T);
+        dfree(t->loss);
+        delete t;
+    });
+}
+
+// train_step_on_target(model, state, queries_deroped, target)  qmodel.cpp:419-433
+int saap_qtrainer_step(saap_ctx* c, saap_qtrainer* t, const float* q, uint64_t n, uint64_t d,
+                       const double* target, double* loss) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(t, "qtrainer");
+        if (d != t->d)
+            invalid("qmodel: query dim " + std::to_string(d) + " does not match model dim " +
+                    std::to_string(t->d));
+        if (n == 0) invalid("qmodel: empty query batch");
+        if (n < 2) invalid("qmodel: train-mode forward needs >= 2 rows for batch stats");
+        need(q, "qtrainer: queries");
+        need(target, "qtrainer: target");
+        const cudaStream_t st = c->stream;
+        if (n > t->n_cap) {
+            SAAP_CUDA(cudaStreamSynchronize(st));
+            qtrainer_free_acts(t);
+            const uint64_t h = t->h, C = t->C;
+            t->x = dmalloc<double>(n * t->d);
+            for (double** a : {&t->z, &t->xhat, &t->y, &t->r, &t->dy, &t->dz}) *a = dmalloc<double>(n * h);
+            for (double** a : {&t->pr, &t->tgt, &t->dl}) *a = dmalloc<double>(n * C);
+            t->loss_rows = dmalloc<double>(n);
+            t->q32 = dmalloc<float>(n * t->d);
+            t->n_cap = n;
+        }
+        h2d(t->q32, q, n * d * 4, st);
+        h2d(t->tgt, target, n * t->C * 8, st);
+        qtrain_forward(t, (uint32_t)n, st);
+        double l = 0;
+        d2h(&l, t->loss, 8, st);
+        sync(c);
+        c->launches += 6;
+        if (!std::isfinite(l))
+            fail(SAAP_ERR_CUDA, "train_step: non-finite loss at step " + std::to_string(t->step + 1));
+        qtrain_update(t, (uint32_t)n, st);
+        c->launches += 14;
+        if (loss) *loss = l;
+        sync(c);
+    });
+}
+
+int saap_qtrainer_read(saap_ctx* c, const saap_qtrainer* t, double* const* params, uint64_t* step) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(t, "qtrainer");
+        const uint64_t d = t->d, h = t->h, C = t->C;
+        const uint64_t cnt[8] = {d * h, h, h, h, h, h, h * C, C};
+        if (params)
+            for (int k = 0; k < 8; ++k)
+                if (params[k]) d2h(params[k], t->p[k], cnt[k] * 8, c->stream);
+        sync(c);
+        if (step) *step = t->step;
+    });
+}
+
+// attention_target_rows(q_roped, keys_roped, assignment, C)  qmodel.cpp:384-407
+int saap_attention_target(saap_ctx* c, const float* q, uint64_t n, uint64_t d, const float* keys,
+                          uint64_t n_keys, const uint32_t* assignment, uint64_t C, double* out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        if (n_keys == 0) invalid("attention_target: empty key set");
+        for (uint64_t k = 0; k < n_keys; ++k)
+            if (assignment[k] >= C) invalid("attention_target: bucket id out of range");
+        if (n == 0) return;
+        if (C * 8 > 200 * 1024) unsupported("attention_target: more than 25600 buckets");
+        const cudaStream_t st = c->stream;
+        size_t o = 0;
+        auto take = [&](size_t bytes) {
+            size_t r = o;
+            o += (bytes + 255) & ~size_t(255);
+            return r;
+        };
+        const size_t o_q = take(n * d * 4), o_k = take(n_keys * d * 4), o_as = take(n_keys * 4),
+                     o_a = take(n * n_keys * 8), o_out = take(n * C * 8);
+        char* b = nullptr;
+        SAAP_CUDA(cudaMalloc(&b, o));
+        std::unique_ptr<char, void (*)(char*)> hold(b, [](char* p) { cudaFree(p); });
+        h2d(b + o_q, q, n * d * 4, st);
+        h2d(b + o_k, keys, n_keys * d * 4, st);
+        h2d(b + o_as, assignment, n_keys * 4, st);
+        launch_attention_target((const float*)(b + o_q), (uint32_t)n, (uint32_t)d,
+                                (const float*)(b + o_k), (uint32_t)n_keys,
+                                (const uint32_t*)(b + o_as), (uint32_t)C, (double*)(b + o_a),
+                                (double*)(b + o_out), st);
+        c->launches += 3;
+        d2h(out, b + o_out, n * C * 8, st);
+        sync(c);
     });
 }
 

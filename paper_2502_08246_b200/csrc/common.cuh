@@ -236,6 +236,25 @@ struct saap_qmodel {
     double* vec = nullptr; // b1, gamma, beta, mean, var (5 x h) then b2 (C)
 };
 
+// Q-model trainer (qtrain.cu): model + TrainerState resident on the device.
+struct saap_qtrainer {
+    saap_ctx* ctx = nullptr;
+    uint64_t d = 0, h = 0, C = 0;
+    double lr = 1e-5, beta1 = 0.9, beta2 = 0.999, eps = 1e-8, bn_momentum = 0.9;
+    uint64_t step = 0;
+    // params in checkpoint order: w1 [d x h], b1, gamma, beta, run_mean,
+    // run_var [h], w2 [h x C], b2 [C]; Adam moments for the 6 trained ones
+    double* p[8] = {};
+    double* m[8] = {};
+    double* v[8] = {};
+    // activations / grads (capacity n_cap rows)
+    uint64_t n_cap = 0;
+    double *x = nullptr, *z = nullptr, *xhat = nullptr, *y = nullptr, *r = nullptr, *pr = nullptr,
+           *tgt = nullptr, *dl = nullptr, *dy = nullptr, *dz = nullptr, *w2T = nullptr;
+    double *mean = nullptr, *var = nullptr, *g[8] = {}, *loss_rows = nullptr, *loss = nullptr;
+    float* q32 = nullptr;
+};
+
 struct saap_router {
     int kind = 0;  // 0 centroid, 1 qmodel
     int use_deroped = 1;
