@@ -152,6 +152,7 @@ void* ensure(saap_ctx* c, saap_scratch& s, size_t bytes) {
     const size_t cap = std::max<size_t>(bytes, 4096) * 5 / 4;
     SAAP_CUDA(cudaMalloc(&s.p, cap));
     s.cap = cap;
+    c->scratch_gen++;
     return s.p;
 }
 
@@ -170,6 +171,26 @@ struct DeviceGuard {
         SAAP_CUDA(cudaSetDevice(c->device));
     }
 };
+
+// live contexts, so destroying a layer / router retires every cached host graph
+// that references it
+std::vector<saap_ctx*>& live_contexts() {
+    static std::vector<saap_ctx*> v;
+    return v;
+}
+void purge_host_graphs(saap_ctx* c, const void* layer, const void* router) {
+    auto& hg = c->host_graphs;
+    for (size_t i = 0; i < hg.size();) {
+        bool hit = (layer && hg[i].layer == layer);
+        for (const void* r : hg[i].routers) hit |= (router && r == router);
+        if (hit) {
+            if (hg[i].exec) cudaGraphExecDestroy(hg[i].exec);
+            hg.erase(hg.begin() + i);
+        } else {
+            ++i;
+        }
+    }
+}
 
 void h2d(void* d, const void* h, size_t bytes, cudaStream_t st) {
     if (bytes) SAAP_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
@@ -376,7 +397,7 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
     const char* v = std::getenv(name);
     return v && *v ? (uint32_t)std::min(32, std::max(1, std::atoi(v))) : dflt;
 }
-const uint32_t kChunkSparse = env_u32("SAAP_CHUNK", 4);
+const uint32_t kChunkSparse = env_u32("SAAP_CHUNK", 8);
 const uint32_t kChunkDense = env_u32("SAAP_CHUNK_DENSE", 16);
 
 // Everything a decode step reads about its cache.
@@ -749,6 +770,7 @@ int saap_ctx_create(int device, saap_ctx** out) {
                                   prop.name};
         SAAP_CUDA(cudaSetDevice(device));
         auto* c = new saap_ctx;
+        live_contexts().push_back(c);
         c->device = device;
         c->sm_count = prop.multiProcessorCount;
         SAAP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -774,6 +796,10 @@ int saap_ctx_destroy(saap_ctx* c) {
             if (s->p) cudaFree(s->p);
         dfree(c->counters);
         dfree(c->tl);
+        for (auto& g : c->host_graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+        auto& lc = live_contexts();
+        lc.erase(std::remove(lc.begin(), lc.end(), c), lc.end());
         if (c->own_stream) cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -958,6 +984,8 @@ int saap_router_create_qmodel(saap_ctx* c, const saap_qmodel* m, saap_router** o
 }
 
 int saap_router_destroy(saap_router* r) {
+    if (r)
+        for (saap_ctx* c : live_contexts()) purge_host_graphs(c, nullptr, r);
     delete r;
     return SAAP_OK;
 }
@@ -1502,6 +1530,7 @@ int saap_layer_destroy(saap_layer* L) {
         if (!L) return;
         cudaSetDevice(L->ctx->device);
         cudaStreamSynchronize(L->ctx->stream);
+        for (saap_ctx* c : live_contexts()) purge_host_graphs(c, L, nullptr);
         dfree(L->meta);
         dfree(L->row_base);
         dfree(L->K);
@@ -1888,15 +1917,70 @@ int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* c
         const uint64_t qn = L->n_groups * G * L->d;
         float* dqr = (float*)ensure(c, c->qr, qn * 4);
         float* dqd = nullptr;
-        h2d(dqr, q_roped, qn * 4, st);
-        if (q_deroped) {
-            dqd = (float*)ensure(c, c->qd, qn * 4);
-            h2d(dqd, q_deroped, qn * 4, st);
-        }
+        // one upload when the caller passes the same rows for both roles
+        const int qmode = !q_deroped ? 0 : (q_deroped == q_roped ? 1 : 2);
+        if (qmode == 2) dqd = (float*)ensure(c, c->qd, qn * 4);
         float* dout = (float*)ensure(c, c->out, qn * 4);
         saap_attn_stats* dst = (saap_attn_stats*)ensure(c, c->stats, L->n_groups * sizeof(saap_attn_stats));
         uint32_t* dsel = selected ? (uint32_t*)ensure(c, c->sel, L->n_groups * std::max<uint64_t>(cfg->probes, 1) * 4) : nullptr;
-        sparse_dev(c, L, routers, dqr, dqd, G, cfg, dout, dst, dsel);
+        h2d(dqr, q_roped, qn * 4, st);
+        if (qmode == 2) h2d(dqd, q_deroped, qn * 4, st);
+        if (qmode == 1) dqd = dqr;
+        // Repeated calls with the same (layer, routers, cfg, shapes) replay a
+        // CUDA graph of the step captured on the second call (the first sizes
+        // the scratch); timing and trace modes stay eager.
+        static const bool no_graph = std::getenv("SAAP_NO_HOST_GRAPH") || std::getenv("SAAP_STEP_TRACE") ||
+                                     std::getenv("SAAP_DECODE_TRACE") || std::getenv("SAAP_PLAN_TRACE");
+        saap_ctx::HostGraph* hg = nullptr;
+        if (!no_graph && !c->timing) {
+            std::vector<const void*> rs(routers, routers + L->n_groups);
+            const uint64_t ck[4] = {cfg->probes, cfg->block_size, cfg->sink_count, cfg->recent_count};
+            for (auto& e : c->host_graphs)
+                if (e.layer == L && e.routers == rs && std::equal(ck, ck + 4, e.cfg) && e.G == G &&
+                    e.qmode == qmode && e.sel == (selected != nullptr)) {
+                    hg = &e;
+                    break;
+                }
+            if (!hg) {
+                c->host_graphs.emplace_back();
+                hg = &c->host_graphs.back();
+                hg->layer = L;
+                hg->routers = rs;
+                std::copy(ck, ck + 4, hg->cfg);
+                hg->G = G;
+                hg->qmode = qmode;
+                hg->sel = selected != nullptr;
+            }
+        }
+        if (hg && hg->exec && hg->gen == c->scratch_gen) {
+            SAAP_CUDA(cudaGraphLaunch(hg->exec, st));
+            c->launches += 3;
+        } else {
+            sparse_dev(c, L, routers, dqr, dqd, G, cfg, dout, dst, dsel);
+            if (hg && hg->seen++ > 0) {
+                if (hg->exec) cudaGraphExecDestroy(hg->exec);
+                hg->exec = nullptr;
+                const uint64_t gen = c->scratch_gen, launches = c->launches;
+                SAAP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                c->capturing = true;
+                cudaGraph_t graph = nullptr;
+                try {
+                    sparse_dev(c, L, routers, dqr, dqd, G, cfg, dout, dst, dsel);
+                } catch (...) {
+                    c->capturing = false;
+                    cudaStreamEndCapture(st, &graph);
+                    if (graph) cudaGraphDestroy(graph);
+                    throw;
+                }
+                c->capturing = false;
+                c->launches = launches;  // captured, not run
+                SAAP_CUDA(cudaStreamEndCapture(st, &graph));
+                const cudaError_t ie = cudaGraphInstantiate(&hg->exec, graph, 0);
+                cudaGraphDestroy(graph);
+                SAAP_CUDA(ie);
+                hg->gen = gen;
+            }
+        }
         d2h(out, dout, qn * 4, st);
         if (stats) d2h(stats, dst, L->n_groups * sizeof(saap_attn_stats), st);
         if (selected && cfg->probes) d2h(selected, dsel, L->n_groups * cfg->probes * 4, st);

@@ -198,6 +198,17 @@ struct saap_ctx {
     saap_scratch runs, dyn_cnt, part_flag;  // zero between steps (the combine re-arms them)
     unsigned long long* tl = nullptr;  // debug step timeline (SAAP_STEP_TRACE)
     saap_b200::StepCounters* counters = nullptr;  // persistent, 128 B
+    // host-API graph cache (saap_sparse_attention): graphs reference scratch,
+    // so any scratch reallocation bumps scratch_gen and retires them
+    uint64_t scratch_gen = 0;
+    struct HostGraph {
+        const void* layer = nullptr;
+        std::vector<const void*> routers;
+        uint64_t cfg[4] = {}, G = 0, gen = 0;
+        int qmode = 0, sel = 0, seen = 0;
+        cudaGraphExec_t exec = nullptr;
+    };
+    std::vector<HostGraph> host_graphs;
     // capture state
     bool capturing = false;
     int assign_mode = 0;  // 0: tcgen05 path where applicable, 1: exact CUDA-core only

@@ -155,3 +155,29 @@ def test_dense_stream_many_contexts(ctx, port):
     for i in (0, 7, 23):
         q, K, V = cases[i]
         assert max_rel_diff(full[i], port.full_attention(q, K, V)) <= TOL
+
+
+def test_host_api_graph_replay_tracks_inputs(ctx, port):
+    """saap_sparse_attention replays a cached CUDA graph from the third
+    identical call on: new query values, a rebuilt layer and a replacement
+    layer must all be honoured (graphs are retired with their layer)."""
+    C = 256
+    for rebuild in range(2):
+        cases = _shared_cases(4, 5000, C, 128, 4, seed=11 + rebuild)
+        L, routers = _layer(ctx, cases, C, 2047, [0] * 4)
+        cfg = sb.SparseAttnConfig(16, 128, sb.DenseWindow(1, 2047))
+        rs = np.random.RandomState(rebuild)
+        for call in range(5):
+            q = np.stack([bf16_round(c["qr"][:4] + 0.05 * call * rs.randn(4, 128).astype(np.float32))
+                          for c in cases])
+            out, stats, sel = L.sparse_attention(routers, q, q, cfg, want_selected=True)
+            for i in (0, 3):
+                c = cases[i]
+                _, off, idx = port_index(port, c, C)
+                want_sel = port.centroid_select(c["cent"], q[i], 16)
+                assert np.array_equal(sel[i], want_sel)
+                w, ks, mv = port.sparse_attention(q[i], c["K"], c["V"], 1, off, idx, want_sel, 16,
+                                                  128, 2047)[:3]
+                assert (stats[i].keys_scored, stats[i].max_visited_bucket) == (ks, mv)
+                assert max_rel_diff(out[i], w) <= TOL
+        del L, routers
