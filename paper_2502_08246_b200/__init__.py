@@ -746,8 +746,12 @@ class Layer:
             return None
         if isinstance(routers, BucketRouter):
             routers = [routers] * self.n_groups
-        self._keep_routers = list(routers)
-        return (C.c_void_p * self.n_groups)(*[r.h.value for r in routers])
+        key = tuple(map(id, routers))
+        if key != getattr(self, "_routers_key", None):  # repeated steps reuse the handle array
+            self._keep_routers = list(routers)
+            self._routers_arr = (C.c_void_p * self.n_groups)(*[r.h.value for r in routers])
+            self._routers_key = key
+        return self._routers_arr
 
     def sparse_attention(self, routers, q_roped, q_deroped, cfg: SparseAttnConfig,
                          want_selected=False):

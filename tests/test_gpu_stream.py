@@ -181,3 +181,34 @@ def test_host_api_graph_replay_tracks_inputs(ctx, port):
                 assert (stats[i].keys_scored, stats[i].max_visited_bucket) == (ks, mv)
                 assert max_rel_diff(out[i], w) <= TOL
         del L, routers
+
+
+def test_host_api_zero_copy_outputs(ctx, port):
+    """Page-locked output / stats buffers are written in place by the kernels
+    (no D2H stage); results equal the pageable path, across graph replays."""
+    import ctypes as ct
+
+    import torch
+    C = 256
+    cases = _shared_cases(4, 5000, C, 128, 4, seed=21)
+    L, routers = _layer(ctx, cases, C, 2047, [0] * 4)
+    cfg = sb.SparseAttnConfig(16, 128, sb.DenseWindow(1, 2047))
+    out_pin = torch.empty(4, 4, 128, pin_memory=True)
+    st_pin = torch.empty(4 * ct.sizeof(sb.AttnStats), dtype=torch.uint8, pin_memory=True)
+    st = (sb.AttnStats * 4).from_address(st_pin.data_ptr())
+    rs = np.random.RandomState(4)
+    for call in range(4):
+        q = np.ascontiguousarray(np.stack([bf16_round(c["qr"][:4] + 0.1 * call * rs.randn(4, 128).astype(np.float32))
+                                           for c in cases]))
+        want, wst, _ = L.sparse_attention(routers, q, q, cfg)
+        out_pin.fill_(np.nan)
+        c = cfg.c()
+        sb._check(sb.lib().saap_sparse_attention(
+            ctx.h, L.h, L._routers(routers), q.ctypes.data_as(ct.c_void_p),
+            q.ctypes.data_as(ct.c_void_p), ct.c_uint64(4), ct.byref(c),
+            ct.c_void_p(out_pin.data_ptr()), st, None))
+        got = out_pin.numpy()
+        assert np.isfinite(got).all()
+        assert max_rel_diff(got, want) <= 1e-4
+        assert [s.keys_scored for s in st] == [s.keys_scored for s in wst]
+        assert [s.max_visited_bucket for s in st] == [s.max_visited_bucket for s in wst]
