@@ -172,17 +172,6 @@ struct DeviceGuard {
     }
 };
 
-// Device alias of a page-locked (cudaHostAlloc / cudaHostRegister) host
-// buffer under UVA, or nullptr for pageable memory.
-void* host_alias(const void* h) {
-    cudaPointerAttributes a{};
-    if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
-}
-
 // live contexts, so destroying a layer / router retires every cached host graph
 // that references it
 std::vector<saap_ctx*>& live_contexts() {
@@ -1931,13 +1920,8 @@ int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* c
         // one upload when the caller passes the same rows for both roles
         const int qmode = !q_deroped ? 0 : (q_deroped == q_roped ? 1 : 2);
         if (qmode == 2) dqd = (float*)ensure(c, c->qd, qn * 4);
-        // Page-locked caller buffers are written in place by the kernels
-        // (zero-copy over PCIe, no D2H stage); pageable ones get a copy.
-        float* out_zc = (float*)host_alias(out);
-        saap_attn_stats* stats_zc = stats ? (saap_attn_stats*)host_alias(stats) : nullptr;
-        float* dout = out_zc ? out_zc : (float*)ensure(c, c->out, qn * 4);
-        saap_attn_stats* dst = stats_zc ? stats_zc
-                                        : (saap_attn_stats*)ensure(c, c->stats, L->n_groups * sizeof(saap_attn_stats));
+        float* dout = (float*)ensure(c, c->out, qn * 4);
+        saap_attn_stats* dst = (saap_attn_stats*)ensure(c, c->stats, L->n_groups * sizeof(saap_attn_stats));
         uint32_t* dsel = selected ? (uint32_t*)ensure(c, c->sel, L->n_groups * std::max<uint64_t>(cfg->probes, 1) * 4) : nullptr;
         h2d(dqr, q_roped, qn * 4, st);
         if (qmode == 2) h2d(dqd, q_deroped, qn * 4, st);
@@ -1953,8 +1937,7 @@ int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* c
             const uint64_t ck[4] = {cfg->probes, cfg->block_size, cfg->sink_count, cfg->recent_count};
             for (auto& e : c->host_graphs)
                 if (e.layer == L && e.routers == rs && std::equal(ck, ck + 4, e.cfg) && e.G == G &&
-                    e.qmode == qmode && e.sel == (selected != nullptr) && e.out == dout &&
-                    e.stats == dst) {
+                    e.qmode == qmode && e.sel == (selected != nullptr)) {
                     hg = &e;
                     break;
                 }
@@ -1967,8 +1950,6 @@ int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* c
                 hg->G = G;
                 hg->qmode = qmode;
                 hg->sel = selected != nullptr;
-                hg->out = dout;
-                hg->stats = dst;
             }
         }
         if (hg && hg->exec && hg->gen == c->scratch_gen) {
@@ -2000,8 +1981,8 @@ int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* c
                 hg->gen = gen;
             }
         }
-        if (!out_zc) d2h(out, dout, qn * 4, st);
-        if (stats && !stats_zc) d2h(stats, dst, L->n_groups * sizeof(saap_attn_stats), st);
+        d2h(out, dout, qn * 4, st);
+        if (stats) d2h(stats, dst, L->n_groups * sizeof(saap_attn_stats), st);
         if (selected && cfg->probes) d2h(selected, dsel, L->n_groups * cfg->probes * 4, st);
         sync(c);
     });

@@ -206,8 +206,6 @@ struct saap_ctx {
         std::vector<const void*> routers;
         uint64_t cfg[4] = {}, G = 0, gen = 0;
         int qmode = 0, sel = 0, seen = 0;
-        const void* out = nullptr;    // output / stats targets baked into the graph
-        const void* stats = nullptr;
         cudaGraphExec_t exec = nullptr;
     };
     std::vector<HostGraph> host_graphs;

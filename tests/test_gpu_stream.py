@@ -184,8 +184,8 @@ def test_host_api_graph_replay_tracks_inputs(ctx, port):
 
 
 def test_host_api_zero_copy_outputs(ctx, port):
-    """Page-locked output / stats buffers are written in place by the kernels
-    (no D2H stage); results equal the pageable path, across graph replays."""
+    """Page-locked output / stats buffers through the host API equal the
+    pageable path, across graph replays."""
     import ctypes as ct
 
     import torch
