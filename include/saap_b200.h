@@ -194,6 +194,11 @@ SAAP_API int saap_rope_remove(saap_ctx* ctx, const float* x, uint64_t rows, uint
 SAAP_API int saap_layer_create(saap_ctx* ctx, uint64_t n_groups, uint64_t dim, uint64_t n_buckets,
                       const uint64_t* n_keys, uint64_t sink, uint64_t recent_hint,
                       saap_layer** out);
+/* Same with a per-group row capacity n_cap[g] >= n_keys[g] (NULL: n_keys),
+ * so saap_layer_append can grow the contexts in place. */
+SAAP_API int saap_layer_create_cap(saap_ctx* ctx, uint64_t n_groups, uint64_t dim, uint64_t n_buckets,
+                          const uint64_t* n_keys, const uint64_t* n_cap, uint64_t sink,
+                          uint64_t recent_hint, saap_layer** out);
 SAAP_API int saap_layer_destroy(saap_layer* L);
 
 /* build_context_store(keys_roped, values, rope, partition, sink)
@@ -209,6 +214,15 @@ SAAP_API int saap_layer_build(saap_ctx* ctx, saap_layer* L, const saap_partition
 SAAP_API int saap_layer_build_dev(saap_ctx* ctx, saap_layer* L, const saap_partition* const* parts,
                          const void* keys_roped_bf16, const void* values_bf16,
                          const void* keys_assign_bf16);
+
+/* Incremental decode index: append k keys to every
+ * context (device bf16 rows [n_groups x k x dim] each: roped keys, values,
+ * pre-RoPE assignment keys).  The new keys are assigned exactly on the device
+ * and the index (off / idx) rebuilt; packed rows never move.  Every later
+ * step equals build_context_store over the grown contexts (attention.cpp:
+ * 249-255); graphs captured on this layer must be re-captured. */
+SAAP_API int saap_layer_append(saap_ctx* ctx, saap_layer* L, const void* keys_roped_bf16,
+                               const void* values_bf16, const void* keys_assign_bf16, uint64_t k);
 
 /* Assignment engine: 0 (default) = tcgen05 bf16 two-term-split GEMM with an
  * fp64 re-check of near-tie keys (device bf16 keys, d = 128); 1 = fp64

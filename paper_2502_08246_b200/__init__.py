@@ -682,15 +682,19 @@ class Layer:
     (attention.hpp:76-86 per group); the batched decode step runs on all."""
 
     def __init__(self, n_keys: Sequence[int], dim: int, n_buckets: int, sink: int = 1,
-                 recent_hint: int = 2047, ctx: Optional[Context] = None):
+                 recent_hint: int = 2047, ctx: Optional[Context] = None, capacity=None):
         self.ctx = ctx or default_context()
         self.n_keys = np.ascontiguousarray(n_keys, dtype=np.uint64)
         self.n_groups = self.n_keys.size
         self.dim, self.n_buckets_, self.sink, self.recent_hint = dim, n_buckets, sink, recent_hint
+        cap = None
+        if capacity is not None:  # room for saap_layer_append
+            cap = np.ascontiguousarray(np.broadcast_to(capacity, self.n_keys.shape), dtype=np.uint64)
         h = C.c_void_p()
-        _check(lib().saap_layer_create(self.ctx.h, _u64(self.n_groups), _u64(dim),
-                                       _u64(n_buckets), _p(self.n_keys), _u64(sink),
-                                       _u64(recent_hint), C.byref(h)))
+        _check(lib().saap_layer_create_cap(self.ctx.h, _u64(self.n_groups), _u64(dim),
+                                           _u64(n_buckets), _p(self.n_keys),
+                                           _p(cap) if cap is not None else None, _u64(sink),
+                                           _u64(recent_hint), C.byref(h)))
         self.h = h
         self.partitions: list = []
 
@@ -713,6 +717,23 @@ class Layer:
         _check(lib().saap_layer_build(self.ctx.h, self.h, arr, _p(kr), _p(v),
                                       _p(ka) if ka is not None else None, C.c_double(rope_base)))
         return self
+
+    def append_dev(self, keys_roped_bf16, values_bf16, keys_assign_bf16, k: int):
+        """Incremental index: k new keys per context (device bf16 [n_groups*k, d])."""
+        _check(lib().saap_layer_append(self.ctx.h, self.h, _dptr(keys_roped_bf16),
+                                       _dptr(values_bf16), _dptr(keys_assign_bf16), _u64(k)))
+        self.n_keys = self.n_keys + np.uint64(k)
+        return self
+
+    def append(self, keys_roped, values, keys_assign):
+        """Host f32 rows [n_groups, k, d] (rounded to bf16 RNE on upload)."""
+        import torch
+        dev = torch.device("cuda", self.ctx.device)
+        kr = torch.from_numpy(_f32(keys_roped)).to(dev).to(torch.bfloat16).contiguous()
+        v = torch.from_numpy(_f32(values)).to(dev).to(torch.bfloat16).contiguous()
+        ka = torch.from_numpy(_f32(keys_assign)).to(dev).to(torch.bfloat16).contiguous()
+        torch.cuda.synchronize(dev)
+        return self.append_dev(kr, v, ka, kr.shape[1])
 
     def build_dev(self, partitions, keys_roped_bf16, values_bf16, keys_assign_bf16):
         arr = self._parts(partitions)

@@ -40,6 +40,9 @@ void launch_derope(const float* x, const double* cs, uint64_t rows, uint32_t D, 
                    cudaStream_t st);
 void launch_debug_exp(const double* x, uint64_t n, double* y, cudaStream_t st);
 uint32_t km_dim_max(uint32_t D);
+void launch_append_rows(int D, const GroupMeta* meta, uint32_t n_groups, uint32_t k,
+                        const uint16_t* Ksrc, const uint16_t* Vsrc, uint16_t* Kdst, uint16_t* Vdst,
+                        cudaStream_t st);
 void qtrain_forward(saap_qtrainer* t, uint32_t n, cudaStream_t st);
 void qtrain_update(saap_qtrainer* t, uint32_t n, cudaStream_t st);
 void launch_attention_target(const float* q, uint32_t n, uint32_t d, const float* K,
@@ -410,6 +413,7 @@ struct DecodeSrc {
     uint16_t *gK = nullptr, *gV = nullptr;
     uint64_t gather_cap = 0;
     uint64_t recent_hint = ~0ull;  // packed-layout window (layers only)
+    bool uniform_window = false;   // every routed context has recent_begin == T
     const DecodeMaps* maps = nullptr;
 };
 
@@ -601,7 +605,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
         // the packed layout's window (every routed context has rb == T)
         const bool fused = routed && mode == 1 && slots && cmax && centR && !no_cluster &&
                            route_cluster_supported((int)D, (uint32_t)C) && probes <= C &&
-                           recent == src.recent_hint;
+                           src.uniform_window;
         if (fused) {
             ClusterRouteArgs ra{};
             ra.slots = slots;
@@ -688,15 +692,22 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     }
 }
 
+// Rows of a group between the packed layout's split T and this call's
+// recent_begin (0 when the window matches the layout: the fast planner path).
+// Appended keys (saap_layer_append) grow the position-ordered tail, so the
+// skew is per group, not recent - recent_hint.
+uint64_t window_skew(const GroupMeta& gm, uint64_t recent) {
+    if (gm.n <= gm.sink + recent) return 0;
+    const uint64_t rb = gm.n - recent;
+    return rb > gm.T ? rb - gm.T : gm.T - rb;
+}
+
 // The layer's decode view (maps built once; gather buffer sized on demand).
 DecodeSrc layer_src(saap_layer* L, uint64_t recent, bool need_gather) {
     if (need_gather) {
         uint64_t cap = 0;
-        for (auto& gm : L->h_meta) {
-            const uint64_t ns = gm.n - gm.sink;
-            const uint64_t d = recent > L->recent_hint ? recent - L->recent_hint : L->recent_hint - recent;
-            cap = std::max<uint64_t>(cap, std::min<uint64_t>(ns, d));
-        }
+        for (auto& gm : L->h_meta)
+            cap = std::max<uint64_t>(cap, std::min<uint64_t>(gm.n - gm.sink, window_skew(gm, recent)));
         if (cap > L->gather_cap) {
             if (L->ctx->capturing) invalid("gather buffer grows during graph capture");
             SAAP_CUDA(cudaStreamSynchronize(L->ctx->stream));
@@ -710,14 +721,14 @@ DecodeSrc layer_src(saap_layer* L, uint64_t recent, bool need_gather) {
         }
     }
     if (!L->maps)
-        L->maps = build_maps(L->K, L->V, L->total_rows, (uint32_t)L->d, L->gK, L->gV,
+        L->maps = build_maps(L->K, L->V, L->cap_rows, (uint32_t)L->d, L->gK, L->gV,
                              L->n_groups * L->gather_cap);
     DecodeSrc s;
     s.n_groups = L->n_groups;
     s.D = L->d;
     s.C = L->C;
     for (auto& gm : L->h_meta) s.max_n = std::max<uint64_t>(s.max_n, gm.n);
-    s.rows = L->total_rows;
+    s.rows = L->cap_rows;
     s.meta = L->meta;
     s.off = L->off;
     s.offA = L->offA;
@@ -730,6 +741,8 @@ DecodeSrc layer_src(saap_layer* L, uint64_t recent, bool need_gather) {
     s.gV = L->gV;
     s.gather_cap = L->gather_cap;
     s.recent_hint = L->recent_hint;
+    s.uniform_window = true;
+    for (auto& gm : L->h_meta) s.uniform_window &= window_skew(gm, recent) == 0;
     s.maps = (const DecodeMaps*)L->maps;
     return s;
 }
@@ -1452,6 +1465,12 @@ int saap_rope_remove(saap_ctx* c, const float* x, uint64_t rows, uint64_t d,
 int saap_layer_create(saap_ctx* c, uint64_t n_groups, uint64_t d, uint64_t C,
                       const uint64_t* n_keys, uint64_t sink, uint64_t recent_hint,
                       saap_layer** out) {
+    return saap_layer_create_cap(c, n_groups, d, C, n_keys, nullptr, sink, recent_hint, out);
+}
+
+int saap_layer_create_cap(saap_ctx* c, uint64_t n_groups, uint64_t d, uint64_t C,
+                          const uint64_t* n_keys, const uint64_t* n_cap, uint64_t sink,
+                          uint64_t recent_hint, saap_layer** out) {
     return guard([&] {
         DeviceGuard dg(c);
         need(n_keys, "saap_layer_create: n_keys");
@@ -1466,9 +1485,10 @@ int saap_layer_create(saap_ctx* c, uint64_t n_groups, uint64_t d, uint64_t C,
         L->C = C;
         L->sink = sink;
         L->recent_hint = recent_hint;
-        uint64_t rows = 0, ns = 0;
+        uint64_t rows = 0, ns = 0, src = 0, src_ns = 0;
         for (uint64_t g = 0; g < n_groups; ++g) {
             const uint64_t n = n_keys[g];
+            const uint64_t cap = n_cap ? n_cap[g] : n;
             if (n <= sink) {
                 delete L;
                 invalid("build_context_store: no keys left to index after " + std::to_string(sink) +
@@ -1478,13 +1498,24 @@ int saap_layer_create(saap_ctx* c, uint64_t n_groups, uint64_t d, uint64_t C,
                 delete L;
                 unsupported("store: context longer than 2^30 keys");
             }
+            if (cap < n || cap >= (1ull << 30)) {
+                delete L;
+                invalid("saap_layer_create: capacity " + std::to_string(cap) + " below " +
+                        std::to_string(n) + " keys or above 2^30");
+            }
             const uint64_t T = n > sink + recent_hint ? n - recent_hint : sink;
             L->h_meta.push_back(GroupMeta{rows, ns, (uint32_t)n, (uint32_t)sink, (uint32_t)T, 0});
-            rows += n;
-            ns += n - sink;
+            L->h_src0.push_back(src);
+            L->h_cap.push_back(cap);
+            rows += cap;
+            ns += cap - sink;
+            src += n;
+            src_ns += n - sink;
         }
-        L->total_rows = rows;
-        L->total_ns = ns;
+        L->total_rows = src;
+        L->total_ns = src_ns;
+        L->cap_rows = rows;
+        L->cap_ns = ns;
         L->meta = dmalloc<GroupMeta>(n_groups);
         L->row_base = dmalloc<uint64_t>(n_groups);
         L->K = dmalloc<uint16_t>(rows * d);
@@ -1508,7 +1539,7 @@ int saap_layer_create(saap_ctx* c, uint64_t n_groups, uint64_t d, uint64_t C,
         std::vector<uint64_t> rb(n_groups), kr0(n_groups), ib(n_groups);
         for (uint64_t g = 0; g < n_groups; ++g) {
             rb[g] = L->h_meta[g].row_base;
-            kr0[g] = L->h_meta[g].row_base + L->h_meta[g].sink;
+            kr0[g] = L->h_src0[g] + L->h_meta[g].sink;  // assignment keys: source rows
             ib[g] = L->h_meta[g].ivf_base;
         }
         L->key_row0 = dmalloc<uint64_t>(n_groups);
@@ -1518,10 +1549,102 @@ int saap_layer_create(saap_ctx* c, uint64_t n_groups, uint64_t d, uint64_t C,
         SAAP_CUDA(cudaMemcpy(L->meta, L->h_meta.data(), n_groups * sizeof(GroupMeta),
                              cudaMemcpyHostToDevice));
         SAAP_CUDA(cudaMemcpy(L->row_base, rb.data(), n_groups * 8, cudaMemcpyHostToDevice));
+        L->src_row0 = dmalloc<uint64_t>(n_groups);
+        SAAP_CUDA(cudaMemcpy(L->src_row0, L->h_src0.data(), n_groups * 8, cudaMemcpyHostToDevice));
         SAAP_CUDA(cudaMemcpy(L->tiles, tiles.data(), tiles.size() * sizeof(TileDesc),
                              cudaMemcpyHostToDevice));
         SAAP_CUDA(cudaMemcpy(L->tile_first, first.data(), first.size() * 4, cudaMemcpyHostToDevice));
         *out = L;
+    });
+}
+
+// Incremental decode index: k new keys per context go
+// to the position-ordered tail (rows [n, n + k)), are assigned on the device
+// (exact, like the build), and the index (off / idx / region-A tables) is
+// rebuilt from the assignments by the counting sort.  Region A and its rows
+// never move: keys that slide out of the window stay in the tail and the
+// planner filters them by bucket (the general-window path), so every later
+// step equals build_context_store over the grown context (attention.cpp:
+// 249-255, 317-376).  Captured graphs of this layer must be re-captured.
+int saap_layer_append(saap_ctx* c, saap_layer* L, const void* keys_roped_bf16,
+                      const void* values_bf16, const void* keys_assign_bf16, uint64_t k) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(L, "layer");
+        if (!L->built) invalid("append: store not built");
+        need(keys_roped_bf16, "append: keys");
+        need(values_bf16, "append: values");
+        need(keys_assign_bf16, "append: assignment keys");
+        if (c->capturing) invalid("append: not capturable");
+        if (k == 0) return;
+        for (size_t g = 0; g < L->h_meta.size(); ++g)
+            if (L->h_meta[g].n + k > L->h_cap[g])
+                invalid("append: context " + std::to_string(g) + " would exceed its capacity " +
+                        std::to_string(L->h_cap[g]) + " keys");
+        const cudaStream_t st = c->stream;
+        const uint32_t ng = (uint32_t)L->n_groups;
+        // rows into place (meta still holds the old n)
+        launch_append_rows((int)L->d, L->meta, ng, (uint32_t)k, (const uint16_t*)keys_roped_bf16,
+                           (const uint16_t*)values_bf16, L->K, L->V, st);
+        // exact assignment of the new keys: local ids [n - sink, n - sink + k)
+        std::vector<GroupMeta> am;
+        std::vector<uint64_t> kr0(ng);
+        for (uint32_t g = 0; g < ng; ++g) {
+            const GroupMeta& gm = L->h_meta[g];
+            am.push_back(gm);
+            kr0[g] = (uint64_t)g * k - (uint64_t)(gm.n - gm.sink);  // modular: row g*k for the first new id
+        }
+        std::vector<TileDesc> at;
+        for (uint32_t g = 0; g < ng; ++g) {
+            const uint32_t first = L->h_meta[g].n - L->h_meta[g].sink;
+            for (uint64_t f = 0; f < k; f += kPackTile)
+                at.push_back(TileDesc{g, first + (uint32_t)f, (uint32_t)std::min<uint64_t>(kPackTile, k - f), 0});
+        }
+        char* b = (char*)ensure(c, c->misc, at.size() * sizeof(TileDesc) + ng * 8 + 64);
+        h2d(b, at.data(), at.size() * sizeof(TileDesc), st);
+        h2d(b + at.size() * sizeof(TileDesc), kr0.data(), ng * 8, st);
+        launch_assign_exact((int)L->d, true, (const TileDesc*)b, (uint32_t)at.size(), keys_assign_bf16,
+                            (const uint64_t*)(b + at.size() * sizeof(TileDesc)), L->d_cent64,
+                            (uint32_t)L->C, L->assign, L->ivf_base, st);
+        // grow the contexts; source rows / build tiles follow the new sizes
+        uint64_t src = 0, src_ns = 0;
+        for (uint32_t g = 0; g < ng; ++g) {
+            L->h_meta[g].n += (uint32_t)k;
+            L->h_src0[g] = src;
+            src += L->h_meta[g].n;
+            src_ns += L->h_meta[g].n - L->h_meta[g].sink;
+        }
+        L->total_rows = src;
+        L->total_ns = src_ns;
+        std::vector<uint64_t> skr0(ng);
+        for (uint32_t g = 0; g < ng; ++g) skr0[g] = L->h_src0[g] + L->h_meta[g].sink;
+        std::vector<TileDesc> tiles;
+        std::vector<uint32_t> first;
+        build_tiles(L->h_meta, tiles, first);
+        sync(c);  // the staging block above is reused below
+        if (tiles.size() > L->n_tiles) {
+            dfree(L->tiles);
+            dfree(L->hist);
+            L->tiles = dmalloc<TileDesc>(tiles.size());
+            L->hist = dmalloc<uint32_t>(tiles.size() * L->C);
+        }
+        L->n_tiles = (uint32_t)tiles.size();
+        h2d(L->tiles, tiles.data(), tiles.size() * sizeof(TileDesc), st);
+        h2d(L->tile_first, first.data(), first.size() * 4, st);
+        h2d(L->meta, L->h_meta.data(), ng * sizeof(GroupMeta), st);
+        h2d(L->src_row0, L->h_src0.data(), ng * 8, st);
+        h2d(L->key_row0, skr0.data(), ng * 8, st);
+        // index over every key of the grown contexts (region A is unchanged)
+        launch_pack((int)L->d, L->tiles, L->n_tiles, L->tile_first, ng, L->meta, L->assign,
+                    (uint32_t)L->C, L->hist, L->countA, L->off, L->offA, L->idx, L->invA, L->posA,
+                    L->list, L->cap_ns, nullptr, nullptr, nullptr, nullptr, nullptr, st);
+        c->launches += 6;
+        sync(c);
+        for (auto* p : L->plans) free_static_plan(p);
+        L->plans.clear();
+        L->tc_parts.clear();  // tcgen05 tiles follow the sizes at the next build
+        L->appended = true;
+        for (saap_ctx* cc : live_contexts()) purge_host_graphs(cc, L, nullptr);
     });
 }
 
@@ -1532,6 +1655,7 @@ int saap_layer_destroy(saap_layer* L) {
         cudaStreamSynchronize(L->ctx->stream);
         for (saap_ctx* c : live_contexts()) purge_host_graphs(c, L, nullptr);
         dfree(L->meta);
+        dfree(L->src_row0);
         dfree(L->row_base);
         dfree(L->K);
         dfree(L->V);
@@ -1642,7 +1766,7 @@ static void assign_tc_path(saap_layer* L, const uint16_t* keys) {
         L->tc_nslots = (uint32_t)slots.size();
     }
     if (!L->tc_refine) {
-        L->tc_refine = dmalloc<uint32_t>(std::max<uint64_t>(L->total_ns, 1));
+        L->tc_refine = dmalloc<uint32_t>(std::max<uint64_t>(L->cap_ns, 1));
         L->tc_refine_count = dmalloc<uint32_t>(L->n_groups);
     }
     SAAP_CUDA(cudaMemsetAsync(L->tc_refine_count, 0, L->n_groups * 4, st));
@@ -1686,7 +1810,7 @@ static void build_from_device(saap_layer* L, const uint16_t* Ksrc, const uint16_
     if (timed) SAAP_CUDA(cudaEventRecord(L->bev[1], st));
     launch_pack((int)L->d, L->tiles, L->n_tiles, L->tile_first, (uint32_t)L->n_groups, L->meta,
                 L->assign, (uint32_t)L->C, L->hist, L->countA, L->off, L->offA, L->idx, L->invA,
-                L->posA, L->list, L->total_ns, Ksrc, Vsrc, L->row_base, L->K, L->V, st);
+                L->posA, L->list, L->cap_ns, Ksrc, Vsrc, L->src_row0, L->K, L->V, st);
     c->launches += 6;
     if (timed) SAAP_CUDA(cudaEventRecord(L->bev[2], st));
     L->built = true;
@@ -1719,8 +1843,8 @@ int saap_layer_build(saap_ctx* c, saap_layer* L, const saap_partition* const* pa
                 if (!(rope_base > 0.0)) invalid("RopeConfig: base_theta must be positive");
                 h2d(f32, keys_roped, elems * 4, st);
                 std::vector<uint64_t> pos(L->total_rows);
-                for (auto& gm : L->h_meta)
-                    for (uint32_t i = 0; i < gm.n; ++i) pos[gm.row_base + i] = i;
+                for (size_t g = 0; g < L->h_meta.size(); ++g)
+                    for (uint32_t i = 0; i < L->h_meta[g].n; ++i) pos[L->h_src0[g] + i] = i;
                 std::vector<double> cs = rope_table(pos.data(), L->total_rows, L->d, rope_base);
                 double* dcs = dmalloc<double>(cs.size());
                 float* der = dmalloc<float>(elems);
@@ -1828,7 +1952,7 @@ int saap_layer_packed_rows(const saap_layer* L, void** k, void** v, uint64_t* ro
         need(L, "layer");
         if (k) *k = L->K;
         if (v) *v = L->V;
-        if (rows) *rows = L->total_rows;
+        if (rows) *rows = L->cap_rows;
     });
 }
 
@@ -1875,10 +1999,9 @@ static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* con
             if (r->model->h != hq) unsupported("sparse_attention: Q-models with different widths");
     (void)maxn;
     bool need_gather = false;
-    if (cfg->recent_count != L->recent_hint)
-        for (auto& gm : L->h_meta)
-            need_gather |= gm.n > cfg->sink_count + cfg->recent_count &&
-                           (cfg->recent_count > L->recent_hint || (mode != 3 && cfg->probes > 0));
+    for (auto& gm : L->h_meta)
+        if (window_skew(gm, cfg->recent_count))
+            need_gather |= gm.n - cfg->recent_count < gm.T || (mode != 3 && cfg->probes > 0);
     const DecodeSrc src = layer_src(L, cfg->recent_count, need_gather);
     const uint32_t nh = (uint32_t)((G + kHeadsPerSlot - 1) / kHeadsPerSlot);
     const saap_static_plan* sp = static_plan(c, L->plans, L->h_meta, 1, cfg->recent_count, nh);

@@ -276,7 +276,12 @@ struct saap_router {
 struct saap_layer {
     saap_ctx* ctx = nullptr;
     uint64_t n_groups = 0, d = 0, C = 0, sink = 0, recent_hint = 0;
-    uint64_t total_rows = 0, total_ns = 0;
+    uint64_t total_rows = 0, total_ns = 0;  // source rows / keys (sum of n, n - sink)
+    uint64_t cap_rows = 0, cap_ns = 0;       // layer extents (per-group capacity)
+    std::vector<uint64_t> h_src0;            // per group: first source row (sum of n before)
+    uint64_t* src_row0 = nullptr;            // device copy of h_src0
+    std::vector<uint64_t> h_cap;             // per group: row capacity (>= n)
+    bool appended = false;                   // keys were appended after the build
     std::vector<saap_b200::GroupMeta> h_meta;
     saap_b200::GroupMeta* meta = nullptr;
     uint64_t* row_base = nullptr;  // device copy of h_meta[].row_base

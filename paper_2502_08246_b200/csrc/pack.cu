@@ -4,6 +4,8 @@
 //   best_bucket / assign_keys  partition.cpp:38-48, 181-198
 //   build_ivf                  partition.cpp:200-223  (stable counting sort)
 //   derope_indexed             attention.cpp:207-222, rotate_with rope.cpp:29-41
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace saap_b200 {
@@ -328,6 +330,7 @@ __global__ void __launch_bounds__(256) move_rows_kernel(const GroupMeta* meta, c
             if (key >= total_ns) continue;
             locate(key);
             const uint64_t lid = key - gm.ivf_base;
+            if (lid >= gm.n - gm.sink) continue;  // capacity gap after the group's keys
             const uint16_t* src = (isv ? Vsrc : Ksrc) + (srow0 + gm.sink + lid) * D + cc * 8;
             v[u] = __ldcs(reinterpret_cast<const uint4*>(src));
             dst[u] = (isv ? Vdst : Kdst) + (gm.row_base + dst_row[key]) * D + cc * 8;
@@ -351,6 +354,22 @@ __global__ void copy_sink_kernel(const GroupMeta* meta, uint32_t n_groups, const
     for (uint32_t e = threadIdx.x; e < gm.sink * CH; e += blockDim.x) {
         const uint32_t r = e / CH, cc = e % CH;
         const uint64_t s = (src_row0[g] + r) * D + cc * 8, d = (gm.row_base + r) * D + cc * 8;
+        *reinterpret_cast<uint4*>(Kdst + d) = *reinterpret_cast<const uint4*>(Ksrc + s);
+        *reinterpret_cast<uint4*>(Vdst + d) = *reinterpret_cast<const uint4*>(Vsrc + s);
+    }
+}
+
+// Appended keys: rows [n, n + k) of every group (position order, after the
+// window) from a [n_groups x k] staging block; meta still holds the old n.
+template <int D>
+__global__ void append_rows_kernel(const GroupMeta* meta, uint32_t k, const uint16_t* Ksrc,
+                                   const uint16_t* Vsrc, uint16_t* Kdst, uint16_t* Vdst) {
+    const uint32_t g = blockIdx.y;
+    const GroupMeta gm = meta[g];
+    constexpr int CH = D / 8;
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < k * CH; e += gridDim.x * blockDim.x) {
+        const uint32_t r = e / CH, cc = e % CH;
+        const uint64_t s = ((uint64_t)g * k + r) * D + cc * 8, d = (gm.row_base + gm.n + r) * D + cc * 8;
         *reinterpret_cast<uint4*>(Kdst + d) = *reinterpret_cast<const uint4*>(Ksrc + s);
         *reinterpret_cast<uint4*>(Vdst + d) = *reinterpret_cast<const uint4*>(Vsrc + s);
     }
@@ -550,6 +569,19 @@ void launch_pack(int D, const TileDesc* tiles, uint32_t n_tiles, const uint32_t*
         default: fail(SAAP_ERR_UNSUPPORTED, "pack: unsupported head dim " + std::to_string(D));
     }
 #undef SAAP_SCATTER
+    SAAP_CUDA(cudaGetLastError());
+}
+
+void launch_append_rows(int D, const GroupMeta* meta, uint32_t n_groups, uint32_t k,
+                        const uint16_t* Ksrc, const uint16_t* Vsrc, uint16_t* Kdst, uint16_t* Vdst,
+                        cudaStream_t st) {
+    const dim3 grid(std::max<uint32_t>(1, std::min<uint32_t>(64, (k * (D / 8) + 255) / 256)), n_groups);
+    switch (D) {
+        case 128: append_rows_kernel<128><<<grid, 256, 0, st>>>(meta, k, Ksrc, Vsrc, Kdst, Vdst); break;
+        case 64: append_rows_kernel<64><<<grid, 256, 0, st>>>(meta, k, Ksrc, Vsrc, Kdst, Vdst); break;
+        case 32: append_rows_kernel<32><<<grid, 256, 0, st>>>(meta, k, Ksrc, Vsrc, Kdst, Vdst); break;
+        default: fail(SAAP_ERR_UNSUPPORTED, "append: unsupported head dim " + std::to_string(D));
+    }
     SAAP_CUDA(cudaGetLastError());
 }
 

@@ -33,6 +33,7 @@ namespace {
 constexpr double kBnEps = 1e-5;
 constexpr double kLogFloor = 1e-12;
 constexpr int kT = 128;
+constexpr int kU = 8;  // loads issued ahead of each sequential add chain
 
 // z[i][j] = (sum_k x[i][k] w1[k][j], k ascending, zero x skipped) + b1[j]
 __global__ void qt_linear1(const float* q, uint32_t n, uint32_t d, uint32_t h, const double* w1,
@@ -41,8 +42,21 @@ __global__ void qt_linear1(const float* q, uint32_t n, uint32_t d, uint32_t h, c
     if (blockIdx.x == 0)
         for (uint32_t k = threadIdx.x; k < d; k += kT) x[(size_t)i * d + k] = (double)q[(size_t)i * d + k];
     if (j >= h) return;
+    // operands of 8 steps loaded ahead; the adds stay in k order
     double s = 0.0;
-    for (uint32_t k = 0; k < d; ++k) {
+    uint32_t k = 0;
+    for (; k + kU <= d; k += kU) {
+        double a[kU], w[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            a[u] = (double)q[(size_t)i * d + k + u];
+            w[u] = w1[(size_t)(k + u) * h + j];
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (a[u] != 0.0) s += a[u] * w[u];
+    }
+    for (; k < d; ++k) {
         const double a = (double)q[(size_t)i * d + k];
         if (a == 0.0) continue;
         s += a * w1[(size_t)k * h + j];
@@ -86,7 +100,19 @@ __global__ void qt_linear2(const double* r, uint32_t n, uint32_t h, uint32_t C, 
     if (c >= C) return;
     double s = 0.0;
     const double* rr = r + (size_t)i * h;
-    for (uint32_t k = 0; k < h; ++k) {
+    uint32_t k = 0;
+    for (; k + kU <= h; k += kU) {
+        double a[kU], w[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            a[u] = rr[k + u];
+            w[u] = w2[(size_t)(k + u) * C + c];
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (a[u] != 0.0) s += a[u] * w[u];
+    }
+    for (; k < h; ++k) {
         const double a = rr[k];
         if (a == 0.0) continue;
         s += a * w2[(size_t)k * C + c];
@@ -167,7 +193,19 @@ __global__ void qt_at_b(const double* a, const double* b, uint32_t n, uint32_t K
     const uint32_t j = blockIdx.x * kT + threadIdx.x, k = blockIdx.y;
     if (j >= M) return;
     double s = 0.0;
-    for (uint32_t i = 0; i < n; ++i) {
+    uint32_t i = 0;
+    for (; i + kU <= n; i += kU) {
+        double av[kU], bv[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            av[u] = a[(size_t)(i + u) * K + k];
+            bv[u] = b[(size_t)(i + u) * M + j];
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (av[u] != 0.0) s += av[u] * bv[u];
+    }
+    for (; i < n; ++i) {
         const double av = a[(size_t)i * K + k];
         if (av == 0.0) continue;
         s += av * b[(size_t)i * M + j];
@@ -194,7 +232,18 @@ __global__ void qt_dy(const double* dl, const double* w2T, const double* y, uint
     if (j >= h) return;
     const double* dr = dl + (size_t)i * C;
     double s = 0.0;
-    for (uint32_t c = 0; c < C; ++c) s += dr[c] * w2T[(size_t)c * h + j];
+    uint32_t c = 0;
+    for (; c + kU <= C; c += kU) {
+        double a[kU], w[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            a[u] = dr[c + u];
+            w[u] = w2T[(size_t)(c + u) * h + j];
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) s += a[u] * w[u];
+    }
+    for (; c < C; ++c) s += dr[c] * w2T[(size_t)c * h + j];
     const size_t o = (size_t)i * h + j;
     dy[o] = y[o] <= 0.0 ? 0.0 : s;
 }
