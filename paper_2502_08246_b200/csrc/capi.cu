@@ -24,7 +24,10 @@ void launch_combine(int D, const CombineArgs& ca, uint32_t n_qslots, cudaStream_
 void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st);
 void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t n_tiles,
                          const void* keys, const uint64_t* key_row0, const double* const* cent64,
-                         uint32_t C, uint32_t* out, const uint64_t* out_base, cudaStream_t st);
+                         uint32_t C, uint32_t* out, const uint64_t* out_base, cudaStream_t st,
+                         uint32_t max_tile_count = 1u << 31);
+void launch_append_off(const GroupMeta* meta, uint32_t n_groups, const uint32_t* assign, uint32_t k,
+                       uint32_t C, uint32_t* off, cudaStream_t st);
 void launch_pack(int D, const TileDesc* tiles, uint32_t n_tiles, const uint32_t* tile_first,
                  uint32_t n_groups, const GroupMeta* meta, const uint32_t* assign, uint32_t C,
                  uint32_t* hist, uint32_t* countA, uint32_t* off, uint32_t* offA, uint32_t* idx,
@@ -1558,6 +1561,32 @@ int saap_layer_create_cap(saap_ctx* c, uint64_t n_groups, uint64_t d, uint64_t C
     });
 }
 
+// Re-sorts idx (and re-derives the other index tables, unchanged for region
+// A) from the assignments after appends: the build's counting sort, no rows move.
+void ensure_index(saap_ctx* c, saap_layer* L) {
+    if (!L->idx_stale) return;
+    if (c->capturing) invalid("index re-sort after an append during graph capture: run once uncaptured first");
+    const cudaStream_t st = c->stream;
+    std::vector<TileDesc> tiles;
+    std::vector<uint32_t> first;
+    build_tiles(L->h_meta, tiles, first);
+    if (tiles.size() > L->n_tiles) {
+        SAAP_CUDA(cudaStreamSynchronize(st));
+        dfree(L->tiles);
+        dfree(L->hist);
+        L->tiles = dmalloc<TileDesc>(tiles.size());
+        L->hist = dmalloc<uint32_t>(tiles.size() * L->C);
+    }
+    L->n_tiles = (uint32_t)tiles.size();
+    h2d(L->tiles, tiles.data(), tiles.size() * sizeof(TileDesc), st);
+    h2d(L->tile_first, first.data(), first.size() * 4, st);
+    launch_pack((int)L->d, L->tiles, L->n_tiles, L->tile_first, (uint32_t)L->n_groups, L->meta,
+                L->assign, (uint32_t)L->C, L->hist, L->countA, L->off, L->offA, L->idx, L->invA,
+                L->posA, L->list, L->cap_ns, nullptr, nullptr, nullptr, nullptr, nullptr, st);
+    c->launches += 4;
+    L->idx_stale = false;
+}
+
 // Incremental decode index: k new keys per context go
 // to the position-ordered tail (rows [n, n + k)), are assigned on the device
 // (exact, like the build), and the index (off / idx / region-A tables) is
@@ -1605,8 +1634,8 @@ int saap_layer_append(saap_ctx* c, saap_layer* L, const void* keys_roped_bf16,
         h2d(b + at.size() * sizeof(TileDesc), kr0.data(), ng * 8, st);
         launch_assign_exact((int)L->d, true, (const TileDesc*)b, (uint32_t)at.size(), keys_assign_bf16,
                             (const uint64_t*)(b + at.size() * sizeof(TileDesc)), L->d_cent64,
-                            (uint32_t)L->C, L->assign, L->ivf_base, st);
-        // grow the contexts; source rows / build tiles follow the new sizes
+                            (uint32_t)L->C, L->assign, L->ivf_base, st, (uint32_t)std::min<uint64_t>(k, kPackTile));
+        // grow the contexts; source rows follow the new sizes
         uint64_t src = 0, src_ns = 0;
         for (uint32_t g = 0; g < ng; ++g) {
             L->h_meta[g].n += (uint32_t)k;
@@ -1618,28 +1647,15 @@ int saap_layer_append(saap_ctx* c, saap_layer* L, const void* keys_roped_bf16,
         L->total_ns = src_ns;
         std::vector<uint64_t> skr0(ng);
         for (uint32_t g = 0; g < ng; ++g) skr0[g] = L->h_src0[g] + L->h_meta[g].sink;
-        std::vector<TileDesc> tiles;
-        std::vector<uint32_t> first;
-        build_tiles(L->h_meta, tiles, first);
-        sync(c);  // the staging block above is reused below
-        if (tiles.size() > L->n_tiles) {
-            dfree(L->tiles);
-            dfree(L->hist);
-            L->tiles = dmalloc<TileDesc>(tiles.size());
-            L->hist = dmalloc<uint32_t>(tiles.size() * L->C);
-        }
-        L->n_tiles = (uint32_t)tiles.size();
-        h2d(L->tiles, tiles.data(), tiles.size() * sizeof(TileDesc), st);
-        h2d(L->tile_first, first.data(), first.size() * 4, st);
         h2d(L->meta, L->h_meta.data(), ng * sizeof(GroupMeta), st);
         h2d(L->src_row0, L->h_src0.data(), ng * 8, st);
         h2d(L->key_row0, skr0.data(), ng * 8, st);
-        // index over every key of the grown contexts (region A is unchanged)
-        launch_pack((int)L->d, L->tiles, L->n_tiles, L->tile_first, ng, L->meta, L->assign,
-                    (uint32_t)L->C, L->hist, L->countA, L->off, L->offA, L->idx, L->invA, L->posA,
-                    L->list, L->cap_ns, nullptr, nullptr, nullptr, nullptr, nullptr, st);
-        c->launches += 6;
-        sync(c);
+        // raw bucket sizes grow in place; idx (ids in bucket order) is only
+        // read by read_index and by windows reaching into region A, so it is
+        // re-sorted lazily (ensure_index)
+        launch_append_off(L->meta, ng, L->assign, (uint32_t)k, (uint32_t)L->C, L->off, st);
+        c->launches += 3;
+        L->idx_stale = true;
         for (auto* p : L->plans) free_static_plan(p);
         L->plans.clear();
         L->tc_parts.clear();  // tcgen05 tiles follow the sizes at the next build
@@ -1814,6 +1830,7 @@ static void build_from_device(saap_layer* L, const uint16_t* Ksrc, const uint16_
     c->launches += 6;
     if (timed) SAAP_CUDA(cudaEventRecord(L->bev[2], st));
     L->built = true;
+    L->idx_stale = false;
 }
 
 int saap_layer_build(saap_ctx* c, saap_layer* L, const saap_partition* const* parts,
@@ -1932,6 +1949,7 @@ int saap_layer_read_index(saap_ctx* c, const saap_layer* L, uint64_t g, uint32_t
         need(L, "layer");
         if (!L->built) invalid("store not built");
         if (g >= L->n_groups) invalid("group out of range");
+        ensure_index(c, const_cast<saap_layer*>(L));
         const GroupMeta& gm = L->h_meta[g];
         const uint64_t ns = gm.n - gm.sink;
         const cudaStream_t st = c->stream;
@@ -1998,10 +2016,14 @@ static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* con
         for (auto* r : L->cached_routers)
             if (r->model->h != hq) unsupported("sparse_attention: Q-models with different widths");
     (void)maxn;
-    bool need_gather = false;
+    bool need_gather = false, into_region_a = false;
     for (auto& gm : L->h_meta)
-        if (window_skew(gm, cfg->recent_count))
-            need_gather |= gm.n - cfg->recent_count < gm.T || (mode != 3 && cfg->probes > 0);
+        if (window_skew(gm, cfg->recent_count)) {
+            const bool below = gm.n - cfg->recent_count < gm.T;  // window reaches into region A
+            into_region_a |= below;
+            need_gather |= below || (mode != 3 && cfg->probes > 0);
+        }
+    if (into_region_a) ensure_index(c, L);
     const DecodeSrc src = layer_src(L, cfg->recent_count, need_gather);
     const uint32_t nh = (uint32_t)((G + kHeadsPerSlot - 1) / kHeadsPerSlot);
     const saap_static_plan* sp = static_plan(c, L->plans, L->h_meta, 1, cfg->recent_count, nh);

@@ -282,6 +282,7 @@ struct saap_layer {
     uint64_t* src_row0 = nullptr;            // device copy of h_src0
     std::vector<uint64_t> h_cap;             // per group: row capacity (>= n)
     bool appended = false;                   // keys were appended after the build
+    bool idx_stale = false;                  // idx not yet re-sorted after an append
     std::vector<saap_b200::GroupMeta> h_meta;
     saap_b200::GroupMeta* meta = nullptr;
     uint64_t* row_base = nullptr;  // device copy of h_meta[].row_base

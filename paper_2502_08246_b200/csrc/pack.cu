@@ -511,8 +511,10 @@ __global__ void __launch_bounds__(256) coverage_kernel(const GroupMeta* meta, co
 // ------------------------------------------------------------ launchers
 void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t n_tiles,
                          const void* keys, const uint64_t* key_row0, const double* const* cent64,
-                         uint32_t C, uint32_t* out, const uint64_t* out_base, cudaStream_t st) {
-    dim3 grid(n_tiles, kPackTile / 128);
+                         uint32_t C, uint32_t* out, const uint64_t* out_base, cudaStream_t st,
+                         uint32_t max_tile_count) {
+    // CTAs of 128 keys per tile: only as many as the largest tile needs
+    dim3 grid(n_tiles, (std::min<uint32_t>(max_tile_count, kPackTile) + 127) / 128);
 #define SAAP_ASSIGN(DD)                                                                       \
     if (bf16_keys)                                                                            \
         assign_exact_kernel<uint16_t, DD><<<grid, 128, 0, st>>>(                              \
@@ -582,6 +584,62 @@ void launch_append_rows(int D, const GroupMeta* meta, uint32_t n_groups, uint32_
         case 32: append_rows_kernel<32><<<grid, 256, 0, st>>>(meta, k, Ksrc, Vsrc, Kdst, Vdst); break;
         default: fail(SAAP_ERR_UNSUPPORTED, "append: unsupported head dim " + std::to_string(D));
     }
+    SAAP_CUDA(cudaGetLastError());
+}
+
+// Incremental off update for appended keys: off[c] += #new keys of buckets < c
+// (the raw per-bucket sizes of the grown context; attention.cpp:356).
+__global__ void __launch_bounds__(1024) append_off_kernel(const GroupMeta* meta, const uint32_t* assign,
+                                                          uint32_t k, uint32_t C, uint32_t* off) {
+    extern __shared__ uint32_t hs[];  // C counters
+    __shared__ uint32_t wsum[32];
+    const uint32_t g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const GroupMeta gm = meta[g];  // n already grown
+    for (uint32_t c = tid; c < C; c += blockDim.x) hs[c] = 0;
+    __syncthreads();
+    const uint32_t first = gm.n - gm.sink - k;
+    for (uint32_t e = tid; e < k; e += blockDim.x) atomicAdd(&hs[assign[gm.ivf_base + first + e]], 1u);
+    __syncthreads();
+    // block exclusive scan over C (each thread a contiguous chunk)
+    const uint32_t per = (C + blockDim.x - 1) / blockDim.x;
+    const uint32_t lo = min(C, tid * per), hi = min(C, lo + per);
+    uint32_t sum = 0;
+    for (uint32_t c = lo; c < hi; ++c) sum += hs[c];
+    uint32_t incl = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= (uint32_t)o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < blockDim.x / 32 ? wsum[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, w, o);
+            if (lane >= (uint32_t)o) w += v;
+        }
+        wsum[lane] = w;
+    }
+    __syncthreads();
+    uint32_t run = incl - sum + (warp ? wsum[warp - 1] : 0);
+    uint32_t* og = off + (size_t)g * (C + 1);
+    for (uint32_t c = lo; c < hi; ++c) {
+        og[c] += run;
+        run += hs[c];
+    }
+    if (tid == 0) og[C] += k;
+}
+
+void launch_append_off(const GroupMeta* meta, uint32_t n_groups, const uint32_t* assign, uint32_t k,
+                       uint32_t C, uint32_t* off, cudaStream_t st) {
+    const size_t smem = (size_t)C * 4;
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        SAAP_CUDA(cudaFuncSetAttribute(append_off_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        configured = smem;
+    }
+    append_off_kernel<<<n_groups, 1024, smem, st>>>(meta, assign, k, C, off);
     SAAP_CUDA(cudaGetLastError());
 }
 
