@@ -443,9 +443,13 @@ DecodeMaps* build_maps(const void* K, const void* V, uint64_t rows, uint32_t D, 
 // for full attention (mode 0).  Segments take 8-aligned virtual rows and are
 // cut into 128-row tiles (attention.cpp:342-347: the window is absorbed
 // before any bucket).
+// reuse: refresh that plan in place (stream-ordered uploads into its
+// buffers when they are large enough) after the layout grew by an append
 saap_static_plan* build_static_plan(const std::vector<GroupMeta>& meta, int mode, uint64_t recent,
-                                    uint32_t nh) {
-    auto* sp = new saap_static_plan;
+                                    uint32_t nh, saap_static_plan* reuse = nullptr,
+                                    cudaStream_t st = nullptr) {
+    auto* sp = reuse ? reuse : new saap_static_plan;
+    sp->max_slot_tiles = 0;
     sp->mode = mode;
     sp->recent = recent;
     sp->n_hchunks = nh;
@@ -497,7 +501,18 @@ saap_static_plan* build_static_plan(const std::vector<GroupMeta>& meta, int mode
         sp->max_slot_tiles = std::max<uint32_t>(sp->max_slot_tiles, (uint32_t)ntiles);
     }
     sp->n_tiles = (uint32_t)tiles.size();
-    sp->tiles = dmalloc<TileRec>(std::max<size_t>(tiles.size(), 1));
+    if (reuse && tiles.size() <= sp->cap_tiles) {
+        h2d(sp->tiles, tiles.data(), tiles.size() * sizeof(TileRec), st);
+        h2d(sp->cnt, cnt.data(), cnt.size() * 4, st);
+        return sp;
+    }
+    if (reuse) {
+        SAAP_CUDA(cudaStreamSynchronize(st));
+        cudaFree(sp->tiles);
+        cudaFree(sp->cnt);
+    }
+    sp->cap_tiles = std::max<size_t>(tiles.size(), 1) + (reuse ? tiles.size() / 8 : 0);
+    sp->tiles = dmalloc<TileRec>(sp->cap_tiles);
     sp->cnt = dmalloc<uint32_t>(std::max<size_t>(cnt.size(), 1));
     if (!tiles.empty())
         SAAP_CUDA(cudaMemcpy(sp->tiles, tiles.data(), tiles.size() * sizeof(TileRec), cudaMemcpyHostToDevice));
@@ -519,7 +534,13 @@ const saap_static_plan* static_plan(saap_ctx* c, std::vector<saap_static_plan*>&
                                     uint32_t nh) {
     const uint64_t rkey = mode == 0 ? 0 : recent;
     for (auto* p : cache)
-        if (p->mode == mode && p->recent == rkey && p->n_hchunks == nh) return p;
+        if (p->mode == mode && p->recent == rkey && p->n_hchunks == nh) {
+            if (!p->stale) return p;
+            if (c->capturing) invalid("decode plan refresh after an append during graph capture: run once uncaptured first");
+            build_static_plan(meta, mode, rkey, nh, p, c->stream);
+            p->stale = false;
+            return p;
+        }
     if (c->capturing) invalid("decode plan for a new window/head count during graph capture: run once uncaptured first");
     cache.push_back(build_static_plan(meta, mode, rkey, nh));
     return cache.back();
@@ -1656,8 +1677,7 @@ int saap_layer_append(saap_ctx* c, saap_layer* L, const void* keys_roped_bf16,
         launch_append_off(L->meta, ng, L->assign, (uint32_t)k, (uint32_t)L->C, L->off, st);
         c->launches += 3;
         L->idx_stale = true;
-        for (auto* p : L->plans) free_static_plan(p);
-        L->plans.clear();
+        for (auto* p : L->plans) p->stale = true;  // refreshed in place at the next step
         L->tc_parts.clear();  // tcgen05 tiles follow the sizes at the next build
         L->appended = true;
         for (saap_ctx* cc : live_contexts()) purge_host_graphs(cc, L, nullptr);

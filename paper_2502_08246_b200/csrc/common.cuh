@@ -227,6 +227,8 @@ struct saap_static_plan {
     uint32_t n_tiles = 0;
     uint32_t* cnt = nullptr;    // [qslots] static tiles per query slot (device)
     uint32_t max_slot_tiles = 0;
+    size_t cap_tiles = 0;  // TileRec capacity of `tiles`
+    bool stale = false;    // the layout grew (append): rebuild in place before use
 };
 
 struct saap_partition {
