@@ -339,7 +339,7 @@ struct RouteGeo {
 };
 RouteGeo route_geo(uint64_t C, uint64_t probes) {
     RouteGeo r;
-    r.slice = C <= 256 ? (uint32_t)C : 256u;  // slab = D x slice f32 in shared memory
+    r.slice = C <= kSliceMax ? (uint32_t)C : (uint32_t)kSliceMax;  // one thread per centroid
     r.n_slices = (uint32_t)((C + r.slice - 1) / r.slice);
     r.keep = (uint32_t)std::min<uint64_t>(probes, r.slice);
     r.n_cand = r.n_slices * r.keep;

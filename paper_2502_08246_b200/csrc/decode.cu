@@ -202,43 +202,22 @@ __device__ __forceinline__ double pooled_sum(const T* q, uint32_t G, size_t stri
 }
 
 // Stage 1: score a slice of centroids (one thread per centroid) and keep the
-// slice's top-`keep` in reference order.  The slice's transposed f32
-// centroids [D x slice] are staged in shared memory by bulk copies, so the
-// sequential fp64 chains read shared memory, not L2.
+// slice's top-`keep` in reference order.  Each thread reads its centroid's
+// column of the transposed f32 centroids straight from global memory (a warp
+// reads consecutive centroids: coalesced), eight loads ahead of the ordered
+// fp64 chain, so a slice can hold kSliceMax centroids with no shared-memory
+// slab.
 __global__ void __launch_bounds__(kSliceMax) route_score_kernel(RouteArgs a) {
-    extern __shared__ __align__(16) float slab[];  // [D][slice]
     __shared__ double pooled[128];
     __shared__ double xs[kSliceMax];
     __shared__ uint32_t xi[kSliceMax];
-    __shared__ __align__(8) uint64_t bar;
     pdl_trigger();
     const uint32_t g = blockIdx.x, sl = blockIdx.y, tid = threadIdx.x;
     const uint32_t c0 = sl * a.slice, nsl = min(a.slice, a.C - c0);
     if (a.mode == 1) {
-        const float* cT = a.centT[g];
-        const bool bulk = (a.C % 4 == 0) && (c0 % 4 == 0) && (nsl % 4 == 0) && (a.slice % 4 == 0);
-        if (bulk) {
-            if (tid == 0) {
-                mbar_init(&bar, 1);
-                fence_mbar_init();
-            }
-            __syncthreads();
-            if (tid == 0) mbar_arrive_expect_tx(&bar, a.D * nsl * 4);
-            __syncthreads();
-            for (uint32_t j = tid; j < a.D; j += blockDim.x)
-                bulk_g2s(slab + j * a.slice, cT + (size_t)j * a.C + c0, nsl * 4, &bar);
-        } else {
-            for (uint32_t e = tid; e < a.D * nsl; e += blockDim.x) {
-                const uint32_t j = e / nsl, c = e % nsl;
-                slab[j * a.slice + c] = cT[(size_t)j * a.C + c0 + c];
-            }
-        }
         // pooled_j = sum_i q_ij (fp64, rows in order)   attention.cpp:289-295
         const float* q = a.q_route + (size_t)g * a.G * a.D;
-        for (uint32_t j = tid; j < a.D; j += blockDim.x) {
-            pooled[j] = pooled_sum(q + j, a.G, a.D);
-        }
-        if (bulk) mbar_wait(&bar, 0);
+        for (uint32_t j = tid; j < a.D; j += blockDim.x) pooled[j] = pooled_sum(q + j, a.G, a.D);
         __syncthreads();
     }
     double sc = -INFINITY;
@@ -248,9 +227,14 @@ __global__ void __launch_bounds__(kSliceMax) route_score_kernel(RouteArgs a) {
         double s = 0.0;
         if (a.mode == 1) {
             // s_c = sum_j pooled_j * c_cj, mul rounded before add  attention.cpp:296-304
-#pragma unroll 8
-            for (uint32_t j = 0; j < a.D; ++j)
-                s = __dadd_rn(s, __dmul_rn(pooled[j], (double)slab[j * a.slice + tid]));
+            const float* col = a.centT[g] + c;
+            for (uint32_t j = 0; j < a.D; j += 8) {  // D is a multiple of 8
+                float v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldg(col + (size_t)(j + u) * a.C);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) s = __dadd_rn(s, __dmul_rn(pooled[j + u], (double)v[u]));
+            }
         } else {
             // Q-model: score_c = sum_i p_ic over the group rows   qmodel.cpp:493-499
             s = pooled_sum(a.scores + (size_t)g * a.G * a.C + c, a.G, a.C);
@@ -2130,14 +2114,7 @@ void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cu
 void launch_route_score(const RouteArgs& a, uint32_t n_groups, cudaStream_t st) {
     uint32_t threads = 32;
     while (threads < a.slice) threads <<= 1;
-    const size_t smem = a.mode == 1 ? (size_t)a.D * a.slice * 4 : 0;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        SAAP_CUDA(cudaFuncSetAttribute(route_score_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
-    }
-    route_score_kernel<<<dim3(n_groups, a.n_slices), threads, smem, st>>>(a);
+    route_score_kernel<<<dim3(n_groups, a.n_slices), threads, 0, st>>>(a);
     SAAP_CUDA(cudaGetLastError());
 }
 
