@@ -337,9 +337,18 @@ void check_router_dims(const saap_router* r, uint64_t d, uint64_t C, uint64_t l)
 struct RouteGeo {
     uint32_t slice, n_slices, keep, n_cand, P2;
 };
-RouteGeo route_geo(uint64_t C, uint64_t probes) {
+RouteGeo route_geo(uint64_t C, uint64_t probes, uint64_t n_groups, int sm_count) {
     RouteGeo r;
     r.slice = C <= kSliceMax ? (uint32_t)C : (uint32_t)kSliceMax;  // one thread per centroid
+    // smaller slices until the launch covers the SMs, while the planner's
+    // candidate merge (next_pow2(n_slices * keep) entries) stays <= 4096
+    while (r.slice > 128 && r.slice % 2 == 0 &&
+           n_groups * ((C + r.slice - 1) / r.slice) < (uint64_t)sm_count) {
+        const uint64_t half = r.slice / 2;
+        const uint64_t nc = ((C + half - 1) / half) * std::min<uint64_t>(probes, half);
+        if (next_pow2((uint32_t)std::max<uint64_t>(nc, 1)) > 4096) break;
+        r.slice = (uint32_t)half;
+    }
     r.n_slices = (uint32_t)((C + r.slice - 1) / r.slice);
     r.keep = (uint32_t)std::min<uint64_t>(probes, r.slice);
     r.n_cand = r.n_slices * r.keep;
@@ -355,7 +364,7 @@ void enqueue_route_score(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
                          const float* q_route, const double* probs, PlanArgs& pa,
                          const float* cmax = nullptr, const float* const* centR = nullptr,
                          const ApproxSlot* slots = nullptr, uint32_t n_slots = 0) {
-    const RouteGeo geo = route_geo(C, probes);
+    const RouteGeo geo = route_geo(C, probes, n_groups, c->sm_count);
     const bool approx = mode == 1 && C <= kPlanThreads && cmax != nullptr && centR != nullptr;
     double* cs = (double*)ensure(c, c->cand_s, n_groups * geo.n_cand * sizeof(double));
     uint32_t* ci = (uint32_t*)ensure(c, c->cand_i, n_groups * geo.n_cand * sizeof(uint32_t));
