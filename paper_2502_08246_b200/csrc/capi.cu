@@ -341,12 +341,12 @@ RouteGeo route_geo(uint64_t C, uint64_t probes, uint64_t n_groups, int sm_count)
     RouteGeo r;
     r.slice = C <= kSliceMax ? (uint32_t)C : (uint32_t)kSliceMax;  // one thread per centroid
     // smaller slices until the launch covers the SMs, while the planner's
-    // candidate merge (next_pow2(n_slices * keep) entries) stays <= 4096
+    // candidate merge (next_pow2(n_slices * keep) entries) stays <= 256
     while (r.slice > 128 && r.slice % 2 == 0 &&
            n_groups * ((C + r.slice - 1) / r.slice) < (uint64_t)sm_count) {
         const uint64_t half = r.slice / 2;
         const uint64_t nc = ((C + half - 1) / half) * std::min<uint64_t>(probes, half);
-        if (next_pow2((uint32_t)std::max<uint64_t>(nc, 1)) > 4096) break;
+        if (next_pow2((uint32_t)std::max<uint64_t>(nc, 1)) > 256) break;
         r.slice = (uint32_t)half;
     }
     r.n_slices = (uint32_t)((C + r.slice - 1) / r.slice);
