@@ -1280,7 +1280,10 @@ struct DecodeCfg {
     static constexpr int NT = D / 8;  // PV n-tiles
 };
 
-constexpr int kRecRing = 3;  // work records in flight ahead of the TMA issue
+#ifndef SAAP_REC_RING
+#define SAAP_REC_RING 3
+#endif
+constexpr int kRecRing = SAAP_REC_RING;  // work records in flight ahead of the TMA issue
 
 template <int D>
 struct DecodeSmem {
