@@ -159,3 +159,18 @@ def test_kmeans_golden_matches_live_reference():
         assert np.array_equal(cent.view(np.uint32), g[f"{name}_cent"].view(np.uint32)), name
         assert np.array_equal(obj.view(np.uint64), g[f"{name}_obj"].view(np.uint64)), name
         assert [zk, rep, nxt] == g[f"{name}_stats"].tolist(), name
+
+
+def test_kmeans_validation_before_any_device_work():
+    """kmeans_train's argument checks (partition.cpp:54-66) fire in the host
+    mirror before the Rng draws or the device is touched."""
+    import paper_2502_08246_b200 as sb
+    keys = np.zeros((3, 2), np.float32)
+    r = sb.Rng(14)
+    with pytest.raises(sb.InvalidArgument, match="kmeans_train: 3 keys cannot seed 4 buckets"):
+        sb.kmeans_train(keys, 4, 10, r)
+    with pytest.raises(sb.InvalidArgument, match="kmeans_train: need at least 1 bucket"):
+        sb.kmeans_train(keys, 0, 10, r)
+    with pytest.raises(sb.InvalidArgument, match="kmeans_train: iters must be >= 1"):
+        sb.kmeans_train(keys, 2, 0, r)
+    assert r.next_u64() == sb.Rng(14).next_u64()
