@@ -83,3 +83,30 @@ def test_append_graph_steps_and_rebuild(ctx, port):
     out2, st2, _ = L2.sparse_attention(r, q, q, cfg)
     assert st2[0].keys_scored == stats[0].keys_scored
     assert max_rel_diff(out2[0], out[0]) <= TOL
+
+
+def test_capacity_layout_device_build_tcgen05(ctx, port):
+    """Device build (tcgen05 assignment at d=128) into a layer with spare
+    capacity per context: index and attention equal the reference."""
+    import torch
+    C, d, hint = 256, 128, 1024
+    cases = [make_case(d=d, n=6000 + 500 * i, C=C, n_q=4, seed=60 + i, use_ref=False) for i in range(3)]
+    ns = [c["K"].shape[0] for c in cases]
+    parts = [sb.Partition(c["cent"], ctx) for c in cases]
+    L = sb.Layer(ns, d, C, 1, hint, ctx, capacity=[n + 777 for n in ns])
+    dev = torch.device("cuda", 0)
+    cat = lambda k: torch.from_numpy(np.concatenate([c[k] for c in cases])).to(dev).to(torch.bfloat16)
+    K, V, Kd = cat("K"), cat("V"), cat("Kd")
+    torch.cuda.synchronize()
+    L.build_dev(parts, K, V, Kd)
+    ctx.synchronize()
+    routers = [sb.CentroidRouter(p, True) for p in parts]
+    q = np.stack([c["qr"][:4] for c in cases])
+    cfg = sb.SparseAttnConfig(16, 128, sb.DenseWindow(1, hint))
+    out, stats, _ = L.sparse_attention(routers, q, q, cfg)
+    for i, c in enumerate(cases):
+        ga, gix = L.read_index(i)
+        a, off, idx, sel, w, ks, mv = _ref_step(port, c, ns[i], C, q[i], 16, hint)
+        assert np.array_equal(ga, a) and np.array_equal(gix.off, off) and np.array_equal(gix.idx, idx)
+        assert (stats[i].keys_scored, stats[i].max_visited_bucket) == (ks, mv)
+        assert max_rel_diff(out[i], w) <= TOL
