@@ -47,6 +47,7 @@ extern "C" {
 #define SAAP_ERR_UNSUPPORTED 3      /* shape outside the kernels' envelope */
 #define SAAP_ERR_NO_DEVICE 4        /* no sm_100 device: no fallback exists */
 #define SAAP_ERR_IO 5               /* reference: saap::IoError; kind via saap_last_io_kind() */
+#define SAAP_ERR_RUNTIME 6          /* reference: std::runtime_error (e.g. non-finite training loss) */
 
 typedef struct saap_ctx saap_ctx;             /* device + stream + scratch */
 typedef struct saap_partition saap_partition; /* saap::Partition (partition.hpp:14-23) */
@@ -170,7 +171,7 @@ SAAP_API int saap_qtrainer_create(saap_ctx* ctx, uint64_t dim, uint64_t hidden, 
 SAAP_API int saap_qtrainer_destroy(saap_qtrainer* t);
 /* train_step_on_target(model, state, queries_deroped [n x dim] f32,
  * target [n x C] fp64) -> pre-step loss (kl_loss with CUDA log: within
- * 1e-12 relative of glibc's).  Throws (SAAP_ERR_CUDA, "train_step:
+ * 1e-12 relative of glibc's).  Throws (SAAP_ERR_RUNTIME, "train_step:
  * non-finite loss at step k") before touching the state, like the reference. */
 SAAP_API int saap_qtrainer_step(saap_ctx* ctx, saap_qtrainer* t, const float* q, uint64_t n,
                                 uint64_t dim, const double* target, double* loss);

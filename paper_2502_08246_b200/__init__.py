@@ -43,7 +43,7 @@ LIB_PATH = os.path.join(_DIR, "libsaap_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_DIR), "include", "saap_b200.h")
 
 (SAAP_OK, SAAP_ERR_INVALID_ARGUMENT, SAAP_ERR_CUDA, SAAP_ERR_UNSUPPORTED, SAAP_ERR_NO_DEVICE,
- SAAP_ERR_IO) = range(6)
+ SAAP_ERR_IO, SAAP_ERR_RUNTIME) = range(7)
 
 
 class SaapError(RuntimeError):
@@ -61,6 +61,11 @@ class Unsupported(SaapError):
 
 class NoDevice(SaapError):
     code = SAAP_ERR_NO_DEVICE
+
+
+class RuntimeFailure(SaapError):
+    """The reference would throw std::runtime_error with this message."""
+    code = SAAP_ERR_RUNTIME
 
 
 IO_KINDS = ("OpenFailed", "BadMagic", "BadVersion", "BadDtype", "BadShape", "Truncated")
@@ -103,6 +108,8 @@ def _check(rc):
         raise NoDevice(msg)
     if rc == SAAP_ERR_IO:
         raise IoError(msg, IO_KINDS[lib().saap_last_io_kind()])
+    if rc == SAAP_ERR_RUNTIME:
+        raise RuntimeFailure(msg)
     raise SaapError(msg)
 
 

@@ -1415,7 +1415,7 @@ int saap_qtrainer_step(saap_ctx* c, saap_qtrainer* t, const float* q, uint64_t n
         sync(c);
         c->launches += 6;
         if (!std::isfinite(l))
-            fail(SAAP_ERR_CUDA, "train_step: non-finite loss at step " + std::to_string(t->step + 1));
+            fail(SAAP_ERR_RUNTIME, "train_step: non-finite loss at step " + std::to_string(t->step + 1));
         qtrain_update(t, (uint32_t)n, st);
         c->launches += 14;
         if (loss) *loss = l;

@@ -76,7 +76,7 @@ def test_qtrain_errors_and_nonfinite_loss(ctx):
         tr.train_step_on_target(np.zeros((4, 8), np.float32), np.zeros((4, C)))
     bad = np.array(g["target"][:24])
     bad[0, 0] = np.inf
-    with pytest.raises(sb.SaapError, match="train_step: non-finite loss at step 1"):
+    with pytest.raises(sb.RuntimeFailure, match="train_step: non-finite loss at step 1"):
         tr.train_step_on_target(g["qd"][0], bad)
     # the failed step left the state untouched
     got = tr.params()
