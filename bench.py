@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--router", default="centroid", choices=["centroid", "qmodel"],
+                    help="BucketRouter plugin: CentroidRouter (de-roped) or QModelRouter (random-init "
+                         "weights of the reference's shape, hidden 1024)")
     return ap.parse_args()
 
 
@@ -59,7 +62,8 @@ def workload_config(a, n):
         "workload": (f"C3: Llama-3-8B attention shape ({a.q_heads} Q / {a.kv_heads} KV heads, "
                      f"d={a.dim}, bf16 KV) decode, batch {a.batch}, {a.ctx_len} ctx, "
                      f"C={a.buckets}, l={a.probes}, window {a.sink}+{a.recent}, "
-                     "de-roped centroid router"),
+                     + ("de-roped centroid router" if a.router == "centroid"
+                        else "Q-model router (hidden 1024, random-init)")),
         "model": "Llama-3-8B attention shape (random-init centroids)",
         "global_batch": a.batch,
         "seq_len": a.ctx_len,
@@ -268,6 +272,7 @@ def ours(a):
     # ---- per layer: centroids per KV head, clustered keys, values; build stores
     layers = []
     t_build = []
+    qm_routers = None
     for li in range(a.layers):
         gen = torch.Generator(device=dev)
         gen.manual_seed(1000 * li + 17)
@@ -294,7 +299,20 @@ def ours(a):
         e1.record(stream)
         torch.cuda.synchronize()
         t_build.append(e0.elapsed_time(e1))
-        routers = [sb.CentroidRouter(p, True) for p in parts]
+        if a.router == "qmodel":
+            if qm_routers is None:
+                qm_routers = []
+                rq = np.random.default_rng(77 + rank)
+                for hl in range(heads_local):  # qmodel_init shapes / scales (qmodel.cpp:337-357)
+                    h = 1024
+                    prm = {"w1": rq.normal(0, np.sqrt(2.0 / d), (d, h)), "b1": np.zeros((1, h)),
+                           "bn_gamma": np.ones((1, h)), "bn_beta": np.zeros((1, h)),
+                           "bn_run_mean": np.zeros((1, h)), "bn_run_var": np.ones((1, h)),
+                           "w2": rq.normal(0, np.sqrt(1.0 / h), (h, C)), "b2": np.zeros((1, C))}
+                    qm_routers.append(sb.QModelRouter(sb.QModel(prm, ctx)))
+            routers = [qm_routers[gi % heads_local] for gi in range(n_groups)]
+        else:
+            routers = [sb.CentroidRouter(p, True) for p in parts]
         kv = sb.KVCache(ctx, n_groups, d, K, V, [gi * N for gi in range(n_groups)], [N] * n_groups)
         layers.append(dict(L=L, K=K, V=V, routers=routers, parts=parts_h, kv=kv, cents=cents))
 
@@ -521,7 +539,7 @@ def ours(a):
 
     # ---- CPU baseline (rank 0, N=1): the reference on the same data, bounded sample
     cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+    if rank == 0 and world == 1 and not a.no_cpu_baseline and a.router == "centroid":
         lay = layers[0]
         sample = []
         for hl in range(min(heads_local, 8)):
