@@ -16,6 +16,7 @@ namespace saap_b200 {
 
 
 constexpr int kQmRows = 4;  // group rows per pass (one W2 sweep per 4 rows)
+constexpr int kQmU = 8;     // weight loads issued ahead of the ordered chains
 
 __global__ void __launch_bounds__(1024) qmodel_probs_kernel(QModelArgs a) {
     extern __shared__ __align__(16) double qsm[];
@@ -45,7 +46,21 @@ __global__ void __launch_bounds__(1024) qmodel_probs_kernel(QModelArgs a) {
             double z[kQmRows];
 #pragma unroll
             for (int i = 0; i < kQmRows; ++i) z[i] = 0.0;
-            for (uint32_t k = 0; k < a.d; ++k) {
+            // weights of kQmU steps in flight; the chains still add in k order
+            uint32_t k = 0;
+            for (; k + kQmU <= a.d; k += kQmU) {
+                double w[kQmU];
+#pragma unroll
+                for (int u = 0; u < kQmU; ++u) w[u] = w1[(size_t)(k + u) * a.h + j];
+#pragma unroll
+                for (int u = 0; u < kQmU; ++u)
+#pragma unroll
+                    for (int i = 0; i < kQmRows; ++i) {
+                        const double av = x[i * a.d + k + u];
+                        if ((uint32_t)i < nr && av != 0.0) z[i] = __dadd_rn(z[i], __dmul_rn(av, w[u]));
+                    }
+            }
+            for (; k < a.d; ++k) {
                 const double w = w1[(size_t)k * a.h + j];
 #pragma unroll
                 for (int i = 0; i < kQmRows; ++i) {
@@ -72,7 +87,20 @@ __global__ void __launch_bounds__(1024) qmodel_probs_kernel(QModelArgs a) {
             double s[kQmRows];
 #pragma unroll
             for (int i = 0; i < kQmRows; ++i) s[i] = 0.0;
-            for (uint32_t k = 0; k < a.h; ++k) {
+            uint32_t k = 0;
+            for (; k + kQmU <= a.h; k += kQmU) {
+                double w[kQmU];
+#pragma unroll
+                for (int u = 0; u < kQmU; ++u) w[u] = w2[(size_t)(k + u) * a.C + c];
+#pragma unroll
+                for (int u = 0; u < kQmU; ++u)
+#pragma unroll
+                    for (int i = 0; i < kQmRows; ++i) {
+                        const double av = r[i * a.h + k + u];
+                        if ((uint32_t)i < nr && av != 0.0) s[i] = __dadd_rn(s[i], __dmul_rn(av, w[u]));
+                    }
+            }
+            for (; k < a.h; ++k) {
                 const double w = w2[(size_t)k * a.C + c];
 #pragma unroll
                 for (int i = 0; i < kQmRows; ++i) {
