@@ -183,6 +183,7 @@ struct QModelArgs {
     const double* const* prm;  // per group: w1, w2, vec (3 pointers)
     uint32_t G, d, h, C;
     double* probs;             // [groups][G][C]
+    double* hid;               // [groups][G][h] scratch: post-ReLU hidden rows
 };
 
 // host: TMA descriptor for a [rows x D] bf16 row-major tensor, boxes of

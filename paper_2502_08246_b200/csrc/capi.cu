@@ -584,7 +584,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     uint32_t* dcnt = plan ? (uint32_t*)ensure_zero(c, c->dyn_cnt, qslots * 4) : nullptr;
     if (plan && !stats) stats = (saap_attn_stats*)ensure(c, c->stats, n_groups * sizeof(saap_attn_stats));
     double* probs = nullptr;
-    if (mode == 2) probs = (double*)ensure(c, c->probs, n_groups * G * C * sizeof(double));
+    if (mode == 2) probs = (double*)ensure(c, c->probs, n_groups * G * (C + qm_hidden) * sizeof(double));
 
     cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
     if (c->timing && !c->capturing) {
@@ -601,6 +601,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
             qa.h = qm_hidden;
             qa.C = (uint32_t)C;
             qa.probs = probs;
+            qa.hid = probs + n_groups * G * C;
             launch_qmodel_probs(qa, (uint32_t)n_groups, st);
             c->launches++;
         }
@@ -1061,7 +1062,7 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
         ptrs[1] = (void*)r->model->w2;
         ptrs[2] = (void*)r->model->vec;
         mode = 2;
-        probs = (double*)ensure(c, c->probs, G * C * 8);
+        probs = (double*)ensure(c, c->probs, G * (C + r->model->h) * 8);
     }
     h2d(dmeta, &gm, sizeof gm, st);
     h2d(dptr, ptrs, sizeof(void*) * 4, st);
@@ -1075,6 +1076,7 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
         qa.h = (uint32_t)r->model->h;
         qa.C = (uint32_t)C;
         qa.probs = probs;
+        qa.hid = probs + G * C;
         launch_qmodel_probs(qa, 1, st);
         c->launches++;
     }

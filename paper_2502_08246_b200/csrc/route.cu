@@ -18,137 +18,127 @@ namespace saap_b200 {
 constexpr int kQmRows = 4;  // group rows per pass (one W2 sweep per 4 rows)
 constexpr int kQmU = 8;     // weight loads issued ahead of the ordered chains
 
-__global__ void __launch_bounds__(1024) qmodel_probs_kernel(QModelArgs a) {
-    extern __shared__ __align__(16) double qsm[];
-    const uint32_t g = blockIdx.x;
-    const double* w1 = a.prm[3 * g + 0];
-    const double* w2 = a.prm[3 * g + 1];
-    const double* vec = a.prm[3 * g + 2];
-    const double* b1 = vec;
-    const double* gamma = vec + a.h;
-    const double* beta = vec + 2 * a.h;
-    const double* mean = vec + 3 * a.h;
-    const double* var = vec + 4 * a.h;
-    const double* b2 = vec + 5 * a.h;
-    double* x = qsm;                      // kQmRows x d
-    double* r = x + kQmRows * a.d;        // kQmRows x h
-    double* lg = r + kQmRows * a.h;       // kQmRows x C
-    __shared__ double red[32][kQmRows];
-    __shared__ double s_tot[kQmRows], s_max[kQmRows];
+// The forward pass runs as three grids so a step's 64 (context) rows of work
+// spread over the SMs: hidden units (one thread per (row block, unit)),
+// logits (one thread per (row block, bucket)), then one CTA per row for the
+// softmax.  Every chain keeps the reference's order; loads run ahead of it.
+constexpr int kQmT = 128;
 
+__global__ void __launch_bounds__(kQmT) qm_hidden_kernel(QModelArgs a) {
+    extern __shared__ __align__(16) double xs[];  // kQmRows x d
+    const uint32_t g = blockIdx.x, j = blockIdx.y * kQmT + threadIdx.x;
+    const double* w1 = a.prm[3 * g + 0];
+    const double* vec = a.prm[3 * g + 2];
+    const double *b1 = vec, *gamma = vec + a.h, *beta = vec + 2 * a.h, *mean = vec + 3 * a.h,
+                 *var = vec + 4 * a.h;
     for (uint32_t i0 = 0; i0 < a.G; i0 += kQmRows) {
         const uint32_t nr = min((uint32_t)kQmRows, a.G - i0);
-        for (uint32_t e = threadIdx.x; e < nr * a.d; e += blockDim.x)
-            x[e] = (double)a.q[((size_t)g * a.G + i0) * a.d + e];
         __syncthreads();
-        // hidden layer: z = x W1 (+ b1), BN(running stats), ReLU
-        for (uint32_t j = threadIdx.x; j < a.h; j += blockDim.x) {
-            double z[kQmRows];
+        for (uint32_t e = threadIdx.x; e < nr * a.d; e += kQmT)
+            xs[e] = (double)a.q[((size_t)g * a.G + i0) * a.d + e];
+        __syncthreads();
+        if (j >= a.h) continue;
+        double z[kQmRows];
 #pragma unroll
-            for (int i = 0; i < kQmRows; ++i) z[i] = 0.0;
-            // weights of kQmU steps in flight; the chains still add in k order
-            uint32_t k = 0;
-            for (; k + kQmU <= a.d; k += kQmU) {
-                double w[kQmU];
+        for (int i = 0; i < kQmRows; ++i) z[i] = 0.0;
+        uint32_t k = 0;
+        for (; k + kQmU <= a.d; k += kQmU) {
+            double w[kQmU];
 #pragma unroll
-                for (int u = 0; u < kQmU; ++u) w[u] = w1[(size_t)(k + u) * a.h + j];
+            for (int u = 0; u < kQmU; ++u) w[u] = w1[(size_t)(k + u) * a.h + j];
 #pragma unroll
-                for (int u = 0; u < kQmU; ++u)
-#pragma unroll
-                    for (int i = 0; i < kQmRows; ++i) {
-                        const double av = x[i * a.d + k + u];
-                        if ((uint32_t)i < nr && av != 0.0) z[i] = __dadd_rn(z[i], __dmul_rn(av, w[u]));
-                    }
-            }
-            for (; k < a.d; ++k) {
-                const double w = w1[(size_t)k * a.h + j];
+            for (int u = 0; u < kQmU; ++u)
 #pragma unroll
                 for (int i = 0; i < kQmRows; ++i) {
-                    const double av = x[i * a.d + k];
-                    if ((uint32_t)i < nr && av != 0.0) z[i] = __dadd_rn(z[i], __dmul_rn(av, w));
+                    const double av = xs[i * a.d + k + u];
+                    if ((uint32_t)i < nr && av != 0.0) z[i] = __dadd_rn(z[i], __dmul_rn(av, w[u]));
                 }
-            }
-            const double inv_std = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(var[j], 1e-5)));
+        }
+        for (; k < a.d; ++k) {
+            const double w = w1[(size_t)k * a.h + j];
 #pragma unroll
             for (int i = 0; i < kQmRows; ++i) {
-                if ((uint32_t)i >= nr) continue;
-                const double zz = __dadd_rn(z[i], b1[j]);
-                const double xh = __dmul_rn(__dadd_rn(zz, -mean[j]), inv_std);
-                const double y = __dadd_rn(__dmul_rn(gamma[j], xh), beta[j]);
-                r[i * a.h + j] = y > 0.0 ? y : 0.0;
+                const double av = xs[i * a.d + k];
+                if ((uint32_t)i < nr && av != 0.0) z[i] = __dadd_rn(z[i], __dmul_rn(av, w));
             }
         }
-        __syncthreads();
-        // logits = r W2 (+ b2)
-        double mx[kQmRows];
-#pragma unroll
-        for (int i = 0; i < kQmRows; ++i) mx[i] = -INFINITY;
-        for (uint32_t c = threadIdx.x; c < a.C; c += blockDim.x) {
-            double s[kQmRows];
-#pragma unroll
-            for (int i = 0; i < kQmRows; ++i) s[i] = 0.0;
-            uint32_t k = 0;
-            for (; k + kQmU <= a.h; k += kQmU) {
-                double w[kQmU];
-#pragma unroll
-                for (int u = 0; u < kQmU; ++u) w[u] = w2[(size_t)(k + u) * a.C + c];
-#pragma unroll
-                for (int u = 0; u < kQmU; ++u)
-#pragma unroll
-                    for (int i = 0; i < kQmRows; ++i) {
-                        const double av = r[i * a.h + k + u];
-                        if ((uint32_t)i < nr && av != 0.0) s[i] = __dadd_rn(s[i], __dmul_rn(av, w[u]));
-                    }
-            }
-            for (; k < a.h; ++k) {
-                const double w = w2[(size_t)k * a.C + c];
-#pragma unroll
-                for (int i = 0; i < kQmRows; ++i) {
-                    const double av = r[i * a.h + k];
-                    if ((uint32_t)i < nr && av != 0.0) s[i] = __dadd_rn(s[i], __dmul_rn(av, w));
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < kQmRows; ++i) {
-                s[i] = __dadd_rn(s[i], b2[c]);
-                lg[i * a.C + c] = s[i];
-                mx[i] = fmax(mx[i], s[i]);
-            }
-        }
-        // row max (order-free)
-        const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const double inv_std = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(var[j], 1e-5)));
 #pragma unroll
         for (int i = 0; i < kQmRows; ++i) {
-            double v = mx[i];
-            for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
-            if (lane == 0) red[warp][i] = v;
+            if ((uint32_t)i >= nr) continue;
+            const double zz = __dadd_rn(z[i], b1[j]);
+            const double xh = __dmul_rn(__dadd_rn(zz, -mean[j]), inv_std);
+            const double y = __dadd_rn(__dmul_rn(gamma[j], xh), beta[j]);
+            a.hid[((size_t)g * a.G + i0 + i) * a.h + j] = y > 0.0 ? y : 0.0;
         }
-        __syncthreads();
-        if (threadIdx.x < kQmRows) {
-            double v = -INFINITY;
-            for (uint32_t w = 0; w < blockDim.x / 32; ++w) v = fmax(v, red[w][threadIdx.x]);
-            s_max[threadIdx.x] = v;
-        }
-        __syncthreads();
-        for (uint32_t e = threadIdx.x; e < nr * a.C; e += blockDim.x) {
-            const uint32_t i = e / a.C;
-            lg[e] = exp_glibc(__dadd_rn(lg[e], -s_max[i]));
-        }
-        __syncthreads();
-        // denominator: one sequential chain per row (qmodel.cpp:116-119)
-        if (threadIdx.x < nr) {
-            double t = 0.0;
-            const double* row = lg + threadIdx.x * a.C;
-            for (uint32_t c = 0; c < a.C; ++c) t = __dadd_rn(t, row[c]);
-            s_tot[threadIdx.x] = __ddiv_rn(1.0, t);
-        }
-        __syncthreads();
-        for (uint32_t e = threadIdx.x; e < nr * a.C; e += blockDim.x) {
-            const uint32_t i = e / a.C;
-            a.probs[((size_t)g * a.G + i0 + i) * a.C + (e % a.C)] = __dmul_rn(lg[e], s_tot[i]);
-        }
-        __syncthreads();
     }
+}
+
+__global__ void __launch_bounds__(kQmT) qm_logits_kernel(QModelArgs a) {
+    extern __shared__ __align__(16) double rs[];  // kQmRows x h
+    const uint32_t g = blockIdx.x, c = blockIdx.y * kQmT + threadIdx.x;
+    const double* w2 = a.prm[3 * g + 1];
+    const double* b2 = a.prm[3 * g + 2] + 5 * a.h;
+    for (uint32_t i0 = 0; i0 < a.G; i0 += kQmRows) {
+        const uint32_t nr = min((uint32_t)kQmRows, a.G - i0);
+        __syncthreads();
+        for (uint32_t e = threadIdx.x; e < nr * a.h; e += kQmT)
+            rs[e] = a.hid[((size_t)g * a.G + i0) * a.h + e];
+        __syncthreads();
+        if (c >= a.C) continue;
+        double s[kQmRows];
+#pragma unroll
+        for (int i = 0; i < kQmRows; ++i) s[i] = 0.0;
+        uint32_t k = 0;
+        for (; k + kQmU <= a.h; k += kQmU) {
+            double w[kQmU];
+#pragma unroll
+            for (int u = 0; u < kQmU; ++u) w[u] = w2[(size_t)(k + u) * a.C + c];
+#pragma unroll
+            for (int u = 0; u < kQmU; ++u)
+#pragma unroll
+                for (int i = 0; i < kQmRows; ++i) {
+                    const double av = rs[i * a.h + k + u];
+                    if ((uint32_t)i < nr && av != 0.0) s[i] = __dadd_rn(s[i], __dmul_rn(av, w[u]));
+                }
+        }
+        for (; k < a.h; ++k) {
+            const double w = w2[(size_t)k * a.C + c];
+#pragma unroll
+            for (int i = 0; i < kQmRows; ++i) {
+                const double av = rs[i * a.h + k];
+                if ((uint32_t)i < nr && av != 0.0) s[i] = __dadd_rn(s[i], __dmul_rn(av, w));
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kQmRows; ++i)
+            if ((uint32_t)i < nr) a.probs[((size_t)g * a.G + i0 + i) * a.C + c] = __dadd_rn(s[i], b2[c]);
+    }
+}
+
+// softmax_rows_inplace on one (context, row): max (order-free), glibc exp,
+// one sequential denominator (qmodel.cpp:108-125)
+__global__ void __launch_bounds__(256) qm_softmax_kernel(QModelArgs a) {
+    __shared__ double red[8];
+    __shared__ double s_inv;
+    double* row = a.probs + (size_t)blockIdx.x * a.C;
+    double mx = -INFINITY;
+    for (uint32_t c = threadIdx.x; c < a.C; c += blockDim.x) mx = fmax(mx, row[c]);
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w]);
+    for (uint32_t c = threadIdx.x; c < a.C; c += blockDim.x) row[c] = exp_glibc(__dadd_rn(row[c], -mx));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (uint32_t c = 0; c < a.C; ++c) t = __dadd_rn(t, row[c]);
+        s_inv = __ddiv_rn(1.0, t);
+    }
+    __syncthreads();
+    const double inv = s_inv;
+    for (uint32_t c = threadIdx.x; c < a.C; c += blockDim.x) row[c] = __dmul_rn(row[c], inv);
 }
 
 __global__ void debug_exp_kernel(const double* x, uint64_t n, double* y) {
@@ -164,14 +154,19 @@ void launch_debug_exp(const double* x, uint64_t n, double* y, cudaStream_t st) {
 }
 
 void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st) {
-    const size_t smem = (size_t)kQmRows * (a.d + a.h + a.C) * sizeof(double);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        SAAP_CUDA(cudaFuncSetAttribute(qmodel_probs_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
+    const size_t sm1 = (size_t)kQmRows * a.d * sizeof(double), sm2 = (size_t)kQmRows * a.h * sizeof(double);
+    static size_t cfg1 = 0, cfg2 = 0;
+    if (sm1 > 48 * 1024 && sm1 > cfg1) {
+        SAAP_CUDA(cudaFuncSetAttribute(qm_hidden_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+        cfg1 = sm1;
     }
-    qmodel_probs_kernel<<<n_groups, 1024, smem, st>>>(a);
+    if (sm2 > 48 * 1024 && sm2 > cfg2) {
+        SAAP_CUDA(cudaFuncSetAttribute(qm_logits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+        cfg2 = sm2;
+    }
+    qm_hidden_kernel<<<dim3(n_groups, (a.h + kQmT - 1) / kQmT), kQmT, sm1, st>>>(a);
+    qm_logits_kernel<<<dim3(n_groups, (a.C + kQmT - 1) / kQmT), kQmT, sm2, st>>>(a);
+    qm_softmax_kernel<<<n_groups * a.G, 256, 0, st>>>(a);
     SAAP_CUDA(cudaGetLastError());
 }
 
