@@ -17,6 +17,7 @@ namespace saap_b200 {
 
 constexpr int kQmRows = 4;  // group rows per pass (one W2 sweep per 4 rows)
 constexpr int kQmU = 8;     // weight loads issued ahead of the ordered chains
+constexpr int kQmP = 16;    // logits: weights per pipeline stage (two stages in flight)
 
 // The forward pass runs as three grids so a step's 64 (context) rows of work
 // spread over the SMs: hidden units (one thread per (row block, unit)),
@@ -89,18 +90,28 @@ __global__ void __launch_bounds__(kQmT) qm_logits_kernel(QModelArgs a) {
         double s[kQmRows];
 #pragma unroll
         for (int i = 0; i < kQmRows; ++i) s[i] = 0.0;
+        // software pipeline: the next kQmP weights load while these are used
+        constexpr int P = kQmP;
+        const uint32_t kfull = a.h / P * P;
+        double wa[P], wb[P];
+        if (kfull) {
+#pragma unroll
+            for (int u = 0; u < P; ++u) wa[u] = w2[(size_t)u * a.C + c];
+        }
         uint32_t k = 0;
-        for (; k + kQmU <= a.h; k += kQmU) {
-            double w[kQmU];
+        for (; k < kfull; k += P) {
+            const bool more = k + P < kfull;
 #pragma unroll
-            for (int u = 0; u < kQmU; ++u) w[u] = w2[(size_t)(k + u) * a.C + c];
+            for (int u = 0; u < P; ++u) wb[u] = more ? w2[(size_t)(k + P + u) * a.C + c] : 0.0;
 #pragma unroll
-            for (int u = 0; u < kQmU; ++u)
+            for (int u = 0; u < P; ++u)
 #pragma unroll
                 for (int i = 0; i < kQmRows; ++i) {
                     const double av = rs[i * a.h + k + u];
-                    if ((uint32_t)i < nr && av != 0.0) s[i] = __dadd_rn(s[i], __dmul_rn(av, w[u]));
+                    if ((uint32_t)i < nr && av != 0.0) s[i] = __dadd_rn(s[i], __dmul_rn(av, wa[u]));
                 }
+#pragma unroll
+            for (int u = 0; u < P; ++u) wa[u] = wb[u];
         }
         for (; k < a.h; ++k) {
             const double w = w2[(size_t)k * a.C + c];
