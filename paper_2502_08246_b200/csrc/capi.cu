@@ -21,7 +21,7 @@ void launch_route_approx(int D, const ApproxArgs& a, uint32_t n_slots, cudaStrea
 void launch_route_score(const RouteArgs& a, uint32_t n_groups, cudaStream_t st);
 void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st);
 void launch_combine(int D, const CombineArgs& ca, uint32_t n_qslots, cudaStream_t st);
-void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st);
+void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st, uint32_t n_slots = 0);
 void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t n_tiles,
                          const void* keys, const uint64_t* key_row0, const double* const* cent64,
                          uint32_t C, uint32_t* out, const uint64_t* out_base, cudaStream_t st,
@@ -310,6 +310,26 @@ void bind_routers(saap_layer* L, const saap_router* const* routers, int& mode, i
         }
         if (!L->d_qm) L->d_qm = (const double**)(dmalloc<void*>(3 * L->n_groups));
         SAAP_CUDA(cudaMemcpy(L->d_qm, p.data(), p.size() * sizeof(void*), cudaMemcpyHostToDevice));
+        // slots: contexts routed by one Q-model share its W2 loads
+        std::vector<const saap_qmodel*> uniq;
+        std::vector<std::vector<uint32_t>> members;
+        for (size_t g = 0; g < rs.size(); ++g) {
+            auto it = std::find(uniq.begin(), uniq.end(), rs[g]->model);
+            if (it == uniq.end()) {
+                uniq.push_back(rs[g]->model);
+                members.emplace_back();
+                it = uniq.end() - 1;
+            }
+            members[it - uniq.begin()].push_back((uint32_t)g);
+        }
+        std::vector<uint32_t> tab;
+        for (auto& m : members)
+            for (size_t k0 = 0; k0 < m.size(); k0 += kQmSlot)
+                for (size_t k = 0; k < (size_t)kQmSlot; ++k)
+                    tab.push_back(k0 + k < m.size() ? m[k0 + k] : 0xFFFFFFFFu);
+        if (!L->d_qm_slots) L->d_qm_slots = dmalloc<uint32_t>(L->n_groups * kQmSlot);
+        SAAP_CUDA(cudaMemcpy(L->d_qm_slots, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+        L->n_qm_slots = (uint32_t)(tab.size() / kQmSlot);
     }
     L->cached_routers = rs;
 }
@@ -564,7 +584,8 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
                     saap_attn_stats* stats, uint32_t* selected, uint32_t chunk,
                     uint32_t qm_hidden = 0, const float* cmax = nullptr,
                     const float* const* centR = nullptr, const ApproxSlot* slots = nullptr,
-                    uint32_t n_slots = 0) {
+                    uint32_t n_slots = 0, const uint32_t* qm_slots = nullptr,
+                    uint32_t n_qm_slots = 0) {
     const cudaStream_t st = c->stream;
     const uint64_t n_groups = src.n_groups, D = src.D, C = src.C;
     const uint64_t n_hchunks = (G + kHeadsPerSlot - 1) / kHeadsPerSlot;
@@ -602,7 +623,8 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
             qa.C = (uint32_t)C;
             qa.probs = probs;
             qa.hid = probs + n_groups * G * C;
-            launch_qmodel_probs(qa, (uint32_t)n_groups, st);
+            qa.slot_g = qm_slots;
+            launch_qmodel_probs(qa, (uint32_t)n_groups, st, n_qm_slots);
             c->launches++;
         }
         PlanArgs pa{};
@@ -1737,6 +1759,7 @@ int saap_layer_destroy(saap_layer* L) {
         dfree(L->d_cmax);
         dfree(L->d_route_slots);
         dfree(L->d_qm);
+        dfree(L->d_qm_slots);
         delete L;
     });
 }
@@ -2061,7 +2084,8 @@ static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* con
     enqueue_decode(c, src, sp, mode, L->d_centT, L->d_qm, qr, q_route, G, cfg->probes,
                    cfg->recent_count, out, stats, selected, kChunkSparse, (uint32_t)hq,
                    mode == 1 ? L->d_cmax : nullptr, mode == 1 ? L->d_centR : nullptr,
-                   mode == 1 ? (const ApproxSlot*)L->d_route_slots : nullptr, mode == 1 ? L->n_route_slots : 0);
+                   mode == 1 ? (const ApproxSlot*)L->d_route_slots : nullptr, mode == 1 ? L->n_route_slots : 0,
+                   mode == 2 ? L->d_qm_slots : nullptr, mode == 2 ? L->n_qm_slots : 0);
 }
 
 int saap_sparse_attention_dev(saap_ctx* c, const saap_layer* L, const saap_router* const* routers,

@@ -330,6 +330,8 @@ struct saap_layer {
     void* d_route_slots = nullptr;     // ApproxSlot[]: approximate-scoring slots (<= 8 contexts of one partition)
     uint32_t n_route_slots = 0;
     const double** d_qm = nullptr;     // per group: w1, w2, vec (3 pointers)
+    uint32_t* d_qm_slots = nullptr;    // [n_qm_slots][kQmSlot] contexts sharing a Q-model
+    uint32_t n_qm_slots = 0;
     // decode: TMA maps over the packed cache (+ gather buffer), built lazily
     void* maps = nullptr;              // DecodeMaps (host copy)
     uint16_t* gK = nullptr;            // gather buffer for general windows

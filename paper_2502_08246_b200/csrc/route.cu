@@ -75,22 +75,35 @@ __global__ void __launch_bounds__(kQmT) qm_hidden_kernel(QModelArgs a) {
     }
 }
 
+// logits = r W2 + b2.  A CTA serves one slot (contexts sharing the model)
+// and 128 buckets; rows go kQmRowsL at a time so each W2 load feeds 8
+// ordered chains, and the next kQmP weights load while these are used.
+constexpr int kQmRowsL = 8;
 __global__ void __launch_bounds__(kQmT) qm_logits_kernel(QModelArgs a) {
-    extern __shared__ __align__(16) double rs[];  // kQmRows x h
-    const uint32_t g = blockIdx.x, c = blockIdx.y * kQmT + threadIdx.x;
-    const double* w2 = a.prm[3 * g + 1];
-    const double* b2 = a.prm[3 * g + 2] + 5 * a.h;
-    for (uint32_t i0 = 0; i0 < a.G; i0 += kQmRows) {
-        const uint32_t nr = min((uint32_t)kQmRows, a.G - i0);
+    extern __shared__ __align__(16) double rs[];  // kQmRowsL x h
+    const uint32_t slot = blockIdx.x, c = blockIdx.y * kQmT + threadIdx.x;
+    const uint32_t* sg = a.slot_g ? a.slot_g + (size_t)slot * kQmSlot : nullptr;
+    uint32_t ng = 1;
+    if (sg)
+        while (ng < kQmSlot && sg[ng] != 0xFFFFFFFFu) ++ng;
+    const uint32_t g0 = sg ? sg[0] : slot;
+    const double* w2 = a.prm[3 * g0 + 1];
+    const double* b2 = a.prm[3 * g0 + 2] + 5 * a.h;
+    const uint32_t R = ng * a.G;
+    auto row_of = [&](uint32_t r) -> size_t {  // slot row -> (context, query row)
+        const uint32_t g = sg ? sg[r / a.G] : slot;
+        return (size_t)g * a.G + r % a.G;
+    };
+    for (uint32_t r0 = 0; r0 < R; r0 += kQmRowsL) {
+        const uint32_t nr = min((uint32_t)kQmRowsL, R - r0);
         __syncthreads();
         for (uint32_t e = threadIdx.x; e < nr * a.h; e += kQmT)
-            rs[e] = a.hid[((size_t)g * a.G + i0) * a.h + e];
+            rs[e] = a.hid[row_of(r0 + e / a.h) * a.h + e % a.h];
         __syncthreads();
         if (c >= a.C) continue;
-        double s[kQmRows];
+        double s[kQmRowsL];
 #pragma unroll
-        for (int i = 0; i < kQmRows; ++i) s[i] = 0.0;
-        // software pipeline: the next kQmP weights load while these are used
+        for (int i = 0; i < kQmRowsL; ++i) s[i] = 0.0;
         constexpr int P = kQmP;
         const uint32_t kfull = a.h / P * P;
         double wa[P], wb[P];
@@ -106,7 +119,7 @@ __global__ void __launch_bounds__(kQmT) qm_logits_kernel(QModelArgs a) {
 #pragma unroll
             for (int u = 0; u < P; ++u)
 #pragma unroll
-                for (int i = 0; i < kQmRows; ++i) {
+                for (int i = 0; i < kQmRowsL; ++i) {
                     const double av = rs[i * a.h + k + u];
                     if ((uint32_t)i < nr && av != 0.0) s[i] = __dadd_rn(s[i], __dmul_rn(av, wa[u]));
                 }
@@ -116,14 +129,14 @@ __global__ void __launch_bounds__(kQmT) qm_logits_kernel(QModelArgs a) {
         for (; k < a.h; ++k) {
             const double w = w2[(size_t)k * a.C + c];
 #pragma unroll
-            for (int i = 0; i < kQmRows; ++i) {
+            for (int i = 0; i < kQmRowsL; ++i) {
                 const double av = rs[i * a.h + k];
                 if ((uint32_t)i < nr && av != 0.0) s[i] = __dadd_rn(s[i], __dmul_rn(av, w));
             }
         }
 #pragma unroll
-        for (int i = 0; i < kQmRows; ++i)
-            if ((uint32_t)i < nr) a.probs[((size_t)g * a.G + i0 + i) * a.C + c] = __dadd_rn(s[i], b2[c]);
+        for (int i = 0; i < kQmRowsL; ++i)
+            if ((uint32_t)i < nr) a.probs[row_of(r0 + i) * a.C + c] = __dadd_rn(s[i], b2[c]);
     }
 }
 
@@ -164,8 +177,8 @@ void launch_debug_exp(const double* x, uint64_t n, double* y, cudaStream_t st) {
     SAAP_CUDA(cudaGetLastError());
 }
 
-void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st) {
-    const size_t sm1 = (size_t)kQmRows * a.d * sizeof(double), sm2 = (size_t)kQmRows * a.h * sizeof(double);
+void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st, uint32_t n_slots) {
+    const size_t sm1 = (size_t)kQmRows * a.d * sizeof(double), sm2 = (size_t)kQmRowsL * a.h * sizeof(double);
     static size_t cfg1 = 0, cfg2 = 0;
     if (sm1 > 48 * 1024 && sm1 > cfg1) {
         SAAP_CUDA(cudaFuncSetAttribute(qm_hidden_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
@@ -176,7 +189,7 @@ void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st
         cfg2 = sm2;
     }
     qm_hidden_kernel<<<dim3(n_groups, (a.h + kQmT - 1) / kQmT), kQmT, sm1, st>>>(a);
-    qm_logits_kernel<<<dim3(n_groups, (a.C + kQmT - 1) / kQmT), kQmT, sm2, st>>>(a);
+    qm_logits_kernel<<<dim3(a.slot_g ? n_slots : n_groups, (a.C + kQmT - 1) / kQmT), kQmT, sm2, st>>>(a);
     qm_softmax_kernel<<<n_groups * a.G, 256, 0, st>>>(a);
     SAAP_CUDA(cudaGetLastError());
 }
