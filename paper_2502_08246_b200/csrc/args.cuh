@@ -186,7 +186,10 @@ struct QModelArgs {
     double* hid;               // [groups][G][h] scratch: post-ReLU hidden rows
     const uint32_t* slot_g;    // optional [n_slots][kQmSlot] groups sharing one model (pad ~0u)
 };
-constexpr int kQmSlot = 8;     // contexts of one Q-model whose logits share the W2 loads
+#ifndef SAAP_QM_SLOT
+#define SAAP_QM_SLOT 2
+#endif
+constexpr int kQmSlot = SAAP_QM_SLOT;  // contexts of one Q-model whose logits share the W2 loads
 
 // host: TMA descriptor for a [rows x D] bf16 row-major tensor, boxes of
 // (min(D,64) elements x box_rows rows) with the matching swizzle.
