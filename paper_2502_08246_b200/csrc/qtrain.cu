@@ -137,9 +137,17 @@ __global__ void qt_softmax_rows(double* a, uint32_t cols) {
     mx = red[0];
     for (uint32_t j = threadIdx.x; j < cols; j += kT) row[j] = exp_glibc(row[j] - mx);
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {  // loads run ahead of the ordered chain
         double t = 0.0;
-        for (uint32_t j = 0; j < cols; ++j) t += row[j];
+        uint32_t j = 0;
+        for (; j + kU <= cols; j += kU) {
+            double v[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) v[u] = row[j + u];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) t += v[u];
+        }
+        for (; j < cols; ++j) t += row[j];
         s_tot = 1.0 / t;
     }
     __syncthreads();

@@ -155,9 +155,17 @@ __global__ void __launch_bounds__(256) qm_softmax_kernel(QModelArgs a) {
     for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w]);
     for (uint32_t c = threadIdx.x; c < a.C; c += blockDim.x) row[c] = exp_glibc(__dadd_rn(row[c], -mx));
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {  // loads run ahead of the ordered chain
         double t = 0.0;
-        for (uint32_t c = 0; c < a.C; ++c) t = __dadd_rn(t, row[c]);
+        uint32_t c = 0;
+        for (; c + 8 <= a.C; c += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = row[c + u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t = __dadd_rn(t, v[u]);
+        }
+        for (; c < a.C; ++c) t = __dadd_rn(t, row[c]);
         s_inv = __ddiv_rn(1.0, t);
     }
     __syncthreads();
