@@ -25,36 +25,23 @@ constexpr int kQmP = 16;    // logits: weights per pipeline stage (two stages in
 // softmax.  Every chain keeps the reference's order; loads run ahead of it.
 constexpr int kQmT = 128;
 
-// hidden = ReLU(BN(x W1 + b1)) per slot (contexts sharing the model), 8 rows
-// per pass so each W1 load feeds 8 ordered chains; loads pipelined.
 __global__ void __launch_bounds__(kQmT) qm_hidden_kernel(QModelArgs a) {
-    extern __shared__ __align__(16) double xs[];  // 8 x d
-    constexpr int NR = 8;
-    const uint32_t slot = blockIdx.x, j = blockIdx.y * kQmT + threadIdx.x;
-    const uint32_t* sg = a.slot_g ? a.slot_g + (size_t)slot * kQmSlot : nullptr;
-    uint32_t ng = 1;
-    if (sg)
-        while (ng < kQmSlot && sg[ng] != 0xFFFFFFFFu) ++ng;
-    const uint32_t g0 = sg ? sg[0] : slot;
-    const double* w1 = a.prm[3 * g0 + 0];
-    const double* vec = a.prm[3 * g0 + 2];
+    extern __shared__ __align__(16) double xs[];  // kQmRows x d
+    const uint32_t g = blockIdx.x, j = blockIdx.y * kQmT + threadIdx.x;
+    const double* w1 = a.prm[3 * g + 0];
+    const double* vec = a.prm[3 * g + 2];
     const double *b1 = vec, *gamma = vec + a.h, *beta = vec + 2 * a.h, *mean = vec + 3 * a.h,
                  *var = vec + 4 * a.h;
-    const uint32_t R = ng * a.G;
-    auto row_of = [&](uint32_t r) -> size_t {
-        const uint32_t g = sg ? sg[r / a.G] : slot;
-        return (size_t)g * a.G + r % a.G;
-    };
-    for (uint32_t r0 = 0; r0 < R; r0 += NR) {
-        const uint32_t nr = min((uint32_t)NR, R - r0);
+    for (uint32_t i0 = 0; i0 < a.G; i0 += kQmRows) {
+        const uint32_t nr = min((uint32_t)kQmRows, a.G - i0);
         __syncthreads();
         for (uint32_t e = threadIdx.x; e < nr * a.d; e += kQmT)
-            xs[e] = (double)a.q[row_of(r0 + e / a.d) * a.d + e % a.d];
+            xs[e] = (double)a.q[((size_t)g * a.G + i0) * a.d + e];
         __syncthreads();
         if (j >= a.h) continue;
-        double z[NR];
+        double z[kQmRows];
 #pragma unroll
-        for (int i = 0; i < NR; ++i) z[i] = 0.0;
+        for (int i = 0; i < kQmRows; ++i) z[i] = 0.0;
         uint32_t k = 0;
         for (; k + kQmU <= a.d; k += kQmU) {
             double w[kQmU];
@@ -63,7 +50,7 @@ __global__ void __launch_bounds__(kQmT) qm_hidden_kernel(QModelArgs a) {
 #pragma unroll
             for (int u = 0; u < kQmU; ++u)
 #pragma unroll
-                for (int i = 0; i < NR; ++i) {
+                for (int i = 0; i < kQmRows; ++i) {
                     const double av = xs[i * a.d + k + u];
                     if ((uint32_t)i < nr && av != 0.0) z[i] = __dadd_rn(z[i], __dmul_rn(av, w[u]));
                 }
@@ -71,19 +58,19 @@ __global__ void __launch_bounds__(kQmT) qm_hidden_kernel(QModelArgs a) {
         for (; k < a.d; ++k) {
             const double w = w1[(size_t)k * a.h + j];
 #pragma unroll
-            for (int i = 0; i < NR; ++i) {
+            for (int i = 0; i < kQmRows; ++i) {
                 const double av = xs[i * a.d + k];
                 if ((uint32_t)i < nr && av != 0.0) z[i] = __dadd_rn(z[i], __dmul_rn(av, w));
             }
         }
         const double inv_std = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(var[j], 1e-5)));
 #pragma unroll
-        for (int i = 0; i < NR; ++i) {
+        for (int i = 0; i < kQmRows; ++i) {
             if ((uint32_t)i >= nr) continue;
             const double zz = __dadd_rn(z[i], b1[j]);
             const double xh = __dmul_rn(__dadd_rn(zz, -mean[j]), inv_std);
             const double y = __dadd_rn(__dmul_rn(gamma[j], xh), beta[j]);
-            a.hid[row_of(r0 + i) * a.h + j] = y > 0.0 ? y : 0.0;
+            a.hid[((size_t)g * a.G + i0 + i) * a.h + j] = y > 0.0 ? y : 0.0;
         }
     }
 }
@@ -199,7 +186,7 @@ void launch_debug_exp(const double* x, uint64_t n, double* y, cudaStream_t st) {
 }
 
 void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st, uint32_t n_slots) {
-    const size_t sm1 = (size_t)8 * a.d * sizeof(double), sm2 = (size_t)kQmRowsL * a.h * sizeof(double);
+    const size_t sm1 = (size_t)kQmRows * a.d * sizeof(double), sm2 = (size_t)kQmRowsL * a.h * sizeof(double);
     static size_t cfg1 = 0, cfg2 = 0;
     if (sm1 > 48 * 1024 && sm1 > cfg1) {
         SAAP_CUDA(cudaFuncSetAttribute(qm_hidden_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
@@ -209,7 +196,7 @@ void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st
         SAAP_CUDA(cudaFuncSetAttribute(qm_logits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
         cfg2 = sm2;
     }
-    qm_hidden_kernel<<<dim3(a.slot_g ? n_slots : n_groups, (a.h + kQmT - 1) / kQmT), kQmT, sm1, st>>>(a);
+    qm_hidden_kernel<<<dim3(n_groups, (a.h + kQmT - 1) / kQmT), kQmT, sm1, st>>>(a);
     qm_logits_kernel<<<dim3(a.slot_g ? n_slots : n_groups, (a.C + kQmT - 1) / kQmT), kQmT, sm2, st>>>(a);
     qm_softmax_kernel<<<n_groups * a.G, 256, 0, st>>>(a);
     SAAP_CUDA(cudaGetLastError());
