@@ -79,9 +79,13 @@ __global__ void __launch_bounds__(kQmT) qm_hidden_kernel(QModelArgs a) {
 // and 128 buckets; rows go kQmRowsL at a time so each W2 load feeds 8
 // ordered chains, and the next kQmP weights load while these are used.
 constexpr int kQmRowsL = 8;
-__global__ void __launch_bounds__(kQmT) qm_logits_kernel(QModelArgs a) {
+#ifndef SAAP_QM_TL
+#define SAAP_QM_TL 256
+#endif
+constexpr int kQmTL = SAAP_QM_TL;  // buckets per logits CTA
+__global__ void __launch_bounds__(kQmTL) qm_logits_kernel(QModelArgs a) {
     extern __shared__ __align__(16) double rs[];  // kQmRowsL x h
-    const uint32_t slot = blockIdx.x, c = blockIdx.y * kQmT + threadIdx.x;
+    const uint32_t slot = blockIdx.x, c = blockIdx.y * kQmTL + threadIdx.x;
     const uint32_t* sg = a.slot_g ? a.slot_g + (size_t)slot * kQmSlot : nullptr;
     uint32_t ng = 1;
     if (sg)
@@ -97,7 +101,7 @@ __global__ void __launch_bounds__(kQmT) qm_logits_kernel(QModelArgs a) {
     for (uint32_t r0 = 0; r0 < R; r0 += kQmRowsL) {
         const uint32_t nr = min((uint32_t)kQmRowsL, R - r0);
         __syncthreads();
-        for (uint32_t e = threadIdx.x; e < nr * a.h; e += kQmT)
+        for (uint32_t e = threadIdx.x; e < nr * a.h; e += kQmTL)
             rs[e] = a.hid[row_of(r0 + e / a.h) * a.h + e % a.h];
         __syncthreads();
         if (c >= a.C) continue;
@@ -197,7 +201,7 @@ void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st
         cfg2 = sm2;
     }
     qm_hidden_kernel<<<dim3(n_groups, (a.h + kQmT - 1) / kQmT), kQmT, sm1, st>>>(a);
-    qm_logits_kernel<<<dim3(a.slot_g ? n_slots : n_groups, (a.C + kQmT - 1) / kQmT), kQmT, sm2, st>>>(a);
+    qm_logits_kernel<<<dim3(a.slot_g ? n_slots : n_groups, (a.C + kQmTL - 1) / kQmTL), kQmTL, sm2, st>>>(a);
     qm_softmax_kernel<<<n_groups * a.G, 256, 0, st>>>(a);
     SAAP_CUDA(cudaGetLastError());
 }
