@@ -56,6 +56,7 @@ typedef struct saap_router saap_router;       /* saap::BucketRouter (attention.h
 typedef struct saap_layer saap_layer;         /* n_groups ContextStores (attention.hpp:76-86) */
 typedef struct saap_graph saap_graph;         /* captured decode step (CUDA graph) */
 typedef struct saap_qtrainer saap_qtrainer;   /* QModel + TrainerState (qmodel.hpp:66-75) */
+typedef struct saap_accum saap_accum;         /* PartialAccumulator (attention.hpp:30-39) */
 
 /* saap::SparseAttnConfig (attention.hpp:21-25) with DenseWindow (:16-19). */
 typedef struct {
@@ -182,6 +183,37 @@ SAAP_API int saap_qtrainer_read(saap_ctx* ctx, const saap_qtrainer* t, double* c
 SAAP_API int saap_attention_target(saap_ctx* ctx, const float* q_roped, uint64_t n, uint64_t dim,
                                    const float* keys_roped, uint64_t n_keys,
                                    const uint32_t* assignment, uint64_t n_buckets, double* out);
+
+/* ---- partial-attention accumulators (attention.hpp:27-70), fp64 on the
+ * device, bit-exact with the reference.  Host f32 blocks are row-major; only
+ * the absorbed rows are uploaded.  State read/write is for interop. */
+SAAP_API int saap_accum_create(saap_ctx* ctx, uint64_t heads, uint64_t value_dim, saap_accum** out);
+SAAP_API int saap_accum_destroy(saap_accum* a);
+SAAP_API int saap_accum_read(saap_ctx* ctx, const saap_accum* a, double* out_acc, double* sumexp,
+                             double* runmax);
+SAAP_API int saap_accum_write(saap_ctx* ctx, saap_accum* a, const double* out_acc,
+                              const double* sumexp, const double* runmax);
+/* pattn_absorb(acc, q_group, keys, values, ids)          attention.cpp:85-89 */
+SAAP_API int saap_pattn_absorb(saap_ctx* ctx, saap_accum* a, const float* q, uint64_t G, uint64_t dim,
+                               const float* keys, const float* values, uint64_t n_keys,
+                               uint64_t n_values, uint64_t value_dim, const uint64_t* ids,
+                               uint64_t count);
+/* pattn_absorb_range(acc, q_group, keys, values, begin, end)  attention.cpp:91-100 */
+SAAP_API int saap_pattn_absorb_range(saap_ctx* ctx, saap_accum* a, const float* q, uint64_t G,
+                                     uint64_t dim, const float* keys, const float* values,
+                                     uint64_t n_keys, uint64_t n_values, uint64_t value_dim,
+                                     uint64_t begin, uint64_t end);
+/* merge_into(acc, part) / merge_partials(parts)           attention.cpp:102-139 */
+SAAP_API int saap_merge_into(saap_ctx* ctx, saap_accum* a, const saap_accum* part);
+SAAP_API int saap_merge_partials(saap_ctx* ctx, const saap_accum* const* parts, uint64_t n,
+                                 saap_accum* out);
+/* pattn_finalize(acc, &any_empty)                          attention.cpp:141-161 */
+SAAP_API int saap_pattn_finalize(saap_ctx* ctx, const saap_accum* a, float* out, int* any_empty);
+/* attention_over_ids(q_group, keys, values, ids, &any_empty) attention.cpp:197-203 */
+SAAP_API int saap_attention_over_ids(saap_ctx* ctx, const float* q, uint64_t G, uint64_t dim,
+                                     const float* keys, const float* values, uint64_t n_keys,
+                                     uint64_t n_values, uint64_t value_dim, const uint64_t* ids,
+                                     uint64_t count, float* out, int* any_empty);
 
 /* rope_remove_block(keys, positions, {dim, base})  rope.cpp:87-90 */
 SAAP_API int saap_rope_remove(saap_ctx* ctx, const float* x, uint64_t rows, uint64_t dim,

@@ -383,6 +383,32 @@ class Ref:
                                                 _u64(n_buckets), _p(out)))
         return out
 
+    # ---- PartialAccumulator state ops (attention.cpp:34-161), in/out arrays
+    def acc_absorb(self, state, q, K, V, ids=None, begin=0, end=0):
+        out, se, rm = (np.array(x, np.float64, copy=True) for x in state)
+        q, K, V = _f32(q), _f32(K), _f32(V)
+        ids_a = np.ascontiguousarray(ids if ids is not None else [], np.uint64)
+        self._chk(self.lib.ref_pattn_absorb_state(
+            _p(q), _u64(q.shape[0]), _u64(q.shape[1]), _p(K), _p(V), _u64(K.shape[0]),
+            _u64(V.shape[1]), _p(ids_a), _u64(ids_a.size), _u64(begin), _u64(end),
+            C.c_int(0 if ids is not None else 1), _p(out), _p(se), _p(rm)))
+        return out, se, rm
+
+    def acc_merge(self, state, part):
+        out, se, rm = (np.array(x, np.float64, copy=True) for x in state)
+        po, ps, pr = (np.ascontiguousarray(x, np.float64) for x in part)
+        self._chk(self.lib.ref_merge_state(_u64(out.shape[0]), _u64(out.shape[1]), _p(out), _p(se),
+                                           _p(rm), _p(po), _p(ps), _p(pr)))
+        return out, se, rm
+
+    def acc_finalize(self, state):
+        out, se, rm = (np.ascontiguousarray(x, np.float64) for x in state)
+        res = np.empty(out.shape, np.float32)
+        e = C.c_int()
+        self._chk(self.lib.ref_finalize_state(_u64(out.shape[0]), _u64(out.shape[1]), _p(out), _p(se),
+                                              _p(rm), _p(res), C.byref(e)))
+        return res, bool(e.value)
+
     def assign_keys(self, keys, cent, threads=1):
         keys, cent = _f32(keys), _f32(cent)
         out = np.empty(keys.shape[0], np.uint32)

@@ -622,3 +622,56 @@ int ref_attention_target(const float* q, std::uint64_t n, std::uint64_t d, const
     });
 }
 }  // extern "C"
+
+// ---------------------------------------------------------------- accumulators
+// PartialAccumulator state as flat arrays (out_acc [H x dv], sumexp, runmax),
+// in/out, so tests can drive the reference and the device in lockstep.
+namespace {
+PartialAccumulator acc_from(std::uint64_t H, std::uint64_t dv, const double* out, const double* se,
+                            const double* rm) {
+    PartialAccumulator a(H, dv);
+    std::copy(out, out + H * dv, a.out_acc.data.begin());
+    std::copy(se, se + H, a.sumexp.begin());
+    std::copy(rm, rm + H, a.runmax.begin());
+    return a;
+}
+void acc_to(const PartialAccumulator& a, double* out, double* se, double* rm) {
+    std::copy(a.out_acc.data.begin(), a.out_acc.data.end(), out);
+    std::copy(a.sumexp.begin(), a.sumexp.end(), se);
+    std::copy(a.runmax.begin(), a.runmax.end(), rm);
+}
+}  // namespace
+
+extern "C" {
+int ref_pattn_absorb_state(const float* q, std::uint64_t G, std::uint64_t d, const float* K,
+                           const float* V, std::uint64_t n, std::uint64_t dv, const std::uint64_t* ids,
+                           std::uint64_t count, std::uint64_t begin, std::uint64_t end, int range,
+                           double* out, double* se, double* rm) {
+    return guard([&] {
+        PartialAccumulator a = acc_from(G, dv, out, se, rm);
+        if (range) pattn_absorb_range(a, block(q, G, d), block(K, n, d), block(V, n, dv), begin, end);
+        else pattn_absorb(a, block(q, G, d), block(K, n, d), block(V, n, dv),
+                          std::span<const std::uint64_t>(ids, count));
+        acc_to(a, out, se, rm);
+    });
+}
+
+int ref_merge_state(std::uint64_t H, std::uint64_t dv, double* out, double* se, double* rm,
+                    const double* pout, const double* pse, const double* prm) {
+    return guard([&] {
+        PartialAccumulator a = acc_from(H, dv, out, se, rm);
+        merge_into(a, acc_from(H, dv, pout, pse, prm));
+        acc_to(a, out, se, rm);
+    });
+}
+
+int ref_finalize_state(std::uint64_t H, std::uint64_t dv, const double* out, const double* se,
+                       const double* rm, float* res, int* any_empty) {
+    return guard([&] {
+        bool e = false;
+        TensorBlock t = pattn_finalize(acc_from(H, dv, out, se, rm), &e);
+        put(t, res);
+        *any_empty = e ? 1 : 0;
+    });
+}
+}  // extern "C"

@@ -12,6 +12,7 @@ reference (proj/core)      here
 kmeans_train / Rng         :func:`kmeans_train` / :class:`Rng` (partition.cpp:52-179)
 tensor_read/_write, u64_*  :func:`tensor_read` ... (tensor_io.cpp:104-152)
 train_step_on_target       :class:`QModelTrainer` (qmodel.cpp:227-433)
+PartialAccumulator & ops   :class:`PartialAccumulator`, :func:`pattn_absorb` ... (attention.cpp:34-203)
 attention_target_rows      :func:`attention_target_rows` (qmodel.cpp:384-407)
 partition_/ivf_/qmodel_ load/save  (partition.cpp:260-296, qmodel.cpp:530-589)
 assign_keys                :func:`assign_keys`  (partition.cpp:191-198)
@@ -477,6 +478,92 @@ def qmodel_read(dir_path) -> dict:
 
 def qmodel_load(dir_path, ctx: Optional[Context] = None) -> "QModel":
     return QModel(qmodel_read(dir_path), ctx)
+
+
+# --------------------------------------------------------------------------
+class PartialAccumulator:
+    """saap::PartialAccumulator (attention.hpp:30-39) on the device: fp64
+    out_acc [heads x value_dim], sumexp, runmax; updated bit-exactly like the
+    reference by :func:`pattn_absorb`, :func:`merge_into`, ..."""
+
+    def __init__(self, heads: int, value_dim: int, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.heads_, self.value_dim = int(heads), int(value_dim)
+        h = C.c_void_p()
+        _check(lib().saap_accum_create(self.ctx.h, _u64(heads), _u64(value_dim), C.byref(h)))
+        self.h = h
+
+    def heads(self):
+        return self.heads_
+
+    def state(self):
+        """(out_acc, sumexp, runmax) as fp64 arrays."""
+        out = np.empty((self.heads_, self.value_dim))
+        se, rm = np.empty(self.heads_), np.empty(self.heads_)
+        _check(lib().saap_accum_read(self.ctx.h, self.h, _p(out), _p(se), _p(rm)))
+        return out, se, rm
+
+    def set_state(self, out_acc, sumexp, runmax):
+        o, se, rm = _f64(out_acc), _f64(sumexp), _f64(runmax)
+        _check(lib().saap_accum_write(self.ctx.h, self.h, _p(o), _p(se), _p(rm)))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().saap_accum_destroy(self.h)
+            self.h = None
+
+
+def pattn_absorb(acc: PartialAccumulator, q_group, keys, values, ids) -> None:
+    """attention.cpp:85-89."""
+    q, k, v = _f32(q_group), _f32(keys), _f32(values)
+    ids = np.ascontiguousarray(ids, np.uint64)
+    _check(lib().saap_pattn_absorb(acc.ctx.h, acc.h, _p(q), _u64(q.shape[0]), _u64(q.shape[1]),
+                                   _p(k), _p(v), _u64(k.shape[0]), _u64(v.shape[0]),
+                                   _u64(v.shape[1]), _p(ids), _u64(ids.size)))
+
+
+def pattn_absorb_range(acc: PartialAccumulator, q_group, keys, values, begin, end) -> None:
+    """attention.cpp:91-100."""
+    q, k, v = _f32(q_group), _f32(keys), _f32(values)
+    _check(lib().saap_pattn_absorb_range(acc.ctx.h, acc.h, _p(q), _u64(q.shape[0]), _u64(q.shape[1]),
+                                         _p(k), _p(v), _u64(k.shape[0]), _u64(v.shape[0]),
+                                         _u64(v.shape[1]), _u64(begin), _u64(end)))
+
+
+def merge_into(acc: PartialAccumulator, part: PartialAccumulator) -> None:
+    """attention.cpp:102-128."""
+    _check(lib().saap_merge_into(acc.ctx.h, acc.h, part.h))
+
+
+def merge_partials(parts: Sequence[PartialAccumulator]) -> PartialAccumulator:
+    """attention.cpp:130-139."""
+    if not parts:
+        raise InvalidArgument("merge_partials: empty list")
+    out = PartialAccumulator(parts[0].heads_, parts[0].value_dim, parts[0].ctx)
+    arr = (C.c_void_p * len(parts))(*[p.h.value for p in parts])
+    _check(lib().saap_merge_partials(out.ctx.h, arr, _u64(len(parts)), out.h))
+    return out
+
+
+def pattn_finalize(acc: PartialAccumulator):
+    """attention.cpp:141-161 -> (output [heads x value_dim] f32, any_empty)."""
+    out = np.empty((acc.heads_, acc.value_dim), np.float32)
+    e = C.c_int()
+    _check(lib().saap_pattn_finalize(acc.ctx.h, acc.h, _p(out), C.byref(e)))
+    return out, bool(e.value)
+
+
+def attention_over_ids(q_group, keys, values, ids, ctx: Optional[Context] = None):
+    """attention.cpp:197-203 -> (output, any_empty)."""
+    ctx = ctx or default_context()
+    q, k, v = _f32(q_group), _f32(keys), _f32(values)
+    ids = np.ascontiguousarray(ids, np.uint64)
+    out = np.empty((q.shape[0], v.shape[1]), np.float32)
+    e = C.c_int()
+    _check(lib().saap_attention_over_ids(ctx.h, _p(q), _u64(q.shape[0]), _u64(q.shape[1]), _p(k),
+                                         _p(v), _u64(k.shape[0]), _u64(v.shape[0]), _u64(v.shape[1]),
+                                         _p(ids), _u64(ids.size), _p(out), C.byref(e)))
+    return out, bool(e.value)
 
 
 # --------------------------------------------------------------------------

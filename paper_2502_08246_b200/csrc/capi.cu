@@ -43,6 +43,16 @@ void launch_derope(const float* x, const double* cs, uint64_t rows, uint32_t D, 
                    cudaStream_t st);
 void launch_debug_exp(const double* x, uint64_t n, double* y, cudaStream_t st);
 uint32_t km_dim_max(uint32_t D);
+void launch_acc_init(double* out, double* sumexp, double* runmax, uint32_t H, uint32_t dv,
+                     cudaStream_t st);
+void launch_acc_absorb(const float* q, uint32_t H, uint32_t d, const float* K, const float* V,
+                       uint32_t n, uint32_t dv, double scale, double* S, double* rescale,
+                       double* out, double* sumexp, double* runmax, cudaStream_t st);
+void launch_acc_merge(double* out, double* sumexp, double* runmax, const double* p_out,
+                      const double* p_sumexp, const double* p_runmax, uint32_t H, uint32_t dv,
+                      cudaStream_t st);
+void launch_acc_finalize(const double* out_acc, const double* sumexp, uint32_t H, uint32_t dv,
+                         float* out, int* any_empty, cudaStream_t st);
 void launch_append_rows(int D, const GroupMeta* meta, uint32_t n_groups, uint32_t k,
                         const uint16_t* Ksrc, const uint16_t* Vsrc, uint16_t* Kdst, uint16_t* Vdst,
                         cudaStream_t st);
@@ -1494,6 +1504,221 @@ int saap_attention_target(saap_ctx* c, const float* q, uint64_t n, uint64_t d, c
         d2h(out, b + o_out, n * C * 8, st);
         sync(c);
     });
+}
+
+// ---------------------------------------------------------------- accumulators
+// PartialAccumulator and its operations (attention.hpp:30-70, attention.cpp:
+// 34-161, 197-203), fp64 on the device, bit-exact (accum.cu).
+int saap_accum_create(saap_ctx* c, uint64_t heads, uint64_t value_dim, saap_accum** out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(out, "accumulator: out");
+        auto* a = new saap_accum();
+        std::unique_ptr<saap_accum> hold(a);
+        a->ctx = c;
+        a->heads = heads;
+        a->dv = value_dim;
+        a->out = dmalloc<double>(std::max<uint64_t>(heads * value_dim, 1));
+        a->sumexp = dmalloc<double>(std::max<uint64_t>(heads, 1));
+        a->runmax = dmalloc<double>(std::max<uint64_t>(heads, 1));
+        a->rescale = dmalloc<double>(std::max<uint64_t>(heads, 1));
+        if (heads) launch_acc_init(a->out, a->sumexp, a->runmax, (uint32_t)heads, (uint32_t)value_dim, c->stream);
+        sync(c);
+        *out = hold.release();
+    });
+}
+
+int saap_accum_destroy(saap_accum* a) {
+    return guard([&] {
+        if (!a) return;
+        cudaSetDevice(a->ctx->device);
+        dfree(a->out);
+        dfree(a->sumexp);
+        dfree(a->runmax);
+        dfree(a->rescale);
+        delete a;
+    });
+}
+
+int saap_accum_read(saap_ctx* c, const saap_accum* a, double* out_acc, double* sumexp, double* runmax) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(a, "accumulator");
+        if (out_acc) d2h(out_acc, a->out, a->heads * a->dv * 8, c->stream);
+        if (sumexp) d2h(sumexp, a->sumexp, a->heads * 8, c->stream);
+        if (runmax) d2h(runmax, a->runmax, a->heads * 8, c->stream);
+        sync(c);
+    });
+}
+
+int saap_accum_write(saap_ctx* c, saap_accum* a, const double* out_acc, const double* sumexp,
+                     const double* runmax) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(a, "accumulator");
+        if (out_acc) h2d(a->out, out_acc, a->heads * a->dv * 8, c->stream);
+        if (sumexp) h2d(a->sumexp, sumexp, a->heads * 8, c->stream);
+        if (runmax) h2d(a->runmax, runmax, a->heads * 8, c->stream);
+        sync(c);
+    });
+}
+
+// shared absorb: validation as absorb_impl (:38-48), rows staged by id order
+static void absorb_rows(saap_ctx* c, saap_accum* a, const float* q, uint64_t G, uint64_t d,
+                        const float* keys, const float* values, uint64_t n_rows, uint64_t dv,
+                        const uint64_t* ids, uint64_t begin, uint64_t count) {
+    need(a, "accumulator");
+    if (a->heads != G || a->dv != dv)
+        invalid("pattn_absorb: accumulator " + std::to_string(a->heads) + "x" +
+                std::to_string(a->dv) + " does not fit group " + std::to_string(G) + "x" +
+                std::to_string(dv));
+    if (count == 0 || G == 0) return;
+    need(q, "pattn_absorb: queries");
+    need(keys, "pattn_absorb: keys");
+    need(values, "pattn_absorb: values");
+    if (ids)
+        for (uint64_t j = 0; j < count; ++j)
+            if (ids[j] >= n_rows)
+                invalid("pattn_absorb: key id " + std::to_string(ids[j]) + " out of range");
+    if (count >= 0xFFFFFFFFull || d == 0) unsupported("pattn_absorb: shape");
+    std::vector<float> Ks(count * d), Vs(count * dv);
+    for (uint64_t j = 0; j < count; ++j) {
+        const uint64_t r = ids ? ids[j] : begin + j;
+        std::memcpy(&Ks[j * d], keys + r * d, d * 4);
+        std::memcpy(&Vs[j * dv], values + r * dv, dv * 4);
+    }
+    const cudaStream_t st = c->stream;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        size_t r = o;
+        o += (bytes + 255) & ~size_t(255);
+        return r;
+    };
+    const size_t o_q = take(G * d * 4), o_k = take(count * d * 4), o_v = take(count * dv * 4),
+                 o_s = take(G * count * 8);
+    char* b = (char*)ensure(c, c->misc, o);
+    h2d(b + o_q, q, G * d * 4, st);
+    h2d(b + o_k, Ks.data(), count * d * 4, st);
+    h2d(b + o_v, Vs.data(), count * dv * 4, st);
+    launch_acc_absorb((const float*)(b + o_q), (uint32_t)G, (uint32_t)d, (const float*)(b + o_k),
+                      (const float*)(b + o_v), (uint32_t)count, (uint32_t)dv,
+                      1.0 / std::sqrt((double)d), (double*)(b + o_s), a->rescale, a->out, a->sumexp,
+                      a->runmax, st);
+    c->launches += 3;
+    sync(c);
+}
+
+int saap_pattn_absorb(saap_ctx* c, saap_accum* a, const float* q, uint64_t G, uint64_t d,
+                      const float* keys, const float* values, uint64_t n_keys, uint64_t n_values,
+                      uint64_t dv, const uint64_t* ids, uint64_t count) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        if (n_keys != n_values)
+            invalid("attention: " + std::to_string(n_keys) + " keys vs " + std::to_string(n_values) +
+                    " values");
+        if (count) need(ids, "pattn_absorb: ids");
+        absorb_rows(c, a, q, G, d, keys, values, n_keys, dv, ids, 0, count);
+    });
+}
+
+int saap_pattn_absorb_range(saap_ctx* c, saap_accum* a, const float* q, uint64_t G, uint64_t d,
+                            const float* keys, const float* values, uint64_t n_keys,
+                            uint64_t n_values, uint64_t dv, uint64_t begin, uint64_t end) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        if (end > n_keys || begin > end)
+            invalid("pattn_absorb_range: bad range [" + std::to_string(begin) + ", " +
+                    std::to_string(end) + ")");
+        if (n_keys != n_values)
+            invalid("attention: " + std::to_string(n_keys) + " keys vs " + std::to_string(n_values) +
+                    " values");
+        absorb_rows(c, a, q, G, d, keys, values, n_keys, dv, nullptr, begin, end - begin);
+    });
+}
+
+int saap_merge_into(saap_ctx* c, saap_accum* a, const saap_accum* part) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(a, "merge_into: accumulator");
+        need(part, "merge_into: part");
+        if (a->heads != part->heads || a->dv != part->dv)
+            invalid("merge_into: accumulator shapes differ");
+        if (!a->heads) return;
+        launch_acc_merge(a->out, a->sumexp, a->runmax, part->out, part->sumexp, part->runmax,
+                         (uint32_t)a->heads, (uint32_t)a->dv, c->stream);
+        c->launches++;
+        sync(c);
+    });
+}
+
+// merge_partials(parts): result = parts[0] merged with parts[1..] in order
+int saap_merge_partials(saap_ctx* c, const saap_accum* const* parts, uint64_t n, saap_accum* out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        if (n == 0) invalid("merge_partials: empty list");
+        need(parts, "merge_partials: parts");
+        need(out, "merge_partials: out");
+        const saap_accum* p0 = parts[0];
+        need(p0, "merge_partials: part");
+        if (out->heads != p0->heads || out->dv != p0->dv) invalid("merge_into: accumulator shapes differ");
+        const cudaStream_t st = c->stream;
+        if (out != p0) {
+            SAAP_CUDA(cudaMemcpyAsync(out->out, p0->out, p0->heads * p0->dv * 8, cudaMemcpyDeviceToDevice, st));
+            SAAP_CUDA(cudaMemcpyAsync(out->sumexp, p0->sumexp, p0->heads * 8, cudaMemcpyDeviceToDevice, st));
+            SAAP_CUDA(cudaMemcpyAsync(out->runmax, p0->runmax, p0->heads * 8, cudaMemcpyDeviceToDevice, st));
+        }
+        for (uint64_t i = 1; i < n; ++i) {
+            need(parts[i], "merge_partials: part");
+            if (parts[i]->heads != out->heads || parts[i]->dv != out->dv)
+                invalid("merge_into: accumulator shapes differ");
+            if (!out->heads) continue;
+            launch_acc_merge(out->out, out->sumexp, out->runmax, parts[i]->out, parts[i]->sumexp,
+                             parts[i]->runmax, (uint32_t)out->heads, (uint32_t)out->dv, st);
+            c->launches++;
+        }
+        sync(c);
+    });
+}
+
+int saap_pattn_finalize(saap_ctx* c, const saap_accum* a, float* out, int* any_empty) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(a, "pattn_finalize: accumulator");
+        need(out, "pattn_finalize: out");
+        const cudaStream_t st = c->stream;
+        char* b = (char*)ensure(c, c->misc, a->heads * a->dv * 4 + 256);
+        int* flag = (int*)b;
+        float* dout = (float*)(b + 256);
+        SAAP_CUDA(cudaMemsetAsync(flag, 0, 4, st));
+        if (a->heads) {
+            launch_acc_finalize(a->out, a->sumexp, (uint32_t)a->heads, (uint32_t)a->dv, dout, flag, st);
+            c->launches++;
+        }
+        int fl = 0;
+        d2h(out, dout, a->heads * a->dv * 4, st);
+        d2h(&fl, flag, 4, st);
+        sync(c);
+        if (any_empty) *any_empty = fl;
+    });
+}
+
+// attention_over_ids(q, keys, values, ids): one absorb into a fresh
+// accumulator, then finalize (attention.cpp:197-203)
+int saap_attention_over_ids(saap_ctx* c, const float* q, uint64_t G, uint64_t d, const float* keys,
+                            const float* values, uint64_t n_keys, uint64_t n_values, uint64_t dv,
+                            const uint64_t* ids, uint64_t count, float* out, int* any_empty) {
+    saap_accum* a = nullptr;
+    int rc = saap_accum_create(c, G, dv, &a);
+    if (rc != SAAP_OK) return rc;
+    rc = saap_pattn_absorb(c, a, q, G, d, keys, values, n_keys, n_values, dv, ids, count);
+    if (rc == SAAP_OK) rc = saap_pattn_finalize(c, a, out, any_empty);
+    if (rc != SAAP_OK) {
+        const std::string keep = g_err;
+        saap_accum_destroy(a);
+        g_err = keep;
+        return rc;
+    }
+    return saap_accum_destroy(a);
 }
 
 int saap_rope_remove(saap_ctx* c, const float* x, uint64_t rows, uint64_t d,

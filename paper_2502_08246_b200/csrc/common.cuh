@@ -268,6 +268,17 @@ struct saap_qtrainer {
     float* q32 = nullptr;
 };
 
+// PartialAccumulator on the device (accum.cu): out_acc [heads x dv], sumexp,
+// runmax (fp64), plus absorb scratch.
+struct saap_accum {
+    saap_ctx* ctx = nullptr;
+    uint64_t heads = 0, dv = 0;
+    double* out = nullptr;
+    double* sumexp = nullptr;
+    double* runmax = nullptr;
+    double* rescale = nullptr;
+};
+
 struct saap_router {
     int kind = 0;  // 0 centroid, 1 qmodel
     int use_deroped = 1;
