@@ -155,6 +155,67 @@ KeyAssignment assign_keys(const TB& keys, const P& p) {
     return a;
 }
 
+// PartialAccumulator (attention.hpp:30-39) on the device; the operations
+// below mirror pattn_absorb[_range], merge_into, merge_partials,
+// pattn_finalize and attention_over_ids (attention.cpp:85-203), bit-exact.
+class PartialAccumulator {
+public:
+    PartialAccumulator(std::size_t heads, std::size_t value_dim, Context& ctx = Context::current())
+            : ctx_(&ctx), heads_(heads), dv_(value_dim) {
+        saap_accum* a = nullptr;
+        check(saap_accum_create(ctx.get(), heads, value_dim, &a));
+        h_.reset(a);
+    }
+    std::size_t heads() const { return heads_; }
+    std::size_t value_dim() const { return dv_; }
+    saap_accum* get() const { return h_.get(); }
+    Context& ctx() const { return *ctx_; }
+
+private:
+    struct Del {
+        void operator()(saap_accum* a) const { saap_accum_destroy(a); }
+    };
+    Context* ctx_;
+    std::size_t heads_, dv_;
+    std::unique_ptr<saap_accum, Del> h_;
+};
+
+template <typename TB, typename Ids>
+void pattn_absorb(PartialAccumulator& acc, const TB& q, const TB& keys, const TB& values, const Ids& ids) {
+    const std::vector<std::uint64_t> v(ids.begin(), ids.end());
+    check(saap_pattn_absorb(acc.ctx().get(), acc.get(), q.data.data(), q.rows, q.dim, keys.data.data(),
+                            values.data.data(), keys.rows, values.rows, values.dim, v.data(), v.size()));
+}
+template <typename TB>
+void pattn_absorb_range(PartialAccumulator& acc, const TB& q, const TB& keys, const TB& values,
+                        std::size_t begin, std::size_t end) {
+    check(saap_pattn_absorb_range(acc.ctx().get(), acc.get(), q.data.data(), q.rows, q.dim,
+                                  keys.data.data(), values.data.data(), keys.rows, values.rows,
+                                  values.dim, begin, end));
+}
+inline void merge_into(PartialAccumulator& acc, const PartialAccumulator& part) {
+    check(saap_merge_into(acc.ctx().get(), acc.get(), part.get()));
+}
+inline TensorBlock pattn_finalize(const PartialAccumulator& acc, bool* any_empty = nullptr) {
+    TensorBlock out(acc.heads(), acc.value_dim());
+    int e = 0;
+    check(saap_pattn_finalize(acc.ctx().get(), acc.get(), out.data.data(), &e));
+    if (any_empty) *any_empty = e != 0;
+    return out;
+}
+template <typename TB, typename Ids>
+TensorBlock attention_over_ids(const TB& q, const TB& keys, const TB& values, const Ids& ids,
+                               bool* any_empty = nullptr) {
+    const std::vector<std::uint64_t> v(ids.begin(), ids.end());
+    TensorBlock out(q.rows, values.dim);
+    int e = 0;
+    check(saap_attention_over_ids(Context::current().get(), q.data.data(), q.rows, q.dim,
+                                  keys.data.data(), values.data.data(), keys.rows, values.rows,
+                                  values.dim, v.data(), v.size(), out.data.data(), &e));
+    if (any_empty) *any_empty = e != 0;
+    return out;
+}
+
 // Stand-in for saap::Rng (tensor.hpp:87-131): only the draws kmeans_train
 // makes.  With the reference headers, pass saap::Rng itself.
 class Rng {

@@ -133,6 +133,16 @@ int main() {
                   "kmeans_train too few keys message");
         }
     }
+    // attention_over_ids: fp64 on the device, bit-exact with the reference
+    {
+        std::vector<std::uint64_t> ids;
+        for (std::uint64_t i = 0; i < 700; ++i) ids.push_back((i * 7919) % n);
+        bool e1 = false, e2 = false;
+        saap::TensorBlock a1 = saap::attention_over_ids(qr, p.keys_roped, p.values, ids, &e1);
+        saap_b200::TensorBlock a2 = saap_b200::attention_over_ids(qr, p.keys_roped, p.values, ids, &e2);
+        check(e1 == e2 && std::memcmp(a1.data.data(), a2.data.data(), a1.data.size() * 4) == 0,
+              "attention_over_ids bit-exact");
+    }
     std::printf("%d failed\n", g_fail);
     return g_fail;
 }
