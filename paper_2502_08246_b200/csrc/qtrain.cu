@@ -34,6 +34,7 @@ constexpr double kBnEps = 1e-5;
 constexpr double kLogFloor = 1e-12;
 constexpr int kT = 128;
 constexpr int kU = 8;  // loads issued ahead of each sequential add chain
+constexpr int kP = 16;  // weights per pipeline stage (two stages in flight)
 
 // z[i][j] = (sum_k x[i][k] w1[k][j], k ascending, zero x skipped) + b1[j]
 __global__ void qt_linear1(const float* q, uint32_t n, uint32_t d, uint32_t h, const double* w1,
@@ -100,17 +101,25 @@ __global__ void qt_linear2(const double* r, uint32_t n, uint32_t h, uint32_t C, 
     if (c >= C) return;
     double s = 0.0;
     const double* rr = r + (size_t)i * h;
-    uint32_t k = 0;
-    for (; k + kU <= h; k += kU) {
-        double a[kU], w[kU];
+    // two stages of kP weights in flight ahead of the ordered chain
+    const uint32_t kfull = h / kP * kP;
+    double wa[kP], wb[kP];
+    if (kfull) {
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            a[u] = rr[k + u];
-            w[u] = w2[(size_t)(k + u) * C + c];
+        for (int u = 0; u < kP; ++u) wa[u] = w2[(size_t)u * C + c];
+    }
+    uint32_t k = 0;
+    for (; k < kfull; k += kP) {
+        const bool more = k + kP < kfull;
+#pragma unroll
+        for (int u = 0; u < kP; ++u) wb[u] = more ? w2[(size_t)(k + kP + u) * C + c] : 0.0;
+#pragma unroll
+        for (int u = 0; u < kP; ++u) {
+            const double a = rr[k + u];
+            if (a != 0.0) s += a * wa[u];
         }
 #pragma unroll
-        for (int u = 0; u < kU; ++u)
-            if (a[u] != 0.0) s += a[u] * w[u];
+        for (int u = 0; u < kP; ++u) wa[u] = wb[u];
     }
     for (; k < h; ++k) {
         const double a = rr[k];
@@ -240,16 +249,21 @@ __global__ void qt_dy(const double* dl, const double* w2T, const double* y, uint
     if (j >= h) return;
     const double* dr = dl + (size_t)i * C;
     double s = 0.0;
+    const uint32_t cfull = C / kP * kP;
+    double wa[kP], wb[kP];
+    if (cfull) {
+#pragma unroll
+        for (int u = 0; u < kP; ++u) wa[u] = w2T[(size_t)u * h + j];
+    }
     uint32_t c = 0;
-    for (; c + kU <= C; c += kU) {
-        double a[kU], w[kU];
+    for (; c < cfull; c += kP) {
+        const bool more = c + kP < cfull;
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            a[u] = dr[c + u];
-            w[u] = w2T[(size_t)(c + u) * h + j];
-        }
+        for (int u = 0; u < kP; ++u) wb[u] = more ? w2T[(size_t)(c + kP + u) * h + j] : 0.0;
 #pragma unroll
-        for (int u = 0; u < kU; ++u) s += a[u] * w[u];
+        for (int u = 0; u < kP; ++u) s += dr[c + u] * wa[u];
+#pragma unroll
+        for (int u = 0; u < kP; ++u) wa[u] = wb[u];
     }
     for (; c < C; ++c) s += dr[c] * w2T[(size_t)c * h + j];
     const size_t o = (size_t)i * h + j;
