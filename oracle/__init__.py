@@ -409,6 +409,19 @@ class Ref:
                                               _p(rm), _p(res), C.byref(e)))
         return res, bool(e.value)
 
+    def build_context_store_kmeans(self, keys_roped, values, rope_base, n_buckets, iters, sink, seed):
+        kr, v = _f32(keys_roped), _f32(values)
+        n, d = kr.shape
+        cent = np.empty((n_buckets, d), np.float32)
+        a = np.empty(n - sink, np.uint32)
+        off = np.empty(n_buckets + 1, np.uint64)
+        idx = np.empty(n - sink, np.uint64)
+        obj = np.empty(iters, np.float64)
+        self._chk(self.lib.ref_build_context_store_kmeans(
+            _p(kr), _p(v), _u64(n), _u64(d), C.c_double(rope_base), _u64(n_buckets), _u64(iters),
+            _u64(sink), _u64(seed), _p(cent), _p(a), _p(off), _p(idx), _p(obj)))
+        return cent, a, off, idx, obj
+
     def assign_keys(self, keys, cent, threads=1):
         keys, cent = _f32(keys), _f32(cent)
         out = np.empty(keys.shape[0], np.uint32)

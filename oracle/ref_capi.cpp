@@ -675,3 +675,25 @@ int ref_finalize_state(std::uint64_t H, std::uint64_t dv, const double* out, con
     });
 }
 }  // extern "C"
+
+extern "C" {
+// build_context_store(keys_roped, values, rope, C, iters, sink, Rng(seed), &stats)
+// (attention.cpp:238-246) -> trained centroids + the store's index
+int ref_build_context_store_kmeans(const float* keys_roped, const float* values, std::uint64_t n,
+                                   std::uint64_t d, double rope_base, std::uint64_t C,
+                                   std::uint64_t iters, std::uint64_t sink, std::uint64_t seed,
+                                   float* centroids, std::uint32_t* assignment, std::uint64_t* off,
+                                   std::uint64_t* idx, double* objective) {
+    return guard([&] {
+        Rng rng(seed);
+        KMeansStats st;
+        ContextStore s = build_context_store(block(keys_roped, n, d), block(values, n, d),
+                                             RopeConfig{d, rope_base}, C, iters, sink, rng, &st);
+        put(s.partition.centroids, centroids);
+        std::copy(s.assignment.bucket_of.begin(), s.assignment.bucket_of.end(), assignment);
+        std::copy(s.index.off.begin(), s.index.off.end(), off);
+        std::copy(s.index.idx.begin(), s.index.idx.end(), idx);
+        std::copy(st.objective_per_iter.begin(), st.objective_per_iter.end(), objective);
+    });
+}
+}  // extern "C"

@@ -953,6 +953,31 @@ def build_context_store(keys_roped, values, rope_base, partition: Partition, sin
     return st
 
 
+def build_context_store_kmeans(keys_roped, values, rope_base, n_buckets, kmeans_iters,
+                               sink_count, rng: "Rng", stats: Optional["KMeansStats"] = None,
+                               recent_hint=2047, ctx: Optional[Context] = None) -> ContextStore:
+    """build_context_store(keys_roped, values, rope, C, kmeans_iters, sink, rng,
+    stats) (attention.cpp:238-246): de-rope the non-sink keys on the device
+    (glibc-exact table), train the partition with the device k-means, build
+    the store.  The trained partition is ``store.partition``."""
+    kr = _f32(keys_roped)
+    v = _f32(values)
+    if kr.shape[0] != v.shape[0]:
+        raise InvalidArgument(f"attention: {kr.shape[0]} keys vs {v.shape[0]} values")
+    if kr.shape[0] <= sink_count:
+        raise InvalidArgument(f"build_context_store: no keys left to index after {sink_count} "
+                              "sink keys")
+    ctx = ctx or default_context()
+    pos = np.arange(sink_count, kr.shape[0], dtype=np.uint64)
+    deroped = rope_remove_block(kr[sink_count:], pos, rope_base, ctx)
+    part = kmeans_train(deroped, n_buckets, kmeans_iters, rng, stats, ctx)
+    kd = np.concatenate([kr[:sink_count], deroped]) if sink_count else deroped
+    st = build_context_store(kr, v, rope_base, part, sink_count, keys_deroped=kd,
+                             recent_hint=recent_hint)
+    st.partition = part
+    return st
+
+
 def sparse_attention(q_group_roped, q_group_deroped, store: ContextStore, router: BucketRouter,
                      cfg: SparseAttnConfig) -> AttnResult:
     qr = _f32(q_group_roped)[None]

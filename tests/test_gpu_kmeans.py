@@ -97,3 +97,23 @@ def test_assign_keys_other_dims(ctx, d):
     got = sb.assign_keys(keys, sb.Partition(cent, ctx))
     assert np.array_equal(got, oracle.port().assign_keys(keys, cent))
     assert got[7] == 0 and got[11] == 5
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+def test_build_context_store_with_kmeans_training(ctx):
+    """build_context_store(keys_roped, values, rope, C, iters, sink, rng, stats)
+    (attention.cpp:238-246): device de-rope + device k-means + build equal the
+    reference's centroids, objective, assignments and index bit-exactly."""
+    import paper_2502_08246_b200 as sb
+    R = oracle.ref()
+    spec = oracle.HeadSpec(dim=64, seed=4, drift_rate=5e-4)
+    p = R.generate_prompt(spec, 6000, 1, 2)
+    cent, a, off, idx, obj = R.build_context_store_kmeans(p["keys_roped"], p["values"], 500000.0,
+                                                          64, 4, 1, 17)
+    st = sb.KMeansStats()
+    store = sb.build_context_store_kmeans(p["keys_roped"], p["values"], 500000.0, 64, 4, 1,
+                                          sb.Rng(17), st, ctx=ctx)
+    assert np.array_equal(_bits(store.partition.centroids), _bits(cent))
+    assert np.array_equal(_bits(np.array(st.objective_per_iter)), _bits(obj))
+    ga, gix = store.read_index(0)
+    assert np.array_equal(ga, a) and np.array_equal(gix.off, off) and np.array_equal(gix.idx, idx)
