@@ -119,6 +119,10 @@ SAAP_API int saap_router_select(saap_ctx* ctx, const saap_router* r, const float
 SAAP_API int saap_batched_bucket_select(saap_ctx* ctx, const saap_qmodel* m, const float* q_deroped,
                                uint64_t G, uint64_t dim, uint64_t l, uint32_t* out);
 
+/* qmodel_forward(model, queries_deroped) eval mode (qmodel.cpp:375-377):
+ * [n x C] probabilities (fp64 on the device, f32 out like Mat::to_tensor). */
+SAAP_API int saap_qmodel_forward(saap_ctx* ctx, const saap_qmodel* m, const float* q_deroped,
+                                 uint64_t n, uint64_t dim, float* out);
 /* ---- key assignment and IVF ------------------------------------------ */
 /* assign_keys(keys, partition)               partition.cpp:191-198 */
 SAAP_API int saap_assign_keys(saap_ctx* ctx, const saap_partition* p, const float* keys, uint64_t n,

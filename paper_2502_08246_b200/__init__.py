@@ -385,6 +385,15 @@ class QModelRouter(BucketRouter):
         self.h = h
 
 
+def qmodel_forward(model: QModel, queries_deroped) -> np.ndarray:
+    """Eval-mode forward (qmodel.cpp:375-377): [n x C] probabilities (f32)."""
+    q = _f32(queries_deroped)
+    out = np.empty((q.shape[0], model.C), np.float32)
+    _check(lib().saap_qmodel_forward(model.ctx.h, model.h, _p(q), _u64(q.shape[0]),
+                                     _u64(q.shape[1]), _p(out)))
+    return out
+
+
 def batched_bucket_select(model: QModel, query_group, l) -> np.ndarray:
     q = _f32(query_group)
     out = np.empty(max(int(l), 0), np.uint32)

@@ -1163,6 +1163,46 @@ int saap_batched_bucket_select(saap_ctx* c, const saap_qmodel* m, const float* q
     });
 }
 
+// qmodel_forward(model, queries_deroped) in eval mode (qmodel.cpp:375-377):
+// row-softmax probabilities, fp64 on the device, narrowed to f32 like
+// Mat::to_tensor.  Same kernels as the router (route.cu).
+int saap_qmodel_forward(saap_ctx* c, const saap_qmodel* m, const float* q, uint64_t n, uint64_t d,
+                        float* out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(m, "model");
+        if (d != m->d)
+            invalid("qmodel: query dim " + std::to_string(d) + " does not match model dim " +
+                    std::to_string(m->d));
+        if (n == 0) invalid("qmodel: empty query batch");
+        need(q, "qmodel_forward: queries");
+        need(out, "qmodel_forward: out");
+        const cudaStream_t st = c->stream;
+        const uint64_t C = m->C;
+        float* dq = (float*)ensure(c, c->qd, n * d * 4);
+        double* probs = (double*)ensure(c, c->probs, n * (C + m->h) * 8);
+        void** dptr = (void**)ensure(c, c->misc, 3 * sizeof(void*));
+        const void* ptrs[3] = {m->w1, m->w2, m->vec};
+        h2d(dq, q, n * d * 4, st);
+        h2d(dptr, ptrs, sizeof ptrs, st);
+        QModelArgs qa{};
+        qa.q = dq;
+        qa.prm = (const double* const*)dptr;
+        qa.G = (uint32_t)n;
+        qa.d = (uint32_t)d;
+        qa.h = (uint32_t)m->h;
+        qa.C = (uint32_t)C;
+        qa.probs = probs;
+        qa.hid = probs + n * C;
+        launch_qmodel_probs(qa, 1, st);
+        c->launches += 3;
+        std::vector<double> p64(n * C);
+        d2h(p64.data(), probs, n * C * 8, st);
+        sync(c);
+        for (uint64_t i = 0; i < n * C; ++i) out[i] = (float)p64[i];
+    });
+}
+
 // ============================================================ assignment / IVF / rope
 int saap_assign_keys(saap_ctx* c, const saap_partition* p, const float* keys, uint64_t n,
                      uint64_t d, uint32_t* out) {

@@ -346,3 +346,18 @@ def test_coverage_matches_oracle(ctx, port, hint, recent):
     got = sb.attention_mass_coverage(case["qr"][:4], st, sel, sb.DenseWindow(1, recent))
     want = port.coverage(case["qr"][:4], case["K"], 1, a, 128, sel, recent)
     assert abs(got - want) <= 1e-4 * max(1.0, abs(want))
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="needs oracle/_ref")
+def test_qmodel_forward_bit_exact(ctx):
+    """qmodel_forward eval mode (qmodel.cpp:375-377): probabilities identical."""
+    R = oracle.ref()
+    m = R.qmodel_init(64, 256, 96, 3)
+    rs = np.random.RandomState(8)
+    m["bn_run_mean"] = rs.randn(1, 256) * 0.1
+    m["bn_run_var"] = 1 + rs.rand(1, 256)
+    q = rs.randn(7, 64).astype(np.float32)
+    q[2, :10] = 0.0
+    got = sb.qmodel_forward(sb.QModel(m, ctx), q)
+    want = R.qmodel_forward(m, q)
+    assert np.array_equal(got.view(np.uint32), np.asarray(want, np.float32).view(np.uint32))
