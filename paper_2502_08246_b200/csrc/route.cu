@@ -42,18 +42,27 @@ __global__ void __launch_bounds__(kQmT) qm_hidden_kernel(QModelArgs a) {
         double z[kQmRows];
 #pragma unroll
         for (int i = 0; i < kQmRows; ++i) z[i] = 0.0;
+        constexpr int P = kQmP;  // two stages of W1 loads in flight
+        const uint32_t kfull = a.d / P * P;
+        double wa[P], wb[P];
+        if (kfull) {
+#pragma unroll
+            for (int u = 0; u < P; ++u) wa[u] = w1[(size_t)u * a.h + j];
+        }
         uint32_t k = 0;
-        for (; k + kQmU <= a.d; k += kQmU) {
-            double w[kQmU];
+        for (; k < kfull; k += P) {
+            const bool more = k + P < kfull;
 #pragma unroll
-            for (int u = 0; u < kQmU; ++u) w[u] = w1[(size_t)(k + u) * a.h + j];
+            for (int u = 0; u < P; ++u) wb[u] = more ? w1[(size_t)(k + P + u) * a.h + j] : 0.0;
 #pragma unroll
-            for (int u = 0; u < kQmU; ++u)
+            for (int u = 0; u < P; ++u)
 #pragma unroll
                 for (int i = 0; i < kQmRows; ++i) {
                     const double av = xs[i * a.d + k + u];
-                    if ((uint32_t)i < nr && av != 0.0) z[i] = __dadd_rn(z[i], __dmul_rn(av, w[u]));
+                    if ((uint32_t)i < nr && av != 0.0) z[i] = __dadd_rn(z[i], __dmul_rn(av, wa[u]));
                 }
+#pragma unroll
+            for (int u = 0; u < P; ++u) wa[u] = wb[u];
         }
         for (; k < a.d; ++k) {
             const double w = w1[(size_t)k * a.h + j];
