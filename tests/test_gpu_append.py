@@ -110,3 +110,32 @@ def test_capacity_layout_device_build_tcgen05(ctx, port):
         assert np.array_equal(ga, a) and np.array_equal(gix.off, off) and np.array_equal(gix.idx, idx)
         assert (stats[i].keys_scored, stats[i].max_visited_bucket) == (ks, mv)
         assert max_rel_diff(out[i], w) <= TOL
+
+
+def test_append_with_qmodel_router(ctx, port):
+    """Appends under the Q-model router (the learned SAAP classifier)."""
+    import oracle
+    if not oracle.ref_available():
+        pytest.skip("needs oracle/_ref for qmodel_init")
+    C, d, hint, n0, grow = 64, 64, 400, 2500, 300
+    m = oracle.ref().qmodel_init(d, 128, C, 5)
+    case = make_case(d=d, n=n0 + grow, C=C, n_q=4, seed=77, use_ref=False)
+    p = sb.Partition(case["cent"], ctx)
+    L = sb.Layer([n0], d, C, 1, hint, ctx, capacity=n0 + grow)
+    L.build([p], case["K"][:n0], case["V"][:n0], case["Kd"][:n0])
+    r = [sb.QModelRouter(sb.QModel(m, ctx))]
+    q = case["qr"][None, :4]
+    n = n0
+    for k in (3, 297):
+        L.append(case["K"][None, n:n + k], case["V"][None, n:n + k], case["Kd"][None, n:n + k])
+        n += k
+        cfg = sb.SparseAttnConfig(8, 128, sb.DenseWindow(1, hint))
+        out, stats, sel = L.sparse_attention(r, q, q, cfg, want_selected=True)
+        a = port.assign_keys(case["Kd"][1:n], case["cent"])
+        off, idx = port.build_ivf(a, C)
+        wsel = port.qmodel_select(m, q[0], 8)
+        assert np.array_equal(sel[0], wsel)
+        w, ks, mv, _ = port.sparse_attention(q[0], case["K"][:n], case["V"][:n], 1, off, idx, wsel, 8,
+                                             128, hint)
+        assert (stats[0].keys_scored, stats[0].max_visited_bucket) == (ks, mv)
+        assert max_rel_diff(out[0], w) <= TOL
