@@ -200,13 +200,13 @@ SAAP_API int saap_accum_write(saap_ctx* ctx, saap_accum* a, const double* out_ac
 /* pattn_absorb(acc, q_group, keys, values, ids)          attention.cpp:85-89 */
 SAAP_API int saap_pattn_absorb(saap_ctx* ctx, saap_accum* a, const float* q, uint64_t G, uint64_t dim,
                                const float* keys, const float* values, uint64_t n_keys,
-                               uint64_t n_values, uint64_t value_dim, const uint64_t* ids,
-                               uint64_t count);
+                               uint64_t key_dim, uint64_t n_values, uint64_t value_dim,
+                               const uint64_t* ids, uint64_t count);
 /* pattn_absorb_range(acc, q_group, keys, values, begin, end)  attention.cpp:91-100 */
 SAAP_API int saap_pattn_absorb_range(saap_ctx* ctx, saap_accum* a, const float* q, uint64_t G,
                                      uint64_t dim, const float* keys, const float* values,
-                                     uint64_t n_keys, uint64_t n_values, uint64_t value_dim,
-                                     uint64_t begin, uint64_t end);
+                                     uint64_t n_keys, uint64_t key_dim, uint64_t n_values,
+                                     uint64_t value_dim, uint64_t begin, uint64_t end);
 /* merge_into(acc, part) / merge_partials(parts)           attention.cpp:102-139 */
 SAAP_API int saap_merge_into(saap_ctx* ctx, saap_accum* a, const saap_accum* part);
 SAAP_API int saap_merge_partials(saap_ctx* ctx, const saap_accum* const* parts, uint64_t n,
@@ -216,8 +216,9 @@ SAAP_API int saap_pattn_finalize(saap_ctx* ctx, const saap_accum* a, float* out,
 /* attention_over_ids(q_group, keys, values, ids, &any_empty) attention.cpp:197-203 */
 SAAP_API int saap_attention_over_ids(saap_ctx* ctx, const float* q, uint64_t G, uint64_t dim,
                                      const float* keys, const float* values, uint64_t n_keys,
-                                     uint64_t n_values, uint64_t value_dim, const uint64_t* ids,
-                                     uint64_t count, float* out, int* any_empty);
+                                     uint64_t key_dim, uint64_t n_values, uint64_t value_dim,
+                                     const uint64_t* ids, uint64_t count, float* out,
+                                     int* any_empty);
 
 /* rope_remove_block(keys, positions, {dim, base})  rope.cpp:87-90 */
 SAAP_API int saap_rope_remove(saap_ctx* ctx, const float* x, uint64_t rows, uint64_t dim,

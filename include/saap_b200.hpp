@@ -184,14 +184,15 @@ template <typename TB, typename Ids>
 void pattn_absorb(PartialAccumulator& acc, const TB& q, const TB& keys, const TB& values, const Ids& ids) {
     const std::vector<std::uint64_t> v(ids.begin(), ids.end());
     check(saap_pattn_absorb(acc.ctx().get(), acc.get(), q.data.data(), q.rows, q.dim, keys.data.data(),
-                            values.data.data(), keys.rows, values.rows, values.dim, v.data(), v.size()));
+                            values.data.data(), keys.rows, keys.dim, values.rows, values.dim, v.data(),
+                            v.size()));
 }
 template <typename TB>
 void pattn_absorb_range(PartialAccumulator& acc, const TB& q, const TB& keys, const TB& values,
                         std::size_t begin, std::size_t end) {
     check(saap_pattn_absorb_range(acc.ctx().get(), acc.get(), q.data.data(), q.rows, q.dim,
-                                  keys.data.data(), values.data.data(), keys.rows, values.rows,
-                                  values.dim, begin, end));
+                                  keys.data.data(), values.data.data(), keys.rows, keys.dim,
+                                  values.rows, values.dim, begin, end));
 }
 inline void merge_into(PartialAccumulator& acc, const PartialAccumulator& part) {
     check(saap_merge_into(acc.ctx().get(), acc.get(), part.get()));
@@ -210,8 +211,8 @@ TensorBlock attention_over_ids(const TB& q, const TB& keys, const TB& values, co
     TensorBlock out(q.rows, values.dim);
     int e = 0;
     check(saap_attention_over_ids(Context::current().get(), q.data.data(), q.rows, q.dim,
-                                  keys.data.data(), values.data.data(), keys.rows, values.rows,
-                                  values.dim, v.data(), v.size(), out.data.data(), &e));
+                                  keys.data.data(), values.data.data(), keys.rows, keys.dim,
+                                  values.rows, values.dim, v.data(), v.size(), out.data.data(), &e));
     if (any_empty) *any_empty = e != 0;
     return out;
 }

@@ -527,7 +527,7 @@ def pattn_absorb(acc: PartialAccumulator, q_group, keys, values, ids) -> None:
     q, k, v = _f32(q_group), _f32(keys), _f32(values)
     ids = np.ascontiguousarray(ids, np.uint64)
     _check(lib().saap_pattn_absorb(acc.ctx.h, acc.h, _p(q), _u64(q.shape[0]), _u64(q.shape[1]),
-                                   _p(k), _p(v), _u64(k.shape[0]), _u64(v.shape[0]),
+                                   _p(k), _p(v), _u64(k.shape[0]), _u64(k.shape[1]), _u64(v.shape[0]),
                                    _u64(v.shape[1]), _p(ids), _u64(ids.size)))
 
 
@@ -535,8 +535,8 @@ def pattn_absorb_range(acc: PartialAccumulator, q_group, keys, values, begin, en
     """attention.cpp:91-100."""
     q, k, v = _f32(q_group), _f32(keys), _f32(values)
     _check(lib().saap_pattn_absorb_range(acc.ctx.h, acc.h, _p(q), _u64(q.shape[0]), _u64(q.shape[1]),
-                                         _p(k), _p(v), _u64(k.shape[0]), _u64(v.shape[0]),
-                                         _u64(v.shape[1]), _u64(begin), _u64(end)))
+                                         _p(k), _p(v), _u64(k.shape[0]), _u64(k.shape[1]),
+                                         _u64(v.shape[0]), _u64(v.shape[1]), _u64(begin), _u64(end)))
 
 
 def merge_into(acc: PartialAccumulator, part: PartialAccumulator) -> None:
@@ -570,8 +570,8 @@ def attention_over_ids(q_group, keys, values, ids, ctx: Optional[Context] = None
     out = np.empty((q.shape[0], v.shape[1]), np.float32)
     e = C.c_int()
     _check(lib().saap_attention_over_ids(ctx.h, _p(q), _u64(q.shape[0]), _u64(q.shape[1]), _p(k),
-                                         _p(v), _u64(k.shape[0]), _u64(v.shape[0]), _u64(v.shape[1]),
-                                         _p(ids), _u64(ids.size), _p(out), C.byref(e)))
+                                         _p(v), _u64(k.shape[0]), _u64(k.shape[1]), _u64(v.shape[0]),
+                                         _u64(v.shape[1]), _p(ids), _u64(ids.size), _p(out), C.byref(e)))
     return out, bool(e.value)
 
 

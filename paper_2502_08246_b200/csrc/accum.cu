@@ -122,8 +122,10 @@ __global__ void __launch_bounds__(kAT) acc_finalize_kernel(const double* out_acc
 }
 
 __global__ void acc_init_kernel(double* out, double* sumexp, double* runmax, uint32_t H, uint32_t dv) {
-    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < H * dv; e += gridDim.x * blockDim.x) {
-        out[e] = 0.0;
+    // value_dim 0 still has H (sumexp, runmax) pairs (attention.cpp:82-83)
+    const uint32_t n = max(H * dv, H);
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+        if (e < H * dv) out[e] = 0.0;
         if (e < H) {
             sumexp[e] = 0.0;
             runmax[e] = -INFINITY;
@@ -135,7 +137,7 @@ __global__ void acc_init_kernel(double* out, double* sumexp, double* runmax, uin
 
 void launch_acc_init(double* out, double* sumexp, double* runmax, uint32_t H, uint32_t dv,
                      cudaStream_t st) {
-    acc_init_kernel<<<std::max<uint32_t>(1, std::min<uint32_t>(1024, (H * dv + 255) / 256)), 256, 0, st>>>(
+    acc_init_kernel<<<std::max<uint32_t>(1, std::min<uint32_t>(1024, (std::max(H * dv, H) + 255) / 256)), 256, 0, st>>>(
             out, sumexp, runmax, H, dv);
     SAAP_CUDA(cudaGetLastError());
 }

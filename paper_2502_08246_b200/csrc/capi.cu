@@ -784,6 +784,8 @@ DecodeSrc layer_src(saap_layer* L, uint64_t recent, bool need_gather) {
             L->gather_cap = cap;
             delete (DecodeMaps*)L->maps;
             L->maps = nullptr;
+            // saved step graphs hold the old gK/gV and maps as kernel arguments
+            L->ctx->scratch_gen++;
         }
     }
     if (!L->maps)
@@ -1141,7 +1143,13 @@ int saap_router_select(saap_ctx* c, const saap_router* r, const float* q_roped,
         need(r, "router");
         if (l == 0) return;  // attention.cpp:278-280, 311-313
         check_router_dims(r, d, 0, l);
-        if (G == 0) invalid("qmodel: empty query batch");
+        if (G == 0) {
+            if (r->kind == 1) invalid("qmodel: empty query batch");
+            // CentroidRouter: pooled = 0 scores every centroid 0, so the
+            // (score desc, id asc) order gives ids 0..l-1 (attention.cpp:284-305)
+            for (uint64_t i = 0; i < l; ++i) out[i] = (uint32_t)i;
+            return;
+        }
         const bool deroped = r->kind == 1 || r->use_deroped;
         const float* q = deroped ? q_deroped : q_roped;
         need(q, "router queries");
@@ -1605,13 +1613,15 @@ int saap_accum_write(saap_ctx* c, saap_accum* a, const double* out_acc, const do
 
 // shared absorb: validation as absorb_impl (:38-48), rows staged by id order
 static void absorb_rows(saap_ctx* c, saap_accum* a, const float* q, uint64_t G, uint64_t d,
-                        const float* keys, const float* values, uint64_t n_rows, uint64_t dv,
-                        const uint64_t* ids, uint64_t begin, uint64_t count) {
+                        const float* keys, const float* values, uint64_t n_rows, uint64_t kd,
+                        uint64_t dv, const uint64_t* ids, uint64_t begin, uint64_t count) {
     need(a, "accumulator");
     if (a->heads != G || a->dv != dv)
         invalid("pattn_absorb: accumulator " + std::to_string(a->heads) + "x" +
                 std::to_string(a->dv) + " does not fit group " + std::to_string(G) + "x" +
                 std::to_string(dv));
+    if (d != kd)  // absorb_impl :40-43, after check_kv / check_acc
+        invalid("pattn_absorb: query dim " + std::to_string(d) + " vs key dim " + std::to_string(kd));
     if (count == 0 || G == 0) return;
     need(q, "pattn_absorb: queries");
     need(keys, "pattn_absorb: keys");
@@ -1649,21 +1659,22 @@ static void absorb_rows(saap_ctx* c, saap_accum* a, const float* q, uint64_t G, 
 }
 
 int saap_pattn_absorb(saap_ctx* c, saap_accum* a, const float* q, uint64_t G, uint64_t d,
-                      const float* keys, const float* values, uint64_t n_keys, uint64_t n_values,
-                      uint64_t dv, const uint64_t* ids, uint64_t count) {
+                      const float* keys, const float* values, uint64_t n_keys, uint64_t key_dim,
+                      uint64_t n_values, uint64_t dv, const uint64_t* ids, uint64_t count) {
     return guard([&] {
         DeviceGuard dg(c);
         if (n_keys != n_values)
             invalid("attention: " + std::to_string(n_keys) + " keys vs " + std::to_string(n_values) +
                     " values");
         if (count) need(ids, "pattn_absorb: ids");
-        absorb_rows(c, a, q, G, d, keys, values, n_keys, dv, ids, 0, count);
+        absorb_rows(c, a, q, G, d, keys, values, n_keys, key_dim, dv, ids, 0, count);
     });
 }
 
 int saap_pattn_absorb_range(saap_ctx* c, saap_accum* a, const float* q, uint64_t G, uint64_t d,
                             const float* keys, const float* values, uint64_t n_keys,
-                            uint64_t n_values, uint64_t dv, uint64_t begin, uint64_t end) {
+                            uint64_t key_dim, uint64_t n_values, uint64_t dv, uint64_t begin,
+                            uint64_t end) {
     return guard([&] {
         DeviceGuard dg(c);
         if (end > n_keys || begin > end)
@@ -1672,7 +1683,7 @@ int saap_pattn_absorb_range(saap_ctx* c, saap_accum* a, const float* q, uint64_t
         if (n_keys != n_values)
             invalid("attention: " + std::to_string(n_keys) + " keys vs " + std::to_string(n_values) +
                     " values");
-        absorb_rows(c, a, q, G, d, keys, values, n_keys, dv, nullptr, begin, end - begin);
+        absorb_rows(c, a, q, G, d, keys, values, n_keys, key_dim, dv, nullptr, begin, end - begin);
     });
 }
 
@@ -1745,12 +1756,13 @@ int saap_pattn_finalize(saap_ctx* c, const saap_accum* a, float* out, int* any_e
 // attention_over_ids(q, keys, values, ids): one absorb into a fresh
 // accumulator, then finalize (attention.cpp:197-203)
 int saap_attention_over_ids(saap_ctx* c, const float* q, uint64_t G, uint64_t d, const float* keys,
-                            const float* values, uint64_t n_keys, uint64_t n_values, uint64_t dv,
-                            const uint64_t* ids, uint64_t count, float* out, int* any_empty) {
+                            const float* values, uint64_t n_keys, uint64_t key_dim,
+                            uint64_t n_values, uint64_t dv, const uint64_t* ids, uint64_t count,
+                            float* out, int* any_empty) {
     saap_accum* a = nullptr;
     int rc = saap_accum_create(c, G, dv, &a);
     if (rc != SAAP_OK) return rc;
-    rc = saap_pattn_absorb(c, a, q, G, d, keys, values, n_keys, n_values, dv, ids, count);
+    rc = saap_pattn_absorb(c, a, q, G, d, keys, values, n_keys, key_dim, n_values, dv, ids, count);
     if (rc == SAAP_OK) rc = saap_pattn_finalize(c, a, out, any_empty);
     if (rc != SAAP_OK) {
         const std::string keep = g_err;
@@ -2418,6 +2430,13 @@ int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* c
             }
         }
         if (hg && hg->exec && hg->gen == c->scratch_gen) {
+            // the graph reads the layer's router tables (centroid / Q-model
+            // pointers, slots), which another router set may have rewritten
+            if (!std::equal(L->cached_routers.begin(), L->cached_routers.end(), hg->routers.begin(),
+                            hg->routers.end())) {
+                int m = 0, u = 0;
+                bind_routers(const_cast<saap_layer*>(L), routers, m, u);
+            }
             SAAP_CUDA(cudaGraphLaunch(hg->exec, st));
             c->launches += 3;
         } else {
