@@ -381,6 +381,35 @@ SAAP_API int saap_synth_fill_dev(saap_ctx* ctx, void* out_bf16, uint64_t rows, u
                         uint64_t seed, int kind, const float* centers_dev,
                         uint64_t n_centers, float center_scale, float noise);
 
+/* ---- synthetic benchmark inputs (the reference's generator, host code).
+ * HeadSpec synthdata.hpp:24-56 (field for field; saap_head_spec_default
+ * writes the reference's defaults).  Bit-identical to the reference's
+ * generate_prompt on every output word; host-only (no device needed). */
+typedef struct saap_head_spec {
+    uint64_t dim, n_clusters;
+    double key_offset, query_offset, key_center_scale, cluster_code_scale, key_noise, stable_noise,
+            sink_norm, drift_rate, query_noise, query_pull, query_boost, local_boost, target_beacon,
+            ood_shift, planted_longrange_fraction;
+    uint64_t n_targets, local_range, longrange_threshold, window_guard, lowfreq_pairs;
+    double rope_base;
+    uint64_t seed;
+} saap_head_spec;
+SAAP_API void saap_head_spec_default(saap_head_spec* spec);
+/* generate_prompt(spec, n_keys, n_q, prompt_seed)   synthdata.cpp:169-281.
+ * Key/value blocks [n_keys x dim] are written as f32, or as bf16 (RNE) when
+ * out_bf16 != 0; query blocks [n_q x dim] are always f32.  Any output may be
+ * NULL.  planted_target: int64[n_q] (-1 = none).  threads <= 0: all cores. */
+SAAP_API int saap_generate_prompt(const saap_head_spec* spec, uint64_t n_keys, uint64_t n_q,
+                                  uint64_t prompt_seed, int out_bf16, void* keys_deroped,
+                                  void* keys_roped, void* values, float* q_deroped, float* q_roped,
+                                  int64_t* planted_target, int threads);
+/* train_head_partition(spec, n_keys, n_buckets, iters, sink)  experiments.cpp:284-295:
+ * the generator's partition prompt on the host, kmeans_train on the device
+ * (saap_kmeans_train, bit-exact).  centroids: f32 [n_buckets x dim]. */
+SAAP_API int saap_train_head_partition(saap_ctx* ctx, const saap_head_spec* spec, uint64_t n_keys,
+                                       uint64_t n_buckets, uint64_t iters, uint64_t sink_count,
+                                       float* centroids, int threads);
+
 #ifdef __cplusplus
 }
 #endif

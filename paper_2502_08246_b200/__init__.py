@@ -747,6 +747,91 @@ def kmeans_train(keys, n_buckets, iters, rng: Rng, stats: Optional[KMeansStats] 
 
 
 # --------------------------------------------------------------------------
+# Synthetic benchmark inputs: the reference's generator (synthdata.cpp) as
+# host code in the library (csrc/synthdata.cpp), bit-identical output words.
+class _HeadSpecC(C.Structure):
+    _fields_ = ([("dim", C.c_uint64), ("n_clusters", C.c_uint64)]
+                + [(k, C.c_double) for k in (
+                    "key_offset", "query_offset", "key_center_scale", "cluster_code_scale",
+                    "key_noise", "stable_noise", "sink_norm", "drift_rate", "query_noise",
+                    "query_pull", "query_boost", "local_boost", "target_beacon", "ood_shift",
+                    "planted_longrange_fraction")]
+                + [(k, C.c_uint64) for k in ("n_targets", "local_range", "longrange_threshold",
+                                             "window_guard", "lowfreq_pairs")]
+                + [("rope_base", C.c_double), ("seed", C.c_uint64)])
+
+
+class HeadSpec:
+    """saap::HeadSpec (synthdata.hpp:24-56): reference defaults, any field
+    overridable by keyword (``HeadSpec(dim=128, seed=3, drift_rate=0.0)``)."""
+
+    def __init__(self, **kw):
+        s = _HeadSpecC()
+        lib().saap_head_spec_default(C.byref(s))
+        for k, v in kw.items():
+            if not hasattr(s, k):
+                raise TypeError(f"HeadSpec has no field {k!r}")
+            setattr(s, k, v)
+        self._c = s
+
+    def __getattr__(self, k):
+        return getattr(self.__dict__["_c"], k)
+
+    def c(self):
+        return self._c
+
+
+@dataclass
+class SyntheticPrompt:
+    """saap::SyntheticPrompt (synthdata.hpp:63-76); key/value blocks are f32
+    or, with ``bf16=True``, uint16 bf16 bit patterns (RNE)."""
+    keys_deroped: Optional[np.ndarray]
+    keys_roped: Optional[np.ndarray]
+    values: Optional[np.ndarray]
+    queries_deroped: np.ndarray
+    queries_roped: np.ndarray
+    planted_target: np.ndarray
+
+
+def generate_prompt(spec: HeadSpec, n_keys: int, n_q: int, prompt_seed: int = 0, bf16=False,
+                    want=("keys_deroped", "keys_roped", "values"), threads: int = 0,
+                    out=None) -> SyntheticPrompt:
+    """generate_prompt (synthdata.cpp:169-281) on the host cores.  ``out`` may
+    supply preallocated key/value arrays by name (e.g. pinned host buffers)."""
+    d = int(spec.dim)
+    dt = np.uint16 if bf16 else np.float32
+    out = dict(out or {})
+    blk = {}
+    for k in ("keys_deroped", "keys_roped", "values"):
+        if k in out:
+            blk[k] = out[k]
+            assert blk[k].dtype == dt and blk[k].shape == (n_keys, d) and blk[k].flags.c_contiguous
+        else:
+            blk[k] = np.empty((n_keys, d), dt) if k in want else None
+    qd, qr = np.empty((n_q, d), np.float32), np.empty((n_q, d), np.float32)
+    planted = np.empty(n_q, np.int64)
+    pp = [None if blk[k] is None else _p(blk[k]) for k in ("keys_deroped", "keys_roped", "values")]
+    _check(lib().saap_generate_prompt(C.byref(spec.c()), _u64(n_keys), _u64(n_q), _u64(prompt_seed),
+                                      C.c_int(1 if bf16 else 0), *pp, _p(qd), _p(qr), _p(planted),
+                                      C.c_int(threads)))
+    return SyntheticPrompt(blk["keys_deroped"], blk["keys_roped"], blk["values"], qd, qr, planted)
+
+
+def train_head_partition(spec: HeadSpec, n_keys: int, n_buckets: int, kmeans_iters: int = 10,
+                         sink_count: int = 1, ctx: Optional[Context] = None,
+                         threads: int = 0) -> np.ndarray:
+    """train_head_partition (experiments.cpp:284-295): the partition prompt on
+    the host, kmeans_train on the device (bit-exact).  Returns the f32
+    centroids [n_buckets x dim]."""
+    ctx = ctx or default_context()
+    cent = np.empty((int(n_buckets), int(spec.dim)), np.float32)
+    _check(lib().saap_train_head_partition(ctx.h, C.byref(spec.c()), _u64(n_keys), _u64(n_buckets),
+                                           _u64(kmeans_iters), _u64(sink_count), _p(cent),
+                                           C.c_int(threads)))
+    return cent
+
+
+# --------------------------------------------------------------------------
 def assign_keys(keys, p: Partition) -> np.ndarray:
     """KeyAssignment.bucket_of (partition.cpp:191-198), bit-exact."""
     k = _f32(keys)
