@@ -5,18 +5,32 @@ One step = one decode step of one layer for the whole job: routing +
 planning + split-K sparse attention + LSE combine for every (sequence, KV
 head) context — batch 8 x 8 KV heads (Llama-3-8B GQA 32Q/8KV, d=128, bf16
 KV) at 128k context, C=1024 buckets, l=32 probes, window 1+2047 — plus, at
-N>1 GPUs, the NCCL all-gather of the per-head outputs.  KV heads are sharded
-over ranks (strong scaling: total work fixed).  The dense decode kernel (the
+N>1 GPUs, the all-gather of the per-head outputs.  KV heads are sharded over
+ranks (strong scaling: total work fixed).  The dense decode kernel (the
 in-run baseline) runs on the same position-ordered cache.
+
+Inputs are the reference's own synthetic contract:
+generate_prompt(HeadSpec{dim 128, drift 0, seed 1 + 8*layer + kv_head},
+131072 keys, 4 queries, prompt_seed = sequence) through the library's host
+port of the generator (bit-identical to the reference, tests/test_synth.py),
+partitions from train_head_partition(spec, 131072, 1024, 10, 1) on the device
+k-means (bit-exact; layer 0 is checked against the reference-trained
+centroids in tests/golden/c3_partitions_drift0.npz), every K/V/Q/pre-RoPE
+key rounded to bf16.  A second row repeats the step on the default-drift
+(5e-4, imbalanced buckets) inputs.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Prints one JSON line (rank 0).  Synthetic data (counter-based generator on
-the device), random-init centroids; see DESIGN.md §5.
+Prints one JSON line (rank 0).  At N=1 the `parity` block compares the GPU
+step with the compiled reference on the same inputs (all 64 groups of layer
+0): routed lists, keys_scored, max_visited_bucket, empty flags bit-exact,
+outputs max_rel_diff <= 1e-3, mse vs exact attention and the routed lists'
+attention-mass coverage (key recall) within tolerance.
 """
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -30,6 +44,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "SAAP decode-attention µs/step & speedup vs dense at 128k ctx; HBM GB/s"
 UNIT = "us/step"
+PARTITIONS_FILE = os.path.join(ROOT, "tests", "golden", "c3_partitions_drift0.npz")
+TOL = 1e-3
 
 
 def parse():
@@ -47,13 +63,17 @@ def parse():
     ap.add_argument("--probes", type=int, default=32)
     ap.add_argument("--recent", type=int, default=2047)
     ap.add_argument("--sink", type=int, default=1)
-    ap.add_argument("--layers", type=int, default=4, help="distinct layer caches rotated per step")
+    ap.add_argument("--drift", type=float, default=0.0, help="HeadSpec.drift_rate of the primary row")
+    ap.add_argument("--kmeans-iters", type=int, default=10)
+    ap.add_argument("--layers", type=int, default=2, help="distinct layer caches rotated per step")
+    ap.add_argument("--no-imbalanced", action="store_true",
+                    help="skip the default-drift (5e-4) imbalanced-bucket row")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--router", default="centroid", choices=["centroid", "qmodel"],
-                    help="BucketRouter plugin: CentroidRouter (de-roped) or QModelRouter (random-init "
-                         "weights of the reference's shape, hidden 1024)")
+                    help="BucketRouter plugin: CentroidRouter (de-roped) or QModelRouter "
+                         "(qmodel_init weights of the reference's shape, hidden 1024)")
     return ap.parse_args()
 
 
@@ -63,14 +83,35 @@ def workload_config(a, n):
                      f"d={a.dim}, bf16 KV) decode, batch {a.batch}, {a.ctx_len} ctx, "
                      f"C={a.buckets}, l={a.probes}, window {a.sink}+{a.recent}, "
                      + ("de-roped centroid router" if a.router == "centroid"
-                        else "Q-model router (hidden 1024, random-init)")),
-        "model": "Llama-3-8B attention shape (random-init centroids)",
+                        else "Q-model router (hidden 1024, qmodel_init weights)")),
+        "inputs": (f"generate_prompt(HeadSpec dim {a.dim}, drift {a.drift}, seed 1+8*layer+head), "
+                   f"train_head_partition({a.ctx_len}, {a.buckets}, {a.kmeans_iters} iters), bf16"),
         "global_batch": a.batch,
         "seq_len": a.ctx_len,
         "parallelism": f"kv-head shard x{n}",
         "l2": (f"inputs larger than L2: {a.layers} distinct layer caches rotated per step "
-               "(sparse touched set per step > 126 MB L2)"),
+               "(sparse touched set per step ~200 MB > 126 MB L2)"),
     }
+
+
+def bf16_bits_round(x):
+    """f32 -> nearest-even bf16, returned as f32 (host rounding of the queries)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    b = x.view(np.uint32).astype(np.uint64)
+    r = ((b + 0x7FFF + ((b >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32).reshape(x.shape)
+
+
+def cpu_info():
+    model = platform.processor() or ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model
 
 
 # ---------------------------------------------------------------- clocks
@@ -130,121 +171,180 @@ def measured_peaks():
 
 
 def ncu_traffic():
-    """dram bytes per launch of the decode kernel from the committed ncu capture."""
+    """DRAM bytes per decode launch from the committed ncu capture of this build."""
     p = os.path.join(ROOT, "profiles", "decode_kernel_ncu.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("dram_bytes_per_launch")
+            d = json.load(open(p))
+            return d.get("dram_bytes_per_launch"), d.get("source")
         except Exception:
-            return None
-    return None
+            return None, None
+    return None, None
 
 
-# ---------------------------------------------------------------- CPU reference
 def cpu_threads(a):
     return a.cpu_threads or len(os.sched_getaffinity(0))
 
 
-def run_cpu_reference(stores_data, queries, a, steps, warmup, threads):
-    """Time the reference's sparse_attention (oracle/_ref, unmodified sources)
-    on a bounded sample: len(stores_data) distinct 128k contexts x the query
-    groups of the batch = batch*kv_heads groups per step."""
-    import oracle
-    if oracle.ref_available():
-        R = oracle.ref()
-        kind = "reference"
-    else:
-        R = None
-        kind = "port"
-    stores, routers = [], []
-    for sd in stores_data:
-        if R is not None:
-            stores.append(R.store(sd["K"], sd["V"], sd["cent"], a.sink, sd["assign"]))
-            routers.append(R.centroid_router(sd["cent"], True))
-        else:
-            stores.append(sd)
-            routers.append(None)
-    n_groups = queries.shape[0]
-    S = [stores[g % len(stores)] for g in range(n_groups)]
-    Rt = [routers[g % len(routers)] for g in range(n_groups)]
-
-    def step():
-        if R is not None:
-            out, ks = R.sparse_attention_batch(S, Rt, queries, queries, a.probes, 128, a.sink,
-                                               a.recent, threads)
-            return ks
-        P = oracle.port()
-        ks = []
-        for g in range(n_groups):
-            sd = S[g]
-            sel = P.centroid_select(sd["cent"], queries[g], a.probes)
-            off, idx = P.build_ivf(sd["assign"], a.buckets)
-            ks.append(P.sparse_attention(queries[g], sd["K"], sd["V"], a.sink, off, idx, sel,
-                                         a.probes, 128, a.recent)[1])
-        return np.array(ks)
-
-    for _ in range(warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        ks = step()
-    dt = (time.perf_counter() - t0) / steps
-    return dt * 1e6, kind, (threads if R is not None else 1), ks
+def group_of(gi, heads_local, h0):
+    """group index -> (sequence, KV head); groups are sequence-major."""
+    s, hl = divmod(gi, heads_local)
+    return s, h0 + hl
 
 
-# ---------------------------------------------------------------- synthetic data (CPU)
-def cpu_synth_store(a, seed):
-    rs = np.random.RandomState(seed)
-    from oracle import bf16_round
-    cent = rs.randn(a.buckets, a.dim)
-    cent = (cent / np.linalg.norm(cent, axis=1, keepdims=True)).astype(np.float32)
-    lab = rs.randint(0, a.buckets, a.ctx_len)
-    K = bf16_round(cent[lab] * 4.0 + rs.randn(a.ctx_len, a.dim).astype(np.float32))
-    V = bf16_round(rs.randn(a.ctx_len, a.dim).astype(np.float32))
-    return cent, K, V
-
-
+# ---------------------------------------------------------------- reference arm
 def reference_arm(a):
-    """--impl reference: the reference CPU path on the host cores, rank 0 only."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: the compiled reference (oracle/_ref, the unmodified
+    reference sources) on the host cores, on the same inputs as our arm:
+    generate_prompt per (sequence, KV head), the reference-trained partitions
+    (tests/golden), reference assign_keys / build_ivf stores, and one decode
+    step = sparse_attention for all batch x kv_heads groups on a thread pool.
+    Rank 0 only."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     import oracle
     from oracle import bf16_round
     threads = cpu_threads(a)
-    n_groups = a.batch * a.kv_heads
-    n_stores = min(a.kv_heads, n_groups)
-    stores = []
-    for h in range(n_stores):
-        cent, K, V = cpu_synth_store(a, 1000 + h)
-        if oracle.ref_available():
-            assign = oracle.ref().assign_keys(K[a.sink:], cent, threads=threads)
-        else:
-            assign = oracle.port().assign_keys(K[a.sink:], cent)
-        stores.append({"cent": cent, "K": K, "V": V, "assign": assign})
-    rs = np.random.RandomState(7)
     G = a.q_heads // a.kv_heads
-    q = np.stack([bf16_round(stores[g % n_stores]["cent"][rs.randint(a.buckets)] * 6.0
-                             + rs.randn(G, a.dim).astype(np.float32)) for g in range(n_groups)])
-    us, kind, cores, ks = run_cpu_reference(stores, q, a, a.steps, a.warmup, threads)
+    n_groups = a.batch * a.kv_heads
+    if not oracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}), flush=True)
+        return
+    R = oracle.ref()
+    t0 = time.time()
+    cents = load_reference_partitions(a)
+    trained_here = cents is None
+    if trained_here:  # another config: the reference trains them (slow, single-threaded k-means)
+        cents = [R.train_head_partition(oracle.HeadSpec(dim=a.dim, seed=1 + h, drift_rate=a.drift),
+                                        a.ctx_len, a.buckets, a.kmeans_iters, a.sink)
+                 for h in range(a.kv_heads)]
+    stores, routers, qr, qd = [], [], [], []
+    rts = [R.centroid_router(cents[h], True) for h in range(a.kv_heads)]
+    spec = oracle.HeadSpec(dim=a.dim, seed=1, drift_rate=a.drift)
+    for s in range(a.batch):
+        blocks, q_d, q_r = R.generate_prompts(spec, [1 + h for h in range(a.kv_heads)],
+                                              [s] * a.kv_heads, a.ctx_len, G, threads)
+        for h in range(a.kv_heads):
+            K = bf16_round(blocks["keys_roped"][h])
+            V = bf16_round(blocks["values"][h])
+            Kd = bf16_round(blocks["keys_deroped"][h])
+            assign = R.assign_keys(Kd[a.sink:], cents[h], threads=threads)
+            stores.append(R.store(K, V, cents[h], a.sink, assign))
+            routers.append(rts[h])
+            qr.append(bf16_round(q_r[h]))
+            qd.append(bf16_round(q_d[h]))
+        del blocks
+    qr, qd = np.stack(qr), np.stack(qd)
+    prep_s = time.time() - t0
+
+    def step():
+        return R.sparse_attention_batch(stores, routers, qr, qd, a.probes, 128, a.sink, a.recent,
+                                        threads)[1]
+
+    for _ in range(a.warmup):
+        step()
+    t1 = time.perf_counter()
+    for _ in range(a.steps):
+        ks = step()
+    us = (time.perf_counter() - t1) / a.steps * 1e6
     line = {
         "metric": METRIC, "value": round(us, 3), "unit": UNIT, "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(us / 1e3, 4),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (clustered keys, random unit centroids; numpy)",
+        "data": "synthetic: the reference's generate_prompt + train_head_partition, bf16-rounded",
         "config": workload_config(a, a.gpus), "impl": "reference",
-        "cpu_baseline": {"value": round(us, 3), "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": (f"{n_stores} distinct {a.ctx_len}-key contexts x "
-                                    f"{n_groups // n_stores} query groups = {n_groups} "
-                                    "(sequence, KV head) groups per step")},
+        "cpu_baseline": {"value": round(us, 3), "unit": UNIT, "cores": threads, "kind": "reference",
+                         "cpu": cpu_info(),
+                         "sample": (f"the full step: {n_groups} (sequence, KV head) groups of "
+                                    f"{a.ctx_len} keys, sparse_attention on a {threads}-thread pool"
+                                    + ("" if not trained_here else "; partitions trained in-run"))},
         "e2e": {"value": round(us, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "selectivity": float(np.mean(ks) / a.ctx_len),
+        "prep_s": round(prep_s, 1),
     }
     print(json.dumps(line), flush=True)
 
 
+def load_reference_partitions(a):
+    """The reference-trained C3 partitions (tests/golden), when they match the config."""
+    if not (os.path.exists(PARTITIONS_FILE) and a.drift == 0.0 and a.dim == 128):
+        return None
+    f = np.load(PARTITIONS_FILE)
+    n, C, iters, sink = [int(x) for x in f["meta"]]
+    if (n, C, iters, sink) != (a.ctx_len, a.buckets, a.kmeans_iters, a.sink) or \
+            f["centroids"].shape[0] < a.kv_heads:
+        return None
+    return [f["centroids"][h] for h in range(a.kv_heads)]
+
+
 # ---------------------------------------------------------------- our arm
+class Inputs:
+    """One layer's inputs for this rank's groups, on the device."""
+
+
+def make_layer_inputs(sb, torch, ctx, a, li, drift, heads_local, h0, dev, threads):
+    G, d, C, N = a.q_heads // a.kv_heads, a.dim, a.buckets, a.ctx_len
+    n_groups = a.batch * heads_local
+    specs = [sb.HeadSpec(dim=d, seed=1 + 8 * li + h0 + hl, drift_rate=drift) for hl in range(heads_local)]
+    t0 = time.time()
+    cents = [sb.train_head_partition(sp, N, C, a.kmeans_iters, a.sink, ctx, threads) for sp in specs]
+    t_part = time.time() - t0
+    K = torch.empty(n_groups * N, d, dtype=torch.bfloat16, device=dev)
+    V = torch.empty_like(K)
+    Kd = torch.empty_like(K)
+    qr = np.empty((n_groups, G, d), np.float32)
+    qd = np.empty((n_groups, G, d), np.float32)
+    pin = {k: torch.empty(N, d, dtype=torch.int16, pin_memory=True)
+           for k in ("keys_roped", "values", "keys_deroped")}
+    host = {k: v.numpy().view(np.uint16) for k, v in pin.items()}
+    t0 = time.time()
+    for gi in range(n_groups):
+        s, hl = divmod(gi, heads_local)
+        p = sb.generate_prompt(specs[hl], N, G, s, bf16=True, threads=threads, out=host)
+        rows = slice(gi * N, (gi + 1) * N)
+        K[rows].view(torch.int16).copy_(pin["keys_roped"])
+        V[rows].view(torch.int16).copy_(pin["values"])
+        Kd[rows].view(torch.int16).copy_(pin["keys_deroped"])
+        qr[gi] = bf16_bits_round(p.queries_roped)
+        qd[gi] = bf16_bits_round(p.queries_deroped)
+    t_gen = time.time() - t0
+    lay = Inputs()
+    lay.K, lay.V, lay.Kd, lay.qr, lay.qd, lay.cents = K, V, Kd, qr, qd, cents
+    lay.t_part, lay.t_gen = t_part, t_gen
+    return lay
+
+
+def build_c3_layer(sb, torch, ctx, a, li, drift, heads_local, h0, dev, stream, threads,
+                   qm_routers=None):
+    """Inputs + the packed layer (tcgen05-assigned, bucket-contiguous), the
+    routers (CentroidRouter de-roped, or the given Q-model routers) and the
+    position-ordered dense cache of one layer for this rank's groups."""
+    G, d, C, N = a.q_heads // a.kv_heads, a.dim, a.buckets, a.ctx_len
+    n_groups = a.batch * heads_local
+    inp = make_layer_inputs(sb, torch, ctx, a, li, drift, heads_local, h0, dev, threads)
+    parts_h = [sb.Partition(c, ctx) for c in inp.cents]
+    parts = [parts_h[gi % heads_local] for gi in range(n_groups)]
+    L = sb.Layer([N] * n_groups, d, C, a.sink, a.recent, ctx)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    L.build_dev(parts, inp.K, inp.V, inp.Kd)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    inp.t_build_ms = e0.elapsed_time(e1)
+    if qm_routers is not None:
+        routers = [qm_routers[gi % heads_local] for gi in range(n_groups)]
+    else:
+        routers = [sb.CentroidRouter(p, True) for p in parts]
+    inp.kv = sb.KVCache(ctx, n_groups, d, inp.K, inp.V, [gi * N for gi in range(n_groups)],
+                        [N] * n_groups)
+    inp.L, inp.routers, inp.parts = L, routers, parts_h
+    inp.qr_t = torch.from_numpy(inp.qr).to(dev)
+    inp.qd_t = torch.from_numpy(inp.qd).to(dev)
+    return inp
+
+
 def ours(a):
     import torch
     import torch.distributed as dist
@@ -262,97 +362,74 @@ def ours(a):
     heads_local, h0 = sh.heads_local, sh.head0
     G = a.q_heads // a.kv_heads
     d, C, N = a.dim, a.buckets, a.ctx_len
-    n_groups = sh.n_groups  # group = (sequence, local KV head)
+    n_groups = sh.n_groups  # group = (sequence, local KV head), sequence-major
+    threads = cpu_threads(a)
 
     stream = torch.cuda.Stream()
     ctx = sb.Context(local)
     ctx.set_stream(stream.cuda_stream)
     dev = torch.device("cuda", local)
+    cfg = sb.SparseAttnConfig(a.probes, 128, sb.DenseWindow(a.sink, a.recent))
 
-    # ---- per layer: centroids per KV head, clustered keys, values; build stores
-    layers = []
-    t_build = []
     qm_routers = None
-    for li in range(a.layers):
-        gen = torch.Generator(device=dev)
-        gen.manual_seed(1000 * li + 17)
-        cents = torch.randn(a.kv_heads, C, d, device=dev, generator=gen)
-        cents = (cents / cents.norm(dim=-1, keepdim=True)).float()
-        K = torch.empty(n_groups * N, d, dtype=torch.bfloat16, device=dev)
-        V = torch.empty_like(K)
-        for gi in range(n_groups):
-            s, hl = divmod(gi, heads_local)
-            h = h0 + hl
-            seed = (li * 1_000_003 + s * 7919 + h * 104729) & 0xFFFFFFFF
-            rows = slice(gi * N, (gi + 1) * N)
-            with torch.cuda.stream(stream):
-                sb.synth_fill(ctx, K[rows], N, d, seed, 1, cents[h], C, 4.0, 1.0)
-                sb.synth_fill(ctx, V[rows], N, d, seed ^ 0x5555, 0, None, 0, 0.0, 1.0)
-        ctx.synchronize()
-        parts_h = [sb.Partition(cents[h0 + hl].cpu().numpy(), ctx) for hl in range(heads_local)]
-        parts = [parts_h[gi % heads_local] for gi in range(n_groups)]
-        L = sb.Layer([N] * n_groups, d, C, a.sink, a.recent, ctx)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        L.build_dev(parts, K, V, K)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        t_build.append(e0.elapsed_time(e1))
-        if a.router == "qmodel":
-            if qm_routers is None:
-                qm_routers = []
-                rq = np.random.default_rng(77 + rank)
-                for hl in range(heads_local):  # qmodel_init shapes / scales (qmodel.cpp:337-357)
-                    h = 1024
-                    prm = {"w1": rq.normal(0, np.sqrt(2.0 / d), (d, h)), "b1": np.zeros((1, h)),
-                           "bn_gamma": np.ones((1, h)), "bn_beta": np.zeros((1, h)),
-                           "bn_run_mean": np.zeros((1, h)), "bn_run_var": np.ones((1, h)),
-                           "w2": rq.normal(0, np.sqrt(1.0 / h), (h, C)), "b2": np.zeros((1, C))}
-                    qm_routers.append(sb.QModelRouter(sb.QModel(prm, ctx)))
-            routers = [qm_routers[gi % heads_local] for gi in range(n_groups)]
-        else:
-            routers = [sb.CentroidRouter(p, True) for p in parts]
-        kv = sb.KVCache(ctx, n_groups, d, K, V, [gi * N for gi in range(n_groups)], [N] * n_groups)
-        layers.append(dict(L=L, K=K, V=V, routers=routers, parts=parts_h, kv=kv, cents=cents))
+    if a.router == "qmodel":
+        qm_routers = []
+        rq = np.random.default_rng(77 + rank)
+        for hl in range(heads_local):  # qmodel_init shapes / scales (qmodel.cpp:337-357)
+            h = 1024
+            prm = {"w1": rq.normal(0, np.sqrt(2.0 / d), (d, h)), "b1": np.zeros((1, h)),
+                   "bn_gamma": np.ones((1, h)), "bn_beta": np.zeros((1, h)),
+                   "bn_run_mean": np.zeros((1, h)), "bn_run_var": np.ones((1, h)),
+                   "w2": rq.normal(0, np.sqrt(1.0 / h), (h, C)), "b2": np.zeros((1, C))}
+            qm_routers.append(sb.QModelRouter(sb.QModel(prm, ctx)))
 
-    peak_early, _ = measured_peaks()
+    def build_layer(li, drift):
+        return build_c3_layer(sb, torch, ctx, a, li, drift, heads_local, h0, dev, stream, threads,
+                              qm_routers)
+
+    t_setup = time.time()
+    layers = [build_layer(li, a.drift) for li in range(a.layers)]
+    imb = []
+    if not a.no_imbalanced:
+        imb = [build_layer(li, 5e-4) for li in range(a.layers)]
+    t_setup = time.time() - t_setup
+
+    # layer 0's device-trained partitions vs the reference-trained file
+    part_check = None
+    ref_parts = load_reference_partitions(a)
+    if ref_parts is not None:
+        eq = [bool(np.array_equal(layers[0].cents[hl].view(np.uint32),
+                                  ref_parts[h0 + hl].view(np.uint32))) for hl in range(heads_local)]
+        part_check = {"heads": heads_local, "bit_exact": int(sum(eq)),
+                      "source": os.path.relpath(PARTITIONS_FILE, ROOT)}
+
     # ---- prefill (C4-style): rebuild layer 0 with device timing per phase
+    peak, peak_kind = measured_peaks()
     ctx.enable_timing(True)
     pre_a, pre_p = [], []
     lay0 = layers[0]
-    parts0 = [lay0["parts"][gi % heads_local] for gi in range(n_groups)]
+    parts0 = [lay0.parts[gi % heads_local] for gi in range(n_groups)]
     for _ in range(3):
-        lay0["L"].build_dev(parts0, lay0["K"], lay0["V"], lay0["K"])
-        ta, tp = lay0["L"].build_timing()
+        lay0.L.build_dev(parts0, lay0.K, lay0.V, lay0.Kd)
+        ta, tp = lay0.L.build_timing()
         pre_a.append(ta)
         pre_p.append(tp)
     ctx.timing()  # clear decode records
     ctx.enable_timing(False)
-    used_tc, refined = lay0["L"].assign_info()
+    used_tc, refined = lay0.L.assign_info()
     n_keys_prefill = n_groups * (N - a.sink)
     assign_ms, pack_ms = float(np.median(pre_a)), float(np.median(pre_p))
     pack_bytes = n_keys_prefill * (8 * d + 16)
 
-    # ---- queries: each group's 4 heads look for one cluster of its KV head
-    gq = torch.Generator(device=dev)
-    gq.manual_seed(4242 + rank)
-    q = torch.empty(n_groups, G, d, device=dev)
-    for gi in range(n_groups):
-        h = h0 + gi % heads_local
-        tgt = layers[0]["cents"][h][torch.randint(C, (1,), device=dev, generator=gq)]
-        q[gi] = (tgt * 6.0 + torch.randn(G, d, device=dev, generator=gq)).bfloat16().float()
     out = torch.empty(n_groups, G, d, device=dev)
     out_dense = torch.empty_like(out)
     stats = torch.zeros(n_groups, 3, dtype=torch.int64, device=dev)
-    cfg = sb.SparseAttnConfig(a.probes, 128, sb.DenseWindow(a.sink, a.recent))
 
-    def sparse_step(li):
-        lay = layers[li]
-        lay["L"].sparse_attention_dev(lay["routers"], q, q, G, cfg, out, stats)
+    def sparse_step(lay):
+        lay.L.sparse_attention_dev(lay.routers, lay.qr_t, lay.qd_t, G, cfg, out, stats)
 
-    def dense_step(li):
-        layers[li]["kv"].dense_attention_dev(q, G, out_dense)
+    def dense_step(lay):
+        lay.kv.dense_attention_dev(lay.qr_t, G, out_dense)
 
     def gather():
         if world > 1:
@@ -360,23 +437,26 @@ def ours(a):
                 gather_outputs(out, sh, dist)
 
     # eager warm-up sizes the scratch, then capture one graph per layer
-    for li in range(a.layers):
-        sparse_step(li)
+    for lay in layers + imb:
+        sparse_step(lay)
         if not a.no_dense:
-            dense_step(li)
+            dense_step(lay)
     ctx.synchronize()
-    graphs, dgraphs = [], []
     kernels_per_step = None
-    for li in range(a.layers):
+
+    def capture(fn, lay):
+        nonlocal kernels_per_step
         n0 = ctx.launch_count
         ctx.graph_begin()
-        sparse_step(li)
-        graphs.append(ctx.graph_end())
-        kernels_per_step = ctx.launch_count - n0  # our kernels captured in one step's graph
-        if not a.no_dense:
-            ctx.graph_begin()
-            dense_step(li)
-            dgraphs.append(ctx.graph_end())
+        fn(lay)
+        g = ctx.graph_end()
+        if fn is sparse_step:
+            kernels_per_step = ctx.launch_count - n0  # our kernels in one step's graph
+        return g
+
+    graphs = [capture(sparse_step, lay) for lay in layers]
+    igraphs = [capture(sparse_step, lay) for lay in imb]
+    dgraphs = [capture(dense_step, lay) for lay in layers] if not a.no_dense else []
 
     clock = ClockSampler(local)
     clock.start()
@@ -404,176 +484,96 @@ def ours(a):
         return ms
 
     def sparse_graph_step(i):
-        graphs[i % a.layers].launch()
+        graphs[i % len(graphs)].launch()
         gather()
 
     ms_sparse = timed(sparse_graph_step, a.steps, a.warmup)
+    ms_imb = timed(lambda i: (igraphs[i % len(igraphs)].launch(), gather()), a.steps, a.warmup) \
+        if igraphs else None
     ms_dense = None
     if not a.no_dense:
-        ms_dense = timed(lambda i: dgraphs[i % a.layers].launch(), max(10, a.steps // 5),
+        ms_dense = timed(lambda i: dgraphs[i % len(dgraphs)].launch(), max(10, a.steps // 5),
                          a.warmup)
-    ms_gather = None
-    if world > 1:
-        ms_gather = timed(lambda i: gather(), a.steps, a.warmup)
+    ms_gather = timed(lambda i: gather(), a.steps, a.warmup) if world > 1 else None
 
     # ---- per-kernel device time (eager, events around the kernels)
-    ctx.enable_timing(True)
-    reps = 20
-    for i in range(reps):
-        sparse_step(i % a.layers)
-    plan_ms, attn_ms, n = ctx.timing()
-    attn_ms /= max(n, 1)
-    plan_ms /= max(n, 1)
-    dense_attn_ms = None
-    if not a.no_dense:
-        for i in range(reps // 2):
-            dense_step(i % a.layers)
-        _, dms, dn = ctx.timing()
-        dense_attn_ms = dms / max(dn, 1)
-    ctx.enable_timing(False)
-    plan_trace = None
-    if os.environ.get("SAAP_PLAN_TRACE"):
-        import ctypes as ct
-        buf = (ct.c_uint64 * (16 + 6 * 1024))()
-        if sb.lib().saap_debug_plan_trace(ctx.h, buf) == 0:
-            plan_trace = list(buf)[:16]
-            cta = np.array(list(buf)[16:], dtype=np.float64).reshape(1024, 6)[:, :3]
-            cta = cta[cta[:, 0] > 0]
-            if len(cta):
-                t0 = cta[:, 0].min()
-                plan_trace.append({k: [round(float(v), 2) for v in np.percentile((cta[:, i] - t0) / 1e3, [0, 50, 100])]
-                                   for i, k in enumerate(["start_us", "exchanged_us", "end_us"])})
-    step_trace = None
-    graph_plan_trace = None
-    # SAAP_TRACE_DENSE=1: the step / decode traces follow the dense step instead
-    tgraphs = dgraphs if os.environ.get("SAAP_TRACE_DENSE") and dgraphs else graphs
-    if os.environ.get("SAAP_STEP_TRACE"):
-        import ctypes as ct
-        buf = (ct.c_uint64 * 16)()
-        sb._check(sb.lib().saap_debug_step_trace(ctx.h, buf, 1))
-        if os.environ.get("SAAP_STEP_TRACE_EAGER"):
-            ctx.enable_timing(True)  # the eager step with its timing events
-            sparse_step(0)
-            ctx.synchronize()
-            ctx.timing()
-            ctx.enable_timing(False)
-        else:
-            tgraphs[0].launch()
-        ctx.synchronize()
-        sb._check(sb.lib().saap_debug_step_trace(ctx.h, buf, 0))
-        if os.environ.get("SAAP_PLAN_TRACE"):  # routing phases of this (overlapped) step
-            pbuf = (ct.c_uint64 * (16 + 6 * 1024))()
-            if sb.lib().saap_debug_plan_trace(ctx.h, pbuf) == 0:
-                cta = np.array(list(pbuf)[16:], dtype=np.float64).reshape(1024, 6)
-                cta = cta[cta[:, 0] > 0]
-                tt0 = cta[:, 0].min() if len(cta) else 0
-                own = cta[cta[:, 3] > 0]
-                slow = own[np.argsort(own[:, 3])[-4:]] if len(own) else own
-                graph_plan_trace = [list(pbuf)[:13]] + [
-                    {k: [round(float(x), 2) for x in np.percentile((own[:, i] - tt0) / 1e3, [0, 50, 100])]
-                     for i, k in enumerate(["start_us", "exchanged_us", "selected_us", "end_us"])},
-                    {"slowest_owner_ctas_us_and_candidates": [[round(float((r[i] - tt0) / 1e3), 2) for i in range(4)] + [int(r[4])]
-                                                              for r in slow]}] if len(own) else None
-        v = list(buf)
-        t0 = min(x for x in v[0::2] if x)
-        names = ["approx", "plan", "decode", "combine", "run_published", "slot_complete"]
-        step_trace = {n: [round((v[2 * k] - t0) / 1e3, 2) if v[2 * k] != 2**64 - 1 else None,
-                          round((v[2 * k + 1] - t0) / 1e3, 2) if v[2 * k + 1] else None]
-                      for k, n in enumerate(names)}
-    decode_trace = None
-    if os.environ.get("SAAP_DECODE_TRACE"):
-        import ctypes as ct
-        tgraphs[0].launch()  # trace the sparse (or dense) step
-        ctx.synchronize()
-        nc = ctx.sm_count
-        buf = (ct.c_uint64 * (16 * nc))()
-        if sb.lib().saap_debug_decode_trace(ctx.h, buf, ct.c_uint64(nc)) == 0:
-            t = np.array(list(buf), dtype=np.float64).reshape(nc, 16)
-            t0 = t[:, 0].min()
-            os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-            np.save(os.path.join(ROOT, "gpurun_out", "decode_trace.npy"), t)
-            rel = lambda x: [round(float(v), 2) for v in np.percentile((x - t0) / 1e3, [0, 50, 100])]
-            decode_trace = {"start_us": rel(t[:, 0]), "first_tile_us": rel(t[:, 1]),
-                            "end_us": rel(t[:, 2]),
-                            "tiles_per_cta": [int(v) for v in np.percentile(t[:, 3], [0, 50, 100])],
-                            "producer_empty_wait_frac": round(float(np.median(t[:, 4] / np.maximum(t[:, 5], 1))), 3),
-                            "consumer_full_wait_frac": round(float(np.median(t[:, 6] / np.maximum(t[:, 5], 1))), 3),
-                            "producer_feed_frac": round(float(np.median(t[:, 7] / np.maximum(t[:, 5], 1))), 3),
-                            "producer_record_wait_frac": round(float(np.median(t[:, 8] / np.maximum(t[:, 5], 1))), 3),
-                            "producer_tma_issue_frac": round(float(np.median(t[:, 9] / np.maximum(t[:, 5], 1))), 3),
-                            "first_record_us": rel(t[:, 10]), "first_tma_us": rel(t[:, 11])}
+    def kernel_times(lays, dense):
+        ctx.enable_timing(True)
+        reps = 20
+        for i in range(reps):
+            (dense_step if dense else sparse_step)(lays[i % len(lays)])
+        plan_ms, attn_ms, n = ctx.timing()
+        ctx.enable_timing(False)
+        return plan_ms / max(n, 1), attn_ms / max(n, 1)
 
-    # ---- counters, quality vs dense
-    keys_scored = []
-    mse_vals = []
-    for li in range(a.layers):
-        sparse_step(li)
-        dense_step(li)
-        torch.cuda.synchronize()
-        keys_scored.append(int(stats[:, 0].sum().item()))
-        mse_vals.append(((out - out_dense) ** 2).mean().item())
-    ks_step = float(np.mean(keys_scored))
+    plan_ms, attn_ms = kernel_times(layers, False)
+    dense_attn_ms = kernel_times(layers, True)[1] if not a.no_dense else None
+    iplan_ms, iattn_ms = kernel_times(imb, False) if imb else (None, None)
+
+    # ---- counters, quality vs dense (our own dense kernel)
+    def counters(lays):
+        ks, ms = [], []
+        for lay in lays:
+            sparse_step(lay)
+            dense_step(lay)
+            torch.cuda.synchronize()
+            ks.append(int(stats[:, 0].sum().item()))
+            ms.append(((out - out_dense) ** 2).mean().item())
+        return float(np.mean(ks)), float(np.mean(ms))
+
+    ks_step, mse_dense = counters(layers)
+    iks_step, imse_dense = counters(imb) if imb else (None, None)
     bytes_step = ks_step * d * 2 * 2
     dense_bytes = n_groups * N * d * 2 * 2
 
     # ---- end to end through the public host API (pinned host buffers)
     import ctypes as ct
-    qh = torch.empty(n_groups, G, d, pin_memory=True)
-    qh.copy_(q.cpu())
+    qr_h = torch.empty(n_groups, G, d, pin_memory=True)
+    qd_h = torch.empty(n_groups, G, d, pin_memory=True)
+    qr_h.copy_(torch.from_numpy(layers[0].qr))
+    qd_h.copy_(torch.from_numpy(layers[0].qd))
     oh = torch.empty(n_groups, G, d, pin_memory=True)
-    # page-locked stats buffer (one fast D2H like the outputs)
     st_pin = torch.empty(n_groups * ct.sizeof(sb.AttnStats), dtype=torch.uint8, pin_memory=True)
     st_h = (sb.AttnStats * n_groups).from_address(st_pin.data_ptr())
     lib = sb.lib()
     ccfg = cfg.c()
 
     def e2e_step(i):
-        lay = layers[i % a.layers]
+        lay = layers[i % len(layers)]
         sb._check(lib.saap_sparse_attention(
-            ctx.h, lay["L"].h, lay["L"]._routers(lay["routers"]), ct.c_void_p(qh.data_ptr()),
-            ct.c_void_p(qh.data_ptr()), ct.c_uint64(G), ct.byref(ccfg), ct.c_void_p(oh.data_ptr()),
+            ctx.h, lay.L.h, lay.L._routers(lay.routers), ct.c_void_p(qr_h.data_ptr()),
+            ct.c_void_p(qd_h.data_ptr()), ct.c_uint64(G), ct.byref(ccfg), ct.c_void_p(oh.data_ptr()),
             st_h, None))
 
     ms_e2e = timed(e2e_step, a.steps, a.warmup)
     clk = clock.stop()
 
-    # ---- CPU baseline (rank 0, N=1): the reference on the same data, bounded sample
-    cpu = None
+    # ---- parity + CPU baseline (rank 0, N=1): the compiled reference on the same inputs
+    parity, cpu, iparity = None, None, None
     if rank == 0 and world == 1 and not a.no_cpu_baseline and a.router == "centroid":
-        lay = layers[0]
-        sample = []
-        for hl in range(min(heads_local, 8)):
-            gi = hl  # sequence 0, KV head hl
-            assign, _ = lay["L"].read_index(gi)
-            sample.append({
-                "cent": lay["parts"][hl].centroids,
-                "K": lay["K"][gi * N:(gi + 1) * N].float().cpu().numpy(),
-                "V": lay["V"][gi * N:(gi + 1) * N].float().cpu().numpy(),
-                "assign": assign})
-        qs = q.cpu().numpy()
-        # reorder: store index = gi % heads_local matches group (s, hl)
-        threads = cpu_threads(a)
-        us_cpu, kind, cores, _ = run_cpu_reference(sample, qs, a, 2, 1, threads)
-        cpu = {"value": round(us_cpu, 1), "unit": UNIT, "cores": cores, "kind": kind,
-               "sample": (f"{len(sample)} distinct {N}-key contexts (layer 0, sequence 0, "
-                          f"KV heads 0-{len(sample) - 1}) x {n_groups // len(sample)} query groups "
-                          f"= {n_groups} groups = one full step's work, 2 timed steps")}
+        parity, cpu = parity_leg(sb, torch, ctx, a, layers[0], list(range(n_groups)), sparse_step,
+                                 dense_step, out, out_dense, stats, heads_local, h0, threads,
+                                 timed_groups=True)
+        if imb:  # imbalanced row: sequence 0's contexts
+            iparity, _ = parity_leg(sb, torch, ctx, a, imb[0], list(range(heads_local)), sparse_step,
+                                    dense_step, out, out_dense, stats, heads_local, h0, threads,
+                                    timed_groups=False)
 
-    peak, peak_kind = measured_peaks()
     us = ms_sparse * 1e3
-    # per-rank algorithmic bytes / per-rank attention-kernel time
     achieved = (bytes_step / (attn_ms * 1e-3) / 1e9) if attn_ms else None
+    traffic, traffic_src = ncu_traffic()
     line = {
         "metric": METRIC, "value": round(us, 3), "unit": UNIT, "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_sparse, 5),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (device counter-based clustered keys, random unit centroids)",
+        "data": ("synthetic: the reference's generate_prompt (library host port, bit-identical) + "
+                 "train_head_partition (device k-means, bit-exact), bf16-rounded"),
         "config": workload_config(a, world),
         "dense_us_per_step": round(ms_dense * 1e3, 3) if ms_dense else None,
         "speedup_vs_dense": round(ms_dense / ms_sparse, 3) if ms_dense else None,
         "attention_time_reduction": round(1 - ms_sparse / ms_dense, 4) if ms_dense else None,
         "selectivity": round(ks_step / (n_groups * N), 5),
-        "mse_vs_dense": float(np.mean(mse_vals)),
+        "mse_vs_dense": mse_dense,
         "hbm_gbs": round(achieved, 1) if achieved else None,
         "kernel_us": {"route_plan": round(plan_ms * 1e3, 2), "sparse_attention": round(attn_ms * 1e3, 2),
                       "dense_attention": round(dense_attn_ms * 1e3, 2) if dense_attn_ms else None},
@@ -581,23 +581,30 @@ def ours(a):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
                      "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4) if achieved else None,
-                     "traffic": ncu_traffic(),
+                     "traffic": traffic, "traffic_source": traffic_src,
                      "peak_kind": peak_kind,
                      "bytes_per_launch": int(bytes_step),
                      "dense_achieved": round(dense_bytes / (dense_attn_ms * 1e-3) / 1e9, 1)
                      if dense_attn_ms else None},
+        "parity": parity,
+        "partition_vs_reference": part_check,
+        "imbalanced": None if not imb else {
+            "drift_rate": 5e-4, "us_per_step": round(ms_imb * 1e3, 3),
+            "speedup_vs_dense": round(ms_dense / ms_imb, 3) if ms_dense else None,
+            "selectivity": round(iks_step / (n_groups * N), 5), "mse_vs_dense": imse_dense,
+            "kernel_us": {"route_plan": round(iplan_ms * 1e3, 2),
+                          "sparse_attention": round(iattn_ms * 1e3, 2)},
+            "hbm_gbs": round(iks_step * d * 4 / (iattn_ms * 1e-3) / 1e9, 1),
+            "parity": iparity},
         "cpu_baseline": cpu,
         "e2e": {"value": round(ms_e2e * 1e3, 3), "unit": UNIT,
-                "h2d_bytes_per_step": int(q.numel() * 4),
-                "d2h_bytes_per_step": int(out.numel() * 4 + n_groups * 24)},
+                "h2d_bytes_per_step": int(2 * n_groups * G * d * 4),
+                "d2h_bytes_per_step": int(n_groups * G * d * 4 + n_groups * ct.sizeof(sb.AttnStats))},
         "clocks": clk,
         "gpu_launches": int(kernels_per_step * a.steps),
         "kernels_per_step": int(kernels_per_step),
-        "prefill_build_ms_per_layer": round(float(np.mean(t_build)), 2),
-        "plan_trace_cycles": plan_trace,
-        "decode_trace": decode_trace,
-        "step_trace_us": step_trace,
-        "graph_plan_trace": graph_plan_trace,
+        "setup_s": round(t_setup, 1),
+        "prefill_build_ms_per_layer": round(float(np.mean([l.t_build_ms for l in layers])), 2),
         "prefill": {
             "keys": n_keys_prefill, "assign_ms": round(assign_ms, 3), "pack_ms": round(pack_ms, 3),
             "keys_per_s": round(n_keys_prefill / ((assign_ms + pack_ms) * 1e-3), 1),
@@ -606,13 +613,113 @@ def ours(a):
             "assign_frac_of_bf16_sustained": round(2 * n_keys_prefill * C * d / (assign_ms * 1e-3) / 1e12
                                                    / 1389.8, 4),
             "pack_gbs": round(pack_bytes / (pack_ms * 1e-3) / 1e9, 1),
-            "pack_frac": round(pack_bytes / (pack_ms * 1e-3) / 1e9 / peak_early, 4),
+            "pack_frac": round(pack_bytes / (pack_ms * 1e-3) / 1e9 / peak, 4),
         },
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def parity_leg(sb, torch, ctx, a, lay, groups, sparse_step, dense_step, out, out_dense, stats,
+               heads_local, h0, threads, timed_groups):
+    """The compiled reference on this layer's inputs for `groups`: assignment
+    (sequence 0's contexts, full length), routed lists, counters, outputs,
+    mse vs exact attention and coverage; plus the reference's step time."""
+    import oracle
+    if not oracle.ref_available():
+        return {"skipped": "oracle/_ref not built"}, None
+    R = oracle.ref()
+    G, d, N, C = a.q_heads // a.kv_heads, a.dim, a.ctx_len, a.buckets
+    n_groups = len(lay.routers)
+    sel_t = torch.empty(n_groups, a.probes, dtype=torch.int32, device=out.device)
+    lay.L.sparse_attention_dev(lay.routers, lay.qr_t, lay.qd_t, G,
+                               sb.SparseAttnConfig(a.probes, 128, sb.DenseWindow(a.sink, a.recent)),
+                               out, stats, selected=sel_t)
+    torch.cuda.synchronize()
+    g_out, g_st = out.cpu().numpy().copy(), stats.cpu().numpy().copy()
+    g_sel = sel_t.cpu().numpy().view(np.uint32).copy()
+    dense_step(lay)
+    torch.cuda.synchronize()
+    g_full = out_dense.cpu().numpy().copy()
+    g_cov = lay.L.coverage(lay.qr, g_sel, sb.DenseWindow(a.sink, a.recent))
+
+    rts = {}
+    stores, routers = [], []
+    assign_exact, assign_checked = 0, 0
+    for gi in groups:
+        s, hl = divmod(gi, heads_local)
+        rows = slice(gi * N, (gi + 1) * N)
+        K = lay.K[rows].float().cpu().numpy()
+        V = lay.V[rows].float().cpu().numpy()
+        g_assign, g_ix = lay.L.read_index(gi)
+        cent = lay.cents[hl]
+        if s == 0:  # the reference's assign_keys + build_ivf on every key of these contexts
+            Kd = lay.Kd[rows][a.sink:].float().cpu().numpy()
+            r_assign = R.assign_keys(Kd, cent, threads=threads)
+            r_off, r_idx = R.build_ivf(r_assign, C)
+            assign_checked += 1
+            assign_exact += int(np.array_equal(r_assign, g_assign) and np.array_equal(r_off, g_ix.off)
+                                and np.array_equal(r_idx, g_ix.idx))
+            del Kd
+        stores.append(R.store(K, V, cent, a.sink, g_assign))
+        if hl not in rts:
+            rts[hl] = R.centroid_router(cent, True)
+        routers.append(rts[hl])
+        del K, V
+    qr, qd = lay.qr[groups], lay.qd[groups]
+    t0 = time.time()
+    ref = R.parity_batch(stores, routers, qr, qd, a.probes, 128, a.sink, a.recent, threads)
+    t_parity = time.time() - t0
+    gs = np.array(groups)
+    sel_eq = int(sum(np.array_equal(ref["selected"][i], g_sel[g]) for i, g in enumerate(groups)))
+    ks_eq = int(np.sum(ref["keys_scored"] == g_st[gs, 0].astype(np.uint64)))
+    mv_eq = int(np.sum(ref["max_visited"] == g_st[gs, 1].astype(np.uint64)))
+    em_eq = int(np.sum(ref["empty"] == g_st[gs, 2]))
+    err = max(oracle.max_rel_diff(g_out[g], ref["out"][i]) for i, g in enumerate(groups))
+    err_full = max(oracle.max_rel_diff(g_full[g], ref["full"][i]) for i, g in enumerate(groups))
+    mse_g = float(np.mean([R.mse(g_out[g], g_full[g]) for g in groups]))
+    mse_r = float(np.mean([R.mse(ref["out"][i], ref["full"][i]) for i in range(len(groups))]))
+    cov_g, cov_r = float(np.mean(g_cov[gs])), float(np.mean(ref["coverage"]))
+    cov_err = float(np.max(np.abs(g_cov[gs] - ref["coverage"])))
+    n = len(groups)
+    ok = (sel_eq == n and ks_eq == n and mv_eq == n and em_eq == n and err <= TOL
+          and err_full <= TOL and assign_exact == assign_checked
+          and abs(mse_g - mse_r) <= TOL * mse_r and cov_err <= TOL)
+    parity = {
+        "groups": n, "pass": bool(ok),
+        "assignment_bit_exact": f"{assign_exact}/{assign_checked} contexts (all {N - a.sink} keys, off, idx)",
+        "selected_lists_bit_exact": f"{sel_eq}/{n}",
+        "keys_scored_exact": f"{ks_eq}/{n}", "max_visited_bucket_exact": f"{mv_eq}/{n}",
+        "empty_attention_exact": f"{em_eq}/{n}",
+        "sparse_max_rel_diff": err, "dense_max_rel_diff": err_full, "tolerance": TOL,
+        "mse_vs_exact": {"gpu": mse_g, "reference": mse_r, "rel_diff": abs(mse_g - mse_r) / mse_r},
+        "coverage": {"gpu": cov_g, "reference": cov_r, "max_abs_diff": cov_err},
+        "reference_parity_pass_s": round(t_parity, 1),
+    }
+    cpu = None
+    if timed_groups:
+        def step():
+            return R.sparse_attention_batch(stores, routers, qr, qd, a.probes, 128, a.sink,
+                                            a.recent, threads)
+        step()
+        t1 = time.perf_counter()
+        reps = 3
+        for _ in range(reps):
+            step()
+        us_cpu = (time.perf_counter() - t1) / reps * 1e6
+        t1 = time.perf_counter()
+        R.sparse_attention_batch(stores[:1], routers[:1], qr[:1], qd[:1], a.probes, 128, a.sink,
+                                 a.recent, 1)
+        us_one = (time.perf_counter() - t1) * 1e6
+        cpu = {"value": round(us_cpu, 1), "unit": UNIT, "cores": threads, "kind": "reference",
+               "cpu": cpu_info(),
+               "sample": (f"the full step ({n} groups of layer 0, the same inputs as the GPU step), "
+                          f"{threads}-thread pool over groups, {reps} timed steps"),
+               "single_thread_us_per_group": round(us_one, 1)}
+    del stores
+    return parity, cpu
 
 
 def main():

@@ -344,13 +344,23 @@ SAAP_API int saap_ctx_timing(saap_ctx* ctx, double* route_plan_ms, double* atten
 
 /* Kernel launches issued by this context so far (bench "gpu_launches"). */
 SAAP_API int saap_ctx_launch_count(saap_ctx* ctx, uint64_t* out);
+/* Tuning and diagnostics, per context (no environment variables are read):
+ *   chunk (8), chunk_dense (16)   work-stream tiles per decode ticket
+ *   tail_per_cta (1)              guided-tail singles per CTA
+ *   decode_poll_ns (100), combine_poll_ns (1000)   polling back-off
+ *   decode_wait (0)               1: decode starts after routing (no overlap)
+ *   cluster_route (1)             0: general routing path only
+ *   host_graph (1)                0: saap_sparse_attention never replays graphs
+ *   trace_step / trace_decode / trace_plan (0)     saap_debug_*_trace buffers
+ * Unknown names / out-of-range values: SAAP_ERR_INVALID_ARGUMENT. */
+SAAP_API int saap_ctx_set_option(saap_ctx* ctx, const char* name, int64_t value);
 
 /* ---- diagnostics ------------------------------------------------------- */
 /* out[i] = the device port of glibc exp(x[i]) used by the Q-model router
  * softmax (host arrays); lets tests pin it against the host libm. */
 SAAP_API int saap_debug_exp(saap_ctx* ctx, const double* x, uint64_t n, double* out);
 
-/* With SAAP_PLAN_TRACE set: clock64 offsets of the planner's phases for
+/* With option trace_plan set: clock64 offsets of the planner's phases for
  * context 0 of the last routed decode step (16 x u64), then per fused routing
  * CTA {start, scores exchanged, selected, end (globaltimer ns), candidates,
  * 0} (6 x 1024 x u64). */
@@ -362,13 +372,13 @@ SAAP_API int saap_debug_plan_trace(saap_ctx* ctx, uint64_t* out);
  * counters, nonzero partial/ready flags}. */
 SAAP_API int saap_debug_step_state(saap_ctx* ctx, uint64_t* out);
 
-/* With SAAP_STEP_TRACE set when the context was created: reset (reset=1) or
+/* With option trace_step set: reset (reset=1) or
  * read (reset=0) the step timeline: first start / last end (globaltimer ns)
  * of {approximate routing, planner, decode, combine, last run published,
  * last slot complete, -, -} (16 x u64). */
 SAAP_API int saap_debug_step_trace(saap_ctx* ctx, uint64_t* out, int reset);
 
-/* With SAAP_DECODE_TRACE set: per attention CTA of the last decode step
+/* With option trace_decode set: per attention CTA of the last decode step
  * {start, first tile, end (globaltimer ns), tiles consumed, producer cycles
  * waiting for a free stage, producer cycles total, consumer cycles waiting
  * for data, producer cycles feeding work records, producer cycles waiting for

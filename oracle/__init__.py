@@ -514,6 +514,44 @@ class Ref:
                                    C.byref(out)))
         return out.value
 
+    def generate_prompts(self, spec: HeadSpec, seeds, prompt_seeds, n_keys, n_q, threads,
+                         want=("keys_deroped", "keys_roped", "values")):
+        """generate_prompt for (spec with seed=seeds[i], prompt_seeds[i]) on a pool."""
+        n, d = len(seeds), spec.dim
+        blocks = {k: [np.empty((n_keys, d), np.float32) if k in want else None for _ in range(n)]
+                  for k in ("keys_deroped", "keys_roped", "values")}
+        arr = {k: (C.c_void_p * n)(*[(b.ctypes.data if b is not None else None) for b in v])
+               for k, v in blocks.items()}
+        qd = np.empty((n, n_q, d), np.float32)
+        qr = np.empty((n, n_q, d), np.float32)
+        s = spec.c()
+        self._chk(self.lib.ref_generate_prompts(
+            C.byref(s), _u64(n), _p(np.ascontiguousarray(seeds, np.uint64)),
+            _p(np.ascontiguousarray(prompt_seeds, np.uint64)), _u64(n_keys), _u64(n_q),
+            _u64(threads), arr["keys_deroped"], arr["keys_roped"], arr["values"], _p(qd), _p(qr)))
+        return blocks, qd, qr
+
+    def parity_batch(self, stores, routers, q_roped, q_deroped, probes, block_size, sink, recent,
+                     threads):
+        """Per group: routed list, sparse_attention (+ counters), full_attention,
+        attention_mass_coverage of the routed list (ref_capi.cpp ref_parity_batch)."""
+        n = len(stores)
+        qr, qd = _f32(q_roped), _f32(q_deroped)
+        G, d = qr.shape[1], qr.shape[2]
+        sp = (C.c_void_p * n)(*[s.h for s in stores])
+        rp = (C.c_void_p * n)(*[r.h for r in routers])
+        o = {"out": np.empty((n, G, d), np.float32), "full": np.empty((n, G, d), np.float32),
+             "selected": np.empty((n, max(probes, 1)), np.uint32),
+             "keys_scored": np.empty(n, np.uint64), "max_visited": np.empty(n, np.uint64),
+             "empty": np.empty(n, np.int32), "coverage": np.empty(n, np.float64)}
+        self._chk(self.lib.ref_parity_batch(
+            _u64(n), sp, rp, _p(qr), _p(qd), _u64(G), _u64(d), _u64(probes), _u64(block_size),
+            _u64(sink), _u64(recent), _u64(threads), _p(o["out"]), _p(o["full"]),
+            _p(o["selected"]), _p(o["keys_scored"]), _p(o["max_visited"]), _p(o["empty"]),
+            _p(o["coverage"])))
+        o["selected"] = o["selected"][:, :probes]
+        return o
+
     # persistent handles
     def store(self, keys_roped, values, cent, sink, assignment):
         return RefStore(self, keys_roped, values, cent, sink, assignment)

@@ -475,6 +475,98 @@ int ref_sparse_attention_batch(std::uint64_t n_groups, void* const* stores,
     });
 }
 
+// The parity pass of the bench (tests too): per (store, router, group) on
+// a thread pool, everything the GPU step is compared with -- the routed list
+// (router.select), sparse_attention (output + counters), full_attention (the
+// exact output, for mse) and attention_mass_coverage of the routed list.
+int ref_parity_batch(std::uint64_t n_groups, void* const* stores, void* const* routers,
+                     const float* q_roped, const float* q_deroped, std::uint64_t G,
+                     std::uint64_t d, std::uint64_t probes, std::uint64_t block_size,
+                     std::uint64_t sink, std::uint64_t recent, std::uint64_t threads,
+                     float* out_sparse, float* out_full, std::uint32_t* selected,
+                     std::uint64_t* keys_scored, std::uint64_t* max_visited, int* empty,
+                     double* coverage) {
+    return guard([&] {
+        const std::size_t T = std::max<std::uint64_t>(1, threads);
+        std::atomic<std::uint64_t> next{0};
+        std::atomic<int> failed{0};
+        std::vector<std::thread> pool;
+        for (std::size_t t = 0; t < T; ++t) {
+            pool.emplace_back([&] {
+                for (;;) {
+                    const std::uint64_t g = next.fetch_add(1);
+                    if (g >= n_groups) return;
+                    try {
+                        const ContextStore& s = static_cast<RefStore*>(stores[g])->store;
+                        const BucketRouter& r = *static_cast<RefRouter*>(routers[g])->router;
+                        TensorBlock qr = block(q_roped + g * G * d, G, d);
+                        TensorBlock qd = block(q_deroped + g * G * d, G, d);
+                        auto ids = r.select(qr, qd, probes);
+                        std::copy(ids.begin(), ids.end(), selected + g * probes);
+                        SparseAttnConfig cfg;
+                        cfg.probes = probes;
+                        cfg.block_size = block_size;
+                        cfg.dense = DenseWindow{sink, recent};
+                        AttnResult a = sparse_attention(qr, qd, s, r, cfg);
+                        put(a.output, out_sparse + g * G * d);
+                        keys_scored[g] = a.keys_scored;
+                        max_visited[g] = a.max_visited_bucket;
+                        empty[g] = a.empty_attention ? 1 : 0;
+                        put(full_attention(qr, s.keys, s.values), out_full + g * G * d);
+                        coverage[g] = attention_mass_coverage(
+                                qr, s, std::span<const std::uint32_t>(ids.data(), ids.size()),
+                                DenseWindow{sink, recent});
+                    } catch (const std::exception&) {
+                        failed = 1;
+                        return;
+                    }
+                }
+            });
+        }
+        for (auto& th : pool) th.join();
+        if (failed) throw std::runtime_error("ref_parity_batch: a group failed");
+    });
+}
+
+// generate_prompt for many (spec seed, prompt seed) pairs on a thread pool
+// (the reference generator is single-threaded; prompts are independent).
+int ref_generate_prompts(const RefSpec* spec, std::uint64_t n_prompts, const std::uint64_t* seeds,
+                         const std::uint64_t* prompt_seeds, std::uint64_t n_keys, std::uint64_t n_q,
+                         std::uint64_t threads, float* const* keys_deroped,
+                         float* const* keys_roped, float* const* values, float* q_deroped,
+                         float* q_roped) {
+    return guard([&] {
+        const std::size_t T = std::max<std::uint64_t>(1, threads);
+        std::atomic<std::uint64_t> next{0};
+        std::atomic<int> failed{0};
+        std::vector<std::thread> pool;
+        const std::size_t d = spec->dim;
+        for (std::size_t t = 0; t < T; ++t) {
+            pool.emplace_back([&] {
+                for (;;) {
+                    const std::uint64_t i = next.fetch_add(1);
+                    if (i >= n_prompts) return;
+                    try {
+                        RefSpec sp = *spec;
+                        sp.seed = seeds[i];
+                        SyntheticPrompt p = generate_prompt(make_spec(&sp), n_keys, n_q, prompt_seeds[i]);
+                        if (keys_deroped && keys_deroped[i]) put(p.keys_deroped, keys_deroped[i]);
+                        if (keys_roped && keys_roped[i]) put(p.keys_roped, keys_roped[i]);
+                        if (values && values[i]) put(p.values, values[i]);
+                        if (q_deroped) put(p.queries_deroped, q_deroped + i * n_q * d);
+                        if (q_roped) put(p.queries_roped, q_roped + i * n_q * d);
+                    } catch (const std::exception&) {
+                        failed = 1;
+                        return;
+                    }
+                }
+            });
+        }
+        for (auto& th : pool) th.join();
+        if (failed) throw std::runtime_error("ref_generate_prompts: a prompt failed");
+    });
+}
+
 } // extern "C"
 
 // ---------------------------------------------------------------- artifacts

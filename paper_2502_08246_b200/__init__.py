@@ -236,6 +236,13 @@ class Context:
         _check(lib().saap_ctx_launch_count(self.h, C.byref(v)))
         return v.value
 
+    def set_option(self, name: str, value: int):
+        """Per-context tuning / diagnostics (saap_ctx_set_option): chunk,
+        chunk_dense, tail_per_cta, decode_poll_ns, combine_poll_ns,
+        decode_wait, cluster_route, host_graph, trace_step, trace_decode,
+        trace_plan."""
+        _check(lib().saap_ctx_set_option(self.h, name.encode(), C.c_int64(int(value))))
+
     def set_assign_mode(self, mode: int):
         """0: tcgen05 assignment (bf16 device keys, d=128) + fp64 re-check; 1: fp64 only."""
         _check(lib().saap_ctx_set_assign_mode(self.h, C.c_int(mode)))

@@ -437,14 +437,6 @@ void enqueue_route_score(saap_ctx* c, uint64_t n_groups, uint64_t D, uint64_t C,
     pa.cand_i = ci;
 }
 
-// work-stream tiles per decode ticket (SAAP_CHUNK / SAAP_CHUNK_DENSE override, tuning only)
-uint32_t env_u32(const char* name, uint32_t dflt) {
-    const char* v = std::getenv(name);
-    return v && *v ? (uint32_t)std::min(32, std::max(1, std::atoi(v))) : dflt;
-}
-const uint32_t kChunkSparse = env_u32("SAAP_CHUNK", 8);
-const uint32_t kChunkDense = env_u32("SAAP_CHUNK_DENSE", 16);
-
 // Everything a decode step reads about its cache.
 struct DecodeSrc {
     uint64_t n_groups = 0, D = 0, C = 1, max_n = 0, rows = 0;
@@ -665,8 +657,8 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
         pa.stats = stats;
         pa.selected = selected;
         const bool routed = (mode == 1 || mode == 2) && probes > 0;
-        static const bool trace_on = std::getenv("SAAP_PLAN_TRACE") != nullptr;
-        static const bool no_cluster = std::getenv("SAAP_NO_CLUSTER_ROUTE") != nullptr;
+        const bool trace_on = c->opt.trace_plan != 0;
+        const bool no_cluster = c->opt.cluster_route == 0;
         // fused cluster routing: centroid router, C a power of two <= 1024,
         // the packed layout's window (every routed context has rb == T)
         const bool fused = routed && mode == 1 && slots && cmax && centR && !no_cluster &&
@@ -726,16 +718,13 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     const uint64_t max_stream = sp->n_tiles + n_groups * dyn_per_group * n_hchunks;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)c->sm_count,
                                                                     (max_stream + chunk - 1) / chunk));
-    da.tail = env_u32("SAAP_TAIL_PER_CTA", 1) * (uint32_t)grid;
-    static const uint32_t dec_poll = env_u32("SAAP_DEC_POLL_NS", 100);
-    da.poll_ns = dec_poll;
+    da.tail = c->opt.tail_per_cta * (uint32_t)grid;
+    da.poll_ns = c->opt.decode_poll_ns;
     da.tl = c->tl;
-    static const int wait_env = std::getenv("SAAP_DECODE_WAIT") ? std::atoi(std::getenv("SAAP_DECODE_WAIT")) : 0;
-    da.wait_plan = plan && wait_env ? 1u : 0u;
+    da.wait_plan = plan && c->opt.decode_wait ? 1u : 0u;
     // static tickets: enough to give every CTA a share of the window
     da.chunk_st = plan ? std::max<uint32_t>(1u, std::min<uint32_t>(chunk, sp->n_tiles / (uint32_t)grid)) : chunk;
-    static const bool dtrace_on = std::getenv("SAAP_DECODE_TRACE") != nullptr;
-    if (dtrace_on) da.dtrace = (unsigned long long*)ensure(c, c->dtrace, (size_t)c->sm_count * 128);
+    if (c->opt.trace_decode) da.dtrace = (unsigned long long*)ensure(c, c->dtrace, (size_t)c->sm_count * 128);
     launch_decode((int)D, *src.maps, da, grid, st);
     CombineArgs ca{};
     ca.st_cnt = sp->cnt;
@@ -749,7 +738,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     ca.n_hchunks = (uint32_t)n_hchunks;
     ca.out = out;
     ca.tl = c->tl;
-    ca.poll_ns = std::getenv("SAAP_POLL_NS") ? (uint32_t)std::atoi(std::getenv("SAAP_POLL_NS")) : 1000u;
+    ca.poll_ns = c->opt.combine_poll_ns;
     launch_combine((int)D, ca, (uint32_t)qslots, st);
     c->launches += 2;
     if (e2) {
@@ -857,10 +846,6 @@ int saap_ctx_create(int device, saap_ctx** out) {
         SAAP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = true;
         c->counters = dmalloc<StepCounters>(1);
-        if (std::getenv("SAAP_STEP_TRACE")) {
-            c->tl = dmalloc<unsigned long long>(16);
-            SAAP_CUDA(cudaMemset(c->tl, 0, 128));
-        }
         SAAP_CUDA(cudaMemset(c->counters, 0, sizeof(StepCounters)));
         *out = c;
     });
@@ -951,6 +936,49 @@ int saap_ctx_launch_count(saap_ctx* c, uint64_t* out) {
     return guard([&] {
         need(c, "ctx");
         *out = c->launches;
+    });
+}
+
+// Tuning / diagnostic options (the round-1 environment knobs), per context.
+int saap_ctx_set_option(saap_ctx* c, const char* name, int64_t value) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(name, "option name");
+        const std::string n(name);
+        auto& o = c->opt;
+        auto clamp = [&](int64_t lo, int64_t hi) {
+            if (value < lo || value > hi)
+                invalid("saap_ctx_set_option: " + n + "=" + std::to_string(value) + " outside [" +
+                        std::to_string(lo) + ", " + std::to_string(hi) + "]");
+            return (uint32_t)value;
+        };
+        if (c->capturing) invalid("saap_ctx_set_option during graph capture");
+        if (n == "chunk") o.chunk = clamp(1, 32);
+        else if (n == "chunk_dense") o.chunk_dense = clamp(1, 32);
+        else if (n == "tail_per_cta") o.tail_per_cta = clamp(0, 8);
+        else if (n == "decode_poll_ns") o.decode_poll_ns = clamp(0, 100000);
+        else if (n == "combine_poll_ns") o.combine_poll_ns = clamp(0, 100000);
+        else if (n == "decode_wait") o.decode_wait = clamp(0, 1);
+        else if (n == "cluster_route") o.cluster_route = clamp(0, 1);
+        else if (n == "host_graph") o.host_graph = clamp(0, 1);
+        else if (n == "trace_decode") o.trace_decode = clamp(0, 1);
+        else if (n == "trace_plan") o.trace_plan = clamp(0, 1);
+        else if (n == "trace_step") {
+            o.trace_step = clamp(0, 1);
+            if (o.trace_step && !c->tl) {
+                c->tl = dmalloc<unsigned long long>(16);
+                SAAP_CUDA(cudaMemset(c->tl, 0, 128));
+            } else if (!o.trace_step && c->tl) {
+                sync(c);
+                dfree(c->tl);
+            }
+        } else {
+            invalid("saap_ctx_set_option: unknown option '" + n + "'");
+        }
+        // saved host-API step graphs hold the old launch parameters
+        for (auto& g : c->host_graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+        c->host_graphs.clear();
     });
 }
 
@@ -2359,7 +2387,7 @@ static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* con
     const uint32_t nh = (uint32_t)((G + kHeadsPerSlot - 1) / kHeadsPerSlot);
     const saap_static_plan* sp = static_plan(c, L->plans, L->h_meta, 1, cfg->recent_count, nh);
     enqueue_decode(c, src, sp, mode, L->d_centT, L->d_qm, qr, q_route, G, cfg->probes,
-                   cfg->recent_count, out, stats, selected, kChunkSparse, (uint32_t)hq,
+                   cfg->recent_count, out, stats, selected, c->opt.chunk, (uint32_t)hq,
                    mode == 1 ? L->d_cmax : nullptr, mode == 1 ? L->d_centR : nullptr,
                    mode == 1 ? (const ApproxSlot*)L->d_route_slots : nullptr, mode == 1 ? L->n_route_slots : 0,
                    mode == 2 ? L->d_qm_slots : nullptr, mode == 2 ? L->n_qm_slots : 0);
@@ -2406,8 +2434,8 @@ int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* c
         // Repeated calls with the same (layer, routers, cfg, shapes) replay a
         // CUDA graph of the step captured on the second call (the first sizes
         // the scratch); timing and trace modes stay eager.
-        static const bool no_graph = std::getenv("SAAP_NO_HOST_GRAPH") || std::getenv("SAAP_STEP_TRACE") ||
-                                     std::getenv("SAAP_DECODE_TRACE") || std::getenv("SAAP_PLAN_TRACE");
+        const bool no_graph = !c->opt.host_graph || c->opt.trace_step || c->opt.trace_decode ||
+                              c->opt.trace_plan;
         saap_ctx::HostGraph* hg = nullptr;
         if (!no_graph && !c->timing) {
             std::vector<const void*> rs(routers, routers + L->n_groups);
@@ -2517,7 +2545,7 @@ int saap_layer_full_attention(saap_ctx* c, const saap_layer* L, const float* q, 
         const uint32_t nh = (uint32_t)((G + kHeadsPerSlot - 1) / kHeadsPerSlot);
         const saap_static_plan* sp = static_plan(c, const_cast<saap_layer*>(L)->plans, L->h_meta, 0, 0, nh);
         enqueue_decode(c, src, sp, 0, nullptr, nullptr, dq, nullptr, G, 0, 0, dout, nullptr, nullptr,
-                       kChunkDense);
+                       c->opt.chunk_dense);
         d2h(out, dout, qn * 4, st);
         sync(c);
     });
@@ -2565,7 +2593,7 @@ int saap_full_attention(saap_ctx* c, const float* q, uint64_t G, const float* ke
         if (c->capturing) invalid("full_attention: not capturable (uploads its keys)");
         saap_static_plan* sp = build_static_plan({gm}, 0, 0, nh);
         enqueue_decode(c, src, sp, 0, nullptr, nullptr, dq, nullptr, G, 0, 0, dout, nullptr, nullptr,
-                       kChunkDense);
+                       c->opt.chunk_dense);
         d2h(out, dout, G * d * 4, st);
         sync(c);
         free_static_plan(sp);
@@ -2640,7 +2668,7 @@ int saap_dense_attention_dev(saap_ctx* c, const saap_kvcache* kc, const float* q
         const saap_static_plan* sp =
                 static_plan(c, const_cast<saap_kvcache*>(kc)->plans, kc->h_meta, 0, 0, nh);
         enqueue_decode(c, src, sp, 0, nullptr, nullptr, q, nullptr, G, 0, 0, out, nullptr, nullptr,
-                       kChunkDense);
+                       c->opt.chunk_dense);
     });
 }
 
@@ -2697,7 +2725,7 @@ int saap_debug_exp(saap_ctx* c, const double* x, uint64_t n, double* out) {
 int saap_debug_plan_trace(saap_ctx* c, uint64_t* out) {
     return guard([&] {
         DeviceGuard dg(c);
-        if (!c->trace.p) invalid("plan tracing off: set SAAP_PLAN_TRACE before the first decode");
+        if (!c->trace.p) invalid("plan tracing off: set option trace_plan before the first decode");
         d2h(out, c->trace.p, 128 + 48 * 1024, c->stream);
         sync(c);
     });
@@ -2741,7 +2769,7 @@ int saap_debug_step_state(saap_ctx* c, uint64_t* out) {
 int saap_debug_step_trace(saap_ctx* c, uint64_t* out, int reset) {
     return guard([&] {
         DeviceGuard dg(c);
-        if (!c->tl) invalid("step tracing off: set SAAP_STEP_TRACE before creating the context");
+        if (!c->tl) invalid("step tracing off: saap_ctx_set_option(ctx, \"trace_step\", 1) first");
         if (reset) {
             uint64_t init[16];
             for (int k = 0; k < 8; ++k) {
@@ -2759,7 +2787,7 @@ int saap_debug_step_trace(saap_ctx* c, uint64_t* out, int reset) {
 int saap_debug_decode_trace(saap_ctx* c, uint64_t* out, uint64_t n_ctas) {
     return guard([&] {
         DeviceGuard dg(c);
-        if (!c->dtrace.p) invalid("decode tracing off: set SAAP_DECODE_TRACE before the first decode");
+        if (!c->dtrace.p) invalid("decode tracing off: set option trace_decode before the first decode");
         if (n_ctas > (uint64_t)c->sm_count) invalid("decode trace: more CTAs than SMs");
         d2h(out, c->dtrace.p, n_ctas * 128, c->stream);
         sync(c);

@@ -196,7 +196,7 @@ struct saap_ctx {
     // growable device scratch (sized by uncaptured calls; graphs reuse it)
     saap_scratch approx, trace, dtrace, cand_s, cand_i, tiles, part_O, part_ml, probs, stats, sel, qr, qd, out, misc, zeros;
     saap_scratch runs, dyn_cnt, part_flag;  // zero between steps (the combine re-arms them)
-    unsigned long long* tl = nullptr;  // debug step timeline (SAAP_STEP_TRACE)
+    unsigned long long* tl = nullptr;  // debug step timeline (option trace_step)
     saap_b200::StepCounters* counters = nullptr;  // persistent, 128 B
     // host-API graph cache (saap_sparse_attention): graphs reference scratch,
     // so any scratch reallocation bumps scratch_gen and retires them
@@ -215,6 +215,20 @@ struct saap_ctx {
     // optional per-kernel timing (eager steps)
     bool timing = false;
     std::vector<cudaEvent_t> ev;  // triples: before plan, before attention, after
+    // tuning / diagnostics, per context (saap_ctx_set_option; no environment reads)
+    struct Options {
+        uint32_t chunk = 8;             // work-stream tiles per decode ticket (sparse)
+        uint32_t chunk_dense = 16;      // ... (dense / full attention)
+        uint32_t tail_per_cta = 1;      // guided-tail singles per CTA
+        uint32_t decode_poll_ns = 100;  // producer back-off while waiting for the planner
+        uint32_t combine_poll_ns = 1000;  // combine back-off while no run is published
+        uint32_t decode_wait = 0;       // 1: decode waits for routing to finish (PDL grid wait)
+        uint32_t cluster_route = 1;     // 0: force the general routing path
+        uint32_t host_graph = 1;        // 0: saap_sparse_attention never replays graphs
+        uint32_t trace_step = 0;        // step timeline (saap_debug_step_trace)
+        uint32_t trace_decode = 0;      // per-CTA decode timeline (saap_debug_decode_trace)
+        uint32_t trace_plan = 0;        // routing phases (saap_debug_plan_trace)
+    } opt;
 };
 
 // Host-planned static part of a decode work stream (the dense window, or
