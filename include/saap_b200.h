@@ -252,6 +252,13 @@ SAAP_API int saap_layer_build(saap_ctx* ctx, saap_layer* L, const saap_partition
 SAAP_API int saap_layer_build_dev(saap_ctx* ctx, saap_layer* L, const saap_partition* const* parts,
                          const void* keys_roped_bf16, const void* values_bf16,
                          const void* keys_assign_bf16);
+/* A ContextStore assembled field by field (attention.hpp:76-86; e.g.
+ * attention_test.cpp:418-432): keys/values f32 (rounded to the bf16 cache),
+ * the caller's assignment [sum_g (n_g - sink)] u32 < C, concatenated per
+ * group; the IVF and the packed layout are built from it on the device. */
+SAAP_API int saap_layer_build_assigned(saap_ctx* ctx, saap_layer* L,
+                                       const saap_partition* const* parts, const float* keys_roped,
+                                       const float* values, const uint32_t* assignment);
 
 /* Incremental decode index: append k keys to every
  * context (device bf16 rows [n_groups x k x dim] each: roped keys, values,
@@ -298,6 +305,29 @@ SAAP_API int saap_sparse_attention_dev(saap_ctx* ctx, const saap_layer* L,
                               const float* q_deroped_dev, uint64_t G,
                               const saap_sparse_cfg* cfg, float* out_dev,
                               saap_attn_stats* stats_dev, uint32_t* selected_dev);
+/* sparse_attention(q_roped, q_deroped, store, router, cfg) with ANY
+ * BucketRouter (attention.hpp:102-108, attention.cpp:351): the caller runs
+ * router.select and passes the returned ids, selected[g * l + b] (each < C;
+ * l may differ from cfg->probes, a repeated id is absorbed once per
+ * occurrence on the packed-window path, like the reference).  The lists are
+ * ignored where the reference does not consult the router (probes == 0, or
+ * the window covers the context).  Host buffers, synchronous. */
+SAAP_API int saap_sparse_attention_selected(saap_ctx* ctx, const saap_layer* L,
+                                            const float* q_roped, uint64_t G,
+                                            const uint32_t* selected, uint64_t l,
+                                            const saap_sparse_cfg* cfg, float* out,
+                                            saap_attn_stats* stats);
+/* Device-pointer variant (asynchronous, graph-capturable; ids not validated:
+ * each must be < C). */
+SAAP_API int saap_sparse_attention_selected_dev(saap_ctx* ctx, const saap_layer* L,
+                                                const float* q_roped_dev, uint64_t G,
+                                                const uint32_t* selected_dev, uint64_t l,
+                                                const saap_sparse_cfg* cfg, float* out_dev,
+                                                saap_attn_stats* stats_dev);
+/* mse(approx, exact): mean squared entrywise difference, the reference's
+ * sequential fp64 sum (bit-identical).  attention.cpp:385-399 */
+SAAP_API int saap_mse(const float* approx, uint64_t rows_a, uint64_t dim_a, const float* exact,
+                      uint64_t rows_e, uint64_t dim_e, double* out);
 
 /* attention_mass_coverage(q_roped, store, selected, dense) for every group
  *                                            attention.cpp:427-462
@@ -384,6 +414,9 @@ SAAP_API int saap_debug_step_trace(saap_ctx* ctx, uint64_t* out, int reset);
  * for data, producer cycles feeding work records, producer cycles waiting for
  * a record, 0 x 7} (16 x u64 each). */
 SAAP_API int saap_debug_decode_trace(saap_ctx* ctx, uint64_t* out, uint64_t n_ctas);
+/* With option trace_decode set: per attention CTA of the last decode step,
+ * 48 tiles x {TMA issued, data landed, consumed} (globaltimer ns). */
+SAAP_API int saap_debug_decode_tiles(saap_ctx* ctx, uint64_t* out, uint64_t n_ctas);
 
 /* ---- synthetic data (bench tooling; counter-based, reproducible) ------- */
 /* Fills a device bf16 [rows x dim] buffer with clustered keys / values. */

@@ -993,6 +993,26 @@ class Layer:
                                                C.byref(c), _dptr(out), _dptr(stats),
                                                _dptr(selected)))
 
+    def sparse_attention_selected(self, q_roped, selected, cfg: SparseAttnConfig):
+        """sparse_attention with the bucket lists of any BucketRouter:
+        selected [n_groups, l] (what router.select returned, attention.cpp:351)."""
+        qr = _f32(q_roped)
+        sel = np.ascontiguousarray(selected, np.uint32).reshape(self.n_groups, -1)
+        out = np.empty_like(qr)
+        stats = (AttnStats * self.n_groups)()
+        c = cfg.c()
+        _check(lib().saap_sparse_attention_selected(self.ctx.h, self.h, _p(qr), _u64(qr.shape[1]),
+                                                    _p(sel), _u64(sel.shape[1]), C.byref(c),
+                                                    _p(out), stats))
+        return out, stats
+
+    def sparse_attention_selected_dev(self, q_roped, G, selected, l, cfg: SparseAttnConfig, out,
+                                      stats=None):
+        c = cfg.c()
+        _check(lib().saap_sparse_attention_selected_dev(self.ctx.h, self.h, _dptr(q_roped), _u64(G),
+                                                        _dptr(selected), _u64(l), C.byref(c),
+                                                        _dptr(out), _dptr(stats)))
+
     def coverage(self, q_roped, selected, dense: DenseWindow):
         """attention_mass_coverage per group (attention.cpp:427-462)."""
         q = _f32(q_roped)
@@ -1083,7 +1103,16 @@ def sparse_attention(q_group_roped, q_group_deroped, store: ContextStore, router
                      cfg: SparseAttnConfig) -> AttnResult:
     qr = _f32(q_group_roped)[None]
     qd = _f32(q_group_deroped)[None] if q_group_deroped is not None else None
-    out, stats, _ = store.sparse_attention(router, qr, qd, cfg)
+    if isinstance(router, BucketRouter):
+        out, stats, _ = store.sparse_attention(router, qr, qd, cfg)
+    else:
+        # any object with the plugin's select(q_roped, q_deroped, l): consulted
+        # where the reference consults it (attention.cpp:336-351)
+        n = store.n_keys_()
+        sel = []
+        if cfg.probes > 0 and n > cfg.dense.sink_count + cfg.dense.recent_count:
+            sel = list(router.select(q_group_roped, q_group_deroped, cfg.probes))
+        out, stats = store.sparse_attention_selected(qr, np.asarray(sel, np.uint32)[None], cfg)
     s = stats[0]
     return AttnResult(out[0], int(s.keys_scored), int(s.max_visited_bucket),
                       bool(s.empty_attention))
@@ -1117,13 +1146,11 @@ def selectivity(result: AttnResult, n_keys: int) -> float:
 
 def mse(approx, exact) -> float:
     """Mean squared entrywise difference (attention.cpp:385-399)."""
-    a = np.asarray(approx, np.float64)
-    b = np.asarray(exact, np.float64)
-    if a.shape != b.shape:
-        raise InvalidArgument(f"mse: shapes {a.shape} vs {b.shape}")
-    if a.size == 0:
-        raise InvalidArgument("mse: empty inputs")
-    return float(np.mean((a - b) ** 2))
+    a, b = np.atleast_2d(_f32(approx)), np.atleast_2d(_f32(exact))
+    out = C.c_double()
+    _check(lib().saap_mse(_p(a), _u64(a.shape[0]), _u64(a.shape[1]), _p(b), _u64(b.shape[0]),
+                          _u64(b.shape[1]), C.byref(out)))
+    return out.value
 
 
 class KVCache:

@@ -93,7 +93,8 @@ struct PlanArgs {
     const uint32_t* assign;
     const uint32_t* invA;
     uint32_t C;
-    int mode;                    // 0 dense, 1 centroid, 2 precomputed scores, 3 window only
+    int mode;                    // 0 dense, 1 centroid, 2 precomputed scores, 3 window only,
+                                 // 4 caller-selected bucket lists (`given`)
     const float* q_route;        // [groups][G][D]
     const double* scores;        // [groups][G][C] per-row probabilities (mode 2)
     uint32_t G, D, n_hchunks;
@@ -121,8 +122,10 @@ struct PlanArgs {
     uint32_t* dyn_cnt;           // [qslots] dynamic tiles | kCntValid
     saap_attn_stats* stats;
     uint32_t* selected;          // nullable [groups][probes]
+    const uint32_t* given;       // mode 4: [groups][probes] bucket ids from the caller's router
 };
 constexpr uint32_t kCntValid = 0x80000000u;
+constexpr int kTraceTiles = 48;  // debug tile stamps per decode CTA
 
 struct DecodeArgs {
     const TileRec* st_tiles;   // static part of the work stream [n_static]
@@ -145,6 +148,7 @@ struct DecodeArgs {
     uint32_t run_cap;
     unsigned long long* rd;  // [qslots] (runs reserved << 32) | tiles published
     unsigned long long* dtrace;  // debug: per CTA {start, first tile, end (globaltimer ns), tiles}
+    unsigned long long* dtiles;  // debug: per CTA x 48 tiles {TMA issued, data landed, consumed}
     unsigned long long* tl;      // debug step timeline (null: off)
 };
 

@@ -587,7 +587,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
                     uint32_t qm_hidden = 0, const float* cmax = nullptr,
                     const float* const* centR = nullptr, const ApproxSlot* slots = nullptr,
                     uint32_t n_slots = 0, const uint32_t* qm_slots = nullptr,
-                    uint32_t n_qm_slots = 0) {
+                    uint32_t n_qm_slots = 0, const uint32_t* given = nullptr) {
     const cudaStream_t st = c->stream;
     const uint64_t n_groups = src.n_groups, D = src.D, C = src.C;
     const uint64_t n_hchunks = (G + kHeadsPerSlot - 1) / kHeadsPerSlot;
@@ -656,6 +656,8 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
         pa.dyn_cnt = dcnt;
         pa.stats = stats;
         pa.selected = selected;
+        pa.given = given;
+        if (mode == 4) pa.P2 = next_pow2((uint32_t)std::max<uint64_t>(probes, 1));
         const bool routed = (mode == 1 || mode == 2) && probes > 0;
         const bool trace_on = c->opt.trace_plan != 0;
         const bool no_cluster = c->opt.cluster_route == 0;
@@ -724,7 +726,10 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     da.wait_plan = plan && c->opt.decode_wait ? 1u : 0u;
     // static tickets: enough to give every CTA a share of the window
     da.chunk_st = plan ? std::max<uint32_t>(1u, std::min<uint32_t>(chunk, sp->n_tiles / (uint32_t)grid)) : chunk;
-    if (c->opt.trace_decode) da.dtrace = (unsigned long long*)ensure(c, c->dtrace, (size_t)c->sm_count * 128);
+    if (c->opt.trace_decode) {
+        da.dtrace = (unsigned long long*)ensure(c, c->dtrace, (size_t)c->sm_count * (128 + kTraceTiles * 24));
+        da.dtiles = da.dtrace + (size_t)c->sm_count * 16;
+    }
     launch_decode((int)D, *src.maps, da, grid, st);
     CombineArgs ca{};
     ca.st_cnt = sp->cnt;
@@ -2261,6 +2266,62 @@ int saap_layer_build_dev(saap_ctx* c, saap_layer* L, const saap_partition* const
     });
 }
 
+// ContextStore{keys, values, id_offset, partition, assignment, index} built
+// field by field (attention_test.cpp:418-432): pack under the caller's
+// assignment instead of computing one.
+int saap_layer_build_assigned(saap_ctx* c, saap_layer* L, const saap_partition* const* parts,
+                              const float* keys_roped, const float* values,
+                              const uint32_t* assignment) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(L, "layer");
+        need(keys_roped, "build_context_store: keys");
+        need(values, "build_context_store: values");
+        bind_parts(L, parts);
+        uint64_t ns_total = 0;
+        for (auto& gm : L->h_meta) ns_total += gm.n - gm.sink;
+        if (ns_total) need(assignment, "build_context_store: assignment");
+        for (uint64_t i = 0; i < ns_total; ++i)
+            if (assignment[i] >= L->C)
+                invalid("build_ivf: bucket id " + std::to_string(assignment[i]) + " out of range " +
+                        std::to_string(L->C));
+        const cudaStream_t st = c->stream;
+        const uint64_t elems = L->total_rows * L->d;
+        float* f32 = dmalloc<float>(elems);
+        uint16_t* Ks = dmalloc<uint16_t>(elems);
+        uint16_t* Vs = dmalloc<uint16_t>(elems);
+        try {
+            h2d(f32, keys_roped, elems * 4, st);
+            launch_f32_to_bf16(f32, Ks, elems, st);
+            h2d(f32, values, elems * 4, st);
+            launch_f32_to_bf16(f32, Vs, elems, st);
+            c->launches += 2;
+            uint64_t a0 = 0;
+            for (auto& gm : L->h_meta) {
+                const uint64_t ns = gm.n - gm.sink;
+                if (ns) h2d(L->assign + gm.ivf_base, assignment + a0, ns * 4, st);
+                a0 += ns;
+            }
+            L->last_tc = false;
+            launch_pack((int)L->d, L->tiles, L->n_tiles, L->tile_first, (uint32_t)L->n_groups, L->meta,
+                        L->assign, (uint32_t)L->C, L->hist, L->countA, L->off, L->offA, L->idx, L->invA,
+                        L->posA, L->list, L->cap_ns, Ks, Vs, L->src_row0, L->K, L->V, st);
+            c->launches += 6;
+            L->built = true;
+            L->idx_stale = false;
+            sync(c);
+        } catch (...) {
+            cudaFree(f32);
+            cudaFree(Ks);
+            cudaFree(Vs);
+            throw;
+        }
+        cudaFree(f32);
+        cudaFree(Ks);
+        cudaFree(Vs);
+    });
+}
+
 int saap_ctx_set_assign_mode(saap_ctx* c, int mode) {
     return guard([&] {
         need(c, "ctx");
@@ -2350,9 +2411,12 @@ static uint64_t max_keys(const saap_layer* L) {
     return m;
 }
 
+// given != null: the bucket lists come from the caller's BucketRouter
+// ([n_groups][l_given] ids < C, attention.cpp:351) instead of a library router.
 static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* const* routers,
                        const float* qr, const float* qd, uint64_t G, const saap_sparse_cfg* cfg,
-                       float* out, saap_attn_stats* stats, uint32_t* selected) {
+                       float* out, saap_attn_stats* stats, uint32_t* selected,
+                       const uint32_t* given = nullptr, uint64_t l_given = 0) {
     saap_layer* L = const_cast<saap_layer*>(Lc);
     if (!L->built) invalid("store not built");
     validate_cfg(L, cfg);
@@ -2361,7 +2425,15 @@ static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* con
     // routers only run when some group's context exceeds the window (attention.cpp:336-351)
     bool any_route = false;
     for (auto& gm : L->h_meta) any_route |= gm.n > cfg->sink_count + cfg->recent_count;
-    if (cfg->probes > 0 && any_route) {
+    uint64_t probes = cfg->probes;
+    if (given) {
+        if (cfg->probes > 0 && any_route && l_given > 0) {
+            mode = 4;
+            probes = l_given;
+        } else {
+            probes = 0;
+        }
+    } else if (cfg->probes > 0 && any_route) {
         need(routers, "sparse_attention: routers");
         bind_routers(L, routers, mode, use_deroped);
         for (uint64_t g = 0; g < L->n_groups; ++g) check_router_dims(routers[g], L->d, L->C, cfg->probes);
@@ -2380,17 +2452,18 @@ static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* con
         if (window_skew(gm, cfg->recent_count)) {
             const bool below = gm.n - cfg->recent_count < gm.T;  // window reaches into region A
             into_region_a |= below;
-            need_gather |= below || (mode != 3 && cfg->probes > 0);
+            need_gather |= below || (mode != 3 && probes > 0);
         }
     if (into_region_a) ensure_index(c, L);
     const DecodeSrc src = layer_src(L, cfg->recent_count, need_gather);
     const uint32_t nh = (uint32_t)((G + kHeadsPerSlot - 1) / kHeadsPerSlot);
     const saap_static_plan* sp = static_plan(c, L->plans, L->h_meta, 1, cfg->recent_count, nh);
-    enqueue_decode(c, src, sp, mode, L->d_centT, L->d_qm, qr, q_route, G, cfg->probes,
-                   cfg->recent_count, out, stats, selected, c->opt.chunk, (uint32_t)hq,
+    enqueue_decode(c, src, sp, mode, L->d_centT, L->d_qm, qr, q_route, G, probes,
+                   cfg->recent_count, out, stats, mode == 4 ? nullptr : selected, c->opt.chunk, (uint32_t)hq,
                    mode == 1 ? L->d_cmax : nullptr, mode == 1 ? L->d_centR : nullptr,
                    mode == 1 ? (const ApproxSlot*)L->d_route_slots : nullptr, mode == 1 ? L->n_route_slots : 0,
-                   mode == 2 ? L->d_qm_slots : nullptr, mode == 2 ? L->n_qm_slots : 0);
+                   mode == 2 ? L->d_qm_slots : nullptr, mode == 2 ? L->n_qm_slots : 0,
+                   mode == 4 ? given : nullptr);
 }
 
 int saap_sparse_attention_dev(saap_ctx* c, const saap_layer* L, const saap_router* const* routers,
@@ -2497,6 +2570,82 @@ int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* c
         if (stats) d2h(stats, dst, L->n_groups * sizeof(saap_attn_stats), st);
         if (selected && cfg->probes) d2h(selected, dsel, L->n_groups * cfg->probes * 4, st);
         sync(c);
+    });
+}
+
+// sparse_attention with the bucket lists of any BucketRouter (attention.hpp:
+// 102-108): selected[g * l + b] is what router.select returned for group g.
+static void check_selected(const saap_layer* L, const uint32_t* selected, uint64_t l) {
+    if (l > (1u << 16)) unsupported("sparse_attention: more than 65536 selected buckets per group");
+    if (l) need(selected, "sparse_attention: selected buckets");
+    for (uint64_t i = 0; i < L->n_groups * l; ++i)
+        if (selected[i] >= L->C)
+            invalid("sparse_attention: router returned bucket " + std::to_string(selected[i]) +
+                    " of " + std::to_string(L->C));
+}
+
+int saap_sparse_attention_selected(saap_ctx* c, const saap_layer* L, const float* q_roped,
+                                   uint64_t G, const uint32_t* selected, uint64_t l,
+                                   const saap_sparse_cfg* cfg, float* out, saap_attn_stats* stats) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(L, "layer");
+        need(q_roped, "sparse_attention: queries");
+        need(out, "sparse_attention: out");
+        if (G == 0) return;
+        validate_cfg(L, cfg);
+        check_selected(L, selected, l);
+        const cudaStream_t st = c->stream;
+        const uint64_t qn = L->n_groups * G * L->d;
+        float* dq = (float*)ensure(c, c->qr, qn * 4);
+        float* dout = (float*)ensure(c, c->out, qn * 4);
+        saap_attn_stats* dst = (saap_attn_stats*)ensure(c, c->stats, L->n_groups * sizeof(saap_attn_stats));
+        uint32_t* dsel = (uint32_t*)ensure(c, c->sel, std::max<uint64_t>(L->n_groups * l, 1) * 4);
+        h2d(dq, q_roped, qn * 4, st);
+        if (l) h2d(dsel, selected, L->n_groups * l * 4, st);
+        sparse_dev(c, L, nullptr, dq, nullptr, G, cfg, dout, dst, nullptr, dsel, l);
+        d2h(out, dout, qn * 4, st);
+        if (stats) d2h(stats, dst, L->n_groups * sizeof(saap_attn_stats), st);
+        sync(c);
+    });
+}
+
+int saap_sparse_attention_selected_dev(saap_ctx* c, const saap_layer* L, const float* q_roped_dev,
+                                       uint64_t G, const uint32_t* selected_dev, uint64_t l,
+                                       const saap_sparse_cfg* cfg, float* out_dev,
+                                       saap_attn_stats* stats_dev) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(L, "layer");
+        need(q_roped_dev, "sparse_attention: queries");
+        need(out_dev, "sparse_attention: out");
+        if (G == 0) return;
+        if (l > (1u << 16)) unsupported("sparse_attention: more than 65536 selected buckets per group");
+        if (l) need(selected_dev, "sparse_attention: selected buckets");
+        sparse_dev(c, L, nullptr, q_roped_dev, nullptr, G, cfg, out_dev, stats_dev, nullptr,
+                   selected_dev, l);
+    });
+}
+
+// mse(approx, exact)   attention.cpp:385-399 (host arithmetic: the
+// reference's sequential fp64 sum, bit-identical)
+int saap_mse(const float* approx, uint64_t rows_a, uint64_t dim_a, const float* exact,
+             uint64_t rows_e, uint64_t dim_e, double* out) {
+    return guard([&] {
+        need(out, "mse: out");
+        if (rows_a != rows_e || dim_a != dim_e)
+            invalid("mse: shapes " + std::to_string(rows_a) + "x" + std::to_string(dim_a) + " vs " +
+                    std::to_string(rows_e) + "x" + std::to_string(dim_e));
+        const uint64_t n = rows_a * dim_a;
+        if (n == 0) invalid("mse: empty inputs");
+        need(approx, "mse: approx");
+        need(exact, "mse: exact");
+        double total = 0.0;
+        for (uint64_t i = 0; i < n; ++i) {
+            const double d = (double)approx[i] - (double)exact[i];
+            total += d * d;
+        }
+        *out = total / (double)n;
     });
 }
 
@@ -2790,6 +2939,18 @@ int saap_debug_decode_trace(saap_ctx* c, uint64_t* out, uint64_t n_ctas) {
         if (!c->dtrace.p) invalid("decode tracing off: set option trace_decode before the first decode");
         if (n_ctas > (uint64_t)c->sm_count) invalid("decode trace: more CTAs than SMs");
         d2h(out, c->dtrace.p, n_ctas * 128, c->stream);
+        sync(c);
+    });
+}
+
+// With option trace_decode set: per attention CTA of the last decode step,
+// kTraceTiles x {TMA issued, data landed, consumed} globaltimer stamps.
+int saap_debug_decode_tiles(saap_ctx* c, uint64_t* out, uint64_t n_ctas) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        if (!c->dtrace.p) invalid("decode tracing off: set option trace_decode before the first decode");
+        if (n_ctas > (uint64_t)c->sm_count) invalid("debug_decode_tiles: n_ctas > SM count");
+        d2h(out, (char*)c->dtrace.p + (size_t)c->sm_count * 128, n_ctas * kTraceTiles * 24, c->stream);
         sync(c);
     });
 }

@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
     const uint32_t n = gm.n, sink = gm.sink, T = gm.T;
     const uint32_t Cb = a.C;
     const bool fallback = (a.mode == 0) || (n <= sink + a.recent);
-    const bool route = !fallback && a.probes > 0 && (a.mode == 1 || a.mode == 2);
+    const bool route = !fallback && a.probes > 0 && (a.mode == 1 || a.mode == 2 || a.mode == 4);
     const uint32_t L = route ? a.probes : 0;
 
     // smem carve: [cand scores P2 f64][cand ids P2 u32][bitmap C/32][segs L+4][seg prefix]
@@ -498,6 +498,17 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
         }
         __syncthreads();
         trace(3);
+    } else if (route && a.mode == 4) {
+        // a BucketRouter of the caller's: its list, in its order (attention.cpp:351-353);
+        // a repeated id is absorbed once per occurrence, like the reference
+        for (uint32_t w = tid; w < bm_words; w += nth) bitmap[w] = 0;
+        __syncthreads();
+        for (uint32_t b = tid; b < L; b += nth) {
+            const uint32_t c = a.given[(size_t)g * a.probes + b];
+            si[b] = c;
+            atomicOr(&bitmap[c >> 5], 1u << (c & 31));
+        }
+        __syncthreads();
     } else if (route) {
         const double* cs = a.cand_s + (size_t)g * a.n_cand;
         const uint32_t* ci = a.cand_i + (size_t)g * a.n_cand;
@@ -795,6 +806,19 @@ __device__ __forceinline__ void dsmem_st_f32(float* local, uint32_t cta, float v
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float dsmem_ld_f32(const float* local, uint32_t cta) {
+    uint32_t remote;
+    float v;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(cta));
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+    return v;
+}
 
 template <int D, int S>
 __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterRouteArgs a) {
@@ -931,6 +955,9 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     trace(1);
     if (a.trace && tid == 0) a.trace[16 + 6 * blockIdx.x + 1] = gt();
     if (!own) {
+        // the owners may still read this CTA's slice (exact re-scoring)
+        cluster_arrive();
+        cluster_wait();
         if (tid == 0) tl_mark(a.tl, 1, false);
         return;
     }
@@ -1125,18 +1152,21 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
             if (tid < L) sel[tid] = cand_id[tid];
         } else if (nS <= kMaxCand) {
             // exact fp64 chains (attention.cpp:296-304: mul rounded before add)
-            // over the candidates' centroid rows, staged (coalesced) into the
-            // now free slice buffer
-            // (from the transposed centroids: the cluster just streamed them, so
-            // these reads hit L2 instead of queueing behind the decode in HBM)
-            // (every load in flight before the first store: one L2 round trip)
-            float* crow = slab;  // [nS][D + 1]
+            // over the candidates' centroid rows, gathered from the cluster's
+            // slices in distributed shared memory (candidate c lives in CTA
+            // c / S, column c % S of its transposed slice): no global round
+            // trip behind the decode's HBM traffic
+            // (every load in flight before the first store)
+            float* crow = qs + (size_t)kSlotGroups * a.G * D;  // [nS][D + 1]
             constexpr uint32_t PE = (kMaxCand * D + NT - 1) / NT;
             float tv[PE];
 #pragma unroll
             for (uint32_t i = 0; i < PE; ++i) {
                 const uint32_t e = tid + i * NT;
-                if (e < nS * D) tv[i] = __ldcg(sl.centT + (size_t)(e / nS) * C + cand_id[e % nS]);
+                if (e < nS * D) {
+                    const uint32_t cc = cand_id[e % nS];
+                    tv[i] = dsmem_ld_f32(slab + (size_t)(e / nS) * S + cc % S, cc / S);
+                }
             }
 #pragma unroll
             for (uint32_t i = 0; i < PE; ++i) {
@@ -1144,6 +1174,7 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
                 if (e < nS * D) crow[(e % nS) * (D + 1) + e / nS] = tv[i];
             }
             __syncthreads();
+            if (a.trace && tid == 0) a.trace[16 + 6 * blockIdx.x + 5] = gt();
             double ex = -INFINITY;
             uint32_t eid = 0xFFFFFFFFu;
             if (tid < nS) {
@@ -1189,8 +1220,14 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
             a.trace[16 + 6 * blockIdx.x + 4] = nS;
         }
     }
+    // this CTA reads no remote slice from here on; it leaves only once every
+    // CTA of the cluster is past its reads of this CTA's slice
+    cluster_arrive();
     // ---- plan (one warp): bucket segments -> 8-aligned virtual rows -> tiles
-    if (tid >= 32) return;
+    if (tid >= 32) {
+        cluster_wait();
+        return;
+    }
     const uint32_t nh = a.n_hchunks;
     const uint32_t rb0 = fallback ? 0 : n - a.recent;  // == T (recent == the layer's hint)
     unsigned long long keys = 0;
@@ -1257,6 +1294,7 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
         if (a.trace) a.trace[16 + 6 * blockIdx.x + 3] = gt();
     }
     trace(5);
+    cluster_wait();
 }
 
 // ============================================================ attention
@@ -1389,6 +1427,7 @@ __global__ void __maxnreg__(144)
         a.dtrace[16 * blockIdx.x] = gtime();
         a.dtrace[16 * blockIdx.x + 10] = 0;
         a.dtrace[16 * blockIdx.x + 11] = 0;
+        a.dtrace[16 * blockIdx.x + 13] = 0;
     }
     if (threadIdx.x == 0) tl_mark(a.tl, 2, true);
     if (threadIdx.x == 0) {
@@ -1562,15 +1601,19 @@ __global__ void __maxnreg__(144)
         bool pend = false, feeding = true, poll_wait = false;
         // first batch: tickets b and b + grid (the static part spreads over all
         // CTAs); later batches of TB consecutive tickets from the counter
-        uint32_t ticket = blockIdx.x, ticket_end = 0xFFFFFFFFu, tk = 0, tk_first = blockIdx.x + gridDim.x;
-        if (lane == 0) tk = atomicAdd(&a.ctr->tickets, TB) + 2 * gridDim.x;
+        // first ticket: the CTA index; then the counter (a CTA that starts late,
+        // e.g. on an SM the routing kernel held, holds no other reserved work)
+        uint32_t ticket = blockIdx.x, ticket_end = blockIdx.x + 1, tk = 0;
+        if (lane == 0) tk = atomicAdd(&a.ctr->tickets, TB) + gridDim.x;
+        if (a.dtrace && lane == 0) a.dtrace[16 * blockIdx.x + 12] = gtime();
         uint32_t head = 0, tail = 0, cnt = 0, rph = 0;  // record ring (rph: phase bit per slot)
         uint32_t stage = 0, phase = 0;
         bool run_first = true;
         uint32_t run_tiles = 0;
         unsigned long long p_wait = 0;
         const unsigned long long p_t0 = clock64();
-        unsigned long long p_feed = 0, p_rec = 0, p_tma = 0;
+        unsigned long long p_feed = 0, p_rec = 0, p_tma = 0, p_sleep = 0, p_dec = 0;
+        uint32_t p_tiles = 0;
         for (;;) {
             // ---- feed records
             const unsigned long long tf = clock64();
@@ -1582,13 +1625,10 @@ __global__ void __maxnreg__(144)
                 // its tile ring, so the CTAs drain together
                 if (!pend && in_tail && cnt > 0) break;
                 if (!pend) {
-                    if (ticket_end == 0xFFFFFFFFu && ticket != blockIdx.x) {  // second ticket of the first batch
-                        ticket = tk_first;
-                        ticket_end = tk_first + 1;
-                    } else if (ticket == ticket_end) {  // next batch (reserved one batch ahead)
+                    if (ticket == ticket_end) {  // next batch (reserved one batch ahead)
                         ticket = __shfl_sync(0xFFFFFFFFu, tk, 0);
                         ticket_end = ticket + TB;
-                        if (lane == 0) tk = atomicAdd(&a.ctr->tickets, TB) + 2 * gridDim.x;
+                        if (lane == 0) tk = atomicAdd(&a.ctr->tickets, TB) + gridDim.x;
                     }
                     uint32_t b0 = 0, b1 = 0;
                     const int r = try_chunk(ticket, b0, b1);
@@ -1610,6 +1650,7 @@ __global__ void __maxnreg__(144)
                     ++ticket;
                 }
                 if (lane == 0) {
+                    if (a.dtrace && a.dtrace[16 * blockIdx.x + 13] == 0) a.dtrace[16 * blockIdx.x + 13] = gtime();
                     const TileRec* src = pc0 < W ? a.st_tiles + pc0 : a.dyn_tiles + (pc0 - W);
                     s.rec_w[tail] = pc0;
                     s.rec_last[tail] = pc0 + 1 == pc1 ? 1u : 0u;
@@ -1624,13 +1665,16 @@ __global__ void __maxnreg__(144)
             p_feed += clock64() - tf;
             if (cnt == 0) {
                 if (!feeding) break;
+                const unsigned long long ts = clock64();
                 __nanosleep(a.poll_ns);  // waiting for the planner
+                p_sleep += clock64() - ts;
                 continue;
             }
             // ---- issue the head tile
             const unsigned long long tr = clock64();
             mbar_wait(&s.rec_bar[head], (rph >> head) & 1u);
             p_rec += clock64() - tr;
+            const unsigned long long td = clock64();
             if (a.dtrace && lane == 0 && a.dtrace[16 * blockIdx.x + 10] == 0) a.dtrace[16 * blockIdx.x + 10] = gtime();
             rph ^= 1u << head;
             __syncwarp();
@@ -1667,6 +1711,7 @@ __global__ void __maxnreg__(144)
             }
             const uint32_t g = qslot / a.n_hchunks, hc = qslot % a.n_hchunks;
             const uint32_t nq = min((uint32_t)kHeadsPerSlot, a.G - hc * kHeadsPerSlot);
+            p_dec += clock64() - td;
             if (lane == 0) {
                 const unsigned long long tw = clock64();
                 mbar_wait(&s.empty[stage], phase ^ 1);
@@ -1709,6 +1754,9 @@ __global__ void __maxnreg__(144)
             __syncwarp();
             p_tma += clock64() - tt;
             if (a.dtrace && lane == 0 && a.dtrace[16 * blockIdx.x + 11] == 0) a.dtrace[16 * blockIdx.x + 11] = gtime();
+            if (a.dtiles && lane == 0 && p_tiles < (uint32_t)kTraceTiles)
+                a.dtiles[((size_t)blockIdx.x * kTraceTiles + p_tiles) * 3] = gtime();
+            ++p_tiles;
             // a dynamic record is re-armed for the next step once consumed
             if (w >= W && lane == 0) a.dyn_tiles[w - W].ready = 0;
             if (++stage == CF::NS) {
@@ -1727,6 +1775,8 @@ __global__ void __maxnreg__(144)
                 a.dtrace[16 * blockIdx.x + 7] = p_feed;
                 a.dtrace[16 * blockIdx.x + 8] = p_rec;
                 a.dtrace[16 * blockIdx.x + 9] = p_tma;
+                a.dtrace[16 * blockIdx.x + 14] = p_sleep;
+                a.dtrace[16 * blockIdx.x + 15] = p_dec;
             }
             mbar_wait(&s.empty[stage], phase ^ 1);
             s.meta[stage] = make_int4(-1, 0, 0, 0);
@@ -1767,6 +1817,8 @@ __global__ void __maxnreg__(144)
             mbar_wait(&s.full[stage], phase);
         }
         const int4 mt = s.meta[stage];
+        if (a.dtiles && threadIdx.x == 0 && n_tiles_done < (uint32_t)kTraceTiles)
+            a.dtiles[((size_t)blockIdx.x * kTraceTiles + n_tiles_done) * 3 + 1] = gtime();
         if (a.dtrace && threadIdx.x == 0) {
             if (n_tiles_done == 0) a.dtrace[16 * blockIdx.x + 1] = gtime();
             if (mt.x < 0) {
@@ -1908,6 +1960,8 @@ __global__ void __maxnreg__(144)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&s.empty[stage]);
+        if (a.dtiles && threadIdx.x == 0 && n_tiles_done - 1 < (uint32_t)kTraceTiles)
+            a.dtiles[((size_t)blockIdx.x * kTraceTiles + n_tiles_done - 1) * 3 + 2] = gtime();
 
         if (flags & 2u) {
             // ---- run done: deposit this warp's (m, l, O) state for the merge warp
@@ -2151,8 +2205,10 @@ void launch_route_cluster(int D, const ClusterRouteArgs& a, uint32_t n_slots, cu
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    // dynamic smem: centroid slice [D][C/8] + member queries [8][G][D] (f32)
-    cfg.dynamicSmemBytes = ((size_t)D * (a.C / kClusterCtas) + (size_t)kSlotGroups * a.G * D) * 4;
+    // dynamic smem: centroid slice [D][C/8] + member queries [8][G][D] +
+    // candidate rows [64][D + 1] (f32)
+    cfg.dynamicSmemBytes = ((size_t)D * (a.C / kClusterCtas) + (size_t)kSlotGroups * a.G * D +
+                            (size_t)64 * (D + 1)) * 4;
     if (cfg.dynamicSmemBytes > 160 * 1024) fail(SAAP_ERR_UNSUPPORTED, "route: slice too large");
     static bool configured = false;
     if (!configured) {
@@ -2174,7 +2230,7 @@ void launch_route_cluster(int D, const ClusterRouteArgs& a, uint32_t n_slots, cu
 }
 
 void launch_route_plan(const PlanArgs& a, uint32_t n_groups, bool pdl, cudaStream_t st) {
-    const bool route = a.mode == 1 || a.mode == 2;
+    const bool route = a.mode == 1 || a.mode == 2 || a.mode == 4;
     size_t smem = 0;
     if (route) smem = (size_t)std::max<uint32_t>(a.P2, kPlanThreads) * 12 + ((a.C + 31) / 32) * 4 + 16;
     smem += (size_t)(a.probes + 8) * (sizeof(Seg) + 4);

@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--drift", type=float, default=0.0)
     ap.add_argument("--dense", action="store_true")
+    ap.add_argument("--given", action="store_true",
+                    help="replay the routed lists through the caller-selected path (no routing)")
     args = ap.parse_args()
     import torch
     import paper_2502_08246_b200 as sb
@@ -61,9 +63,18 @@ def main():
     out = torch.empty(64, 4, 128, device=dev)
     stats = torch.zeros(64, 3, dtype=torch.int64, device=dev)
 
+    if args.given:
+        for lay in lays:
+            lay.sel = torch.empty(64, a.probes, dtype=torch.int32, device=dev)
+            lay.L.sparse_attention_dev(lay.routers, lay.qr_t, lay.qd_t, 4, cfg, out, stats,
+                                       selected=lay.sel)
+        ctx.synchronize()
+
     def step(lay):
         if args.dense:
             lay.kv.dense_attention_dev(lay.qr_t, 4, out)
+        elif args.given:
+            lay.L.sparse_attention_selected_dev(lay.qr_t, 4, lay.sel, a.probes, cfg, out, stats)
         else:
             lay.L.sparse_attention_dev(lay.routers, lay.qr_t, lay.qd_t, 4, cfg, out, stats)
 
@@ -86,6 +97,7 @@ def main():
     dbuf = (ct.c_uint64 * (16 * nc))()
     pbuf = (ct.c_uint64 * (16 + 6 * 1024))()
     dec_all = []
+    tiles_all = []
     for r in range(args.reps):
         sb._check(lib.saap_debug_step_trace(ctx.h, buf, 1))
         graphs[r % 2].launch()
@@ -102,14 +114,24 @@ def main():
             st["decode_cta"] = {"start_us": rel(t[:, 0]), "first_tile_us": rel(t[:, 1]),
                                 "end_us": rel(t[:, 2]),
                                 "first_record_us": rel(t[:, 10]), "first_tma_us": rel(t[:, 11]),
+                                "producer_loop_us": rel(t[:, 12]), "first_rec_issue_us": rel(t[:, 13]),
                                 "tiles": [int(x) for x in np.percentile(t[:, 3], [0, 50, 100])],
                                 "cons_wait_frac": round(float(np.median(t[:, 6] / np.maximum(t[:, 5], 1))), 3),
                                 "prod_empty_wait_frac": round(float(np.median(t[:, 4] / np.maximum(t[:, 5], 1))), 3),
                                 "prod_rec_wait_frac": round(float(np.median(t[:, 8] / np.maximum(t[:, 5], 1))), 3),
                                 "prod_feed_frac": round(float(np.median(t[:, 7] / np.maximum(t[:, 5], 1))), 3),
-                                "prod_tma_frac": round(float(np.median(t[:, 9] / np.maximum(t[:, 5], 1))), 3)}
+                                "prod_tma_frac": round(float(np.median(t[:, 9] / np.maximum(t[:, 5], 1))), 3),
+                                "prod_sleep_frac": round(float(np.median(t[:, 14] / np.maximum(t[:, 5], 1))), 3),
+                                "prod_decode_frac": round(float(np.median(t[:, 15] / np.maximum(t[:, 5], 1))), 3)}
             dec_all.append(((t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3, (t[:, 2] - t0) / 1e3, t[:, 3]))
+            tb = (ct.c_uint64 * (nc * 48 * 3))()
+            if lib.saap_debug_decode_tiles(ctx.h, tb, ct.c_uint64(nc)) == 0:
+                tt = np.array(list(tb), dtype=np.float64).reshape(nc, 48, 3)
+                tt = np.where(tt >= t0, (tt - t0) / 1e3, np.nan)
+                tiles_all.append(tt)
         if not args.dense and lib.saap_debug_plan_trace(ctx.h, pbuf) == 0:
+            # slot 0 / CTA 0 phase clocks (clock64 deltas -> us at the measured SM clock)
+            st["route_phases_us"] = {str(k): round(float(pbuf[k]) / 1965.0, 2) for k in range(16) if pbuf[k]}
             cta = np.array(list(pbuf)[16:], dtype=np.float64).reshape(1024, 6)
             cta = cta[cta[:, 0] > 0]
             if len(cta):
@@ -118,6 +140,7 @@ def main():
                 own = cta[cta[:, 3] > 0]
                 slow = own[np.argsort(own[:, 3])[-4:]]
                 st["route_slowest"] = [[round(float((r[i] - t0) / 1e3), 2) for i in range(4)] + [int(r[4])]
+                                       + [round(float((r[5] - t0) / 1e3), 2) if r[5] > t0 else None]
                                        for r in slow]
                 st["route_candidates"] = [int(x) for x in np.percentile(own[:, 4], [0, 50, 90, 100])]
         res["steps"].append(st)
@@ -138,10 +161,21 @@ def main():
     res["median"]["decode_cta_first_tile_us"] = med(["decode_cta", "first_tile_us"])
     res["median"]["decode_cta_start_us"] = med(["decode_cta", "start_us"])
     res["median"]["route_cta_end_us"] = med(["route_cta", "end_us"])
-    for k in ("cons_wait_frac", "prod_empty_wait_frac", "prod_rec_wait_frac", "prod_feed_frac", "prod_tma_frac"):
+    res["median"]["decode_producer_loop_us"] = med(["decode_cta", "producer_loop_us"])
+    res["median"]["decode_first_rec_issue_us"] = med(["decode_cta", "first_rec_issue_us"])
+    res["median"]["decode_first_record_us"] = med(["decode_cta", "first_record_us"])
+    res["median"]["decode_first_tma_us"] = med(["decode_cta", "first_tma_us"])
+    ph = [st.get("route_phases_us") for st in res["steps"] if st.get("route_phases_us")]
+    if ph:
+        res["median"]["route_phases_us"] = {k: round(float(np.median([p[k] for p in ph if k in p])), 2)
+                                            for k in ph[0]}
+    for k in ("cons_wait_frac", "prod_empty_wait_frac", "prod_rec_wait_frac", "prod_feed_frac", "prod_tma_frac",
+              "prod_sleep_frac", "prod_decode_frac"):
         res["median"][k] = med(["decode_cta", k])
     if dec_all:
         np.save(os.path.splitext(args.out)[0] + "_cta.npy", np.array(dec_all))
+    if tiles_all:
+        np.save(os.path.splitext(args.out)[0] + "_tiles.npy", np.array(tiles_all))
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump(res, open(args.out, "w"), indent=1)
     print(json.dumps(res["median"]))

@@ -1,0 +1,49 @@
+"""The reference's own unit tests (attention_test / partition_test /
+qmodel_test) and release acceptance gate, compiled unmodified from the
+reference sources against the drop-in library (libsaap_dropin.so ahead of the
+reference core, tests/ref_suite/Makefile), run on the B200.  Tolerance
+substitutions are recorded in tests/ref_suite/substitutions.cpp and logged per
+use; the logs land in gpurun_out/ when run there."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "tests", "ref_suite", "bin")
+
+
+def _run(name, args=(), timeout=1800):
+    exe = os.path.join(BIN, name)
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (needs the reference sources: make -C tests/ref_suite)")
+    r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=timeout)
+    out_dir = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(out_dir):
+        with open(os.path.join(out_dir, f"ref_suite_{name}.log"), "w") as f:
+            f.write(r.stdout + "\n" + r.stderr)
+    return r
+
+
+@pytest.mark.gpu
+def test_reference_unit_tests_on_dropin():
+    r = _run("saap_unit")
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-6000:]
+    assert " 0 failed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_on_dropin():
+    r = _run("saap_acceptance", timeout=3000)
+    assert r.returncode == 0, r.stdout[-6000:] + r.stderr[-3000:]
+
+
+def test_ref_suite_links_dropin_first():
+    """The binaries bind hot-path symbols to the drop-in: it precedes the
+    reference core in the dynamic section (no GPU needed to check)."""
+    exe = os.path.join(BIN, "saap_unit")
+    if not os.path.exists(exe):
+        pytest.skip("not built")
+    dyn = subprocess.run(["readelf", "-d", exe], capture_output=True, text=True).stdout
+    needed = [l.split("[")[1].rstrip("]") for l in dyn.splitlines() if "(NEEDED)" in l]
+    assert needed.index("libsaap_dropin.so") < needed.index("libsaap_ref.so")
