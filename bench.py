@@ -356,8 +356,10 @@ def ours(a):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2502_08246_b200.shard import HeadShard, gather_outputs
+        # host plumbing only (NCCL id hand-off, barriers, max over ranks); the
+        # data path is the library's NCCL communicator (saap_comm)
+        dist.init_process_group("gloo")
+    from paper_2502_08246_b200.shard import Comm, HeadShard, unique_id
     sh = HeadShard(rank, world, a.kv_heads, a.batch)
     heads_local, h0 = sh.heads_local, sh.head0
     G = a.q_heads // a.kv_heads
@@ -368,6 +370,11 @@ def ours(a):
     stream = torch.cuda.Stream()
     ctx = sb.Context(local)
     ctx.set_stream(stream.cuda_stream)
+    comm = None
+    if world > 1:
+        box = [unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        comm = Comm(ctx, world, rank, box[0])
     dev = torch.device("cuda", local)
     cfg = sb.SparseAttnConfig(a.probes, 128, sb.DenseWindow(a.sink, a.recent))
 
@@ -425,16 +432,21 @@ def ours(a):
     out_dense = torch.empty_like(out)
     stats = torch.zeros(n_groups, 3, dtype=torch.int64, device=dev)
 
-    def sparse_step(lay):
-        lay.L.sparse_attention_dev(lay.routers, lay.qr_t, lay.qd_t, G, cfg, out, stats)
+    # the timed step's output: at N>1 the communicator's registered send
+    # buffer, so the all-gather starts without a copy
+    out_full = torch.empty(a.batch, a.kv_heads * G, d, device=dev) if world > 1 else None
+    step_out = comm.send_buffer(out.numel() * 4) if comm is not None else out
+
+    def sparse_step(lay, target=None):
+        lay.L.sparse_attention_dev(lay.routers, lay.qr_t, lay.qd_t, G, cfg,
+                                   step_out if target is None else target, stats)
 
     def dense_step(lay):
         lay.kv.dense_attention_dev(lay.qr_t, G, out_dense)
 
     def gather():
-        if world > 1:
-            with torch.cuda.stream(stream):
-                gather_outputs(out, sh, dist)
+        if comm is not None:
+            comm.allgather_heads(step_out, sh, G, d, out_full)
 
     # eager warm-up sizes the scratch, then capture one graph per layer
     for lay in layers + imb:
@@ -477,8 +489,8 @@ def ours(a):
         if world > 1:
             dist.barrier()
         ms = s.elapsed_time(e) / steps
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
+        if world > 1:  # max over ranks (host scalars over the gloo plumbing)
+            t = torch.tensor([ms], dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
@@ -514,7 +526,7 @@ def ours(a):
     def counters(lays):
         ks, ms = [], []
         for lay in lays:
-            sparse_step(lay)
+            sparse_step(lay, out)
             dense_step(lay)
             torch.cuda.synchronize()
             ks.append(int(stats[:, 0].sum().item()))
@@ -601,8 +613,9 @@ def ours(a):
                 "h2d_bytes_per_step": int(2 * n_groups * G * d * 4),
                 "d2h_bytes_per_step": int(n_groups * G * d * 4 + n_groups * ct.sizeof(sb.AttnStats))},
         "clocks": clk,
-        "gpu_launches": int(kernels_per_step * a.steps),
-        "kernels_per_step": int(kernels_per_step),
+        "gpu_launches": int((kernels_per_step + (1 if world > 1 else 0)) * a.steps),
+        "kernels_per_step": int(kernels_per_step) + (1 if world > 1 else 0),
+        "comm": comm.info() if comm is not None else None,
         "setup_s": round(t_setup, 1),
         "prefill_build_ms_per_layer": round(float(np.mean([l.t_build_ms for l in layers])), 2),
         "prefill": {
@@ -618,6 +631,9 @@ def ours(a):
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        torch.cuda.synchronize()
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -722,8 +738,31 @@ def parity_leg(sb, torch, ctx, a, lay, groups, sparse_step, dense_step, out, out
     return parity, cpu
 
 
+def spawn_ranks(a):
+    """`bench.py --gpus N` outside torchrun: start N ranks (one process per
+    GPU, the torchrun environment contract) and wait; rank 0 prints."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    procs = []
+    for r in range(a.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(a.gpus),
+                   LOCAL_WORLD_SIZE=str(a.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                                      env=env))
+    rc = 0
+    for p in procs:
+        rc = max(rc, p.wait())
+    sys.exit(rc)
+
+
 def main():
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(a)
+    if int(os.environ.get("WORLD_SIZE", "1")) != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE', '1')}")
     if a.impl == "reference":
         reference_arm(a)
     else:

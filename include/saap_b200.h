@@ -268,6 +268,10 @@ SAAP_API int saap_layer_build_assigned(saap_ctx* ctx, saap_layer* L,
  * 249-255); graphs captured on this layer must be re-captured. */
 SAAP_API int saap_layer_append(saap_ctx* ctx, saap_layer* L, const void* keys_roped_bf16,
                                const void* values_bf16, const void* keys_assign_bf16, uint64_t k);
+/* Same from host f32 rows [n_groups x k x dim] each (rounded to the bf16
+ * cache on the device; synchronous). */
+SAAP_API int saap_layer_append_host(saap_ctx* ctx, saap_layer* L, const float* keys_roped,
+                                    const float* values, const float* keys_assign, uint64_t k);
 
 /* Assignment engine: 0 (default) = tcgen05 bf16 two-term-split GEMM with an
  * fp64 re-check of near-tie keys (device bf16 keys, d = 128); 1 = fp64
@@ -357,6 +361,39 @@ SAAP_API int saap_dense_attention_dev(saap_ctx* ctx, const saap_kvcache* c, cons
 /* full_attention(q, keys, values) on host f32 arrays. attention.cpp:163-195 */
 SAAP_API int saap_full_attention(saap_ctx* ctx, const float* q, uint64_t G, const float* keys,
                         const float* values, uint64_t n, uint64_t dim, float* out);
+
+/* ---- multi-GPU: KV heads sharded over ranks ----------
+ * One process per GPU; rank r owns KV heads [r*H/N, (r+1)*H/N) of every
+ * sequence (GQA: its query heads read no other rank's cache), so the only
+ * exchange of a layer step is gathering the attention outputs.  NCCL is
+ * loaded at run time (libnccl.so.2).  The reference has no multi-GPU path
+ * (single-threaded CPU); this replaces running one KV cache per GPU by hand
+ * (PAPER.md:539). */
+typedef struct saap_comm saap_comm;
+/* ncclGetUniqueId: 128 opaque bytes rank 0 hands to every rank. */
+SAAP_API int saap_comm_unique_id(uint8_t* id128);
+/* ncclCommInitRank on the context's device (collective). */
+SAAP_API int saap_comm_init(saap_ctx* ctx, int nranks, int rank, const uint8_t* id128,
+                            saap_comm** out);
+SAAP_API int saap_comm_destroy(saap_comm* comm);
+/* symmetric = 1 when the gather buffers are NCCL symmetric windows
+ * (ncclMemAlloc + ncclCommWindowRegister, NCCL >= 2.27). */
+SAAP_API int saap_comm_info(const saap_comm* comm, int* nranks, int* rank, int* symmetric,
+                            int* nccl_version);
+/* The communicator's (registered) send buffer of >= bytes: point the decode
+ * step's outputs here and the gather starts without a copy (collective when
+ * it grows). */
+SAAP_API int saap_comm_send_buffer(saap_comm* comm, uint64_t bytes, void** out_dev);
+/* Heads owned by `rank`: head0, heads_local (invalid if H % N != 0). */
+SAAP_API int saap_shard_heads(uint64_t kv_heads, int nranks, int rank, uint64_t* head0,
+                              uint64_t* heads_local);
+/* All-gather of the per-rank outputs [batch][heads_local][G][d] f32 (device)
+ * into [batch][nranks * heads_local][G][d] on every rank (ncclAllGather +
+ * one permute kernel, on the context's stream; collective, graph-capturable
+ * once the buffers exist). */
+SAAP_API int saap_allgather_heads(saap_ctx* ctx, saap_comm* comm, const float* out_local_dev,
+                                  uint64_t batch, uint64_t heads_local, uint64_t G, uint64_t dim,
+                                  float* out_full_dev);
 
 /* ---- CUDA graphs over the asynchronous calls --------------------------- */
 SAAP_API int saap_graph_begin(saap_ctx* ctx);

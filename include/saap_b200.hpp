@@ -1,16 +1,14 @@
 // saap_b200.hpp — header-only C++ host API over the C ABI, mirroring the
 // reference's hot-path interface (/root/reference/proj/core/include/saap/
 // {partition,attention,qmodel}.hpp): same function names, argument meaning
-// and error behaviour (std::invalid_argument with the reference's message).
+// and error behaviour (std::invalid_argument with the reference's message),
+// in namespace saap_b200.  Functions are templates over any type with the
+// reference's field names, so the reference's own structs can be passed.
 //
-// The reference's own structs can be passed directly: every function is a
-// template over any type with the reference's field names (TensorBlock
-// {rows, dim, data}, Partition{centroids}, KeyAssignment{bucket_of},
-// SparseAttnConfig{probes, block_size, dense{sink_count, recent_count}}), so
-// a maintainer swaps `saap::sparse_attention(...)` for
-// `saap_b200::sparse_attention(...)` without touching call sites
-// (INTEGRATION.md).  Light-weight stand-in types are provided for callers
-// without the reference headers.
+// This header is for code written against the B200 library.  To run an
+// existing program that calls saap:: unchanged, link libsaap_dropin.so
+// (paper_2502_08246_b200/dropin/) ahead of the reference core instead: it
+// defines the reference's own symbols.
 #pragma once
 
 #include <algorithm>
@@ -390,6 +388,110 @@ AttnResult sparse_attention(const TB& q_roped, const TB& q_deroped, const Contex
 inline double selectivity(const AttnResult& r, std::size_t n_keys) {
     if (n_keys == 0) throw std::invalid_argument("selectivity: empty context");
     return static_cast<double>(r.keys_scored) / static_cast<double>(n_keys);
+}
+
+// QModelRouter(model) (attention.hpp:127-140): Q-model parameters in the
+// reference's fp64 layout (any type with QModel's Mat members).
+class QModelRouter : public BucketRouter {
+public:
+    template <typename QM>
+    explicit QModelRouter(const QM& m, Context& ctx = Context::current()) {
+        ctx_ = &ctx;
+        check(saap_qmodel_create(ctx.get(), m.w1.rows, m.w1.cols, m.w2.cols, m.w1.data.data(),
+                                 m.b1.data.data(), m.bn_gamma.data.data(), m.bn_beta.data.data(),
+                                 m.bn_run_mean.data.data(), m.bn_run_var.data.data(),
+                                 m.w2.data.data(), m.b2.data.data(), &qm_));
+        check(saap_router_create_qmodel(ctx.get(), qm_, &h_));
+    }
+    ~QModelRouter() override {
+        saap_router_destroy(h_);
+        h_ = nullptr;
+        saap_qmodel_destroy(qm_);
+    }
+    saap_qmodel* model() const { return qm_; }
+
+private:
+    saap_qmodel* qm_ = nullptr;
+};
+
+// batched_bucket_select(model, q_group, l)   qmodel.cpp:485-511
+template <typename TB>
+std::vector<std::uint32_t> batched_bucket_select(const QModelRouter& r, const TB& q, std::size_t l) {
+    std::vector<std::uint32_t> out(l);
+    check(saap_batched_bucket_select(Context::current().get(), r.model(), q.data.data(), q.rows,
+                                     q.dim, l, out.data()));
+    return out;
+}
+
+// merge_partials(parts)   attention.cpp:130-139 (bit-exact fp64 on the device)
+inline PartialAccumulator merge_partials(const std::vector<const PartialAccumulator*>& parts) {
+    if (parts.empty()) throw std::invalid_argument("merge_partials: empty list");
+    PartialAccumulator out(parts[0]->heads(), parts[0]->value_dim(), parts[0]->ctx());
+    std::vector<const saap_accum*> hs;
+    for (auto* p : parts) hs.push_back(p->get());
+    check(saap_merge_partials(out.ctx().get(), hs.data(), hs.size(), out.get()));
+    return out;
+}
+
+// mse(approx, exact)   attention.cpp:385-399 (bit-identical sequential fp64 sum)
+template <typename TB>
+double mse(const TB& approx, const TB& exact) {
+    double out = 0.0;
+    check(saap_mse(approx.data.data(), approx.rows, approx.dim, exact.data.data(), exact.rows,
+                   exact.dim, &out));
+    return out;
+}
+
+// attention_mass_coverage(q_roped, store, selected, dense)  attention.cpp:427-462
+template <typename TB, typename Sel, typename DW>
+double attention_mass_coverage(const TB& q_roped, const ContextStore& store, const Sel& selected,
+                               const DW& dense) {
+    const std::vector<std::uint32_t> sel(selected.begin(), selected.end());
+    double out = 0.0;
+    check(saap_attention_mass_coverage(store.ctx().get(), store.get(), q_roped.data.data(),
+                                       q_roped.rows, sel.data(), sel.size(), dense.sink_count,
+                                       dense.recent_count, &out));
+    return out;
+}
+
+// build_context_store(keys_roped, values, rope, partition, sink)  attention.cpp:249-255,
+// RopeConfig-shaped `rope` ({dim, base_theta}); the de-rope runs on the device
+template <typename TB, typename Rope, typename P>
+std::unique_ptr<ContextStore> build_context_store(const TB& keys_roped, const TB& values,
+                                                  const Rope& rope, const P& partition,
+                                                  std::size_t sink_count) {
+    if (keys_roped.rows <= sink_count)
+        throw std::invalid_argument("build_context_store: no keys left to index after " +
+                                    std::to_string(sink_count) + " sink keys");
+    if (rope.dim == 0 || rope.dim % 2 != 0)
+        throw std::invalid_argument("RopeConfig: dim must be even and positive, got " +
+                                    std::to_string(rope.dim));
+    if (keys_roped.dim != rope.dim)
+        throw std::invalid_argument("rope: block dim " + std::to_string(keys_roped.dim) +
+                                    " does not match configured dim " + std::to_string(rope.dim));
+    return std::make_unique<ContextStore>(keys_roped, values, rope.base_theta, partition,
+                                          sink_count);
+}
+
+// build_context_store(keys_roped, values, rope, C, kmeans_iters, sink, rng, stats)
+// attention.cpp:238-246: device de-rope, device k-means (the caller's Rng
+// draws the seeds), then the store under the trained partition.
+template <typename TB, typename Rope, typename RngT, typename StatsT = KMeansStats>
+std::unique_ptr<ContextStore> build_context_store(const TB& keys_roped, const TB& values,
+                                                  const Rope& rope, std::size_t n_buckets,
+                                                  std::size_t kmeans_iters, std::size_t sink_count,
+                                                  RngT& rng, StatsT* stats = nullptr) {
+    if (keys_roped.rows <= sink_count)
+        throw std::invalid_argument("build_context_store: no keys left to index after " +
+                                    std::to_string(sink_count) + " sink keys");
+    const std::size_t n = keys_roped.rows - sink_count, d = keys_roped.dim;
+    TensorBlock de(n, d);
+    std::vector<std::uint64_t> pos(n);
+    for (std::size_t i = 0; i < n; ++i) pos[i] = sink_count + i;
+    check(saap_rope_remove(Context::current().get(), keys_roped.data.data() + sink_count * d, n, d,
+                           pos.data(), rope.base_theta, de.data.data()));
+    Partition p = kmeans_train(de, n_buckets, kmeans_iters, rng, stats);
+    return build_context_store(keys_roped, values, rope, p, sink_count);
 }
 
 }  // namespace saap_b200

@@ -921,14 +921,12 @@ class Layer:
         return self
 
     def append(self, keys_roped, values, keys_assign):
-        """Host f32 rows [n_groups, k, d] (rounded to bf16 RNE on upload)."""
-        import torch
-        dev = torch.device("cuda", self.ctx.device)
-        kr = torch.from_numpy(_f32(keys_roped)).to(dev).to(torch.bfloat16).contiguous()
-        v = torch.from_numpy(_f32(values)).to(dev).to(torch.bfloat16).contiguous()
-        ka = torch.from_numpy(_f32(keys_assign)).to(dev).to(torch.bfloat16).contiguous()
-        torch.cuda.synchronize(dev)
-        return self.append_dev(kr, v, ka, kr.shape[1])
+        """Host f32 rows [n_groups, k, d] (rounded to bf16 RNE on the device)."""
+        kr, v, ka = _f32(keys_roped), _f32(values), _f32(keys_assign)
+        k = kr.shape[1]
+        _check(lib().saap_layer_append_host(self.ctx.h, self.h, _p(kr), _p(v), _p(ka), _u64(k)))
+        self.n_keys = self.n_keys + np.uint64(k)
+        return self
 
     def build_dev(self, partitions, keys_roped_bf16, values_bf16, keys_assign_bf16):
         arr = self._parts(partitions)

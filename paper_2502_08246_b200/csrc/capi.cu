@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "api.cuh"
 #include "args.cuh"
 
 namespace saap_b200 {
@@ -109,37 +110,6 @@ using namespace saap_b200;
 
 namespace {
 
-thread_local std::string g_err;
-
-struct Failure {
-    int code;
-    std::string msg;
-};
-
-template <typename F>
-int guard(F&& f) {
-    try {
-        f();
-        return SAAP_OK;
-    } catch (const Failure& e) {
-        g_err = e.msg;
-        return e.code;
-    } catch (const std::bad_alloc&) {
-        g_err = "host allocation failed";
-        return SAAP_ERR_CUDA;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return SAAP_ERR_CUDA;
-    }
-}
-
-[[noreturn]] void invalid(const std::string& m) { throw Failure{SAAP_ERR_INVALID_ARGUMENT, m}; }
-[[noreturn]] void unsupported(const std::string& m) { throw Failure{SAAP_ERR_UNSUPPORTED, m}; }
-
-void need(const void* p, const char* what) {
-    if (!p) invalid(std::string(what) + ": null argument");
-}
-
 template <typename T>
 T* dmalloc(size_t count) {
     void* p = nullptr;
@@ -181,12 +151,6 @@ void* ensure_zero(saap_ctx* c, saap_scratch& s, size_t bytes) {
     return p;
 }
 
-struct DeviceGuard {
-    explicit DeviceGuard(const saap_ctx* c) {
-        if (!c) invalid("null context");
-        SAAP_CUDA(cudaSetDevice(c->device));
-    }
-};
 
 // live contexts, so destroying a layer / router retires every cached host graph
 // that references it
@@ -724,6 +688,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     da.poll_ns = c->opt.decode_poll_ns;
     da.tl = c->tl;
     da.wait_plan = plan && c->opt.decode_wait ? 1u : 0u;
+    da.debug_skip = c->opt.debug_skip;
     // static tickets: enough to give every CTA a share of the window
     da.chunk_st = plan ? std::max<uint32_t>(1u, std::min<uint32_t>(chunk, sp->n_tiles / (uint32_t)grid)) : chunk;
     if (c->opt.trace_decode) {
@@ -965,6 +930,7 @@ int saap_ctx_set_option(saap_ctx* c, const char* name, int64_t value) {
         else if (n == "combine_poll_ns") o.combine_poll_ns = clamp(0, 100000);
         else if (n == "decode_wait") o.decode_wait = clamp(0, 1);
         else if (n == "cluster_route") o.cluster_route = clamp(0, 1);
+        else if (n == "debug_skip") o.debug_skip = clamp(0, 1);
         else if (n == "host_graph") o.host_graph = clamp(0, 1);
         else if (n == "trace_decode") o.trace_decode = clamp(0, 1);
         else if (n == "trace_plan") o.trace_plan = clamp(0, 1);
@@ -2025,6 +1991,43 @@ int saap_layer_append(saap_ctx* c, saap_layer* L, const void* keys_roped_bf16,
         L->appended = true;
         for (saap_ctx* cc : live_contexts()) purge_host_graphs(cc, L, nullptr);
     });
+}
+
+// Host f32 rows [n_groups x k x dim] each, rounded to the bf16 cache (RNE)
+// on the device, then appended like saap_layer_append.
+int saap_layer_append_host(saap_ctx* c, saap_layer* L, const float* keys_roped,
+                           const float* values, const float* keys_assign, uint64_t k) {
+    int rc = SAAP_OK;
+    const int g = guard([&] {
+        DeviceGuard dg(c);
+        need(L, "layer");
+        need(keys_roped, "append: keys");
+        need(values, "append: values");
+        need(keys_assign, "append: assignment keys");
+        if (k == 0) return;
+        const uint64_t elems = L->n_groups * k * L->d;
+        float* f32 = dmalloc<float>(elems);
+        uint16_t* b = dmalloc<uint16_t>(3 * elems);
+        const cudaStream_t st = c->stream;
+        try {
+            const float* src[3] = {keys_roped, values, keys_assign};
+            for (int i = 0; i < 3; ++i) {
+                h2d(f32, src[i], elems * 4, st);
+                launch_f32_to_bf16(f32, b + i * elems, elems, st);
+                c->launches++;
+            }
+            sync(c);
+            rc = saap_layer_append(c, L, b, b + elems, b + 2 * elems, k);
+            sync(c);
+        } catch (...) {
+            cudaFree(f32);
+            cudaFree(b);
+            throw;
+        }
+        cudaFree(f32);
+        cudaFree(b);
+    });
+    return g != SAAP_OK ? g : rc;
 }
 
 int saap_layer_destroy(saap_layer* L) {

@@ -121,6 +121,18 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
             : "memory");
     return ok != 0;
 }
+// non-blocking test of a phase's completion
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
     }
@@ -223,6 +235,7 @@ struct saap_ctx {
         uint32_t decode_poll_ns = 100;  // producer back-off while waiting for the planner
         uint32_t combine_poll_ns = 1000;  // combine back-off while no run is published
         uint32_t decode_wait = 0;       // 1: decode waits for routing to finish (PDL grid wait)
+        uint32_t debug_skip = 0;        // profiling only (wrong outputs): 1 skip consumer math
         uint32_t cluster_route = 1;     // 0: force the general routing path
         uint32_t host_graph = 1;        // 0: saap_sparse_attention never replays graphs
         uint32_t trace_step = 0;        // step timeline (saap_debug_step_trace)

@@ -1873,7 +1873,7 @@ __global__ void __maxnreg__(144)
             l_run = 0.f;
         }
         const uint32_t vbits = ((&s.valid[stage].x)[warp >> 1] >> ((warp & 1) * 16)) & 0xFFFFu;
-        if (vbits) {
+        if (vbits && !a.debug_skip) {
             // ---- S = [q1; q2; q3] K^T for this warp's 16 rows
             const uint32_t kbase = smem_u32(&s.K[stage][0]);
             float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};

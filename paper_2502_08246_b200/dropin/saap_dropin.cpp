@@ -158,7 +158,9 @@ struct PartKey {
     size_t C, d;
     bool operator==(const PartKey& o) const { return h == o.h && C == o.C && d == o.d; }
 };
-Lru<DevPartition, PartKey> g_parts(64);
+// (heap-allocated and never destroyed: device objects must not be released by
+// static destructors that may run after the CUDA runtime has shut down)
+Lru<DevPartition, PartKey>& g_parts = *new Lru<DevPartition, PartKey>(64);
 
 std::shared_ptr<DevPartition> device_partition(const saap::Partition& P) {
     const auto& c = P.centroids;
@@ -187,7 +189,7 @@ struct DevQModel {
 std::vector<const saap::Mat*> qm_params(const saap::QModel& q) {
     return {&q.w1, &q.b1, &q.bn_gamma, &q.bn_beta, &q.bn_run_mean, &q.bn_run_var, &q.w2, &q.b2};
 }
-Lru<DevQModel, uint64_t> g_qms(8);
+Lru<DevQModel, uint64_t>& g_qms = *new Lru<DevQModel, uint64_t>(8);
 
 std::shared_ptr<DevQModel> device_qmodel(const saap::QModel& q) {
     std::vector<double> flat;
@@ -237,7 +239,7 @@ struct StoreKey {
                dv == o.dv && ns == o.ns && C == o.C && sink == o.sink && fp == o.fp;
     }
 };
-Lru<DevStore, StoreKey> g_stores(16);
+Lru<DevStore, StoreKey>& g_stores = *new Lru<DevStore, StoreKey>(16);
 
 StoreKey store_key(const saap::ContextStore& s) {
     uint64_t fp = sample_hash(s.keys.data, 1);

@@ -1,14 +1,21 @@
 """KV-head sharding of a decode step over ranks.
 
-Each rank owns a contiguous block of KV heads for every sequence; under GQA
-its query heads need no other rank's keys, so the only exchange per layer
-step is gathering the per-head attention outputs.  ``torch.distributed`` is
-plumbing here (NCCL on GPUs, gloo in the CPU tests); the attention itself is
-libsaap_b200.
+One process per GPU.  Each rank owns a contiguous block of KV heads for every
+sequence; under GQA its query heads need no other rank's keys, so the only
+exchange per layer step is gathering the per-head attention outputs.  The
+geometry (``saap_shard_heads``) and the gather (``saap_allgather_heads``:
+NCCL all-gather into symmetric-window buffers + a permute kernel) are the
+C ABI's; this module only binds them.  Exchanging the 128-byte NCCL unique id
+is the caller's plumbing (any channel: a TCP store, MPI, a file).
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
+
+import numpy as np
+
+from . import Context, _check, _dptr, _u64, lib
 
 
 @dataclass(frozen=True)
@@ -19,16 +26,22 @@ class HeadShard:
     batch: int
 
     def __post_init__(self):
-        if self.kv_heads % self.world:
-            raise ValueError(f"{self.kv_heads} KV heads do not split over {self.world} ranks")
+        h0, hl = C.c_uint64(), C.c_uint64()
+        try:
+            _check(lib().saap_shard_heads(_u64(self.kv_heads), C.c_int(self.world),
+                                          C.c_int(self.rank), C.byref(h0), C.byref(hl)))
+        except ValueError as e:
+            raise ValueError(str(e)) from None
+        object.__setattr__(self, "_h0", h0.value)
+        object.__setattr__(self, "_hl", hl.value)
 
     @property
     def heads_local(self) -> int:
-        return self.kv_heads // self.world
+        return self._hl
 
     @property
     def head0(self) -> int:
-        return self.rank * self.heads_local
+        return self._h0
 
     @property
     def n_groups(self) -> int:
@@ -47,20 +60,62 @@ class HeadShard:
         return s, self.head0 + hl
 
 
-def gather_outputs(out_local, shard: HeadShard, dist=None):
-    """All-gather per-rank outputs [batch*heads_local, G, d] into the full
-    [batch, kv_heads*G, d] attention output (query heads in model order)."""
-    import torch
-    if dist is None:
-        import torch.distributed as dist
-    G, d = out_local.shape[1], out_local.shape[2]
-    buf = torch.empty((shard.world,) + tuple(out_local.shape), dtype=out_local.dtype,
-                      device=out_local.device)
-    if shard.world > 1:
-        dist.all_gather_into_tensor(buf.view(-1), out_local.contiguous().view(-1))
-    else:
-        buf[0].copy_(out_local)
-    # buf[r, s*hl + j] -> (seq s, kv head r*hl + j)
+def gather_layout(blocks, shard: HeadShard):
+    """Host statement of what saap_allgather_heads produces: rank blocks
+    [world][batch*heads_local][G][d] -> [batch][kv_heads*G][d] (query heads
+    in model order).  Used by the tests as the layout oracle."""
+    b = np.asarray(blocks)
+    w, _, G, d = b.shape
     hl = shard.heads_local
-    full = buf.view(shard.world, shard.batch, hl, G, d).permute(1, 0, 2, 3, 4)
+    full = b.reshape(w, shard.batch, hl, G, d).transpose(1, 0, 2, 3, 4)
     return full.reshape(shard.batch, shard.kv_heads * G, d)
+
+
+def unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0 creates it and hands it to every rank)."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib().saap_comm_unique_id(buf))
+    return bytes(buf)
+
+
+class Comm:
+    """saap_comm: the NCCL communicator of the head-sharded step."""
+
+    def __init__(self, ctx: Context, world: int, rank: int, uid: bytes):
+        if len(uid) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        self.ctx, self.world, self.rank = ctx, world, rank
+        h = C.c_void_p()
+        _check(lib().saap_comm_init(ctx.h, C.c_int(world), C.c_int(rank),
+                                    (C.c_uint8 * 128).from_buffer_copy(uid), C.byref(h)))
+        self.h = h
+
+    def info(self):
+        n, r, sym, ver = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _check(lib().saap_comm_info(self.h, C.byref(n), C.byref(r), C.byref(sym), C.byref(ver)))
+        return {"nranks": n.value, "rank": r.value, "symmetric": bool(sym.value),
+                "nccl_version": ver.value}
+
+    def send_buffer(self, nbytes: int) -> int:
+        """Device pointer of the registered send buffer (write the step's
+        outputs here: the gather then needs no copy)."""
+        p = C.c_void_p()
+        _check(lib().saap_comm_send_buffer(self.h, _u64(nbytes), C.byref(p)))
+        return p.value
+
+    def allgather_heads(self, out_local, shard: HeadShard, G: int, d: int, out_full):
+        """[batch*heads_local, G, d] on each rank -> [batch, kv_heads*G, d]."""
+        _check(lib().saap_allgather_heads(self.ctx.h, self.h, _dptr(out_local), _u64(shard.batch),
+                                          _u64(shard.heads_local), _u64(G), _u64(d),
+                                          _dptr(out_full)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().saap_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,9 @@
+#!/bin/bash
+# feeder/issuer split: traces (given, routed, dense), timing sweep, correctness
+mkdir -p gpurun_out
+timeout 300 python scripts/trace_step.py --given --reps 6 --out gpurun_out/r2n_given.json > gpurun_out/r2n_given.log 2>&1; tail -1 gpurun_out/r2n_given.log
+timeout 300 python scripts/trace_step.py --reps 6 --out gpurun_out/r2n_route.json > gpurun_out/r2n_route.log 2>&1; tail -1 gpurun_out/r2n_route.log
+timeout 300 python scripts/sweep_opts.py "" "chunk=4" "chunk=16" 2>&1 | tail -1
+timeout 300 python scripts/sweep_opts.py --dense "" 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_stream.py tests/test_gpu_parity.py tests/test_gpu_c3.py tests/test_gpu_regressions.py -q -x --timeout 400 -p no:cacheprovider 2>&1 | tail -3
+timeout 900 python -m pytest tests/test_gpu_ref_suite.py -q --timeout 900 -p no:cacheprovider 2>&1 | tail -3

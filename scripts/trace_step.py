@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--drift", type=float, default=0.0)
     ap.add_argument("--dense", action="store_true")
+    ap.add_argument("--plain", action="store_true", help="no tracing; run --reps eager steps and exit")
     ap.add_argument("--given", action="store_true",
                     help="replay the routed lists through the caller-selected path (no routing)")
     args = ap.parse_args()
@@ -43,9 +44,12 @@ def main():
     for kv in args.opt:
         k, v = kv.split("=")
         ctx.set_option(k, int(v))
-    ctx.set_option("trace_step", 1)
-    ctx.set_option("trace_decode", 1)
-    ctx.set_option("trace_plan", 1)
+    if args.plain:  # no tracing: a clean run for ncu (-k decode_kernel)
+        pass
+    else:
+        ctx.set_option("trace_step", 1)
+        ctx.set_option("trace_decode", 1)
+        ctx.set_option("trace_plan", 1)
     threads = len(os.sched_getaffinity(0))
     lays = []
     for li in range(2):
@@ -81,6 +85,12 @@ def main():
     for i in range(6):
         step(lays[i % 2])
     ctx.synchronize()
+    if args.plain:
+        for i in range(args.reps):
+            step(lays[i % 2])
+        ctx.synchronize()
+        print("plain steps done")
+        return
     graphs = []
     for lay in lays:  # trace graph replays (the bench's timed path), not eager launches
         ctx.graph_begin()
