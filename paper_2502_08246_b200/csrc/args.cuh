@@ -28,8 +28,25 @@ struct alignas(16) TileRec {
     uint32_t qslot;  // group * n_hchunks + head chunk
     uint32_t ready;  // dynamic tiles: 1 = published
     uint32_t end;    // 1: last tile of its slot's contiguous range (a run ends here)
+    // derived from the pieces by the planner (tile_finish), so the decode's
+    // TMA issuer reads them instead of reducing over the pieces per tile
+    uint32_t rows8;     // sum of the pieces' 8-rounded rows (bytes = rows8 * 2 * row bytes)
+    uint32_t pad[3];
+    uint32_t valid[4];  // 128-bit mask of the tile's valid smem rows
     PieceRec p[kMaxPieces];
 };
+// rows8 and the validity mask of a tile whose pieces are set
+__host__ __device__ inline void tile_finish(TileRec& t) {
+    uint32_t r8 = 0, vm[4] = {0u, 0u, 0u, 0u};
+    for (uint32_t i = 0; i < t.npieces; ++i) {
+        const uint32_t len = t.p[i].len & 0x7FFFFFFFu, s0 = t.p[i].srow;
+        r8 += (len + 7) & ~7u;
+        for (uint32_t r = s0; r < s0 + len && r < 128; ++r) vm[r >> 5] |= 1u << (r & 31);
+    }
+    t.rows8 = r8;
+    t.pad[0] = t.pad[1] = t.pad[2] = 0;
+    for (int q = 0; q < 4; ++q) t.valid[q] = vm[q];
+}
 constexpr uint32_t kPieceGather = 0x80000000u;
 
 // Routing, stage 1: one CTA scores a slice of <= kSliceMax centroids and

@@ -489,6 +489,7 @@ saap_static_plan* build_static_plan(const std::vector<GroupMeta>& meta, int mode
                 t.qslot = (uint32_t)(g * nh + hc);
                 t.ready = 0;
                 t.end = i + 1 == gt.size() ? 1u : 0u;
+                tile_finish(t);
                 tiles.push_back(t);
             }
             cnt[g * nh + hc] = (uint32_t)ntiles;
@@ -690,9 +691,12 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     da.wait_plan = plan && c->opt.decode_wait ? 1u : 0u;
     da.debug_skip = c->opt.debug_skip;
     // static tickets: enough to give every CTA a share of the window
-    da.chunk_st = plan ? std::max<uint32_t>(1u, std::min<uint32_t>(chunk, sp->n_tiles / (uint32_t)grid)) : chunk;
+    // pre-assigned first chunk per CTA (no atomic before its first loads): with
+    // a planner running, CTAs on the SMs it holds start late, so they hold
+    // only 2 tiles of reserved work; everything else is claimed from the counter
+    da.chunk_st = plan ? std::max<uint32_t>(1u, std::min<uint32_t>(2u, sp->n_tiles / (uint32_t)grid)) : chunk;
     if (c->opt.trace_decode) {
-        da.dtrace = (unsigned long long*)ensure(c, c->dtrace, (size_t)c->sm_count * (128 + kTraceTiles * 24));
+        da.dtrace = (unsigned long long*)ensure(c, c->dtrace, (size_t)c->sm_count * (128 + kTraceTiles * 64));
         da.dtiles = da.dtrace + (size_t)c->sm_count * 16;
     }
     launch_decode((int)D, *src.maps, da, grid, st);
@@ -2947,13 +2951,13 @@ int saap_debug_decode_trace(saap_ctx* c, uint64_t* out, uint64_t n_ctas) {
 }
 
 // With option trace_decode set: per attention CTA of the last decode step,
-// kTraceTiles x {TMA issued, data landed, consumed} globaltimer stamps.
+// kTraceTiles x {TMA issued | flags, data landed, consumed, producer phase stamps x5}.
 int saap_debug_decode_tiles(saap_ctx* c, uint64_t* out, uint64_t n_ctas) {
     return guard([&] {
         DeviceGuard dg(c);
         if (!c->dtrace.p) invalid("decode tracing off: set option trace_decode before the first decode");
         if (n_ctas > (uint64_t)c->sm_count) invalid("debug_decode_tiles: n_ctas > SM count");
-        d2h(out, (char*)c->dtrace.p + (size_t)c->sm_count * 128, n_ctas * kTraceTiles * 24, c->stream);
+        d2h(out, (char*)c->dtrace.p + (size_t)c->sm_count * 128, n_ctas * kTraceTiles * 64, c->stream);
         sync(c);
     });
 }

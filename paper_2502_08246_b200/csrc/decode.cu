@@ -63,7 +63,8 @@ __device__ __forceinline__ void emit_tiles(TileRec* base, uint32_t ntiles, uint3
             if (vpre[mid] <= v_lo) lo = mid;
             else hi = mid;
         }
-        uint32_t np = 0;
+        uint32_t np = 0, r8 = 0;
+        uint32_t vm[4] = {0u, 0u, 0u, 0u};
 #pragma unroll 1
         for (uint32_t b = lo; b < ns; ++b) {
             const uint32_t v0 = vpre[b];
@@ -72,17 +73,28 @@ __device__ __forceinline__ void emit_tiles(TileRec* base, uint32_t ntiles, uint3
             const uint32_t a0 = max(v0, v_lo), kend = min(v0 + sg.len, v_hi);
             if (kend <= a0) continue;
             const uint64_t row = (sg.kind == KIND_LIST ? 0 : row_base) + sg.start + (a0 - v0);
-            const uint4 pr = make_uint4((kend - a0) | (sg.kind == KIND_LIST ? kPieceGather : 0u), a0 - v_lo,
+            const uint32_t len = kend - a0, s0 = a0 - v_lo;
+            const uint4 pr = make_uint4(len | (sg.kind == KIND_LIST ? kPieceGather : 0u), s0,
                                         (uint32_t)row, (uint32_t)(row >> 32));
 #pragma unroll 1
             for (uint32_t hc = 0; hc < nh; ++hc)
                 *reinterpret_cast<uint4*>(&base[(size_t)hc * ntiles + t].p[np]) = pr;
             ++np;
+            r8 += (len + 7) & ~7u;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // rows [s0, s0 + len) of the tile's 128
+                const uint32_t qlo = max(s0, (uint32_t)q * 32), qhi = min(s0 + len, (uint32_t)q * 32 + 32);
+                if (qhi > qlo)
+                    vm[q] |= (qhi - qlo == 32 ? 0xFFFFFFFFu : ((1u << (qhi - qlo)) - 1u)) << (qlo - q * 32);
+            }
         }
 #pragma unroll 1
-        for (uint32_t hc = 0; hc < nh; ++hc)
-            *reinterpret_cast<uint4*>(&base[(size_t)hc * ntiles + t]) =
-                make_uint4(np, qslot0 + hc, 0u, t + 1 == ntiles ? 1u : 0u);
+        for (uint32_t hc = 0; hc < nh; ++hc) {
+            TileRec& tr = base[(size_t)hc * ntiles + t];
+            *reinterpret_cast<uint4*>(&tr.rows8) = make_uint4(r8, 0u, 0u, 0u);
+            *reinterpret_cast<uint4*>(&tr.valid[0]) = make_uint4(vm[0], vm[1], vm[2], vm[3]);
+            *reinterpret_cast<uint4*>(&tr) = make_uint4(np, qslot0 + hc, 0u, t + 1 == ntiles ? 1u : 0u);
+        }
     }
 }
 
@@ -803,6 +815,11 @@ __device__ __forceinline__ void dsmem_st_f32(float* local, uint32_t cta, float v
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(cta));
     asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
 }
+__device__ __forceinline__ void dsmem_st_f64(double* local, uint32_t cta, double v) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(cta));
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(v) : "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -827,7 +844,7 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     static_assert(NT % S == 0 && D % TPC == 0 && DPT % 4 == 0, "slice geometry");
     constexpr uint32_t kMaxC = 1024;
     constexpr uint32_t kMaxCand = 64;
-    __shared__ float sc_all[kMaxC];            // this CTA's context: every centroid's fp32 score
+    __shared__ double sc_all[kMaxC];           // this CTA's context: every centroid's approximate score
     __shared__ double pd[D];                   // own context: pooled query in fp64
     __shared__ uint32_t s_off[kMaxC + 1], s_offA[kMaxC + 1];
     __shared__ uint32_t hist[256];
@@ -835,8 +852,7 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     // phase-local buffers share one region: scoring | exact sort | planning
     union Phase {
         struct {
-            float pf[kSlotGroups][D];    // pooled queries (f32) of the slot's contexts
-            float red[kSlotGroups][NT];  // partial dot products
+            double pf[kSlotGroups][D];    // pooled queries (fp64) of the slot's contexts
         } score;
         struct {
             double xs[kMaxC];
@@ -849,13 +865,12 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     };
     __shared__ __align__(16) Phase ph;
     auto& pf = ph.score.pf;
-    auto& red = ph.score.red;
     auto& xs = ph.sort.xs;
     auto& xi = ph.sort.xi;
     auto& segs = ph.plan.segs;
     auto& vpre = ph.plan.vpre;
     __shared__ uint32_t s_pref, s_need, s_ncand, s_nb, s_bsel, s_bcnt;
-    __shared__ float s_mm[2][NT / 32], s_bnd[32];
+    __shared__ double s_mm[2][NT / 32], s_bnd[32], s_tl;
     __shared__ double s_n2[NT / 32];
     pdl_trigger();
     const uint32_t tid = threadIdx.x, lane = tid & 31;
@@ -878,6 +893,9 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     const ApproxSlot sl = a.slots[slot];
     const uint32_t ng = sl.count, C = a.C;  // C == 8 * S
     float* qs = slab + (size_t)D * S;          // [ng][G][D] member queries
+    // partial dot products [8][NT] (fp64) during scoring; the same bytes hold
+    // the candidate rows of the exact re-scoring later
+    double (*red)[NT] = reinterpret_cast<double (*)[NT]>(qs + (size_t)kSlotGroups * a.G * D);
     const bool own = rank < ng;
     const uint32_t g = own ? sl.group[rank] : 0u;
     // ---- loads, all in one round trip: the slice rows and the member query
@@ -910,7 +928,7 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     for (uint32_t e = tid; e < ng * D; e += NT) {
         const uint32_t k = e / D, j = e % D;
         const double ps = pooled_sum(qs + (size_t)k * a.G * D + j, a.G, D);
-        pf[k][j] = (float)ps;
+        pf[k][j] = ps;
         if (k == rank) pd[j] = ps;
     }
     __syncthreads();
@@ -923,19 +941,20 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
 #pragma unroll
     for (int jj = 0; jj < (int)DPT; ++jj) cv[jj] = slab[(part * DPT + jj) * S + cl];
     // the slot's contexts are independent accumulation chains (ILP)
-    float x[kSlotGroups];
+    // fp64 FMA chains: |approx - reference| ~ 1e-14 relative, so the
+    // candidate band below almost never holds more than the l winners
+    double x[kSlotGroups];
 #pragma unroll
-    for (int k = 0; k < kSlotGroups; ++k) x[k] = 0.f;
+    for (int k = 0; k < kSlotGroups; ++k) x[k] = 0.0;
 #pragma unroll
-    for (int j4 = 0; j4 < (int)DPT / 4; ++j4) {
+    for (int j2 = 0; j2 < (int)DPT / 2; ++j2) {
+        const double c0 = (double)cv[2 * j2], c1 = (double)cv[2 * j2 + 1];
 #pragma unroll
         for (int k = 0; k < kSlotGroups; ++k) {
             if ((uint32_t)k < ng) {
-                const float4 p4 = reinterpret_cast<const float4*>(&pf[k][part * DPT])[j4];
-                x[k] = fmaf(p4.x, cv[4 * j4], x[k]);
-                x[k] = fmaf(p4.y, cv[4 * j4 + 1], x[k]);
-                x[k] = fmaf(p4.z, cv[4 * j4 + 2], x[k]);
-                x[k] = fmaf(p4.w, cv[4 * j4 + 3], x[k]);
+                const double2 p2 = reinterpret_cast<const double2*>(&pf[k][part * DPT])[j2];
+                x[k] = fma(p2.x, c0, x[k]);
+                x[k] = fma(p2.y, c1, x[k]);
             }
         }
     }
@@ -946,9 +965,9 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     trace(6);
     for (uint32_t e = tid; e < ng * S; e += NT) {
         const uint32_t k = e / S, cc = e % S;
-        float x = 0.f;
+        double x = 0.0;
         for (uint32_t p = 0; p < TPC; ++p) x += red[k][p * S + cc];
-        dsmem_st_f32(&sc_all[rank * S + cc], k, x);
+        dsmem_st_f64(&sc_all[rank * S + cc], k, x);
     }
     trace(7);
     cluster_sync_all();  // every owner now holds all C scores of its context
@@ -973,13 +992,13 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
         for (int o = 16; o; o >>= 1) part2 += __shfl_xor_sync(0xFFFFFFFFu, part2, o);
         if (lane == 0) s_n2[tid >> 5] = part2;
         // radix select (8-bit digits, MSB first): the L-th largest score
-        uint32_t key[PER];
-        float av[PER];
+        uint32_t key[PER];  // (radix fallback: order-preserving keys of the f32-rounded scores)
+        double av[PER];
 #pragma unroll
         for (uint32_t i = 0; i < PER; ++i) {
             const uint32_t cc = tid + i * NT;
             av[i] = cc < C ? sc_all[cc] : -INFINITY;
-            const uint32_t u = __float_as_uint(av[i]);
+            const uint32_t u = __float_as_uint((float)av[i]);
             key[i] = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
         }
         // the L-th largest score.  Pass 1: 256 linear buckets over [min, max]
@@ -987,17 +1006,17 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
         // pass 2: one warp ranks its (usually few) members.  Radix select
         // (8-bit digits, MSB first) when the boundary bucket holds > 32.
         {
-            float lmn = INFINITY, lmx = -INFINITY;
+            double lmn = INFINITY, lmx = -INFINITY;
 #pragma unroll
             for (uint32_t i = 0; i < PER; ++i)
                 if (tid + i * NT < C) {
-                    lmn = fminf(lmn, av[i]);
-                    lmx = fmaxf(lmx, av[i]);
+                    lmn = fmin(lmn, av[i]);
+                    lmx = fmax(lmx, av[i]);
                 }
 #pragma unroll
             for (int o = 16; o; o >>= 1) {
-                lmn = fminf(lmn, __shfl_xor_sync(0xFFFFFFFFu, lmn, o));
-                lmx = fmaxf(lmx, __shfl_xor_sync(0xFFFFFFFFu, lmx, o));
+                lmn = fmin(lmn, __shfl_xor_sync(0xFFFFFFFFu, lmn, o));
+                lmx = fmax(lmx, __shfl_xor_sync(0xFFFFFFFFu, lmx, o));
             }
             if (lane == 0) {
                 s_mm[0][tid >> 5] = lmn;
@@ -1009,14 +1028,14 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
                 s_bcnt = 0xFFFFFFFFu;
             }
             __syncthreads();
-            float vmn = s_mm[0][0], vmx = s_mm[1][0];
+            double vmn = s_mm[0][0], vmx = s_mm[1][0];
 #pragma unroll
             for (uint32_t w = 1; w < NT / 32; ++w) {
-                vmn = fminf(vmn, s_mm[0][w]);
-                vmx = fmaxf(vmx, s_mm[1][w]);
+                vmn = fmin(vmn, s_mm[0][w]);
+                vmx = fmax(vmx, s_mm[1][w]);
             }
-            const float span = vmx - vmn, scale = 256.f / span;
-            const bool lin = span > 0.f && scale < INFINITY && vmx < INFINITY && vmn > -INFINITY;
+            const double span = vmx - vmn, scale = 256.0 / span;
+            const bool lin = span > 0.0 && scale < INFINITY && vmx < INFINITY && vmn > -INFINITY;
             uint32_t bk[PER];
             if (lin) {
 #pragma unroll
@@ -1063,16 +1082,13 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
                 __syncthreads();
                 if (tid < 32) {
                     const uint32_t nb = s_nb;
-                    const float v = tid < nb ? s_bnd[tid] : -INFINITY;
+                    const double v = tid < nb ? s_bnd[tid] : -INFINITY;
                     uint32_t rank = 0;
                     for (uint32_t k = 0; k < nb; ++k) {
-                        const float u = s_bnd[k];
+                        const double u = s_bnd[k];
                         rank += (u > v || (u == v && k < tid)) ? 1u : 0u;
                     }
-                    if (tid < nb && rank == s_need - 1) {
-                        const uint32_t u = __float_as_uint(v);
-                        s_pref = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-                    }
+                    if (tid < nb && rank == s_need - 1) s_tl = v;  // the exact l-th largest
                 }
                 __syncthreads();
             } else {
@@ -1117,19 +1133,28 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
                 }
                 __syncthreads();
             }
+            // radix select ran on the f32-rounded scores: the l-th largest
+            // f32 key, lowered by its rounding (<= 2^-24 relative) so the
+            // band below stays a superset
+            if (tid == 0) {
+                const uint32_t tk = s_pref;
+                const double t32 = (double)__uint_as_float((tk & 0x80000000u) ? (tk & 0x7FFFFFFFu) : ~tk);
+                s_tl = t32 - fabs(t32) * 0x1p-23;
+            }
+            __syncthreads();
             }
         }
         trace(2);
-        const uint32_t tk = s_pref;
-        const float t_l = __uint_as_float((tk & 0x80000000u) ? (tk & 0x7FFFFFFFu) : ~tk);
+        const double t_l = s_tl;
         double n2 = 0.0;
         for (uint32_t w = 0; w < NT / 32; ++w) n2 += s_n2[w];
-        // |approx - exact| <= B: pooled rounded to f32 (<= u sum|p_j c_j|) plus
-        // fp32 accumulation over a path of DPT chained FMAs and TPC partial
-        // sums (<= gamma_{DPT+TPC} sum|p_j c_j|), sum|p_j c_j| <= |p|_2 max|c|_2,
-        // u = 2^-24; doubled, then widened 1.5x for the f32 threshold arithmetic
-        const float B2 = (float)(2.0 * 1.5 * (double)(DPT + TPC + 1) * 0x1p-24 * sqrt(n2) *
-                                 (double)a.cmax[g]);
+        // |approx - exact| <= B: the pooled query is the reference's fp64 sum
+        // exactly; the approximate dot (FMA chains of DPT terms, TPC partial
+        // sums) and the reference's sequential chain (D products, D sums)
+        // each lie within gamma_n sum|p_j c_j| of the real dot product,
+        // sum|p_j c_j| <= |p|_2 max|c|_2, u = 2^-53; the band is 2B, widened 2x
+        const double B2 = 2.0 * 2.0 * (double)(DPT + TPC + 2 * D + 2) * 0x1p-53 * sqrt(n2) *
+                          (double)a.cmax[g] * 1.01;
         if (tid == 0) s_ncand = 0;
         __syncthreads();
 #pragma unroll
@@ -1318,17 +1343,17 @@ struct DecodeCfg {
     static constexpr int NT = D / 8;  // PV n-tiles
 };
 
-#ifndef SAAP_REC_RING
-#define SAAP_REC_RING 3
-#endif
-constexpr int kRecRing = SAAP_REC_RING;  // work records in flight ahead of the TMA issue
+constexpr int kUnit = 8;  // work records per bulk copy (two units in flight)
 
 template <int D>
 struct DecodeSmem {
     using CF = DecodeCfg<D>;
     uint8_t K[CF::NS][CF::TILE_BYTES];
     uint8_t V[CF::NS][CF::TILE_BYTES];
-    float qraw[CF::NS][kHeadsPerSlot][D];  // f32 queries of the run's slot (first tile of a run)
+    // the run's A fragments (3-term bf16 split of its f32 queries), built once per run by
+    // the 8 consumer warps together: per k-step 16 lanes x {t1, t3} x {lo, hi}
+    // + 16 lanes x {t2} x {lo, hi}
+    alignas(16) uint32_t qfrag[CF::KSTEPS * 96];
     float redO[kComputeWarps][kHeadsPerSlot][D];
     float redm[kComputeWarps][kHeadsPerSlot];
     float redl[kComputeWarps][kHeadsPerSlot];
@@ -1339,11 +1364,10 @@ struct DecodeSmem {
     uint64_t st_full;     // the 8 consumer warps deposited a run's (m, l, O) states
     uint64_t st_empty;    // the merge warp has read them
     uint32_t st_slot, st_tiles, st_run;
-    // producer's work-record ring: records of upcoming tiles, bulk-copied ahead
-    alignas(16) TileRec rec[kRecRing];
-    uint64_t rec_bar[kRecRing];
-    uint32_t rec_w[kRecRing];     // work-stream index of the record
-    uint32_t rec_last[kRecRing];  // last tile of its chunk
+    // producer's record units: up to kUnit consecutive work records per bulk
+    // copy, two in flight
+    alignas(16) TileRec urec[2][kUnit];
+    uint64_t urec_bar[2];
 };
 
 // byte offset of (row, 16-byte chunk of the row) in a tile laid out as 8-row
@@ -1437,7 +1461,7 @@ __global__ void __maxnreg__(144)
         }
         mbar_init(&s.st_full, kComputeWarps);
         mbar_init(&s.st_empty, 1);
-        for (int i = 0; i < kRecRing; ++i) mbar_init(&s.rec_bar[i], 1);
+        for (int i = 0; i < 2; ++i) mbar_init(&s.urec_bar[i], 1);
         fence_mbar_init();
     }
     // (gap rows of a tile hold stale shared memory: their V fragments are
@@ -1460,8 +1484,13 @@ __global__ void __maxnreg__(144)
         for (;;) {
             mbar_wait(&s.st_full, ph);
             ph ^= 1;
-            const uint32_t slot = s.st_slot, tiles = s.st_tiles, run = s.st_run;
+            const uint32_t slot = s.st_slot, tiles = s.st_tiles;
             if (slot == 0xFFFFFFFFu) break;
+            // the run's partial slot (reserved here, off the consumers' path;
+            // before its tiles are counted, so a complete count implies every
+            // run is reserved)
+            unsigned long long run_raw = 0;
+            if (lane == 0) run_raw = atomicAdd(&a.rd[slot], 1ull << 32);
             // lane = (warp w, head h): per-head max and scale of every warp state
             const int w = lane >> 2, h = lane & 3;
             const float mw = s.redm[w][h];
@@ -1484,6 +1513,7 @@ __global__ void __maxnreg__(144)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.st_empty);  // state buffer free
+            const uint32_t run = __shfl_sync(0xFFFFFFFFu, (uint32_t)(run_raw >> 32), 0);
             const size_t pidx = (size_t)slot * a.run_cap + run;
             float* pO = a.part_O + pidx * NOUT;
 #pragma unroll
@@ -1508,77 +1538,31 @@ __global__ void __maxnreg__(144)
 
     if (warp == kComputeWarps) {
         // ------------------------------------------------ producer
-        // Work stream: [static tiles | dynamic tiles].  Tickets (the CTA index,
-        // then a global counter) map to chunks of `chunk` tiles; the last
-        // `tail` tiles of the stream are single-tile chunks so the CTAs finish
-        // together.  A feeder keeps up to kRecRing work records in flight
-        // (bulk copies into shared memory) ahead of the TMA issue.
+        // Work stream: [static tiles | dynamic tiles].  Guided self-scheduling
+        // over one tile counter: CTA b first takes static tiles
+        // [b*CS, (b+1)*CS) without an atomic, then claims chunks from the
+        // counter whose size shrinks with the remaining work once the stream
+        // length is final (ceil(rem / 2P), capped at `chunk`), so no CTA holds
+        // a large chunk when the others run dry.  A claim is issued one chunk
+        // ahead (its atomic travels while the current chunk is issued).
+        // A chunk's records arrive in units of up to kUnit consecutive records,
+        // one bulk copy each, double-buffered.  Each record carries its byte
+        // count and row mask (tile_finish), so issuing a tile is a stage wait,
+        // one expect_tx and one TMA request per piece for K and V.
         asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.map[lane]) : "memory");
         const uint64_t pol = l2_evict_first_policy();
-        const uint32_t W = a.n_static, CH = a.chunk, M = a.tail;
-        constexpr uint32_t TB = 1;  // tickets per grab (the next grab travels while these feed)
-        uint32_t fin_tot = 0;       // stream length once final (0: not yet)
-        bool fin = false, all_pub = a.n_plan_groups == 0;
-        // Ticket j -> work-stream tiles [b0, b1); 1 ok, 0 not yet reserved by
-        // the planner, -1 end.  Static tickets first (chunk_st tiles each, spread
-        // over the CTAs; for a static-only stream its last M tiles go out one
-        // per ticket), then the dynamic part: CH-tile chunks, its last M tiles
-        // one per ticket.
-        const uint32_t CS = a.chunk_st;
-        // Guided tail: a region of R tiles goes out in CH-tile chunks, then its
-        // last 3M tiles as 2M tiles in pairs and M singles, so CTAs finish
-        // within about a tile of each other.
-        bool in_tail = false;  // the last ticket was a pair or a single
-        auto guided = [&](uint32_t d, uint32_t R, uint32_t ch, uint32_t& b0, uint32_t& b1) -> bool {
-            const uint32_t tail = 3 * M;
-            const uint32_t B = R > tail ? (R - tail) / ch * ch : 0u, nb = B / ch;
-            in_tail = d >= nb;
-            if (d < nb) {
-                b0 = d * ch;
-                b1 = b0 + ch;
-                return true;
-            }
-            const uint32_t rest = R - B, S1 = rest > M ? (rest - M) / 2 * 2 : 0u, np = S1 / 2, e = d - nb;
-            if (e < np) {
-                b0 = B + 2 * e;
-                b1 = b0 + 2;
-                return true;
-            }
-            b0 = B + S1 + (e - np);
-            b1 = b0 + 1;
-            return b0 < R;
+        const uint32_t W = a.n_static, CH = a.chunk;
+        const uint32_t CS = a.chunk_st, P = gridDim.x;
+        const uint32_t pre = min(W, P * CS);  // tiles of the pre-assigned first chunks
+        uint32_t total = a.n_plan_groups ? 0xFFFFFFFFu : W;  // stream length once final
+        uint32_t known = W;                                  // W + reserved dynamic tiles
+        auto refresh = [&]() {
+            if (total != 0xFFFFFFFFu) return;
+            const unsigned long long dr = ld_acquire_u64(&a.ctr->dynres);
+            known = W + (uint32_t)dr;
+            if ((uint32_t)(dr >> 32) >= a.n_plan_groups) total = known;
         };
-        const uint32_t ks = a.n_plan_groups ? (W + CS - 1) / CS : 0xFFFFFFFFu;  // static tickets
-        auto try_chunk = [&](uint32_t j, uint32_t& b0, uint32_t& b1) -> int {
-            if (a.n_plan_groups == 0) return guided(j, W, CS, b0, b1) ? 1 : -1;  // static stream
-            if (j < ks) {
-                b0 = j * CS;
-                b1 = min(W, b0 + CS);
-                return 1;
-            }
-            const uint32_t d = j - ks;
-            uint32_t D = fin_tot;
-            if (!fin) {
-                const unsigned long long dr = ld_acquire_u64(&a.ctr->dynres);
-                D = (uint32_t)dr;
-                if ((uint32_t)(dr >> 32) >= a.n_plan_groups) {
-                    fin = true;
-                    fin_tot = D;
-                }
-            }
-            if (fin) {
-                if (!guided(d, D, CH, b0, b1)) return -1;
-                b0 += W;
-                b1 += W;
-                return 1;
-            }
-            if ((d + 2) * CH + 3 * M <= D) {  // big in any final mapping
-                b0 = W + d * CH;
-                b1 = b0 + CH;
-                return 1;
-            }
-            return 0;
-        };
+        bool all_pub = a.n_plan_groups == 0;
         // dynamic records are published with release stores: once every
         // planner CTA reported (one acquire) no per-record check is needed;
         // before that every lane acquires one flag of the chunk, and the warp
@@ -1597,186 +1581,211 @@ __global__ void __maxnreg__(144)
             __syncwarp();
             return all;
         };
-        uint32_t pc0 = 0, pc1 = 0;
-        bool pend = false, feeding = true, poll_wait = false;
-        // first batch: tickets b and b + grid (the static part spreads over all
-        // CTAs); later batches of TB consecutive tickets from the counter
-        // first ticket: the CTA index; then the counter (a CTA that starts late,
-        // e.g. on an SM the routing kernel held, holds no other reserved work)
-        uint32_t ticket = blockIdx.x, ticket_end = blockIdx.x + 1, tk = 0;
-        if (lane == 0) tk = atomicAdd(&a.ctr->tickets, TB) + gridDim.x;
+        // claims: [pre + returned, + size)
+        uint32_t cl_ret = 0, cl_size = 0, hint = pre;
+        auto claim = [&]() {
+            uint32_t sz = CH;
+            if (total != 0xFFFFFFFFu) {
+                // the counter has moved on by about one claim per CTA since
+                // this CTA's last claim returned `hint`
+                const uint32_t seen = hint + P * cl_size;
+                const uint32_t rem = total > seen ? total - seen : 0u;
+                sz = max(1u, min(CH, (rem + 2 * P - 1) / (2 * P)));
+            }
+            if (lane == 0) cl_ret = atomicAdd(&a.ctr->tickets, sz);
+            cl_size = sz;
+        };
+        bool first = true, claimed = false;
         if (a.dtrace && lane == 0) a.dtrace[16 * blockIdx.x + 12] = gtime();
-        uint32_t head = 0, tail = 0, cnt = 0, rph = 0;  // record ring (rph: phase bit per slot)
+        uint32_t pc0 = 0, pc1 = 0;  // the current chunk's remaining tiles
+        bool pend = false, feeding = true;
+        // unit slots 0/1 in registers (selects, no local memory)
+        uint32_t u_cnt0 = 0, u_cnt1 = 0, u_base0 = 0, u_base1 = 0;
+        bool u_last0 = false, u_last1 = false;
+        uint32_t u_ph = 0;  // phase bit per unit slot
+        // next unit of records into `slot`: false when none can be fetched now
+        // (planner behind, or end of stream: feeding = false)
+        auto fetch_unit = [&](int slot) -> bool {
+            if (!feeding) return false;
+            if (!pend) {
+                uint32_t b0 = 0, b1 = 0;
+                if (first && blockIdx.x * CS < pre) {
+                    b0 = blockIdx.x * CS;
+                    b1 = min(pre, b0 + CS);
+                } else {
+                    if (!claimed) {
+                        refresh();
+                        claim();
+                        claimed = true;
+                    }
+                    b0 = pre + __shfl_sync(0xFFFFFFFFu, cl_ret, 0);
+                    b1 = b0 + cl_size;
+                    refresh();
+                    if (total != 0xFFFFFFFFu) {
+                        if (b0 >= total) {
+                            feeding = false;
+                            return false;
+                        }
+                        b1 = min(b1, total);
+                    } else if (b1 > known) {
+                        return false;  // not reserved by the planner yet
+                    }
+                    if (b1 > W && !dyn_ready(b0, b1)) return false;
+                    hint = b1;
+                    claim();  // the next claim travels while this chunk is issued
+                }
+                first = false;
+                // acquired generic-proxy data (records, gathered rows) is read by
+                // the bulk and tensor copies (async proxy)
+                if (b1 > W) asm volatile("fence.proxy.async.global;" ::: "memory");
+                pc0 = b0;
+                pc1 = b1;
+                pend = true;
+            }
+            // a unit stays in one record array (static | dynamic)
+            const uint32_t n = min(min(pc1 - pc0, (uint32_t)kUnit), pc0 < W ? W - pc0 : 0xFFFFFFFFu);
+            if (lane == 0) {
+                if (a.dtrace && a.dtrace[16 * blockIdx.x + 13] == 0) a.dtrace[16 * blockIdx.x + 13] = gtime();
+                const TileRec* src = pc0 < W ? a.st_tiles + pc0 : a.dyn_tiles + (pc0 - W);
+                mbar_arrive_expect_tx(&s.urec_bar[slot], n * (uint32_t)sizeof(TileRec));
+                bulk_g2s(&s.urec[slot][0], src, n * (uint32_t)sizeof(TileRec), &s.urec_bar[slot]);
+            }
+            __syncwarp();
+            if (slot) {
+                u_cnt1 = n;
+                u_base1 = pc0;
+                u_last1 = pc0 + n == pc1;
+            } else {
+                u_cnt0 = n;
+                u_base0 = pc0;
+                u_last0 = pc0 + n == pc1;
+            }
+            pc0 += n;
+            if (pc0 == pc1) pend = false;
+            return true;
+        };
         uint32_t stage = 0, phase = 0;
         bool run_first = true;
         uint32_t run_tiles = 0;
-        unsigned long long p_wait = 0;
+        unsigned long long p_wait = 0, p_sleep = 0;
         const unsigned long long p_t0 = clock64();
-        unsigned long long p_feed = 0, p_rec = 0, p_tma = 0, p_sleep = 0, p_dec = 0;
         uint32_t p_tiles = 0;
-        for (;;) {
-            // ---- feed records
-            const unsigned long long tf = clock64();
-            while (cnt < (uint32_t)kRecRing && feeding) {
-                // waiting for the planner: re-poll only when the ring runs low
-                // (each poll is a round trip on the producer's path)
-                if (!pend && poll_wait && cnt > 1) break;
-                // in the stream's tail a CTA holds at most one record beyond
-                // its tile ring, so the CTAs drain together
-                if (!pend && in_tail && cnt > 0) break;
-                if (!pend) {
-                    if (ticket == ticket_end) {  // next batch (reserved one batch ahead)
-                        ticket = __shfl_sync(0xFFFFFFFFu, tk, 0);
-                        ticket_end = ticket + TB;
-                        if (lane == 0) tk = atomicAdd(&a.ctr->tickets, TB) + gridDim.x;
-                    }
-                    uint32_t b0 = 0, b1 = 0;
-                    const int r = try_chunk(ticket, b0, b1);
-                    if (r < 0) {
-                        feeding = false;
-                        break;
-                    }
-                    if (r == 0 || (b1 > W && !dyn_ready(b0, b1))) {  // retry after issuing
-                        poll_wait = true;
-                        break;
-                    }
-                    poll_wait = false;
-                    // acquired generic-proxy data (records, gathered rows) is read by
-                    // every lane's bulk and tensor copies (async proxy)
-                    if (b1 > W) asm volatile("fence.proxy.async.global;" ::: "memory");
-                    pc0 = b0;
-                    pc1 = b1;
-                    pend = true;
-                    ++ticket;
-                }
-                if (lane == 0) {
-                    if (a.dtrace && a.dtrace[16 * blockIdx.x + 13] == 0) a.dtrace[16 * blockIdx.x + 13] = gtime();
-                    const TileRec* src = pc0 < W ? a.st_tiles + pc0 : a.dyn_tiles + (pc0 - W);
-                    s.rec_w[tail] = pc0;
-                    s.rec_last[tail] = pc0 + 1 == pc1 ? 1u : 0u;
-                    mbar_arrive_expect_tx(&s.rec_bar[tail], (uint32_t)sizeof(TileRec));
-                    bulk_g2s(&s.rec[tail], src, (uint32_t)sizeof(TileRec), &s.rec_bar[tail]);
-                }
-                ++pc0;
-                if (pc0 == pc1) pend = false;
-                tail = tail + 1 == (uint32_t)kRecRing ? 0u : tail + 1;
-                ++cnt;
-            }
-            p_feed += clock64() - tf;
-            if (cnt == 0) {
-                if (!feeding) break;
-                const unsigned long long ts = clock64();
-                __nanosleep(a.poll_ns);  // waiting for the planner
-                p_sleep += clock64() - ts;
-                continue;
-            }
-            // ---- issue the head tile
-            const unsigned long long tr = clock64();
-            mbar_wait(&s.rec_bar[head], (rph >> head) & 1u);
-            p_rec += clock64() - tr;
-            const unsigned long long td = clock64();
-            if (a.dtrace && lane == 0 && a.dtrace[16 * blockIdx.x + 10] == 0) a.dtrace[16 * blockIdx.x + 10] = gtime();
-            rph ^= 1u << head;
-            __syncwarp();
-            const uint32_t w = s.rec_w[head];
-            const bool last_in_chunk = s.rec_last[head] != 0;
-            const uint4 hdr = *reinterpret_cast<const uint4*>(&s.rec[head]);
-            const uint32_t np = hdr.x, qslot = hdr.y;
-            const bool last_of_run = last_in_chunk || hdr.w != 0;
-            uint32_t len = 0, srow = 0, gat = 0;
-            uint64_t row = 0;
-            if ((uint32_t)lane < np) {
-                const uint4 v = *reinterpret_cast<const uint4*>(&s.rec[head].p[lane]);
-                len = v.x & ~kPieceGather;
-                gat = v.x & kPieceGather;
-                srow = v.y;
-                row = ((uint64_t)v.w << 32) | v.z;
-            }
-            ++run_tiles;
-            const uint32_t r8 = (len + 7) & ~7u;
-            uint32_t bytes = r8 * CF::RB * 2;
-            uint32_t vm[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t lo = max(srow, (uint32_t)q * 32), hi = min(srow + len, (uint32_t)q * 32 + 32);
-                uint32_t m = 0;
-                if (hi > lo) m = (hi - lo == 32 ? 0xFFFFFFFFu : ((1u << (hi - lo)) - 1u)) << (lo - q * 32);
-                vm[q] = m;
-            }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                bytes += __shfl_xor_sync(0xFFFFFFFFu, bytes, o);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) vm[q] |= __shfl_xor_sync(0xFFFFFFFFu, vm[q], o);
-            }
-            const uint32_t g = qslot / a.n_hchunks, hc = qslot % a.n_hchunks;
-            const uint32_t nq = min((uint32_t)kHeadsPerSlot, a.G - hc * kHeadsPerSlot);
-            p_dec += clock64() - td;
-            if (lane == 0) {
-                const unsigned long long tw = clock64();
-                mbar_wait(&s.empty[stage], phase ^ 1);
-                p_wait += clock64() - tw;
-                s.valid[stage] = make_uint4(vm[0], vm[1], vm[2], vm[3]);
-                const uint32_t flags = (run_first ? 1u : 0u) | (last_of_run ? 2u : 0u) | (nq << 8);
-                s.meta[stage] = make_int4((int)qslot, (int)flags, 0, (int)run_tiles);
-                const uint32_t qbytes = nq * D * 4;
-                mbar_arrive_expect_tx(&s.full[stage], bytes + (run_first ? qbytes : 0));
-                if (run_first)
-                    bulk_g2s(&s.qraw[stage][0][0], a.q + ((size_t)g * a.G + hc * kHeadsPerSlot) * D,
-                             qbytes, &s.full[stage]);
-            }
-            __syncwarp();
-            const unsigned long long tt = clock64();
-            if (len) {
-                // one request per piece for K and one for V: a box of r8/8 groups
-                // when the rounded-up rows exist; else the piece's whole groups
-                // plus a bounds-checked 8-row box (zero fill past the end)
-                const CUtensorMap* mk = &maps.map[(gat ? 2 : 0) * kBoxSizes];
-                const CUtensorMap* mv = mk + kBoxSizes;
-                const uint64_t lim = gat ? maps.grows : maps.rows;
-                const uint32_t off = (srow >> 3) * 8 * CF::RB;
-                if (row + r8 <= lim) {
-                    tma4d(&s.K[stage][off], mk + (r8 / 8 - 1), (int)row, &s.full[stage], pol);
-                    tma4d(&s.V[stage][off], mv + (r8 / 8 - 1), (int)row, &s.full[stage], pol);
-                } else {
-                    const uint32_t full = len & ~7u;
-                    if (full) {
-                        tma4d(&s.K[stage][off], mk + (full / 8 - 1), (int)row, &s.full[stage], pol);
-                        tma4d(&s.V[stage][off], mv + (full / 8 - 1), (int)row, &s.full[stage], pol);
-                    }
-                    if (r8 > full) {
-                        const uint32_t off2 = ((srow + full) >> 3) * 8 * CF::RB;
-                        tma4d(&s.K[stage][off2], mk, (int)(row + full), &s.full[stage], pol);
-                        tma4d(&s.V[stage][off2], mv, (int)(row + full), &s.full[stage], pol);
-                    }
-                }
-            }
-            __syncwarp();
-            p_tma += clock64() - tt;
-            if (a.dtrace && lane == 0 && a.dtrace[16 * blockIdx.x + 11] == 0) a.dtrace[16 * blockIdx.x + 11] = gtime();
+        auto pstamp = [&](int k) {
             if (a.dtiles && lane == 0 && p_tiles < (uint32_t)kTraceTiles)
-                a.dtiles[((size_t)blockIdx.x * kTraceTiles + p_tiles) * 3] = gtime();
-            ++p_tiles;
-            // a dynamic record is re-armed for the next step once consumed
-            if (w >= W && lane == 0) a.dyn_tiles[w - W].ready = 0;
-            if (++stage == CF::NS) {
-                stage = 0;
-                phase ^= 1;
+                a.dtiles[((size_t)blockIdx.x * kTraceTiles + p_tiles) * 8 + k] = gtime();
+        };
+        int cur = 0;
+        while (!fetch_unit(cur) && feeding) {  // the first unit (the planner may be behind)
+            const unsigned long long ts = clock64();
+            __nanosleep(a.poll_ns);
+            p_sleep += clock64() - ts;
+        }
+        while (cur ? u_cnt1 : u_cnt0) {
+            const int nx = cur ^ 1;
+            // the next unit travels while this one is issued
+            bool have_next = fetch_unit(nx);
+            mbar_wait(&s.urec_bar[cur], (u_ph >> cur) & 1u);
+            u_ph ^= 1u << cur;
+            if (a.dtrace && lane == 0 && a.dtrace[16 * blockIdx.x + 10] == 0) a.dtrace[16 * blockIdx.x + 10] = gtime();
+            const uint32_t ucnt = cur ? u_cnt1 : u_cnt0, ubase = cur ? u_base1 : u_base0;
+            const bool ulast = cur ? u_last1 : u_last0;
+            // dynamic records are re-armed for the next step once copied
+            if (ubase >= W && (uint32_t)lane < ucnt) a.dyn_tiles[ubase - W + lane].ready = 0;
+            for (uint32_t i = 0; i < ucnt; ++i) {
+                pstamp(3);
+                const TileRec& R = s.urec[cur][i];
+                const uint4 hdr = *reinterpret_cast<const uint4*>(&R);
+                const uint32_t np = hdr.x, qslot = hdr.y;
+                const bool last_in_chunk = ulast && i + 1 == ucnt;
+                const bool last_of_run = last_in_chunk || hdr.w != 0;
+                uint32_t len = 0, srow = 0, gat = 0;
+                uint64_t row = 0;
+                if ((uint32_t)lane < np) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(&R.p[lane]);
+                    len = v.x & ~kPieceGather;
+                    gat = v.x & kPieceGather;
+                    srow = v.y;
+                    row = ((uint64_t)v.w << 32) | v.z;
+                }
+                ++run_tiles;
+                if (lane == 0) {
+                    const unsigned long long tw = clock64();
+                    mbar_wait(&s.empty[stage], phase ^ 1);
+                    p_wait += clock64() - tw;
+                    pstamp(7);
+                    s.valid[stage] = *reinterpret_cast<const uint4*>(&R.valid[0]);
+                    const uint32_t g = qslot / a.n_hchunks, hc = qslot - g * a.n_hchunks;
+                    const uint32_t nq = min((uint32_t)kHeadsPerSlot, a.G - hc * kHeadsPerSlot);
+                    const uint32_t flags = (run_first ? 1u : 0u) | (last_of_run ? 2u : 0u) | (nq << 8);
+                    const uint32_t qoff = (uint32_t)(((size_t)g * a.G + hc * kHeadsPerSlot) * D);
+                    s.meta[stage] = make_int4((int)qslot, (int)flags, (int)qoff, (int)run_tiles);
+                    const uint32_t bytes = R.rows8 * (uint32_t)CF::RB * 2u;
+                    mbar_arrive_expect_tx(&s.full[stage], bytes);
+                }
+                __syncwarp();
+                if (run_first) {
+                    // the run's query rows (<= 2 KB) into this SM's L1 ahead of the
+                    // consumers' fragment build (no shared-memory staging)
+                    const uint32_t g = qslot / a.n_hchunks, hc = qslot - g * a.n_hchunks;
+                    const uint32_t nq = min((uint32_t)kHeadsPerSlot, a.G - hc * kHeadsPerSlot);
+                    const float* qb = a.q + ((size_t)g * a.G + hc * kHeadsPerSlot) * D;
+                    if ((uint32_t)lane * 32u < nq * D)
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(qb + lane * 32) : "memory");
+                }
+                if (len) {
+                    // one request per piece for K and one for V: a box of r8/8 groups
+                    // when the rounded-up rows exist; else the piece's whole groups
+                    // plus a bounds-checked 8-row box (zero fill past the end)
+                    const uint32_t r8 = (len + 7) & ~7u;
+                    const CUtensorMap* mk = &maps.map[(gat ? 2 : 0) * kBoxSizes];
+                    const CUtensorMap* mv = mk + kBoxSizes;
+                    const uint64_t lim = gat ? maps.grows : maps.rows;
+                    const uint32_t off = (srow >> 3) * 8 * CF::RB;
+                    if (row + r8 <= lim) {
+                        tma4d(&s.K[stage][off], mk + (r8 / 8 - 1), (int)row, &s.full[stage], pol);
+                        tma4d(&s.V[stage][off], mv + (r8 / 8 - 1), (int)row, &s.full[stage], pol);
+                    } else {
+                        const uint32_t full = len & ~7u;
+                        if (full) {
+                            tma4d(&s.K[stage][off], mk + (full / 8 - 1), (int)row, &s.full[stage], pol);
+                            tma4d(&s.V[stage][off], mv + (full / 8 - 1), (int)row, &s.full[stage], pol);
+                        }
+                        if (r8 > full) {
+                            const uint32_t off2 = ((srow + full) >> 3) * 8 * CF::RB;
+                            tma4d(&s.K[stage][off2], mk, (int)(row + full), &s.full[stage], pol);
+                            tma4d(&s.V[stage][off2], mv, (int)(row + full), &s.full[stage], pol);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (a.dtrace && lane == 0 && a.dtrace[16 * blockIdx.x + 11] == 0) a.dtrace[16 * blockIdx.x + 11] = gtime();
+                if (a.dtiles && lane == 0 && p_tiles < (uint32_t)kTraceTiles)
+                    a.dtiles[((size_t)blockIdx.x * kTraceTiles + p_tiles) * 8] =
+                            (gtime() & ~63ull) | np | (last_in_chunk ? 32u : 0u);  // stamp | pieces | chunk end
+                ++p_tiles;
+                if (++stage == CF::NS) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+                run_first = last_of_run;
+                if (last_of_run) run_tiles = 0;
             }
-            head = head + 1 == (uint32_t)kRecRing ? 0u : head + 1;
-            --cnt;
-            run_first = last_of_run;
-            if (last_of_run) run_tiles = 0;
+            if (cur) u_cnt1 = 0;
+            else u_cnt0 = 0;
+            if (!have_next) {  // fetch now (poll while the planner is behind)
+                while (!fetch_unit(nx) && feeding) {
+                    const unsigned long long ts = clock64();
+                    __nanosleep(a.poll_ns);
+                    p_sleep += clock64() - ts;
+                }
+            }
+            cur = nx;
         }
         if (lane == 0) {
             if (a.dtrace) {
                 a.dtrace[16 * blockIdx.x + 4] = p_wait;
                 a.dtrace[16 * blockIdx.x + 5] = clock64() - p_t0;
-                a.dtrace[16 * blockIdx.x + 7] = p_feed;
-                a.dtrace[16 * blockIdx.x + 8] = p_rec;
-                a.dtrace[16 * blockIdx.x + 9] = p_tma;
                 a.dtrace[16 * blockIdx.x + 14] = p_sleep;
-                a.dtrace[16 * blockIdx.x + 15] = p_dec;
             }
             mbar_wait(&s.empty[stage], phase ^ 1);
             s.meta[stage] = make_int4(-1, 0, 0, 0);
@@ -1800,10 +1809,14 @@ __global__ void __maxnreg__(144)
     const int row0 = warp * 16;     // this warp's 16 rows of the tile
     const int mtx = lane >> 3, r8 = lane & 7;
 
-    uint32_t qa[CF::KSTEPS][4];  // A fragments of [q1; q2; q3; 0]
+    // A fragments of [q1; q2; q3; 0] live in s.qfrag for the whole run (the next
+    // run's build starts only once every consumer warp reached it)
+    const uint32_t qf_off = upper ? 64u + 2u * (uint32_t)(lane - 16) : 4u * (uint32_t)lane;
     float o[CF::NT][4];
     float m_run = -INFINITY, l_run = 0.f;
-    uint32_t st_ph = 0, run_idx = 0;
+    uint32_t st_ph = 0;
+    // named barrier of the 8 consumer warps (run starts share one fragment build)
+    auto consumer_bar = []() { asm volatile("bar.sync 1, %0;" ::"n"(kComputeWarps * 32) : "memory"); };
 
     uint32_t stage = 0, phase = 0;
     uint32_t n_tiles_done = 0;
@@ -1818,7 +1831,7 @@ __global__ void __maxnreg__(144)
         }
         const int4 mt = s.meta[stage];
         if (a.dtiles && threadIdx.x == 0 && n_tiles_done < (uint32_t)kTraceTiles)
-            a.dtiles[((size_t)blockIdx.x * kTraceTiles + n_tiles_done) * 3 + 1] = gtime();
+            a.dtiles[((size_t)blockIdx.x * kTraceTiles + n_tiles_done) * 8 + 1] = gtime();
         if (a.dtrace && threadIdx.x == 0) {
             if (n_tiles_done == 0) a.dtrace[16 * blockIdx.x + 1] = gtime();
             if (mt.x < 0) {
@@ -1838,40 +1851,39 @@ __global__ void __maxnreg__(144)
             break;
         }
         const uint32_t flags = (uint32_t)mt.y;
-        if ((flags & 1u) && threadIdx.x == 0)  // the run's partial slot, reserved early
-            run_idx = (uint32_t)(atomicAdd(&a.rd[(uint32_t)mt.x], 1ull << 32) >> 32);
         if (flags & 1u) {
             // A operand [q1; q2; q3; 0]: 3-term bf16 split of the f32 queries
             // (~fp32-exact).  Rows g (lanes < 16: q1, else q2) and g + 8 (q3 / 0).
+            // Warp w converts k-steps w, w + 8, ... for every lane position into
+            // qfrag (each element converted once per CTA, not once per warp);
+            // the consumer warps then load their fragments.
             const uint32_t nq = (flags >> 8) & 7u;
-            const float* qh = &s.qraw[stage][hq][0];
+            const float* qh = a.q + (uint32_t)mt.z + hq * D;  // L1 (prefetched by the producer)
             const bool live = (uint32_t)hq < nq;
-#pragma unroll
-            for (int k = 0; k < CF::KSTEPS; ++k) {
-                const float2 lo2 = live ? *reinterpret_cast<const float2*>(qh + 16 * k + 2 * tig) : make_float2(0.f, 0.f);
-                const float2 hi2 = live ? *reinterpret_cast<const float2*>(qh + 16 * k + 8 + 2 * tig) : make_float2(0.f, 0.f);
+            consumer_bar();  // every warp has loaded the previous run's fragments
+            for (int k = warp; k < CF::KSTEPS; k += kComputeWarps) {
+                const float2 lo2 = live ? __ldg(reinterpret_cast<const float2*>(qh + 16 * k + 2 * tig)) : make_float2(0.f, 0.f);
+                const float2 hi2 = live ? __ldg(reinterpret_cast<const float2*>(qh + 16 * k + 8 + 2 * tig)) : make_float2(0.f, 0.f);
                 // x = t1 + t2 + t3 (bf16 terms, hardware RNE conversions)
                 const uint32_t a1 = bf16x2_rn(lo2.x, lo2.y), b1 = bf16x2_rn(hi2.x, hi2.y);
                 const float ra0 = lo2.x - bf16lo(a1), ra1 = lo2.y - bf16hi(a1);
                 const float rb0 = hi2.x - bf16lo(b1), rb1 = hi2.y - bf16hi(b1);
                 const uint32_t a2 = bf16x2_rn(ra0, ra1), b2 = bf16x2_rn(rb0, rb1);
-                if (!upper) {
-                    qa[k][0] = a1;
-                    qa[k][1] = bf16x2_rn(ra0 - bf16lo(a2), ra1 - bf16hi(a2));
-                    qa[k][2] = b1;
-                    qa[k][3] = bf16x2_rn(rb0 - bf16lo(b2), rb1 - bf16hi(b2));
-                } else {
-                    qa[k][0] = a2;
-                    qa[k][1] = 0u;
-                    qa[k][2] = b2;
-                    qa[k][3] = 0u;
-                }
+                if (!upper)
+                    *reinterpret_cast<uint4*>(&s.qfrag[k * 96 + 4 * lane]) =
+                            make_uint4(a1, bf16x2_rn(ra0 - bf16lo(a2), ra1 - bf16hi(a2)), b1,
+                                       bf16x2_rn(rb0 - bf16lo(b2), rb1 - bf16hi(b2)));
+                else
+                    *reinterpret_cast<uint2*>(&s.qfrag[k * 96 + 64 + 2 * (lane - 16)]) = make_uint2(a2, b2);
             }
+            consumer_bar();  // fragments complete (read from qfrag by every tile of the run)
 #pragma unroll
             for (int n = 0; n < CF::NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
             m_run = -INFINITY;
             l_run = 0.f;
         }
+        if (a.dtiles && threadIdx.x == 0 && n_tiles_done - 1 < (uint32_t)kTraceTiles)
+            a.dtiles[((size_t)blockIdx.x * kTraceTiles + n_tiles_done - 1) * 8 + 4] = gtime();
         const uint32_t vbits = ((&s.valid[stage].x)[warp >> 1] >> ((warp & 1) * 16)) & 0xFFFFu;
         if (vbits && !a.debug_skip) {
             // ---- S = [q1; q2; q3] K^T for this warp's 16 rows
@@ -1883,8 +1895,22 @@ __global__ void __maxnreg__(144)
                 const uint32_t chunk = 2 * k + (mtx & 1);  // 16-byte chunk within the row
                 uint32_t b0, b1, b2, b3;
                 ldsm_x4(kbase + toff<D>(krow, chunk), b0, b1, b2, b3);
-                mma16816(c0, qa[k][0], qa[k][1], qa[k][2], qa[k][3], b0, b1);
-                mma16816(c1, qa[k][0], qa[k][1], qa[k][2], qa[k][3], b2, b3);
+                uint32_t qa0, qa1, qa2, qa3;
+                if (!upper) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(&s.qfrag[k * 96 + qf_off]);
+                    qa0 = v.x;
+                    qa1 = v.y;
+                    qa2 = v.z;
+                    qa3 = v.w;
+                } else {
+                    const uint2 v = *reinterpret_cast<const uint2*>(&s.qfrag[k * 96 + qf_off]);
+                    qa0 = v.x;
+                    qa1 = 0u;
+                    qa2 = v.y;
+                    qa3 = 0u;
+                }
+                mma16816(c0, qa0, qa1, qa2, qa3, b0, b1);
+                mma16816(c1, qa0, qa1, qa2, qa3, b2, b3);
             }
             // scores for head hq; keys c0 -> row0 + 2*tig + {0,1}, c1 -> row0 + 8 + 2*tig + {0,1}
             // rows g + g+8 here, g+4 (+ zero row g+12) on lane ^ 16
@@ -1938,6 +1964,8 @@ __global__ void __maxnreg__(144)
                     pa3 = 0u;
                 }
             }
+            if (a.dtiles && threadIdx.x == 0 && n_tiles_done - 1 < (uint32_t)kTraceTiles)
+                a.dtiles[((size_t)blockIdx.x * kTraceTiles + n_tiles_done - 1) * 8 + 5] = gtime();
             // ---- O += P V   (B = V rows via ldmatrix.trans)
             const uint32_t vbase = smem_u32(&s.V[stage][0]);
             const uint32_t vrow = row0 + (mtx & 1) * 8 + r8;
@@ -1961,7 +1989,7 @@ __global__ void __maxnreg__(144)
         __syncwarp();
         if (lane == 0) mbar_arrive(&s.empty[stage]);
         if (a.dtiles && threadIdx.x == 0 && n_tiles_done - 1 < (uint32_t)kTraceTiles)
-            a.dtiles[((size_t)blockIdx.x * kTraceTiles + n_tiles_done - 1) * 3 + 2] = gtime();
+            a.dtiles[((size_t)blockIdx.x * kTraceTiles + n_tiles_done - 1) * 8 + 2] = gtime();
 
         if (flags & 2u) {
             // ---- run done: deposit this warp's (m, l, O) state for the merge warp
@@ -1991,7 +2019,6 @@ __global__ void __maxnreg__(144)
             if (threadIdx.x == 0) {
                 s.st_slot = slot;
                 s.st_tiles = (uint32_t)mt.w;
-                s.st_run = run_idx;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.st_full);
@@ -2145,6 +2172,10 @@ void launch_combine(int D, const CombineArgs& ca, uint32_t n_qslots, cudaStream_
 #undef SAAP_COMBINE
 }
 
+// a combine CTA (1 KB) must fit next to a decode CTA on one SM (228 KB, 1 KB
+// reserved per CTA) so each slot is combined as soon as it completes
+static_assert(sizeof(DecodeSmem<128>) + 1024 + 1024 + 2048 <= 228 * 1024, "decode smem leaves no room for combine CTAs");
+
 template <int D>
 static void launch_decode_t(const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st) {
     const size_t smem = sizeof(DecodeSmem<D>) + 1024;
@@ -2205,10 +2236,10 @@ void launch_route_cluster(int D, const ClusterRouteArgs& a, uint32_t n_slots, cu
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    // dynamic smem: centroid slice [D][C/8] + member queries [8][G][D] +
-    // candidate rows [64][D + 1] (f32)
-    cfg.dynamicSmemBytes = ((size_t)D * (a.C / kClusterCtas) + (size_t)kSlotGroups * a.G * D +
-                            (size_t)64 * (D + 1)) * 4;
+    // dynamic smem: centroid slice [D][C/8] + member queries [8][G][D] (f32)
+    // + partial dots [8][512] (f64) / candidate rows [64][D + 1] (f32)
+    cfg.dynamicSmemBytes = ((size_t)D * (a.C / kClusterCtas) + (size_t)kSlotGroups * a.G * D) * 4 +
+                           std::max<size_t>((size_t)64 * (D + 1) * 4, (size_t)kSlotGroups * kClusterThreads * 8);
     if (cfg.dynamicSmemBytes > 160 * 1024) fail(SAAP_ERR_UNSUPPORTED, "route: slice too large");
     static bool configured = false;
     if (!configured) {

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--drift", type=float, default=0.0)
     ap.add_argument("--dense", action="store_true")
+    ap.add_argument("--given", action="store_true", help="caller-selected lists (no routing kernel)")
     args = ap.parse_args()
     import torch
     import paper_2502_08246_b200 as sb
@@ -35,9 +36,18 @@ def main():
     out = torch.empty(64, 4, 128, device=dev)
     stats = torch.zeros(64, 3, dtype=torch.int64, device=dev)
 
+    if args.given:
+        for lay in lays:
+            lay.sel = torch.empty(64, a.probes, dtype=torch.int32, device=dev)
+            lay.L.sparse_attention_dev(lay.routers, lay.qr_t, lay.qd_t, 4, cfg, out, stats,
+                                       selected=lay.sel)
+        ctx.synchronize()
+
     def step(lay):
         if args.dense:
             lay.kv.dense_attention_dev(lay.qr_t, 4, out)
+        elif args.given:
+            lay.L.sparse_attention_selected_dev(lay.qr_t, 4, lay.sel, a.probes, cfg, out, stats)
         else:
             lay.L.sparse_attention_dev(lay.routers, lay.qr_t, lay.qd_t, 4, cfg, out, stats)
 

@@ -134,10 +134,14 @@ def main():
                                 "prod_sleep_frac": round(float(np.median(t[:, 14] / np.maximum(t[:, 5], 1))), 3),
                                 "prod_decode_frac": round(float(np.median(t[:, 15] / np.maximum(t[:, 5], 1))), 3)}
             dec_all.append(((t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3, (t[:, 2] - t0) / 1e3, t[:, 3]))
-            tb = (ct.c_uint64 * (nc * 48 * 3))()
+            tb = (ct.c_uint64 * (nc * 48 * 8))()
             if lib.saap_debug_decode_tiles(ctx.h, tb, ct.c_uint64(nc)) == 0:
-                tt = np.array(list(tb), dtype=np.float64).reshape(nc, 48, 3)
-                tt = np.where(tt >= t0, (tt - t0) / 1e3, np.nan)
+                raw = np.array(list(tb), dtype=np.uint64).reshape(nc, 48, 8)
+                flags = (raw[:, :, 0] & np.uint64(63)).astype(np.float64)  # pieces | 32 chunk end
+                raw[:, :, 0] &= ~np.uint64(63)
+                ok = raw >= np.uint64(t0)
+                tt = np.where(ok, (raw.astype(np.int64) - np.int64(t0)).astype(np.float64) / 1e3, np.nan)
+                tt = np.concatenate([tt, flags[:, :, None]], axis=2)
                 tiles_all.append(tt)
         if not args.dense and lib.saap_debug_plan_trace(ctx.h, pbuf) == 0:
             # slot 0 / CTA 0 phase clocks (clock64 deltas -> us at the measured SM clock)
