@@ -154,6 +154,7 @@ struct DecodeArgs {
     uint32_t tail;             // the stream's last `tail` tiles go out one per ticket
     uint32_t wait_plan;        // 1: wait for the planner grid before streaming
     uint32_t debug_skip;       // profiling only: 1 consumers skip the math, 2 producer skips TMA
+    uint32_t min_chunk;        // smallest guided claim (tiles)
     uint32_t poll_ns;          // producer's sleep between polls for planner tiles
     StepCounters* ctr;
     const float* q;            // [groups][G][D] attention queries (f32)

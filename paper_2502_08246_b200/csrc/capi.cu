@@ -690,6 +690,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     da.tl = c->tl;
     da.wait_plan = plan && c->opt.decode_wait ? 1u : 0u;
     da.debug_skip = c->opt.debug_skip;
+    da.min_chunk = c->opt.min_chunk;
     // static tickets: enough to give every CTA a share of the window
     // pre-assigned first chunk per CTA (no atomic before its first loads): with
     // a planner running, CTAs on the SMs it holds start late, so they hold
@@ -840,6 +841,9 @@ int saap_ctx_destroy(saap_ctx* c) {
             if (g.exec) cudaGraphExecDestroy(g.exec);
         auto& lc = live_contexts();
         lc.erase(std::remove(lc.begin(), lc.end(), c), lc.end());
+        if (c->side) cudaStreamDestroy(c->side);
+        if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+        if (c->ev_join) cudaEventDestroy(c->ev_join);
         if (c->own_stream) cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -935,6 +939,7 @@ int saap_ctx_set_option(saap_ctx* c, const char* name, int64_t value) {
         else if (n == "decode_wait") o.decode_wait = clamp(0, 1);
         else if (n == "cluster_route") o.cluster_route = clamp(0, 1);
         else if (n == "debug_skip") o.debug_skip = clamp(0, 1);
+        else if (n == "min_chunk") o.min_chunk = clamp(1, 16);
         else if (n == "host_graph") o.host_graph = clamp(0, 1);
         else if (n == "trace_decode") o.trace_decode = clamp(0, 1);
         else if (n == "trace_plan") o.trace_plan = clamp(0, 1);
@@ -2487,6 +2492,16 @@ int saap_sparse_attention_dev(saap_ctx* c, const saap_layer* L, const saap_route
     });
 }
 
+static bool pinned(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* const* routers,
                           const float* q_roped, const float* q_deroped, uint64_t G,
                           const saap_sparse_cfg* cfg, float* out, saap_attn_stats* stats,
@@ -2508,21 +2523,48 @@ int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* c
         float* dout = (float*)ensure(c, c->out, qn * 4);
         saap_attn_stats* dst = (saap_attn_stats*)ensure(c, c->stats, L->n_groups * sizeof(saap_attn_stats));
         uint32_t* dsel = selected ? (uint32_t*)ensure(c, c->sel, L->n_groups * std::max<uint64_t>(cfg->probes, 1) * 4) : nullptr;
-        h2d(dqr, q_roped, qn * 4, st);
-        if (qmode == 2) h2d(dqd, q_deroped, qn * 4, st);
         if (qmode == 1) dqd = dqr;
+        auto upload = [&] {
+            if (qmode == 2) {
+                // the two query uploads run concurrently (the attention rows on
+                // a side branch), joined before the step's first kernel
+                if (!c->side) {
+                    SAAP_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+                    SAAP_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+                    SAAP_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+                }
+                SAAP_CUDA(cudaEventRecord(c->ev_fork, st));
+                SAAP_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+                h2d(dqr, q_roped, qn * 4, c->side);
+                SAAP_CUDA(cudaEventRecord(c->ev_join, c->side));
+                h2d(dqd, q_deroped, qn * 4, st);
+                SAAP_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));
+            } else {
+                h2d(dqr, q_roped, qn * 4, st);
+            }
+        };
+        auto download = [&] {
+            d2h(out, dout, qn * 4, st);
+            if (stats) d2h(stats, dst, L->n_groups * sizeof(saap_attn_stats), st);
+            if (selected && cfg->probes) d2h(selected, dsel, L->n_groups * cfg->probes * 4, st);
+        };
         // Repeated calls with the same (layer, routers, cfg, shapes) replay a
         // CUDA graph of the step captured on the second call (the first sizes
-        // the scratch); timing and trace modes stay eager.
+        // the scratch); with pinned caller buffers the graph also carries the
+        // uploads and downloads, so a call is one graph launch and one
+        // synchronize.  Timing and trace modes stay eager.
         const bool no_graph = !c->opt.host_graph || c->opt.trace_step || c->opt.trace_decode ||
                               c->opt.trace_plan;
         saap_ctx::HostGraph* hg = nullptr;
         if (!no_graph && !c->timing) {
-            std::vector<const void*> rs(routers, routers + L->n_groups);
             const uint64_t ck[4] = {cfg->probes, cfg->block_size, cfg->sink_count, cfg->recent_count};
             for (auto& e : c->host_graphs)
-                if (e.layer == L && e.routers == rs && std::equal(ck, ck + 4, e.cfg) && e.G == G &&
-                    e.qmode == qmode && e.sel == (selected != nullptr)) {
+                if (e.layer == L && e.routers.size() == L->n_groups &&
+                    std::equal(e.routers.begin(), e.routers.end(), (const void* const*)routers) &&
+                    std::equal(ck, ck + 4, e.cfg) && e.G == G && e.qmode == qmode &&
+                    e.sel == (selected != nullptr) &&
+                    (!e.copies || (e.h_qr == q_roped && e.h_qd == q_deroped && e.h_out == out &&
+                                   e.h_stats == stats && e.h_sel == selected))) {
                     hg = &e;
                     break;
                 }
@@ -2530,11 +2572,20 @@ int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* c
                 c->host_graphs.emplace_back();
                 hg = &c->host_graphs.back();
                 hg->layer = L;
-                hg->routers = rs;
+                hg->routers.assign(routers, routers + L->n_groups);
                 std::copy(ck, ck + 4, hg->cfg);
                 hg->G = G;
                 hg->qmode = qmode;
                 hg->sel = selected != nullptr;
+                hg->copies = pinned(q_roped) && (qmode != 2 || pinned(q_deroped)) && pinned(out) &&
+                             pinned(stats) && pinned(selected);
+                if (hg->copies) {
+                    hg->h_qr = q_roped;
+                    hg->h_qd = q_deroped;
+                    hg->h_out = out;
+                    hg->h_stats = stats;
+                    hg->h_sel = selected;
+                }
             }
         }
         if (hg && hg->exec && hg->gen == c->scratch_gen) {
@@ -2545,11 +2596,16 @@ int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* c
                 int m = 0, u = 0;
                 bind_routers(const_cast<saap_layer*>(L), routers, m, u);
             }
+            if (!hg->copies) upload();
             SAAP_CUDA(cudaGraphLaunch(hg->exec, st));
-            c->launches += 3;
+            c->launches += hg->nlaunch;
+            if (!hg->copies) download();
         } else {
+            upload();
             sparse_dev(c, L, routers, dqr, dqd, G, cfg, dout, dst, dsel);
+            download();
             if (hg && hg->seen++ > 0) {
+                sync(c);
                 if (hg->exec) cudaGraphExecDestroy(hg->exec);
                 hg->exec = nullptr;
                 const uint64_t gen = c->scratch_gen, launches = c->launches;
@@ -2557,7 +2613,9 @@ int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* c
                 c->capturing = true;
                 cudaGraph_t graph = nullptr;
                 try {
+                    if (hg->copies) upload();
                     sparse_dev(c, L, routers, dqr, dqd, G, cfg, dout, dst, dsel);
+                    if (hg->copies) download();
                 } catch (...) {
                     c->capturing = false;
                     cudaStreamEndCapture(st, &graph);
@@ -2565,6 +2623,7 @@ int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* c
                     throw;
                 }
                 c->capturing = false;
+                hg->nlaunch = c->launches - launches;
                 c->launches = launches;  // captured, not run
                 SAAP_CUDA(cudaStreamEndCapture(st, &graph));
                 const cudaError_t ie = cudaGraphInstantiate(&hg->exec, graph, 0);
@@ -2573,9 +2632,6 @@ int saap_sparse_attention(saap_ctx* c, const saap_layer* L, const saap_router* c
                 hg->gen = gen;
             }
         }
-        d2h(out, dout, qn * 4, st);
-        if (stats) d2h(stats, dst, L->n_groups * sizeof(saap_attn_stats), st);
-        if (selected && cfg->probes) d2h(selected, dsel, L->n_groups * cfg->probes * 4, st);
         sync(c);
     });
 }

@@ -166,6 +166,17 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long atom_acq_rel_add_u64(unsigned long long* p,
+                                                                unsigned long long v) {
+    unsigned long long old;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ uint32_t atom_acq_rel_add_u32(uint32_t* p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
 __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -203,6 +214,9 @@ struct saap_ctx {
     int device = 0;
     int sm_count = 0;
     cudaStream_t stream = nullptr;
+    // host API: the two query uploads run on parallel branches
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool own_stream = false;
     uint64_t launches = 0;
     // growable device scratch (sized by uncaptured calls; graphs reuse it)
@@ -218,6 +232,12 @@ struct saap_ctx {
         std::vector<const void*> routers;
         uint64_t cfg[4] = {}, G = 0, gen = 0;
         int qmode = 0, sel = 0, seen = 0;
+        // pinned caller buffers: the graph carries the copies too (H2D queries,
+        // D2H outputs / counters / lists); null: copies outside the graph
+        const void *h_qr = nullptr, *h_qd = nullptr;
+        void *h_out = nullptr, *h_stats = nullptr, *h_sel = nullptr;
+        bool copies = false;
+        uint64_t nlaunch = 0;  // kernels in the captured step
         cudaGraphExec_t exec = nullptr;
     };
     std::vector<HostGraph> host_graphs;
@@ -231,7 +251,8 @@ struct saap_ctx {
     struct Options {
         uint32_t chunk = 8;             // work-stream tiles per decode ticket (sparse)
         uint32_t chunk_dense = 16;      // ... (dense / full attention)
-        uint32_t tail_per_cta = 1;      // guided-tail singles per CTA
+        uint32_t tail_per_cta = 1;      // (unused since guided claims)
+        uint32_t min_chunk = 4;         // smallest guided claim at the stream's end (tiles)
         uint32_t decode_poll_ns = 100;  // producer back-off while waiting for the planner
         uint32_t combine_poll_ns = 1000;  // combine back-off while no run is published
         uint32_t decode_wait = 0;       // 1: decode waits for routing to finish (PDL grid wait)

@@ -1590,7 +1590,7 @@ __global__ void __maxnreg__(144)
                 // this CTA's last claim returned `hint`
                 const uint32_t seen = hint + P * cl_size;
                 const uint32_t rem = total > seen ? total - seen : 0u;
-                sz = max(1u, min(CH, (rem + 2 * P - 1) / (2 * P)));
+                sz = max(min(a.min_chunk, CH), min(CH, (rem + 2 * P - 1) / (2 * P)));
             }
             if (lane == 0) cl_ret = atomicAdd(&a.ctr->tickets, sz);
             cl_size = sz;

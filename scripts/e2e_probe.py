@@ -91,6 +91,23 @@ def main():
             oh.copy_(out, non_blocking=True)
         stream.synchronize()
     res["torch_copies_graph_sync"] = wall(copies)
+    qh2 = torch.empty(ng, G, d, pin_memory=True)
+    qh2.copy_(q.cpu())
+
+    def e2e_two():  # distinct roped / de-roped buffers (the bench's case)
+        sb._check(lib.saap_sparse_attention(ctx.h, L.h, rarr, ct.c_void_p(qh.data_ptr()),
+                                            ct.c_void_p(qh2.data_ptr()), ct.c_uint64(G),
+                                            ct.byref(ccfg), ct.c_void_p(oh.data_ptr()), st_h, None))
+    res["host_api_e2e_two_q"] = wall(e2e_two)
+    qd_dev = torch.empty_like(q)
+
+    def copies_only():
+        with torch.cuda.stream(stream):
+            q.copy_(qh, non_blocking=True)
+            qd_dev.copy_(qh2, non_blocking=True)
+            oh.copy_(out, non_blocking=True)
+        stream.synchronize()
+    res["copies_only_sync"] = wall(copies_only)
     print({k: round(v, 1) for k, v in res.items()})
 
 

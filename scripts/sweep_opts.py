@@ -20,11 +20,13 @@ def main():
     ap.add_argument("--drift", type=float, default=0.0)
     ap.add_argument("--dense", action="store_true")
     ap.add_argument("--given", action="store_true", help="caller-selected lists (no routing kernel)")
+    ap.add_argument("--probes", type=int, default=32)
+    ap.add_argument("--ctx-len", type=int, default=131072)
     args = ap.parse_args()
     import torch
     import paper_2502_08246_b200 as sb
-    a = argparse.Namespace(ctx_len=131072, batch=8, kv_heads=8, q_heads=32, dim=128, buckets=1024,
-                           probes=32, recent=2047, sink=1, kmeans_iters=10)
+    a = argparse.Namespace(ctx_len=args.ctx_len, batch=8, kv_heads=8, q_heads=32, dim=128, buckets=1024,
+                           probes=args.probes, recent=2047, sink=1, kmeans_iters=10)
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream()
     ctx = sb.Context(0)
@@ -81,7 +83,8 @@ def main():
         print(json.dumps({setting or "default": [round(t, 2) for t in ts]}), flush=True)
         for k in kv:  # back to the defaults for the next setting
             ctx.set_option(k, {"chunk": 8, "chunk_dense": 16, "tail_per_cta": 1, "decode_poll_ns": 100,
-                               "combine_poll_ns": 1000, "decode_wait": 0, "cluster_route": 1}.get(k, 0))
+                               "combine_poll_ns": 1000, "decode_wait": 0, "cluster_route": 1,
+                               "min_chunk": 4}.get(k, 0))
     print(json.dumps(res))
 
 

@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--drift", type=float, default=0.0)
     ap.add_argument("--dense", action="store_true")
     ap.add_argument("--plain", action="store_true", help="no tracing; run --reps eager steps and exit")
+    ap.add_argument("--ctx-len", type=int, default=131072)
+    ap.add_argument("--probes", type=int, default=32)
     ap.add_argument("--given", action="store_true",
                     help="replay the routed lists through the caller-selected path (no routing)")
     args = ap.parse_args()
@@ -35,8 +37,8 @@ def main():
     import paper_2502_08246_b200 as sb
     if not hasattr(sb.Context, "set_option"):
         raise SystemExit("library without context options")
-    a = argparse.Namespace(ctx_len=131072, batch=8, kv_heads=8, q_heads=32, dim=128, buckets=1024,
-                           probes=32, recent=2047, sink=1, kmeans_iters=10)
+    a = argparse.Namespace(ctx_len=args.ctx_len, batch=8, kv_heads=8, q_heads=32, dim=128, buckets=1024,
+                           probes=args.probes, recent=2047, sink=1, kmeans_iters=10)
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream()
     ctx = sb.Context(0)
