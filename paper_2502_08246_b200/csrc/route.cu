@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(kQmTL) qm_logits_kernel(QModelArgs a) {
 __global__ void __launch_bounds__(256) qm_softmax_kernel(QModelArgs a) {
     __shared__ double red[8];
     __shared__ double s_inv;
+    extern __shared__ double ex[];  // the row's exps: the ordered sum reads shared memory
     double* row = a.probs + (size_t)blockIdx.x * a.C;
     double mx = -INFINITY;
     for (uint32_t c = threadIdx.x; c < a.C; c += blockDim.x) mx = fmax(mx, row[c]);
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(256) qm_softmax_kernel(QModelArgs a) {
     __syncthreads();
     mx = red[0];
     for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w]);
-    for (uint32_t c = threadIdx.x; c < a.C; c += blockDim.x) row[c] = exp_glibc(__dadd_rn(row[c], -mx));
+    for (uint32_t c = threadIdx.x; c < a.C; c += blockDim.x) ex[c] = exp_glibc(__dadd_rn(row[c], -mx));
     __syncthreads();
     if (threadIdx.x == 0) {  // loads run ahead of the ordered chain
         double t = 0.0;
@@ -174,16 +175,16 @@ __global__ void __launch_bounds__(256) qm_softmax_kernel(QModelArgs a) {
         for (; c + 8 <= a.C; c += 8) {
             double v[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = row[c + u];
+            for (int u = 0; u < 8; ++u) v[u] = ex[c + u];
 #pragma unroll
             for (int u = 0; u < 8; ++u) t = __dadd_rn(t, v[u]);
         }
-        for (; c < a.C; ++c) t = __dadd_rn(t, row[c]);
+        for (; c < a.C; ++c) t = __dadd_rn(t, ex[c]);
         s_inv = __ddiv_rn(1.0, t);
     }
     __syncthreads();
     const double inv = s_inv;
-    for (uint32_t c = threadIdx.x; c < a.C; c += blockDim.x) row[c] = __dmul_rn(row[c], inv);
+    for (uint32_t c = threadIdx.x; c < a.C; c += blockDim.x) row[c] = __dmul_rn(ex[c], inv);
 }
 
 __global__ void debug_exp_kernel(const double* x, uint64_t n, double* y) {
@@ -211,7 +212,13 @@ void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st
     }
     qm_hidden_kernel<<<dim3(n_groups, (a.h + kQmT - 1) / kQmT), kQmT, sm1, st>>>(a);
     qm_logits_kernel<<<dim3(a.slot_g ? n_slots : n_groups, (a.C + kQmTL - 1) / kQmTL), kQmTL, sm2, st>>>(a);
-    qm_softmax_kernel<<<n_groups * a.G, 256, 0, st>>>(a);
+    const size_t sm3 = (size_t)a.C * sizeof(double);
+    static size_t cfg3 = 0;
+    if (sm3 > 48 * 1024 && sm3 > cfg3) {
+        SAAP_CUDA(cudaFuncSetAttribute(qm_softmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3));
+        cfg3 = sm3;
+    }
+    qm_softmax_kernel<<<n_groups * a.G, 256, sm3, st>>>(a);
     SAAP_CUDA(cudaGetLastError());
 }
 
