@@ -423,6 +423,16 @@ def ours(a):
         pre_p.append(tp)
     ctx.timing()  # clear decode records
     ctx.enable_timing(False)
+    # C4: 131,072 tokens x 32 layers x 8 KV heads = 33.5M keys, as 4 back-to-back
+    # builds of this layer's 8.4M keys (assign + pack), device time
+    torch.cuda.synchronize()
+    c4e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    c4e[0].record(stream)
+    for _ in range(4):
+        lay0.L.build_dev(parts0, lay0.K, lay0.V, lay0.Kd)
+    c4e[1].record(stream)
+    torch.cuda.synchronize()
+    c4_ms = c4e[0].elapsed_time(c4e[1])
     used_tc, refined = lay0.L.assign_info()
     n_keys_prefill = n_groups * (N - a.sink)
     assign_ms, pack_ms = float(np.median(pre_a)), float(np.median(pre_p))
@@ -631,6 +641,9 @@ def ours(a):
                                                    / 1389.8, 4),
             "pack_gbs": round(pack_bytes / (pack_ms * 1e-3) / 1e9, 1),
             "pack_frac": round(pack_bytes / (pack_ms * 1e-3) / 1e9 / peak, 4),
+            "c4": {"keys": 4 * n_keys_prefill, "ms": round(c4_ms, 3),
+                   "keys_per_s": round(4 * n_keys_prefill / (c4_ms * 1e-3), 1),
+                   "note": "131072 tokens x 32 layers x 8 KV heads, as 4 builds of 64 contexts"},
         },
     }
     if rank == 0:

@@ -1248,72 +1248,73 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     // this CTA reads no remote slice from here on; it leaves only once every
     // CTA of the cluster is past its reads of this CTA's slice
     cluster_arrive();
-    // ---- plan (one warp): bucket segments -> 8-aligned virtual rows -> tiles
-    if (tid >= 32) {
-        cluster_wait();
-        return;
-    }
+    // ---- plan: warp 0 lays the bucket segments out as 8-aligned virtual rows
+    // and reserves the context's tiles; every thread then writes tile records
     const uint32_t nh = a.n_hchunks;
     const uint32_t rb0 = fallback ? 0 : n - a.recent;  // == T (recent == the layer's hint)
-    unsigned long long keys = 0;
-    uint32_t mx = 0, vrows = 0;
-    for (uint32_t b0 = 0; b0 < L; b0 += 32) {
-        const uint32_t b = b0 + lane;
-        uint32_t lenA = 0, st = 0;
-        if (b < L) {
-            const uint32_t cc = sel[b];
-            mx = max(mx, s_off[cc + 1] - s_off[cc]);  // raw bucket size (attention.cpp:356)
-            lenA = s_offA[cc + 1] - s_offA[cc];
-            st = sink + s_offA[cc];
-        }
-        keys += lenA;
-        const uint32_t v8 = (lenA + 7) & ~7u;
-        uint32_t incl = v8;
+    __shared__ uint32_t s_tile0, s_ntiles;
+    if (tid < 32) {
+        unsigned long long keys = 0;
+        uint32_t mx = 0, vrows = 0;
+        for (uint32_t b0 = 0; b0 < L; b0 += 32) {
+            const uint32_t b = b0 + lane;
+            uint32_t lenA = 0, st = 0;
+            if (b < L) {
+                const uint32_t cc = sel[b];
+                mx = max(mx, s_off[cc + 1] - s_off[cc]);  // raw bucket size (attention.cpp:356)
+                lenA = s_offA[cc + 1] - s_offA[cc];
+                st = sink + s_offA[cc];
+            }
+            keys += lenA;
+            const uint32_t v8 = (lenA + 7) & ~7u;
+            uint32_t incl = v8;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= (uint32_t)o) incl += v;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= (uint32_t)o) incl += v;
+            }
+            if (b < L) {
+                segs[b] = Seg{KIND_ROWS, lenA, st};
+                vpre[b] = vrows + incl - v8;
+            }
+            vrows += __shfl_sync(0xFFFFFFFFu, incl, 31);
         }
-        if (b < L) {
-            segs[b] = Seg{KIND_ROWS, lenA, st};
-            vpre[b] = vrows + incl - v8;
-        }
-        vrows += __shfl_sync(0xFFFFFFFFu, incl, 31);
-    }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        keys += __shfl_xor_sync(0xFFFFFFFFu, keys, o);
-        mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
-    }
-    const uint32_t ntiles = (vrows + kTileRows - 1) / kTileRows;
-    uint32_t tile0 = 0;
-    if (lane == 0) {
-        tile0 = (uint32_t)atomicAdd(&a.ctr->dynres, (1ull << 32) | (unsigned long long)(ntiles * nh));
-        for (uint32_t hc = 0; hc < nh; ++hc) a.dyn_cnt[g * nh + hc] = ntiles | kCntValid;
-        saap_attn_stats stt;
-        stt.keys_scored = fallback ? (unsigned long long)n : (unsigned long long)sink + (n - rb0) + keys;
-        stt.max_visited_bucket = fallback ? 0 : mx;
-        stt.empty_attention = stt.keys_scored == 0 ? 1 : 0;
-        stt.reserved = 0;
-        a.stats[g] = stt;
+        for (int o = 16; o; o >>= 1) {
+            keys += __shfl_xor_sync(0xFFFFFFFFu, keys, o);
+            mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+        }
+        const uint32_t ntiles = (vrows + kTileRows - 1) / kTileRows;
+        if (lane == 0) {
+            s_tile0 = (uint32_t)atomicAdd(&a.ctr->dynres, (1ull << 32) | (unsigned long long)(ntiles * nh));
+            s_ntiles = ntiles;
+            for (uint32_t hc = 0; hc < nh; ++hc) a.dyn_cnt[g * nh + hc] = ntiles | kCntValid;
+            saap_attn_stats stt;
+            stt.keys_scored = fallback ? (unsigned long long)n : (unsigned long long)sink + (n - rb0) + keys;
+            stt.max_visited_bucket = fallback ? 0 : mx;
+            stt.empty_attention = stt.keys_scored == 0 ? 1 : 0;
+            stt.reserved = 0;
+            a.stats[g] = stt;
+        }
     }
     (void)T;
-    tile0 = __shfl_sync(0xFFFFFFFFu, tile0, 0);
+    __syncthreads();
+    const uint32_t ntiles = s_ntiles, tile0 = s_tile0;
     trace(8);
     if (ntiles) {
-        emit_tiles(a.dyn_tiles + tile0, ntiles, nh, g * nh, segs, vpre, L, gm.row_base, lane, 32);
-        // one fence per lane orders every record the warp wrote (the warp
-        // barrier makes the other lanes' writes cumulative) before the flags
-        __syncwarp();
-        trace(9);
+        emit_tiles(a.dyn_tiles + tile0, ntiles, nh, g * nh, segs, vpre, L, gm.row_base, tid, NT);
+        // every thread orders its own records; the barrier makes them all
+        // precede every ready flag
         __threadfence();
-        __syncwarp();
-        trace(10);
-        for (uint32_t e = lane; e < ntiles * nh; e += 32)
+        __syncthreads();
+        trace(9);
+        for (uint32_t e = tid; e < ntiles * nh; e += NT)
             *reinterpret_cast<volatile uint32_t*>(&a.dyn_tiles[tile0 + e].ready) = 1u;
+        trace(10);
     }
-    if (lane == 0) {
-        if (!ntiles) __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
         atomicAdd(&a.ctr->published, 1u);
         tl_mark(a.tl, 1, false);
         if (a.trace) a.trace[16 + 6 * blockIdx.x + 3] = gt();
