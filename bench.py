@@ -71,6 +71,7 @@ def parse():
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-c1", action="store_true", help="skip the C1-shape sub-line")
     ap.add_argument("--router", default="centroid", choices=["centroid", "qmodel"],
                     help="BucketRouter plugin: CentroidRouter (de-roped) or QModelRouter "
                          "(qmodel_init weights of the reference's shape, hidden 1024)")
@@ -171,15 +172,20 @@ def measured_peaks():
 
 
 def ncu_traffic():
-    """DRAM bytes per decode launch from the committed ncu capture of this build."""
+    """DRAM bytes per decode launch from the committed ncu capture, and whether
+    that capture was taken on this build's decode kernel source (git blob hash
+    of csrc/decode.cu stamped into the capture record)."""
+    import hashlib
     p = os.path.join(ROOT, "profiles", "decode_kernel_ncu.json")
-    if os.path.exists(p):
-        try:
-            d = json.load(open(p))
-            return d.get("dram_bytes_per_launch"), d.get("source")
-        except Exception:
-            return None, None
-    return None, None
+    if not os.path.exists(p):
+        return None, None, None
+    try:
+        d = json.load(open(p))
+        src = open(os.path.join(ROOT, "paper_2502_08246_b200", "csrc", "decode.cu"), "rb").read()
+        blob = hashlib.sha1(b"blob %d\0" % len(src) + src).hexdigest()
+        return d.get("dram_bytes_per_launch"), d.get("source"), blob == d.get("decode_cu_blob")
+    except Exception:
+        return None, None, None
 
 
 def cpu_threads(a):
@@ -585,9 +591,13 @@ def ours(a):
                                     dense_step, out, out_dense, stats, heads_local, h0, threads,
                                     timed_groups=False)
 
+    c1 = None
+    if rank == 0 and world == 1 and a.router == "centroid" and not a.no_c1:
+        c1 = c1_line(sb, torch, ctx, stream, dev, a, threads, timed_ref=not a.no_cpu_baseline)
+
     us = ms_sparse * 1e3
     achieved = (bytes_step / (attn_ms * 1e-3) / 1e9) if attn_ms else None
-    traffic, traffic_src = ncu_traffic()
+    traffic, traffic_src, traffic_same_build = ncu_traffic()
     line = {
         "metric": METRIC, "value": round(us, 3), "unit": UNIT, "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_sparse, 5),
@@ -608,6 +618,7 @@ def ours(a):
                      "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4) if achieved else None,
                      "traffic": traffic, "traffic_source": traffic_src,
+                     "traffic_same_build": traffic_same_build,
                      "peak_kind": peak_kind,
                      "bytes_per_launch": int(bytes_step),
                      "dense_achieved": round(dense_bytes / (dense_attn_ms * 1e-3) / 1e9, 1)
@@ -623,6 +634,7 @@ def ours(a):
             "hbm_gbs": round(iks_step * d * 4 / (iattn_ms * 1e-3) / 1e9, 1),
             "parity": iparity},
         "cpu_baseline": cpu,
+        "c1": c1,
         "e2e": {"value": round(ms_e2e * 1e3, 3), "unit": UNIT,
                 "h2d_bytes_per_step": int(2 * n_groups * G * d * 4),
                 "d2h_bytes_per_step": int(n_groups * G * d * 4 + n_groups * ct.sizeof(sb.AttnStats))},
@@ -653,6 +665,69 @@ def ours(a):
         comm.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def c1_line(sb, torch, ctx, stream, dev, a, threads, timed_ref=True):
+    """C1 (BASELINE.json configs[0], the CPU reference's own benchmark shape):
+    one context of 16,384 keys (d=128, HeadSpec defaults, drift 5e-4), C=1024,
+    l=32, window 1+2047, 64 decode queries routed and attended one by one
+    (G=1: the harness convention, experiments.cpp:435), as one batched step of
+    64 groups over the same cache.  Reference: the compiled reference's
+    sparse_attention for the same 64 queries on the host cores."""
+    N, C, L, nq = 16384, 1024, 32, 64
+    spec = sb.HeadSpec(dim=128, seed=1, drift_rate=5e-4)
+    p = sb.generate_prompt(spec, N, nq, 0, bf16=True, threads=threads,
+                           want=("keys_deroped", "keys_roped", "values"))
+    cent = sb.train_head_partition(spec, N, C, 10, 1, ctx, threads)
+    part = sb.Partition(cent, ctx)
+    to_dev = lambda x: torch.from_numpy(x.view(np.int16)).to(dev).view(torch.bfloat16)
+    K, V, Kd = to_dev(p.keys_roped), to_dev(p.values), to_dev(p.keys_deroped)
+    L_ = sb.Layer([N] * nq, 128, C, 1, 2047, ctx)
+    L_.build_dev([part] * nq, K.repeat(nq, 1), V.repeat(nq, 1), Kd.repeat(nq, 1))
+    routers = [sb.CentroidRouter(part, True)] * nq
+    qr = torch.from_numpy(bf16_bits_round(p.queries_roped).reshape(nq, 1, 128)).to(dev)
+    qd = torch.from_numpy(bf16_bits_round(p.queries_deroped).reshape(nq, 1, 128)).to(dev)
+    cfg = sb.SparseAttnConfig(L, 128, sb.DenseWindow(1, 2047))
+    out = torch.empty(nq, 1, 128, device=dev)
+    stats = torch.zeros(nq, 3, dtype=torch.int64, device=dev)
+    step = lambda: L_.sparse_attention_dev(routers, qr, qd, 1, cfg, out, stats)
+    step()
+    ctx.synchronize()
+    ctx.graph_begin()
+    step()
+    g = ctx.graph_end()
+    for _ in range(10):
+        g.launch()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(200):
+        g.launch()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / 200 * 1e3
+    res = {"workload": "C1: one context of 16384 keys (d=128, drift 5e-4), C=1024, l=32, window 1+2047, "
+                       "64 queries routed and attended one by one (G=1), one batched step",
+           "us_per_step": round(us, 2), "us_per_query": round(us / nq, 3),
+           "selectivity": round(float(stats[:, 0].float().mean().item()) / N, 5)}
+    if timed_ref:
+        import oracle
+        if oracle.ref_available():
+            R = oracle.ref()
+            Kf = (p.keys_roped.astype(np.uint32) << 16).view(np.float32)
+            Vf = (p.values.astype(np.uint32) << 16).view(np.float32)
+            Kdf = (p.keys_deroped.astype(np.uint32) << 16).view(np.float32)
+            assign = R.assign_keys(Kdf[1:], cent, threads=threads)
+            st = R.store(Kf, Vf, cent, 1, assign)
+            rt = R.centroid_router(cent, True)
+            qr_h, qd_h = qr.cpu().numpy(), qd.cpu().numpy()
+            t0 = time.perf_counter()
+            ref = R.sparse_attention_batch([st] * nq, [rt] * nq, qr_h, qd_h, L, 128, 1, 2047, 1)
+            one = (time.perf_counter() - t0) * 1e6
+            ks = np.asarray(ref[1]).reshape(-1)
+            res["reference_single_thread_us_per_step"] = round(one, 1)
+            res["keys_scored_exact"] = f"{int(np.sum(ks == stats[:, 0].cpu().numpy()))}/{nq}"
+    return res
 
 
 def parity_leg(sb, torch, ctx, a, lay, groups, sparse_step, dense_step, out, out_dense, stats,

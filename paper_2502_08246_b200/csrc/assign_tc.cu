@@ -34,7 +34,8 @@ constexpr uint32_t A_TILE_BYTES = TM * KD * 2;         // 32 KB
 constexpr uint32_t B_TERM_BYTES = CN * KD * 2;         // 32 KB
 constexpr uint32_t B_STAGE_BYTES = 2 * B_TERM_BYTES;   // hi + mid
 constexpr uint32_t TMEM_COLS = 512;
-constexpr int THREADS = 320;  // warps 0-7 epilogue, 8 TMA, 9 MMA
+constexpr int EPI = 8;        // epilogue warps: (tile, TMEM lane quarter)
+constexpr int THREADS = (EPI + 2) * 32;  // warps 0..EPI-1 epilogue, EPI TMA, EPI+1 MMA
 }  // namespace tc
 
 struct TcTile {
@@ -112,34 +113,44 @@ struct __align__(1024) TcSmem {
     uint8_t A[tc::NT][tc::A_TILE_BYTES];          // [tile][box(2)][128 rows][128 B]
     uint8_t B[tc::NSTAGE][tc::B_STAGE_BYTES];     // [stage][term(2)][box(2)][CN rows][128 B]
     uint64_t a_full;
+    uint64_t a_empty;  // the pair's last MMAs have read A (tcgen05.commit)
     uint64_t b_full[tc::NSTAGE];
     uint64_t b_empty[tc::NSTAGE];
     uint64_t t_full[2];
     uint64_t t_empty[2];
     uint32_t tmem_base;
+    // column-half partial results of the epilogue: [tile][row] best, second, id
+    float pb1[tc::NT][tc::TM], pb2[tc::NT][tc::TM];
+    uint32_t pi1[tc::NT][tc::TM];
 };
 
+// Persistent: one CTA per SM walks key-tile pairs p = blockIdx.x, + gridDim.x,
+// ...  TMEM is allocated and the barriers initialised once; the next pair's
+// centroid chunks stream as soon as a B stage frees, and its key tiles load as
+// soon as the last MMAs of the current pair have read A, so the fill of one
+// pair overlaps the epilogue drain of the previous one.
 __global__ void __launch_bounds__(tc::THREADS, 1)
         assign_tc_kernel(const __grid_constant__ CUtensorMap map_k,
                          const __grid_constant__ CUtensorMap map_hi,
-                         const __grid_constant__ CUtensorMap map_mid, TcAssignArgs a) {
+                         const __grid_constant__ CUtensorMap map_mid, TcAssignArgs a,
+                         uint32_t n_pairs) {
     using namespace tc;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     TcSmem& s = *reinterpret_cast<TcSmem*>(
             (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const TcTile t0 = a.tiles[blockIdx.x * NT];
     const uint32_t nchunks = a.Cpad / CN;
 
     if (threadIdx.x == 0) {
         mbar_init(&s.a_full, 1);
+        mbar_init(&s.a_empty, 1);
         for (int i = 0; i < NSTAGE; ++i) {
             mbar_init(&s.b_full[i], 1);
             mbar_init(&s.b_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s.t_full[i], 1);
-            mbar_init(&s.t_empty[i], 8);  // one arrive per epilogue warp
+            mbar_init(&s.t_empty[i], EPI);  // one arrive per epilogue warp
         }
         fence_mbar_init();
     }
@@ -154,120 +165,151 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = s.tmem_base;
 
-    if (warp == 8) {
+    if (warp == EPI) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(&map_k) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(&map_hi) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(&map_mid) : "memory");
-            mbar_arrive_expect_tx(&s.a_full, NT * A_TILE_BYTES);
-            for (int t = 0; t < NT; ++t) {
-                const TcTile tt = a.tiles[blockIdx.x * NT + t];
-                const int y = (int)(a.key_row0[tt.group] + tt.lid0);
-                for (int b = 0; b < 2; ++b)
-                    tma_load_2d(&s.A[t][b * TM * 128], &map_k, b * BOX, y, &s.a_full);
-            }
-            const int ybase = (int)(t0.part * a.Cpad);
-            for (uint32_t j = 0; j < nchunks; ++j) {
-                const uint32_t st = j % NSTAGE, ph = (j / NSTAGE) & 1;
-                mbar_wait(&s.b_empty[st], ph ^ 1);
-                mbar_arrive_expect_tx(&s.b_full[st], B_STAGE_BYTES);
-                for (int term = 0; term < 2; ++term)
+            uint32_t jg = 0, np = 0;  // chunks / pairs issued by this CTA
+            for (uint32_t p = blockIdx.x; p < n_pairs; p += gridDim.x, ++np) {
+                if (np) mbar_wait(&s.a_empty, (np - 1) & 1);  // previous pair's MMAs read A
+                mbar_arrive_expect_tx(&s.a_full, NT * A_TILE_BYTES);
+                for (int t = 0; t < NT; ++t) {
+                    const TcTile tt = a.tiles[p * NT + t];
+                    const int y = (int)(a.key_row0[tt.group] + tt.lid0);
                     for (int b = 0; b < 2; ++b)
-                        tma_load_2d(&s.B[st][term * B_TERM_BYTES + b * CN * 128],
-                                    term ? &map_mid : &map_hi, b * BOX, ybase + (int)(j * CN),
-                                    &s.b_full[st]);
+                        tma_load_2d(&s.A[t][b * TM * 128], &map_k, b * BOX, y, &s.a_full);
+                }
+                const int ybase = (int)(a.tiles[p * NT].part * a.Cpad);
+                for (uint32_t j = 0; j < nchunks; ++j, ++jg) {
+                    const uint32_t st = jg % NSTAGE, ph = (jg / NSTAGE) & 1;
+                    mbar_wait(&s.b_empty[st], ph ^ 1);
+                    mbar_arrive_expect_tx(&s.b_full[st], B_STAGE_BYTES);
+                    for (int term = 0; term < 2; ++term)
+                        for (int b = 0; b < 2; ++b)
+                            tma_load_2d(&s.B[st][term * B_TERM_BYTES + b * CN * 128],
+                                        term ? &map_mid : &map_hi, b * BOX, ybase + (int)(j * CN),
+                                        &s.b_full[st]);
+                }
             }
         }
-    } else if (warp == 9) {
+    } else if (warp == EPI + 1) {
         // ------------------------------------------------ MMA issuer (one thread)
         if (lane == 0) {
             constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) |
                                        ((uint32_t)(CN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
-            mbar_wait(&s.a_full, 0);
-            for (uint32_t j = 0; j < nchunks; ++j) {
-                const uint32_t st = j % NSTAGE, ph = (j / NSTAGE) & 1;
-                const uint32_t buf = j & 1, bph = (j >> 1) & 1;
-                mbar_wait(&s.b_full[st], ph);
-                mbar_wait(&s.t_empty[buf], bph ^ 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                for (int t = 0; t < NT; ++t) {
-                    const uint32_t dcol = tmem + buf * (NT * CN) + t * CN;
-                    for (int term = 0; term < 2; ++term) {
+            uint32_t jg = 0, np = 0;
+            for (uint32_t p = blockIdx.x; p < n_pairs; p += gridDim.x, ++np) {
+                mbar_wait(&s.a_full, np & 1);
+                for (uint32_t j = 0; j < nchunks; ++j, ++jg) {
+                    const uint32_t st = jg % NSTAGE, ph = (jg / NSTAGE) & 1;
+                    const uint32_t buf = jg & 1, bph = (jg >> 1) & 1;
+                    mbar_wait(&s.b_full[st], ph);
+                    mbar_wait(&s.t_empty[buf], bph ^ 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    for (int t = 0; t < NT; ++t) {
+                        const uint32_t dcol = tmem + buf * (NT * CN) + t * CN;
+                        for (int term = 0; term < 2; ++term) {
 #pragma unroll
-                        for (int kk = 0; kk < KD / 16; ++kk) {
-                            const uint32_t aoff = (kk >> 2) * TM * 128 + (kk & 3) * 32;
-                            const uint32_t boff = term * B_TERM_BYTES + (kk >> 2) * CN * 128 + (kk & 3) * 32;
-                            umma_bf16(dcol, umma_desc_sw128(smem_u32(&s.A[t][0]) + aoff),
-                                      umma_desc_sw128(smem_u32(&s.B[st][0]) + boff), idesc,
-                                      (term | kk) != 0);
+                            for (int kk = 0; kk < KD / 16; ++kk) {
+                                const uint32_t aoff = (kk >> 2) * TM * 128 + (kk & 3) * 32;
+                                const uint32_t boff = term * B_TERM_BYTES + (kk >> 2) * CN * 128 + (kk & 3) * 32;
+                                umma_bf16(dcol, umma_desc_sw128(smem_u32(&s.A[t][0]) + aoff),
+                                          umma_desc_sw128(smem_u32(&s.B[st][0]) + boff), idesc,
+                                          (term | kk) != 0);
+                            }
                         }
                     }
+                    umma_commit(&s.b_empty[st]);
+                    umma_commit(&s.t_full[buf]);
                 }
-                umma_commit(&s.b_empty[st]);
-                umma_commit(&s.t_full[buf]);
+                umma_commit(&s.a_empty);  // A free for the next pair
             }
         }
     } else {
         // ------------------------------------------------ epilogue: warp w drains
-        // tile w/4, TMEM lanes 32*(w%4).. (lane = key row); branchless top-3
-        const int t = warp >> 2, q4 = warp & 3;
+        // tile w/4, TMEM lanes 32*(w%4).. (lane = key row); branchless top-2
+        // (EPI = 16 would split each chunk's columns into halves merged per
+        // pair: measured slower, the extra warps contend for TMEM reads)
+        const int t = (warp >> 2) & 1, q4 = warp & 3, half = EPI == 16 ? warp >> 3 : 0;
         const int row = q4 * 32 + lane;
-        const TcTile tt = a.tiles[blockIdx.x * NT + t];
-        float b1 = -INFINITY, b2 = -INFINITY;
-        uint32_t i1 = 0;
-        float n2 = 0.f;
-        if ((uint32_t)row < tt.count) {
-            const uint4* kp = reinterpret_cast<const uint4*>(a.keys + (a.key_row0[tt.group] + tt.lid0 + row) * KD);
+        uint32_t jg = 0;
+        for (uint32_t p = blockIdx.x; p < n_pairs; p += gridDim.x) {
+            const TcTile tt = a.tiles[p * NT + t];
+            float b1 = -INFINITY, b2 = -INFINITY;
+            uint32_t i1 = 0;
+            float n2 = 0.f;
+            if (half == 0 && (uint32_t)row < tt.count) {
+                const uint4* kp = reinterpret_cast<const uint4*>(a.keys + (a.key_row0[tt.group] + tt.lid0 + row) * KD);
 #pragma unroll
-            for (int q = 0; q < KD / 8; ++q) {
-                const uint4 u = kp[q];
-                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+                for (int q = 0; q < KD / 8; ++q) {
+                    const uint4 u = kp[q];
+                    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float lo = bf16lo(w4[e]), hi = bf16hi(w4[e]);
-                    n2 = fmaf(lo, lo, fmaf(hi, hi, n2));
+                    for (int e = 0; e < 4; ++e) {
+                        const float lo = bf16lo(w4[e]), hi = bf16hi(w4[e]);
+                        n2 = fmaf(lo, lo, fmaf(hi, hi, n2));
+                    }
                 }
             }
-        }
-        const float bound = 0x1p-14f * 1.0001f * sqrtf(n2) * a.cmax[tt.part];
-        const uint32_t taddr0 = tmem + ((uint32_t)(q4 * 32) << 16) + t * CN;
-        for (uint32_t j = 0; j < nchunks; ++j) {
-            const uint32_t buf = j & 1, bph = (j >> 1) & 1;
-            mbar_wait(&s.t_full[buf], bph);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t lim = (j + 1) * CN > a.C ? a.C - j * CN : CN;  // valid columns
+            const float bound = 0x1p-14f * 1.0001f * sqrtf(n2) * a.cmax[tt.part];
+            const uint32_t taddr0 = tmem + ((uint32_t)(q4 * 32) << 16) + t * CN;
+            for (uint32_t j = 0; j < nchunks; ++j, ++jg) {
+                const uint32_t buf = jg & 1, bph = (jg >> 1) & 1;
+                mbar_wait(&s.t_full[buf], bph);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t lim = (j + 1) * CN > a.C ? a.C - j * CN : CN;  // valid columns
 #pragma unroll 1
-            for (int q = 0; q < CN / 32; ++q) {
-                float v[32];
-                tmem_ld32(taddr0 + buf * (NT * CN) + q * 32, v);
-                const uint32_t c0 = j * CN + q * 32;
-                if ((uint32_t)(q * 32 + 32) > lim) {
+                for (int q = half * (CN / 32) / (EPI / 8); q < (half + 1) * (CN / 32) / (EPI / 8); ++q) {
+                    float v[32];
+                    tmem_ld32(taddr0 + buf * (NT * CN) + q * 32, v);
+                    const uint32_t c0 = j * CN + q * 32;
+                    if ((uint32_t)(q * 32 + 32) > lim) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if ((uint32_t)(q * 32 + i) >= lim) v[i] = -INFINITY;
+                        for (int i = 0; i < 32; ++i)
+                            if ((uint32_t)(q * 32 + i) >= lim) v[i] = -INFINITY;
+                    }
+                    // running best (value, lowest id) and second-best value
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float x = v[i];
+                        b2 = fmaxf(b2, fminf(x, b1));
+                        const bool g1 = x > b1;
+                        b1 = g1 ? x : b1;
+                        i1 = g1 ? c0 + i : i1;
+                    }
                 }
-                // running best (value, lowest id) and second-best value
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const float x = v[i];
-                    b2 = fmaxf(b2, fminf(x, b1));
-                    const bool g1 = x > b1;
-                    b1 = g1 ? x : b1;
-                    i1 = g1 ? c0 + i : i1;
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s.t_empty[buf]);
+            }
+            // merge the column halves: half 1 hands its (best, second, id) over
+            if (EPI == 16 && half == 1) {
+                s.pb1[t][row] = b1;
+                s.pb2[t][row] = b2;
+                s.pi1[t][row] = i1;
+            }
+            if (EPI == 16) asm volatile("bar.sync 1, %0;" ::"n"(EPI * 32) : "memory");
+            if (EPI == 16 && half == 0) {
+                const float ob1 = s.pb1[t][row], ob2 = s.pb2[t][row];
+                const uint32_t oi1 = s.pi1[t][row];
+                // equal bests: the lower id wins (each half scanned its ids in order)
+                b2 = fmaxf(fmaxf(b2, ob2), fminf(b1, ob1));
+                if (ob1 > b1 || (ob1 == b1 && oi1 < i1)) {
+                    b1 = ob1;
+                    i1 = oi1;
                 }
             }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s.t_empty[buf]);
-        }
-        if ((uint32_t)row < tt.count) {
-            const uint32_t lid = tt.lid0 + row;
-            if (b1 - b2 > 2.f * bound) {
-                a.out[a.out_base[tt.group] + lid] = i1;
-            } else {  // ambiguous (near tie, exact tie, zero key): fp64 re-scan
-                const uint32_t slot = atomicAdd(&a.refine_count[tt.group], 1u);
-                a.refine[a.out_base[tt.group] + slot] = lid;
+            if (EPI == 16) asm volatile("bar.sync 1, %0;" ::"n"(EPI * 32) : "memory");
+            if (half == 0 && (uint32_t)row < tt.count) {
+                const uint32_t lid = tt.lid0 + row;
+                if (b1 - b2 > 2.f * bound) {
+                    a.out[a.out_base[tt.group] + lid] = i1;
+                } else {  // ambiguous (near tie, exact tie, zero key): fp64 re-scan
+                    const uint32_t slot = atomicAdd(&a.refine_count[tt.group], 1u);
+                    a.refine[a.out_base[tt.group] + slot] = lid;
+                }
             }
         }
     }
@@ -493,7 +535,12 @@ void launch_assign_tc(const uint16_t* keys, uint64_t key_rows, const uint16_t* h
                                        (int)smem));
         configured = true;
     }
-    assign_tc_kernel<<<n_tiles / tc::NT, tc::THREADS, smem, st>>>(mk, mh, mm, args);
+    const uint32_t n_pairs = n_tiles / tc::NT;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint32_t grid = std::max<uint32_t>(1u, std::min<uint32_t>(n_pairs, (uint32_t)sms));
+    assign_tc_kernel<<<grid, tc::THREADS, smem, st>>>(mk, mh, mm, args, n_pairs);
     SAAP_CUDA(cudaGetLastError());
 }
 
