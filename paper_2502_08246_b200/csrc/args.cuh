@@ -82,7 +82,10 @@ struct ApproxArgs {
 };
 // Fused routing + planning for the centroid router (C <= 1024, power of two):
 // one cluster of 8 CTAs per approximate-scoring slot.
+constexpr int kInlineSlots = 16;  // slot table carried in the launch parameters
 struct ClusterRouteArgs {
+    ApproxSlot islots[kInlineSlots];  // slots [0, n_inline) (else read from `slots`)
+    uint32_t n_inline;
     const ApproxSlot* slots;
     const GroupMeta* meta;
     const uint32_t* off;
@@ -155,6 +158,9 @@ struct DecodeArgs {
     uint32_t wait_plan;        // 1: wait for the planner grid before streaming
     uint32_t debug_skip;       // profiling only: 1 consumers skip the math, 2 producer skips TMA
     uint32_t min_chunk;        // smallest guided claim (tiles)
+    uint32_t claim_lead;       // claim the next chunk when <= this many tiles of the current one are unissued
+    uint32_t inflight;         // 0: ring depth; else at most this many tiles issued and unconsumed
+    uint32_t fetch_lead;       // fetch the next unit's records at <= this many unissued tiles
     uint32_t poll_ns;          // producer's sleep between polls for planner tiles
     StepCounters* ctr;
     const float* q;            // [groups][G][D] attention queries (f32)

@@ -275,6 +275,7 @@ void bind_routers(saap_layer* L, const saap_router* const* routers, int& mode, i
         SAAP_CUDA(cudaMemcpy(L->d_route_slots, tab.data(), tab.size() * sizeof(ApproxSlot),
                              cudaMemcpyHostToDevice));
         L->n_route_slots = (uint32_t)tab.size();
+        L->h_route_slots.assign((const uint8_t*)tab.data(), (const uint8_t*)(tab.data() + tab.size()));
     } else {
         std::vector<const double*> p(3 * L->n_groups);
         for (size_t g = 0; g < L->n_groups; ++g) {
@@ -552,7 +553,8 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
                     uint32_t qm_hidden = 0, const float* cmax = nullptr,
                     const float* const* centR = nullptr, const ApproxSlot* slots = nullptr,
                     uint32_t n_slots = 0, const uint32_t* qm_slots = nullptr,
-                    uint32_t n_qm_slots = 0, const uint32_t* given = nullptr) {
+                    uint32_t n_qm_slots = 0, const uint32_t* given = nullptr,
+                    const ApproxSlot* h_slots = nullptr) {
     const cudaStream_t st = c->stream;
     const uint64_t n_groups = src.n_groups, D = src.D, C = src.C;
     const uint64_t n_hchunks = (G + kHeadsPerSlot - 1) / kHeadsPerSlot;
@@ -634,6 +636,10 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
         if (fused) {
             ClusterRouteArgs ra{};
             ra.slots = slots;
+            if (h_slots && n_slots <= (uint32_t)kInlineSlots) {  // (one fewer round trip)
+                std::copy(h_slots, h_slots + n_slots, ra.islots);
+                ra.n_inline = n_slots;
+            }
             ra.meta = src.meta;
             ra.off = src.off;
             ra.offA = src.offA;
@@ -691,6 +697,9 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     da.wait_plan = plan && c->opt.decode_wait ? 1u : 0u;
     da.debug_skip = c->opt.debug_skip;
     da.min_chunk = c->opt.min_chunk;
+    da.claim_lead = c->opt.claim_lead;
+    da.fetch_lead = c->opt.fetch_lead;
+    da.inflight = c->opt.inflight;
     // static tickets: enough to give every CTA a share of the window
     // pre-assigned first chunk per CTA (no atomic before its first loads): with
     // a planner running, CTAs on the SMs it holds start late, so they hold
@@ -938,8 +947,11 @@ int saap_ctx_set_option(saap_ctx* c, const char* name, int64_t value) {
         else if (n == "combine_poll_ns") o.combine_poll_ns = clamp(0, 100000);
         else if (n == "decode_wait") o.decode_wait = clamp(0, 1);
         else if (n == "cluster_route") o.cluster_route = clamp(0, 1);
-        else if (n == "debug_skip") o.debug_skip = clamp(0, 1);
+        else if (n == "debug_skip") o.debug_skip = clamp(0, 2);
         else if (n == "min_chunk") o.min_chunk = clamp(1, 16);
+        else if (n == "claim_lead") o.claim_lead = clamp(0, 32);
+        else if (n == "fetch_lead") o.fetch_lead = clamp(0, 32);
+        else if (n == "inflight") o.inflight = clamp(0, 8);
         else if (n == "host_graph") o.host_graph = clamp(0, 1);
         else if (n == "trace_decode") o.trace_decode = clamp(0, 1);
         else if (n == "trace_plan") o.trace_plan = clamp(0, 1);
@@ -2475,7 +2487,8 @@ static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* con
                    mode == 1 ? L->d_cmax : nullptr, mode == 1 ? L->d_centR : nullptr,
                    mode == 1 ? (const ApproxSlot*)L->d_route_slots : nullptr, mode == 1 ? L->n_route_slots : 0,
                    mode == 2 ? L->d_qm_slots : nullptr, mode == 2 ? L->n_qm_slots : 0,
-                   mode == 4 ? given : nullptr);
+                   mode == 4 ? given : nullptr,
+                   mode == 1 && !L->h_route_slots.empty() ? (const ApproxSlot*)L->h_route_slots.data() : nullptr);
 }
 
 int saap_sparse_attention_dev(saap_ctx* c, const saap_layer* L, const saap_router* const* routers,

@@ -253,10 +253,13 @@ struct saap_ctx {
         uint32_t chunk_dense = 16;      // ... (dense / full attention)
         uint32_t tail_per_cta = 1;      // (unused since guided claims)
         uint32_t min_chunk = 4;         // smallest guided claim at the stream's end (tiles)
+        uint32_t claim_lead = 3;        // decode producer: claim when <= this many tiles are left to issue
+        uint32_t inflight = 0;          // ... 0: ring depth, else max tiles issued and unconsumed
+        uint32_t fetch_lead = 2;        // ... fetch the next records when <= this many are left
         uint32_t decode_poll_ns = 100;  // producer back-off while waiting for the planner
         uint32_t combine_poll_ns = 1000;  // combine back-off while no run is published
         uint32_t decode_wait = 0;       // 1: decode waits for routing to finish (PDL grid wait)
-        uint32_t debug_skip = 0;        // profiling only (wrong outputs): 1 skip consumer math
+        uint32_t debug_skip = 0;        // profiling only (wrong outputs): 1 skip consumer math, 2 skip K/V loads
         uint32_t cluster_route = 1;     // 0: force the general routing path
         uint32_t host_graph = 1;        // 0: saap_sparse_attention never replays graphs
         uint32_t trace_step = 0;        // step timeline (saap_debug_step_trace)
@@ -388,6 +391,7 @@ struct saap_layer {
     float* d_cmax = nullptr;           // per group partition cmax
     void* d_route_slots = nullptr;     // ApproxSlot[]: approximate-scoring slots (<= 8 contexts of one partition)
     uint32_t n_route_slots = 0;
+    std::vector<uint8_t> h_route_slots;  // host copy of the ApproxSlot table (inlined into the routing launch)
     const double** d_qm = nullptr;     // per group: w1, w2, vec (3 pointers)
     uint32_t* d_qm_slots = nullptr;    // [n_qm_slots][kQmSlot] contexts sharing a Q-model
     uint32_t n_qm_slots = 0;

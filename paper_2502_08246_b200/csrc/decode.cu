@@ -800,10 +800,11 @@ __global__ void __launch_bounds__(kPlanThreads) route_plan_kernel(PlanArgs a) {
 // centroids [r*C/8, (r+1)*C/8) for every context of the slot in fp32 (its
 // centroid slice stays in registers) and stores context k's scores into CTA
 // k's shared memory (distributed shared memory).  After one cluster barrier
-// CTA k owns all C scores of context k and selects its top-l exactly: fp32
-// radix select, candidates within the error bound 2B of the l-th score, exact
-// fp64 chains (reference operation order) only when the boundary is
-// ambiguous or the ordered list is requested.  Warp 0 then plans and
+// CTA k owns all C scores of context k and selects its top-l exactly: select
+// of the l-th score, candidates within the error bound 2B of it; when more
+// than l, an fp64 re-scoring of the candidates with its own (1e-9 x smaller)
+// band, and exact fp64 chains (reference operation order) only when that is
+// still ambiguous or the ordered list is requested.  Warp 0 then plans and
 // publishes the context's bucket tiles.
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -829,22 +830,15 @@ __device__ __forceinline__ void cluster_arrive() {
 __device__ __forceinline__ void cluster_wait() {
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-__device__ __forceinline__ float dsmem_ld_f32(const float* local, uint32_t cta) {
-    uint32_t remote;
-    float v;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(cta));
-    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
-    return v;
-}
 
 template <int D, int S>
-__global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterRouteArgs a) {
+__global__ void __launch_bounds__(kClusterThreads, 1) route_cluster_kernel(ClusterRouteArgs a) {
     constexpr uint32_t NT = kClusterThreads;
     constexpr uint32_t TPC = NT / S, DPT = D / TPC;  // threads per centroid, dims per thread
     static_assert(NT % S == 0 && D % TPC == 0 && DPT % 4 == 0, "slice geometry");
     constexpr uint32_t kMaxC = 1024;
     constexpr uint32_t kMaxCand = 64;
-    __shared__ double sc_all[kMaxC];           // this CTA's context: every centroid's approximate score
+    __shared__ float sc_all[kMaxC];            // this CTA's context: every centroid's approximate (f32) score
     __shared__ double pd[D];                   // own context: pooled query in fp64
     __shared__ uint32_t s_off[kMaxC + 1], s_offA[kMaxC + 1];
     __shared__ uint32_t hist[256];
@@ -852,7 +846,7 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     // phase-local buffers share one region: scoring | exact sort | planning
     union Phase {
         struct {
-            double pf[kSlotGroups][D];    // pooled queries (fp64) of the slot's contexts
+            float pf[kSlotGroups][D];     // pooled queries (f32-rounded) of the slot's contexts
         } score;
         struct {
             double xs[kMaxC];
@@ -890,12 +884,12 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     };
     extern __shared__ __align__(16) float dyn_smem[];
     float* slab = dyn_smem;                    // [D][S] this CTA's centroid slice (transposed)
-    const ApproxSlot sl = a.slots[slot];
+    const ApproxSlot sl = slot < a.n_inline ? a.islots[slot] : a.slots[slot];
     const uint32_t ng = sl.count, C = a.C;  // C == 8 * S
     float* qs = slab + (size_t)D * S;          // [ng][G][D] member queries
-    // partial dot products [8][NT] (fp64) during scoring; the same bytes hold
-    // the candidate rows of the exact re-scoring later
-    double (*red)[NT] = reinterpret_cast<double (*)[NT]>(qs + (size_t)kSlotGroups * a.G * D);
+    // partial dot products [8][NT] during scoring; the same bytes hold the
+    // candidate rows of the re-scoring later
+    float (*red)[NT] = reinterpret_cast<float (*)[NT]>(qs + (size_t)kSlotGroups * a.G * D);
     const bool own = rank < ng;
     const uint32_t g = own ? sl.group[rank] : 0u;
     // ---- loads, all in one round trip: the slice rows and the member query
@@ -925,37 +919,39 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     }
     mbar_wait(&bar, 0);
     // pooled_j = sum_i q_ij in fp64, rows in order   attention.cpp:289-295
-    for (uint32_t e = tid; e < ng * D; e += NT) {
+    // (rows of absent members are zero: the scoring below runs every chain)
+    for (uint32_t e = tid; e < kSlotGroups * D; e += NT) {
         const uint32_t k = e / D, j = e % D;
-        const double ps = pooled_sum(qs + (size_t)k * a.G * D + j, a.G, D);
-        pf[k][j] = ps;
+        const double ps = k < ng ? pooled_sum(qs + (size_t)k * a.G * D + j, a.G, D) : 0.0;
+        pf[k][j] = (float)ps;
         if (k == rank) pd[j] = ps;
     }
     __syncthreads();
     trace(0);
-    // ---- fp32 scores of this CTA's slice for every member, to the owners
-    // the slice column stays in registers; pooled rows are float4 broadcasts
-    // (shared-memory traffic ~1/4 of an FMA each)
+    // ---- f32 scores of this CTA's slice for every member, to the owners
+    // the slice column stays in registers; pooled rows are float4 broadcasts.
+    // f32 FMA chains (4x the fp64 rate): the candidate band below holds more
+    // than the l winners only when a score lies within ~1e-5 |p| cmax of the
+    // boundary; those contexts are re-scored in fp64 (and exactly if needed)
     const uint32_t cl = tid % S, part = tid / S;
     float cv[DPT];
 #pragma unroll
     for (int jj = 0; jj < (int)DPT; ++jj) cv[jj] = slab[(part * DPT + jj) * S + cl];
     // the slot's contexts are independent accumulation chains (ILP)
-    // fp64 FMA chains: |approx - reference| ~ 1e-14 relative, so the
-    // candidate band below almost never holds more than the l winners
-    double x[kSlotGroups];
+    float x[kSlotGroups];
 #pragma unroll
-    for (int k = 0; k < kSlotGroups; ++k) x[k] = 0.0;
+    for (int k = 0; k < kSlotGroups; ++k) x[k] = 0.f;
 #pragma unroll
-    for (int j2 = 0; j2 < (int)DPT / 2; ++j2) {
-        const double c0 = (double)cv[2 * j2], c1 = (double)cv[2 * j2 + 1];
+    for (int j4 = 0; j4 < (int)DPT / 4; ++j4) {
+        float4 p4[kSlotGroups];
+#pragma unroll
+        for (int k = 0; k < kSlotGroups; ++k) p4[k] = reinterpret_cast<const float4*>(&pf[k][part * DPT])[j4];
 #pragma unroll
         for (int k = 0; k < kSlotGroups; ++k) {
-            if ((uint32_t)k < ng) {
-                const double2 p2 = reinterpret_cast<const double2*>(&pf[k][part * DPT])[j2];
-                x[k] = fma(p2.x, c0, x[k]);
-                x[k] = fma(p2.y, c1, x[k]);
-            }
+            x[k] = fmaf(p4[k].x, cv[4 * j4], x[k]);
+            x[k] = fmaf(p4[k].y, cv[4 * j4 + 1], x[k]);
+            x[k] = fmaf(p4[k].z, cv[4 * j4 + 2], x[k]);
+            x[k] = fmaf(p4[k].w, cv[4 * j4 + 3], x[k]);
         }
     }
 #pragma unroll
@@ -965,18 +961,18 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     trace(6);
     for (uint32_t e = tid; e < ng * S; e += NT) {
         const uint32_t k = e / S, cc = e % S;
-        double x = 0.0;
+        float x = 0.f;
         for (uint32_t p = 0; p < TPC; ++p) x += red[k][p * S + cc];
-        dsmem_st_f64(&sc_all[rank * S + cc], k, x);
+        dsmem_st_f32(&sc_all[rank * S + cc], k, x);
     }
     trace(7);
-    cluster_sync_all();  // every owner now holds all C scores of its context
+    // every owner now holds all C scores of its context; no distributed
+    // shared memory is touched after this barrier, so each CTA leaves as soon
+    // as it is done (its SM goes to a decode CTA)
+    cluster_sync_all();
     trace(1);
     if (a.trace && tid == 0) a.trace[16 + 6 * blockIdx.x + 1] = gt();
     if (!own) {
-        // the owners may still read this CTA's slice (exact re-scoring)
-        cluster_arrive();
-        cluster_wait();
         if (tid == 0) tl_mark(a.tl, 1, false);
         return;
     }
@@ -1148,13 +1144,14 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
         const double t_l = s_tl;
         double n2 = 0.0;
         for (uint32_t w = 0; w < NT / 32; ++w) n2 += s_n2[w];
-        // |approx - exact| <= B: the pooled query is the reference's fp64 sum
-        // exactly; the approximate dot (FMA chains of DPT terms, TPC partial
-        // sums) and the reference's sequential chain (D products, D sums)
-        // each lie within gamma_n sum|p_j c_j| of the real dot product,
-        // sum|p_j c_j| <= |p|_2 max|c|_2, u = 2^-53; the band is 2B, widened 2x
-        const double B2 = 2.0 * 2.0 * (double)(DPT + TPC + 2 * D + 2) * 0x1p-53 * sqrt(n2) *
-                          (double)a.cmax[g] * 1.01;
+        // |approx - exact| <= B: the approximate dot (f32 FMA chains of DPT
+        // terms over the f32-rounded pooled query, TPC partial sums in f32)
+        // and the reference's sequential fp64 chain of the fp64 pooled query
+        // (D products, D sums) each lie within gamma_n sum|p_j c_j| of the
+        // real dot product (u = 2^-24 and 2^-53), sum|p_j c_j| <= |p|_2
+        // max|c|_2; the band is 2B, widened 2x
+        const double pc = sqrt(n2) * (double)a.cmax[g];
+        const double B2 = 2.0 * 2.0 * ((double)(DPT + TPC + 2) * 0x1p-24 + (double)(2 * D + 2) * 0x1p-53) * pc * 1.01;
         if (tid == 0) s_ncand = 0;
         __syncthreads();
 #pragma unroll
@@ -1176,45 +1173,74 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
         if (a.selected == nullptr && nS == L && L <= kMaxCand) {
             if (tid < L) sel[tid] = cand_id[tid];
         } else if (nS <= kMaxCand) {
-            // exact fp64 chains (attention.cpp:296-304: mul rounded before add)
-            // over the candidates' centroid rows, gathered from the cluster's
-            // slices in distributed shared memory (candidate c lives in CTA
-            // c / S, column c % S of its transposed slice): no global round
-            // trip behind the decode's HBM traffic
-            // (every load in flight before the first store)
-            float* crow = qs + (size_t)kSlotGroups * a.G * D;  // [nS][D + 1]
-            constexpr uint32_t PE = (kMaxCand * D + NT - 1) / NT;
-            float tv[PE];
-#pragma unroll
-            for (uint32_t i = 0; i < PE; ++i) {
-                const uint32_t e = tid + i * NT;
-                if (e < nS * D) {
-                    const uint32_t cc = cand_id[e % nS];
-                    tv[i] = dsmem_ld_f32(slab + (size_t)(e / nS) * S + cc % S, cc / S);
-                }
-            }
-#pragma unroll
-            for (uint32_t i = 0; i < PE; ++i) {
-                const uint32_t e = tid + i * NT;
-                if (e < nS * D) crow[(e % nS) * (D + 1) + e / nS] = tv[i];
-            }
-            __syncthreads();
-            if (a.trace && tid == 0) a.trace[16 + 6 * blockIdx.x + 5] = gt();
-            double ex = -INFINITY;
-            uint32_t eid = 0xFFFFFFFFu;
-            if (tid < nS) {
-                const float* row = crow + tid * (D + 1);
+            // the candidates' centroid rows come from global memory (row-major,
+            // L2-resident; one round trip with every load in flight).
+            // First an fp64 FMA re-scoring (TPR threads per candidate): its
+            // band (~1e-14 |p| cmax) almost always holds exactly the l winners
+            const float* cR = a.centR[g];
+            bool done = false;
+            if (a.selected == nullptr) {
+                constexpr uint32_t TPR = NT / kMaxCand, DPR = D / TPR;
+                static_assert(NT % kMaxCand == 0 && D % (4 * TPR) == 0 && TPR <= 32, "re-scoring geometry");
+                const uint32_t ci = tid / TPR, pr = tid % TPR;
                 double sx = 0.0;
+                if (ci < nS) {
+                    const float4* row = reinterpret_cast<const float4*>(cR + (size_t)cand_id[ci] * D + pr * DPR);
+                    float4 v[DPR / 4];
+#pragma unroll
+                    for (uint32_t i = 0; i < DPR / 4; ++i) v[i] = __ldg(row + i);
+                    const double* pp = pd + pr * DPR;
+#pragma unroll
+                    for (uint32_t i = 0; i < DPR / 4; ++i) {
+                        sx = fma(pp[4 * i], (double)v[i].x, sx);
+                        sx = fma(pp[4 * i + 1], (double)v[i].y, sx);
+                        sx = fma(pp[4 * i + 2], (double)v[i].z, sx);
+                        sx = fma(pp[4 * i + 3], (double)v[i].w, sx);
+                    }
+                }
+#pragma unroll
+                for (uint32_t o = 1; o < TPR; o <<= 1) sx += __shfl_xor_sync(0xFFFFFFFFu, sx, o);
+                if (pr == 0 && ci < nS) xs[ci] = sx;
+                if (tid == 0) s_nb = 0;
+                __syncthreads();
+                if (a.trace && tid == 0) a.trace[16 + 6 * blockIdx.x + 5] = gt();
+                if (tid < nS) {  // the l-th largest fp64 score, by rank
+                    const double v = xs[tid];
+                    uint32_t r = 0;
 #pragma unroll 8
-                for (uint32_t j = 0; j < D; ++j) sx = __dadd_rn(sx, __dmul_rn(pd[j], (double)row[j]));
-                ex = sx;
-                eid = cand_id[tid];
+                    for (uint32_t k = 0; k < nS; ++k) {
+                        const double u = xs[k];
+                        r += (u > v || (u == v && k < tid)) ? 1u : 0u;
+                    }
+                    if (r == L - 1) s_tl = v;
+                }
+                __syncthreads();
+                const double B64 = 2.0 * 2.0 * (double)(DPR + TPR + 2 * D + 2) * 0x1p-53 * pc * 1.01;
+                if (tid < nS && xs[tid] >= s_tl - B64) xi[atomicAdd(&s_nb, 1u)] = cand_id[tid];
+                __syncthreads();
+                done = s_nb == L;
+                if (done && tid < L) sel[tid] = xi[tid];
+                __syncthreads();
             }
-            uint32_t p2s = 1;
-            while (p2s < nS) p2s <<= 1;
-            bitonic_regs(ex, eid, p2s, xs, xi);  // (score desc, id asc): attention.cpp:263-268
-            __syncthreads();
-            if (tid < L) sel[tid] = eid;
+            if (!done) {
+                // exact fp64 chains (attention.cpp:296-304: mul rounded before
+                // add), ordered (score desc, id asc): attention.cpp:263-268
+                double ex = -INFINITY;
+                uint32_t eid = 0xFFFFFFFFu;
+                if (tid < nS) {
+                    const float* row = cR + (size_t)cand_id[tid] * D;
+                    double sx = 0.0;
+#pragma unroll 8
+                    for (uint32_t j = 0; j < D; ++j) sx = __dadd_rn(sx, __dmul_rn(pd[j], (double)__ldg(row + j)));
+                    ex = sx;
+                    eid = cand_id[tid];
+                }
+                uint32_t p2s = 1;
+                while (p2s < nS) p2s <<= 1;
+                bitonic_regs(ex, eid, p2s, xs, xi);
+                __syncthreads();
+                if (tid < L) sel[tid] = eid;
+            }
         } else {
             // degenerate (many near-ties): exact chains for every candidate
             uint32_t P2 = 1;
@@ -1245,14 +1271,12 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
             a.trace[16 + 6 * blockIdx.x + 4] = nS;
         }
     }
-    // this CTA reads no remote slice from here on; it leaves only once every
-    // CTA of the cluster is past its reads of this CTA's slice
-    cluster_arrive();
     // ---- plan: warp 0 lays the bucket segments out as 8-aligned virtual rows
     // and reserves the context's tiles; every thread then writes tile records
     const uint32_t nh = a.n_hchunks;
     const uint32_t rb0 = fallback ? 0 : n - a.recent;  // == T (recent == the layer's hint)
     __shared__ uint32_t s_tile0, s_ntiles;
+    unsigned long long res = 0;  // warp 0 lane 0: the pending tile reservation
     if (tid < 32) {
         unsigned long long keys = 0;
         uint32_t mx = 0, vrows = 0;
@@ -1286,7 +1310,9 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
         }
         const uint32_t ntiles = (vrows + kTileRows - 1) / kTileRows;
         if (lane == 0) {
-            s_tile0 = (uint32_t)atomicAdd(&a.ctr->dynres, (1ull << 32) | (unsigned long long)(ntiles * nh));
+            // the reservation travels while the records are built (its
+            // result is read only after emit_tiles)
+            res = atomicAdd(&a.ctr->dynres, (1ull << 32) | (unsigned long long)(ntiles * nh));
             s_ntiles = ntiles;
             for (uint32_t hc = 0; hc < nh; ++hc) a.dyn_cnt[g * nh + hc] = ntiles | kCntValid;
             saap_attn_stats stt;
@@ -1299,10 +1325,25 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
     }
     (void)T;
     __syncthreads();
-    const uint32_t ntiles = s_ntiles, tile0 = s_tile0;
+    const uint32_t ntiles = s_ntiles;
+    // records are built in shared memory (the centroid slice is no longer
+    // read) and copied out once the reservation is back
+    TileRec* stage = reinterpret_cast<TileRec*>(slab);
+    const bool staged = ntiles * nh <= (uint32_t)((size_t)D * S * 4 / sizeof(TileRec));
+    if (ntiles && staged) emit_tiles(stage, ntiles, nh, g * nh, segs, vpre, L, gm.row_base, tid, NT);
+    if (tid == 0) s_tile0 = (uint32_t)res;
+    __syncthreads();
+    const uint32_t tile0 = s_tile0;
     trace(8);
     if (ntiles) {
-        emit_tiles(a.dyn_tiles + tile0, ntiles, nh, g * nh, segs, vpre, L, gm.row_base, tid, NT);
+        if (staged) {
+            constexpr uint32_t W16 = sizeof(TileRec) / 16;
+            const uint4* src = reinterpret_cast<const uint4*>(stage);
+            uint4* dst = reinterpret_cast<uint4*>(a.dyn_tiles + tile0);
+            for (uint32_t e = tid; e < ntiles * nh * W16; e += NT) dst[e] = src[e];
+        } else {
+            emit_tiles(a.dyn_tiles + tile0, ntiles, nh, g * nh, segs, vpre, L, gm.row_base, tid, NT);
+        }
         // every thread orders its own records; the barrier makes them all
         // precede every ready flag
         __threadfence();
@@ -1320,7 +1361,6 @@ __global__ void __launch_bounds__(kClusterThreads) route_cluster_kernel(ClusterR
         if (a.trace) a.trace[16 + 6 * blockIdx.x + 3] = gt();
     }
     trace(5);
-    cluster_wait();
 }
 
 // ============================================================ attention
@@ -1557,9 +1597,13 @@ __global__ void __maxnreg__(144)
         const uint32_t pre = min(W, P * CS);  // tiles of the pre-assigned first chunks
         uint32_t total = a.n_plan_groups ? 0xFFFFFFFFu : W;  // stream length once final
         uint32_t known = W;                                  // W + reserved dynamic tiles
+        // (shared counters are read by lane 0 and broadcast: every lane must
+        // see the same stream length and claim size, whatever their timing)
         auto refresh = [&]() {
             if (total != 0xFFFFFFFFu) return;
-            const unsigned long long dr = ld_acquire_u64(&a.ctr->dynres);
+            unsigned long long dr = 0;
+            if (lane == 0) dr = ld_acquire_u64(&a.ctr->dynres);
+            dr = __shfl_sync(0xFFFFFFFFu, dr, 0);
             known = W + (uint32_t)dr;
             if ((uint32_t)(dr >> 32) >= a.n_plan_groups) total = known;
         };
@@ -1570,7 +1614,9 @@ __global__ void __maxnreg__(144)
         // barrier orders them before lane 0's (async-proxy) record copies
         auto dyn_ready = [&](uint32_t b0, uint32_t b1) -> bool {
             if (all_pub) return true;
-            if (ld_acquire_u32(&a.ctr->published) >= a.n_plan_groups) {
+            uint32_t pub = 0;
+            if (lane == 0) pub = ld_acquire_u32(&a.ctr->published);
+            if (__shfl_sync(0xFFFFFFFFu, pub, 0) >= a.n_plan_groups) {
                 all_pub = true;
                 __syncwarp();
                 return true;
@@ -1582,8 +1628,14 @@ __global__ void __maxnreg__(144)
             __syncwarp();
             return all;
         };
-        // claims: [pre + returned, + size)
+        // claims: [pre + returned, + size).  A claim is issued late -- when
+        // claim_lead tiles of the current chunk are left to issue -- so a CTA
+        // never holds more than about one chunk beyond its ring: at the
+        // stream's end no CTA sits on tiles while the others run dry.  Its
+        // atomic travels while those tiles are issued (the result register is
+        // read only when the next chunk's records are fetched).
         uint32_t cl_ret = 0, cl_size = 0, hint = pre;
+        bool cl_pend = false;
         auto claim = [&]() {
             uint32_t sz = CH;
             if (total != 0xFFFFFFFFu) {
@@ -1595,8 +1647,9 @@ __global__ void __maxnreg__(144)
             }
             if (lane == 0) cl_ret = atomicAdd(&a.ctr->tickets, sz);
             cl_size = sz;
+            cl_pend = true;
         };
-        bool first = true, claimed = false;
+        bool first = true;
         if (a.dtrace && lane == 0) a.dtrace[16 * blockIdx.x + 12] = gtime();
         uint32_t pc0 = 0, pc1 = 0;  // the current chunk's remaining tiles
         bool pend = false, feeding = true;
@@ -1614,10 +1667,9 @@ __global__ void __maxnreg__(144)
                     b0 = blockIdx.x * CS;
                     b1 = min(pre, b0 + CS);
                 } else {
-                    if (!claimed) {
+                    if (!cl_pend) {
                         refresh();
                         claim();
-                        claimed = true;
                     }
                     b0 = pre + __shfl_sync(0xFFFFFFFFu, cl_ret, 0);
                     b1 = b0 + cl_size;
@@ -1633,7 +1685,7 @@ __global__ void __maxnreg__(144)
                     }
                     if (b1 > W && !dyn_ready(b0, b1)) return false;
                     hint = b1;
-                    claim();  // the next claim travels while this chunk is issued
+                    cl_pend = false;
                 }
                 first = false;
                 // acquired generic-proxy data (records, gathered rows) is read by
@@ -1683,8 +1735,9 @@ __global__ void __maxnreg__(144)
         }
         while (cur ? u_cnt1 : u_cnt0) {
             const int nx = cur ^ 1;
-            // the next unit travels while this one is issued
-            bool have_next = fetch_unit(nx);
+            // the next unit's records are fetched (and the chunk after this
+            // one claimed) while this unit's last tiles are issued
+            bool have_next = false;
             mbar_wait(&s.urec_bar[cur], (u_ph >> cur) & 1u);
             u_ph ^= 1u << cur;
             if (a.dtrace && lane == 0 && a.dtrace[16 * blockIdx.x + 10] == 0) a.dtrace[16 * blockIdx.x + 10] = gtime();
@@ -1711,6 +1764,12 @@ __global__ void __maxnreg__(144)
                 ++run_tiles;
                 if (lane == 0) {
                     const unsigned long long tw = clock64();
+                    if (a.inflight && a.inflight < (uint32_t)CF::NS && p_tiles >= a.inflight) {
+                        // at most `inflight` tiles loading or unconsumed: wait for tile
+                        // p_tiles - inflight (its stage's (j / NS)-th completion)
+                        const uint32_t j = p_tiles - a.inflight;
+                        mbar_wait(&s.empty[j % CF::NS], (j / CF::NS) & 1u);
+                    }
                     mbar_wait(&s.empty[stage], phase ^ 1);
                     p_wait += clock64() - tw;
                     pstamp(7);
@@ -1720,7 +1779,7 @@ __global__ void __maxnreg__(144)
                     const uint32_t flags = (run_first ? 1u : 0u) | (last_of_run ? 2u : 0u) | (nq << 8);
                     const uint32_t qoff = (uint32_t)(((size_t)g * a.G + hc * kHeadsPerSlot) * D);
                     s.meta[stage] = make_int4((int)qslot, (int)flags, (int)qoff, (int)run_tiles);
-                    const uint32_t bytes = R.rows8 * (uint32_t)CF::RB * 2u;
+                    const uint32_t bytes = a.debug_skip == 2 ? 0u : R.rows8 * (uint32_t)CF::RB * 2u;
                     mbar_arrive_expect_tx(&s.full[stage], bytes);
                 }
                 __syncwarp();
@@ -1733,7 +1792,7 @@ __global__ void __maxnreg__(144)
                     if ((uint32_t)lane * 32u < nq * D)
                         asm volatile("prefetch.global.L1 [%0];" ::"l"(qb + lane * 32) : "memory");
                 }
-                if (len) {
+                if (len && a.debug_skip != 2) {
                     // one request per piece for K and one for V: a box of r8/8 groups
                     // when the rounded-up rows exist; else the piece's whole groups
                     // plus a bounds-checked 8-row box (zero fill past the end)
@@ -1770,6 +1829,16 @@ __global__ void __maxnreg__(144)
                 }
                 run_first = last_of_run;
                 if (last_of_run) run_tiles = 0;
+                __syncwarp();
+                if (!have_next && feeding) {
+                    const uint32_t left = ucnt - 1 - i;  // tiles of this unit still to issue
+                    // (pend: the chunk has units after this one -- no claim yet)
+                    if (!pend && !cl_pend && left <= a.claim_lead) {
+                        refresh();
+                        claim();
+                    }
+                    if (left <= a.fetch_lead) have_next = fetch_unit(nx);
+                }
             }
             if (cur) u_cnt1 = 0;
             else u_cnt0 = 0;
@@ -1886,7 +1955,7 @@ __global__ void __maxnreg__(144)
         if (a.dtiles && threadIdx.x == 0 && n_tiles_done - 1 < (uint32_t)kTraceTiles)
             a.dtiles[((size_t)blockIdx.x * kTraceTiles + n_tiles_done - 1) * 8 + 4] = gtime();
         const uint32_t vbits = ((&s.valid[stage].x)[warp >> 1] >> ((warp & 1) * 16)) & 0xFFFFu;
-        if (vbits && !a.debug_skip) {
+        if (vbits && a.debug_skip != 1) {
             // ---- S = [q1; q2; q3] K^T for this warp's 16 rows
             const uint32_t kbase = smem_u32(&s.K[stage][0]);
             float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
@@ -2238,7 +2307,7 @@ void launch_route_cluster(int D, const ClusterRouteArgs& a, uint32_t n_slots, cu
     cfg.attrs = at;
     cfg.numAttrs = 1;
     // dynamic smem: centroid slice [D][C/8] + member queries [8][G][D] (f32)
-    // + partial dots [8][512] (f64) / candidate rows [64][D + 1] (f32)
+    // + partial dots [8][512] (f32; sized for f64)
     cfg.dynamicSmemBytes = ((size_t)D * (a.C / kClusterCtas) + (size_t)kSlotGroups * a.G * D) * 4 +
                            std::max<size_t>((size_t)64 * (D + 1) * 4, (size_t)kSlotGroups * kClusterThreads * 8);
     if (cfg.dynamicSmemBytes > 160 * 1024) fail(SAAP_ERR_UNSUPPORTED, "route: slice too large");
