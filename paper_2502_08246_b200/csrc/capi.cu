@@ -20,7 +20,7 @@ void launch_route_cluster(int D, const ClusterRouteArgs& a, uint32_t n_slots, cu
 bool route_cluster_supported(int D, uint32_t C);
 void launch_route_approx(int D, const ApproxArgs& a, uint32_t n_slots, cudaStream_t st);
 void launch_route_score(const RouteArgs& a, uint32_t n_groups, cudaStream_t st);
-void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st);
+void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st, bool tc);
 void launch_combine(int D, const CombineArgs& ca, uint32_t n_qslots, cudaStream_t st);
 void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st, uint32_t n_slots = 0);
 void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t n_tiles,
@@ -709,7 +709,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
         da.dtrace = (unsigned long long*)ensure(c, c->dtrace, (size_t)c->sm_count * (128 + kTraceTiles * 64));
         da.dtiles = da.dtrace + (size_t)c->sm_count * 16;
     }
-    launch_decode((int)D, *src.maps, da, grid, st);
+    launch_decode((int)D, *src.maps, da, grid, st, c->opt.decode_tc != 0);
     CombineArgs ca{};
     ca.st_cnt = sp->cnt;
     ca.dyn_cnt = dcnt;
@@ -952,6 +952,7 @@ int saap_ctx_set_option(saap_ctx* c, const char* name, int64_t value) {
         else if (n == "claim_lead") o.claim_lead = clamp(0, 32);
         else if (n == "fetch_lead") o.fetch_lead = clamp(0, 32);
         else if (n == "inflight") o.inflight = clamp(0, 8);
+        else if (n == "decode_tc") o.decode_tc = clamp(0, 1);
         else if (n == "host_graph") o.host_graph = clamp(0, 1);
         else if (n == "trace_decode") o.trace_decode = clamp(0, 1);
         else if (n == "trace_plan") o.trace_plan = clamp(0, 1);

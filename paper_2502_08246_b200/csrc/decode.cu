@@ -1389,6 +1389,7 @@ constexpr int kUnit = 8;  // work records per bulk copy (two units in flight)
 template <int D>
 struct DecodeSmem {
     using CF = DecodeCfg<D>;
+    static constexpr bool kPostQ = false;
     uint8_t K[CF::NS][CF::TILE_BYTES];
     uint8_t V[CF::NS][CF::TILE_BYTES];
     // the run's A fragments (3-term bf16 split of its f32 queries), built once per run by
@@ -1473,6 +1474,327 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 __device__ __forceinline__ float bf16_round(float x) {
     return __uint_as_float((uint32_t)f32_to_bf16_rne(x) << 16);
+}
+
+// The decode producer warp (shared by the mma.sync and tcgen05 decode
+// kernels): claims work-stream chunks, fetches their records and issues the
+// K/V tile loads into the stage ring of `s` (full/empty barriers, meta,
+// valid, urec).
+template <int D, class SM>
+__device__ __forceinline__ void decode_producer(const DecodeArgs& a, const DecodeMaps& maps, SM& s,
+                                                int lane) {
+    using CF = DecodeCfg<D>;
+    auto gtime = []() {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        return t;
+    };
+    // ------------------------------------------------ producer
+    // Work stream: [static tiles | dynamic tiles].  Guided self-scheduling
+    // over one tile counter: CTA b first takes static tiles
+    // [b*CS, (b+1)*CS) without an atomic, then claims chunks from the
+    // counter whose size shrinks with the remaining work once the stream
+    // length is final (ceil(rem / 2P), capped at `chunk`), so no CTA holds
+    // a large chunk when the others run dry.  A claim is issued one chunk
+    // ahead (its atomic travels while the current chunk is issued).
+    // A chunk's records arrive in units of up to kUnit consecutive records,
+    // one bulk copy each, double-buffered.  Each record carries its byte
+    // count and row mask (tile_finish), so issuing a tile is a stage wait,
+    // one expect_tx and one TMA request per piece for K and V.
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.map[lane]) : "memory");
+    const uint64_t pol = l2_evict_first_policy();
+    const uint32_t W = a.n_static, CH = a.chunk;
+    const uint32_t CS = a.chunk_st, P = gridDim.x;
+    const uint32_t pre = min(W, P * CS);  // tiles of the pre-assigned first chunks
+    uint32_t total = a.n_plan_groups ? 0xFFFFFFFFu : W;  // stream length once final
+    uint32_t known = W;                                  // W + reserved dynamic tiles
+    // (shared counters are read by lane 0 and broadcast: every lane must
+    // see the same stream length and claim size, whatever their timing)
+    auto refresh = [&]() {
+        if (total != 0xFFFFFFFFu) return;
+        unsigned long long dr = 0;
+        if (lane == 0) dr = ld_acquire_u64(&a.ctr->dynres);
+        dr = __shfl_sync(0xFFFFFFFFu, dr, 0);
+        known = W + (uint32_t)dr;
+        if ((uint32_t)(dr >> 32) >= a.n_plan_groups) total = known;
+    };
+    bool all_pub = a.n_plan_groups == 0;
+    // dynamic records are published with release stores: once every
+    // planner CTA reported (one acquire) no per-record check is needed;
+    // before that every lane acquires one flag of the chunk, and the warp
+    // barrier orders them before lane 0's (async-proxy) record copies
+    auto dyn_ready = [&](uint32_t b0, uint32_t b1) -> bool {
+        if (all_pub) return true;
+        uint32_t pub = 0;
+        if (lane == 0) pub = ld_acquire_u32(&a.ctr->published);
+        if (__shfl_sync(0xFFFFFFFFu, pub, 0) >= a.n_plan_groups) {
+            all_pub = true;
+            __syncwarp();
+            return true;
+        }
+        bool ok = true;
+        const uint32_t i = max(b0, W) + lane;
+        if (i < b1) ok = ld_acquire_u32(&a.dyn_tiles[i - W].ready) != 0;
+        const bool all = __all_sync(0xFFFFFFFFu, ok);
+        __syncwarp();
+        return all;
+    };
+    // claims: [pre + returned, + size).  A claim is issued late -- when
+    // claim_lead tiles of the current chunk are left to issue -- so a CTA
+    // never holds more than about one chunk beyond its ring: at the
+    // stream's end no CTA sits on tiles while the others run dry.  Its
+    // atomic travels while those tiles are issued (the result register is
+    // read only when the next chunk's records are fetched).
+    uint32_t cl_ret = 0, cl_size = 0, hint = pre;
+    bool cl_pend = false;
+    auto claim = [&]() {
+        uint32_t sz = CH;
+        if (total != 0xFFFFFFFFu) {
+            // the counter has moved on by about one claim per CTA since
+            // this CTA's last claim returned `hint`
+            const uint32_t seen = hint + P * cl_size;
+            const uint32_t rem = total > seen ? total - seen : 0u;
+            sz = max(min(a.min_chunk, CH), min(CH, (rem + 2 * P - 1) / (2 * P)));
+        }
+        if (lane == 0) cl_ret = atomicAdd(&a.ctr->tickets, sz);
+        cl_size = sz;
+        cl_pend = true;
+    };
+    bool first = true;
+    if (a.dtrace && lane == 0) a.dtrace[16 * blockIdx.x + 12] = gtime();
+    uint32_t pc0 = 0, pc1 = 0;  // the current chunk's remaining tiles
+    bool pend = false, feeding = true;
+    // unit slots 0/1 in registers (selects, no local memory)
+    uint32_t u_cnt0 = 0, u_cnt1 = 0, u_base0 = 0, u_base1 = 0;
+    bool u_last0 = false, u_last1 = false;
+    uint32_t u_ph = 0;  // phase bit per unit slot
+    // next unit of records into `slot`: false when none can be fetched now
+    // (planner behind, or end of stream: feeding = false)
+    auto fetch_unit = [&](int slot) -> bool {
+        if (!feeding) return false;
+        if (!pend) {
+            uint32_t b0 = 0, b1 = 0;
+            if (first && blockIdx.x * CS < pre) {
+                b0 = blockIdx.x * CS;
+                b1 = min(pre, b0 + CS);
+            } else {
+                if (!cl_pend) {
+                    refresh();
+                    claim();
+                }
+                b0 = pre + __shfl_sync(0xFFFFFFFFu, cl_ret, 0);
+                b1 = b0 + cl_size;
+                refresh();
+                if (total != 0xFFFFFFFFu) {
+                    if (b0 >= total) {
+                        feeding = false;
+                        return false;
+                    }
+                    b1 = min(b1, total);
+                } else if (b1 > known) {
+                    return false;  // not reserved by the planner yet
+                }
+                if (b1 > W && !dyn_ready(b0, b1)) return false;
+                hint = b1;
+                cl_pend = false;
+            }
+            first = false;
+            // acquired generic-proxy data (records, gathered rows) is read by
+            // the bulk and tensor copies (async proxy)
+            if (b1 > W) asm volatile("fence.proxy.async.global;" ::: "memory");
+            pc0 = b0;
+            pc1 = b1;
+            pend = true;
+        }
+        // a unit stays in one record array (static | dynamic)
+        const uint32_t n = min(min(pc1 - pc0, (uint32_t)kUnit), pc0 < W ? W - pc0 : 0xFFFFFFFFu);
+        if (lane == 0) {
+            if (a.dtrace && a.dtrace[16 * blockIdx.x + 13] == 0) a.dtrace[16 * blockIdx.x + 13] = gtime();
+            const TileRec* src = pc0 < W ? a.st_tiles + pc0 : a.dyn_tiles + (pc0 - W);
+            mbar_arrive_expect_tx(&s.urec_bar[slot], n * (uint32_t)sizeof(TileRec));
+            bulk_g2s(&s.urec[slot][0], src, n * (uint32_t)sizeof(TileRec), &s.urec_bar[slot]);
+        }
+        __syncwarp();
+        if (slot) {
+            u_cnt1 = n;
+            u_base1 = pc0;
+            u_last1 = pc0 + n == pc1;
+        } else {
+            u_cnt0 = n;
+            u_base0 = pc0;
+            u_last0 = pc0 + n == pc1;
+        }
+        pc0 += n;
+        if (pc0 == pc1) pend = false;
+        return true;
+    };
+    uint32_t stage = 0, phase = 0;
+    bool run_first = true;
+    uint32_t run_tiles = 0;
+    unsigned long long p_wait = 0, p_sleep = 0;
+    const unsigned long long p_t0 = clock64();
+    uint32_t p_tiles = 0;
+    auto pstamp = [&](int k) {
+        if (a.dtiles && lane == 0 && p_tiles < (uint32_t)kTraceTiles)
+            a.dtiles[((size_t)blockIdx.x * kTraceTiles + p_tiles) * 8 + k] = gtime();
+    };
+    int cur = 0;
+    while (!fetch_unit(cur) && feeding) {  // the first unit (the planner may be behind)
+        const unsigned long long ts = clock64();
+        __nanosleep(a.poll_ns);
+        p_sleep += clock64() - ts;
+    }
+    while (cur ? u_cnt1 : u_cnt0) {
+        const int nx = cur ^ 1;
+        // the next unit's records are fetched (and the chunk after this
+        // one claimed) while this unit's last tiles are issued
+        bool have_next = false;
+        mbar_wait(&s.urec_bar[cur], (u_ph >> cur) & 1u);
+        u_ph ^= 1u << cur;
+        if (a.dtrace && lane == 0 && a.dtrace[16 * blockIdx.x + 10] == 0) a.dtrace[16 * blockIdx.x + 10] = gtime();
+        const uint32_t ucnt = cur ? u_cnt1 : u_cnt0, ubase = cur ? u_base1 : u_base0;
+        const bool ulast = cur ? u_last1 : u_last0;
+        // dynamic records are re-armed for the next step once copied
+        if (ubase >= W && (uint32_t)lane < ucnt) a.dyn_tiles[ubase - W + lane].ready = 0;
+        for (uint32_t i = 0; i < ucnt; ++i) {
+            pstamp(3);
+            const TileRec& R = s.urec[cur][i];
+            const uint4 hdr = *reinterpret_cast<const uint4*>(&R);
+            const uint32_t np = hdr.x, qslot = hdr.y;
+            const bool last_in_chunk = ulast && i + 1 == ucnt;
+            const bool last_of_run = last_in_chunk || hdr.w != 0;
+            uint32_t len = 0, srow = 0, gat = 0;
+            uint64_t row = 0;
+            if ((uint32_t)lane < np) {
+                const uint4 v = *reinterpret_cast<const uint4*>(&R.p[lane]);
+                len = v.x & ~kPieceGather;
+                gat = v.x & kPieceGather;
+                srow = v.y;
+                row = ((uint64_t)v.w << 32) | v.z;
+            }
+            ++run_tiles;
+            if (lane == 0) {
+                const unsigned long long tw = clock64();
+                if (a.inflight && a.inflight < (uint32_t)CF::NS && p_tiles >= a.inflight) {
+                    // at most `inflight` tiles loading or unconsumed: wait for tile
+                    // p_tiles - inflight (its stage's (j / NS)-th completion)
+                    const uint32_t j = p_tiles - a.inflight;
+                    mbar_wait(&s.empty[j % CF::NS], (j / CF::NS) & 1u);
+                }
+                mbar_wait(&s.empty[stage], phase ^ 1);
+                p_wait += clock64() - tw;
+                pstamp(7);
+                s.valid[stage] = *reinterpret_cast<const uint4*>(&R.valid[0]);
+                const uint32_t g = qslot / a.n_hchunks, hc = qslot - g * a.n_hchunks;
+                const uint32_t nq = min((uint32_t)kHeadsPerSlot, a.G - hc * kHeadsPerSlot);
+                const uint32_t flags = (run_first ? 1u : 0u) | (last_of_run ? 2u : 0u) | (nq << 8);
+                const uint32_t qoff = (uint32_t)(((size_t)g * a.G + hc * kHeadsPerSlot) * D);
+                s.meta[stage] = make_int4((int)qslot, (int)flags, (int)qoff, (int)run_tiles);
+                const uint32_t bytes = a.debug_skip == 2 ? 0u : R.rows8 * (uint32_t)CF::RB * 2u;
+                mbar_arrive_expect_tx(&s.full[stage], bytes);
+            }
+            __syncwarp();
+            if (run_first) {
+                // the run's query rows (<= 2 KB) into this SM's L1 ahead of the
+                // consumers' fragment build (no shared-memory staging)
+                const uint32_t g = qslot / a.n_hchunks, hc = qslot - g * a.n_hchunks;
+                const uint32_t nq = min((uint32_t)kHeadsPerSlot, a.G - hc * kHeadsPerSlot);
+                const float* qb = a.q + ((size_t)g * a.G + hc * kHeadsPerSlot) * D;
+                if ((uint32_t)lane * 32u < nq * D)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(qb + lane * 32) : "memory");
+                if constexpr (SM::kPostQ) {  // the Q warp builds the run's B operand now
+                    if (lane == 0) {
+                        const uint32_t r = s.n_qreq++, qbi = r & 1;
+                        mbar_wait(&s.q_req_empty[qbi], ((r >> 1) & 1) ^ 1);
+                        s.qreq_off[qbi] = (uint32_t)(((size_t)g * a.G + hc * kHeadsPerSlot) * D);
+                        s.qreq_nq[qbi] = nq;
+                        mbar_arrive(&s.q_req[qbi]);
+                    }
+                }
+            }
+            if (len && a.debug_skip != 2) {
+                // one request per piece for K and one for V: a box of r8/8 groups
+                // when the rounded-up rows exist; else the piece's whole groups
+                // plus a bounds-checked 8-row box (zero fill past the end)
+                const uint32_t r8 = (len + 7) & ~7u;
+                const CUtensorMap* mk = &maps.map[(gat ? 2 : 0) * kBoxSizes];
+                const CUtensorMap* mv = mk + kBoxSizes;
+                const uint64_t lim = gat ? maps.grows : maps.rows;
+                const uint32_t off = (srow >> 3) * 8 * CF::RB;
+                if (row + r8 <= lim) {
+                    tma4d(&s.K[stage][off], mk + (r8 / 8 - 1), (int)row, &s.full[stage], pol);
+                    tma4d(&s.V[stage][off], mv + (r8 / 8 - 1), (int)row, &s.full[stage], pol);
+                } else {
+                    const uint32_t full = len & ~7u;
+                    if (full) {
+                        tma4d(&s.K[stage][off], mk + (full / 8 - 1), (int)row, &s.full[stage], pol);
+                        tma4d(&s.V[stage][off], mv + (full / 8 - 1), (int)row, &s.full[stage], pol);
+                    }
+                    if (r8 > full) {
+                        const uint32_t off2 = ((srow + full) >> 3) * 8 * CF::RB;
+                        tma4d(&s.K[stage][off2], mk, (int)(row + full), &s.full[stage], pol);
+                        tma4d(&s.V[stage][off2], mv, (int)(row + full), &s.full[stage], pol);
+                    }
+                }
+            }
+            __syncwarp();
+            if (a.dtrace && lane == 0 && a.dtrace[16 * blockIdx.x + 11] == 0) a.dtrace[16 * blockIdx.x + 11] = gtime();
+            if (a.dtiles && lane == 0 && p_tiles < (uint32_t)kTraceTiles)
+                a.dtiles[((size_t)blockIdx.x * kTraceTiles + p_tiles) * 8] =
+                        (gtime() & ~63ull) | np | (last_in_chunk ? 32u : 0u);  // stamp | pieces | chunk end
+            ++p_tiles;
+            if (++stage == CF::NS) {
+                stage = 0;
+                phase ^= 1;
+            }
+            run_first = last_of_run;
+            if (last_of_run) run_tiles = 0;
+            __syncwarp();
+            if (!have_next && feeding) {
+                const uint32_t left = ucnt - 1 - i;  // tiles of this unit still to issue
+                // (pend: the chunk has units after this one -- no claim yet)
+                if (!pend && !cl_pend && left <= a.claim_lead) {
+                    refresh();
+                    claim();
+                }
+                if (left <= a.fetch_lead) have_next = fetch_unit(nx);
+            }
+        }
+        if (cur) u_cnt1 = 0;
+        else u_cnt0 = 0;
+        if (!have_next) {  // fetch now (poll while the planner is behind)
+            while (!fetch_unit(nx) && feeding) {
+                const unsigned long long ts = clock64();
+                __nanosleep(a.poll_ns);
+                p_sleep += clock64() - ts;
+            }
+        }
+        cur = nx;
+    }
+    if (lane == 0) {
+        if (a.dtrace) {
+            a.dtrace[16 * blockIdx.x + 4] = p_wait;
+            a.dtrace[16 * blockIdx.x + 5] = clock64() - p_t0;
+            a.dtrace[16 * blockIdx.x + 14] = p_sleep;
+        }
+        mbar_wait(&s.empty[stage], phase ^ 1);
+        if constexpr (SM::kPostQ) {  // stop the Q warp
+            const uint32_t r = s.n_qreq++, qbi = r & 1;
+            mbar_wait(&s.q_req_empty[qbi], ((r >> 1) & 1) ^ 1);
+            s.qreq_nq[qbi] = 0xFFu;
+            mbar_arrive(&s.q_req[qbi]);
+        }
+        s.meta[stage] = make_int4(-1, 0, 0, 0);
+        mbar_arrive(&s.full[stage]);
+        // the last CTA out re-arms the step counters (every reader is done)
+        if (atomicAdd(&a.ctr->exited, 1u) == gridDim.x - 1) {
+            a.ctr->tickets = 0;
+            a.ctr->dynres = 0;
+            a.ctr->published = 0;
+            a.ctr->exited = 0;
+            __threadfence();
+        }
+    }
 }
 
 template <int D>
@@ -1578,297 +1900,7 @@ __global__ void __maxnreg__(144)
     }
 
     if (warp == kComputeWarps) {
-        // ------------------------------------------------ producer
-        // Work stream: [static tiles | dynamic tiles].  Guided self-scheduling
-        // over one tile counter: CTA b first takes static tiles
-        // [b*CS, (b+1)*CS) without an atomic, then claims chunks from the
-        // counter whose size shrinks with the remaining work once the stream
-        // length is final (ceil(rem / 2P), capped at `chunk`), so no CTA holds
-        // a large chunk when the others run dry.  A claim is issued one chunk
-        // ahead (its atomic travels while the current chunk is issued).
-        // A chunk's records arrive in units of up to kUnit consecutive records,
-        // one bulk copy each, double-buffered.  Each record carries its byte
-        // count and row mask (tile_finish), so issuing a tile is a stage wait,
-        // one expect_tx and one TMA request per piece for K and V.
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.map[lane]) : "memory");
-        const uint64_t pol = l2_evict_first_policy();
-        const uint32_t W = a.n_static, CH = a.chunk;
-        const uint32_t CS = a.chunk_st, P = gridDim.x;
-        const uint32_t pre = min(W, P * CS);  // tiles of the pre-assigned first chunks
-        uint32_t total = a.n_plan_groups ? 0xFFFFFFFFu : W;  // stream length once final
-        uint32_t known = W;                                  // W + reserved dynamic tiles
-        // (shared counters are read by lane 0 and broadcast: every lane must
-        // see the same stream length and claim size, whatever their timing)
-        auto refresh = [&]() {
-            if (total != 0xFFFFFFFFu) return;
-            unsigned long long dr = 0;
-            if (lane == 0) dr = ld_acquire_u64(&a.ctr->dynres);
-            dr = __shfl_sync(0xFFFFFFFFu, dr, 0);
-            known = W + (uint32_t)dr;
-            if ((uint32_t)(dr >> 32) >= a.n_plan_groups) total = known;
-        };
-        bool all_pub = a.n_plan_groups == 0;
-        // dynamic records are published with release stores: once every
-        // planner CTA reported (one acquire) no per-record check is needed;
-        // before that every lane acquires one flag of the chunk, and the warp
-        // barrier orders them before lane 0's (async-proxy) record copies
-        auto dyn_ready = [&](uint32_t b0, uint32_t b1) -> bool {
-            if (all_pub) return true;
-            uint32_t pub = 0;
-            if (lane == 0) pub = ld_acquire_u32(&a.ctr->published);
-            if (__shfl_sync(0xFFFFFFFFu, pub, 0) >= a.n_plan_groups) {
-                all_pub = true;
-                __syncwarp();
-                return true;
-            }
-            bool ok = true;
-            const uint32_t i = max(b0, W) + lane;
-            if (i < b1) ok = ld_acquire_u32(&a.dyn_tiles[i - W].ready) != 0;
-            const bool all = __all_sync(0xFFFFFFFFu, ok);
-            __syncwarp();
-            return all;
-        };
-        // claims: [pre + returned, + size).  A claim is issued late -- when
-        // claim_lead tiles of the current chunk are left to issue -- so a CTA
-        // never holds more than about one chunk beyond its ring: at the
-        // stream's end no CTA sits on tiles while the others run dry.  Its
-        // atomic travels while those tiles are issued (the result register is
-        // read only when the next chunk's records are fetched).
-        uint32_t cl_ret = 0, cl_size = 0, hint = pre;
-        bool cl_pend = false;
-        auto claim = [&]() {
-            uint32_t sz = CH;
-            if (total != 0xFFFFFFFFu) {
-                // the counter has moved on by about one claim per CTA since
-                // this CTA's last claim returned `hint`
-                const uint32_t seen = hint + P * cl_size;
-                const uint32_t rem = total > seen ? total - seen : 0u;
-                sz = max(min(a.min_chunk, CH), min(CH, (rem + 2 * P - 1) / (2 * P)));
-            }
-            if (lane == 0) cl_ret = atomicAdd(&a.ctr->tickets, sz);
-            cl_size = sz;
-            cl_pend = true;
-        };
-        bool first = true;
-        if (a.dtrace && lane == 0) a.dtrace[16 * blockIdx.x + 12] = gtime();
-        uint32_t pc0 = 0, pc1 = 0;  // the current chunk's remaining tiles
-        bool pend = false, feeding = true;
-        // unit slots 0/1 in registers (selects, no local memory)
-        uint32_t u_cnt0 = 0, u_cnt1 = 0, u_base0 = 0, u_base1 = 0;
-        bool u_last0 = false, u_last1 = false;
-        uint32_t u_ph = 0;  // phase bit per unit slot
-        // next unit of records into `slot`: false when none can be fetched now
-        // (planner behind, or end of stream: feeding = false)
-        auto fetch_unit = [&](int slot) -> bool {
-            if (!feeding) return false;
-            if (!pend) {
-                uint32_t b0 = 0, b1 = 0;
-                if (first && blockIdx.x * CS < pre) {
-                    b0 = blockIdx.x * CS;
-                    b1 = min(pre, b0 + CS);
-                } else {
-                    if (!cl_pend) {
-                        refresh();
-                        claim();
-                    }
-                    b0 = pre + __shfl_sync(0xFFFFFFFFu, cl_ret, 0);
-                    b1 = b0 + cl_size;
-                    refresh();
-                    if (total != 0xFFFFFFFFu) {
-                        if (b0 >= total) {
-                            feeding = false;
-                            return false;
-                        }
-                        b1 = min(b1, total);
-                    } else if (b1 > known) {
-                        return false;  // not reserved by the planner yet
-                    }
-                    if (b1 > W && !dyn_ready(b0, b1)) return false;
-                    hint = b1;
-                    cl_pend = false;
-                }
-                first = false;
-                // acquired generic-proxy data (records, gathered rows) is read by
-                // the bulk and tensor copies (async proxy)
-                if (b1 > W) asm volatile("fence.proxy.async.global;" ::: "memory");
-                pc0 = b0;
-                pc1 = b1;
-                pend = true;
-            }
-            // a unit stays in one record array (static | dynamic)
-            const uint32_t n = min(min(pc1 - pc0, (uint32_t)kUnit), pc0 < W ? W - pc0 : 0xFFFFFFFFu);
-            if (lane == 0) {
-                if (a.dtrace && a.dtrace[16 * blockIdx.x + 13] == 0) a.dtrace[16 * blockIdx.x + 13] = gtime();
-                const TileRec* src = pc0 < W ? a.st_tiles + pc0 : a.dyn_tiles + (pc0 - W);
-                mbar_arrive_expect_tx(&s.urec_bar[slot], n * (uint32_t)sizeof(TileRec));
-                bulk_g2s(&s.urec[slot][0], src, n * (uint32_t)sizeof(TileRec), &s.urec_bar[slot]);
-            }
-            __syncwarp();
-            if (slot) {
-                u_cnt1 = n;
-                u_base1 = pc0;
-                u_last1 = pc0 + n == pc1;
-            } else {
-                u_cnt0 = n;
-                u_base0 = pc0;
-                u_last0 = pc0 + n == pc1;
-            }
-            pc0 += n;
-            if (pc0 == pc1) pend = false;
-            return true;
-        };
-        uint32_t stage = 0, phase = 0;
-        bool run_first = true;
-        uint32_t run_tiles = 0;
-        unsigned long long p_wait = 0, p_sleep = 0;
-        const unsigned long long p_t0 = clock64();
-        uint32_t p_tiles = 0;
-        auto pstamp = [&](int k) {
-            if (a.dtiles && lane == 0 && p_tiles < (uint32_t)kTraceTiles)
-                a.dtiles[((size_t)blockIdx.x * kTraceTiles + p_tiles) * 8 + k] = gtime();
-        };
-        int cur = 0;
-        while (!fetch_unit(cur) && feeding) {  // the first unit (the planner may be behind)
-            const unsigned long long ts = clock64();
-            __nanosleep(a.poll_ns);
-            p_sleep += clock64() - ts;
-        }
-        while (cur ? u_cnt1 : u_cnt0) {
-            const int nx = cur ^ 1;
-            // the next unit's records are fetched (and the chunk after this
-            // one claimed) while this unit's last tiles are issued
-            bool have_next = false;
-            mbar_wait(&s.urec_bar[cur], (u_ph >> cur) & 1u);
-            u_ph ^= 1u << cur;
-            if (a.dtrace && lane == 0 && a.dtrace[16 * blockIdx.x + 10] == 0) a.dtrace[16 * blockIdx.x + 10] = gtime();
-            const uint32_t ucnt = cur ? u_cnt1 : u_cnt0, ubase = cur ? u_base1 : u_base0;
-            const bool ulast = cur ? u_last1 : u_last0;
-            // dynamic records are re-armed for the next step once copied
-            if (ubase >= W && (uint32_t)lane < ucnt) a.dyn_tiles[ubase - W + lane].ready = 0;
-            for (uint32_t i = 0; i < ucnt; ++i) {
-                pstamp(3);
-                const TileRec& R = s.urec[cur][i];
-                const uint4 hdr = *reinterpret_cast<const uint4*>(&R);
-                const uint32_t np = hdr.x, qslot = hdr.y;
-                const bool last_in_chunk = ulast && i + 1 == ucnt;
-                const bool last_of_run = last_in_chunk || hdr.w != 0;
-                uint32_t len = 0, srow = 0, gat = 0;
-                uint64_t row = 0;
-                if ((uint32_t)lane < np) {
-                    const uint4 v = *reinterpret_cast<const uint4*>(&R.p[lane]);
-                    len = v.x & ~kPieceGather;
-                    gat = v.x & kPieceGather;
-                    srow = v.y;
-                    row = ((uint64_t)v.w << 32) | v.z;
-                }
-                ++run_tiles;
-                if (lane == 0) {
-                    const unsigned long long tw = clock64();
-                    if (a.inflight && a.inflight < (uint32_t)CF::NS && p_tiles >= a.inflight) {
-                        // at most `inflight` tiles loading or unconsumed: wait for tile
-                        // p_tiles - inflight (its stage's (j / NS)-th completion)
-                        const uint32_t j = p_tiles - a.inflight;
-                        mbar_wait(&s.empty[j % CF::NS], (j / CF::NS) & 1u);
-                    }
-                    mbar_wait(&s.empty[stage], phase ^ 1);
-                    p_wait += clock64() - tw;
-                    pstamp(7);
-                    s.valid[stage] = *reinterpret_cast<const uint4*>(&R.valid[0]);
-                    const uint32_t g = qslot / a.n_hchunks, hc = qslot - g * a.n_hchunks;
-                    const uint32_t nq = min((uint32_t)kHeadsPerSlot, a.G - hc * kHeadsPerSlot);
-                    const uint32_t flags = (run_first ? 1u : 0u) | (last_of_run ? 2u : 0u) | (nq << 8);
-                    const uint32_t qoff = (uint32_t)(((size_t)g * a.G + hc * kHeadsPerSlot) * D);
-                    s.meta[stage] = make_int4((int)qslot, (int)flags, (int)qoff, (int)run_tiles);
-                    const uint32_t bytes = a.debug_skip == 2 ? 0u : R.rows8 * (uint32_t)CF::RB * 2u;
-                    mbar_arrive_expect_tx(&s.full[stage], bytes);
-                }
-                __syncwarp();
-                if (run_first) {
-                    // the run's query rows (<= 2 KB) into this SM's L1 ahead of the
-                    // consumers' fragment build (no shared-memory staging)
-                    const uint32_t g = qslot / a.n_hchunks, hc = qslot - g * a.n_hchunks;
-                    const uint32_t nq = min((uint32_t)kHeadsPerSlot, a.G - hc * kHeadsPerSlot);
-                    const float* qb = a.q + ((size_t)g * a.G + hc * kHeadsPerSlot) * D;
-                    if ((uint32_t)lane * 32u < nq * D)
-                        asm volatile("prefetch.global.L1 [%0];" ::"l"(qb + lane * 32) : "memory");
-                }
-                if (len && a.debug_skip != 2) {
-                    // one request per piece for K and one for V: a box of r8/8 groups
-                    // when the rounded-up rows exist; else the piece's whole groups
-                    // plus a bounds-checked 8-row box (zero fill past the end)
-                    const uint32_t r8 = (len + 7) & ~7u;
-                    const CUtensorMap* mk = &maps.map[(gat ? 2 : 0) * kBoxSizes];
-                    const CUtensorMap* mv = mk + kBoxSizes;
-                    const uint64_t lim = gat ? maps.grows : maps.rows;
-                    const uint32_t off = (srow >> 3) * 8 * CF::RB;
-                    if (row + r8 <= lim) {
-                        tma4d(&s.K[stage][off], mk + (r8 / 8 - 1), (int)row, &s.full[stage], pol);
-                        tma4d(&s.V[stage][off], mv + (r8 / 8 - 1), (int)row, &s.full[stage], pol);
-                    } else {
-                        const uint32_t full = len & ~7u;
-                        if (full) {
-                            tma4d(&s.K[stage][off], mk + (full / 8 - 1), (int)row, &s.full[stage], pol);
-                            tma4d(&s.V[stage][off], mv + (full / 8 - 1), (int)row, &s.full[stage], pol);
-                        }
-                        if (r8 > full) {
-                            const uint32_t off2 = ((srow + full) >> 3) * 8 * CF::RB;
-                            tma4d(&s.K[stage][off2], mk, (int)(row + full), &s.full[stage], pol);
-                            tma4d(&s.V[stage][off2], mv, (int)(row + full), &s.full[stage], pol);
-                        }
-                    }
-                }
-                __syncwarp();
-                if (a.dtrace && lane == 0 && a.dtrace[16 * blockIdx.x + 11] == 0) a.dtrace[16 * blockIdx.x + 11] = gtime();
-                if (a.dtiles && lane == 0 && p_tiles < (uint32_t)kTraceTiles)
-                    a.dtiles[((size_t)blockIdx.x * kTraceTiles + p_tiles) * 8] =
-                            (gtime() & ~63ull) | np | (last_in_chunk ? 32u : 0u);  // stamp | pieces | chunk end
-                ++p_tiles;
-                if (++stage == CF::NS) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-                run_first = last_of_run;
-                if (last_of_run) run_tiles = 0;
-                __syncwarp();
-                if (!have_next && feeding) {
-                    const uint32_t left = ucnt - 1 - i;  // tiles of this unit still to issue
-                    // (pend: the chunk has units after this one -- no claim yet)
-                    if (!pend && !cl_pend && left <= a.claim_lead) {
-                        refresh();
-                        claim();
-                    }
-                    if (left <= a.fetch_lead) have_next = fetch_unit(nx);
-                }
-            }
-            if (cur) u_cnt1 = 0;
-            else u_cnt0 = 0;
-            if (!have_next) {  // fetch now (poll while the planner is behind)
-                while (!fetch_unit(nx) && feeding) {
-                    const unsigned long long ts = clock64();
-                    __nanosleep(a.poll_ns);
-                    p_sleep += clock64() - ts;
-                }
-            }
-            cur = nx;
-        }
-        if (lane == 0) {
-            if (a.dtrace) {
-                a.dtrace[16 * blockIdx.x + 4] = p_wait;
-                a.dtrace[16 * blockIdx.x + 5] = clock64() - p_t0;
-                a.dtrace[16 * blockIdx.x + 14] = p_sleep;
-            }
-            mbar_wait(&s.empty[stage], phase ^ 1);
-            s.meta[stage] = make_int4(-1, 0, 0, 0);
-            mbar_arrive(&s.full[stage]);
-            // the last CTA out re-arms the step counters (every reader is done)
-            if (atomicAdd(&a.ctr->exited, 1u) == gridDim.x - 1) {
-                a.ctr->tickets = 0;
-                a.ctr->dynres = 0;
-                a.ctr->published = 0;
-                a.ctr->exited = 0;
-                __threadfence();
-            }
-        }
+        decode_producer<D>(a, maps, s, lane);
         return;
     }
 
@@ -2101,6 +2133,485 @@ __global__ void __maxnreg__(144)
     }
 }
 
+// ============================================================ tcgen05 decode (d = 128)
+// Same work stream, producer and partials as decode_kernel; the consumers
+// run on the 5th-gen tensor cores.  Per tile (128 keys):
+//   S^T [128 keys x 16] = K [128 x d] . Q^T      (A = K tile, K-major SW128;
+//                                                 B = [q1;q2;q3] x 4 heads + 4
+//                                                 zero rows, built once per run)
+//   O^T [d x 16]       += V^T [d x 128] . P^T    (A = V tile read MN-major;
+//                                                 B = [p1;p2;p3] x 4 heads)
+// with fp32 accumulation in TMEM (S double-buffered, O double-buffered per
+// run).  One thread issues the MMAs (QK of tile t before PV of tile t-1, so
+// the tensor core works while the softmax warps handle tile t-1); four
+// softmax warps own TMEM lane quarters: thread = key row of S (scores, tile
+// max across the warps, lazy rescale of O in TMEM when a head's max grows
+// by 2^8, 3-term bf16 split of the weights into P) and thread = dimension
+// of O at a run's end (the run partial, same layout as decode_kernel's).
+namespace dtc {
+constexpr int NSW = 4;                 // softmax warps (TMEM lane quarters)
+constexpr int PRODUCER = NSW;          // warp 4
+constexpr int MMA = NSW + 1;           // warp 5
+constexpr int QW = NSW + 2;            // warp 6: builds each run's Q operand
+constexpr int THREADS = (NSW + 3) * 32;
+constexpr uint32_t NQ = 16;            // B rows: 3 terms x 4 heads + 4 zero rows
+constexpr uint32_t TMEM_COLS = 64;     // S[2] x 16 | O[2] x 16
+constexpr uint32_t S_COL = 0, O_COL = 32;
+}  // namespace dtc
+
+template <int D>
+struct DecodeTcSmem {
+    using CF = DecodeCfg<D>;
+    static constexpr bool kPostQ = true;  // the producer posts each run's query rows to the Q warp
+    uint8_t K[CF::NS][CF::TILE_BYTES];
+    uint8_t V[CF::NS][CF::TILE_BYTES];
+    // B operands, [n-group][64-column half][8 rows][128 B] with the 128B swizzle
+    // (the K/V tiles' layout): Qb[run parity] rows n = 4 * term + head over d,
+    // Pb[tile parity] rows n over the tile's 128 keys
+    uint8_t Qb[2][dtc::NQ * D * 2];
+    uint8_t Pb[2][dtc::NQ * kTileRows * 2];
+    uint64_t full[CF::NS];
+    uint64_t empty[CF::NS];
+    uint64_t s_full[2], s_empty[2], p_full[2], p_empty[2];
+    uint64_t q_full[2], q_empty[2], o_full[2], o_empty[2];
+    uint64_t q_req[2], q_req_empty[2];
+    uint32_t qreq_off[2], qreq_nq[2], n_qreq;
+    int4 meta[CF::NS];
+    uint4 valid[CF::NS];
+    alignas(16) TileRec urec[2][kUnit];
+    uint64_t urec_bar[2];
+    uint4 pvinfo[CF::NS];  // MMA thread: per stage (flags, O buffer, run) of the tile awaiting PV
+    float red[2][dtc::NSW][4];
+    float lred[dtc::NSW][4];
+    uint32_t run_slot;
+    uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint64_t umma_sdesc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+    return d;
+}
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_arrive(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+            "%12, %13, %14, %15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+              "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+    asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+            "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+            "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+            "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+            "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+            "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+            "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+            "r"(__float_as_uint(v[15]))
+            : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// byte offset of element (row n, column c) of a 16-row B operand laid out as
+// [n >> 3][c >> 6][n & 7][128 B], 16-byte chunks XOR-swizzled by (n & 7)
+__device__ __forceinline__ uint32_t boff16(uint32_t n, uint32_t c, uint32_t cols) {
+    return (n >> 3) * (cols * 16) + (c >> 6) * 1024 + (n & 7) * 128 + ((((c & 63) >> 3) ^ (n & 7)) << 4) +
+           (c & 7) * 2;
+}
+
+template <int D>
+__global__ void __launch_bounds__(dtc::THREADS, 1)
+        decode_tc_kernel(const __grid_constant__ DecodeArgs a, const __grid_constant__ DecodeMaps maps) {
+    static_assert(D == 128, "tcgen05 decode: d = 128 (O^T has d TMEM lanes)");
+    using CF = DecodeCfg<D>;
+    using namespace dtc;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    auto& s = *reinterpret_cast<DecodeTcSmem<D>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto gtime = []() {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        return t;
+    };
+    if (a.dtrace && threadIdx.x == 0) {
+        a.dtrace[16 * blockIdx.x] = gtime();
+        a.dtrace[16 * blockIdx.x + 10] = 0;
+        a.dtrace[16 * blockIdx.x + 11] = 0;
+        a.dtrace[16 * blockIdx.x + 13] = 0;
+    }
+    if (threadIdx.x == 0) tl_mark(a.tl, 2, true);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < CF::NS; ++i) {
+            mbar_init(&s.full[i], 1);
+            mbar_init(&s.empty[i], 1);  // the PV MMAs' commit
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s.s_full[i], 1);
+            mbar_init(&s.s_empty[i], NSW);
+            mbar_init(&s.p_full[i], NSW);
+            mbar_init(&s.p_empty[i], 1);
+            mbar_init(&s.q_full[i], 1);
+            mbar_init(&s.q_empty[i], 1);
+            mbar_init(&s.o_full[i], 1);
+            mbar_init(&s.o_empty[i], NSW);
+            mbar_init(&s.q_req[i], 1);
+            mbar_init(&s.q_req_empty[i], 1);
+            mbar_init(&s.urec_bar[i], 1);
+        }
+        s.n_qreq = 0;
+        fence_mbar_init();
+    }
+    if (warp < NSW) {
+        // the MMAs read every row of a tile: gap rows must hold finite values,
+        // so the ring starts zeroed (later it only ever holds loaded rows);
+        // the B operands' padding rows stay zero
+        uint4* z = reinterpret_cast<uint4*>(&s.K[0][0]);
+        constexpr uint32_t NZ = (2u * CF::NS * CF::TILE_BYTES + sizeof(s.Qb) + sizeof(s.Pb)) / 16;
+        for (uint32_t i = threadIdx.x; i < NZ; i += NSW * 32) z[i] = make_uint4(0u, 0u, 0u, 0u);
+        fence_async_smem();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(&s.tmem_base)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s.tmem_base;
+    pdl_trigger();
+    if (a.wait_plan) pdl_wait();
+
+    if (warp == PRODUCER) {
+        decode_producer<D>(a, maps, s, lane);
+    } else if (warp == QW) {
+        // ------------------------------------------------ Q warp: each run's B
+        // operand [q1; q2; q3] x 4 heads (3-term bf16 split of the f32 queries)
+        for (uint32_t r = 0;; ++r) {
+            const uint32_t qbi = r & 1;
+            mbar_wait(&s.q_req[qbi], (r >> 1) & 1);
+            const uint32_t qoff = s.qreq_off[qbi], nq = s.qreq_nq[qbi];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.q_req_empty[qbi]);
+            if (nq == 0xFFu) break;
+            mbar_wait(&s.q_empty[qbi], ((r >> 1) & 1) ^ 1);  // run r-2's QK MMAs are done
+            const float* qh = a.q + qoff;
+            uint8_t* qbuf = &s.Qb[qbi][0];
+#pragma unroll
+            for (uint32_t h = 0; h < 4; ++h)
+#pragma unroll
+                for (uint32_t j = 0; j < (uint32_t)D / 32; ++j) {
+                    const uint32_t d = j * 32 + lane;
+                    const float x = h < nq ? __ldg(qh + h * D + d) : 0.f;
+                    const uint16_t t1 = f32_to_bf16_rne(x);
+                    const float r1 = x - __uint_as_float((uint32_t)t1 << 16);
+                    const uint16_t t2 = f32_to_bf16_rne(r1);
+                    const uint16_t t3 = f32_to_bf16_rne(r1 - __uint_as_float((uint32_t)t2 << 16));
+                    *reinterpret_cast<uint16_t*>(qbuf + boff16(h, d, D)) = t1;
+                    *reinterpret_cast<uint16_t*>(qbuf + boff16(4 + h, d, D)) = t2;
+                    *reinterpret_cast<uint16_t*>(qbuf + boff16(8 + h, d, D)) = t3;
+                }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.q_full[qbi]);
+        }
+    } else if (warp == MMA) {
+        // ------------------------------------------------ MMA issuer (one thread)
+        // Two streams, each issued as soon as its inputs are ready (polling,
+        // no blocking wait on either): QK of tile t once its K/V landed, its
+        // run's Q is built and S[t & 1] is free; PV of tile t once its P is
+        // written.  PV right after P frees the K/V stage early (the stage
+        // ring, not the tensor core, bounds the tiles in flight).
+        if (lane == 0) {
+            constexpr uint32_t idesc_qk = (1u << 4) | (1u << 7) | (1u << 10) | ((NQ >> 3) << 17) |
+                                          ((uint32_t)(kTileRows >> 4) << 24);
+            constexpr uint32_t idesc_pv = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((NQ >> 3) << 17) |
+                                          ((uint32_t)(D >> 4) << 24);
+            uint32_t q_stage = 0, q_phase = 0, nqk = 0, npv = 0, ri = 0, qb = 0, ob = 0;
+            bool ended = false;
+            for (;;) {
+                if (npv < nqk) {
+                    const uint32_t pst = npv % CF::NS, pb = npv & 1;
+                    const uint4 inf = s.pvinfo[pst];
+                    bool ok = mbar_test_wait(&s.p_full[pb], (npv >> 1) & 1);
+                    // a run's first PV overwrites O[ob]: run ri - 2's epilogue read it
+                    if (ok && (inf.x & 1u) && inf.z >= 2) ok = mbar_test_wait(&s.o_empty[inf.y], ((inf.z >> 1) & 1) ^ 1);
+                    if (ok) {
+                        tc_fence_after();
+                        if (a.dtiles && npv < (uint32_t)kTraceTiles)
+                            a.dtiles[((size_t)blockIdx.x * kTraceTiles + npv) * 8 + 4] = gtime();
+                        const uint32_t vb = smem_u32(&s.V[pst][0]), pbase = smem_u32(&s.Pb[pb][0]);
+                        const uint32_t dcol = tmem + O_COL + inf.y * NQ;
+#pragma unroll
+                        for (uint32_t kk = 0; kk < kTileRows / 16; ++kk)
+                            umma_f16(dcol, umma_sdesc_sw128(vb + kk * 4096, 1024, 2048),
+                                     umma_sdesc_sw128(pbase + (kk >> 2) * 1024 + (kk & 3) * 32, 16, 2048),
+                                     idesc_pv, ((inf.x & 1u) && kk == 0) ? 0u : 1u);
+                        umma_arrive(&s.empty[pst]);  // K and V of the tile read
+                        umma_arrive(&s.p_empty[pb]);
+                        if (inf.x & 2u) umma_arrive(&s.o_full[inf.y]);
+                        ++npv;
+                    }
+                }
+                if (!ended && mbar_test_wait(&s.full[q_stage], q_phase)) {
+                    const int4 mt = s.meta[q_stage];
+                    if (mt.x < 0) {
+                        ended = true;
+                    } else {
+                        const uint32_t flags = (uint32_t)mt.y;
+                        bool ok = true;
+                        if (flags & 1u) ok = mbar_test_wait(&s.q_full[ri & 1], (ri >> 1) & 1);
+                        if (ok) ok = mbar_test_wait(&s.s_empty[nqk & 1], ((nqk >> 1) & 1) ^ 1);
+                        if (ok) {
+                            uint32_t this_ri = ri - 1;
+                            if (flags & 1u) {
+                                qb = ri & 1;
+                                ob = ri & 1;
+                                this_ri = ri++;
+                            }
+                            tc_fence_after();
+                            const uint32_t sb = nqk & 1;
+                            const uint32_t kb = smem_u32(&s.K[q_stage][0]), qbase = smem_u32(&s.Qb[qb][0]);
+                            if (a.dtiles && nqk < (uint32_t)kTraceTiles)
+                                a.dtiles[((size_t)blockIdx.x * kTraceTiles + nqk) * 8 + 3] = gtime();
+#pragma unroll
+                            for (uint32_t kk = 0; kk < (uint32_t)CF::KSTEPS; ++kk) {
+                                const uint32_t off = (kk >> 2) * 1024 + (kk & 3) * 32;
+                                umma_f16(tmem + S_COL + sb * NQ, umma_sdesc_sw128(kb + off, 16, 2048),
+                                         umma_sdesc_sw128(qbase + off, 16, 2048), idesc_qk, kk ? 1u : 0u);
+                            }
+                            umma_arrive(&s.s_full[sb]);
+                            if (flags & 2u) umma_arrive(&s.q_empty[qb]);
+                            s.pvinfo[q_stage] = make_uint4(flags, ob, this_ri, 0u);
+                            ++nqk;
+                            if (++q_stage == CF::NS) {
+                                q_stage = 0;
+                                q_phase ^= 1;
+                            }
+                        }
+                    }
+                }
+                if (ended && npv == nqk) break;
+            }
+        }
+    } else {
+        // ------------------------------------------------ softmax warps
+        const uint32_t tid = threadIdx.x;  // key row of S / dimension of O
+        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        auto named_bar = []() { asm volatile("bar.sync 1, %0;" ::"n"(NSW * 32) : "memory"); };
+        uint32_t stage = 0, phase = 0, t = 0, ri = 0, ob = 0, cur_run = 0;
+        float m_run[4], l_part[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            m_run[h] = -INFINITY;
+            l_part[h] = 0.f;
+        }
+        unsigned long long run_raw = 0;
+        // a finished run's partial is written after the next tile's weights
+        // (its last PV runs meanwhile)
+        bool epi = false;
+        uint32_t e_ob = 0, e_slot = 0, e_tiles = 0, e_run = 0;
+        unsigned long long e_raw = 0;
+        float e_m[4], e_l[4];
+        auto epilogue = [&]() {
+            mbar_wait(&s.o_full[e_ob], (e_run >> 1) & 1);
+            tc_fence_after();
+            float ov[16];
+            tmem_ld16(tmem + lane_base + O_COL + e_ob * NQ, ov);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.o_empty[e_ob]);
+#pragma unroll
+            for (int o = 16; o; o >>= 1)
+#pragma unroll
+                for (int h = 0; h < 4; ++h) e_l[h] += __shfl_xor_sync(0xFFFFFFFFu, e_l[h], o);
+            if (lane < 4) s.lred[warp][lane] = lane == 0 ? e_l[0] : lane == 1 ? e_l[1] : lane == 2 ? e_l[2] : e_l[3];
+            if (tid == 0) s.run_slot = (uint32_t)(e_raw >> 32);
+            named_bar();
+            const uint32_t run = s.run_slot;
+            const size_t pidx = (size_t)e_slot * a.run_cap + run;
+            float* pO = a.part_O + pidx * (kHeadsPerSlot * D);
+#pragma unroll
+            for (int h = 0; h < 4; ++h) pO[h * D + tid] = (ov[h] + ov[8 + h]) + ov[4 + h];
+            if (tid < 4) {
+                a.part_ml[pidx * 8 + tid] = tid == 0 ? e_m[0] : tid == 1 ? e_m[1] : tid == 2 ? e_m[2] : e_m[3];
+                a.part_ml[pidx * 8 + 4 + tid] = (s.lred[0][tid] + s.lred[1][tid]) + (s.lred[2][tid] + s.lred[3][tid]);
+            }
+            named_bar();
+            if (tid == 0) {
+                st_release_u32(a.part_flag + pidx, 1u);  // the combine folds it in now
+                red_release_add_u64(&a.rd[e_slot], (unsigned long long)e_tiles);
+                tl_mark(a.tl, 4, false);
+            }
+            epi = false;
+        };
+        for (;;) {
+            mbar_wait(&s.full[stage], phase);
+            const int4 mt = s.meta[stage];
+            if (a.dtrace && tid == 0 && t == 0) a.dtrace[16 * blockIdx.x + 1] = gtime();
+            if (mt.x < 0) {
+                if (epi) epilogue();
+                if (a.dtrace && tid == 0) {
+                    a.dtrace[16 * blockIdx.x + 2] = gtime();
+                    a.dtrace[16 * blockIdx.x + 3] = t;
+                }
+                if (tid == 0) tl_mark(a.tl, 2, false);
+                break;
+            }
+            const uint32_t flags = (uint32_t)mt.y, slot = (uint32_t)mt.x;
+            const uint32_t vbits = (&s.valid[stage].x)[tid >> 5];
+            if (flags & 1u) {
+                // run start: reserve the run's partial slot (the atomic travels
+                // during the run)
+                if (tid == 0) run_raw = atomicAdd(&a.rd[slot], 1ull << 32);
+                ob = ri & 1;
+                cur_run = ri;
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    m_run[h] = -INFINITY;
+                    l_part[h] = 0.f;
+                }
+                ++ri;
+            }
+            // ---- scores of this thread's key
+            const uint32_t sb = t & 1;
+            mbar_wait(&s.s_full[sb], (t >> 1) & 1);
+            if (a.dtiles && tid == 0 && t < (uint32_t)kTraceTiles)
+                a.dtiles[((size_t)blockIdx.x * kTraceTiles + t) * 8 + 5] = gtime();
+            tc_fence_after();
+            float sv[16];
+            tmem_ld16(tmem + lane_base + S_COL + sb * NQ, sv);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.s_empty[sb]);
+            if (a.dtiles && tid == 0 && t < (uint32_t)kTraceTiles)
+                a.dtiles[((size_t)blockIdx.x * kTraceTiles + t) * 8 + 1] = gtime();
+            const bool valid = (vbits >> lane) & 1u;
+            float sc[4], mx[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                sc[h] = valid ? ((sv[h] + sv[8 + h]) + sv[4 + h]) * a.qscale : -INFINITY;
+                mx[h] = sc[h];
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1)
+#pragma unroll
+                for (int h = 0; h < 4; ++h) mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xFFFFFFFFu, mx[h], o));
+            if (lane < 4) s.red[t & 1][warp][lane] = lane == 0 ? mx[0] : lane == 1 ? mx[1] : lane == 2 ? mx[2] : mx[3];
+            named_bar();
+            if (a.dtiles && tid == 0 && t < (uint32_t)kTraceTiles)
+                a.dtiles[((size_t)blockIdx.x * kTraceTiles + t) * 8 + 6] = gtime();
+            bool grow = false;
+            float M[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                M[h] = fmaxf(fmaxf(s.red[t & 1][0][h], s.red[t & 1][1][h]), fmaxf(s.red[t & 1][2][h], s.red[t & 1][3][h]));
+                grow |= M[h] > m_run[h] + 8.f;
+            }
+            if (grow) {  // (uniform: every thread sees the same maxima)
+                float alpha[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const bool g = M[h] > m_run[h] + 8.f;
+                    alpha[h] = g ? fast_exp2(m_run[h] - M[h]) : 1.f;  // m_run = -inf -> 0
+                    if (g) m_run[h] = M[h];
+                    l_part[h] *= alpha[h];
+                }
+                if (!(flags & 1u)) {
+                    // O holds this run's earlier tiles: wait for the last PV, rescale in TMEM
+                    mbar_wait(&s.p_empty[(t - 1) & 1], ((t - 1) >> 1) & 1);
+                    tc_fence_after();
+                    float ov[16];
+                    const uint32_t oaddr = tmem + lane_base + O_COL + ob * NQ;
+                    tmem_ld16(oaddr, ov);
+#pragma unroll
+                    for (int i = 0; i < 12; ++i) ov[i] *= alpha[i & 3];
+                    tmem_st16(oaddr, ov);
+                    tc_fence_before();
+                }
+            }
+            // ---- weights, 3-term split into P (row 4 * term + head, column = key)
+            float p[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                p[h] = fast_exp2(sc[h] - (m_run[h] == -INFINITY ? 0.f : m_run[h]));  // -inf -> 0
+                l_part[h] += p[h];
+            }
+            const uint32_t pb = t & 1;
+            mbar_wait(&s.p_empty[pb], ((t >> 1) & 1) ^ 1);
+            if (a.dtiles && tid == 0 && t < (uint32_t)kTraceTiles)
+                a.dtiles[((size_t)blockIdx.x * kTraceTiles + t) * 8 + 7] = gtime();
+            uint8_t* pbuf = &s.Pb[pb][0];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const uint16_t t1 = f32_to_bf16_rne(p[h]);
+                const float r1 = p[h] - __uint_as_float((uint32_t)t1 << 16);
+                const uint16_t t2 = f32_to_bf16_rne(r1);
+                const uint16_t t3 = f32_to_bf16_rne(r1 - __uint_as_float((uint32_t)t2 << 16));
+                *reinterpret_cast<uint16_t*>(pbuf + boff16(h, tid, kTileRows)) = t1;
+                *reinterpret_cast<uint16_t*>(pbuf + boff16(4 + h, tid, kTileRows)) = t2;
+                *reinterpret_cast<uint16_t*>(pbuf + boff16(8 + h, tid, kTileRows)) = t3;
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.p_full[pb]);
+            if (a.dtiles && tid == 0 && t < (uint32_t)kTraceTiles)
+                a.dtiles[((size_t)blockIdx.x * kTraceTiles + t) * 8 + 2] = gtime();
+            if (epi) epilogue();  // the previous run's partial
+            if (flags & 2u) {  // this run's partial after the next tile's weights
+                epi = true;
+                e_ob = ob;
+                e_slot = slot;
+                e_tiles = (uint32_t)mt.w;
+                e_run = cur_run;
+                e_raw = run_raw;
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    e_m[h] = m_run[h];
+                    e_l[h] = l_part[h];
+                }
+            }
+            ++t;
+            if (++stage == CF::NS) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+}
+
 // ============================================================ LSE combine (Alg. 2)
 // One CTA per query slot: O = sum_r O_r 2^(m_r - M) / sum_r l_r 2^(m_r - M)
 // over the slot's run partials (merge_into / pattn_finalize,
@@ -2260,7 +2771,24 @@ static void launch_decode_t(const DecodeMaps& m, const DecodeArgs& a, int grid, 
     launch_pdl(true, decode_kernel<D>, dim3(grid), dim3((kComputeWarps + 2) * 32), smem, st, a, m);
 }
 
-void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st) {
+static void launch_decode_tc(const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st) {
+    const size_t smem = sizeof(DecodeTcSmem<128>) + 1024;
+    static bool configured = false;
+    if (!configured) {
+        SAAP_CUDA(cudaFuncSetAttribute(decode_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        SAAP_CUDA(cudaFuncSetAttribute(decode_tc_kernel<128>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       (int)cudaSharedmemCarveoutMaxShared));
+        configured = true;
+    }
+    launch_pdl(true, decode_tc_kernel<128>, dim3(grid), dim3(dtc::THREADS), smem, st, a, m);
+}
+
+void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st, bool tc) {
+    if (tc && D == 128) {
+        launch_decode_tc(m, a, grid, st);
+        return;
+    }
     switch (D) {
         case 128: launch_decode_t<128>(m, a, grid, st); break;
         case 64: launch_decode_t<64>(m, a, grid, st); break;

@@ -1,0 +1,9 @@
+#!/bin/bash
+# round-2 late evidence: full GPU suite, bench, launch list, decode + route ncu captures
+mkdir -p gpurun_out
+timeout 2400 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/r4l_pytest.log 2>&1; tail -2 gpurun_out/r4l_pytest.log
+timeout 1500 python bench.py > gpurun_out/r4l_bench.json 2> gpurun_out/r4l_bench.err; python -c "
+import json; d=json.loads(open('gpurun_out/r4l_bench.json').read().strip().splitlines()[-1]); print(d['value'], d['e2e']['value'], d.get('kernel_us'), d['roofline']['frac'], d['parity']['pass'], d.get('imbalanced',{}).get('us_per_step'), d['clocks'])"; tail -2 gpurun_out/r4l_bench.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 30 --csv --log-file gpurun_out/r4l_launches.csv python bench.py --steps 2 --warmup 1 --layers 1 --no-imbalanced --no-cpu-baseline --no-c1 > /dev/null 2>&1; tail -3 gpurun_out/r4l_launches.csv | cut -c1-200
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:decode_kernel -s 6 -c 1 -o gpurun_out/r4l_decode python scripts/trace_step.py --plain --reps 8 > gpurun_out/r4l_ncu.log 2>&1; tail -2 gpurun_out/r4l_ncu.log
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:route_cluster -s 6 -c 1 -o gpurun_out/r4l_route python scripts/trace_step.py --plain --reps 8 > gpurun_out/r4l_ncu2.log 2>&1; tail -2 gpurun_out/r4l_ncu2.log

@@ -1,0 +1,4 @@
+#!/bin/bash
+timeout 300 python scripts/sweep_opts.py --dense "debug_skip=2" "debug_skip=2,decode_tc=1" 2>&1 | tail -1
+timeout 300 python scripts/sweep_opts.py --given "debug_skip=2" "debug_skip=2,decode_tc=1" "decode_tc=1" 2>&1 | tail -1
+timeout 300 python scripts/trace_step.py --given --opt decode_tc=1 --out gpurun_out/r4n_tc.json > gpurun_out/r4n_a.log 2>&1; tail -c 200 gpurun_out/r4n_a.log

@@ -212,3 +212,36 @@ def test_host_api_zero_copy_outputs(ctx, port):
         assert max_rel_diff(got, want) <= 1e-4
         assert [s.keys_scored for s in st] == [s.keys_scored for s in wst]
         assert [s.max_visited_bucket for s in st] == [s.max_visited_bucket for s in wst]
+
+
+@pytest.mark.parametrize("G", [4, 13])
+def test_tcgen05_decode_parity(ctx, port, G):
+    """The tcgen05 consumers (`decode_tc` option: S^T = K Q^T and O^T += V^T P^T
+    on the tensor cores, TMEM accumulators, a Q warp per run) against the
+    oracle: routed steps with several head chunks and the ordered path, then
+    full attention over many contexts."""
+    ctx.set_option("decode_tc", 1)
+    try:
+        C = 1024
+        cases = _shared_cases(8, 6000, C, 128, G, seed=91 + G)
+        L, routers = _layer(ctx, cases, C, 2047, [0] * 8)
+        _check_layer(port, L, routers, cases, C, 16, 2047, G, False)
+        _check_layer(port, L, routers, cases, C, 16, 2047, G, True)
+        rs = np.random.RandomState(17)
+        n, d = 9000, 128
+        fc = []
+        for i in range(6):
+            K = bf16_round(rs.randn(n, d).astype(np.float32))
+            V = bf16_round(rs.randn(n, d).astype(np.float32))
+            q = bf16_round((rs.randn(G, d) * 0.3).astype(np.float32))
+            fc.append((q, K, V))
+        cent = unit_rows(rs.randn(64, d))
+        Lf = sb.Layer([n] * len(fc), d, 64, 1, 2047, ctx)
+        Lf.build([sb.Partition(cent, ctx)] * len(fc), np.concatenate([c[1] for c in fc]),
+                 np.concatenate([c[2] for c in fc]), np.concatenate([c[1] for c in fc]))
+        full = Lf.full_attention(np.stack([c[0] for c in fc]))
+        for i in range(len(fc)):
+            q, K, V = fc[i]
+            assert max_rel_diff(full[i], port.full_attention(q, K, V)) <= TOL
+    finally:
+        ctx.set_option("decode_tc", 0)
