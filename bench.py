@@ -72,6 +72,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-c1", action="store_true", help="skip the C1-shape sub-line")
+    ap.add_argument("--no-qmodel", action="store_true", help="skip the Q-model router sub-line")
     ap.add_argument("--router", default="centroid", choices=["centroid", "qmodel"],
                     help="BucketRouter plugin: CentroidRouter (de-roped) or QModelRouter "
                          "(qmodel_init weights of the reference's shape, hidden 1024)")
@@ -384,9 +385,8 @@ def ours(a):
     dev = torch.device("cuda", local)
     cfg = sb.SparseAttnConfig(a.probes, 128, sb.DenseWindow(a.sink, a.recent))
 
-    qm_routers = None
-    if a.router == "qmodel":
-        qm_routers = []
+    def make_qm_routers():
+        rts = []
         rq = np.random.default_rng(77 + rank)
         for hl in range(heads_local):  # qmodel_init shapes / scales (qmodel.cpp:337-357)
             h = 1024
@@ -394,7 +394,10 @@ def ours(a):
                    "bn_gamma": np.ones((1, h)), "bn_beta": np.zeros((1, h)),
                    "bn_run_mean": np.zeros((1, h)), "bn_run_var": np.ones((1, h)),
                    "w2": rq.normal(0, np.sqrt(1.0 / h), (h, C)), "b2": np.zeros((1, C))}
-            qm_routers.append(sb.QModelRouter(sb.QModel(prm, ctx)))
+            rts.append(sb.QModelRouter(sb.QModel(prm, ctx)))
+        return rts
+
+    qm_routers = make_qm_routers() if a.router == "qmodel" else None
 
     def build_layer(li, drift):
         return build_c3_layer(sb, torch, ctx, a, li, drift, heads_local, h0, dev, stream, threads,
@@ -524,6 +527,7 @@ def ours(a):
                          a.warmup)
     ms_gather = timed(lambda i: gather(), a.steps, a.warmup) if world > 1 else None
 
+
     # ---- per-kernel device time (eager, events around the kernels)
     def kernel_times(lays, dense):
         ctx.enable_timing(True)
@@ -537,6 +541,34 @@ def ours(a):
     plan_ms, attn_ms = kernel_times(layers, False)
     dense_attn_ms = kernel_times(layers, True)[1] if not a.no_dense else None
     iplan_ms, iattn_ms = kernel_times(imb, False) if imb else (None, None)
+
+    # ---- Q-model router sub-line: the same layers and step, routed by
+    # Q-models of the reference's shape (hidden 1024, qmodel_init weights)
+    qmodel = None
+    if world == 1 and a.router == "centroid" and not a.no_qmodel:
+        import copy
+        qms = make_qm_routers()
+        qlays = []
+        for lay in layers:
+            ql = copy.copy(lay)
+            ql.routers = [qms[gi % heads_local] for gi in range(n_groups)]
+            qlays.append(ql)
+        for ql in qlays:
+            sparse_step(ql)
+        ctx.synchronize()
+        kps = kernels_per_step
+        qgraphs = [capture(sparse_step, ql) for ql in qlays]
+        kernels_per_step = kps
+        ms_qm = timed(lambda i: qgraphs[i % len(qgraphs)].launch(), a.steps, a.warmup)
+        qplan_ms, qattn_ms = kernel_times(qlays, False)
+        sparse_step(qlays[0], out)
+        torch.cuda.synchronize()
+        qmodel = {"router": "Q-model, hidden 1024, qmodel_init weights (qmodel.cpp:337-357), fp64 forward",
+                  "us_per_step": round(ms_qm * 1e3, 3),
+                  "speedup_vs_dense": round(ms_dense / ms_qm, 3) if ms_dense else None,
+                  "kernel_us": {"route_plan": round(qplan_ms * 1e3, 2),
+                                "sparse_attention": round(qattn_ms * 1e3, 2)},
+                  "keys_scored_per_step": int(stats[:, 0].sum().item())}
 
     # ---- counters, quality vs dense (our own dense kernel)
     def counters(lays):
@@ -635,6 +667,7 @@ def ours(a):
             "parity": iparity},
         "cpu_baseline": cpu,
         "c1": c1,
+        "qmodel": qmodel,
         "e2e": {"value": round(ms_e2e * 1e3, 3), "unit": UNIT,
                 "h2d_bytes_per_step": int(2 * n_groups * G * d * 4),
                 "d2h_bytes_per_step": int(n_groups * G * d * 4 + n_groups * ct.sizeof(sb.AttnStats))},

@@ -214,6 +214,7 @@ struct QModelArgs {
     double* probs;             // [groups][G][C]
     double* hid;               // [groups][G][h] scratch: post-ReLU hidden rows
     const uint32_t* slot_g;    // optional [n_slots][kQmSlot] groups sharing one model (pad ~0u)
+    uint32_t logits_variant;   // qm_logits geometry (rows per thread, CTA width); see launch_qmodel_probs
 };
 #ifndef SAAP_QM_SLOT
 #define SAAP_QM_SLOT 2

@@ -584,6 +584,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     if (plan) {
         if (mode == 2) {
             QModelArgs qa{};
+            qa.logits_variant = c->opt.qm_logits;
             qa.q = q_route;
             qa.prm = qm;
             qa.G = (uint32_t)G;
@@ -953,6 +954,7 @@ int saap_ctx_set_option(saap_ctx* c, const char* name, int64_t value) {
         else if (n == "fetch_lead") o.fetch_lead = clamp(0, 32);
         else if (n == "inflight") o.inflight = clamp(0, 8);
         else if (n == "decode_tc") o.decode_tc = clamp(0, 1);
+        else if (n == "qm_logits") o.qm_logits = clamp(0, 5);
         else if (n == "host_graph") o.host_graph = clamp(0, 1);
         else if (n == "trace_decode") o.trace_decode = clamp(0, 1);
         else if (n == "trace_plan") o.trace_plan = clamp(0, 1);
@@ -1124,6 +1126,7 @@ static void route_once(saap_ctx* c, const saap_router* r, const float* q_route, 
     if (r->kind == 0) h2d(dcmax, &r->part->cmax, 4, st);
     if (mode == 2) {
         QModelArgs qa{};
+        qa.logits_variant = c->opt.qm_logits;
         qa.q = dq;
         qa.prm = (const double* const*)dptr;
         qa.G = (uint32_t)G;
@@ -1215,6 +1218,7 @@ int saap_qmodel_forward(saap_ctx* c, const saap_qmodel* m, const float* q, uint6
         h2d(dq, q, n * d * 4, st);
         h2d(dptr, ptrs, sizeof ptrs, st);
         QModelArgs qa{};
+        qa.logits_variant = c->opt.qm_logits;
         qa.q = dq;
         qa.prm = (const double* const*)dptr;
         qa.G = (uint32_t)n;

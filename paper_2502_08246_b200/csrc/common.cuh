@@ -254,6 +254,7 @@ struct saap_ctx {
         uint32_t tail_per_cta = 1;      // (unused since guided claims)
         uint32_t min_chunk = 4;         // smallest guided claim at the stream's end (tiles)
         uint32_t claim_lead = 3;        // decode producer: claim when <= this many tiles are left to issue
+        uint32_t qm_logits = 0;         // Q-model logits geometry (route.cu launch_qmodel_probs)
         uint32_t decode_tc = 0;         // 1: tcgen05 consumers (d = 128)
         uint32_t inflight = 0;          // ... 0: ring depth, else max tiles issued and unconsumed
         uint32_t fetch_lead = 2;        // ... fetch the next records when <= this many are left

@@ -84,17 +84,13 @@ __global__ void __launch_bounds__(kQmT) qm_hidden_kernel(QModelArgs a) {
     }
 }
 
-// logits = r W2 + b2.  A CTA serves one slot (contexts sharing the model)
-// and 128 buckets; rows go kQmRowsL at a time so each W2 load feeds 8
-// ordered chains, and the next kQmP weights load while these are used.
-constexpr int kQmRowsL = 8;
-#ifndef SAAP_QM_TL
-#define SAAP_QM_TL 256
-#endif
-constexpr int kQmTL = SAAP_QM_TL;  // buckets per logits CTA
-__global__ void __launch_bounds__(kQmTL) qm_logits_kernel(QModelArgs a) {
-    extern __shared__ __align__(16) double rs[];  // kQmRowsL x h
-    const uint32_t slot = blockIdx.x, c = blockIdx.y * kQmTL + threadIdx.x;
+// logits = r W2 + b2.  CTA (slot, bucket block, row block): ROWS query rows
+// of the slot (contexts sharing the model) x TL buckets; each W2 load feeds
+// ROWS ordered chains, and the next P weights load while these are used.
+template <int ROWS, int P, int TL>
+__global__ void __launch_bounds__(TL) qm_logits_kernel(QModelArgs a) {
+    extern __shared__ __align__(16) double rs[];  // ROWS x h
+    const uint32_t slot = blockIdx.x, c = blockIdx.y * TL + threadIdx.x;
     const uint32_t* sg = a.slot_g ? a.slot_g + (size_t)slot * kQmSlot : nullptr;
     uint32_t ng = 1;
     if (sg)
@@ -107,17 +103,16 @@ __global__ void __launch_bounds__(kQmTL) qm_logits_kernel(QModelArgs a) {
         const uint32_t g = sg ? sg[r / a.G] : slot;
         return (size_t)g * a.G + r % a.G;
     };
-    for (uint32_t r0 = 0; r0 < R; r0 += kQmRowsL) {
-        const uint32_t nr = min((uint32_t)kQmRowsL, R - r0);
+    for (uint32_t r0 = blockIdx.z * ROWS; r0 < R; r0 += gridDim.z * ROWS) {
+        const uint32_t nr = min((uint32_t)ROWS, R - r0);
         __syncthreads();
-        for (uint32_t e = threadIdx.x; e < nr * a.h; e += kQmTL)
+        for (uint32_t e = threadIdx.x; e < nr * a.h; e += TL)
             rs[e] = a.hid[row_of(r0 + e / a.h) * a.h + e % a.h];
         __syncthreads();
         if (c >= a.C) continue;
-        double s[kQmRowsL];
+        double s[ROWS];
 #pragma unroll
-        for (int i = 0; i < kQmRowsL; ++i) s[i] = 0.0;
-        constexpr int P = kQmP;
+        for (int i = 0; i < ROWS; ++i) s[i] = 0.0;
         const uint32_t kfull = a.h / P * P;
         double wa[P], wb[P];
         if (kfull) {
@@ -132,7 +127,7 @@ __global__ void __launch_bounds__(kQmTL) qm_logits_kernel(QModelArgs a) {
 #pragma unroll
             for (int u = 0; u < P; ++u)
 #pragma unroll
-                for (int i = 0; i < kQmRowsL; ++i) {
+                for (int i = 0; i < ROWS; ++i) {
                     const double av = rs[i * a.h + k + u];
                     if ((uint32_t)i < nr && av != 0.0) s[i] = __dadd_rn(s[i], __dmul_rn(av, wa[u]));
                 }
@@ -142,15 +137,28 @@ __global__ void __launch_bounds__(kQmTL) qm_logits_kernel(QModelArgs a) {
         for (; k < a.h; ++k) {
             const double w = w2[(size_t)k * a.C + c];
 #pragma unroll
-            for (int i = 0; i < kQmRowsL; ++i) {
+            for (int i = 0; i < ROWS; ++i) {
                 const double av = rs[i * a.h + k];
                 if ((uint32_t)i < nr && av != 0.0) s[i] = __dadd_rn(s[i], __dmul_rn(av, w));
             }
         }
 #pragma unroll
-        for (int i = 0; i < kQmRowsL; ++i)
+        for (int i = 0; i < ROWS; ++i)
             if ((uint32_t)i < nr) a.probs[row_of(r0 + i) * a.C + c] = __dadd_rn(s[i], b2[c]);
     }
+}
+
+template <int ROWS, int P, int TL>
+static void launch_qm_logits(const QModelArgs& a, uint32_t n_slots, cudaStream_t st) {
+    const size_t sm = (size_t)ROWS * a.h * sizeof(double);
+    static size_t cfg = 0;
+    if (sm > 48 * 1024 && sm > cfg) {
+        SAAP_CUDA(cudaFuncSetAttribute(qm_logits_kernel<ROWS, P, TL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sm));
+        cfg = sm;
+    }
+    const uint32_t rows = (a.slot_g ? kQmSlot : 1u) * a.G;
+    qm_logits_kernel<ROWS, P, TL><<<dim3(n_slots, (a.C + TL - 1) / TL, (rows + ROWS - 1) / ROWS), TL, sm, st>>>(a);
 }
 
 // softmax_rows_inplace on one (context, row): max (order-free), glibc exp,
@@ -200,18 +208,23 @@ void launch_debug_exp(const double* x, uint64_t n, double* y, cudaStream_t st) {
 }
 
 void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st, uint32_t n_slots) {
-    const size_t sm1 = (size_t)kQmRows * a.d * sizeof(double), sm2 = (size_t)kQmRowsL * a.h * sizeof(double);
-    static size_t cfg1 = 0, cfg2 = 0;
+    const size_t sm1 = (size_t)kQmRows * a.d * sizeof(double);
+    static size_t cfg1 = 0;
     if (sm1 > 48 * 1024 && sm1 > cfg1) {
         SAAP_CUDA(cudaFuncSetAttribute(qm_hidden_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
         cfg1 = sm1;
     }
-    if (sm2 > 48 * 1024 && sm2 > cfg2) {
-        SAAP_CUDA(cudaFuncSetAttribute(qm_logits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-        cfg2 = sm2;
-    }
     qm_hidden_kernel<<<dim3(n_groups, (a.h + kQmT - 1) / kQmT), kQmT, sm1, st>>>(a);
-    qm_logits_kernel<<<dim3(a.slot_g ? n_slots : n_groups, (a.C + kQmTL - 1) / kQmTL), kQmTL, sm2, st>>>(a);
+    // logits geometry (a.logits_variant): rows per thread x CTA width
+    const uint32_t ns = a.slot_g ? n_slots : n_groups;
+    switch (a.logits_variant) {
+        case 1: launch_qm_logits<4, 8, 128>(a, ns, st); break;
+        case 2: launch_qm_logits<2, 8, 128>(a, ns, st); break;
+        case 3: launch_qm_logits<1, 8, 128>(a, ns, st); break;
+        case 4: launch_qm_logits<4, 16, 256>(a, ns, st); break;
+        case 5: launch_qm_logits<2, 4, 64>(a, ns, st); break;
+        default: launch_qm_logits<8, 16, 256>(a, ns, st); break;
+    }
     const size_t sm3 = (size_t)a.C * sizeof(double);
     static size_t cfg3 = 0;
     if (sm3 > 48 * 1024 && sm3 > cfg3) {
