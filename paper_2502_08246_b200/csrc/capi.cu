@@ -283,6 +283,8 @@ void bind_routers(saap_layer* L, const saap_router* const* routers, int& mode, i
             p[3 * g + 1] = rs[g]->model->w2;
             p[3 * g + 2] = rs[g]->model->vec;
         }
+        L->qm_w2_finite = true;
+        for (size_t g = 0; g < L->n_groups; ++g) L->qm_w2_finite = L->qm_w2_finite && rs[g]->model->w2_finite;
         if (!L->d_qm) L->d_qm = (const double**)(dmalloc<void*>(3 * L->n_groups));
         SAAP_CUDA(cudaMemcpy(L->d_qm, p.data(), p.size() * sizeof(void*), cudaMemcpyHostToDevice));
         // slots: contexts routed by one Q-model share its W2 loads
@@ -554,7 +556,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
                     const float* const* centR = nullptr, const ApproxSlot* slots = nullptr,
                     uint32_t n_slots = 0, const uint32_t* qm_slots = nullptr,
                     uint32_t n_qm_slots = 0, const uint32_t* given = nullptr,
-                    const ApproxSlot* h_slots = nullptr) {
+                    const ApproxSlot* h_slots = nullptr, bool qm_finite = false) {
     const cudaStream_t st = c->stream;
     const uint64_t n_groups = src.n_groups, D = src.D, C = src.C;
     const uint64_t n_hchunks = (G + kHeadsPerSlot - 1) / kHeadsPerSlot;
@@ -585,6 +587,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
         if (mode == 2) {
             QModelArgs qa{};
             qa.logits_variant = c->opt.qm_logits;
+            qa.w2_finite = qm_finite ? 1u : 0u;
             qa.q = q_route;
             qa.prm = qm;
             qa.G = (uint32_t)G;
@@ -954,7 +957,7 @@ int saap_ctx_set_option(saap_ctx* c, const char* name, int64_t value) {
         else if (n == "fetch_lead") o.fetch_lead = clamp(0, 32);
         else if (n == "inflight") o.inflight = clamp(0, 8);
         else if (n == "decode_tc") o.decode_tc = clamp(0, 1);
-        else if (n == "qm_logits") o.qm_logits = clamp(0, 5);
+        else if (n == "qm_logits") o.qm_logits = clamp(0, 7);
         else if (n == "host_graph") o.host_graph = clamp(0, 1);
         else if (n == "trace_decode") o.trace_decode = clamp(0, 1);
         else if (n == "trace_plan") o.trace_plan = clamp(0, 1);
@@ -1048,6 +1051,8 @@ int saap_qmodel_create(saap_ctx* c, uint64_t d, uint64_t h, uint64_t C, const do
         for (int i = 0; i < 5; ++i)
             SAAP_CUDA(cudaMemcpy(m->vec + i * h, parts[i], h * 8, cudaMemcpyHostToDevice));
         SAAP_CUDA(cudaMemcpy(m->vec + 5 * h, b2, C * 8, cudaMemcpyHostToDevice));
+        m->w2_finite = true;
+        for (uint64_t i = 0; i < h * C && m->w2_finite; ++i) m->w2_finite = std::isfinite(w2[i]);
         *out = m;
     });
 }
@@ -2493,7 +2498,8 @@ static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* con
                    mode == 1 ? (const ApproxSlot*)L->d_route_slots : nullptr, mode == 1 ? L->n_route_slots : 0,
                    mode == 2 ? L->d_qm_slots : nullptr, mode == 2 ? L->n_qm_slots : 0,
                    mode == 4 ? given : nullptr,
-                   mode == 1 && !L->h_route_slots.empty() ? (const ApproxSlot*)L->h_route_slots.data() : nullptr);
+                   mode == 1 && !L->h_route_slots.empty() ? (const ApproxSlot*)L->h_route_slots.data() : nullptr,
+                   mode == 2 && L->qm_w2_finite);
 }
 
 int saap_sparse_attention_dev(saap_ctx* c, const saap_layer* L, const saap_router* const* routers,

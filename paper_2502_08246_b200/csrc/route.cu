@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kQmT) qm_hidden_kernel(QModelArgs a) {
 // logits = r W2 + b2.  CTA (slot, bucket block, row block): ROWS query rows
 // of the slot (contexts sharing the model) x TL buckets; each W2 load feeds
 // ROWS ordered chains, and the next P weights load while these are used.
-template <int ROWS, int P, int TL>
+template <int ROWS, int P, int TL, bool SKIP0>
 __global__ void __launch_bounds__(TL) qm_logits_kernel(QModelArgs a) {
     extern __shared__ __align__(16) double rs[];  // ROWS x h
     const uint32_t slot = blockIdx.x, c = blockIdx.y * TL + threadIdx.x;
@@ -129,7 +129,11 @@ __global__ void __launch_bounds__(TL) qm_logits_kernel(QModelArgs a) {
 #pragma unroll
                 for (int i = 0; i < ROWS; ++i) {
                     const double av = rs[i * a.h + k + u];
-                    if ((uint32_t)i < nr && av != 0.0) s[i] = __dadd_rn(s[i], __dmul_rn(av, wa[u]));
+                    if (SKIP0) {
+                        if ((uint32_t)i < nr && av != 0.0) s[i] = __dadd_rn(s[i], __dmul_rn(av, wa[u]));
+                    } else {
+                        s[i] = __dadd_rn(s[i], __dmul_rn(av, wa[u]));
+                    }
                 }
 #pragma unroll
             for (int u = 0; u < P; ++u) wa[u] = wb[u];
@@ -148,17 +152,17 @@ __global__ void __launch_bounds__(TL) qm_logits_kernel(QModelArgs a) {
     }
 }
 
-template <int ROWS, int P, int TL>
+template <int ROWS, int P, int TL, bool SKIP0 = true>
 static void launch_qm_logits(const QModelArgs& a, uint32_t n_slots, cudaStream_t st) {
     const size_t sm = (size_t)ROWS * a.h * sizeof(double);
     static size_t cfg = 0;
     if (sm > 48 * 1024 && sm > cfg) {
-        SAAP_CUDA(cudaFuncSetAttribute(qm_logits_kernel<ROWS, P, TL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SAAP_CUDA(cudaFuncSetAttribute(qm_logits_kernel<ROWS, P, TL, SKIP0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sm));
         cfg = sm;
     }
     const uint32_t rows = (a.slot_g ? kQmSlot : 1u) * a.G;
-    qm_logits_kernel<ROWS, P, TL><<<dim3(n_slots, (a.C + TL - 1) / TL, (rows + ROWS - 1) / ROWS), TL, sm, st>>>(a);
+    qm_logits_kernel<ROWS, P, TL, SKIP0><<<dim3(n_slots, (a.C + TL - 1) / TL, (rows + ROWS - 1) / ROWS), TL, sm, st>>>(a);
 }
 
 // softmax_rows_inplace on one (context, row): max (order-free), glibc exp,
@@ -218,11 +222,17 @@ void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st
     // logits geometry (a.logits_variant): rows per thread x CTA width
     const uint32_t ns = a.slot_g ? n_slots : n_groups;
     switch (a.logits_variant) {
+        case 0:  // default: without the zero-skip test when W2 is finite (same sums)
+            if (a.w2_finite) launch_qm_logits<4, 16, 256, false>(a, ns, st);
+            else launch_qm_logits<8, 16, 256>(a, ns, st);
+            break;
         case 1: launch_qm_logits<4, 8, 128>(a, ns, st); break;
         case 2: launch_qm_logits<2, 8, 128>(a, ns, st); break;
         case 3: launch_qm_logits<1, 8, 128>(a, ns, st); break;
         case 4: launch_qm_logits<4, 16, 256>(a, ns, st); break;
         case 5: launch_qm_logits<2, 4, 64>(a, ns, st); break;
+        case 6: launch_qm_logits<8, 16, 256, false>(a, ns, st); break;
+        case 7: launch_qm_logits<4, 16, 256, false>(a, ns, st); break;
         default: launch_qm_logits<8, 16, 256>(a, ns, st); break;
     }
     const size_t sm3 = (size_t)a.C * sizeof(double);
