@@ -226,11 +226,11 @@ void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st
             if (a.w2_finite) launch_qm_logits<4, 16, 256, false>(a, ns, st);
             else launch_qm_logits<8, 16, 256>(a, ns, st);
             break;
-        case 1: launch_qm_logits<4, 8, 128>(a, ns, st); break;
-        case 2: launch_qm_logits<2, 8, 128>(a, ns, st); break;
-        case 3: launch_qm_logits<1, 8, 128>(a, ns, st); break;
-        case 4: launch_qm_logits<4, 16, 256>(a, ns, st); break;
-        case 5: launch_qm_logits<2, 4, 64>(a, ns, st); break;
+        case 1: launch_qm_logits<2, 16, 256, false>(a, ns, st); break;
+        case 2: launch_qm_logits<4, 8, 256, false>(a, ns, st); break;
+        case 3: launch_qm_logits<4, 16, 128, false>(a, ns, st); break;
+        case 4: launch_qm_logits<8, 16, 128, false>(a, ns, st); break;
+        case 5: launch_qm_logits<4, 32, 256, false>(a, ns, st); break;
         case 6: launch_qm_logits<8, 16, 256, false>(a, ns, st); break;
         case 7: launch_qm_logits<4, 16, 256, false>(a, ns, st); break;
         default: launch_qm_logits<8, 16, 256>(a, ns, st); break;
