@@ -231,32 +231,47 @@ __global__ void __launch_bounds__(1024) scan_buckets_kernel(uint32_t C, const ui
 // live in shared memory, so the only global loads in the loop are the
 // (prefetched) assignments.  Writes idx/invA/posA and each key's destination
 // row for move_rows_kernel.
-__global__ void __launch_bounds__(32) scatter_kernel(
+constexpr int kScatterWarps = 4;  // warps per tile (fewer when C is large): each ranks one sub-range
+__global__ void __launch_bounds__(32 * kScatterWarps) scatter_kernel(
         const TileDesc* tiles, const GroupMeta* meta, const uint32_t* assign, uint32_t C,
         const uint32_t* hist, const uint32_t* off, const uint32_t* offA, uint32_t* idx,
         uint32_t* invA, uint32_t* posA, uint32_t* dst_row) {
-    extern __shared__ uint32_t sm[];  // run[C], shiftA[C]
-    uint32_t* run = sm;
-    uint32_t* shA = sm + C;
-    const uint32_t lane = threadIdx.x;
+    extern __shared__ uint32_t sm[];  // shiftA[C], run[W][C]
+    uint32_t* shA = sm;
+    uint32_t* runw = sm + C;
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
     const TileDesc td = tiles[blockIdx.x];
     const GroupMeta gm = meta[td.group];
     const uint32_t* ht = hist + (size_t)blockIdx.x * C;
     const uint32_t* og = off + (size_t)td.group * (C + 1);
     const uint32_t* oAg = offA + (size_t)td.group * (C + 1);
-    for (uint32_t c = lane; c < C; c += 32) {
+    for (uint32_t e = threadIdx.x; e < W * C; e += blockDim.x) runw[e] = 0;
+    __syncthreads();
+    // warp w ranks keys [e_lo, e_hi) of the tile (whole 32-key steps)
+    const uint32_t sub = ((td.count + W - 1) / W + 31) & ~31u;
+    const uint32_t e_lo = min(td.count, w * sub), e_hi = min(td.count, e_lo + sub);
+    const uint32_t* as = assign + gm.ivf_base + td.first;
+    for (uint32_t e = e_lo + lane; e < e_hi; e += 32) atomicAdd(&runw[w * C + as[e]], 1u);
+    __syncthreads();
+    // exclusive prefix over the warps, from the tile's running position
+    for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
         const uint32_t o = og[c];
-        run[c] = o + ht[c];
+        uint32_t r = o + ht[c];
+        for (uint32_t ww = 0; ww < W; ++ww) {
+            const uint32_t t = runw[ww * C + c];
+            runw[ww * C + c] = r;
+            r += t;
+        }
         shA[c] = oAg[c] - o;
     }
-    const uint32_t* as = assign + gm.ivf_base + td.first;
-    uint32_t cn = lane < td.count ? as[lane] : 0xFFFFFFFFu;
-    __syncwarp();
-    for (uint32_t e0 = 0; e0 < td.count; e0 += 32) {
+    __syncthreads();
+    uint32_t* run = runw + w * C;
+    uint32_t cn = e_lo + lane < e_hi ? as[e_lo + lane] : 0xFFFFFFFFu;
+    for (uint32_t e0 = e_lo; e0 < e_hi; e0 += 32) {
         const uint32_t e = e0 + lane;
-        const bool act = e < td.count;
+        const bool act = e < e_hi;
         const uint32_t c = cn;
-        cn = e + 32 < td.count ? as[e + 32] : 0xFFFFFFFFu;  // next step's bucket in flight
+        cn = e + 32 < e_hi ? as[e + 32] : 0xFFFFFFFFu;  // next step's bucket in flight
         const uint32_t lid = td.first + e;
         const uint32_t peers = __match_any_sync(0xFFFFFFFFu, c);
         const uint32_t leader = __ffs(peers) - 1;
@@ -550,14 +565,17 @@ void launch_pack(int D, const TileDesc* tiles, uint32_t n_tiles, const uint32_t*
     if (n_tiles) hist_kernel<<<n_tiles, 512, hsm, st>>>(tiles, meta, assign, C, hist, countA);
     if (C) scan_tiles_kernel<<<dim3(n_groups, (C + 31) / 32), 1024, 0, st>>>(tile_first, C, hist, tot);
     scan_buckets_kernel<<<n_groups, 1024, 0, st>>>(C, tot, countA, off, offA);
-    const size_t ssm = (size_t)2 * C * 4;
+    uint32_t sw = kScatterWarps;
+    while (sw > 1 && (size_t)(1 + sw) * C * 4 > 200 * 1024) --sw;
+    const size_t ssm = (size_t)(1 + sw) * C * 4;
+    if (ssm > 227 * 1024) fail(SAAP_ERR_UNSUPPORTED, "pack: too many buckets for the scatter kernel");
     if (ssm > 48 * 1024 && ssm > cfg_s) {
         SAAP_CUDA(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)ssm));
         cfg_s = ssm;
     }
     if (n_tiles)
-        scatter_kernel<<<n_tiles, 32, ssm, st>>>(tiles, meta, assign, C, hist, off, offA, idx, invA,
+        scatter_kernel<<<n_tiles, 32 * sw, ssm, st>>>(tiles, meta, assign, C, hist, off, offA, idx, invA,
                                                  posA, Ksrc ? dst_row : nullptr);
 #define SAAP_SCATTER(DD)                                                                         \
     if (total_ns)                                                                                \
