@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(256) move_rows_kernel(const GroupMeta* meta, c
                                                         uint16_t* Kdst, uint16_t* Vdst) {
     constexpr uint32_t CH = D / 8;                 // 16-byte chunks per row
     constexpr uint32_t KPW = 32 / (2 * CH);        // keys per warp step (1 at d=128, 2 at 64, 4 at 32)
-    constexpr int U = 4;                           // warp steps in flight
+    constexpr int U = 1;                           // warp steps in flight
     const uint32_t lane = threadIdx.x & 31, sub = lane / (2 * CH), part = lane % (2 * CH);
     const bool isv = part >= CH;
     const uint32_t cc = isv ? part - CH : part;
@@ -579,7 +579,7 @@ void launch_pack(int D, const TileDesc* tiles, uint32_t n_tiles, const uint32_t*
                                                  posA, Ksrc ? dst_row : nullptr);
 #define SAAP_SCATTER(DD)                                                                         \
     if (total_ns)                                                                                \
-        move_rows_kernel<DD><<<148 * 16, 256, 0, st>>>(meta, nullptr, n_groups, total_ns, dst_row,  \
+        move_rows_kernel<DD><<<148 * 8, 256, 0, st>>>(meta, nullptr, n_groups, total_ns, dst_row,  \
                                                        Ksrc, Vsrc, src_row0, Kdst, Vdst);        \
     copy_sink_kernel<DD><<<n_groups, 128, 0, st>>>(meta, n_groups, Ksrc, Vsrc, src_row0, Kdst, Vdst);
     if (Ksrc) switch (D) {
