@@ -228,4 +228,29 @@ CUtensorMap make_row_map(const void* base, uint64_t rows, uint32_t D, uint32_t b
 // host: the 4-D grouped view above, boxes of 8 * groups rows
 CUtensorMap make_group_map(const void* base, uint64_t rows, uint32_t D, uint32_t groups);
 
+// tcgen05 key assignment (assign_tc.cu): key tiles and kernel arguments
+struct TcTile {
+    uint32_t group;
+    uint32_t lid0;   // first local id of the tile
+    uint32_t count;  // valid keys (0 = padding tile)
+    uint32_t part;   // partition slot (rows part*Cpad.. in the split arrays)
+};
+
+struct TcAssignArgs {
+    const TcTile* tiles;
+    const uint64_t* key_row0;  // per group: row of local id 0 in the key tensor map
+    const uint64_t* out_base;  // per group: assignment base (ivf_base)
+    const float* cmax;         // per partition slot: max centroid norm
+    uint32_t C;                // buckets
+    uint32_t Cpad;             // C rounded up to CN
+    uint32_t* out;
+    uint32_t* refine;          // per group (at out_base): local ids of ambiguous keys
+    uint32_t* refine_count;    // per group
+    const uint16_t* keys;      // same tensor the map covers (for |k|)
+    // split mode (f32 keys): keys = k_hi, map_klo covers k_lo = bf16(k - k_hi);
+    // each pair is one key tile whose second A slot holds k_lo, accumulated
+    // into the first tile's columns; |k| from the f32 keys
+    const float* keys_f32;     // non-null: split mode
+};
+
 }  // namespace saap_b200

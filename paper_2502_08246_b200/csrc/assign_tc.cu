@@ -38,26 +38,6 @@ constexpr int EPI = 8;        // epilogue warps: (tile, TMEM lane quarter)
 constexpr int THREADS = (EPI + 2) * 32;  // warps 0..EPI-1 epilogue, EPI TMA, EPI+1 MMA
 }  // namespace tc
 
-struct TcTile {
-    uint32_t group;
-    uint32_t lid0;   // first local id of the tile
-    uint32_t count;  // valid keys (0 = padding tile)
-    uint32_t part;   // partition slot (rows part*Cpad.. in the split arrays)
-};
-
-struct TcAssignArgs {
-    const TcTile* tiles;
-    const uint64_t* key_row0;  // per group: row of local id 0 in the key tensor map
-    const uint64_t* out_base;  // per group: assignment base (ivf_base)
-    const float* cmax;         // per partition slot: max centroid norm
-    uint32_t C;                // buckets
-    uint32_t Cpad;             // C rounded up to CN
-    uint32_t* out;
-    uint32_t* refine;          // per group (at out_base): local ids of ambiguous keys
-    uint32_t* refine_count;    // per group
-    const uint16_t* keys;      // same tensor the map covers (for |k|)
-};
-
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
     uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
     d |= (uint64_t)1 << 16;    // LBO (unused for swizzled K-major) = 1
@@ -133,7 +113,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         assign_tc_kernel(const __grid_constant__ CUtensorMap map_k,
                          const __grid_constant__ CUtensorMap map_hi,
                          const __grid_constant__ CUtensorMap map_mid, TcAssignArgs a,
-                         uint32_t n_pairs) {
+                         uint32_t n_pairs, const __grid_constant__ CUtensorMap map_klo) {
     using namespace tc;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     TcSmem& s = *reinterpret_cast<TcSmem*>(
@@ -169,6 +149,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(&map_k) : "memory");
+            if (a.keys_f32) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_klo) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(&map_hi) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(&map_mid) : "memory");
             uint32_t jg = 0, np = 0;  // chunks / pairs issued by this CTA
@@ -176,10 +157,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                 if (np) mbar_wait(&s.a_empty, (np - 1) & 1);  // previous pair's MMAs read A
                 mbar_arrive_expect_tx(&s.a_full, NT * A_TILE_BYTES);
                 for (int t = 0; t < NT; ++t) {
-                    const TcTile tt = a.tiles[p * NT + t];
+                    const bool lo = a.keys_f32 && t == 1;  // split mode: slot 1 = k_lo of tile 0
+                    const TcTile tt = a.tiles[p * NT + (lo ? 0 : t)];
                     const int y = (int)(a.key_row0[tt.group] + tt.lid0);
                     for (int b = 0; b < 2; ++b)
-                        tma_load_2d(&s.A[t][b * TM * 128], &map_k, b * BOX, y, &s.a_full);
+                        tma_load_2d(&s.A[t][b * TM * 128], lo ? &map_klo : &map_k, b * BOX, y, &s.a_full);
                 }
                 const int ybase = (int)(a.tiles[p * NT].part * a.Cpad);
                 for (uint32_t j = 0; j < nchunks; ++j, ++jg) {
@@ -209,7 +191,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                     mbar_wait(&s.t_empty[buf], bph ^ 1);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     for (int t = 0; t < NT; ++t) {
-                        const uint32_t dcol = tmem + buf * (NT * CN) + t * CN;
+                        // split mode: k_lo accumulates into tile 0's columns
+                        const bool lo = a.keys_f32 && t == 1;
+                        const uint32_t dcol = tmem + buf * (NT * CN) + (lo ? 0 : t) * CN;
                         for (int term = 0; term < 2; ++term) {
 #pragma unroll
                             for (int kk = 0; kk < KD / 16; ++kk) {
@@ -217,7 +201,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                                 const uint32_t boff = term * B_TERM_BYTES + (kk >> 2) * CN * 128 + (kk & 3) * 32;
                                 umma_bf16(dcol, umma_desc_sw128(smem_u32(&s.A[t][0]) + aoff),
                                           umma_desc_sw128(smem_u32(&s.B[st][0]) + boff), idesc,
-                                          (term | kk) != 0);
+                                          (lo || term || kk) ? 1u : 0u);
                             }
                         }
                     }
@@ -236,24 +220,37 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         const int row = q4 * 32 + lane;
         uint32_t jg = 0;
         for (uint32_t p = blockIdx.x; p < n_pairs; p += gridDim.x) {
+            const bool idle = a.keys_f32 && t == 1;  // split mode: tile 1's columns are unused
             const TcTile tt = a.tiles[p * NT + t];
             float b1 = -INFINITY, b2 = -INFINITY;
             uint32_t i1 = 0;
             float n2 = 0.f;
-            if (half == 0 && (uint32_t)row < tt.count) {
-                const uint4* kp = reinterpret_cast<const uint4*>(a.keys + (a.key_row0[tt.group] + tt.lid0 + row) * KD);
+            if (!idle && half == 0 && (uint32_t)row < tt.count) {
+                if (a.keys_f32) {
+                    const float4* kp = reinterpret_cast<const float4*>(a.keys_f32 + (a.key_row0[tt.group] + tt.lid0 + row) * KD);
 #pragma unroll
-                for (int q = 0; q < KD / 8; ++q) {
-                    const uint4 u = kp[q];
-                    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+                    for (int q = 0; q < KD / 4; ++q) {
+                        const float4 u = kp[q];
+                        n2 = fmaf(u.x, u.x, fmaf(u.y, u.y, fmaf(u.z, u.z, fmaf(u.w, u.w, n2))));
+                    }
+                } else {
+                    const uint4* kp = reinterpret_cast<const uint4*>(a.keys + (a.key_row0[tt.group] + tt.lid0 + row) * KD);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float lo = bf16lo(w4[e]), hi = bf16hi(w4[e]);
-                        n2 = fmaf(lo, lo, fmaf(hi, hi, n2));
+                    for (int q = 0; q < KD / 8; ++q) {
+                        const uint4 u = kp[q];
+                        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float lo = bf16lo(w4[e]), hi = bf16hi(w4[e]);
+                            n2 = fmaf(lo, lo, fmaf(hi, hi, n2));
+                        }
                     }
                 }
             }
-            const float bound = 0x1p-14f * 1.0001f * sqrtf(n2) * a.cmax[tt.part];
+            // split mode: 512 fp32-accumulated products (2^-14) and the key
+            // split residual |k - k_hi - k_lo| <= 2^-18 |k| on top of the
+            // centroid split: 2^-13 covers both
+            const float bound = (a.keys_f32 ? 0x1p-13f : 0x1p-14f) * 1.0001f * sqrtf(n2) * a.cmax[tt.part];
             const uint32_t taddr0 = tmem + ((uint32_t)(q4 * 32) << 16) + t * CN;
             for (uint32_t j = 0; j < nchunks; ++j, ++jg) {
                 const uint32_t buf = jg & 1, bph = (jg >> 1) & 1;
@@ -261,7 +258,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t lim = (j + 1) * CN > a.C ? a.C - j * CN : CN;  // valid columns
 #pragma unroll 1
-                for (int q = half * (CN / 32) / (EPI / 8); q < (half + 1) * (CN / 32) / (EPI / 8); ++q) {
+                for (int q = half * (CN / 32) / (EPI / 8); !idle && q < (half + 1) * (CN / 32) / (EPI / 8); ++q) {
                     float v[32];
                     tmem_ld32(taddr0 + buf * (NT * CN) + q * 32, v);
                     const uint32_t c0 = j * CN + q * 32;
@@ -302,7 +299,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                 }
             }
             if (EPI == 16) asm volatile("bar.sync 1, %0;" ::"n"(EPI * 32) : "memory");
-            if (half == 0 && (uint32_t)row < tt.count) {
+            if (!idle && half == 0 && (uint32_t)row < tt.count) {
                 const uint32_t lid = tt.lid0 + row;
                 if (b1 - b2 > 2.f * bound) {
                     a.out[a.out_base[tt.group] + lid] = i1;
@@ -336,10 +333,12 @@ constexpr int NW = THREADS / 32;
 constexpr int PER = RC / NW;  // chains per thread
 }  // namespace rf
 
-template <int D>
+// (F32: the keys are f32 rows -- the split-mode assignment of f32 keys; the
+// products stay exact in fp64, so the DFMA chain is the reference's)
+template <int D, bool F32 = false>
 __global__ void __launch_bounds__(rf::THREADS) refine_kernel(const uint32_t* list,
                                                              const uint32_t* count,
-                                                             const uint16_t* keys,
+                                                             const void* keys_any,
                                                              const uint64_t* key_row0,
                                                              const double* const* cent64,
                                                              const uint64_t* out_base, uint32_t C,
@@ -347,7 +346,8 @@ __global__ void __launch_bounds__(rf::THREADS) refine_kernel(const uint32_t* lis
     using namespace rf;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     double* cs = reinterpret_cast<double*>(smem_raw);  // [RC][D]
-    __shared__ uint32_t ks[RB * (D / 2 + 1)];           // keys as bf16 pairs (padded rows)
+    constexpr int KW = F32 ? D + 1 : D / 2 + 1;         // words per staged key row (padded)
+    __shared__ uint32_t ks[RB * KW];                    // keys as bf16 pairs, or f32
     __shared__ double red_s[NW][RB];
     __shared__ uint32_t red_i[NW][RB];
     const uint32_t g = blockIdx.y;
@@ -358,12 +358,14 @@ __global__ void __launch_bounds__(rf::THREADS) refine_kernel(const uint32_t* lis
     for (uint32_t b0 = blockIdx.x * RB; b0 < n; b0 += gridDim.x * RB) {
         const uint32_t nb = min((uint32_t)RB, n - b0);
         __syncthreads();
-        for (uint32_t e = tid; e < (uint32_t)RB * (D / 2); e += THREADS) {  // bf16 pairs
-            const uint32_t r = e / (D / 2), j2 = e % (D / 2);
-            ks[r * (D / 2 + 1) + j2] = reinterpret_cast<const uint32_t*>(
-                    keys + (key_row0[g] + lg[b0 + min(r, nb - 1)]) * D)[j2];
+        constexpr uint32_t WPR = F32 ? D : D / 2;  // words per key row
+        for (uint32_t e = tid; e < (uint32_t)RB * WPR; e += THREADS) {
+            const uint32_t r = e / WPR, j2 = e % WPR;
+            const size_t row = key_row0[g] + lg[b0 + min(r, nb - 1)];
+            ks[r * KW + j2] = F32 ? reinterpret_cast<const uint32_t*>(reinterpret_cast<const float*>(keys_any) + row * D)[j2]
+                                  : reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(keys_any) + row * D)[j2];
         }
-        const uint32_t* kw = ks + lane * (D / 2 + 1);
+        const uint32_t* kw = ks + lane * KW;
         double best = -INFINITY;
         uint32_t bid = 0xFFFFFFFFu;
         for (uint32_t c0 = 0; c0 < C; c0 += RC) {
@@ -380,8 +382,9 @@ __global__ void __launch_bounds__(rf::THREADS) refine_kernel(const uint32_t* lis
                 const double* cw = cs + (w + NW * i0) * D;
 #pragma unroll 8
                 for (int j2 = 0; j2 < D / 2; ++j2) {
-                    const double k0 = (double)__uint_as_float(kw[j2] << 16);
-                    const double k1 = (double)__uint_as_float(kw[j2] & 0xFFFF0000u);
+                    const double k0 = F32 ? (double)__uint_as_float(kw[2 * j2]) : (double)__uint_as_float(kw[j2] << 16);
+                    const double k1 = F32 ? (double)__uint_as_float(kw[2 * j2 + 1])
+                                          : (double)__uint_as_float(kw[j2] & 0xFFFF0000u);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const double2 cv = reinterpret_cast<const double2*>(cw + NW * i * D)[j2];
@@ -428,6 +431,16 @@ __global__ void split_centroids_kernel(const float* cent, uint32_t C, uint32_t C
         const float r = x - __uint_as_float((uint32_t)h << 16);
         hi[e] = h;
         mid[e] = f32_to_bf16_rne(r);
+    }
+}
+
+// f32 rows -> (hi, lo) bf16 split (the split-mode assignment's keys)
+__global__ void split_rows_kernel(const float* x, uint64_t n, uint16_t* hi, uint16_t* lo) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n; e += (uint64_t)gridDim.x * blockDim.x) {
+        const float v = x[e];
+        const uint16_t h = f32_to_bf16_rne(v);
+        hi[e] = h;
+        lo[e] = f32_to_bf16_rne(v - __uint_as_float((uint32_t)h << 16));
     }
 }
 
@@ -501,6 +514,12 @@ CUtensorMap make_group_map(const void* base, uint64_t rows, uint32_t D, uint32_t
 
 uint32_t tc_cpad(uint32_t C) { return (C + tc::CN - 1) / tc::CN * tc::CN; }
 
+void launch_split_rows(const float* x, uint64_t n, uint16_t* hi, uint16_t* lo, cudaStream_t st) {
+    if (!n) return;
+    split_rows_kernel<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 32), 256, 0, st>>>(x, n, hi, lo);
+    SAAP_CUDA(cudaGetLastError());
+}
+
 void launch_split_centroids(const float* cent, uint32_t C, uint32_t D, uint16_t* hi, uint16_t* mid,
                             cudaStream_t st) {
     const uint32_t Cpad = tc_cpad(C);
@@ -511,21 +530,24 @@ void launch_split_centroids(const float* cent, uint32_t C, uint32_t D, uint16_t*
 // Host tile list: per group, 128-key tiles padded to an even count so the
 // two tiles of a CTA share one partition.
 void build_tc_tiles(const std::vector<GroupMeta>& meta, const std::vector<uint32_t>& part_slot,
-                    std::vector<TcTile>& tiles) {
+                    std::vector<TcTile>& tiles, bool split) {
     tiles.clear();
     for (size_t g = 0; g < meta.size(); ++g) {
         const uint32_t ns = meta[g].n - meta[g].sink;
         const size_t first = tiles.size();
-        for (uint32_t f = 0; f < ns; f += tc::TM)
+        for (uint32_t f = 0; f < ns; f += tc::TM) {
             tiles.push_back(TcTile{(uint32_t)g, f, std::min<uint32_t>(tc::TM, ns - f), part_slot[g]});
+            if (split) tiles.push_back(TcTile{(uint32_t)g, f, 0, part_slot[g]});  // its k_lo slot
+        }
         if ((tiles.size() - first) % tc::NT) tiles.push_back(TcTile{(uint32_t)g, 0, 0, part_slot[g]});
     }
 }
 
 void launch_assign_tc(const uint16_t* keys, uint64_t key_rows, const uint16_t* hi,
                       const uint16_t* mid, uint32_t n_parts, const TcAssignArgs& args,
-                      uint32_t n_tiles, cudaStream_t st) {
+                      uint32_t n_tiles, cudaStream_t st, const uint16_t* keys_lo) {
     const CUtensorMap mk = make_map(keys, key_rows, tc::TM);
+    const CUtensorMap mlo = make_map(keys_lo ? keys_lo : keys, key_rows, tc::TM);
     const CUtensorMap mh = make_map(hi, (uint64_t)n_parts * args.Cpad, tc::CN);
     const CUtensorMap mm = make_map(mid, (uint64_t)n_parts * args.Cpad, tc::CN);
     const size_t smem = sizeof(TcSmem) + 1024;
@@ -540,24 +562,31 @@ void launch_assign_tc(const uint16_t* keys, uint64_t key_rows, const uint16_t* h
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint32_t grid = std::max<uint32_t>(1u, std::min<uint32_t>(n_pairs, (uint32_t)sms));
-    assign_tc_kernel<<<grid, tc::THREADS, smem, st>>>(mk, mh, mm, args, n_pairs);
+    assign_tc_kernel<<<grid, tc::THREADS, smem, st>>>(mk, mh, mm, args, n_pairs, mlo);
     SAAP_CUDA(cudaGetLastError());
 }
 
-void launch_refine(const uint32_t* list, const uint32_t* count, const uint16_t* keys,
+void launch_refine(const uint32_t* list, const uint32_t* count, const void* keys,
                    const uint64_t* key_row0, const double* const* cent64, const uint64_t* out_base,
-                   uint32_t C, uint32_t* out, uint32_t n_groups, int sm_count, cudaStream_t st) {
+                   uint32_t C, uint32_t* out, uint32_t n_groups, int sm_count, cudaStream_t st,
+                   bool f32_keys) {
     using namespace rf;
     const size_t smem = (size_t)RC * tc::KD * sizeof(double);
     static bool configured = false;
     if (!configured) {
         SAAP_CUDA(cudaFuncSetAttribute(refine_kernel<tc::KD>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        SAAP_CUDA(cudaFuncSetAttribute(refine_kernel<tc::KD, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = true;
     }
     const uint32_t y = std::max<uint32_t>(1, (uint32_t)(2 * sm_count) / std::max<uint32_t>(n_groups, 1));
-    refine_kernel<tc::KD><<<dim3(y, n_groups), THREADS, smem, st>>>(list, count, keys, key_row0, cent64,
-                                                                 out_base, C, out);
+    if (f32_keys)
+        refine_kernel<tc::KD, true><<<dim3(y, n_groups), THREADS, smem, st>>>(list, count, keys, key_row0, cent64,
+                                                                           out_base, C, out);
+    else
+        refine_kernel<tc::KD><<<dim3(y, n_groups), THREADS, smem, st>>>(list, count, keys, key_row0, cent64,
+                                                                     out_base, C, out);
     SAAP_CUDA(cudaGetLastError());
 }
 

@@ -73,32 +73,19 @@ void launch_km_seed(const float* keys, uint32_t D, const uint64_t* seed_rows, ui
                     float* cent, cudaStream_t st);
 void launch_km_update(const float* keys, uint32_t D, const uint32_t* off, const uint32_t* idx,
                       uint32_t C, float* cent, cudaStream_t st);
-struct TcTile {
-    uint32_t group, lid0, count, part;
-};
-struct TcAssignArgs {
-    const TcTile* tiles;
-    const uint64_t* key_row0;
-    const uint64_t* out_base;
-    const float* cmax;
-    uint32_t C;
-    uint32_t Cpad;
-    uint32_t* out;
-    uint32_t* refine;
-    uint32_t* refine_count;
-    const uint16_t* keys;
-};
 uint32_t tc_cpad(uint32_t C);
 void launch_split_centroids(const float* cent, uint32_t C, uint32_t D, uint16_t* hi, uint16_t* mid,
                             cudaStream_t st);
 void build_tc_tiles(const std::vector<GroupMeta>& meta, const std::vector<uint32_t>& part_slot,
-                    std::vector<TcTile>& tiles);
+                    std::vector<TcTile>& tiles, bool split);
 void launch_assign_tc(const uint16_t* keys, uint64_t key_rows, const uint16_t* hi,
                       const uint16_t* mid, uint32_t n_parts, const TcAssignArgs& args,
-                      uint32_t n_tiles, cudaStream_t st);
-void launch_refine(const uint32_t* list, const uint32_t* count, const uint16_t* keys,
+                      uint32_t n_tiles, cudaStream_t st, const uint16_t* keys_lo);
+void launch_refine(const uint32_t* list, const uint32_t* count, const void* keys,
                    const uint64_t* key_row0, const double* const* cent64, const uint64_t* out_base,
-                   uint32_t C, uint32_t* out, uint32_t n_groups, int sm_count, cudaStream_t st);
+                   uint32_t C, uint32_t* out, uint32_t n_groups, int sm_count, cudaStream_t st,
+                   bool f32_keys);
+void launch_split_rows(const float* x, uint64_t n, uint16_t* hi, uint16_t* lo, cudaStream_t st);
 void launch_synth(uint16_t* out, uint64_t rows, uint32_t D, uint64_t seed, int kind,
                   const float* centers, uint64_t n_centers, float center_scale, float noise,
                   cudaStream_t st);
@@ -958,6 +945,7 @@ int saap_ctx_set_option(saap_ctx* c, const char* name, int64_t value) {
         else if (n == "inflight") o.inflight = clamp(0, 8);
         else if (n == "decode_tc") o.decode_tc = clamp(0, 1);
         else if (n == "qm_logits") o.qm_logits = clamp(0, 7);
+        else if (n == "assign_f32_tc") o.assign_f32_tc = clamp(0, 1);
         else if (n == "host_graph") o.host_graph = clamp(0, 1);
         else if (n == "trace_decode") o.trace_decode = clamp(0, 1);
         else if (n == "trace_plan") o.trace_plan = clamp(0, 1);
@@ -2102,6 +2090,8 @@ int saap_layer_destroy(saap_layer* L) {
         dfree(L->d_centR);
         dfree(L->d_cmax);
         dfree(L->d_route_slots);
+        dfree(L->split_hi);
+        dfree(L->split_lo);
         dfree(L->d_qm);
         dfree(L->d_qm_slots);
         delete L;
@@ -2126,11 +2116,15 @@ static void bind_parts(saap_layer* L, const saap_partition* const* parts) {
 }
 
 // assignment + pack from device bf16 sources laid out like the layer rows
-static void assign_tc_path(saap_layer* L, const uint16_t* keys) {
+// keys: bf16 assignment keys; or (split mode, f32 keys) keys = k_hi, keys_lo =
+// k_lo and keys_f32 the f32 rows (norms and the exact re-scoring)
+static void assign_tc_path(saap_layer* L, const uint16_t* keys, const uint16_t* keys_lo = nullptr,
+                           const float* keys_f32 = nullptr) {
     saap_ctx* c = L->ctx;
     const cudaStream_t st = c->stream;
     const uint32_t Cpad = tc_cpad((uint32_t)L->C);
-    if (L->tc_parts != L->parts) {
+    const bool split = keys_f32 != nullptr;
+    if (L->tc_parts != L->parts || L->tc_split != split) {
         // distinct partitions -> slots of the concatenated (hi, mid) split arrays
         std::vector<const saap_partition*> slots;
         std::vector<uint32_t> slot_of(L->n_groups);
@@ -2165,7 +2159,7 @@ static void assign_tc_path(saap_layer* L, const uint16_t* keys) {
             cmax[i] = (float)(m * (1 + 1e-6));
         }
         std::vector<TcTile> tiles;
-        build_tc_tiles(L->h_meta, slot_of, tiles);
+        build_tc_tiles(L->h_meta, slot_of, tiles, split);
         dfree(L->tc_cmax);
         L->tc_cmax = dmalloc<float>(slots.size());
         SAAP_CUDA(cudaMemcpy(L->tc_cmax, cmax.data(), cmax.size() * 4, cudaMemcpyHostToDevice));
@@ -2177,6 +2171,7 @@ static void assign_tc_path(saap_layer* L, const uint16_t* keys) {
         SAAP_CUDA(cudaMemcpy(L->tc_tiles, tiles.data(), tiles.size() * sizeof(TcTile),
                              cudaMemcpyHostToDevice));
         L->tc_parts = L->parts;
+        L->tc_split = split;
         L->tc_nslots = (uint32_t)slots.size();
     }
     if (!L->tc_refine) {
@@ -2195,10 +2190,15 @@ static void assign_tc_path(saap_layer* L, const uint16_t* keys) {
     args.refine = L->tc_refine;
     args.refine_count = L->tc_refine_count;
     args.keys = keys;
+    args.keys_f32 = keys_f32;
     launch_assign_tc(keys, L->total_rows, L->tc_hi, L->tc_mid, L->tc_nslots, args, L->tc_n_tiles,
-                     st);
-    launch_refine(L->tc_refine, L->tc_refine_count, keys, L->key_row0, L->d_cent64, L->ivf_base,
-                  (uint32_t)L->C, L->assign, (uint32_t)L->n_groups, c->sm_count, st);
+                     st, keys_lo);
+    if (split)
+        launch_refine(L->tc_refine, L->tc_refine_count, keys_f32, L->key_row0, L->d_cent64, L->ivf_base,
+                      (uint32_t)L->C, L->assign, (uint32_t)L->n_groups, c->sm_count, st, true);
+    else
+        launch_refine(L->tc_refine, L->tc_refine_count, keys, L->key_row0, L->d_cent64, L->ivf_base,
+                      (uint32_t)L->C, L->assign, (uint32_t)L->n_groups, c->sm_count, st, false);
     c->launches += 2;
     L->last_tc = true;
 }
@@ -2216,6 +2216,21 @@ static void build_from_device(saap_layer* L, const uint16_t* Ksrc, const uint16_
     }
     if (assign_bf16 && L->d == 128 && c->assign_mode == 0) {
         assign_tc_path(L, (const uint16_t*)keys_assign);
+    } else if (!assign_bf16 && L->d == 128 && c->assign_mode == 0 && c->opt.assign_f32_tc) {
+        // f32 keys on the tensor cores: k = k_hi + k_lo (bf16 terms), the
+        // bound widened for the split; ambiguous keys re-scored from the f32 rows
+        const uint64_t elems = L->total_rows * L->d;
+        if (elems > L->split_elems) {  // (kept with the layer: rebuilds reuse them)
+            sync(c);
+            dfree(L->split_hi);
+            dfree(L->split_lo);
+            L->split_hi = dmalloc<uint16_t>(elems);
+            L->split_lo = dmalloc<uint16_t>(elems);
+            L->split_elems = elems;
+        }
+        launch_split_rows((const float*)keys_assign, elems, L->split_hi, L->split_lo, st);
+        assign_tc_path(L, L->split_hi, L->split_lo, (const float*)keys_assign);
+        c->launches++;
     } else {
         launch_assign_exact((int)L->d, assign_bf16, L->tiles, L->n_tiles, keys_assign, L->key_row0,
                             L->d_cent64, (uint32_t)L->C, L->assign, L->ivf_base, st);

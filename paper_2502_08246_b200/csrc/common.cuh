@@ -254,6 +254,7 @@ struct saap_ctx {
         uint32_t tail_per_cta = 1;      // (unused since guided claims)
         uint32_t min_chunk = 4;         // smallest guided claim at the stream's end (tiles)
         uint32_t claim_lead = 3;        // decode producer: claim when <= this many tiles are left to issue
+        uint32_t assign_f32_tc = 1;     // f32 assignment keys on tcgen05 (split keys); 0: fp64 kernel
         uint32_t qm_logits = 0;         // Q-model logits geometry (route.cu launch_qmodel_probs)
         uint32_t decode_tc = 0;         // 1: tcgen05 consumers (d = 128)
         uint32_t inflight = 0;          // ... 0: ring depth, else max tiles issued and unconsumed
@@ -385,6 +386,10 @@ struct saap_layer {
     uint64_t last_refined = 0;
     bool last_tc = false;
     std::vector<const saap_partition*> tc_parts;  // partitions the tc resources were built for
+    bool tc_split = false;                         // tc tile list built for split (f32-key) mode
+    uint16_t* split_hi = nullptr;                  // f32 assignment keys split into bf16 terms
+    uint16_t* split_lo = nullptr;
+    uint64_t split_elems = 0;
     uint32_t tc_nslots = 0;
     cudaEvent_t bev[3] = {nullptr, nullptr, nullptr};  // last build: start, after assign, after pack
     // routing parameter table cache (device arrays of per-group pointers)

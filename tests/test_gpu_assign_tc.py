@@ -80,3 +80,35 @@ def test_tc_matches_exact_mode_multi_partition(ctx, port):
         want = port.assign_keys(c["K"][1:], c["cent"])
         assert np.array_equal(at, want) and np.array_equal(ae, want)
         assert np.array_equal(it.idx, ie.idx)
+
+
+@pytest.mark.parametrize("C", [1024, 100, 16384])
+def test_tc_assignment_f32_keys_bit_exact(ctx, port, C):
+    """Host f32 builds (build_context_store's keys are not bf16-representable
+    after de-RoPE) on the tensor cores: keys split into two bf16 terms, the
+    bound widened for the split, ambiguous keys re-scored from the f32 rows --
+    assignments equal the reference's assign_keys on the f32 keys, and equal
+    the fp64 kernel's."""
+    rs = np.random.RandomState(C + 7)
+    n = 12001
+    cent = unit_rows(rs.randn(C, 128))
+    K = (rs.randn(n, 128) * 2).astype(np.float32)       # f32 keys (not bf16-exact)
+    K[5] = 0.0
+    K[6] = cent[min(3, C - 1)] * np.float32(3.0)          # on a centroid
+    V = rs.randn(n, 128).astype(np.float32)
+    part = sb.Partition(cent, ctx)
+    outs = []
+    for tc in (1, 0):
+        ctx.set_option("assign_f32_tc", tc)
+        try:
+            L = sb.Layer([n], 128, C, 1, 2047, ctx)
+            L.build([part], K, V, K)
+            ctx.synchronize()
+            used, refined = L.assign_info()
+            assert used == bool(tc)
+            outs.append(L.read_index(0)[0])
+        finally:
+            ctx.set_option("assign_f32_tc", 1)
+    want = port.assign_keys(K[1:], cent)
+    assert np.array_equal(outs[0], want)
+    assert np.array_equal(outs[1], want)
