@@ -73,6 +73,12 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-c1", action="store_true", help="skip the C1-shape sub-line")
     ap.add_argument("--no-qmodel", action="store_true", help="skip the Q-model router sub-line")
+    ap.add_argument("--ranks-on-one-gpu", action="store_true",
+                    help="smoke test of the N > 1 plumbing on a one-GPU box: every rank uses device 0 "
+                         "(the numbers are not a scaling measurement; --exchange p2p only)")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: output exchange fused into the combine kernel over peer memory "
+                         "(saap_p2p), or the NCCL all-gather + permute (saap_comm)")
     ap.add_argument("--router", default="centroid", choices=["centroid", "qmodel"],
                     help="BucketRouter plugin: CentroidRouter (de-roped) or QModelRouter "
                          "(qmodel_init weights of the reference's shape, hidden 1024)")
@@ -360,13 +366,13 @@ def ours(a):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if a.ranks_on_one_gpu else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
         # host plumbing only (NCCL id hand-off, barriers, max over ranks); the
         # data path is the library's NCCL communicator (saap_comm)
         dist.init_process_group("gloo")
-    from paper_2502_08246_b200.shard import Comm, HeadShard, unique_id
+    from paper_2502_08246_b200.shard import P2P, Comm, HeadShard, unique_id
     sh = HeadShard(rank, world, a.kv_heads, a.batch)
     heads_local, h0 = sh.heads_local, sh.head0
     G = a.q_heads // a.kv_heads
@@ -377,11 +383,17 @@ def ours(a):
     stream = torch.cuda.Stream()
     ctx = sb.Context(local)
     ctx.set_stream(stream.cuda_stream)
-    comm = None
-    if world > 1:
+    comm = p2p = None
+    if world > 1 and a.exchange == "nccl":
         box = [unique_id() if rank == 0 else None]
         dist.broadcast_object_list(box, src=0)
         comm = Comm(ctx, world, rank, box[0])
+    if world > 1 and a.exchange == "p2p":
+        # fused exchange: IPC handles over the gloo plumbing, peers mapped once
+        p2p = P2P(ctx, world, rank, a.batch * a.kv_heads * (a.q_heads // a.kv_heads) * a.dim * 4)
+        hs = [None] * world
+        dist.all_gather_object(hs, p2p.handle())
+        p2p.open(hs)
     dev = torch.device("cuda", local)
     cfg = sb.SparseAttnConfig(a.probes, 128, sb.DenseWindow(a.sink, a.recent))
 
@@ -467,9 +479,19 @@ def ours(a):
         if comm is not None:
             comm.allgather_heads(step_out, sh, G, d, out_full)
 
-    # eager warm-up sizes the scratch, then capture one graph per layer
-    for lay in layers + imb:
+    # fused exchange: while attached, a step's combine delivers every slot's
+    # rows to all ranks' full buffers; the step waits for one step's arrivals
+    p2p_arrivals = world * n_groups * ((G + 3) // 4)
+
+    def sparse_exchange_step(lay):
         sparse_step(lay)
+        p2p.wait(p2p_arrivals)
+
+    # eager warm-up sizes the scratch, then capture one graph per layer
+    if p2p is not None:
+        p2p.attach(sh)
+    for lay in layers + imb:
+        (sparse_exchange_step if p2p is not None else sparse_step)(lay)
         if not a.no_dense:
             dense_step(lay)
     ctx.synchronize()
@@ -485,8 +507,16 @@ def ours(a):
             kernels_per_step = ctx.launch_count - n0  # our kernels in one step's graph
         return g
 
-    graphs = [capture(sparse_step, lay) for lay in layers]
-    igraphs = [capture(sparse_step, lay) for lay in imb]
+    if p2p is not None:
+        graphs = [capture(sparse_exchange_step, lay) for lay in layers]
+        igraphs = [capture(sparse_exchange_step, lay) for lay in imb]
+        kernels_per_step = None
+        capture(sparse_step, layers[0])  # (count our kernels of one plain step)
+        kernels_per_step += 1  # + the arrival wait
+        p2p.detach()  # the graphs keep the delivering combine; eager steps below do not deliver
+    else:
+        graphs = [capture(sparse_step, lay) for lay in layers]
+        igraphs = [capture(sparse_step, lay) for lay in imb]
     dgraphs = [capture(dense_step, lay) for lay in layers] if not a.no_dense else []
 
     clock = ClockSampler(local)
@@ -525,7 +555,7 @@ def ours(a):
     if not a.no_dense:
         ms_dense = timed(lambda i: dgraphs[i % len(dgraphs)].launch(), max(10, a.steps // 5),
                          a.warmup)
-    ms_gather = timed(lambda i: gather(), a.steps, a.warmup) if world > 1 else None
+    ms_gather = timed(lambda i: gather(), a.steps, a.warmup) if comm is not None else None
 
 
     # ---- per-kernel device time (eager, events around the kernels)
@@ -675,6 +705,9 @@ def ours(a):
         "gpu_launches": int((kernels_per_step + (1 if world > 1 else 0)) * a.steps),
         "kernels_per_step": int(kernels_per_step) + (1 if world > 1 else 0),
         "comm": comm.info() if comm is not None else None,
+        "ranks_share_one_gpu": True if a.ranks_on_one_gpu and world > 1 else None,
+        "exchange": None if world == 1 else ("fused combine -> peer-memory stores (saap_p2p)"
+                                             if p2p is not None else "NCCL all-gather + permute (saap_comm)"),
         "setup_s": round(t_setup, 1),
         "prefill_build_ms_per_layer": round(float(np.mean([l.t_build_ms for l in layers])), 2),
         "prefill": {
@@ -696,6 +729,10 @@ def ours(a):
     if comm is not None:
         torch.cuda.synchronize()
         comm.close()
+    if p2p is not None:
+        torch.cuda.synchronize()
+        dist.barrier()  # peers stop using this rank's mapping first
+        p2p.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -395,6 +395,31 @@ SAAP_API int saap_allgather_heads(saap_ctx* ctx, saap_comm* comm, const float* o
                                   uint64_t batch, uint64_t heads_local, uint64_t G, uint64_t dim,
                                   float* out_full_dev);
 
+/* Fused output exchange over peer memory (no collective call): the step's
+ * combine kernel stores every finished slot's rows straight into each rank's
+ * full output buffer [batch][kv_heads][G][d] (CUDA IPC mappings: NVLink P2P
+ * stores between GPUs) and bumps each rank's arrival counter (system-scope
+ * release); saap_p2p_wait orders the stream after every rank's rows landed.
+ * Setup: create (allocates this rank's full buffer), exchange the 64-byte
+ * handles over any channel (like the NCCL id), open, attach to the context.
+ * While attached, decode steps on the context deliver this way. */
+typedef struct saap_p2p saap_p2p;
+SAAP_API int saap_p2p_create(saap_ctx* ctx, int nranks, int rank, uint64_t full_bytes, saap_p2p** out);
+SAAP_API int saap_p2p_handle(saap_p2p* p, uint8_t* handle64);
+/* all_handles: nranks x 64 bytes in rank order (this rank's own entry unused). */
+SAAP_API int saap_p2p_open(saap_p2p* p, const uint8_t* all_handles);
+SAAP_API int saap_p2p_buffer(saap_p2p* p, void** full_out_dev);
+/* Layout of this rank's groups in the full buffer: group g = seq * heads_local
+ * + local head; global head = head0 + local head.  p = NULL detaches. */
+SAAP_API int saap_p2p_attach(saap_ctx* ctx, saap_p2p* p, uint64_t heads_local, uint64_t head0,
+                             uint64_t kv_heads);
+/* Waits (on the context stream) until `arrivals` more slot deliveries reached
+ * this rank (nranks x query slots per rank for one step); graph-capturable. */
+SAAP_API int saap_p2p_wait(saap_ctx* ctx, saap_p2p* p, uint64_t arrivals);
+/* Copies this rank's full buffer to host memory (after the context stream). */
+SAAP_API int saap_p2p_read(saap_p2p* p, void* host, uint64_t bytes);
+SAAP_API int saap_p2p_destroy(saap_p2p* p);
+
 /* ---- CUDA graphs over the asynchronous calls --------------------------- */
 SAAP_API int saap_graph_begin(saap_ctx* ctx);
 SAAP_API int saap_graph_end(saap_ctx* ctx, saap_graph** out);

@@ -189,6 +189,10 @@ struct CombineArgs {
     uint32_t poll_ns;        // sleep between polls without progress
     float* out;
     unsigned long long* tl;  // debug step timeline (null: off)
+    // fused output exchange (saap_p2p): every rank's full buffer and counter
+    float* const* p2p_out;   // [p2p_n] (null: off)
+    uint32_t* const* p2p_flag;
+    uint32_t p2p_n, p2p_hl, p2p_h0, p2p_kvh;
 };
 
 // Decode tiles live in shared memory as 8-row groups [group][half][8 rows][HALF

@@ -22,6 +22,7 @@ void launch_route_approx(int D, const ApproxArgs& a, uint32_t n_slots, cudaStrea
 void launch_route_score(const RouteArgs& a, uint32_t n_groups, cudaStream_t st);
 void launch_decode(int D, const DecodeMaps& m, const DecodeArgs& a, int grid, cudaStream_t st, bool tc);
 void launch_combine(int D, const CombineArgs& ca, uint32_t n_qslots, cudaStream_t st);
+void p2p_fill(saap_ctx* c, CombineArgs& ca);
 void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st, uint32_t n_slots = 0);
 void launch_assign_exact(int D, bool bf16_keys, const TileDesc* tiles, uint32_t n_tiles,
                          const void* keys, const uint64_t* key_row0, const double* const* cent64,
@@ -714,6 +715,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     ca.out = out;
     ca.tl = c->tl;
     ca.poll_ns = c->opt.combine_poll_ns;
+    if (c->p2p) p2p_fill(c, ca);
     launch_combine((int)D, ca, (uint32_t)qslots, st);
     c->launches += 2;
     if (e2) {

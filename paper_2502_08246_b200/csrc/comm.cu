@@ -17,8 +17,10 @@
 
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "api.cuh"
+#include "args.cuh"
 
 namespace saap_b200 {
 
@@ -101,6 +103,42 @@ struct saap_comm {
     size_t cap = 0;  // bytes per rank block (send), recv = nranks * cap
     ncclWindow_t wsend = nullptr, wrecv = nullptr;
 };
+
+// fused output exchange over peer memory (CUDA IPC mappings)
+struct saap_p2p {
+    saap_ctx* ctx = nullptr;
+    int nranks = 0, rank = 0;
+    uint64_t bytes = 0;          // full output bytes (the counter sits after them)
+    char* base = nullptr;        // this rank's allocation: [full outputs | counter | expected]
+    std::vector<char*> peer;     // mapped bases, rank order (own = base)
+    float** d_out = nullptr;     // device [nranks] full-buffer pointers
+    uint32_t** d_flag = nullptr; // device [nranks] counter pointers
+    bool opened = false;
+};
+
+namespace saap_b200 {
+namespace {
+constexpr uint64_t kP2pTail = 256;  // counter + expected-arrivals word after the outputs
+__global__ void p2p_wait_kernel(volatile uint32_t* flag, uint32_t* expect, uint32_t arrivals) {
+    const uint32_t target = *expect + arrivals;
+    uint32_t v;
+    do {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    } while ((int32_t)(v - target) < 0);
+    *expect = target;
+}
+}  // namespace
+
+void p2p_fill(saap_ctx* c, CombineArgs& ca) {
+    saap_p2p* p = c->p2p;
+    ca.p2p_out = p->d_out;
+    ca.p2p_flag = p->d_flag;
+    ca.p2p_n = (uint32_t)p->nranks;
+    ca.p2p_hl = c->p2p_hl;
+    ca.p2p_h0 = c->p2p_h0;
+    ca.p2p_kvh = c->p2p_kvh;
+}
+}  // namespace saap_b200
 
 namespace {
 
@@ -253,6 +291,136 @@ int saap_allgather_heads(saap_ctx* c, saap_comm* m, const float* out_local, uint
                                                         (uint32_t)heads_local, (uint32_t)(row / 4));
         SAAP_CUDA(cudaGetLastError());
         c->launches++;
+    });
+}
+
+int saap_p2p_create(saap_ctx* c, int nranks, int rank, uint64_t full_bytes, saap_p2p** out) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(out, "p2p: out");
+        if (nranks < 1 || rank < 0 || rank >= nranks)
+            invalid("p2p: rank " + std::to_string(rank) + " of " + std::to_string(nranks));
+        if (full_bytes == 0 || full_bytes % 16) invalid("p2p: full buffer bytes must be a positive multiple of 16");
+        auto* p = new saap_p2p;
+        p->ctx = c;
+        p->nranks = nranks;
+        p->rank = rank;
+        p->bytes = full_bytes;
+        if (cudaMalloc(&p->base, full_bytes + kP2pTail) != cudaSuccess) {
+            delete p;
+            fail(SAAP_ERR_CUDA, "p2p: cudaMalloc");
+        }
+        SAAP_CUDA(cudaMemset(p->base, 0, full_bytes + kP2pTail));
+        *out = p;
+    });
+}
+
+int saap_p2p_handle(saap_p2p* p, uint8_t* handle64) {
+    return guard([&] {
+        need(p, "p2p");
+        need(handle64, "p2p: handle");
+        DeviceGuard dg(p->ctx);
+        cudaIpcMemHandle_t h;
+        SAAP_CUDA(cudaIpcGetMemHandle(&h, p->base));
+        static_assert(sizeof(h) == 64, "IPC handle size");
+        std::memcpy(handle64, &h, 64);
+    });
+}
+
+int saap_p2p_open(saap_p2p* p, const uint8_t* all) {
+    return guard([&] {
+        need(p, "p2p");
+        need(all, "p2p: handles");
+        DeviceGuard dg(p->ctx);
+        if (p->opened) invalid("p2p: already open");
+        p->peer.assign(p->nranks, nullptr);
+        for (int r = 0; r < p->nranks; ++r) {
+            if (r == p->rank) {
+                p->peer[r] = p->base;
+                continue;
+            }
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, all + 64 * (size_t)r, 64);
+            void* q = nullptr;
+            SAAP_CUDA(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+            p->peer[r] = (char*)q;
+        }
+        std::vector<float*> outs(p->nranks);
+        std::vector<uint32_t*> flags(p->nranks);
+        for (int r = 0; r < p->nranks; ++r) {
+            outs[r] = (float*)p->peer[r];
+            flags[r] = (uint32_t*)(p->peer[r] + p->bytes);
+        }
+        SAAP_CUDA(cudaMalloc(&p->d_out, p->nranks * sizeof(float*)));
+        SAAP_CUDA(cudaMalloc(&p->d_flag, p->nranks * sizeof(uint32_t*)));
+        SAAP_CUDA(cudaMemcpy(p->d_out, outs.data(), p->nranks * sizeof(float*), cudaMemcpyHostToDevice));
+        SAAP_CUDA(cudaMemcpy(p->d_flag, flags.data(), p->nranks * sizeof(uint32_t*), cudaMemcpyHostToDevice));
+        p->opened = true;
+    });
+}
+
+int saap_p2p_buffer(saap_p2p* p, void** full_out) {
+    return guard([&] {
+        need(p, "p2p");
+        need(full_out, "p2p: out");
+        *full_out = p->base;
+    });
+}
+
+int saap_p2p_attach(saap_ctx* c, saap_p2p* p, uint64_t heads_local, uint64_t head0, uint64_t kv_heads) {
+    return guard([&] {
+        need(c, "context");
+        if (c->capturing) invalid("saap_p2p_attach during graph capture");
+        if (p && !p->opened) invalid("p2p: attach before open");
+        if (p && (heads_local == 0 || head0 + heads_local > kv_heads))
+            invalid("p2p: heads " + std::to_string(head0) + "+" + std::to_string(heads_local) + " of " +
+                    std::to_string(kv_heads));
+        c->p2p = p;
+        c->p2p_hl = (uint32_t)heads_local;
+        c->p2p_h0 = (uint32_t)head0;
+        c->p2p_kvh = (uint32_t)kv_heads;
+        // saved host-API step graphs hold the old combine arguments
+        for (auto& g : c->host_graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+        c->host_graphs.clear();
+    });
+}
+
+int saap_p2p_wait(saap_ctx* c, saap_p2p* p, uint64_t arrivals) {
+    return guard([&] {
+        DeviceGuard dg(c);
+        need(p, "p2p");
+        if (!p->opened) invalid("p2p: wait before open");
+        uint32_t* flag = (uint32_t*)(p->base + p->bytes);
+        p2p_wait_kernel<<<1, 1, 0, c->stream>>>(flag, flag + 1, (uint32_t)arrivals);
+        SAAP_CUDA(cudaGetLastError());
+        c->launches++;
+    });
+}
+
+int saap_p2p_read(saap_p2p* p, void* host, uint64_t bytes) {
+    return guard([&] {
+        need(p, "p2p");
+        need(host, "p2p: host");
+        DeviceGuard dg(p->ctx);
+        if (bytes > p->bytes) invalid("p2p: read past the full buffer");
+        SAAP_CUDA(cudaStreamSynchronize(p->ctx->stream));
+        SAAP_CUDA(cudaMemcpy(host, p->base, bytes, cudaMemcpyDeviceToHost));
+    });
+}
+
+int saap_p2p_destroy(saap_p2p* p) {
+    return guard([&] {
+        if (!p) return;
+        DeviceGuard dg(p->ctx);
+        cudaStreamSynchronize(p->ctx->stream);
+        if (p->ctx->p2p == p) p->ctx->p2p = nullptr;
+        for (int r = 0; r < (int)p->peer.size(); ++r)
+            if (r != p->rank && p->peer[r]) cudaIpcCloseMemHandle(p->peer[r]);
+        if (p->d_out) cudaFree(p->d_out);
+        if (p->d_flag) cudaFree(p->d_flag);
+        if (p->base) cudaFree(p->base);
+        delete p;
     });
 }
 

@@ -210,9 +210,13 @@ struct saap_scratch {
     size_t cap = 0;
 };
 
+struct saap_p2p;
 struct saap_ctx {
     int device = 0;
     int sm_count = 0;
+    // attached fused output exchange (saap_p2p_attach)
+    saap_p2p* p2p = nullptr;
+    uint32_t p2p_hl = 0, p2p_h0 = 0, p2p_kvh = 0;
     cudaStream_t stream = nullptr;
     // host API: the two query uploads run on parallel branches
     cudaStream_t side = nullptr;

@@ -2724,9 +2724,25 @@ __global__ void __maxnreg__(80) combine_kernel(CombineArgs a) {
         if (a.dyn_cnt) a.dyn_cnt[qsi] = 0;
         a.rd[qsi] = 0;
     }
+    float res[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) res[i] = L > 0.f ? O[i] / L : 0.f;
     if (head < a.G)
 #pragma unroll
-        for (int i = 0; i < PER; ++i) out[i] = L > 0.f ? O[i] / L : 0.f;
+        for (int i = 0; i < PER; ++i) out[i] = res[i];
+    if (a.p2p_out) {
+        // fused exchange: the slot's rows into every rank's full buffer, then
+        // one system-scope arrival per rank (release: fence, then the count)
+        const uint32_t seq = g / a.p2p_hl, lh = g - seq * a.p2p_hl;
+        const size_t fi = (((size_t)seq * a.p2p_kvh + a.p2p_h0 + lh) * a.G + head) * D + (e0 % D);
+        if (head < a.G)
+            for (uint32_t r = 0; r < a.p2p_n; ++r)
+                *reinterpret_cast<float4*>(a.p2p_out[r] + fi) = make_float4(res[0], res[1], res[2], res[3]);
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (uint32_t r = 0; r < a.p2p_n; ++r) atomicAdd_system(a.p2p_flag[r], 1u);
+    }
     if (threadIdx.x == 0) tl_mark(a.tl, 3, false);
 }
 

@@ -119,3 +119,58 @@ class Comm:
             self.close()
         except Exception:
             pass
+
+
+class P2P:
+    """saap_p2p: the fused output exchange over peer memory.  The step's
+    combine kernel stores every finished slot's rows into each rank's full
+    output buffer [batch][kv_heads][G][d] and bumps its arrival counter;
+    `wait` orders the context stream after one step's deliveries."""
+
+    def __init__(self, ctx: Context, world: int, rank: int, full_bytes: int):
+        self.ctx, self.world, self.rank, self.full_bytes = ctx, world, rank, full_bytes
+        h = C.c_void_p()
+        _check(lib().saap_p2p_create(ctx.h, C.c_int(world), C.c_int(rank), _u64(full_bytes), C.byref(h)))
+        self.h = h
+
+    def handle(self) -> bytes:
+        buf = (C.c_uint8 * 64)()
+        _check(lib().saap_p2p_handle(self.h, buf))
+        return bytes(buf)
+
+    def open(self, handles):
+        if len(handles) != self.world or any(len(x) != 64 for x in handles):
+            raise ValueError("one 64-byte handle per rank")
+        blob = b"".join(handles)
+        _check(lib().saap_p2p_open(self.h, (C.c_uint8 * len(blob)).from_buffer_copy(blob)))
+
+    def buffer(self) -> int:
+        p = C.c_void_p()
+        _check(lib().saap_p2p_buffer(self.h, C.byref(p)))
+        return p.value
+
+    def attach(self, shard: HeadShard):
+        _check(lib().saap_p2p_attach(self.ctx.h, self.h, _u64(shard.heads_local), _u64(shard.head0),
+                                     _u64(shard.kv_heads)))
+
+    def detach(self):
+        _check(lib().saap_p2p_attach(self.ctx.h, None, _u64(0), _u64(0), _u64(0)))
+
+    def wait(self, arrivals: int):
+        _check(lib().saap_p2p_wait(self.ctx.h, self.h, _u64(arrivals)))
+
+    def read(self, shape) -> np.ndarray:
+        out = np.empty(shape, np.float32)
+        _check(lib().saap_p2p_read(self.h, out.ctypes.data_as(C.c_void_p), _u64(out.nbytes)))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().saap_p2p_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
