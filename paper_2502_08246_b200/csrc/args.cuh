@@ -219,7 +219,7 @@ struct QModelArgs {
     double* hid;               // [groups][G][h] scratch: post-ReLU hidden rows
     const uint32_t* slot_g;    // optional [n_slots][kQmSlot] groups sharing one model (pad ~0u)
     uint32_t logits_variant;   // qm_logits geometry (rows per thread, CTA width); see launch_qmodel_probs
-    uint32_t w2_finite;        // 1: W2 finite, the zero-skip test of mm (qmodel.cpp:30-51) can go
+    uint32_t w_finite;         // 1: W1 and W2 finite, the zero-skip test of mm (qmodel.cpp:30-51) can go
 };
 #ifndef SAAP_QM_SLOT
 #define SAAP_QM_SLOT 2

@@ -271,8 +271,8 @@ void bind_routers(saap_layer* L, const saap_router* const* routers, int& mode, i
             p[3 * g + 1] = rs[g]->model->w2;
             p[3 * g + 2] = rs[g]->model->vec;
         }
-        L->qm_w2_finite = true;
-        for (size_t g = 0; g < L->n_groups; ++g) L->qm_w2_finite = L->qm_w2_finite && rs[g]->model->w2_finite;
+        L->qm_w_finite = true;
+        for (size_t g = 0; g < L->n_groups; ++g) L->qm_w_finite = L->qm_w_finite && rs[g]->model->w_finite;
         if (!L->d_qm) L->d_qm = (const double**)(dmalloc<void*>(3 * L->n_groups));
         SAAP_CUDA(cudaMemcpy(L->d_qm, p.data(), p.size() * sizeof(void*), cudaMemcpyHostToDevice));
         // slots: contexts routed by one Q-model share its W2 loads
@@ -575,7 +575,7 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
         if (mode == 2) {
             QModelArgs qa{};
             qa.logits_variant = c->opt.qm_logits;
-            qa.w2_finite = qm_finite ? 1u : 0u;
+            qa.w_finite = qm_finite ? 1u : 0u;
             qa.q = q_route;
             qa.prm = qm;
             qa.G = (uint32_t)G;
@@ -1041,8 +1041,9 @@ int saap_qmodel_create(saap_ctx* c, uint64_t d, uint64_t h, uint64_t C, const do
         for (int i = 0; i < 5; ++i)
             SAAP_CUDA(cudaMemcpy(m->vec + i * h, parts[i], h * 8, cudaMemcpyHostToDevice));
         SAAP_CUDA(cudaMemcpy(m->vec + 5 * h, b2, C * 8, cudaMemcpyHostToDevice));
-        m->w2_finite = true;
-        for (uint64_t i = 0; i < h * C && m->w2_finite; ++i) m->w2_finite = std::isfinite(w2[i]);
+        m->w_finite = true;
+        for (uint64_t i = 0; i < h * C && m->w_finite; ++i) m->w_finite = std::isfinite(w2[i]);
+        for (uint64_t i = 0; i < d * h && m->w_finite; ++i) m->w_finite = std::isfinite(w1[i]);
         *out = m;
     });
 }
@@ -2516,7 +2517,7 @@ static void sparse_dev(saap_ctx* c, const saap_layer* Lc, const saap_router* con
                    mode == 2 ? L->d_qm_slots : nullptr, mode == 2 ? L->n_qm_slots : 0,
                    mode == 4 ? given : nullptr,
                    mode == 1 && !L->h_route_slots.empty() ? (const ApproxSlot*)L->h_route_slots.data() : nullptr,
-                   mode == 2 && L->qm_w2_finite);
+                   mode == 2 && L->qm_w_finite);
 }
 
 int saap_sparse_attention_dev(saap_ctx* c, const saap_layer* L, const saap_router* const* routers,

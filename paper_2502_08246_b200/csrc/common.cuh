@@ -305,7 +305,7 @@ struct saap_qmodel {
     double* w1 = nullptr;  // d x h
     double* w2 = nullptr;  // h x C
     double* vec = nullptr; // b1, gamma, beta, mean, var (5 x h) then b2 (C)
-    bool w2_finite = false;  // every W2 weight finite: a zero hidden unit's term adds exactly +-0
+    bool w_finite = false;   // every W1 / W2 weight finite: a zero input's term adds exactly +-0
 };
 
 // Q-model trainer (qtrain.cu): model + TrainerState resident on the device.
@@ -403,7 +403,7 @@ struct saap_layer {
     float* d_cmax = nullptr;           // per group partition cmax
     void* d_route_slots = nullptr;     // ApproxSlot[]: approximate-scoring slots (<= 8 contexts of one partition)
     uint32_t n_route_slots = 0;
-    bool qm_w2_finite = false;  // every bound Q-model's W2 is finite
+    bool qm_w_finite = false;   // every bound Q-model's weights are finite
     std::vector<uint8_t> h_route_slots;  // host copy of the ApproxSlot table (inlined into the routing launch)
     const double** d_qm = nullptr;     // per group: w1, w2, vec (3 pointers)
     uint32_t* d_qm_slots = nullptr;    // [n_qm_slots][kQmSlot] contexts sharing a Q-model

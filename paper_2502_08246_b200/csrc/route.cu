@@ -25,6 +25,7 @@ constexpr int kQmP = 16;    // logits: weights per pipeline stage (two stages in
 // softmax.  Every chain keeps the reference's order; loads run ahead of it.
 constexpr int kQmT = 128;
 
+template <bool SKIP0>
 __global__ void __launch_bounds__(kQmT) qm_hidden_kernel(QModelArgs a) {
     extern __shared__ __align__(16) double xs[];  // kQmRows x d
     const uint32_t g = blockIdx.x, j = blockIdx.y * kQmT + threadIdx.x;
@@ -59,7 +60,11 @@ __global__ void __launch_bounds__(kQmT) qm_hidden_kernel(QModelArgs a) {
 #pragma unroll
                 for (int i = 0; i < kQmRows; ++i) {
                     const double av = xs[i * a.d + k + u];
-                    if ((uint32_t)i < nr && av != 0.0) z[i] = __dadd_rn(z[i], __dmul_rn(av, wa[u]));
+                    if (SKIP0) {
+                        if ((uint32_t)i < nr && av != 0.0) z[i] = __dadd_rn(z[i], __dmul_rn(av, wa[u]));
+                    } else {
+                        z[i] = __dadd_rn(z[i], __dmul_rn(av, wa[u]));
+                    }
                 }
 #pragma unroll
             for (int u = 0; u < P; ++u) wa[u] = wb[u];
@@ -215,15 +220,17 @@ void launch_qmodel_probs(const QModelArgs& a, uint32_t n_groups, cudaStream_t st
     const size_t sm1 = (size_t)kQmRows * a.d * sizeof(double);
     static size_t cfg1 = 0;
     if (sm1 > 48 * 1024 && sm1 > cfg1) {
-        SAAP_CUDA(cudaFuncSetAttribute(qm_hidden_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+        SAAP_CUDA(cudaFuncSetAttribute(qm_hidden_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
+        SAAP_CUDA(cudaFuncSetAttribute(qm_hidden_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1));
         cfg1 = sm1;
     }
-    qm_hidden_kernel<<<dim3(n_groups, (a.h + kQmT - 1) / kQmT), kQmT, sm1, st>>>(a);
+    if (a.w_finite) qm_hidden_kernel<false><<<dim3(n_groups, (a.h + kQmT - 1) / kQmT), kQmT, sm1, st>>>(a);
+    else qm_hidden_kernel<true><<<dim3(n_groups, (a.h + kQmT - 1) / kQmT), kQmT, sm1, st>>>(a);
     // logits geometry (a.logits_variant): rows per thread x CTA width
     const uint32_t ns = a.slot_g ? n_slots : n_groups;
     switch (a.logits_variant) {
-        case 0:  // default: without the zero-skip test when W2 is finite (same sums)
-            if (a.w2_finite) launch_qm_logits<4, 16, 256, false>(a, ns, st);
+        case 0:  // default: without the zero-skip test when the weights are finite (same sums)
+            if (a.w_finite) launch_qm_logits<4, 16, 256, false>(a, ns, st);
             else launch_qm_logits<8, 16, 256>(a, ns, st);
             break;
         case 1: launch_qm_logits<2, 16, 256, false>(a, ns, st); break;

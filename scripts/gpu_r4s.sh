@@ -19,7 +19,7 @@ lay = bench.build_c3_layer(sb, torch, ctx, a, 0, 0.0, 8, 0, dev, stream, len(os.
 cfg = sb.SparseAttnConfig(a.probes, 128, sb.DenseWindow(1, a.recent))
 out = torch.empty(64, 4, 128, device=dev); stats = torch.zeros(64, 3, dtype=torch.int64, device=dev)
 sel_ref = None
-for v in [7, 1, 2, 3, 4, 5]:
+for v in [0]:
     ctx.set_option("qm_logits", v)
     sel = torch.empty(64, 32, dtype=torch.int32, device=dev)
     lay.L.sparse_attention_dev(lay.routers, lay.qr_t, lay.qd_t, 4, cfg, out, stats, selected=sel)
