@@ -68,6 +68,7 @@ struct RouteArgs {
 constexpr int kSlotGroups = 8;  // contexts per approximate-scoring slot
 struct ApproxSlot {
     const float* centT;            // d x C f32 of the slot's partition
+    const float* centB;            // [8][d][C/8] blocked copy (cluster routing; null if C % 8)
     uint32_t count;                // member contexts (<= kSlotGroups)
     uint32_t group[kSlotGroups];
     uint32_t pad;

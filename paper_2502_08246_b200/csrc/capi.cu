@@ -255,6 +255,7 @@ void bind_routers(saap_layer* L, const saap_router* const* routers, int& mode, i
             for (size_t k0 = 0; k0 < members[u].size(); k0 += kSlotGroups) {
                 ApproxSlot sl{};
                 sl.centT = uniq[u]->centT;
+                sl.centB = uniq[u]->centB;
                 sl.count = (uint32_t)std::min<size_t>(kSlotGroups, members[u].size() - k0);
                 for (uint32_t k = 0; k < sl.count; ++k) sl.group[k] = members[u][k0 + k];
                 tab.push_back(sl);
@@ -1002,6 +1003,15 @@ int saap_partition_create(saap_ctx* c, const float* cent, uint64_t C, uint64_t d
         SAAP_CUDA(cudaMemcpy(p->cent, cent, C * d * 4, cudaMemcpyHostToDevice));
         SAAP_CUDA(cudaMemcpy(p->centT, t.data(), C * d * 4, cudaMemcpyHostToDevice));
         SAAP_CUDA(cudaMemcpy(p->cent64, d64.data(), C * d * 8, cudaMemcpyHostToDevice));
+        if (C % kClusterCtas == 0) {  // the cluster router's slabs, contiguous per rank
+            const uint64_t S = C / kClusterCtas;
+            std::vector<float> b(C * d);
+            for (uint64_t r = 0; r < (uint64_t)kClusterCtas; ++r)
+                for (uint64_t j = 0; j < d; ++j)
+                    for (uint64_t s2 = 0; s2 < S; ++s2) b[(r * d + j) * S + s2] = cent[(r * S + s2) * d + j];
+            p->centB = dmalloc<float>(C * d);
+            SAAP_CUDA(cudaMemcpy(p->centB, b.data(), C * d * 4, cudaMemcpyHostToDevice));
+        }
         *out = p;
     });
 }
@@ -1012,6 +1022,7 @@ int saap_partition_destroy(saap_partition* p) {
         cudaSetDevice(p->ctx->device);
         dfree(p->cent);
         dfree(p->centT);
+        dfree(p->centB);
         dfree(p->cent64);
         delete p;
     });

@@ -295,6 +295,7 @@ struct saap_partition {
     float* cent = nullptr;     // C x d f32 (device)
     double* cent64 = nullptr;  // C x d fp64 (device, exact assignment)
     float* centT = nullptr;    // d x C f32 (device, routing slabs; exact in fp64)
+    float* centB = nullptr;    // [8][d][C/8] f32: centT blocked by cluster rank (one bulk copy per slab)
     float cmax = 0.f;          // max centroid L2 norm (routing error bound)
     std::vector<float> host;   // kept for validation / read-back
 };

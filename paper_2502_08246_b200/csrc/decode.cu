@@ -903,8 +903,12 @@ __global__ void __launch_bounds__(kClusterThreads, 1) route_cluster_kernel(Clust
     const uint32_t qbytes = a.G * D * 4;
     if (tid == 0) mbar_arrive_expect_tx(&bar, D * S * 4 + ng * qbytes);
     __syncthreads();
-    for (uint32_t j = tid; j < D; j += NT)
-        bulk_g2s(slab + (size_t)j * S, sl.centT + (size_t)j * C + rank * S, S * 4, &bar);
+    if (sl.centB) {  // the rank's slab is contiguous: one bulk copy
+        if (tid == 0) bulk_g2s(slab, sl.centB + (size_t)rank * D * S, D * S * 4, &bar);
+    } else {
+        for (uint32_t j = tid; j < D; j += NT)
+            bulk_g2s(slab + (size_t)j * S, sl.centT + (size_t)j * C + rank * S, S * 4, &bar);
+    }
     for (uint32_t k = tid; k < ng; k += NT)
         bulk_g2s(qs + (size_t)k * a.G * D, a.q_route + (size_t)sl.group[k] * a.G * D, qbytes, &bar);
     GroupMeta gm{};
