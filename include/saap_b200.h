@@ -437,12 +437,21 @@ SAAP_API int saap_ctx_timing(saap_ctx* ctx, double* route_plan_ms, double* atten
 /* Kernel launches issued by this context so far (bench "gpu_launches"). */
 SAAP_API int saap_ctx_launch_count(saap_ctx* ctx, uint64_t* out);
 /* Tuning and diagnostics, per context (no environment variables are read):
- *   chunk (8), chunk_dense (16)   work-stream tiles per decode ticket
- *   tail_per_cta (1)              guided-tail singles per CTA
+ *   chunk (8), chunk_dense (16)   largest decode claim (tiles), sparse / dense
+ *   min_chunk (4)                 smallest guided claim at the stream's end
+ *   claim_lead (3), fetch_lead (2) claim the next chunk / fetch its records
+ *                                 when this many tiles of the current are left
+ *   inflight (0)                  0: ring depth; else max tiles issued and unconsumed
+ *   tail_per_cta (1)              (unused since guided claims)
  *   decode_poll_ns (100), combine_poll_ns (1000)   polling back-off
  *   decode_wait (0)               1: decode starts after routing (no overlap)
+ *   decode_tc (0)                 1: tcgen05 decode consumers (d = 128; measured slower)
  *   cluster_route (1)             0: general routing path only
+ *   assign_f32_tc (1)             0: f32 assignment keys on the fp64 kernel
+ *   qm_logits (0)                 Q-model logits geometry (sweeps)
  *   host_graph (1)                0: saap_sparse_attention never replays graphs
+ *   debug_skip (0)                profiling only, wrong outputs: 1 no consumer math,
+ *                                 2 no K/V loads
  *   trace_step / trace_decode / trace_plan (0)     saap_debug_*_trace buffers
  * Unknown names / out-of-range values: SAAP_ERR_INVALID_ARGUMENT. */
 SAAP_API int saap_ctx_set_option(saap_ctx* ctx, const char* name, int64_t value);
