@@ -1,0 +1,8 @@
+#!/bin/bash
+# A/B of two library builds on one box (abtest/lib_A.so, abtest/lib_B.so), alternating
+for r in 1 2 3; do
+  for v in A B; do
+    cp abtest/lib_$v.so paper_2502_08246_b200/libsaap_b200.so
+    echo "$v $(timeout 300 python scripts/sweep_opts.py --steps 300 "" 2>&1 | tail -1)"
+  done
+done
