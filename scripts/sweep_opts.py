@@ -22,10 +22,11 @@ def main():
     ap.add_argument("--given", action="store_true", help="caller-selected lists (no routing kernel)")
     ap.add_argument("--probes", type=int, default=32)
     ap.add_argument("--ctx-len", type=int, default=131072)
+    ap.add_argument("--batch", type=int, default=8)
     args = ap.parse_args()
     import torch
     import paper_2502_08246_b200 as sb
-    a = argparse.Namespace(ctx_len=args.ctx_len, batch=8, kv_heads=8, q_heads=32, dim=128, buckets=1024,
+    a = argparse.Namespace(ctx_len=args.ctx_len, batch=args.batch, kv_heads=8, q_heads=32, dim=128, buckets=1024,
                            probes=args.probes, recent=2047, sink=1, kmeans_iters=10)
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream()
@@ -35,12 +36,12 @@ def main():
     lays = [bench.build_c3_layer(sb, torch, ctx, a, li, args.drift, 8, 0, dev, stream, threads)
             for li in range(2)]
     cfg = sb.SparseAttnConfig(a.probes, 128, sb.DenseWindow(1, a.recent))
-    out = torch.empty(64, 4, 128, device=dev)
-    stats = torch.zeros(64, 3, dtype=torch.int64, device=dev)
+    out = torch.empty(args.batch * 8, 4, 128, device=dev)
+    stats = torch.zeros(args.batch * 8, 3, dtype=torch.int64, device=dev)
 
     if args.given:
         for lay in lays:
-            lay.sel = torch.empty(64, a.probes, dtype=torch.int32, device=dev)
+            lay.sel = torch.empty(args.batch * 8, a.probes, dtype=torch.int32, device=dev)
             lay.L.sparse_attention_dev(lay.routers, lay.qr_t, lay.qd_t, 4, cfg, out, stats,
                                        selected=lay.sel)
         ctx.synchronize()
