@@ -384,16 +384,36 @@ def ours(a):
     ctx = sb.Context(local)
     ctx.set_stream(stream.cuda_stream)
     comm = p2p = None
-    if world > 1 and a.exchange == "nccl":
+    exchange = a.exchange
+    if world > 1 and exchange == "p2p":
+        # fused exchange: IPC handles over the gloo plumbing, peers mapped once;
+        # every rank falls back to the NCCL all-gather if any rank cannot map
+        ok = torch.tensor([1], dtype=torch.int32)
+        mine = None
+        try:
+            p2p = P2P(ctx, world, rank, a.batch * a.kv_heads * (a.q_heads // a.kv_heads) * a.dim * 4)
+            mine = p2p.handle()
+        except Exception as e:  # (reported on stderr; the line says which exchange ran)
+            print(f"rank {rank}: peer-memory exchange unavailable ({e}); using NCCL", file=sys.stderr)
+        hs = [None] * world
+        dist.all_gather_object(hs, mine)  # every rank takes part, mapped or not
+        if any(h is None for h in hs):
+            ok[0] = 0
+        else:
+            try:
+                p2p.open(hs)
+            except Exception as e:
+                print(f"rank {rank}: peer mapping failed ({e}); using NCCL", file=sys.stderr)
+                ok[0] = 0
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            if p2p is not None:
+                p2p.close()
+            p2p, exchange = None, "nccl"
+    if world > 1 and exchange == "nccl":
         box = [unique_id() if rank == 0 else None]
         dist.broadcast_object_list(box, src=0)
         comm = Comm(ctx, world, rank, box[0])
-    if world > 1 and a.exchange == "p2p":
-        # fused exchange: IPC handles over the gloo plumbing, peers mapped once
-        p2p = P2P(ctx, world, rank, a.batch * a.kv_heads * (a.q_heads // a.kv_heads) * a.dim * 4)
-        hs = [None] * world
-        dist.all_gather_object(hs, p2p.handle())
-        p2p.open(hs)
     dev = torch.device("cuda", local)
     cfg = sb.SparseAttnConfig(a.probes, 128, sb.DenseWindow(a.sink, a.recent))
 
