@@ -697,7 +697,8 @@ void enqueue_decode(saap_ctx* c, const DecodeSrc& src, const saap_static_plan* s
     // pre-assigned first chunk per CTA (no atomic before its first loads): with
     // a planner running, CTAs on the SMs it holds start late, so they hold
     // only 2 tiles of reserved work; everything else is claimed from the counter
-    da.chunk_st = plan ? std::max<uint32_t>(1u, std::min<uint32_t>(2u, sp->n_tiles / (uint32_t)grid)) : chunk;
+    const uint32_t cst = c->opt.chunk_st ? c->opt.chunk_st : 2u;  // pre-assigned window tiles per CTA
+    da.chunk_st = plan ? std::max<uint32_t>(1u, std::min<uint32_t>(cst, sp->n_tiles / (uint32_t)grid)) : chunk;
     if (c->opt.trace_decode) {
         da.dtrace = (unsigned long long*)ensure(c, c->dtrace, (size_t)c->sm_count * (128 + kTraceTiles * 64));
         da.dtiles = da.dtrace + (size_t)c->sm_count * 16;
@@ -943,6 +944,7 @@ int saap_ctx_set_option(saap_ctx* c, const char* name, int64_t value) {
         else if (n == "cluster_route") o.cluster_route = clamp(0, 1);
         else if (n == "debug_skip") o.debug_skip = clamp(0, 2);
         else if (n == "min_chunk") o.min_chunk = clamp(1, 16);
+        else if (n == "chunk_st") o.chunk_st = clamp(0, 16);
         else if (n == "claim_lead") o.claim_lead = clamp(0, 32);
         else if (n == "fetch_lead") o.fetch_lead = clamp(0, 32);
         else if (n == "inflight") o.inflight = clamp(0, 8);

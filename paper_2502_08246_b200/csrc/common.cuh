@@ -257,6 +257,7 @@ struct saap_ctx {
         uint32_t chunk_dense = 16;      // ... (dense / full attention)
         uint32_t tail_per_cta = 1;      // (unused since guided claims)
         uint32_t min_chunk = 4;         // smallest guided claim at the stream's end (tiles)
+        uint32_t chunk_st = 0;          // pre-assigned window tiles per decode CTA (0: 2)
         uint32_t claim_lead = 3;        // decode producer: claim when <= this many tiles are left to issue
         uint32_t assign_f32_tc = 1;     // f32 assignment keys on tcgen05 (split keys); 0: fp64 kernel
         uint32_t qm_logits = 0;         // Q-model logits geometry (route.cu launch_qmodel_probs)

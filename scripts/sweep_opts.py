@@ -85,7 +85,7 @@ def main():
         for k in kv:  # back to the defaults for the next setting
             ctx.set_option(k, {"chunk": 8, "chunk_dense": 16, "tail_per_cta": 1, "decode_poll_ns": 100,
                                "combine_poll_ns": 1000, "decode_wait": 0, "cluster_route": 1,
-                               "min_chunk": 4, "claim_lead": 3, "fetch_lead": 2, "inflight": 0, "decode_tc": 0, "qm_logits": 0}.get(k, 0))
+                               "min_chunk": 4, "claim_lead": 3, "fetch_lead": 2, "inflight": 0, "decode_tc": 0, "qm_logits": 0, "chunk_st": 0}.get(k, 0))
     print(json.dumps(res))
 
 
