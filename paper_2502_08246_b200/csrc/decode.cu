@@ -1551,18 +1551,37 @@ __device__ __forceinline__ void decode_producer(const DecodeArgs& a, const Decod
     // read only when the next chunk's records are fetched).
     uint32_t cl_ret = 0, cl_size = 0, hint = pre;
     bool cl_pend = false;
-    auto claim = [&]() {
+    // (false: no ticket now -- the planner has not reserved the tiles a claim
+    // would cover yet; the caller polls)
+    auto claim = [&]() -> bool {
         uint32_t sz = CH;
         if (total != 0xFFFFFFFFu) {
             // the counter has moved on by about one claim per CTA since
             // this CTA's last claim returned `hint`
             const uint32_t seen = hint + P * cl_size;
             const uint32_t rem = total > seen ? total - seen : 0u;
-            sz = max(min(a.min_chunk, CH), min(CH, (rem + 2 * P - 1) / (2 * P)));
+            // a dynamic part of at most a tile per CTA goes out a tile per claim
+            const uint32_t lo = a.n_plan_groups && total - W <= P ? 1u : min(a.min_chunk, CH);
+            sz = max(lo, min(CH, (rem + 2 * P - 1) / (2 * P)));
+        } else if (W < P * a.min_chunk) {
+            // small static part (short contexts, small batches): while the
+            // dynamic part is being planned, no ticket past the reserved tiles
+            // (a CTA must not sit on tiles it cannot fetch while the others,
+            // idle, could take them once they are published)
+            uint32_t tk = 0;
+            if (lane == 0) tk = ld_acquire_u32(&a.ctr->tickets);
+            tk = __shfl_sync(0xFFFFFFFFu, tk, 0);
+            const uint32_t pos = pre + tk;
+            if (pos >= known) return false;
+            // static tiles in chunks; reserved dynamic tiles one at a time
+            // until the stream length is final (they are spread over the
+            // CTAs as the contexts' plans arrive)
+            sz = pos < W ? min(CH, W - pos) : 1u;
         }
         if (lane == 0) cl_ret = atomicAdd(&a.ctr->tickets, sz);
         cl_size = sz;
         cl_pend = true;
+        return true;
     };
     bool first = true;
     if (a.dtrace && lane == 0) a.dtrace[16 * blockIdx.x + 12] = gtime();
@@ -1584,7 +1603,7 @@ __device__ __forceinline__ void decode_producer(const DecodeArgs& a, const Decod
             } else {
                 if (!cl_pend) {
                     refresh();
-                    claim();
+                    if (!claim()) return false;  // planner behind: poll
                 }
                 b0 = pre + __shfl_sync(0xFFFFFFFFu, cl_ret, 0);
                 b1 = b0 + cl_size;

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--dense", action="store_true")
     ap.add_argument("--plain", action="store_true", help="no tracing; run --reps eager steps and exit")
     ap.add_argument("--ctx-len", type=int, default=131072)
+    ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--probes", type=int, default=32)
     ap.add_argument("--given", action="store_true",
                     help="replay the routed lists through the caller-selected path (no routing)")
@@ -37,7 +38,7 @@ def main():
     import paper_2502_08246_b200 as sb
     if not hasattr(sb.Context, "set_option"):
         raise SystemExit("library without context options")
-    a = argparse.Namespace(ctx_len=args.ctx_len, batch=8, kv_heads=8, q_heads=32, dim=128, buckets=1024,
+    a = argparse.Namespace(ctx_len=args.ctx_len, batch=args.batch, kv_heads=8, q_heads=32, dim=128, buckets=1024,
                            probes=args.probes, recent=2047, sink=1, kmeans_iters=10)
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream()
@@ -57,7 +58,7 @@ def main():
     for li in range(2):
         inp = bench.make_layer_inputs(sb, torch, ctx, a, li, args.drift, 8, 0, dev, threads)
         parts = [sb.Partition(c, ctx) for c in inp.cents]
-        n_groups = 64
+        n_groups = args.batch * 8
         L = sb.Layer([a.ctx_len] * n_groups, 128, a.buckets, 1, a.recent, ctx)
         L.build_dev([parts[g % 8] for g in range(n_groups)], inp.K, inp.V, inp.Kd)
         inp.L, inp.routers = L, [sb.CentroidRouter(parts[g % 8], True) for g in range(n_groups)]
@@ -66,12 +67,12 @@ def main():
         inp.qr_t, inp.qd_t = torch.from_numpy(inp.qr).to(dev), torch.from_numpy(inp.qd).to(dev)
         lays.append(inp)
     cfg = sb.SparseAttnConfig(a.probes, 128, sb.DenseWindow(1, a.recent))
-    out = torch.empty(64, 4, 128, device=dev)
-    stats = torch.zeros(64, 3, dtype=torch.int64, device=dev)
+    out = torch.empty(args.batch * 8, 4, 128, device=dev)
+    stats = torch.zeros(args.batch * 8, 3, dtype=torch.int64, device=dev)
 
     if args.given:
         for lay in lays:
-            lay.sel = torch.empty(64, a.probes, dtype=torch.int32, device=dev)
+            lay.sel = torch.empty(args.batch * 8, a.probes, dtype=torch.int32, device=dev)
             lay.L.sparse_attention_dev(lay.routers, lay.qr_t, lay.qd_t, 4, cfg, out, stats,
                                        selected=lay.sel)
         ctx.synchronize()
