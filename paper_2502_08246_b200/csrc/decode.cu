@@ -98,6 +98,76 @@ __device__ __forceinline__ void emit_tiles(TileRec* base, uint32_t ntiles, uint3
     }
 }
 
+// Warp-parallel emit_tiles (same records): warp w takes tiles w, w + nw, ...;
+// the lanes take 32 consecutive segments at a time from the tile's first one,
+// each builds its piece, and a ballot orders the non-empty pieces.
+__device__ __forceinline__ void emit_tiles_warp(TileRec* base, uint32_t ntiles, uint32_t nh, uint32_t qslot0,
+                                                const Seg* segs, const uint32_t* vpre, uint32_t ns,
+                                                uint64_t row_base, uint32_t warp, uint32_t nw, uint32_t lane) {
+#pragma unroll 1
+    for (uint32_t t = warp; t < ntiles; t += nw) {
+        const uint32_t v_lo = t * kTileRows, v_hi = v_lo + kTileRows;
+        uint32_t lo = 0, hi = ns;  // last segment with vpre <= v_lo (vpre[0] == 0)
+#pragma unroll 1
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (vpre[mid] <= v_lo) lo = mid;
+            else hi = mid;
+        }
+        uint32_t np = 0, r8 = 0;
+        uint32_t vm[4] = {0u, 0u, 0u, 0u};
+#pragma unroll 1
+        for (uint32_t b0 = lo; b0 < ns; b0 += 32) {
+            const uint32_t b = b0 + lane;
+            bool has = false, more = false;
+            uint32_t len = 0, s0 = 0;
+            uint4 pr = make_uint4(0u, 0u, 0u, 0u);
+            if (b < ns) {
+                const uint32_t v0 = vpre[b];
+                more = v0 < v_hi;
+                if (more) {
+                    const Seg sg = segs[b];
+                    const uint32_t a0 = max(v0, v_lo), kend = min(v0 + sg.len, v_hi);
+                    if (kend > a0) {
+                        has = true;
+                        const uint64_t row = (sg.kind == KIND_LIST ? 0 : row_base) + sg.start + (a0 - v0);
+                        len = kend - a0;
+                        s0 = a0 - v_lo;
+                        pr = make_uint4(len | (sg.kind == KIND_LIST ? kPieceGather : 0u), s0, (uint32_t)row,
+                                        (uint32_t)(row >> 32));
+                    }
+                }
+            }
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, has);
+            if (has) {
+                const uint32_t idx = np + __popc(bal & ((1u << lane) - 1));
+                for (uint32_t hc = 0; hc < nh; ++hc)
+                    *reinterpret_cast<uint4*>(&base[(size_t)hc * ntiles + t].p[idx]) = pr;
+            }
+            np += __popc(bal);
+            r8 += __reduce_add_sync(0xFFFFFFFFu, has ? (len + 7) & ~7u : 0u);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // rows [s0, s0 + len) of the tile's 128
+                uint32_t m = 0;
+                if (has) {
+                    const uint32_t qlo = max(s0, (uint32_t)q * 32), qhi = min(s0 + len, (uint32_t)q * 32 + 32);
+                    if (qhi > qlo) m = (qhi - qlo == 32 ? 0xFFFFFFFFu : ((1u << (qhi - qlo)) - 1u)) << (qlo - q * 32);
+                }
+                vm[q] |= __reduce_or_sync(0xFFFFFFFFu, m);
+            }
+            // segments past the tile end the scan (vpre ascends)
+            if (__shfl_sync(0xFFFFFFFFu, (uint32_t)more, 31) == 0u) break;
+        }
+        for (uint32_t hc = lane; hc < nh; hc += 32) {
+            TileRec& tr = base[(size_t)hc * ntiles + t];
+            *reinterpret_cast<uint4*>(&tr.rows8) = make_uint4(r8, 0u, 0u, 0u);
+            *reinterpret_cast<uint4*>(&tr.valid[0]) = make_uint4(vm[0], vm[1], vm[2], vm[3]);
+            *reinterpret_cast<uint4*>(&tr) = make_uint4(np, qslot0 + hc, 0u, t + 1 == ntiles ? 1u : 0u);
+        }
+        __syncwarp();
+    }
+}
+
 __device__ __forceinline__ bool precedes(double sa, uint32_t ia, double sb, uint32_t ib) {
     return sa > sb || (sa == sb && ia < ib);
 }
@@ -1334,7 +1404,12 @@ __global__ void __launch_bounds__(kClusterThreads, 1) route_cluster_kernel(Clust
     // read) and copied out once the reservation is back
     TileRec* stage = reinterpret_cast<TileRec*>(slab);
     const bool staged = ntiles * nh <= (uint32_t)((size_t)D * S * 4 / sizeof(TileRec));
-    if (ntiles && staged) emit_tiles(stage, ntiles, nh, g * nh, segs, vpre, L, gm.row_base, tid, NT);
+    // (a few tiles: a warp per tile builds its pieces in parallel; many tiles:
+    // a thread per tile)
+    if (ntiles && staged) {
+        if (ntiles <= NT / 32) emit_tiles_warp(stage, ntiles, nh, g * nh, segs, vpre, L, gm.row_base, tid >> 5, NT / 32, lane);
+        else emit_tiles(stage, ntiles, nh, g * nh, segs, vpre, L, gm.row_base, tid, NT);
+    }
     if (tid == 0) s_tile0 = (uint32_t)res;
     __syncthreads();
     const uint32_t tile0 = s_tile0;
