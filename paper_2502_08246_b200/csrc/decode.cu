@@ -1096,13 +1096,18 @@ __global__ void __launch_bounds__(kClusterThreads, 1) route_cluster_kernel(Clust
             if (tid == 0) {
                 s_nb = 0;
                 s_bcnt = 0xFFFFFFFFu;
+                s_ncand = 0;  // (the candidate scan below needs no barrier of its own)
             }
             __syncthreads();
-            double vmn = s_mm[0][0], vmx = s_mm[1][0];
+            // every warp reduces the NT/32 warp extremes itself (one load per
+            // lane and shuffles, no serial scan of shared memory)
+            constexpr uint32_t NW = NT / 32;
+            static_assert(NW <= 32 && (NW & (NW - 1)) == 0, "warp count");
+            double vmn = s_mm[0][lane % NW], vmx = s_mm[1][lane % NW];
 #pragma unroll
-            for (uint32_t w = 1; w < NT / 32; ++w) {
-                vmn = fmin(vmn, s_mm[0][w]);
-                vmx = fmax(vmx, s_mm[1][w]);
+            for (uint32_t o = NW / 2; o; o >>= 1) {
+                vmn = fmin(vmn, __shfl_xor_sync(0xFFFFFFFFu, vmn, o));
+                vmx = fmax(vmx, __shfl_xor_sync(0xFFFFFFFFu, vmx, o));
             }
             const double span = vmx - vmn, scale = 256.0 / span;
             const bool lin = span > 0.0 && scale < INFINITY && vmx < INFINITY && vmn > -INFINITY;
@@ -1217,7 +1222,11 @@ __global__ void __launch_bounds__(kClusterThreads, 1) route_cluster_kernel(Clust
         trace(2);
         const double t_l = s_tl;
         double n2 = 0.0;
-        for (uint32_t w = 0; w < NT / 32; ++w) n2 += s_n2[w];
+        {  // (any order: n2 only sizes the error bound, which carries a 1% margin)
+            n2 = s_n2[lane % (NT / 32)];
+#pragma unroll
+            for (uint32_t o = (NT / 32) / 2; o; o >>= 1) n2 += __shfl_xor_sync(0xFFFFFFFFu, n2, o);
+        }
         // |approx - exact| <= B: the approximate dot (f32 FMA chains of DPT
         // terms over the f32-rounded pooled query, TPC partial sums in f32)
         // and the reference's sequential fp64 chain of the fp64 pooled query
@@ -1226,8 +1235,6 @@ __global__ void __launch_bounds__(kClusterThreads, 1) route_cluster_kernel(Clust
         // max|c|_2; the band is 2B, widened 2x
         const double pc = sqrt(n2) * (double)a.cmax[g];
         const double B2 = 2.0 * 2.0 * ((double)(DPT + TPC + 2) * 0x1p-24 + (double)(2 * D + 2) * 0x1p-53) * pc * 1.01;
-        if (tid == 0) s_ncand = 0;
-        __syncthreads();
 #pragma unroll
         for (uint32_t i = 0; i < PER; ++i) {
             const uint32_t cc = tid + i * NT;
