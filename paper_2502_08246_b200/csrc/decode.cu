@@ -1440,9 +1440,10 @@ __global__ void __launch_bounds__(kClusterThreads, 1) route_cluster_kernel(Clust
         trace(10);
     }
     __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        atomicAdd(&a.ctr->published, 1u);
+    // the context is published by a thread with no unfenced store (the record
+    // copies were fenced above): its release reduction does not wait
+    if (tid == NT - 1) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&a.ctr->published), "r"(1u) : "memory");
         tl_mark(a.tl, 1, false);
         if (a.trace) a.trace[16 + 6 * blockIdx.x + 3] = gt();
     }
