@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-c1", action="store_true", help="skip the C1-shape sub-line")
     ap.add_argument("--no-qmodel", action="store_true", help="skip the Q-model router sub-line")
+    ap.add_argument("--opt", action="append", default=[], metavar="NAME=VALUE",
+                    help="context option (saap_ctx_set_option), repeatable")
     ap.add_argument("--ranks-on-one-gpu", action="store_true",
                     help="smoke test of the N > 1 plumbing on a one-GPU box: every rank uses device 0 "
                          "(the numbers are not a scaling measurement; --exchange p2p only)")
@@ -382,6 +384,9 @@ def ours(a):
 
     stream = torch.cuda.Stream()
     ctx = sb.Context(local)
+    for kv in a.opt:
+        k, v = kv.split("=")
+        ctx.set_option(k, int(v))
     ctx.set_stream(stream.cuda_stream)
     comm = p2p = None
     exchange = a.exchange

@@ -184,8 +184,8 @@ def test_host_api_graph_replay_tracks_inputs(ctx, port):
 
 
 def test_host_api_zero_copy_outputs(ctx, port):
-    """Page-locked output / stats buffers through the host API equal the
-    pageable path, across graph replays."""
+    """Page-locked output / stats buffers (poisoned before each call) through
+    the host API equal the pageable path, across graph replays."""
     import ctypes as ct
 
     import torch
@@ -202,6 +202,7 @@ def test_host_api_zero_copy_outputs(ctx, port):
                                            for c in cases]))
         want, wst, _ = L.sparse_attention(routers, q, q, cfg)
         out_pin.fill_(np.nan)
+        st_pin.fill_(0xFF)
         c = cfg.c()
         sb._check(sb.lib().saap_sparse_attention(
             ctx.h, L.h, L._routers(routers), q.ctypes.data_as(ct.c_void_p),
